@@ -1,0 +1,266 @@
+"""TEST INFRASTRUCTURE ONLY — ctypes wrapper over the CPU oracle (vqmc_oracle.cpp).
+
+The oracle restates the reference VQMC path (arxiv/paper_2106_13308,
+/root/reference/proj) in fp64 C++.  Only tests/, __graft_entry__.smoke() and
+bench.py's cpu_baseline / ``--impl reference`` legs may import this module.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+import subprocess
+
+import numpy as np
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+_LIB_PATH = os.path.join(_HERE, "_build", "libvqmc_oracle.so")
+_lib = None
+
+_dp = np.ctypeslib.ndpointer(dtype=np.float64, flags="C_CONTIGUOUS")
+_ip = np.ctypeslib.ndpointer(dtype=np.int32, flags="C_CONTIGUOUS")
+_u8 = np.ctypeslib.ndpointer(dtype=np.uint8, flags="C_CONTIGUOUS")
+
+
+def build() -> None:
+    subprocess.run(["make", "-s", "-C", _HERE], check=True)
+
+
+def lib():
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(_LIB_PATH):
+        build()
+    L = C.CDLL(_LIB_PATH)
+    L.oracle_last_error.restype = C.c_char_p
+    L.oracle_blas_path.restype = C.c_char_p
+    L.oracle_mix_seed.restype = C.c_uint64
+    L.oracle_mix_seed.argtypes = [C.c_uint64, C.c_uint64]
+    L.oracle_default_made_hidden.argtypes = [C.c_int]
+    L.oracle_uniforms.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int64, _dp]
+    L.oracle_philox_uniforms.argtypes = [C.c_uint64, C.c_uint64, C.c_uint64, C.c_int, C.c_int, _dp]
+    L.oracle_made_init.argtypes = [C.c_int, C.c_int, C.c_uint64, _ip, _dp]
+    L.oracle_forward.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_int, _u8, C.c_void_p, C.c_void_p, C.c_void_p]
+    L.oracle_log_psi.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_int, _u8, _dp]
+    L.oracle_auto_sample.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_int, C.c_uint64, C.c_uint64,
+                                     C.c_void_p, C.c_int, _u8, _dp, C.c_void_p]
+    L.oracle_local_energy.argtypes = [C.c_int, _ip, C.c_int64, C.c_int, _u8, _dp, C.c_void_p]
+    L.oracle_energy_and_variance.argtypes = [_dp, C.c_int, C.POINTER(C.c_double), C.POINTER(C.c_double)]
+    L.oracle_weighted_grad.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_int, _u8, _dp, _dp]
+    L.oracle_gradient_from_locals.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_int, _u8, _dp, _dp]
+    L.oracle_adam_step.argtypes = [C.c_int64, _dp, _dp, _dp, _dp, C.POINTER(C.c_int64),
+                                   C.c_double, C.c_double, C.c_double, C.c_double]
+    L.oracle_allreduce_mean.argtypes = [C.c_int, C.c_int64, _dp, _dp]
+    for fn in ("oracle_random_maxcut_graph",):
+        getattr(L, fn).argtypes = [C.c_int, C.c_uint64, C.c_void_p, C.c_int64, C.POINTER(C.c_int64)]
+    L.oracle_random_regular_graph.argtypes = [C.c_int, C.c_int, C.c_uint64, C.c_void_p, C.c_int64,
+                                              C.POINTER(C.c_int64)]
+    L.oracle_erdos_renyi_graph.argtypes = [C.c_int, C.c_double, C.c_uint64, C.c_void_p, C.c_int64,
+                                           C.POINTER(C.c_int64)]
+    L.oracle_brute_force_maxcut.restype = C.c_int64
+    L.oracle_brute_force_maxcut.argtypes = [C.c_int, _ip, C.c_int64, C.POINTER(C.c_uint64)]
+    L.oracle_train.argtypes = [C.c_int, C.c_int, _ip, C.c_int64, C.c_int, C.c_double, C.c_int, C.c_int,
+                               C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
+                               C.c_void_p, C.c_void_p]
+    L.oracle_enumerate_distribution.argtypes = [C.c_int, C.c_int, _ip, _dp, _dp]
+    L.oracle_goodness_of_fit.argtypes = [C.c_int, _dp, C.c_int64, _u8, _dp]
+    _lib = L
+    return L
+
+
+def _check(rc):
+    if rc != 0:
+        raise RuntimeError(lib().oracle_last_error().decode())
+
+
+def _ptr(a):
+    return None if a is None else a.ctypes.data_as(C.c_void_p)
+
+
+def mix_seed(seed, stream):
+    return lib().oracle_mix_seed(seed, stream)
+
+
+def default_made_hidden(n):
+    return lib().oracle_default_made_hidden(n)
+
+
+def uniforms(seed, stream, count, skip=0):
+    out = np.empty(count, np.float64)
+    _check(lib().oracle_uniforms(seed, stream, skip, count, out))
+    return out
+
+
+def philox_uniforms(seed, stream, call, n, B):
+    out = np.empty((n, B), np.float64)
+    _check(lib().oracle_philox_uniforms(seed, stream, call, n, B, out))
+    return out
+
+
+class Made:
+    """Reference MADE parameters: theta in reference flatten order (models.cpp:264-275)."""
+
+    def __init__(self, n, h, degrees, theta):
+        self.n, self.h = int(n), int(h)
+        self.degrees = np.ascontiguousarray(degrees, np.int32)
+        self.theta = np.ascontiguousarray(theta, np.float64)
+
+    @property
+    def d(self):
+        return 2 * self.h * self.n + self.h + self.n
+
+    def copy(self):
+        return Made(self.n, self.h, self.degrees.copy(), self.theta.copy())
+
+    def split(self):
+        n, h, t = self.n, self.h, self.theta
+        W1 = t[: h * n].reshape(h, n)
+        b1 = t[h * n: h * n + h]
+        W2 = t[h * n + h: h * n + h + n * h].reshape(n, h)
+        b2 = t[h * n + h + n * h:]
+        return W1, b1, W2, b2
+
+
+def made_init(n, h, seed):
+    deg = np.empty(h, np.int32)
+    theta = np.empty(2 * h * n + h + n, np.float64)
+    _check(lib().oracle_made_init(n, h, seed, deg, theta))
+    return Made(n, h, deg, theta)
+
+
+def forward(m: Made, x):
+    x = np.ascontiguousarray(x, np.uint8)
+    B = x.shape[0]
+    p = np.empty((B, m.n)); pr = np.empty((B, m.n)); z1 = np.empty((B, m.h))
+    _check(lib().oracle_forward(m.n, m.h, m.degrees, m.theta, B, x, _ptr(p), _ptr(pr), _ptr(z1)))
+    return p, pr, z1
+
+
+def log_psi(m: Made, x):
+    x = np.ascontiguousarray(x, np.uint8)
+    out = np.empty(x.shape[0])
+    _check(lib().oracle_log_psi(m.n, m.h, m.degrees, m.theta, x.shape[0], x, out))
+    return out
+
+
+def auto_sample(m: Made, B, seed=0, stream=0, uniforms=None, mode=0, want_p=False):
+    """mode 0 = reference n-forward sampler, mode 1 = incremental restatement."""
+    x = np.empty((B, m.n), np.uint8)
+    lp = np.empty(B)
+    p = np.empty((B, m.n)) if want_p else None
+    u = None if uniforms is None else np.ascontiguousarray(uniforms, np.float64)
+    _check(lib().oracle_auto_sample(m.n, m.h, m.degrees, m.theta, B, seed, stream, _ptr(u), mode, x, lp,
+                                    _ptr(p)))
+    return (x, lp, p) if want_p else (x, lp)
+
+
+def local_energy(n, edges, x):
+    x = np.ascontiguousarray(x, np.uint8)
+    e = np.ascontiguousarray(edges, np.int32).reshape(-1)
+    B = x.shape[0]
+    le = np.empty(B); cut = np.empty(B)
+    _check(lib().oracle_local_energy(n, e, e.size // 2, B, x, le, _ptr(cut)))
+    return le, cut
+
+
+def energy_and_variance(l):
+    l = np.ascontiguousarray(l, np.float64)
+    m = C.c_double(); v = C.c_double()
+    _check(lib().oracle_energy_and_variance(l, l.size, C.byref(m), C.byref(v)))
+    return m.value, v.value
+
+
+def weighted_grad(m: Made, x, w):
+    x = np.ascontiguousarray(x, np.uint8)
+    g = np.empty(m.d)
+    _check(lib().oracle_weighted_grad(m.n, m.h, m.degrees, m.theta, x.shape[0], x,
+                                      np.ascontiguousarray(w, np.float64), g))
+    return g
+
+
+def gradient_from_locals(m: Made, x, local):
+    x = np.ascontiguousarray(x, np.uint8)
+    g = np.empty(m.d)
+    _check(lib().oracle_gradient_from_locals(m.n, m.h, m.degrees, m.theta, x.shape[0], x,
+                                             np.ascontiguousarray(local, np.float64), g))
+    return g
+
+
+class AdamState:
+    def __init__(self, d, lr=0.01, b1=0.9, b2=0.999, eps=1e-8):
+        self.m = np.zeros(d); self.v = np.zeros(d); self.t = 0
+        self.lr, self.b1, self.b2, self.eps = lr, b1, b2, eps
+
+
+def adam_step(st: AdamState, params, grad):
+    t = C.c_int64(st.t)
+    _check(lib().oracle_adam_step(params.size, params, np.ascontiguousarray(grad, np.float64), st.m, st.v,
+                                  C.byref(t), st.lr, st.b1, st.b2, st.eps))
+    st.t = t.value
+
+
+def allreduce_mean(vs):
+    vs = np.ascontiguousarray(np.stack(vs), np.float64)
+    out = np.empty(vs.shape[1])
+    _check(lib().oracle_allreduce_mean(vs.shape[0], vs.shape[1], vs, out))
+    return out
+
+
+def _graph(fn, *args):
+    ne = C.c_int64()
+    _check(fn(*args, None, 0, C.byref(ne)))
+    e = np.empty((ne.value, 2), np.int32)
+    _check(fn(*args, _ptr(e), ne.value, C.byref(ne)))
+    return e
+
+
+def random_maxcut_graph(n, seed):
+    return _graph(lib().oracle_random_maxcut_graph, n, seed)
+
+
+def random_regular_graph(n, d, seed):
+    return _graph(lib().oracle_random_regular_graph, n, d, seed)
+
+
+def erdos_renyi_graph(n, p, seed):
+    return _graph(lib().oracle_erdos_renyi_graph, n, p, seed)
+
+
+def brute_force_maxcut(n, edges):
+    e = np.ascontiguousarray(edges, np.int32).reshape(-1)
+    am = C.c_uint64()
+    v = lib().oracle_brute_force_maxcut(n, e, e.size // 2, C.byref(am))
+    if v < 0:
+        raise RuntimeError(lib().oracle_last_error().decode())
+    return int(v), int(am.value)
+
+
+def train(n, edges, h=0, optimizer="adam", lr=0.0, iterations=300, workers=1, minibatch=1024,
+          eval_batch=1024, seed=0, sampler_mode=0, threads=True, want_first_grad=False):
+    """Restated vqmc::train for MADE+AUTO on a Max-Cut instance (trainer.cpp:111-322)."""
+    e = np.ascontiguousarray(edges, np.int32).reshape(-1)
+    hh = h if h > 0 else default_made_hidden(n)
+    d = 2 * hh * n + hh + n
+    stats = np.empty((iterations, 4)); ev = np.empty(4); theta = np.empty(d)
+    g0 = np.empty(d) if want_first_grad else None
+    _check(lib().oracle_train(n, hh, e, e.size // 2, 1 if optimizer == "adam" else 0, lr, iterations,
+                              workers, minibatch, eval_batch, seed, sampler_mode, 1 if threads else 0,
+                              _ptr(stats), _ptr(ev), _ptr(theta), _ptr(g0)))
+    out = dict(stats=stats, final_energy=ev[0], final_energy_std=ev[1], best_cut=ev[2], mean_cut=ev[3],
+               theta=theta, h=hh)
+    if want_first_grad:
+        out["first_grad"] = g0
+    return out
+
+
+def enumerate_distribution(m: Made):
+    p = np.empty(1 << m.n)
+    _check(lib().oracle_enumerate_distribution(m.n, m.h, m.degrees, m.theta, p))
+    return p
+
+
+def goodness_of_fit(n, probs, x):
+    x = np.ascontiguousarray(x, np.uint8)
+    out = np.empty(5)
+    _check(lib().oracle_goodness_of_fit(n, np.ascontiguousarray(probs, np.float64), x.shape[0], x, out))
+    return dict(tv=out[0], chi2=out[1], dof=int(out[2]), z=out[3], reject=bool(out[4]))
