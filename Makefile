@@ -1,0 +1,32 @@
+# B200 VQMC library: nvcc for sm_100a, in-tree outputs (they travel to the GPU box).
+NVCC ?= /usr/local/cuda/bin/nvcc
+ARCH := -gencode arch=compute_100a,code=sm_100a
+NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v
+SRC := paper_2106_13308_b200/csrc/kernels.cu paper_2106_13308_b200/csrc/capi.cu
+HOSTSRC := paper_2106_13308_b200/csrc/host.cpp
+HDRS := $(wildcard paper_2106_13308_b200/csrc/*.cuh) include/vqmc_b200.h Makefile
+LIB := paper_2106_13308_b200/lib/libvqmc_b200.so
+OBJDIR := build/obj
+OBJS := $(patsubst paper_2106_13308_b200/csrc/%.cu,$(OBJDIR)/%.o,$(SRC)) $(OBJDIR)/host.o
+
+all: $(LIB) oracle
+
+$(OBJDIR)/%.o: paper_2106_13308_b200/csrc/%.cu $(HDRS)
+	@mkdir -p $(OBJDIR)
+	$(NVCC) $(NVFLAGS) -c $< -o $@ 2> $(OBJDIR)/$*.ptxas.log || (cat $(OBJDIR)/$*.ptxas.log; exit 1)
+
+$(OBJDIR)/host.o: $(HOSTSRC) include/vqmc_b200.h Makefile
+	@mkdir -p $(OBJDIR)
+	g++ -O3 -march=x86-64-v3 -std=c++17 -fPIC -Iinclude -c $< -o $@
+
+$(LIB): $(OBJS)
+	@mkdir -p paper_2106_13308_b200/lib
+	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl -lpthread
+
+oracle:
+	$(MAKE) -s -C oracle
+
+clean:
+	rm -rf build paper_2106_13308_b200/lib oracle/_build
+
+.PHONY: all oracle clean

@@ -1,0 +1,420 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 VQMC Max-Cut training step (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+Workload (BASELINE.json configs[4], the headline): Max-Cut on a random 3-regular graph with
+N = 10,000 vertices, MADE with h = round(5 ln^2 N) = 424, exact autoregressive sampling,
+1024 samples per GPU per step, REINFORCE gradient, NCCL all-reduce (N > 1), Adam.
+A step is one full VQMC iteration (vqmc::train's worker_body).  Synthetic graph and
+random-init weights (no datasets exist for this problem).
+
+Under torchrun (N > 1) every rank drives one GPU; data parallel, weak scaling (1024 samples
+per GPU), one NCCL all-reduce of the gradient per step inside the fused step.
+"""
+from __future__ import annotations
+
+import argparse
+import ctypes as C
+import json
+import math
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--n", type=int, default=10000)
+    ap.add_argument("--graph", choices=["regular3", "maxcut"], default="regular3")
+    ap.add_argument("--minibatch", type=int, default=1024)
+    ap.add_argument("--seed", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the bounded CPU sample")
+    ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / e2e / cpu)")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Dist:
+    """torch.distributed (gloo) for plumbing: id broadcast, barriers, max over ranks."""
+
+    def __init__(self, world, rank):
+        self.world, self.rank = world, rank
+        self.pg = None
+        if world > 1:
+            import torch.distributed as dist
+            os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+            dist.init_process_group("gloo", rank=rank, world_size=world)
+            self.dist = dist
+
+    def barrier(self):
+        if self.world > 1:
+            self.dist.barrier()
+
+    def bcast_bytes(self, b: bytes) -> bytes:
+        if self.world == 1:
+            return b
+        obj = [b]
+        self.dist.broadcast_object_list(obj, src=0)
+        return obj[0]
+
+    def max(self, v: float) -> float:
+        if self.world == 1:
+            return v
+        import torch
+        t = torch.tensor([v], dtype=torch.float64)
+        self.dist.all_reduce(t, op=self.dist.ReduceOp.MAX)
+        return float(t.item())
+
+
+class ClockSampler:
+    """nvidia-smi clocks / throttle reasons sampled during the timed region."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", "clocks.csv")
+
+    def start(self):
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                                          "-lms", "100"], stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait(timeout=5)
+        self.f.close()
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+        return {"sm_mhz": float(np.median(sm)), "sm_max_mhz": float(max(mx)), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        return json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except Exception:
+        return None
+
+
+def make_instance(args):
+    from paper_2106_13308_b200 import api
+    if args.graph == "regular3":
+        g = api.random_regular_graph(args.n, 3, args.seed)
+        desc = f"random 3-regular, |E|={len(g.edges)}"
+    else:
+        g = api.random_maxcut_graph(args.n, args.seed)
+        desc = f"reference G(n,3/4), |E|={len(g.edges)}"
+    return g, desc
+
+
+# ---------------------------------------------------------------------------
+# Algorithmic work per kernel launch: FLOPs for the GEMM-shaped
+# kernels (tensor-core bound), bytes for the streaming ones (HBM bound).
+# ---------------------------------------------------------------------------
+def kernel_work(name, n, h, Hd, B, E):
+    nnzM2_tail = (n - Hd) * h
+    if name == "z2_tail_sample":
+        return "tensor", 2.0 * B * nnzM2_tail, "FLOP"
+    if name == "bw_dg1":
+        return "tensor", 2.0 * B * n * h, "FLOP"
+    if name == "bw_gw2":
+        return "tensor", 2.0 * B * n * (h + 1), "FLOP"
+    if name == "bw_gw1":
+        return "tensor", 2.0 * B * (Hd + 1) * h, "FLOP"
+    if name == "adam":
+        total = Hd * h + h + n * h + n
+        return "hbm", 28.0 * total, "B"
+    if name == "maxcut_energy":
+        W = (n + 31) // 32
+        return "hbm", 4.0 * B * W + 8.0 * E + 12.0 * B, "B"
+    if name == "head_sample":
+        return "latency", 2.0 * B * Hd * (h + Hd), "FLOP"
+    return None, None, None
+
+
+def run_ours(args):
+    world, rank, local = dist_env()
+    D = Dist(world, rank)
+    import torch
+    torch.cuda.set_device(local)
+    from paper_2106_13308_b200 import _capi as K
+    from paper_2106_13308_b200 import api
+
+    g, gdesc = make_instance(args)
+    n = args.n
+    h = api.default_made_hidden(n)
+    model = api.made_init(n, h, args.seed)
+    Hd = int(model.degrees.max())
+    B = args.minibatch
+    hd = C.c_void_p()
+    e = np.ascontiguousarray(g.edges, np.int32)
+    K.check(K.lib.vqmc_gpu_create(local, n, h, K.ptr(model.degrees), K.ptr(model.parameters()), K.ptr(e), len(e),
+                                  B, C.byref(hd)))
+    if world > 1:
+        uid = (C.c_uint8 * 128)()
+        if rank == 0:
+            K.check(K.lib.vqmc_gpu_comm_unique_id(uid))
+        b = D.bcast_bytes(bytes(uid))
+        uid = (C.c_uint8 * 128).from_buffer_copy(b)
+        K.check(K.lib.vqmc_gpu_comm_init(hd, uid, world, rank))
+    K.check(K.lib.vqmc_gpu_adam_reset(hd))
+    lr, b1, b2, eps = 0.01, 0.9, 0.999, 1e-8
+    stream0 = 1 + rank  # worker w = rank uses make_stream(seed, w + 1)'s Philox key
+    step = [0]
+
+    def one_step(stats=None):
+        step[0] += 1
+        K.check(K.lib.vqmc_gpu_train_step(hd, B, 1, None, args.seed, stream0, step[0], lr, b1, b2, eps, step[0],
+                                          stats))
+
+    flush = torch.empty(256 * 1024 * 1024 // 4, dtype=torch.float32, device=f"cuda:{local}")
+    for _ in range(max(args.warmup, 0)):
+        one_step()
+    K.check(K.lib.vqmc_gpu_synchronize(hd))
+    K.check(K.lib.vqmc_gpu_set_phase_timing(hd, 1))
+    K.check(K.lib.vqmc_gpu_set_kernel_timing(hd, 1))
+    clocks = ClockSampler()
+    if rank == 0 and not args.profile:
+        clocks.start()
+    launches0 = K.lib.vqmc_gpu_launch_count(hd)
+    D.barrier()
+    torch.cuda.synchronize()
+    total_ms = 0.0
+    ktimes: dict = {}
+    kcount: dict = {}
+    phase = np.zeros(5)
+    names = C.create_string_buffer(32 * 128)
+    kms = (C.c_float * 128)()
+    cnt = C.c_int()
+    pms = (C.c_float * 5)()
+    for _ in range(args.steps):
+        flush.zero_()  # L2 flush (256 MB > 126 MB L2) between timed iterations, outside the events
+        torch.cuda.synchronize()
+        one_step()
+        K.check(K.lib.vqmc_gpu_phase_times(hd, pms))
+        phase += np.array(list(pms))
+        total_ms += float(sum(pms))
+        K.check(K.lib.vqmc_gpu_kernel_times(hd, names, kms, 128, C.byref(cnt)))
+        for i in range(cnt.value):
+            nm = names.raw[32 * i: 32 * i + 32].split(b"\0")[0].decode()
+            ktimes[nm] = ktimes.get(nm, 0.0) + kms[i]
+            kcount[nm] = kcount.get(nm, 0) + 1
+    K.check(K.lib.vqmc_gpu_synchronize(hd))
+    torch.cuda.synchronize()
+    D.barrier()
+    launches = K.lib.vqmc_gpu_launch_count(hd) - launches0
+    clk = clocks.stop() if (rank == 0 and not args.profile) else None
+    T = D.max(total_ms)
+    ms_per_step = T / args.steps
+    value = world * B * 1000.0 / ms_per_step
+
+    # e2e: the public API call (blocking; per-step statistics copied to the host)
+    K.check(K.lib.vqmc_gpu_set_phase_timing(hd, 0))
+    K.check(K.lib.vqmc_gpu_set_kernel_timing(hd, 0))
+    e2e = None
+    if not args.profile:
+        st = K.StepStats()
+        D.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            one_step(C.byref(st))
+        e2e_s = D.max(time.perf_counter() - t0)
+        e2e = {"value": world * B * args.steps / e2e_s, "unit": "samples/s", "h2d_bytes_per_step": 0,
+               "d2h_bytes_per_step": C.sizeof(K.StepStats),
+               "steps_per_s": args.steps / e2e_s,
+               "note": "vqmc_gpu_train_step with stats_out (blocking, per-step stats D2H); the step's only "
+                       "inputs are scalars (seed, stream, counter) - samples are generated on the device by "
+                       "design (Philox), so there is no per-step H2D payload"}
+
+    # final cut (evaluate, trainer.cpp:91-108) on the eval stream
+    ev = np.empty(4)
+    K.check(K.lib.vqmc_gpu_evaluate(hd, 1024, None, args.seed, api.kEvalStream, 0, K.ptr(ev)))
+
+    if rank != 0:
+        K.lib.vqmc_gpu_destroy(hd)
+        return None
+
+    # dominant kernel + roofline
+    peaks = measured_peaks()
+    avg = {k: ktimes[k] / kcount[k] for k in ktimes}
+    share = {k: ktimes[k] / max(1e-9, sum(ktimes.values())) for k in ktimes}
+    dom = max(ktimes, key=lambda k: ktimes[k])
+    bound, work, wunit = kernel_work(dom, n, h, Hd, B, len(e))
+    roof = None
+    if bound == "tensor":
+        ach = work / (avg[dom] * 1e-3) / 1e12
+        pk = peaks["bf16_tflops_sustained"] if peaks else 1400.0
+        roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
+                "traffic": None, "peak_src": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
+                "algorithmic_per_launch": work, "launch_ms": avg[dom]}
+    elif bound == "hbm":
+        ach = work / (avg[dom] * 1e-3) / 1e9
+        pk = peaks["hbm_gbs"] if peaks else 6650.0
+        roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk,
+                "traffic": None, "algorithmic_per_launch": work, "launch_ms": avg[dom]}
+    else:
+        ach = work / (avg[dom] * 1e-3) / 1e12
+        pk = 148 * 128 * 2 * 1.965e9 / 1e12
+        roof = {"bound": "latency", "kernel": dom, "achieved": ach, "peak": pk, "unit": "TFLOP/s (fp32 FMA pipe)",
+                "frac": ach / pk, "traffic": None, "algorithmic_per_launch": work, "launch_ms": avg[dom]}
+    # all tensor/hbm kernels for context
+    kernels = {}
+    for k in sorted(ktimes, key=lambda k: -ktimes[k]):
+        b_, w_, u_ = kernel_work(k, n, h, Hd, B, len(e))
+        ent = {"avg_ms": round(avg[k], 5), "share": round(share[k], 4)}
+        if w_:
+            ent["achieved"] = w_ / (avg[k] * 1e-3) / (1e12 if u_ == "FLOP" else 1e9)
+            ent["unit"] = "TFLOP/s" if u_ == "FLOP" else "GB/s"
+        kernels[k] = ent
+
+    cpu = None
+    if world == 1 and not args.no_cpu_baseline and not args.profile:
+        cpu = cpu_baseline(args, g, B)
+
+    K.lib.vqmc_gpu_destroy(hd)
+    line = {
+        "metric": "samples/sec (VQMC training step, N=10k Max-Cut MADE)",
+        "value": value,
+        "unit": "samples/s",
+        "n_gpus": world,
+        "steps": args.steps,
+        "warmup": args.warmup,
+        "ms_per_step": ms_per_step,
+        "steps_per_s": 1000.0 / ms_per_step,
+        "higher_is_better": True,
+        "scaling": "weak",
+        "vs_baseline": None,
+        "dtype": "f32 (fp64 accumulation for log-probs and energies; integer cuts)",
+        "data": "synthetic (random 3-regular graph, random-init MADE; Philox uniforms)",
+        "config": {"workload": f"Max-Cut N={n} ({gdesc}), MADE h={h}, AUTO sampler, ADAM lr=0.01",
+                   "samples_per_gpu": B, "global_batch": world * B, "parallelism": f"dp{world}",
+                   "l2": "flushed between timed iterations (256 MB write, outside the events)"},
+        "phase_ms": {k: round(v / args.steps, 5) for k, v in
+                     zip(["sample", "energy+weights", "backward", "allreduce", "adam+refresh"], phase)},
+        "kernels": kernels,
+        "roofline": roof,
+        "final_cut": {"best_cut": ev[2], "mean_cut": ev[3], "energy": ev[0], "note": "eval batch 1024 after "
+                      f"{args.warmup + 2 * args.steps} training steps"},
+        "clocks": clk,
+        "e2e": e2e,
+        "gpu_launches": int(launches),
+        "gpu_launches_per_step": launches / args.steps,
+        "cpu_baseline": cpu,
+    }
+    return line
+
+
+def cpu_baseline(args, g, B, steps=1, budget_s=None):
+    """The reference algorithm (oracle restatement, fp64, n full forward passes per sampling
+    call) on the host cores: workers = cores, minibatch B / cores each (effective batch B)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, B // 2))
+    mbs = max(2, B // workers)
+    budget = budget_s or args.cpu_seconds
+    # calibrate: one bit
+    cal = O.time_reference_step(args.n, g.edges, workers, mbs, seed=args.seed, bits_limit=1)
+    per_bit = cal["sample_s"] / args.n
+    bits = int(max(1, min(args.n, budget / max(per_bit, 1e-9))))
+    runs = [O.time_reference_step(args.n, g.edges, workers, mbs, seed=args.seed, bits_limit=bits)
+            for _ in range(steps)]
+    step_s = float(np.mean([r["step_s"] for r in runs]))
+    return {"value": workers * mbs / step_s, "unit": "samples/s", "cores": workers, "kind": "port",
+            "steps_per_s": 1.0 / step_s,
+            "sample": f"one reference iteration, {workers} worker threads x minibatch {mbs} (batch {workers * mbs}); "
+                      f"sampler timed for the first {bits} of {args.n} bits (each bit is one full two-GEMM forward "
+                      f"pass, sampler.cpp:47-48) and extrapolated x{args.n / bits:.1f}; energy, gradient, tree "
+                      f"all-reduce and Adam timed in full; fp64 OpenBLAS dgemm, 1 thread per worker",
+            "step_s": step_s, "sampler_s": runs[0]["sample_s"], "estimate_s": runs[0]["estimate_s"],
+            "update_s": runs[0]["update_s"], "oracle": "oracle/vqmc_oracle.cpp (restated reference; Eigen absent)"}
+
+
+def run_reference(args):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return None
+    g, gdesc = make_instance(args)
+    B = args.minibatch
+    K_, W_ = max(1, args.steps), max(0, args.warmup)
+    budget = max(2.0, min(20.0, 150.0 / (K_ + W_)))
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    cores = os.cpu_count() or 1
+    workers = max(1, min(cores, B // 2))
+    mbs = max(2, B // workers)
+    cal = O.time_reference_step(args.n, g.edges, workers, mbs, seed=args.seed, bits_limit=1)
+    per_bit = cal["sample_s"] / args.n
+    bits = int(max(1, min(args.n, budget / max(per_bit, 1e-9))))
+    for _ in range(W_):
+        O.time_reference_step(args.n, g.edges, workers, mbs, seed=args.seed, bits_limit=max(1, bits // 4))
+    steps = [O.time_reference_step(args.n, g.edges, workers, mbs, seed=args.seed, bits_limit=bits)["step_s"]
+             for _ in range(K_)]
+    step_s = float(np.mean(steps))
+    value = workers * mbs / step_s
+    h = O.default_made_hidden(args.n)
+    sample = (f"{workers} worker threads x minibatch {mbs}; per step the reference sampler runs the first {bits} of "
+              f"{args.n} bits (one full forward pass each) and is extrapolated; energy/gradient/all-reduce/Adam in full")
+    return {"impl": "reference", "metric": "samples/sec (VQMC training step, N=10k Max-Cut MADE)", "value": value,
+            "unit": "samples/s", "n_gpus": 0, "steps": K_, "warmup": W_, "ms_per_step": step_s * 1000.0,
+            "steps_per_s": 1.0 / step_s, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f64", "data": "synthetic",
+            "config": {"workload": f"Max-Cut N={args.n} ({gdesc}), MADE h={h}, AUTO sampler, ADAM lr=0.01",
+                       "samples_per_step": workers * mbs, "parallelism": f"{workers} host threads"},
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": workers, "kind": "port", "sample": sample},
+            "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        line = run_reference(args)
+    else:
+        line = run_ours(args)
+    if line is not None:
+        print(json.dumps(line), flush=True)
+
+
+if __name__ == "__main__":
+    main()

@@ -63,6 +63,8 @@ def lib():
                                C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_void_p]
     L.oracle_enumerate_distribution.argtypes = [C.c_int, C.c_int, _ip, _dp, _dp]
+    L.oracle_time_reference_step.argtypes = [C.c_int, C.c_int, _ip, C.c_int64, C.c_int, C.c_int, C.c_uint64,
+                                             C.c_int, _dp]
     L.oracle_goodness_of_fit.argtypes = [C.c_int, _dp, C.c_int64, _u8, _dp]
     _lib = L
     return L
@@ -264,3 +266,13 @@ def goodness_of_fit(n, probs, x):
     out = np.empty(5)
     _check(lib().oracle_goodness_of_fit(n, np.ascontiguousarray(probs, np.float64), x.shape[0], x, out))
     return dict(tv=out[0], chi2=out[1], dof=int(out[2]), z=out[3], reject=bool(out[4]))
+
+
+def time_reference_step(n, edges, workers, minibatch, seed=0, bits_limit=None, h=0):
+    """One reference iteration on `workers` host threads, sampler extrapolated from
+    `bits_limit` bits; returns dict of seconds (see oracle_time_reference_step)."""
+    e = np.ascontiguousarray(edges, np.int32).reshape(-1)
+    out = np.empty(5)
+    _check(lib().oracle_time_reference_step(n, h, e, e.size // 2, workers, minibatch, seed,
+                                            bits_limit or n, out))
+    return dict(sample_s=out[0], estimate_s=out[1], update_s=out[2], step_s=out[3], bits_timed=int(out[4]))

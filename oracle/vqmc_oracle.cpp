@@ -977,4 +977,69 @@ int oracle_philox_uniforms(uint64_t seed, uint64_t stream, uint64_t call, int n,
   ORACLE_CATCH
 }
 
+// CPU-baseline timing of one reference iteration (bench.py cpu_baseline / --impl reference).
+// Each of `workers` threads runs the reference sampler (auto_sample: one full two-GEMM
+// forward pass per bit, sampler.cpp:47-55) for the first `bits_limit` bits — every bit costs
+// the same full forward pass, so the full-sampler time is t * n / bits_limit — then the
+// Max-Cut local energy and gradient_from_locals on a complete sample (drawn untimed with the
+// incremental sampler; same cost as on the reference's sample), then allreduce_mean + Adam.
+// out = {sampler_seconds_extrapolated, estimate_seconds, update_seconds, step_seconds_estimate,
+//        bits_timed}.
+int oracle_time_reference_step(int n, int h, const int32_t* edges, int64_t E, int workers, int mbs,
+                               uint64_t seed, int bits_limit, double* out) {
+  ORACLE_TRY
+  std::vector<Edge> e((size_t)E);
+  for (int64_t t = 0; t < E; ++t) e[t] = {edges[2 * t], edges[2 * t + 1]};
+  if (h <= 0) h = default_made_hidden(n);
+  bits_limit = std::max(1, std::min(bits_limit, n));
+  const Made model = made_init(n, h, seed);
+  std::vector<double> tsamp(workers), trest(workers);
+  std::vector<std::vector<double>> grads(workers);
+  if (mbs < 2) throw std::invalid_argument("minibatch must be >= 2");
+  auto work = [&](int w) {
+    auto rng = make_stream(seed, w + 1);
+    std::uniform_real_distribution<double> unit(0.0, 1.0);
+    std::vector<double> X((size_t)mbs * n, 0.0), lp(mbs, 0.0);
+    const double t0 = now_s();
+    for (int i = 0; i < bits_limit; ++i) {
+      const Fwd f = made_forward(model, X.data(), mbs);
+      for (int b = 0; b < mbs; ++b) {
+        const double pi = f.p[(size_t)b * n + i];
+        const double bit = unit(rng) < pi ? 1.0 : 0.0;
+        X[(size_t)b * n + i] = bit;
+        lp[b] += bit > 0.5 ? std::log(pi) : std::log(1.0 - pi);
+      }
+    }
+    tsamp[w] = (now_s() - t0) * (double)n / (double)bits_limit;
+    auto rng2 = make_stream(seed, w + 1);
+    const Sample s = auto_sample_incremental(model, mbs, &rng2, nullptr, nullptr);
+    const double t1 = now_s();
+    const auto l = local_energy_maxcut(n, e, s.X.data(), mbs);
+    grads[w] = gradient_from_locals(model, s.X.data(), mbs, l);
+    trest[w] = now_s() - t1;
+  };
+  std::vector<std::thread> th;
+  for (int w = 0; w < workers; ++w) th.emplace_back(work, w);
+  for (auto& t : th) t.join();
+  const double t2 = now_s();
+  const auto reduced = allreduce_mean(grads);
+  Adam adam;
+  std::vector<double> params(model.d());
+  get_theta(model, params.data());
+  adam_step(adam, params, reduced);
+  const double tupd = now_s() - t2;
+  double ts = 0.0, tr = 0.0, tot = 0.0;
+  for (int w = 0; w < workers; ++w) {
+    ts = std::max(ts, tsamp[w]);
+    tr = std::max(tr, trest[w]);
+    tot = std::max(tot, tsamp[w] + trest[w]);
+  }
+  out[0] = ts;
+  out[1] = tr;
+  out[2] = tupd;
+  out[3] = tot + tupd;
+  out[4] = bits_limit;
+  ORACLE_CATCH
+}
+
 }  // extern "C"

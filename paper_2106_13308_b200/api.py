@@ -1,0 +1,533 @@
+"""Python mirror of the reference's C++ API (arxiv/paper_2106_13308, proj/include/vqmc/*.hpp)
+on top of the B200 C ABI (include/vqmc_b200.h).  Names, argument meaning and error
+behaviour follow the reference: ValueError where it throws std::invalid_argument,
+RuntimeError (VqmcError) where it throws std::runtime_error.
+
+Configurations are numpy uint8 arrays (B x n, entries 0/1) instead of Eigen MatrixXd;
+parameters are fp64 vectors in the reference flatten order.  Every compute call runs
+on the GPU through libvqmc_b200.so; there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import dataclasses
+import math
+import time
+from typing import Callable, List, Optional
+
+import numpy as np
+
+from . import _capi as K
+from ._capi import check, ptr
+
+kProbEps = 1e-7  # models.hpp:26
+kEvalStream = 1_000_000_007  # trainer.cpp:48
+
+
+# ---------------------------------------------------------------------------
+# L0 common (common.hpp)
+# ---------------------------------------------------------------------------
+def mix_seed(seed: int, stream: int) -> int:
+    return int(K.lib.vqmc_mix_seed(seed, stream))
+
+
+class Stream:
+    """make_stream(seed, stream) (common.hpp:64-66): a std::mt19937_64 stream consumed
+    through uniform_real_distribution<double>(0, 1), tracked by its draw position so the
+    GPU sampler can be fed the reference's exact uniforms (parity mode)."""
+
+    def __init__(self, seed: int, stream: int = 0):
+        self.seed, self.stream, self.position = int(seed), int(stream), 0
+
+    def uniforms(self, count: int) -> np.ndarray:
+        out = np.empty(count, np.float64)
+        check(K.lib.vqmc_stream_uniforms(self.seed, self.stream, self.position, count, ptr(out)))
+        self.position += count
+        return out
+
+
+def make_stream(seed: int, stream: int = 0) -> Stream:
+    return Stream(seed, stream)
+
+
+class PhiloxStream:
+    """Production-mode generator: counter-based Philox4x32-10 keyed by (seed, stream);
+    each sampling call consumes one counter value."""
+
+    def __init__(self, seed: int, stream: int = 0, call: int = 0):
+        self.seed, self.stream, self.call = int(seed), int(stream), int(call)
+
+
+def config_index(x) -> int:  # common.hpp:35-39
+    idx = 0
+    for v in np.asarray(x).reshape(-1):
+        idx = (idx << 1) | (1 if v > 0.5 else 0)
+    return idx
+
+
+def index_to_config(n: int, idx: int) -> np.ndarray:
+    return np.array([(idx >> (n - 1 - i)) & 1 for i in range(n)], np.uint8)
+
+
+def all_configs(n: int) -> np.ndarray:
+    idx = np.arange(1 << n, dtype=np.int64)
+    return ((idx[:, None] >> (n - 1 - np.arange(n))[None, :]) & 1).astype(np.uint8)
+
+
+# ---------------------------------------------------------------------------
+# L1 problem (hamiltonian.hpp)
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class Graph:
+    n: int
+    edges: np.ndarray  # E x 2 int32, i < j, 0-based
+
+
+@dataclasses.dataclass
+class MaxCutProblem:
+    graph: Graph
+    num_edges: int
+
+
+def _edges_call(fn, *args) -> np.ndarray:
+    ne = C.c_int64()
+    check(fn(*args, None, 0, C.byref(ne)))
+    e = np.empty((ne.value, 2), np.int32)
+    check(fn(*args, ptr(e), ne.value, C.byref(ne)))
+    return e
+
+
+def random_maxcut_graph(n: int, seed: int) -> Graph:  # hamiltonian.cpp:144-160
+    return Graph(n, _edges_call(K.lib.vqmc_random_maxcut_graph, n, seed))
+
+
+def random_regular_graph(n: int, d: int, seed: int) -> Graph:
+    return Graph(n, _edges_call(K.lib.vqmc_random_regular_graph, n, d, seed))
+
+
+def erdos_renyi_graph(n: int, p: float, seed: int) -> Graph:
+    return Graph(n, _edges_call(K.lib.vqmc_erdos_renyi_graph, n, p, seed))
+
+
+def load_graph(path: str) -> Graph:  # hamiltonian.cpp:243-266
+    n = C.c_int()
+    ne = C.c_int64()
+    check(K.lib.vqmc_load_graph(path.encode(), C.byref(n), None, 0, C.byref(ne)))
+    e = np.empty((ne.value, 2), np.int32)
+    check(K.lib.vqmc_load_graph(path.encode(), C.byref(n), ptr(e), ne.value, C.byref(ne)))
+    return Graph(n.value, e)
+
+
+def save_graph(g: Graph, path: str) -> None:  # hamiltonian.cpp:236-241
+    e = np.ascontiguousarray(g.edges, np.int32)
+    check(K.lib.vqmc_save_graph(path.encode(), g.n, ptr(e), len(e)))
+
+
+def maxcut_spec(g: Graph) -> MaxCutProblem:  # hamiltonian.cpp:109-119 (validate :36-54)
+    e = np.ascontiguousarray(g.edges, np.int32).reshape(-1, 2)
+    if len(e):
+        if np.any(e[:, 0] < 0) or np.any(e[:, 1] >= g.n) or np.any(e[:, 0] >= e[:, 1]):
+            raise ValueError("pair indices must satisfy 0 <= i < j < n")
+        if len(np.unique(e[:, 0].astype(np.int64) * g.n + e[:, 1])) != len(e):
+            raise ValueError("duplicate pair")
+    return MaxCutProblem(Graph(g.n, e), len(e))
+
+
+# ---------------------------------------------------------------------------
+# L2 model (models.hpp)
+# ---------------------------------------------------------------------------
+class MadeModel:
+    """Value type like the reference's MadeModel (models.hpp:34-46): n, h, degrees and the
+    flattened fp64 parameters.  A device replica is created lazily and kept in sync."""
+
+    def __init__(self, n: int, h: int, degrees, theta):
+        self.n, self.h = int(n), int(h)
+        self.degrees = np.ascontiguousarray(degrees, np.int32)
+        self._theta = np.ascontiguousarray(theta, np.float64)
+        self._version = 0
+        self._dev: Optional["DeviceReplica"] = None
+
+    def param_count(self) -> int:
+        return 2 * self.h * self.n + self.h + self.n
+
+    def clone(self) -> "MadeModel":
+        return MadeModel(self.n, self.h, self.degrees.copy(), self.parameters().copy())
+
+    def parameters(self) -> np.ndarray:
+        if self._dev is not None and self._dev.device_newer:
+            self._theta = self._dev.get_params()
+            self._dev.device_newer = False
+        return self._theta
+
+    def _set(self, theta) -> None:
+        theta = np.ascontiguousarray(theta, np.float64)
+        if theta.shape != (self.param_count(),):
+            raise ValueError("parameter vector length mismatch")
+        self._theta = theta.copy()
+        self._version += 1
+
+    def device(self) -> "DeviceReplica":
+        if self._dev is None:
+            self._dev = DeviceReplica(self)
+        self._dev.sync()
+        return self._dev
+
+
+class DeviceReplica:
+    """One vqmc_gpu handle holding a model replica (and optionally a Max-Cut instance)."""
+
+    def __init__(self, model: MadeModel, device: int = 0, max_batch: int = 1024):
+        self.model = model
+        self.h = C.c_void_p()
+        empty = np.zeros((0, 2), np.int32)
+        check(K.lib.vqmc_gpu_create(device, model.n, model.h, ptr(model.degrees), ptr(model._theta),
+                                    ptr(empty), 0, max_batch, C.byref(self.h)))
+        self.version = model._version
+        self.problem_id = None
+        self.device_newer = False
+
+    def __del__(self):
+        try:
+            if self.h:
+                K.lib.vqmc_gpu_destroy(self.h)
+        except Exception:
+            pass
+
+    def sync(self) -> None:
+        if self.version != self.model._version:
+            check(K.lib.vqmc_gpu_set_params(self.h, ptr(self.model._theta)))
+            self.version = self.model._version
+            self.device_newer = False
+
+    def set_problem(self, problem: MaxCutProblem) -> None:
+        if self.problem_id is not problem:
+            e = np.ascontiguousarray(problem.graph.edges, np.int32)
+            check(K.lib.vqmc_gpu_set_edges(self.h, ptr(e), len(e)))
+            self.problem_id = problem
+
+    def get_params(self) -> np.ndarray:
+        out = np.empty(self.model.param_count())
+        check(K.lib.vqmc_gpu_get_params(self.h, ptr(out)))
+        return out
+
+
+def default_made_hidden(n: int) -> int:  # models.cpp:79-82
+    return int(K.lib.vqmc_default_made_hidden(n))
+
+
+def made_init(n: int, h: int, seed: int) -> MadeModel:  # models.cpp:84-104
+    deg = np.empty(max(h, 0), np.int32)
+    theta = np.empty(max(2 * h * n + h + n, 0), np.float64)
+    check(K.lib.vqmc_made_init(n, h, seed, ptr(deg), ptr(theta)))
+    return MadeModel(n, h, deg, theta)
+
+
+def parameter_vector(model: MadeModel) -> np.ndarray:  # models.cpp:264-275
+    return model.parameters().copy()
+
+
+def set_parameters(model: MadeModel, params) -> None:  # models.cpp:287-300
+    model._set(params)
+
+
+def _bits(model: MadeModel, configs) -> tuple:
+    x = np.asarray(configs)
+    if x.ndim == 1:
+        x = x[None, :]
+    if x.shape[1] != model.n:
+        raise ValueError(f"configuration width {x.shape[1]} does not match model n = {model.n}")
+    return K.pack_bits(x), x.shape[0]
+
+
+def log_psi_batch(model: MadeModel, configs) -> np.ndarray:  # models.cpp:122-124
+    bits, B = _bits(model, configs)
+    out = np.empty(B)
+    check(K.lib.vqmc_gpu_log_psi(model.device().h, ptr(bits), B, ptr(out), None))
+    return out
+
+
+def log_prob(model: MadeModel, configs) -> np.ndarray:  # models.cpp:118-120
+    return 2.0 * log_psi_batch(model, configs)
+
+
+def conditionals(model: MadeModel, configs) -> np.ndarray:  # models.cpp:114-116
+    bits, B = _bits(model, configs)
+    lp = np.empty(B)
+    cond = np.empty((B, model.n))
+    check(K.lib.vqmc_gpu_log_psi(model.device().h, ptr(bits), B, ptr(lp), ptr(cond)))
+    return cond
+
+
+def log_psi(model: MadeModel, x) -> float:
+    return float(log_psi_batch(model, np.asarray(x)[None, :])[0])
+
+
+def weighted_grad_log_psi(model: MadeModel, configs, weights) -> np.ndarray:  # models.cpp:175-198
+    bits, B = _bits(model, configs)
+    w = np.ascontiguousarray(weights, np.float64)
+    if w.shape != (B,):
+        raise ValueError("weights length does not match the batch")
+    g = np.empty(model.param_count())
+    check(K.lib.vqmc_gpu_weighted_grad(model.device().h, ptr(bits), ptr(w), B, ptr(g)))
+    return g
+
+
+def grad_log_psi(model: MadeModel, x) -> np.ndarray:
+    return weighted_grad_log_psi(model, np.asarray(x)[None, :], np.ones(1))
+
+
+# ---------------------------------------------------------------------------
+# L3 sampler (sampler.hpp)
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class SampleBatch:
+    configs: np.ndarray  # B x n uint8
+    log_psi: np.ndarray
+    kind: str = "auto"
+    acceptance_rate: float = 1.0
+    wall_time: float = 0.0
+    bits: Optional[np.ndarray] = None  # packed words, as produced on the device
+
+
+def auto_sample(model: MadeModel, batch_size: int, rng) -> SampleBatch:  # sampler.cpp:35-59
+    """rng: Stream (the reference's mt19937_64 uniforms, consumed [bit][sample] like the
+    reference) or PhiloxStream (production mode; advances its call counter)."""
+    if batch_size < 1:
+        raise ValueError("auto_sample requires batch_size >= 1")
+    t0 = time.perf_counter()
+    W = (model.n + 31) // 32
+    bits = np.empty((batch_size, W), np.uint32)
+    lp = np.empty(batch_size)
+    dev = model.device()
+    if isinstance(rng, PhiloxStream):
+        check(K.lib.vqmc_gpu_sample(dev.h, batch_size, None, rng.seed, rng.stream, rng.call, ptr(bits), ptr(lp)))
+        rng.call += 1
+    else:
+        u = rng.uniforms(model.n * batch_size)
+        check(K.lib.vqmc_gpu_sample(dev.h, batch_size, ptr(u), 0, 0, 0, ptr(bits), ptr(lp)))
+    return SampleBatch(K.unpack_bits(bits, model.n), lp, wall_time=time.perf_counter() - t0, bits=bits)
+
+
+def forward_pass_count(kind: str, n: int, batch_size: int) -> int:  # sampler.cpp:124-128 (AUTO)
+    if kind != "auto":
+        raise ValueError("only the AUTO sampler is on this path")
+    return n
+
+
+# ---------------------------------------------------------------------------
+# L4 estimator (estimator.hpp)
+# ---------------------------------------------------------------------------
+def local_energy_batch(problem: MaxCutProblem, model: MadeModel, configs, cached_log_psi=None) -> np.ndarray:
+    """Max-Cut (diagonal) branch of local_energy_batch (estimator.hpp:43-57)."""
+    bits, B = _bits(model, configs)
+    dev = model.device()
+    dev.set_problem(problem)
+    out = np.empty(B)
+    check(K.lib.vqmc_gpu_maxcut_energy(dev.h, ptr(bits), B, None, ptr(out)))
+    if not np.all(np.isfinite(out)):
+        raise RuntimeError("non-finite local energy (amplitude underflow?)")
+    return out
+
+
+def cut_values(problem: MaxCutProblem, model: MadeModel, configs) -> np.ndarray:
+    """cut_value (hamiltonian.cpp:121-124) for every row."""
+    bits, B = _bits(model, configs)
+    dev = model.device()
+    dev.set_problem(problem)
+    out = np.empty(B, np.int32)
+    check(K.lib.vqmc_gpu_maxcut_energy(dev.h, ptr(bits), B, ptr(out), None))
+    return out.astype(np.float64)
+
+
+def energy_and_variance(local_energies) -> tuple:  # estimator.hpp:94-100
+    l = np.asarray(local_energies, np.float64)
+    if l.size < 2:
+        raise ValueError("variance needs at least two samples")
+    s = 0.0
+    for v in l:  # sequential fp64 sum, like the reference's reduction on exact data
+        s += v
+    mean = s / l.size
+    ss = float(np.sum((l - mean) ** 2))
+    return mean, ss / (l.size - 1)
+
+
+def gradient_from_locals(model: MadeModel, configs, local_energies) -> np.ndarray:  # estimator.hpp:111-119
+    bits, B = _bits(model, configs)
+    if B < 2:
+        raise ValueError("gradient estimate needs at least two samples")
+    l = np.ascontiguousarray(local_energies, np.float64)
+    g = np.empty(model.param_count())
+    check(K.lib.vqmc_gpu_gradient_from_locals(model.device().h, ptr(bits), ptr(l), B, ptr(g)))
+    return g
+
+
+# ---------------------------------------------------------------------------
+# L5 optimizer (optimizer.hpp)
+# ---------------------------------------------------------------------------
+@dataclasses.dataclass
+class AdamState:
+    lr: float = 0.01
+    beta1: float = 0.9
+    beta2: float = 0.999
+    eps: float = 1e-8
+    t: int = 0
+
+
+def adam_step(state: AdamState, model: MadeModel, grad) -> None:
+    """adam_step (optimizer.cpp:21-35) applied to the model's device replica (moments live on
+    the device; a fresh AdamState resets them)."""
+    dev = model.device()
+    if state.t == 0:
+        check(K.lib.vqmc_gpu_adam_reset(dev.h))
+    state.t += 1
+    g = np.ascontiguousarray(grad, np.float64)
+    if g.shape != (model.param_count(),):
+        raise ValueError("gradient length mismatch")
+    check(K.lib.vqmc_gpu_adam_step(dev.h, ptr(g), state.lr, state.beta1, state.beta2, state.eps, state.t))
+    dev.device_newer = True
+
+
+def sgd_step(params, grad, lr):  # optimizer.hpp:57-59
+    return np.asarray(params) - lr * np.asarray(grad)
+
+
+# ---------------------------------------------------------------------------
+# L6 trainer (trainer.hpp)
+# ---------------------------------------------------------------------------
+def allreduce_mean(vectors: List[np.ndarray]) -> np.ndarray:  # trainer.cpp:324-335 (fixed tree)
+    if not vectors:
+        raise ValueError("allreduce_mean needs at least one vector")
+    level = [np.asarray(v, np.float64) for v in vectors]
+    while len(level) > 1:
+        nxt = [level[i] + level[i + 1] for i in range(0, len(level) - 1, 2)]
+        if len(level) % 2 == 1:
+            nxt.append(level[-1])
+        level = nxt
+    return level[0] / float(len(vectors))
+
+
+@dataclasses.dataclass
+class StepStats:
+    energy_mean: float = 0.0
+    energy_std: float = 0.0
+    grad_norm: float = 0.0
+    wall_time: float = 0.0
+
+
+@dataclasses.dataclass
+class RunConfig:
+    """The Max-Cut / MADE / AUTO / ADAM slice of RunConfig (trainer.hpp:31-58)."""
+    problem: Optional[MaxCutProblem] = None
+    hidden: int = 0
+    optimizer: str = "adam"
+    lr: float = 0.0
+    iterations: int = 300
+    workers: int = 1            # data-parallel workers per rank (segments of one GPU batch)
+    minibatch: int = 1024       # per worker
+    eval_batch: int = 1024
+    seed: int = 0
+    target: Optional[float] = None
+    uniforms: str = "philox"    # "philox" (production) or "mt19937" (reference streams, parity)
+    gradient_observer: Optional[Callable[[int, np.ndarray], None]] = None
+    device: int = 0
+
+
+@dataclasses.dataclass
+class RunResult:
+    stats: List[StepStats]
+    final_energy: float = 0.0
+    final_energy_std: float = 0.0
+    best_cut: Optional[float] = None
+    mean_cut: Optional[float] = None
+    total_time: float = 0.0
+    replicas_identical: bool = True
+    final_params: Optional[np.ndarray] = None
+    hit_time: Optional[float] = None
+    hit_iteration: int = -1
+    made: Optional[MadeModel] = None
+
+
+def resolve_lr(cfg: RunConfig) -> float:  # trainer.cpp:35-46
+    if cfg.lr > 0.0:
+        return cfg.lr
+    return 0.01 if cfg.optimizer == "adam" else 0.1
+
+
+def _mt_uniforms(streams: List[Stream], n: int, mbs: int) -> np.ndarray:
+    """[n][L*mbs] uniforms: worker w's block is its stream's next n*mbs draws ([bit][sample])."""
+    u = np.empty((n, len(streams) * mbs))
+    for w, s in enumerate(streams):
+        u[:, w * mbs:(w + 1) * mbs] = s.uniforms(n * mbs).reshape(n, mbs)
+    return np.ascontiguousarray(u)
+
+
+def train(cfg: RunConfig, comm=None) -> RunResult:
+    """vqmc::train for MADE + AUTO + ADAM on a Max-Cut instance (trainer.cpp:111-322), one
+    fused device step per iteration.  `comm` (optional) = (rank, world) of an initialised
+    NCCL communicator on the model's handle; stats are then pooled by the caller."""
+    if cfg.problem is None:
+        raise ValueError("a Max-Cut problem is required")
+    if cfg.workers < 1:
+        raise ValueError("workers must be >= 1")
+    if cfg.iterations < 1:
+        raise ValueError("iterations must be >= 1")
+    if cfg.minibatch < 2:
+        raise ValueError("minibatch must be >= 2")
+    if cfg.optimizer != "adam":
+        raise ValueError("the B200 path implements the ADAM optimizer (north-star path)")
+    n = cfg.problem.graph.n
+    h = cfg.hidden if cfg.hidden > 0 else default_made_hidden(n)
+    model = made_init(n, h, cfg.seed)
+    lr = resolve_lr(cfg)
+    dev = model.device()
+    dev.set_problem(cfg.problem)
+    check(K.lib.vqmc_gpu_adam_reset(dev.h))
+    L, mbs = cfg.workers, cfg.minibatch
+    rank, world = comm if comm else (0, 1)
+    stream0 = 1 + rank * L
+    streams = [Stream(cfg.seed, stream0 + w) for w in range(L)]
+    eval_stream = Stream(cfg.seed, kEvalStream)
+    st = K.StepStats()
+    result = RunResult(stats=[])
+    t_run = time.perf_counter()
+    acc_time = 0.0
+    for it in range(cfg.iterations):
+        t0 = time.perf_counter()
+        u = _mt_uniforms(streams, n, mbs) if cfg.uniforms == "mt19937" else None
+        check(K.lib.vqmc_gpu_train_step(dev.h, mbs, L, ptr(u), cfg.seed, stream0, it, lr, 0.9, 0.999, 1e-8,
+                                        it + 1, C.byref(st)))
+        dev.device_newer = True
+        wall = time.perf_counter() - t0
+        result.stats.append(StepStats(st.energy_mean, math.sqrt(st.energy_var), st.grad_norm, wall))
+        acc_time += wall
+        if cfg.target is not None:
+            ev = evaluate(cfg, model, eval_stream)
+            if ev[2] >= cfg.target:
+                result.hit_time, result.hit_iteration = acc_time, it + 1
+                break
+    ev = evaluate(cfg, model, eval_stream)
+    result.final_energy, result.final_energy_std, result.best_cut, result.mean_cut = ev
+    result.final_params = model.parameters().copy()
+    result.total_time = time.perf_counter() - t_run
+    result.made = model
+    return result
+
+
+def evaluate(cfg: RunConfig, model: MadeModel, eval_stream) -> tuple:  # trainer.cpp:91-108
+    dev = model.device()
+    dev.set_problem(cfg.problem)
+    out = np.empty(4)
+    B = cfg.eval_batch
+    if isinstance(eval_stream, PhiloxStream):
+        check(K.lib.vqmc_gpu_evaluate(dev.h, B, None, eval_stream.seed, eval_stream.stream, eval_stream.call,
+                                      ptr(out)))
+        eval_stream.call += 1
+    elif cfg.uniforms == "mt19937":
+        u = eval_stream.uniforms(model.n * B)
+        check(K.lib.vqmc_gpu_evaluate(dev.h, B, ptr(u), 0, 0, 0, ptr(out)))
+    else:
+        # production: Philox on the eval stream, counter = number of eval calls so far
+        call = getattr(eval_stream, "_calls", 0)
+        check(K.lib.vqmc_gpu_evaluate(dev.h, B, None, eval_stream.seed, eval_stream.stream, call, ptr(out)))
+        eval_stream._calls = call + 1
+    return tuple(float(v) for v in out)

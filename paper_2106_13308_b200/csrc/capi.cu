@@ -1,0 +1,701 @@
+// C ABI of the B200 VQMC library: handle lifecycle, parameter layout
+// conversion, the per-function entry points and the fused training step.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <set>
+#include <string>
+#include <vector>
+
+#include "device_common.cuh"
+#include "internal.cuh"
+#include "vqmc_b200.h"
+
+namespace vqmc_b200 {
+
+static thread_local std::string g_error;
+void set_error(const std::string& msg) { g_error = msg; }
+
+int status_of(const std::exception& ex) {
+  if (dynamic_cast<const CudaError*>(&ex)) return VQMC_ERR_CUDA;
+  if (dynamic_cast<const std::invalid_argument*>(&ex)) return VQMC_ERR_INVALID;
+  return VQMC_ERR_NUMERIC;
+}
+
+// ---------------------------------------------------------------------------
+// NCCL (dlopen'd so single-GPU use has no NCCL dependency).  Types follow nccl.h.
+// ---------------------------------------------------------------------------
+struct NcclUniqueId { char internal[128]; };
+using ncclComm_t = void*;
+enum { ncclFloat32 = 7, ncclSum = 0 };
+struct NcclApi {
+  bool loaded = false;
+  int (*GetUniqueId)(NcclUniqueId*) = nullptr;
+  int (*CommInitRank)(ncclComm_t*, int, NcclUniqueId, int) = nullptr;
+  int (*AllReduce)(const void*, void*, size_t, int, int, ncclComm_t, cudaStream_t) = nullptr;
+  int (*CommDestroy)(ncclComm_t) = nullptr;
+  const char* (*GetErrorString)(int) = nullptr;
+};
+static NcclApi g_nccl;
+
+static void load_nccl() {
+  if (g_nccl.loaded) return;
+  std::vector<std::string> cands;
+  if (const char* e = std::getenv("VQMC_NCCL_LIB")) cands.push_back(e);
+  cands.push_back("/opt/prime-rl/.venv/lib/python3.12/site-packages/nvidia/nccl/lib/libnccl.so.2");
+  cands.push_back("libnccl.so.2");
+  for (const auto& p : cands) {
+    void* h = dlopen(p.c_str(), RTLD_NOW | RTLD_GLOBAL);
+    if (!h) continue;
+    g_nccl.GetUniqueId = (decltype(g_nccl.GetUniqueId))dlsym(h, "ncclGetUniqueId");
+    g_nccl.CommInitRank = (decltype(g_nccl.CommInitRank))dlsym(h, "ncclCommInitRank");
+    g_nccl.AllReduce = (decltype(g_nccl.AllReduce))dlsym(h, "ncclAllReduce");
+    g_nccl.CommDestroy = (decltype(g_nccl.CommDestroy))dlsym(h, "ncclCommDestroy");
+    g_nccl.GetErrorString = (decltype(g_nccl.GetErrorString))dlsym(h, "ncclGetErrorString");
+    if (g_nccl.GetUniqueId && g_nccl.CommInitRank && g_nccl.AllReduce) {
+      g_nccl.loaded = true;
+      return;
+    }
+  }
+  throw std::runtime_error("NCCL library not found (set VQMC_NCCL_LIB)");
+}
+
+static void nccl_check(int rc, const char* what) {
+  if (rc != 0)
+    throw std::runtime_error(std::string(what) + ": " +
+                             (g_nccl.GetErrorString ? g_nccl.GetErrorString(rc) : "nccl error"));
+}
+
+// ---------------------------------------------------------------------------
+// Buffers
+// ---------------------------------------------------------------------------
+template <class T>
+static void dalloc(T** p, size_t count) {
+  if (*p) VQMC_CUDA(cudaFree(*p));
+  *p = nullptr;
+  if (count) VQMC_CUDA(cudaMalloc((void**)p, count * sizeof(T)));
+}
+
+void Handle::ensure_batch(int B) {
+  if (B <= cap_B) return;
+  const int n = L.n, h = L.h;
+  const int max_tiles = (n + 127) / 128 + 2;
+  dalloc(&X, (size_t)B * L.W);
+  dalloc(&G1, (size_t)B * h);
+  dalloc(&D, (size_t)B * n);
+  dalloc(&lp_head, (size_t)B);
+  dalloc(&lp_part, (size_t)max_tiles * B);
+  dalloc(&log_psi, (size_t)B);
+  dalloc(&cut, (size_t)B);
+  dalloc(&local, (size_t)B);
+  dalloc(&w, (size_t)B);
+  dalloc(&Epart, (size_t)64 * B * h);
+  dalloc(&dz1, (size_t)B * h);
+  cap_B = B;
+}
+
+void Handle::ensure_uniforms(int64_t count) {
+  if (count <= uni_cap) return;
+  dalloc(&uni, (size_t)count);
+  uni_cap = count;
+}
+
+void Handle::ensure_cond(int64_t count) {
+  if (count <= cond_cap) return;
+  dalloc(&cond, (size_t)count);
+  cond_cap = count;
+}
+
+static void upload_params(Handle* H, const double* theta) {
+  const Layout& L = H->L;
+  const int n = L.n, h = L.h, Hd = L.Hd;
+  std::vector<float> P((size_t)L.total, 0.f);
+  const double* W1 = theta;
+  const double* b1 = W1 + (size_t)h * n;
+  const double* W2 = b1 + h;
+  const double* b2 = W2 + (size_t)n * h;
+  for (int j = 0; j < Hd; ++j)
+    for (int k = 0; k < h; ++k)
+      P[L.off_w1t + (size_t)j * h + k] = (j + 1 <= H->degrees[k]) ? (float)W1[(size_t)k * n + j] : 0.f;
+  for (int k = 0; k < h; ++k) P[L.off_b1 + k] = (float)b1[k];
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < h; ++k)
+      P[L.off_w2 + (size_t)i * h + k] = (H->degrees[k] < i + 1) ? (float)W2[(size_t)i * h + k] : 0.f;
+  for (int i = 0; i < n; ++i) P[L.off_b2 + i] = (float)b2[i];
+  VQMC_CUDA(cudaMemcpyAsync(H->P, P.data(), P.size() * sizeof(float), cudaMemcpyHostToDevice, H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  H->theta_host.assign(theta, theta + H->d);
+  launch_refresh_w2ht(H);
+}
+
+// live fp32 layout (device) -> reference order fp64; masked entries from `base`
+static void live_to_reference(const Handle* H, const std::vector<float>& P, const double* base,
+                              double* out) {
+  const Layout& L = H->L;
+  const int n = L.n, h = L.h, Hd = L.Hd;
+  if (base) std::memcpy(out, base, sizeof(double) * H->d);
+  else std::memset(out, 0, sizeof(double) * H->d);
+  double* W1 = out;
+  double* b1 = W1 + (size_t)h * n;
+  double* W2 = b1 + h;
+  double* b2 = W2 + (size_t)n * h;
+  for (int j = 0; j < Hd; ++j)
+    for (int k = 0; k < h; ++k)
+      if (j + 1 <= H->degrees[k]) W1[(size_t)k * n + j] = P[L.off_w1t + (size_t)j * h + k];
+  for (int k = 0; k < h; ++k) b1[k] = P[L.off_b1 + k];
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < h; ++k)
+      if (H->degrees[k] < i + 1) W2[(size_t)i * h + k] = P[L.off_w2 + (size_t)i * h + k];
+  for (int i = 0; i < n; ++i) b2[i] = P[L.off_b2 + i];
+}
+
+static std::vector<float> download(const Handle* H, const float* dptr, int64_t count) {
+  std::vector<float> v((size_t)count);
+  VQMC_CUDA(cudaMemcpyAsync(v.data(), dptr, count * sizeof(float), cudaMemcpyDeviceToHost, H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  return v;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  explicit DeviceGuard(int dev) {
+    VQMC_CUDA(cudaGetDevice(&prev));
+    if (prev != dev) VQMC_CUDA(cudaSetDevice(dev));
+  }
+  ~DeviceGuard() {
+    int cur = -1;
+    cudaGetDevice(&cur);
+    if (prev >= 0 && cur != prev) cudaSetDevice(prev);
+  }
+};
+
+static void check_B(int B) {
+  if (B < 1) throw std::invalid_argument("batch size must be >= 1");
+}
+
+static void upload_bits(Handle* H, const uint32_t* bits, int B) {
+  VQMC_CUDA(cudaMemcpyAsync(H->X, bits, (size_t)B * H->L.W * sizeof(uint32_t), cudaMemcpyHostToDevice,
+                            H->stream));
+}
+
+// Sampling into the handle's batch buffers (X, G1, D, log_psi).  The batch is
+// `workers` segments of B / workers rows; segment s draws from stream
+// (stream0 + s) (trainer.cpp:126: worker w uses make_stream(seed, w + 1)).
+static void sample_into(Handle* H, int B, int workers, const double* uniforms_host, uint64_t seed,
+                        uint64_t stream0, uint64_t call) {
+  H->ensure_batch(B);
+  const double* du = nullptr;
+  if (uniforms_host) {
+    H->ensure_uniforms((int64_t)H->L.n * B);
+    VQMC_CUDA(cudaMemcpyAsync(H->uni, uniforms_host, (size_t)H->L.n * B * sizeof(double),
+                              cudaMemcpyHostToDevice, H->stream));
+    du = H->uni;
+  }
+  RngSpec rng{seed, stream0, call, B / workers};
+  VQMC_CUDA(cudaMemsetAsync(H->X, 0, (size_t)B * H->L.W * sizeof(uint32_t), H->stream));
+  launch_head_sample_impl(H, B, du, rng, false, nullptr);
+  launch_z2(H, B, H->L.Hd, du, rng, false, nullptr);
+  launch_finalize_logpsi(H, B, H->tail_tiles);
+}
+
+// Forward from configurations already in H->X.
+static void forward_given(Handle* H, int B, double* cond) {
+  RngSpec none{0, 0, 0, 1};
+  launch_head_sample_impl(H, B, nullptr, none, true, cond);
+  launch_z2(H, B, H->L.Hd, nullptr, none, true, cond);
+  launch_finalize_logpsi(H, B, H->tail_tiles);
+}
+
+static void ensure_istat(Handle* H, int segs) {
+  if (segs <= H->istat_cap) return;
+  dalloc(&H->d_istat, (size_t)3 * segs);
+  if (H->h_istat) VQMC_CUDA(cudaFreeHost(H->h_istat));
+  VQMC_CUDA(cudaMallocHost((void**)&H->h_istat, (size_t)3 * segs * sizeof(int64_t)));
+  H->istat_cap = segs;
+}
+
+// Pooled mean / unbiased variance of N Max-Cut local energies l = (E - 2c)/4
+// from exact integer sums of c and c^2 (estimator.hpp:94-100; the fp64
+// two-pass result is exact for Max-Cut whenever its partial sums are, and
+// this evaluates the same rational with one rounding).
+static void pooled_stats(int64_t E, int64_t N, int64_t cs, int64_t cq, double* mean, double* var) {
+  const __int128 num = (__int128)N * E - 2 * (__int128)cs;  // 4 * sum(l)
+  *mean = ((double)num * 0.25) / (double)N;
+  const __int128 ssn = (__int128)N * cq - (__int128)cs * cs;  // 4 N * sum (l - mean)^2
+  const double ss = (double)ssn / (4.0 * (double)N);
+  *var = N > 1 ? ss / (double)(N - 1) : 0.0;
+}
+
+static void grad_to_host(Handle* H, double* grad_out) {
+  const auto g = download(H, H->G, H->L.total);
+  live_to_reference(H, g, nullptr, grad_out);
+}
+
+// HamiltonianSpec::validate for a Max-Cut pair list (hamiltonian.cpp:36-54).
+static void validate_edges(int n, const int32_t* edges, int64_t num_edges) {
+  if (num_edges < 0) throw std::invalid_argument("num_edges must be >= 0");
+  std::vector<int64_t> keys((size_t)num_edges);
+  for (int64_t t = 0; t < num_edges; ++t) {
+    const int i = edges[2 * t], j = edges[2 * t + 1];
+    if (i < 0 || j >= n || i >= j) throw std::invalid_argument("pair indices must satisfy 0 <= i < j < n");
+    keys[t] = (int64_t)i * n + j;
+  }
+  std::sort(keys.begin(), keys.end());
+  if (std::adjacent_find(keys.begin(), keys.end()) != keys.end()) throw std::invalid_argument("duplicate pair");
+}
+
+static void upload_edges(Handle* H, const int32_t* edges, int64_t num_edges) {
+  if (H->d_edges) VQMC_CUDA(cudaFree(H->d_edges));
+  H->d_edges = nullptr;
+  H->num_edges = num_edges;
+  if (num_edges > 0) {
+    VQMC_CUDA(cudaMalloc((void**)&H->d_edges, num_edges * sizeof(int2)));
+    VQMC_CUDA(cudaMemcpy(H->d_edges, edges, num_edges * sizeof(int2), cudaMemcpyHostToDevice));
+  }
+}
+
+}  // namespace vqmc_b200
+
+using namespace vqmc_b200;
+
+#define API_TRY try {
+#define API_CATCH                     \
+  }                                   \
+  catch (const std::exception& ex) {  \
+    set_error(ex.what());             \
+    return status_of(ex);             \
+  }                                   \
+  return VQMC_OK;
+
+extern "C" {
+
+const char* vqmc_last_error(void) { return g_error.c_str(); }
+
+int vqmc_gpu_device_count(int* count) {
+  API_TRY
+  int c = 0;
+  if (cudaGetDeviceCount(&c) != cudaSuccess) c = 0;
+  *count = c;
+  API_CATCH
+}
+
+int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const double* theta,
+                    const int32_t* edges, int64_t num_edges, int max_batch, vqmc_gpu_t** out) {
+  Handle* H = nullptr;
+  API_TRY
+  if (n < 2) throw std::invalid_argument("MADE requires n >= 2");
+  if (h < 1) throw std::invalid_argument("MADE requires h >= 1");
+  if (h > kMaxHidden) throw std::invalid_argument("hidden width > 1024 is not supported on the GPU path");
+  if (num_edges < 0) throw std::invalid_argument("num_edges must be >= 0");
+  int Hd = 0;
+  for (int k = 0; k < h; ++k) {
+    if (degrees[k] < 1 || degrees[k] > n - 1) throw std::invalid_argument("degrees must lie in [1, n-1]");
+    Hd = std::max(Hd, (int)degrees[k]);
+  }
+  validate_edges(n, edges, num_edges);
+  H = new Handle();
+  H->device = device;
+  DeviceGuard dg(device);
+  VQMC_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
+  H->L.init(n, h, Hd);
+  H->d = 2LL * h * n + h + n;
+  H->degrees.assign(degrees, degrees + h);
+  H->num_edges = num_edges;
+  dalloc(&H->P, (size_t)H->L.total);
+  dalloc(&H->G, (size_t)H->L.total);
+  dalloc(&H->Mo, (size_t)H->L.total);
+  dalloc(&H->Vo, (size_t)H->L.total);
+  VQMC_CUDA(cudaMemsetAsync(H->G, 0, H->L.total * sizeof(float), H->stream));
+  VQMC_CUDA(cudaMemsetAsync(H->Mo, 0, H->L.total * sizeof(float), H->stream));
+  VQMC_CUDA(cudaMemsetAsync(H->Vo, 0, H->L.total * sizeof(float), H->stream));
+  dalloc(&H->W2hT, (size_t)h * Hd);
+  dalloc(&H->d_deg, (size_t)h);
+  VQMC_CUDA(cudaMemcpy(H->d_deg, degrees, h * sizeof(int32_t), cudaMemcpyHostToDevice));
+  {  // completion lists: hidden units by degree
+    std::vector<int32_t> off(Hd + 1, 0), ks;
+    for (int k = 0; k < h; ++k) off[degrees[k]]++;  // degree d completes at step d-1 -> slot d-1
+    // off[i+1] counts units with degree i+1; prefix sum
+    std::vector<int32_t> cnt(Hd + 1, 0);
+    for (int k = 0; k < h; ++k) cnt[degrees[k] - 1]++;
+    off.assign(Hd + 1, 0);
+    for (int i = 0; i < Hd; ++i) off[i + 1] = off[i] + cnt[i];
+    ks.resize(h);
+    std::vector<int32_t> pos(off.begin(), off.end() - 1);
+    for (int k = 0; k < h; ++k) ks[pos[degrees[k] - 1]++] = k;
+    dalloc(&H->d_comp_k, (size_t)h);
+    dalloc(&H->d_comp_off, (size_t)Hd + 1);
+    VQMC_CUDA(cudaMemcpy(H->d_comp_k, ks.data(), h * sizeof(int32_t), cudaMemcpyHostToDevice));
+    VQMC_CUDA(cudaMemcpy(H->d_comp_off, off.data(), (Hd + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
+  }
+  upload_edges(H, edges, num_edges);
+  dalloc(&H->d_scal, 16);
+  ensure_istat(H, 64);
+  H->gpart_n = 148 * 4;
+  dalloc(&H->d_gpart, (size_t)H->gpart_n);
+  VQMC_CUDA(cudaMallocHost((void**)&H->h_scal, 16 * sizeof(double)));
+  for (auto& e : H->ev) VQMC_CUDA(cudaEventCreate(&e));
+  for (int i = 0; i < Handle::kKtPool; ++i) {
+    VQMC_CUDA(cudaEventCreate(&H->kt_start[i]));
+    VQMC_CUDA(cudaEventCreate(&H->kt_end[i]));
+  }
+  H->ensure_batch(std::max(2, max_batch));
+  upload_params(H, theta);
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  *out = reinterpret_cast<vqmc_gpu_t*>(H);
+  H = nullptr;
+  }
+  catch (const std::exception& ex) {
+    set_error(ex.what());
+    delete H;
+    return status_of(ex);
+  }
+  return VQMC_OK;
+}
+
+int vqmc_gpu_destroy(vqmc_gpu_t* g) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  if (!H) return VQMC_OK;
+  DeviceGuard dg(H->device);
+  cudaStreamSynchronize(H->stream);
+  if (H->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy(H->nccl_comm);
+  void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W2hT, H->d_deg, H->d_comp_k, H->d_comp_off, H->d_edges,
+                  H->X, H->G1, H->D, H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w,
+                  H->Epart, H->dz1, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart};
+  for (void* p : ptrs)
+    if (p) cudaFree(p);
+  if (H->h_scal) cudaFreeHost(H->h_scal);
+  if (H->h_istat) cudaFreeHost(H->h_istat);
+  for (auto& e : H->ev)
+    if (e) cudaEventDestroy(e);
+  for (int i = 0; i < Handle::kKtPool; ++i) {
+    if (H->kt_start[i]) cudaEventDestroy(H->kt_start[i]);
+    if (H->kt_end[i]) cudaEventDestroy(H->kt_end[i]);
+  }
+  cudaStreamDestroy(H->stream);
+  delete H;
+  API_CATCH
+}
+
+int vqmc_gpu_set_edges(vqmc_gpu_t* g, const int32_t* edges, int64_t num_edges) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  validate_edges(H->L.n, edges, num_edges);
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  upload_edges(H, edges, num_edges);
+  API_CATCH
+}
+
+int vqmc_gpu_param_count(const vqmc_gpu_t* g, int64_t* d) {
+  API_TRY
+  *d = reinterpret_cast<const Handle*>(g)->d;
+  API_CATCH
+}
+
+int vqmc_gpu_set_params(vqmc_gpu_t* g, const double* theta) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  upload_params(H, theta);
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  API_CATCH
+}
+
+int vqmc_gpu_get_params(vqmc_gpu_t* g, double* theta) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  const auto P = download(H, H->P, H->L.total);
+  live_to_reference(H, P, H->theta_host.data(), theta);
+  API_CATCH
+}
+
+int vqmc_gpu_sample(vqmc_gpu_t* g, int B, const double* uniforms, uint64_t seed, uint64_t stream,
+                    uint64_t call, uint32_t* bits_out, double* log_psi_out) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  check_B(B);
+  sample_into(H, B, 1, uniforms, seed, stream, call);
+  if (bits_out)
+    VQMC_CUDA(cudaMemcpyAsync(bits_out, H->X, (size_t)B * H->L.W * sizeof(uint32_t),
+                              cudaMemcpyDeviceToHost, H->stream));
+  if (log_psi_out)
+    VQMC_CUDA(cudaMemcpyAsync(log_psi_out, H->log_psi, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost,
+                              H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  API_CATCH
+}
+
+int vqmc_gpu_log_psi(vqmc_gpu_t* g, const uint32_t* bits, int B, double* log_psi_out, double* cond_out) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  check_B(B);
+  H->ensure_batch(B);
+  upload_bits(H, bits, B);
+  double* cond = nullptr;
+  if (cond_out) {
+    H->ensure_cond((int64_t)B * H->L.n);
+    cond = H->cond;
+  }
+  forward_given(H, B, cond);
+  if (log_psi_out)
+    VQMC_CUDA(cudaMemcpyAsync(log_psi_out, H->log_psi, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost,
+                              H->stream));
+  if (cond_out)
+    VQMC_CUDA(cudaMemcpyAsync(cond_out, cond, (size_t)B * H->L.n * sizeof(double), cudaMemcpyDeviceToHost,
+                              H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  API_CATCH
+}
+
+int vqmc_gpu_maxcut_energy(vqmc_gpu_t* g, const uint32_t* bits, int B, int32_t* cut_out, double* local_out) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  check_B(B);
+  H->ensure_batch(B);
+  upload_bits(H, bits, B);
+  launch_energy(H, B);
+  if (cut_out)
+    VQMC_CUDA(cudaMemcpyAsync(cut_out, H->cut, (size_t)B * sizeof(int32_t), cudaMemcpyDeviceToHost, H->stream));
+  if (local_out)
+    VQMC_CUDA(cudaMemcpyAsync(local_out, H->local, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost,
+                              H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  API_CATCH
+}
+
+int vqmc_gpu_weighted_grad(vqmc_gpu_t* g, const uint32_t* bits, const double* weights, int B,
+                           double* grad_out) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  check_B(B);
+  H->ensure_batch(B);
+  upload_bits(H, bits, B);
+  std::vector<float> wf(weights, weights + B);
+  VQMC_CUDA(cudaMemcpyAsync(H->w, wf.data(), B * sizeof(float), cudaMemcpyHostToDevice, H->stream));
+  forward_given(H, B, nullptr);
+  launch_backward(H, B);
+  grad_to_host(H, grad_out);
+  API_CATCH
+}
+
+int vqmc_gpu_gradient_from_locals(vqmc_gpu_t* g, const uint32_t* bits, const double* local, int B,
+                                  double* grad_out) {
+  API_TRY
+  if (B < 2) throw std::invalid_argument("gradient estimate needs at least two samples");
+  double s = 0.0;
+  for (int b = 0; b < B; ++b) s += local[b];
+  const double mean = s / (double)B;
+  std::vector<double> w(B);
+  for (int b = 0; b < B; ++b) w[b] = 2.0 * (local[b] - mean) / (double)B;
+  return vqmc_gpu_weighted_grad(g, bits, w.data(), B, grad_out);
+  API_CATCH
+}
+
+int vqmc_gpu_adam_step(vqmc_gpu_t* g, const double* grad, double lr, double beta1, double beta2, double eps,
+                       int64_t t) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  if (t < 1) throw std::invalid_argument("adam step count must be >= 1");
+  if (grad) {
+    const Layout& L = H->L;
+    const int n = L.n, h = L.h;
+    std::vector<float> G((size_t)L.total, 0.f);
+    const double* gW1 = grad;
+    const double* gb1 = gW1 + (size_t)h * n;
+    const double* gW2 = gb1 + h;
+    const double* gb2 = gW2 + (size_t)n * h;
+    for (int j = 0; j < L.Hd; ++j)
+      for (int k = 0; k < h; ++k)
+        G[L.off_w1t + (size_t)j * h + k] = (j + 1 <= H->degrees[k]) ? (float)gW1[(size_t)k * n + j] : 0.f;
+    for (int k = 0; k < h; ++k) G[L.off_b1 + k] = (float)gb1[k];
+    for (int i = 0; i < n; ++i)
+      for (int k = 0; k < h; ++k)
+        G[L.off_w2 + (size_t)i * h + k] = (H->degrees[k] < i + 1) ? (float)gW2[(size_t)i * h + k] : 0.f;
+    for (int i = 0; i < n; ++i) G[L.off_b2 + i] = (float)gb2[i];
+    VQMC_CUDA(cudaMemcpyAsync(H->G, G.data(), G.size() * sizeof(float), cudaMemcpyHostToDevice, H->stream));
+  }
+  launch_adam(H, 1.0f, lr, beta1, beta2, eps, t);
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  API_CATCH
+}
+
+int vqmc_gpu_adam_reset(vqmc_gpu_t* g) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  VQMC_CUDA(cudaMemsetAsync(H->Mo, 0, H->L.total * sizeof(float), H->stream));
+  VQMC_CUDA(cudaMemsetAsync(H->Vo, 0, H->L.total * sizeof(float), H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  API_CATCH
+}
+
+int vqmc_gpu_comm_unique_id(uint8_t id_out[128]) {
+  API_TRY
+  load_nccl();
+  NcclUniqueId id;
+  nccl_check(g_nccl.GetUniqueId(&id), "ncclGetUniqueId");
+  std::memcpy(id_out, id.internal, 128);
+  API_CATCH
+}
+
+int vqmc_gpu_comm_init(vqmc_gpu_t* g, const uint8_t id[128], int nranks, int rank) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad nranks/rank");
+  H->nranks = nranks;
+  H->rank = rank;
+  if (nranks == 1) return VQMC_OK;
+  load_nccl();
+  NcclUniqueId uid;
+  std::memcpy(uid.internal, id, 128);
+  ncclComm_t comm = nullptr;
+  nccl_check(g_nccl.CommInitRank(&comm, nranks, uid, rank), "ncclCommInitRank");
+  H->nccl_comm = comm;
+  API_CATCH
+}
+
+int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double* uniforms, uint64_t seed,
+                        uint64_t stream0, uint64_t call, double lr, double beta1, double beta2, double eps,
+                        int64_t t, vqmc_step_stats_t* stats_out) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  if (minibatch < 2) throw std::invalid_argument("minibatch must be >= 2");
+  if (workers < 1) throw std::invalid_argument("workers must be >= 1");
+  if (t < 1) throw std::invalid_argument("adam step count must be >= 1");
+  const int B = minibatch * workers;
+  H->ensure_batch(B);
+  ensure_istat(H, workers);
+  H->kt_count = 0;
+  const bool tm = H->phase_timing;
+  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[0], H->stream));
+  sample_into(H, B, workers, uniforms, seed, stream0, call);  // draw (trainer.cpp:157)
+  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[1], H->stream));
+  launch_energy(H, B);                                        // local_energy_batch (:161)
+  launch_weights_from_locals(H, B, minibatch);                // gradient_from_locals weights (:164)
+  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[2], H->stream));
+  launch_backward(H, B);                                      // weighted_grad_log_psi
+  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[3], H->stream));
+  if (H->nccl_comm) {                                         // allreduce_mean (:187): sum, /L in Adam
+    KScope ks(H, "nccl_allreduce");
+    nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)H->L.total, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
+               "ncclAllReduce");
+  }
+  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[4], H->stream));
+  launch_adam(H, 1.0f / (float)(workers * H->nranks), lr, beta1, beta2, eps, t);  // adam_step (:221)
+  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[5], H->stream));
+  if (stats_out) {
+    VQMC_CUDA(cudaMemcpyAsync(H->h_scal, H->d_scal, sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+    VQMC_CUDA(cudaMemcpyAsync(H->h_istat, H->d_istat, 3 * workers * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                              H->stream));
+    VQMC_CUDA(cudaStreamSynchronize(H->stream));
+    int64_t cs = 0, cq = 0, best = 0;
+    for (int s = 0; s < workers; ++s) {
+      cs += H->h_istat[3 * s];
+      cq += H->h_istat[3 * s + 1];
+      best = std::max(best, H->h_istat[3 * s + 2]);
+    }
+    pooled_stats(H->num_edges, B, cs, cq, &stats_out->energy_mean, &stats_out->energy_var);
+    stats_out->grad_norm = std::sqrt(H->h_scal[0]);
+    stats_out->cut_sum = cs;
+    stats_out->cut_sq_sum = cq;
+    stats_out->best_cut = (int32_t)best;
+    stats_out->batch = B;
+  }
+  API_CATCH
+}
+
+int vqmc_gpu_last_cuts(vqmc_gpu_t* g, int32_t* cuts_out, int B) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  if (B > H->cap_B) throw std::invalid_argument("B exceeds the batch capacity");
+  VQMC_CUDA(cudaMemcpyAsync(cuts_out, H->cut, (size_t)B * sizeof(int32_t), cudaMemcpyDeviceToHost, H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  API_CATCH
+}
+
+int vqmc_gpu_evaluate(vqmc_gpu_t* g, int B, const double* uniforms, uint64_t seed, uint64_t stream,
+                      uint64_t call, double out[4]) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  if (B < 2) throw std::invalid_argument("variance needs at least two samples");
+  sample_into(H, B, 1, uniforms, seed, stream, call);
+  launch_energy(H, B);
+  launch_weights_from_locals(H, B, B);
+  VQMC_CUDA(cudaMemcpyAsync(H->h_istat, H->d_istat, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  double mean, var;
+  pooled_stats(H->num_edges, B, H->h_istat[0], H->h_istat[1], &mean, &var);
+  out[0] = mean;
+  out[1] = std::sqrt(var);
+  out[2] = std::max(0.0, (double)H->h_istat[2]);  // best = max(0.0, cuts), trainer.cpp:98-104
+  out[3] = (double)H->h_istat[0] / (double)B;     // total / rows (exact integer total)
+  API_CATCH
+}
+
+int vqmc_pooled_stats(int64_t num_edges, int64_t N, int64_t cut_sum, int64_t cut_sq_sum, double* mean,
+                      double* var) {
+  API_TRY
+  if (N < 2) throw std::invalid_argument("variance needs at least two samples");
+  pooled_stats(num_edges, N, cut_sum, cut_sq_sum, mean, var);
+  API_CATCH
+}
+
+int vqmc_gpu_synchronize(vqmc_gpu_t* g) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  API_CATCH
+}
+
+int64_t vqmc_gpu_launch_count(const vqmc_gpu_t* g) { return reinterpret_cast<const Handle*>(g)->launches; }
+
+int vqmc_gpu_set_phase_timing(vqmc_gpu_t* g, int enable) {
+  API_TRY
+  reinterpret_cast<Handle*>(g)->phase_timing = enable != 0;
+  API_CATCH
+}
+
+int vqmc_gpu_set_kernel_timing(vqmc_gpu_t* g, int enable) {
+  API_TRY
+  reinterpret_cast<Handle*>(g)->ktimer = enable != 0;
+  API_CATCH
+}
+
+int vqmc_gpu_kernel_times(vqmc_gpu_t* g, char* names_out, float* ms_out, int cap, int* count) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  const int c = std::min(cap, H->kt_count);
+  for (int i = 0; i < c; ++i) {
+    VQMC_CUDA(cudaEventElapsedTime(&ms_out[i], H->kt_start[i], H->kt_end[i]));
+    std::strncpy(names_out + 32 * i, H->kt_name[i], 31);
+    names_out[32 * i + 31] = 0;
+  }
+  *count = c;
+  API_CATCH
+}
+
+int vqmc_gpu_phase_times(vqmc_gpu_t* g, float out_ms[5]) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  for (int i = 0; i < 5; ++i) VQMC_CUDA(cudaEventElapsedTime(&out_ms[i], H->ev[i], H->ev[i + 1]));
+  API_CATCH
+}
+
+}  // extern "C"

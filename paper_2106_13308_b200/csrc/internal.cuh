@@ -1,0 +1,169 @@
+// Internal declarations of the B200 VQMC library (handle layout, kernels, helpers).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "vqmc_b200.h"
+
+namespace vqmc_b200 {
+
+// ---------------------------------------------------------------------------
+// Errors: C++ exceptions inside the library, mapped to status codes at the ABI.
+// ---------------------------------------------------------------------------
+struct InvalidArgument : std::invalid_argument {
+  using std::invalid_argument::invalid_argument;
+};
+struct NumericError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CudaError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+#define VQMC_CUDA(expr)                                                                  \
+  do {                                                                                   \
+    cudaError_t _e = (expr);                                                             \
+    if (_e != cudaSuccess)                                                               \
+      throw ::vqmc_b200::CudaError(std::string(#expr) + ": " + cudaGetErrorString(_e) + \
+                                   " (" __FILE__ ":" + std::to_string(__LINE__) + ")");  \
+  } while (0)
+
+constexpr double kProbEps = 1e-7;  // proj/include/vqmc/models.hpp:26
+// logit(1 - 1e-7) = ln((1 - 1e-7) / 1e-7): p_raw >= 1 - eps  <=>  z >= kLogitHi.
+constexpr float kLogitHi = 16.118095650958319f;
+constexpr int kMaxHidden = 1024;  // head sampler register tiling limit (32 lanes x 32)
+
+// ---------------------------------------------------------------------------
+// Device-resident parameter layout ("live" layout).  One contiguous fp32
+// buffer so Adam is a single elementwise pass:
+//   W1T [Hd][h]  : W1T[j][k] = M1(k,j) * W1[k][j]   (only inputs j < Hd = max degree
+//                  can ever be live, so the dead columns j >= Hd are not stored)
+//   b1  [h]
+//   W2  [n][h]   : M2(i,k) * W2[i][k]
+//   b2  [n]
+// Masked entries are stored as exact zeros; their gradient is exactly zero, so
+// Adam never moves them (proj/src/optimizer.cpp:21-35 with zero moments).  The
+// reference values of masked / dead entries are kept in a host copy for export.
+// ---------------------------------------------------------------------------
+struct Layout {
+  int n = 0, h = 0, Hd = 0, W = 0;
+  int64_t off_w1t = 0, off_b1 = 0, off_w2 = 0, off_b2 = 0, total = 0;
+  void init(int n_, int h_, int Hd_) {
+    n = n_;
+    h = h_;
+    Hd = Hd_;
+    W = (n + 31) / 32;
+    off_w1t = 0;
+    off_b1 = off_w1t + (int64_t)Hd * h;
+    off_w2 = off_b1 + h;
+    off_b2 = off_w2 + (int64_t)n * h;
+    total = off_b2 + n;
+  }
+};
+
+struct Handle;
+
+// RAII per-kernel event pair (active only when Handle::ktimer is set).
+struct KScope {
+  Handle* H;
+  int slot;
+  KScope(Handle* h, const char* name);
+  ~KScope();
+};
+
+// Kernel launchers (kernels.cu).  All enqueue on h->stream.
+void launch_refresh_w2ht(Handle* h);
+struct RngSpec;
+void launch_head_sample_impl(Handle* h, int B, const double* d_uniforms, RngSpec rng,
+                             bool given_bits, double* d_cond);
+void launch_z2(Handle* h, int B, int col0, const double* d_uniforms, RngSpec rng,
+               bool given_bits, double* d_cond);
+void launch_finalize_logpsi(Handle* h, int B, int n_tiles);
+void launch_energy(Handle* h, int B);
+void launch_weights_from_locals(Handle* h, int B, int seg);
+void launch_backward(Handle* h, int B);
+void launch_adam(Handle* h, float grad_scale, double lr, double b1, double b2, double eps,
+                 int64_t t);
+
+struct Handle {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  Layout L;
+  int64_t d = 0;  // reference parameter count
+  std::vector<int32_t> degrees;
+  std::vector<double> theta_host;  // reference-order copy (masked / dead entries)
+  int64_t num_edges = 0;
+
+  // model
+  float* P = nullptr;      // live params [L.total]
+  float* G = nullptr;      // live grads
+  float* Mo = nullptr;     // Adam m
+  float* Vo = nullptr;     // Adam v
+  float* W2hT = nullptr;   // [h][Hd] transposed head block of W2 (masked)
+  int32_t* d_deg = nullptr;
+  int32_t* d_comp_k = nullptr;    // hidden units sorted by degree
+  int32_t* d_comp_off = nullptr;  // [Hd + 1]: units with degree i+1 at [off[i], off[i+1])
+  int2* d_edges = nullptr;
+
+  // batch buffers (capacity cap_B)
+  int cap_B = 0;
+  uint32_t* X = nullptr;     // [B][W]
+  float* G1 = nullptr;       // [B][h]  relu(z1)
+  float* D = nullptr;        // [B][n]  0.5 (x - p_raw) * clampmask
+  double* lp_head = nullptr; // [B]
+  double* lp_part = nullptr; // [max_tiles][B]
+  double* log_psi = nullptr; // [B]
+  int32_t* cut = nullptr;    // [B]
+  double* local = nullptr;   // [B]
+  float* w = nullptr;        // [B]
+  float* Epart = nullptr;    // [splits][B][h]
+  float* dz1 = nullptr;      // [B][h]
+  double* cond = nullptr;    // [B][n] optional (log_psi with conditionals)
+  double* uni = nullptr;     // [n][B] injected uniforms
+  int64_t uni_cap = 0;
+  int64_t cond_cap = 0;
+
+  // scratch
+  double* d_scal = nullptr;    // fp64 scratch: [0] = ||grad||^2
+  int64_t* d_istat = nullptr;  // per worker segment s: [3s] cut_sum [3s+1] cut_sq_sum [3s+2] best
+  int istat_cap = 0;
+  double* d_gpart = nullptr;   // grad-norm partials
+  int gpart_n = 0;
+  uint32_t* d_flag = nullptr;  // non-finite flag
+  double* d_host_stage = nullptr;
+
+  // pinned host staging for stats
+  double* h_scal = nullptr;
+  int64_t* h_istat = nullptr;  // pinned, istat_cap entries
+
+  // comm
+  void* nccl_comm = nullptr;
+  int nranks = 1, rank = 0;
+
+  // timing
+  bool phase_timing = false;
+  cudaEvent_t ev[6] = {};
+  float phase_ms[5] = {0, 0, 0, 0, 0};
+
+  // per-kernel event timing (bench roofline): pool of event pairs reused each step
+  bool ktimer = false;
+  static constexpr int kKtPool = 128;
+  cudaEvent_t kt_start[kKtPool] = {}, kt_end[kKtPool] = {};
+  const char* kt_name[kKtPool] = {};
+  int kt_count = 0;
+
+  int64_t launches = 0;
+  int tail_tiles = 0;  // column tiles of the last z2 launch (lp partials)
+  int splits = 0;      // split-K factor of the dg1 GEMM
+
+  void ensure_batch(int B);
+  void ensure_uniforms(int64_t count);
+  void ensure_cond(int64_t count);
+};
+
+}  // namespace vqmc_b200
