@@ -198,7 +198,9 @@ def test_log_psi_and_conditionals(n):
     lo = O.log_psi(m, x)
     po, _, _ = O.forward(m, x)
     assert np.all(np.abs(lp - lo) <= 1e-5 * np.abs(lo))
-    assert np.abs(cond - po).max() <= 2e-6
+    # fp32 logits: the logit is a sum of up to h terms of size |W| |g| (|W| <= 1.5 under the
+    # U(-1.5, 1.5) perturbation), so |dz| <= ~1e-4 and |dp| <= p (1 - p) |dz| <= 3e-5
+    assert np.abs(cond - po).max() <= 3e-5
 
 
 def test_normalization_and_autoregressive_invariance():  # models_test.cpp:96-123 on the GPU path
@@ -263,7 +265,12 @@ def test_params_roundtrip_and_adam():
     sel = np.abs(g) > 1e-6 * np.abs(g).max()
     d_ref, d_got = p - m.theta, got - m.theta
     assert np.all(np.abs(d_got[sel] - d_ref[sel]) <= 1e-6 + 1e-4 * np.abs(d_ref[sel]))
-    assert np.all(got[g == 0.0] == m.theta[g == 0.0])  # masked parameters never move
+    zero = g == 0.0  # zero-gradient entries never move (masked ones are returned bit-exact)
+    assert np.all(np.abs(got[zero] - m.theta[zero]) <= 1e-7 * np.abs(m.theta[zero]))
+    h = m.h
+    M2 = (m.degrees[None, :] < np.arange(n)[:, None] + 1)
+    w2 = slice(h * n + h, h * n + h + n * h)
+    assert np.array_equal(got[w2].reshape(n, h)[~M2], m.theta[w2].reshape(n, h)[~M2])
 
 
 def _train_step(dev, mbs, L, U, seed, stream0, call, t):
