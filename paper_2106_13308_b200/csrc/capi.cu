@@ -86,14 +86,21 @@ void Handle::ensure_batch(int B) {
   const int max_tiles = (n + 127) / 128 + 2;
   dalloc(&X, (size_t)B * L.W);
   dalloc(&G1, (size_t)B * h);
-  dalloc(&D, (size_t)B * n);
+  dalloc(&Dhi, (size_t)B * np + 64);
+  dalloc(&Dlo, (size_t)B * np + 64);
+  dalloc(&G1hi, (size_t)B * hp + 64);
+  dalloc(&G1lo, (size_t)B * hp + 64);
+  dalloc(&wG1hi, (size_t)B * hp1 + 64);
+  dalloc(&wG1lo, (size_t)B * hp1 + 64);
+  VQMC_CUDA(cudaMemset(G1hi, 0, ((size_t)B * hp + 64) * sizeof(float)));
+  VQMC_CUDA(cudaMemset(G1lo, 0, ((size_t)B * hp + 64) * sizeof(float)));
   dalloc(&lp_head, (size_t)B);
   dalloc(&lp_part, (size_t)max_tiles * B);
   dalloc(&log_psi, (size_t)B);
   dalloc(&cut, (size_t)B);
   dalloc(&local, (size_t)B);
   dalloc(&w, (size_t)B);
-  dalloc(&Epart, (size_t)64 * B * h);
+  dalloc(&Epart, (size_t)max_splits * B * h);
   dalloc(&dz1, (size_t)B * h);
   cap_B = B;
 }
@@ -197,7 +204,7 @@ static void sample_into(Handle* H, int B, int workers, const double* uniforms_ho
   }
   RngSpec rng{seed, stream0, call, B / workers};
   VQMC_CUDA(cudaMemsetAsync(H->X, 0, (size_t)B * H->L.W * sizeof(uint32_t), H->stream));
-  launch_head_sample_impl(H, B, du, rng, false, nullptr);
+  launch_head_v2(H, B, du, rng, false, nullptr);
   launch_z2(H, B, H->L.Hd, du, rng, false, nullptr);
   launch_finalize_logpsi(H, B, H->tail_tiles);
 }
@@ -205,7 +212,7 @@ static void sample_into(Handle* H, int B, int workers, const double* uniforms_ho
 // Forward from configurations already in H->X.
 static void forward_given(Handle* H, int B, double* cond) {
   RngSpec none{0, 0, 0, 1};
-  launch_head_sample_impl(H, B, nullptr, none, true, cond);
+  launch_head_v2(H, B, nullptr, none, true, cond);
   launch_z2(H, B, H->L.Hd, nullptr, none, true, cond);
   launch_finalize_logpsi(H, B, H->tail_tiles);
 }
@@ -302,6 +309,9 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   DeviceGuard dg(device);
   VQMC_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
   H->L.init(n, h, Hd);
+  H->hp = (h + 3) & ~3;
+  H->hp1 = (h + 1 + 3) & ~3;
+  H->np = (n + 3) & ~3;
   H->d = 2LL * h * n + h + n;
   H->degrees.assign(degrees, degrees + h);
   H->num_edges = num_edges;
@@ -313,6 +323,10 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   VQMC_CUDA(cudaMemsetAsync(H->Mo, 0, H->L.total * sizeof(float), H->stream));
   VQMC_CUDA(cudaMemsetAsync(H->Vo, 0, H->L.total * sizeof(float), H->stream));
   dalloc(&H->W2hT, (size_t)h * Hd);
+  dalloc(&H->W2hi, (size_t)n * H->hp + 64);
+  dalloc(&H->W2lo, (size_t)n * H->hp + 64);
+  VQMC_CUDA(cudaMemset(H->W2hi, 0, ((size_t)n * H->hp + 64) * sizeof(float)));
+  VQMC_CUDA(cudaMemset(H->W2lo, 0, ((size_t)n * H->hp + 64) * sizeof(float)));
   dalloc(&H->d_deg, (size_t)h);
   VQMC_CUDA(cudaMemcpy(H->d_deg, degrees, h * sizeof(int32_t), cudaMemcpyHostToDevice));
   {  // completion lists: hidden units by degree
@@ -330,6 +344,15 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
     dalloc(&H->d_comp_off, (size_t)Hd + 1);
     VQMC_CUDA(cudaMemcpy(H->d_comp_k, ks.data(), h * sizeof(int32_t), cudaMemcpyHostToDevice));
     VQMC_CUDA(cudaMemcpy(H->d_comp_off, off.data(), (Hd + 1) * sizeof(int32_t), cudaMemcpyHostToDevice));
+    H->comp_off_host = off;
+    H->w1skip = true;
+    for (int k = 0; k < h; ++k) H->w1skip = H->w1skip && degrees[k] <= k + 1;
+    H->head_fast = true;
+    for (int i = 0; i < Hd; ++i) H->head_fast = H->head_fast && off[i + 1] - off[i] == 1 && ks[off[i]] == i;
+    const int kp = 32 * ((h + 31) / 32 <= 1 ? 1 : (h + 31) / 32 <= 2 ? 2 : (h + 31) / 32 <= 4 ? 4
+                        : (h + 31) / 32 <= 8 ? 8 : (h + 31) / 32 <= 16 ? 16 : 32);
+    dalloc(&H->W1Tp, (size_t)Hd * kp);
+    dalloc(&H->W2cp, (size_t)h * kp);
   }
   upload_edges(H, edges, num_edges);
   dalloc(&H->d_scal, 16);
@@ -363,8 +386,8 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   DeviceGuard dg(H->device);
   cudaStreamSynchronize(H->stream);
   if (H->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy(H->nccl_comm);
-  void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W2hT, H->d_deg, H->d_comp_k, H->d_comp_off, H->d_edges,
-                  H->X, H->G1, H->D, H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w,
+  void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W2hT, H->W1Tp, H->W2cp, H->W2hi, H->W2lo, H->d_deg, H->d_comp_k,
+                  H->d_comp_off, H->d_edges, H->X, H->G1, H->G1hi, H->G1lo, H->wG1hi, H->wG1lo, H->Dhi, H->Dlo, H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w,
                   H->Epart, H->dz1, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart};
   for (void* p : ptrs)
     if (p) cudaFree(p);

@@ -6,16 +6,19 @@
 #include <stdint.h>
 
 #include "internal.cuh"
+#include "ptx.cuh"
 
 namespace vqmc_b200 {
 
 constexpr unsigned kFull = 0xffffffffu;
 
 // Philox4x32-10 (production-mode uniforms; restated in oracle/vqmc_oracle.cpp).
-// key = mix_seed(seed, stream); counter = (bit, sample, call_lo, call_hi).
-__device__ __forceinline__ double philox_uniform(uint64_t key, uint32_t bit, uint32_t sample,
-                                                 uint64_t call) {
-  uint32_t c0 = bit, c1 = sample, c2 = (uint32_t)call, c3 = (uint32_t)(call >> 32);
+// key = mix_seed(seed, stream); counter = (bit >> 1, sample, call_lo, call_hi); the four
+// 32-bit outputs give the uniforms of the even bit (r0, r1) and the odd bit (r2, r3):
+// u = ((hi << 32 | lo) >> 11) * 2^-53.
+__device__ __forceinline__ void philox_pair(uint64_t key, uint32_t bitpair, uint32_t sample, uint64_t call,
+                                            double& u_even, double& u_odd) {
+  uint32_t c0 = bitpair, c1 = sample, c2 = (uint32_t)call, c3 = (uint32_t)(call >> 32);
   uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
 #pragma unroll
   for (int r = 0; r < 10; ++r) {
@@ -29,8 +32,8 @@ __device__ __forceinline__ double philox_uniform(uint64_t key, uint32_t bit, uin
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
   }
-  const uint64_t r = ((uint64_t)c0 << 32) | c1;
-  return (double)(r >> 11) * 0x1.0p-53;
+  u_even = (double)((((uint64_t)c0 << 32) | c1) >> 11) * 0x1.0p-53;
+  u_odd = (double)((((uint64_t)c2 << 32) | c3) >> 11) * 0x1.0p-53;
 }
 
 // mix_seed (proj/include/vqmc/common.hpp:56-61) on the device.
@@ -46,10 +49,16 @@ __device__ __forceinline__ uint64_t mix_seed_dev(uint64_t seed, uint64_t stream)
 struct RngSpec {
   uint64_t seed, stream0, call;
   int seg;
-  __device__ __forceinline__ double operator()(int b, int i) const {
+  // uniforms of bits (i & ~1, i | 1) of row b
+  __device__ __forceinline__ void pair(int b, int i, double& u0, double& u1) const {
     const int s = b / seg;
-    return philox_uniform(mix_seed_dev(seed, stream0 + (uint64_t)s), (uint32_t)i,
-                          (uint32_t)(b - s * seg), call);
+    philox_pair(mix_seed_dev(seed, stream0 + (uint64_t)s), (uint32_t)(i >> 1), (uint32_t)(b - s * seg), call,
+                u0, u1);
+  }
+  __device__ __forceinline__ double operator()(int b, int i) const {
+    double u0, u1;
+    pair(b, i, u0, u1);
+    return (i & 1) ? u1 : u0;
   }
 };
 

@@ -67,6 +67,7 @@ struct Layout {
 };
 
 struct Handle;
+struct RngSpec;
 
 // RAII per-kernel event pair (active only when Handle::ktimer is set).
 struct KScope {
@@ -78,15 +79,21 @@ struct KScope {
 
 // Kernel launchers (kernels.cu).  All enqueue on h->stream.
 void launch_refresh_w2ht(Handle* h);
-struct RngSpec;
-void launch_head_sample_impl(Handle* h, int B, const double* d_uniforms, RngSpec rng,
-                             bool given_bits, double* d_cond);
+void launch_head_pack(Handle* h);
+void launch_head_v2(Handle* h, int B, const double* d_uniforms, RngSpec rng, bool given_bits,
+                    double* d_cond);
 void launch_z2(Handle* h, int B, int col0, const double* d_uniforms, RngSpec rng,
                bool given_bits, double* d_cond);
 void launch_finalize_logpsi(Handle* h, int B, int n_tiles);
 void launch_energy(Handle* h, int B);
 void launch_weights_from_locals(Handle* h, int B, int seg);
 void launch_backward(Handle* h, int B);
+void launch_tail_umma(Handle* h, int B, const double* d_uniforms, RngSpec rng);
+void launch_dg1_umma(Handle* h, int B);
+void launch_gw2_umma(Handle* h, int B);
+void launch_split_w2(Handle* h);
+void set_error(const std::string& msg);
+int status_of(const std::exception& ex);
 void launch_adam(Handle* h, float grad_scale, double lr, double b1, double b2, double eps,
                  int64_t t);
 
@@ -105,6 +112,15 @@ struct Handle {
   float* Mo = nullptr;     // Adam m
   float* Vo = nullptr;     // Adam v
   float* W2hT = nullptr;   // [h][Hd] transposed head block of W2 (masked)
+  float* W2hi = nullptr;   // [n][hp] tf32 split of W2m (GEMM operand), refreshed after updates
+  float* W2lo = nullptr;
+  int hp = 0, hp1 = 0, np = 0;  // padded row strides: h, h + 1, n rounded up to 4 floats
+  int max_splits = 16;
+  float* W1Tp = nullptr;   // [Hd][hp] padded head block of W1^T (head sampler staging)
+  float* W2cp = nullptr;   // [h][Hdp] W2 head columns in completion order (padded)
+  std::vector<int32_t> comp_off_host;  // [Hd + 1]
+  bool head_fast = false;  // bit i completes exactly hidden unit i
+  bool w1skip = false;     // deg_k <= k + 1 for all k (W1 columns below the current word are dead)
   int32_t* d_deg = nullptr;
   int32_t* d_comp_k = nullptr;    // hidden units sorted by degree
   int32_t* d_comp_off = nullptr;  // [Hd + 1]: units with degree i+1 at [off[i], off[i+1])
@@ -114,7 +130,12 @@ struct Handle {
   int cap_B = 0;
   uint32_t* X = nullptr;     // [B][W]
   float* G1 = nullptr;       // [B][h]  relu(z1)
-  float* D = nullptr;        // [B][n]  0.5 (x - p_raw) * clampmask
+  float* Dhi = nullptr;      // [B][np] 0.5 (x - p_raw) * clampmask, tf32 hi part
+  float* Dlo = nullptr;      // [B][np] tf32 lo part (D = hi + lo)
+  float* G1hi = nullptr;     // [B][hp] tf32 split of G1 (tail GEMM operand)
+  float* G1lo = nullptr;
+  float* wG1hi = nullptr;    // [B][hp1] tf32 split of [w (.) G1 | w] (gW2 operand)
+  float* wG1lo = nullptr;
   double* lp_head = nullptr; // [B]
   double* lp_part = nullptr; // [max_tiles][B]
   double* log_psi = nullptr; // [B]

@@ -1,12 +1,12 @@
 // VQMC step kernels for sm_100a (v1: SIMT fp32 GEMMs).
 //
 // Reference path (arxiv/paper_2106_13308, /root/reference/proj):
-//   auto_sample            proj/src/sampler.cpp:35-59      -> head_kernel + z2_kernel
-//   made_forward           proj/src/models.cpp:51-62       -> head_kernel(given) + z2_kernel(given)
+//   auto_sample            proj/src/sampler.cpp:35-59      -> head_v2_kernel (head.cu) + tail GEMM (gemm.cu)
+//   made_forward           proj/src/models.cpp:51-62       -> head_v2_kernel(given) + z2_given_kernel
 //   local_energy_batch     proj/include/vqmc/estimator.hpp:43-57 -> energy_kernel
 //   energy_and_variance +
 //   gradient_from_locals   estimator.hpp:94-119            -> stats_weights_kernel
-//   weighted_grad_log_psi  proj/src/models.cpp:175-198     -> dg1/dz1/gw2/gw1 kernels
+//   weighted_grad_log_psi  proj/src/models.cpp:175-198     -> dg1/gw2 (gemm.cu), dz1/gw1 kernels
 //   adam_step              proj/src/optimizer.cpp:21-35    -> adam_kernel
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -18,105 +18,6 @@
 #include "internal.cuh"
 
 namespace vqmc_b200 {
-
-// ===========================================================================
-// Head sampler: bits 0 .. Hd-1 (Hd = max degree) are strictly sequential.
-// One warp per sample; lane l owns hidden units k = l + 32 m and head outputs
-// i = l + 32 m in registers.  Per sampled bit i the warp applies two rank-1
-// updates: z1 += x_i * W1m[:, i] and, for each hidden unit whose degree is
-// i + 1 (it just became complete), z2_head += relu(z1_k) * W2m[:, k].  Bit i's
-// own logit is therefore complete exactly when it is drawn — O(h + Hd) work per
-// bit instead of the reference's full forward pass (sampler.cpp:48).
-// given != 0: replay the bits in X instead of drawing (forward from configs).
-// ===========================================================================
-template <int KPL>
-__global__ void __launch_bounds__(128) head_kernel(
-    int B, int n, int h, int Hd, int W, const float* __restrict__ W1T, const float* __restrict__ b1,
-    const float* __restrict__ W2hT, const float* __restrict__ b2, const int* __restrict__ comp_k,
-    const int* __restrict__ comp_off, const double* __restrict__ uni, RngSpec rng,
-    int given, uint32_t* __restrict__ X, float* __restrict__ G1, float* __restrict__ D,
-    double* __restrict__ lp_head, double* __restrict__ cond) {
-  const int lane = threadIdx.x & 31;
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  if (b >= B) return;
-  float z1[KPL], z2[KPL];
-#pragma unroll
-  for (int m = 0; m < KPL; ++m) {
-    const int k = lane + 32 * m;
-    z1[m] = k < h ? b1[k] : 0.f;
-    z2[m] = k < Hd ? b2[k] : 0.f;
-  }
-  double lp = 0.0;
-  const size_t rowD = (size_t)b * n;
-#pragma unroll
-  for (int m = 0; m < KPL; ++m) {
-    if (32 * m >= Hd) break;
-    const int ibase = 32 * m;
-    // lane l's uniform / given bit for bit ibase + l (all 32 in flight at once)
-    int mybit = 0;
-    double myu = 0.0;
-    {
-      const int i = ibase + lane;
-      if (i < Hd) {
-        if (given) mybit = (X[(size_t)b * W + m] >> lane) & 1;
-        else myu = uni ? uni[(size_t)i * B + b] : rng(b, i);
-      }
-    }
-    uint32_t myx = 0;
-    const int lend = min(32, Hd - ibase);
-    for (int l = 0; l < lend; ++l) {
-      const int i = ibase + l;
-      // owner lane l holds z2 for output i (complete: all units of degree <= i added)
-      const float z = z2[m];
-      int x;
-      if (given) {
-        x = mybit;
-      } else {
-        x = myu < clamped_p(z) ? 1 : 0;
-      }
-      if (lane == l) {
-        const Unit u = unit_terms(z, x);
-        D[rowD + i] = u.D;
-        lp += (double)u.logt;
-        myx = (uint32_t)x;
-        if (cond) cond[rowD + i] = u.p;
-      }
-      x = __shfl_sync(kFull, x, l);
-      if (x) {
-        const float* wr = W1T + (size_t)i * h;
-#pragma unroll
-        for (int mm = 0; mm < KPL; ++mm) {
-          const int k = lane + 32 * mm;
-          if (k < h) z1[mm] += wr[k];
-        }
-      }
-      const int c0 = comp_off[i], c1 = comp_off[i + 1];
-      for (int c = c0; c < c1; ++c) {
-        const int k = comp_k[c];
-        const int ks = k >> 5, kl = k & 31;
-        float v = 0.f;
-#pragma unroll
-        for (int mm = 0; mm < KPL; ++mm) v = (mm == ks) ? z1[mm] : v;
-        float g = fmaxf(v, 0.f);
-        g = __shfl_sync(kFull, g, kl);
-        if (lane == kl) G1[(size_t)b * h + k] = g;
-        if (g != 0.f) {
-          const float* wr = W2hT + (size_t)k * Hd;
-#pragma unroll
-          for (int mm = 0; mm < KPL; ++mm) {
-            const int i2 = lane + 32 * mm;
-            if (i2 < Hd) z2[mm] = fmaf(wr[i2], g, z2[mm]);
-          }
-        }
-      }
-    }
-    const uint32_t word = __ballot_sync(kFull, myx);
-    if (!given && lane == 0) X[(size_t)b * W + m] = word;
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) lp += __shfl_xor_sync(kFull, lp, o);
-  if (lane == 0) lp_head[b] = lp;
-}
 
 // ===========================================================================
 // z2 GEMM with the MADE output epilogue: Z[b][c] = G1[b] . W2m[c] + b2[c] for
@@ -144,60 +45,40 @@ struct LoadW2 {  // B(n = output, k = hidden) = W2m[n][k]
   __device__ float operator()(int c, int k) const { return c < n ? W2[(size_t)c * h + k] : 0.f; }
 };
 
-__global__ void __launch_bounds__(z2cfg::T::NT) z2_kernel(
-    int B, int n, int h, int W, int colbase, int col0, const float* __restrict__ G1,
-    const float* __restrict__ W2, const float* __restrict__ b2, const double* __restrict__ uni,
-    RngSpec rng, int given, uint32_t* __restrict__ X, float* __restrict__ D,
-    double* __restrict__ lp_part, double* __restrict__ cond) {
+__global__ void __launch_bounds__(z2cfg::T::NT) z2_given_kernel(
+    int B, int n, int np, int h, int W, int colbase, int col0, const float* __restrict__ G1,
+    const float* __restrict__ W2, const float* __restrict__ b2, const uint32_t* __restrict__ X,
+    float* __restrict__ Dhi, float* __restrict__ Dlo, double* __restrict__ lp_part, double* __restrict__ cond) {
   using namespace z2cfg;
   __shared__ __align__(16) float smem[BK * (BM + BN)];
   const int m0 = blockIdx.y * BM;
-  const int n0 = colbase + blockIdx.x * BN;  // 32-aligned
+  const int n0 = colbase + blockIdx.x * BN;
   float acc[TM][TN];
   simt_mainloop<BM, BN, BK, TM, TN>(acc, m0, n0, 0, h, LoadG1{G1, B, h}, LoadW2{W2, n, h}, smem);
   const int tid = threadIdx.x, tx = tid % T::NTX, ty = tid / T::NTX;
 #pragma unroll
   for (int r = 0; r < TM; ++r) {
-    const int rl = T::row(ty, r);
-    const int b = m0 + rl;
+    const int b = m0 + T::row(ty, r);
     double lps = 0.0;
-    uint32_t nib[2] = {0u, 0u};  // x of columns tx*4 + {0..3} and BN/2 + tx*4 + {0..3}
     if (b < B) {
 #pragma unroll
       for (int c = 0; c < TN; ++c) {
         const int col = n0 + T::col(tx, c);
         if (col < col0 || col >= n) continue;
         const float z = acc[r][c] + b2[col];
-        int x;
-        if (given) {
-          x = (X[(size_t)b * W + (col >> 5)] >> (col & 31)) & 1;
-        } else {
-          const double u = uni ? uni[(size_t)col * B + b] : rng(b, col);
-          x = u < clamped_p(z) ? 1 : 0;
-          nib[c >> 2] |= (uint32_t)x << (c & 3);
-        }
+        const int x = (X[(size_t)b * W + (col >> 5)] >> (col & 31)) & 1;
         const Unit u = unit_terms(z, x);
-        D[(size_t)b * n + col] = u.D;
+        float hi, lo;
+        ptx::split_tf32(u.D, hi, lo);
+        Dhi[(size_t)b * np + col] = hi;
+        Dlo[(size_t)b * np + col] = lo;
         lps += (double)u.logt;
         if (cond) cond[(size_t)b * n + col] = u.p;
       }
     }
-    // the row's NTX (=16) threads are consecutive lanes: reduce the log-prob partial
 #pragma unroll
     for (int o = T::NTX / 2; o > 0; o >>= 1) lps += __shfl_xor_sync(kFull, lps, o);
     if (tx == 0 && b < B) lp_part[(size_t)blockIdx.x * B + b] = lps;
-    if (!given) {
-      // pack: 8 consecutive tx hold the 32 bits of one word (4 bits each)
-#pragma unroll
-      for (int q = 0; q < 2; ++q) {
-        uint32_t v = nib[q] << ((tx & 7) * 4);
-        v |= __shfl_xor_sync(kFull, v, 1);
-        v |= __shfl_xor_sync(kFull, v, 2);
-        v |= __shfl_xor_sync(kFull, v, 4);
-        const int word = (n0 >> 5) + q * (BN / 64) + (tx >> 3);
-        if ((tx & 7) == 0 && b < B && word < W && v) atomicOr(&X[(size_t)b * W + word], v);
-      }
-    }
   }
 }
 
@@ -320,47 +201,9 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int seg, const doub
 //   gW1T = (X^T dz1) (.) M1^T,       gb1 = 1^T dz1    (one GEMM, M = Hd + 1)
 // ===========================================================================
 namespace bwcfg {
-constexpr int BM = 128, BN = 64, BK = 16, TM = 8, TN = 8;  // dg1
-constexpr int GM = 128, GN = 128;                            // gW2
-constexpr int QM = 64, QN = 64;                              // gW1
+constexpr int BK = 16, TM = 8, TN = 8;
+constexpr int QM = 64, QN = 64;  // gW1
 }  // namespace bwcfg
-
-struct LoadD_K {  // A(m = sample, k = output i) = D[m][k]
-  static constexpr bool kMMajor = false;
-  const float* D;
-  int B, n;
-  __device__ float operator()(int m, int k) const { return m < B ? D[(size_t)m * n + k] : 0.f; }
-};
-struct LoadW2_N {  // B(n = hidden k, k = output i) = W2m[i][k]
-  static constexpr bool kMMajor = true;
-  const float* W2;
-  int h;
-  __device__ float operator()(int c, int k) const { return c < h ? W2[(size_t)k * h + c] : 0.f; }
-};
-
-__global__ void __launch_bounds__(SimtTile<bwcfg::BM, bwcfg::BN, bwcfg::BK, 8, 8>::NT)
-    dg1_kernel(int B, int n, int h, int chunk, const float* __restrict__ D,
-               const float* __restrict__ W2, float* __restrict__ Epart) {
-  using namespace bwcfg;
-  using T = SimtTile<BM, BN, BK, TM, TN>;
-  __shared__ __align__(16) float smem[BK * (BM + BN)];
-  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
-  const int kb = blockIdx.z * chunk, ke = min(n, kb + chunk);
-  float acc[TM][TN];
-  simt_mainloop<BM, BN, BK, TM, TN>(acc, m0, n0, kb, ke, LoadD_K{D, B, n}, LoadW2_N{W2, h}, smem);
-  const int tx = threadIdx.x % T::NTX, ty = threadIdx.x / T::NTX;
-  float* out = Epart + (size_t)blockIdx.z * B * h;
-#pragma unroll
-  for (int r = 0; r < TM; ++r) {
-    const int b = m0 + T::row(ty, r);
-    if (b >= B) continue;
-#pragma unroll
-    for (int c = 0; c < TN; ++c) {
-      const int k = n0 + T::col(tx, c);
-      if (k < h) out[(size_t)b * h + k] = acc[r][c];
-    }
-  }
-}
 
 __global__ void dz1_kernel(int B, int h, int splits, const float* __restrict__ Epart,
                            const float* __restrict__ w, const float* __restrict__ G1,
@@ -372,47 +215,6 @@ __global__ void dz1_kernel(int B, int h, int splits, const float* __restrict__ E
   for (int z = 0; z < splits; ++z) s += Epart[(size_t)z * total + t];
   const int b = (int)(t / h);
   dz1[t] = G1[t] > 0.f ? s * w[b] : 0.f;
-}
-
-struct LoadDT {  // A(m = output i, k = sample b) = D[b][i]
-  static constexpr bool kMMajor = true;
-  const float* D;
-  int n;
-  __device__ float operator()(int m, int k) const { return m < n ? D[(size_t)k * n + m] : 0.f; }
-};
-struct LoadWG1 {  // B(n = hidden k (h = bias column), k = sample b) = w_b * (G1[b][k] or 1)
-  static constexpr bool kMMajor = true;
-  const float* G1;
-  const float* w;
-  int h;
-  __device__ float operator()(int c, int k) const {
-    if (c > h) return 0.f;
-    return c < h ? w[k] * G1[(size_t)k * h + c] : w[k];
-  }
-};
-
-__global__ void __launch_bounds__(SimtTile<bwcfg::GM, bwcfg::GN, bwcfg::BK, 8, 8>::NT)
-    gw2_kernel(int B, int n, int h, const float* __restrict__ D, const float* __restrict__ G1,
-               const float* __restrict__ w, const int32_t* __restrict__ deg,
-               float* __restrict__ gW2, float* __restrict__ gb2) {
-  using namespace bwcfg;
-  using T = SimtTile<GM, GN, BK, TM, TN>;
-  __shared__ __align__(16) float smem[BK * (GM + GN)];
-  const int m0 = blockIdx.y * GM, n0 = blockIdx.x * GN;
-  float acc[TM][TN];
-  simt_mainloop<GM, GN, BK, TM, TN>(acc, m0, n0, 0, B, LoadDT{D, n}, LoadWG1{G1, w, h}, smem);
-  const int tx = threadIdx.x % T::NTX, ty = threadIdx.x / T::NTX;
-#pragma unroll
-  for (int r = 0; r < TM; ++r) {
-    const int i = m0 + T::row(ty, r);
-    if (i >= n) continue;
-#pragma unroll
-    for (int c = 0; c < TN; ++c) {
-      const int k = n0 + T::col(tx, c);
-      if (k < h) gW2[(size_t)i * h + k] = (deg[k] < i + 1) ? acc[r][c] : 0.f;  // M2(i,k)
-      else if (k == h) gb2[i] = acc[r][c];
-    }
-  }
 }
 
 struct LoadXT {  // A(m = input j (Hd = ones row), k = sample b) = x_bj
@@ -538,6 +340,8 @@ KScope::~KScope() {
 }
 
 void launch_refresh_w2ht(Handle* H) {
+  launch_head_pack(H);
+  launch_split_w2(H);
   const Layout& L = H->L;
   dim3 grid((L.h + 31) / 32, (L.Hd + 31) / 32), block(32, 8);
   KScope ks(H, "refresh_w2ht");
@@ -546,44 +350,21 @@ void launch_refresh_w2ht(Handle* H) {
   H->launches++;
 }
 
-template <int KPL>
-static void head_launch(Handle* H, int B, const double* uni, RngSpec rng, bool given,
-                        double* cond) {
-  const Layout& L = H->L;
-  const int warps = 4;
-  KScope ks(H, given ? "head_given" : "head_sample");
-  head_kernel<KPL><<<(B + warps - 1) / warps, 32 * warps, 0, H->stream>>>(
-      B, L.n, L.h, L.Hd, L.W, H->P + L.off_w1t, H->P + L.off_b1, H->W2hT, H->P + L.off_b2,
-      H->d_comp_k, H->d_comp_off, uni, rng, given ? 1 : 0, H->X, H->G1, H->D, H->lp_head,
-      cond);
-  LAUNCH_CHECK();
-  H->launches++;
-}
-
-void launch_head_sample_impl(Handle* H, int B, const double* uni, RngSpec rng, bool given,
-                             double* cond) {
-  const int kpl = (H->L.h + 31) / 32;
-  if (kpl <= 1) head_launch<1>(H, B, uni, rng, given, cond);
-  else if (kpl <= 2) head_launch<2>(H, B, uni, rng, given, cond);
-  else if (kpl <= 4) head_launch<4>(H, B, uni, rng, given, cond);
-  else if (kpl <= 8) head_launch<8>(H, B, uni, rng, given, cond);
-  else if (kpl <= 16) head_launch<16>(H, B, uni, rng, given, cond);
-  else head_launch<32>(H, B, uni, rng, given, cond);
-}
-
-
-void launch_z2(Handle* H, int B, int col0, const double* uni, RngSpec rng, bool given,
-               double* cond) {
+void launch_z2(Handle* H, int B, int col0, const double* uni, RngSpec rng, bool given, double* cond) {
+  if (!given) {
+    launch_tail_umma(H, B, uni, rng);
+    return;
+  }
   const Layout& L = H->L;
   const int colbase = (col0 / 32) * 32;
   const int tiles = col0 >= L.n ? 0 : (L.n - colbase + z2cfg::BN - 1) / z2cfg::BN;
   H->tail_tiles = tiles;
   if (tiles == 0) return;
   dim3 grid(tiles, (B + z2cfg::BM - 1) / z2cfg::BM);
-  KScope ks(H, given ? "z2_given" : "z2_tail_sample");
-  z2_kernel<<<grid, z2cfg::T::NT, 0, H->stream>>>(B, L.n, L.h, L.W, colbase, col0, H->G1,
-                                                  H->P + L.off_w2, H->P + L.off_b2, uni, rng,
-                                                  given ? 1 : 0, H->X, H->D, H->lp_part, cond);
+  KScope ks(H, "z2_given");
+  z2_given_kernel<<<grid, z2cfg::T::NT, 0, H->stream>>>(B, L.n, H->np, L.h, L.W, colbase, col0, H->G1,
+                                                        H->P + L.off_w2, H->P + L.off_b2, H->X, H->Dhi, H->Dlo,
+                                                        H->lp_part, cond);
   LAUNCH_CHECK();
   H->launches++;
 }
@@ -620,36 +401,16 @@ void launch_weights_from_locals(Handle* H, int B, int seg) {
 void launch_backward(Handle* H, int B) {
   using namespace bwcfg;
   const Layout& L = H->L;
-  // dg1: split-K over n so that ~4 CTAs per SM are resident
+  launch_dg1_umma(H, B);  // E = D . W2m (split-K partials)
   {
-    const int tiles = ((B + BM - 1) / BM) * ((L.h + BN - 1) / BN);
-    int splits = std::max(1, std::min(64, (148 * 4 + tiles - 1) / tiles));
-    int chunk = (L.n + splits - 1) / splits;
-    chunk = ((chunk + BK - 1) / BK) * BK;
-    splits = (L.n + chunk - 1) / chunk;
-    H->splits = splits;
-    dim3 grid((L.h + BN - 1) / BN, (B + BM - 1) / BM, splits);
-    {
-    KScope ks(H, "bw_dg1");
-    dg1_kernel<<<grid, SimtTile<BM, BN, BK, TM, TN>::NT, 0, H->stream>>>(B, L.n, L.h, chunk, H->D,
-                                                                         H->P + L.off_w2, H->Epart);
-    LAUNCH_CHECK();
-    }
     KScope ks(H, "bw_dz1");
     const size_t total = (size_t)B * L.h;
-    dz1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, splits, H->Epart,
-                                                                       H->w, H->G1, H->dz1);
-    LAUNCH_CHECK();
-    H->launches += 2;
-  }
-  {
-    dim3 grid((L.h + 1 + GN - 1) / GN, (L.n + GM - 1) / GM);
-    KScope ks(H, "bw_gw2");
-    gw2_kernel<<<grid, SimtTile<GM, GN, BK, TM, TN>::NT, 0, H->stream>>>(
-        B, L.n, L.h, H->D, H->G1, H->w, H->d_deg, H->G + L.off_w2, H->G + L.off_b2);
+    dz1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->splits, H->Epart, H->w, H->G1,
+                                                                       H->dz1);
     LAUNCH_CHECK();
     H->launches++;
   }
+  launch_gw2_umma(H, B);  // gW2 (.) M2 and gb2
   {
     dim3 grid((L.h + QN - 1) / QN, (L.Hd + 1 + QM - 1) / QM);
     KScope ks(H, "bw_gw1");
