@@ -605,14 +605,12 @@ double now_s() {
 // ---------------------------------------------------------------------------
 // Production-mode uniforms of the GPU sampler (NOT a reference feature: the
 // reference draws mt19937_64).  Philox4x32-10 (Salmon et al., SC'11), key =
-// mix_seed(seed, stream) split in two 32-bit halves, counter = (bit, sample,
-// call_lo, call_hi); u = ((r0 << 32 | r1) >> 11) * 2^-53 in [0, 1).
-// Restated here so production-mode samples are checkable bit-for-bit.  One call
-// covers bits (2j, 2j+1): counter c0 = bit >> 1, outputs (r0, r1) -> even bit,
-// (r2, r3) -> odd bit.
+// mix_seed(seed, stream) split in two 32-bit halves, counter = (bit >> 2, sample,
+// call_lo, call_hi); one call covers bits 4j .. 4j+3: u(bit) = (r_{bit & 3} + 1/2) * 2^-32.
+// Restated here so production-mode samples are checkable bit-for-bit.
 // ---------------------------------------------------------------------------
 double philox_uniform(uint64_t key64, uint32_t bit, uint32_t sample, uint64_t call) {
-  uint32_t c0 = bit >> 1, c1 = sample, c2 = (uint32_t)call, c3 = (uint32_t)(call >> 32);
+  uint32_t c0 = bit >> 2, c1 = sample, c2 = (uint32_t)call, c3 = (uint32_t)(call >> 32);
   uint32_t k0 = (uint32_t)key64, k1 = (uint32_t)(key64 >> 32);
   for (int r = 0; r < 10; ++r) {
     const uint64_t p0 = (uint64_t)0xD2511F53u * c0;
@@ -624,8 +622,8 @@ double philox_uniform(uint64_t key64, uint32_t bit, uint32_t sample, uint64_t ca
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
   }
-  const uint64_t r = (bit & 1) ? (((uint64_t)c2 << 32) | c3) : (((uint64_t)c0 << 32) | c1);
-  return (double)(r >> 11) * 0x1.0p-53;
+  const uint32_t out[4] = {c0, c1, c2, c3};
+  return ((double)out[bit & 3] + 0.5) * 0x1.0p-32;
 }
 
 }  // namespace

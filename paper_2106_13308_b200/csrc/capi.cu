@@ -83,7 +83,7 @@ static void dalloc(T** p, size_t count) {
 void Handle::ensure_batch(int B) {
   if (B <= cap_B) return;
   const int n = L.n, h = L.h;
-  const int max_tiles = (n + 127) / 128 + 2;
+  const int max_tiles = 2 * ((n + 127) / 128 + 2);  // two epilogue partials per tail tile
   dalloc(&X, (size_t)B * L.W);
   dalloc(&G1, (size_t)B * h);
   dalloc(&Dhi, (size_t)B * np + 64);
@@ -323,6 +323,7 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   VQMC_CUDA(cudaMemsetAsync(H->Mo, 0, H->L.total * sizeof(float), H->stream));
   VQMC_CUDA(cudaMemsetAsync(H->Vo, 0, H->L.total * sizeof(float), H->stream));
   dalloc(&H->W2hT, (size_t)h * Hd);
+  dalloc(&H->gw1_part, (size_t)kGw1MaxSplits * (Hd + 1) * h);
   dalloc(&H->W2hi, (size_t)n * H->hp + 64);
   dalloc(&H->W2lo, (size_t)n * H->hp + 64);
   VQMC_CUDA(cudaMemset(H->W2hi, 0, ((size_t)n * H->hp + 64) * sizeof(float)));
@@ -388,7 +389,7 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   if (H->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy(H->nccl_comm);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W2hT, H->W1Tp, H->W2cp, H->W2hi, H->W2lo, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1hi, H->G1lo, H->wG1hi, H->wG1lo, H->Dhi, H->Dlo, H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w,
-                  H->Epart, H->dz1, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart};
+                  H->Epart, H->dz1, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (H->h_scal) cudaFreeHost(H->h_scal);

@@ -13,15 +13,14 @@ namespace vqmc_b200 {
 constexpr unsigned kFull = 0xffffffffu;
 
 // Philox4x32-10 (production-mode uniforms; restated in oracle/vqmc_oracle.cpp).
-// key = mix_seed(seed, stream); counter = (bit >> 1, sample, call_lo, call_hi); the four
-// 32-bit outputs give the uniforms of the even bit (r0, r1) and the odd bit (r2, r3):
-// u = ((hi << 32 | lo) >> 11) * 2^-53.
-__device__ __forceinline__ void philox_pair(uint64_t key, uint32_t bitpair, uint32_t sample, uint64_t call,
-                                            double& u_even, double& u_odd) {
-  uint32_t c0 = bitpair, c1 = sample, c2 = (uint32_t)call, c3 = (uint32_t)(call >> 32);
+// key = mix_seed(seed, stream); counter = (bit >> 2, sample, call_lo, call_hi); output word
+// j = bit & 3 gives u = (r_j + 1/2) * 2^-32 (32-bit resolution, never 0 or 1).
+__device__ __forceinline__ void philox4(uint64_t key, uint32_t quad, uint32_t sample, uint64_t call,
+                                        uint32_t (&r)[4]) {
+  uint32_t c0 = quad, c1 = sample, c2 = (uint32_t)call, c3 = (uint32_t)(call >> 32);
   uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
 #pragma unroll
-  for (int r = 0; r < 10; ++r) {
+  for (int i = 0; i < 10; ++i) {
     const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
     const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
     const uint32_t n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
@@ -32,9 +31,12 @@ __device__ __forceinline__ void philox_pair(uint64_t key, uint32_t bitpair, uint
     k0 += 0x9E3779B9u;
     k1 += 0xBB67AE85u;
   }
-  u_even = (double)((((uint64_t)c0 << 32) | c1) >> 11) * 0x1.0p-53;
-  u_odd = (double)((((uint64_t)c2 << 32) | c3) >> 11) * 0x1.0p-53;
+  r[0] = c0;
+  r[1] = c1;
+  r[2] = c2;
+  r[3] = c3;
 }
+__device__ __forceinline__ double u32_to_uniform(uint32_t r) { return ((double)r + 0.5) * 0x1.0p-32; }
 
 // mix_seed (proj/include/vqmc/common.hpp:56-61) on the device.
 __device__ __forceinline__ uint64_t mix_seed_dev(uint64_t seed, uint64_t stream) {
@@ -49,16 +51,15 @@ __device__ __forceinline__ uint64_t mix_seed_dev(uint64_t seed, uint64_t stream)
 struct RngSpec {
   uint64_t seed, stream0, call;
   int seg;
-  // uniforms of bits (i & ~1, i | 1) of row b
-  __device__ __forceinline__ void pair(int b, int i, double& u0, double& u1) const {
+  // raw outputs for bits (i & ~3) .. (i | 3) of row b
+  __device__ __forceinline__ void quad(int b, int i, uint32_t (&r)[4]) const {
     const int s = b / seg;
-    philox_pair(mix_seed_dev(seed, stream0 + (uint64_t)s), (uint32_t)(i >> 1), (uint32_t)(b - s * seg), call,
-                u0, u1);
+    philox4(mix_seed_dev(seed, stream0 + (uint64_t)s), (uint32_t)(i >> 2), (uint32_t)(b - s * seg), call, r);
   }
   __device__ __forceinline__ double operator()(int b, int i) const {
-    double u0, u1;
-    pair(b, i, u0, u1);
-    return (i & 1) ? u1 : u0;
+    uint32_t r[4];
+    quad(b, i, r);
+    return u32_to_uniform(r[i & 3]);
   }
 };
 
@@ -81,28 +82,45 @@ struct Unit {
 __device__ __forceinline__ double clamped_p(float z) {
   if (z >= kLogitHi) return 1.0 - kProbEps;
   if (z <= -kLogitHi) return kProbEps;
-  return (double)(1.f / (1.f + expf(-z)));
+  return (double)(1.f / (1.f + __expf(-z)));
 }
 
-__device__ __forceinline__ Unit unit_terms(float z, int x) {
-  Unit o;
-  const bool hi = z >= kLogitHi, lo = z <= -kLogitHi;
-  if (hi || lo) {
-    o.D = 0.f;
-    // log(1e-7) and log1p(-1e-7)
-    const float lsmall = -16.11809565095832f, lbig = -1.00000005e-7f;
-    o.logt = (hi == (x != 0)) ? lbig : lsmall;
-    o.p = hi ? 1.0 - kProbEps : kProbEps;
-  } else {
-    const float sp_pos = softplusf(z);   // -log(1 - p)
-    const float sp_neg = softplusf(-z);  // -log p
-    o.logt = x ? -sp_neg : -sp_pos;
-    // 1 - p_raw = sigmoid(-z) without cancellation
-    o.D = x ? 0.5f / (1.f + expf(z)) : -0.5f / (1.f + expf(-z));
-    o.p = (double)(1.f / (1.f + expf(-z)));
+// Shared transcendental work of one output unit: e = exp(-|z|), r = 1 / (1 + e),
+// log1p(e): sigmoid, its complement and both softplus values follow without cancellation.
+struct UnitPre {
+  float praw, qraw, sp_pos, sp_neg;  // p_raw, 1 - p_raw, softplus(z) = -log(1-p), softplus(-z) = -log p
+  bool hi, lo;                       // clamp active at 1 - eps / at eps
+  __device__ __forceinline__ double p() const {
+    return hi ? 1.0 - kProbEps : (lo ? kProbEps : (double)praw);
   }
+};
+__device__ __forceinline__ UnitPre unit_pre(float z) {
+  UnitPre o;
+  o.hi = z >= kLogitHi;
+  o.lo = z <= -kLogitHi;
+  const float e = __expf(-fabsf(z));
+  const float r = __frcp_rn(1.f + e);
+  const float L = log1pf(e);  // accurate: the log-probs sum n of these terms
+  o.praw = z >= 0.f ? r : e * r;
+  o.qraw = z >= 0.f ? e * r : r;
+  o.sp_pos = fmaxf(z, 0.f) + L;
+  o.sp_neg = fmaxf(-z, 0.f) + L;
   return o;
 }
+__device__ __forceinline__ Unit unit_post(const UnitPre& q, int x) {
+  Unit o;
+  if (q.hi || q.lo) {
+    const float lsmall = -16.11809565095832f, lbig = -1.00000005e-7f;  // log(1e-7), log1p(-1e-7)
+    o.D = 0.f;
+    o.logt = (q.hi == (x != 0)) ? lbig : lsmall;
+  } else {
+    o.logt = x ? -q.sp_neg : -q.sp_pos;
+    o.D = x ? 0.5f * q.qraw : -0.5f * q.praw;
+  }
+  o.p = q.p();
+  return o;
+}
+__device__ __forceinline__ Unit unit_terms(float z, int x) { return unit_post(unit_pre(z), x); }
 
 // ---------------------------------------------------------------------------
 // SIMT fp32 GEMM main loop: acc[TM][TN] += sum_k A(m, k) * B(n, k) over the

@@ -101,6 +101,7 @@ static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, cons
 struct StoreEpi {  // test: C[row][col] = acc
   float* C;
   int ldc;
+  int part;
   __device__ void begin_row(int, const UmmaArgs&) {}
   __device__ void chunk(int row, int col0, const float (&v)[32], const UmmaArgs& a) {
     if (row >= a.M) return;
@@ -112,6 +113,8 @@ struct StoreEpi {  // test: C[row][col] = acc
 };
 
 // Tail sampler: rows = samples, columns = outputs colbase + col (col0 aligned to 32).
+// Two epilogue warp sets share a row (alternate 32-column chunks): each writes its own
+// log-prob partial (lp_part[2 * tile + part]), so the reduction stays deterministic.
 struct TailSampleEpi {
   int B, n, np, W, colbase, col_lo;  // outputs in [col_lo, n) are drawn here
   const float* b2;
@@ -121,61 +124,69 @@ struct TailSampleEpi {
   float* Dhi;
   float* Dlo;
   double* lp_part;
+  int part;
   double lps;
   __device__ void begin_row(int, const UmmaArgs&) { lps = 0.0; }
   __device__ void chunk(int b, int col0, const float (&v)[32], const UmmaArgs&) {
     if (b >= B) return;
-    uint32_t word = 0;
     const int cb = colbase + col0;
     const size_t rowD = (size_t)b * np;
-    if (uni == nullptr) {
-      // production uniforms: one Philox call yields the uniforms of two adjacent bits
+    float dh[32], dl[32];
+    uint32_t word = 0;
 #pragma unroll
-      for (int j = 0; j < 32; j += 2) {
-        const int col = cb + j;
-        double u0, u1;
-        rng.pair(b, col, u0, u1);
+    for (int j = 0; j < 32; j += 4) {
+      double u[4];
+      if (uni == nullptr) {
+        uint32_t r[4];
+        rng.quad(b, cb + j, r);  // one Philox call covers these 4 bits
 #pragma unroll
-        for (int t = 0; t < 2; ++t) {
-          const int c = col + t;
-          if (c < col_lo || c >= n) continue;
-          const float z = v[j + t] + b2[c];
-          const int x = (t ? u1 : u0) < clamped_p(z) ? 1 : 0;
-          word |= (uint32_t)x << (j + t);
-          const Unit u = unit_terms(z, x);
-          float hi, lo;
-          ptx::split_tf32(u.D, hi, lo);
-          Dhi[rowD + c] = hi;
-          Dlo[rowD + c] = lo;
-          lps += (double)u.logt;
-        }
+        for (int t = 0; t < 4; ++t) u[t] = u32_to_uniform(r[t]);
+      } else {
+#pragma unroll
+        for (int t = 0; t < 4; ++t) u[t] = (cb + j + t < n) ? uni[(size_t)(cb + j + t) * B + b] : 1.0;
+      }
+#pragma unroll
+      for (int t = 0; t < 4; ++t) {
+        const int c = cb + j + t;
+        const bool valid = c >= col_lo && c < n;
+        const float z = v[j + t] + (valid ? b2[c] : 0.f);
+        const UnitPre q = unit_pre(z);
+        const int x = (valid && u[t] < q.p()) ? 1 : 0;
+        word |= (uint32_t)x << (j + t);
+        const Unit o = unit_post(q, x);
+        ptx::split_tf32(o.D, dh[j + t], dl[j + t]);
+        if (valid) lps += (double)o.logt;
+      }
+    }
+    if (cb >= col_lo && cb + 32 <= n) {
+      float4* ph = reinterpret_cast<float4*>(Dhi + rowD + cb);
+      float4* pl = reinterpret_cast<float4*>(Dlo + rowD + cb);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        ph[j] = make_float4(dh[4 * j], dh[4 * j + 1], dh[4 * j + 2], dh[4 * j + 3]);
+        pl[j] = make_float4(dl[4 * j], dl[4 * j + 1], dl[4 * j + 2], dl[4 * j + 3]);
       }
     } else {
 #pragma unroll
       for (int j = 0; j < 32; ++j) {
         const int c = cb + j;
-        if (c < col_lo || c >= n) continue;
-        const float z = v[j] + b2[c];
-        const int x = uni[(size_t)c * B + b] < clamped_p(z) ? 1 : 0;
-        word |= (uint32_t)x << j;
-        const Unit u = unit_terms(z, x);
-        float hi, lo;
-        ptx::split_tf32(u.D, hi, lo);
-        Dhi[rowD + c] = hi;
-        Dlo[rowD + c] = lo;
-        lps += (double)u.logt;
+        if (c >= col_lo && c < n) {
+          Dhi[rowD + c] = dh[j];
+          Dlo[rowD + c] = dl[j];
+        }
       }
     }
     if (word) atomicOr(&X[(size_t)b * W + (cb >> 5)], word);
   }
   __device__ void end_row(int b, const UmmaArgs&) {
-    if (b < B) lp_part[(size_t)blockIdx.x * B + b] = lps;
+    if (b < B) lp_part[(size_t)(2 * blockIdx.x + part) * B + b] = lps;
   }
 };
 
 struct PartialEpi {  // split-K partial: out[z][row][col]
   float* out;
   int rows, cols;
+  int part;
   __device__ void begin_row(int, const UmmaArgs&) {}
   __device__ void chunk(int row, int col0, const float (&v)[32], const UmmaArgs&) {
     if (row >= rows) return;
@@ -189,6 +200,7 @@ struct PartialEpi {  // split-K partial: out[z][row][col]
 
 struct Gw2Epi {  // rows = outputs i, columns = hidden k (k == h: bias column -> gb2)
   int n, h;
+  int part;
   const int32_t* deg;
   float* gW2;
   float* gb2;
@@ -259,8 +271,8 @@ void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng) {
   const CUtensorMap al = tmap_kmajor(H->G1lo, L.h, B, H->hp, kUmmaBM);
   const CUtensorMap bh = tmap_kmajor(H->W2hi + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
   const CUtensorMap bl = tmap_kmajor(H->W2lo + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
-  TailSampleEpi e{B, L.n, H->np, L.W, colbase, L.Hd, H->P + L.off_b2, uni, rng, H->X, H->Dhi, H->Dlo, H->lp_part, 0.0};
-  H->tail_tiles = (ncols + BN - 1) / BN;
+  TailSampleEpi e{B, L.n, H->np, L.W, colbase, L.Hd, H->P + L.off_b2, uni, rng, H->X, H->Dhi, H->Dlo, H->lp_part, 0, 0.0};
+  H->tail_tiles = 2 * ((ncols + BN - 1) / BN);  // two epilogue partials per column tile
   launch_umma<BN, false, false>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols, L.h, 1, e, H->stream);
 }
 
@@ -278,7 +290,7 @@ void launch_dg1_umma(Handle* H, int B) {
   const CUtensorMap al = tmap_kmajor(H->Dlo, L.n, B, H->np, kUmmaBM);
   const CUtensorMap bh = tmap_mnmajor(H->W2hi, L.h, L.n, H->hp, BN);
   const CUtensorMap bl = tmap_mnmajor(H->W2lo, L.h, L.n, H->hp, BN);
-  PartialEpi e{H->Epart, B, L.h};
+  PartialEpi e{H->Epart, B, L.h, 0};
   launch_umma<BN, false, true>(H, "bw_dg1_umma", ah, al, bh, bl, B, L.h, L.n, splits, e, H->stream);
 }
 
@@ -297,7 +309,7 @@ void launch_gw2_umma(Handle* H, int B) {
   const CUtensorMap al = tmap_mnmajor(H->Dlo, L.n, B, H->np, kUmmaBM);
   const CUtensorMap bh = tmap_mnmajor(H->wG1hi, L.h + 1, B, H->hp1, BN);
   const CUtensorMap bl = tmap_mnmajor(H->wG1lo, L.h + 1, B, H->hp1, BN);
-  Gw2Epi e{L.n, L.h, H->d_deg, H->G + L.off_w2, H->G + L.off_b2};
+  Gw2Epi e{L.n, L.h, 0, H->d_deg, H->G + L.off_w2, H->G + L.off_b2};
   launch_umma<BN, true, true>(H, "bw_gw2_umma", ah, al, bh, bl, L.n, L.h + 1, B, 1, e, H->stream);
 }
 
@@ -341,7 +353,7 @@ extern "C" int vqmc_test_umma_gemm(int M, int N, int K, int a_mn, int b_mn, int 
     else { ah = tmap_kmajor(dAh, K, M, lda, kUmmaBM); al = tmap_kmajor(dAl, K, M, lda, kUmmaBM); }
     if (b_mn) { bh = tmap_mnmajor(dBh, N, K, ldb, bnv); bl = tmap_mnmajor(dBl, N, K, ldb, bnv); }
     else { bh = tmap_kmajor(dBh, K, N, ldb, bnv); bl = tmap_kmajor(dBl, K, N, ldb, bnv); }
-    PartialEpi e{dC, M, N};
+    PartialEpi e{dC, M, N, 0};
 #define GO(BNV, AM, BM_)                                                                       \
   launch_umma<BNV, AM, BM_>(nullptr, "test", ah, al, bh, bl, M, N, K, splits, e, (cudaStream_t)0)
     if (bnv == 128) {

@@ -36,7 +36,8 @@ struct CudaError : std::runtime_error {
 constexpr double kProbEps = 1e-7;  // proj/include/vqmc/models.hpp:26
 // logit(1 - 1e-7) = ln((1 - 1e-7) / 1e-7): p_raw >= 1 - eps  <=>  z >= kLogitHi.
 constexpr float kLogitHi = 16.118095650958319f;
-constexpr int kMaxHidden = 1024;  // head sampler register tiling limit (32 lanes x 32)
+constexpr int kMaxHidden = 1024;
+constexpr int kGw1MaxSplits = 16;  // split-K of the gW1 GEMM over the batch  // head sampler register tiling limit (32 lanes x 32)
 
 // ---------------------------------------------------------------------------
 // Device-resident parameter layout ("live" layout).  One contiguous fp32
@@ -144,6 +145,7 @@ struct Handle {
   float* w = nullptr;        // [B]
   float* Epart = nullptr;    // [splits][B][h]
   float* dz1 = nullptr;      // [B][h]
+  float* gw1_part = nullptr; // [kGw1MaxSplits][Hd + 1][h]
   double* cond = nullptr;    // [B][n] optional (log_psi with conditionals)
   double* uni = nullptr;     // [n][B] injected uniforms
   int64_t uni_cap = 0;

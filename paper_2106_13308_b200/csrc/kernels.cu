@@ -234,17 +234,19 @@ struct LoadDz1 {  // B(n = hidden k, k = sample b) = dz1[b][k]
   __device__ float operator()(int c, int k) const { return c < h ? dz1[(size_t)k * h + c] : 0.f; }
 };
 
+// gW1 partial sums over a chunk of samples (split-K over the batch; deterministic reduction below).
 __global__ void __launch_bounds__(SimtTile<bwcfg::QM, bwcfg::QN, bwcfg::BK, 8, 8>::NT)
-    gw1_kernel(int B, int h, int Hd, int W, const uint32_t* __restrict__ X,
-               const float* __restrict__ dz1, const int32_t* __restrict__ deg,
-               float* __restrict__ gW1T, float* __restrict__ gb1) {
+    gw1_kernel(int B, int h, int Hd, int W, int chunk, const uint32_t* __restrict__ X,
+               const float* __restrict__ dz1, float* __restrict__ part) {
   using namespace bwcfg;
   using T = SimtTile<QM, QN, BK, TM, TN>;
   __shared__ __align__(16) float smem[BK * (QM + QN)];
   const int m0 = blockIdx.y * QM, n0 = blockIdx.x * QN;
+  const int kb = blockIdx.z * chunk, ke = min(B, kb + chunk);
   float acc[TM][TN];
-  simt_mainloop<QM, QN, BK, TM, TN>(acc, m0, n0, 0, B, LoadXT{X, W, Hd}, LoadDz1{dz1, h}, smem);
+  simt_mainloop<QM, QN, BK, TM, TN>(acc, m0, n0, kb, ke, LoadXT{X, W, Hd}, LoadDz1{dz1, h}, smem);
   const int tx = threadIdx.x % T::NTX, ty = threadIdx.x / T::NTX;
+  float* out = part + (size_t)blockIdx.z * (Hd + 1) * h;
 #pragma unroll
   for (int r = 0; r < TM; ++r) {
     const int j = m0 + T::row(ty, r);
@@ -252,11 +254,23 @@ __global__ void __launch_bounds__(SimtTile<bwcfg::QM, bwcfg::QN, bwcfg::BK, 8, 8
 #pragma unroll
     for (int c = 0; c < TN; ++c) {
       const int k = n0 + T::col(tx, c);
-      if (k >= h) continue;
-      if (j < Hd) gW1T[(size_t)j * h + k] = (j + 1 <= deg[k]) ? acc[r][c] : 0.f;  // M1(k,j)
-      else gb1[k] = acc[r][c];
+      if (k < h) out[(size_t)j * h + k] = acc[r][c];
     }
   }
+}
+
+// gW1T = (sum of partials) (.) M1^T, gb1 = the ones row (j == Hd).
+__global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __restrict__ part,
+                                    const int32_t* __restrict__ deg, float* __restrict__ gW1T,
+                                    float* __restrict__ gb1) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int total = (Hd + 1) * h;
+  if (t >= total) return;
+  float s = 0.f;
+  for (int z = 0; z < splits; ++z) s += part[(size_t)z * total + t];
+  const int j = t / h, k = t % h;
+  if (j < Hd) gW1T[(size_t)j * h + k] = (j + 1 <= deg[k]) ? s : 0.f;  // M1(k, j)
+  else gb1[k] = s;
 }
 
 // ===========================================================================
@@ -412,12 +426,24 @@ void launch_backward(Handle* H, int B) {
   }
   launch_gw2_umma(H, B);  // gW2 (.) M2 and gb2
   {
-    dim3 grid((L.h + QN - 1) / QN, (L.Hd + 1 + QM - 1) / QM);
-    KScope ks(H, "bw_gw1");
-    gw1_kernel<<<grid, SimtTile<QM, QN, BK, TM, TN>::NT, 0, H->stream>>>(
-        B, L.h, L.Hd, L.W, H->X, H->dz1, H->d_deg, H->G + L.off_w1t, H->G + L.off_b1);
+    const int tiles = ((L.h + QN - 1) / QN) * ((L.Hd + 1 + QM - 1) / QM);
+    int splits = std::max(1, std::min(kGw1MaxSplits, (4 * 148 + tiles - 1) / tiles));
+    int chunk = (B + splits - 1) / splits;
+    chunk = ((chunk + BK - 1) / BK) * BK;
+    splits = (B + chunk - 1) / chunk;
+    dim3 grid((L.h + QN - 1) / QN, (L.Hd + 1 + QM - 1) / QM, splits);
+    {
+      KScope ks(H, "bw_gw1");
+      gw1_kernel<<<grid, SimtTile<QM, QN, BK, TM, TN>::NT, 0, H->stream>>>(B, L.h, L.Hd, L.W, chunk, H->X, H->dz1,
+                                                                           H->gw1_part);
+      LAUNCH_CHECK();
+    }
+    KScope ks(H, "bw_gw1_finalize");
+    const int total = (L.Hd + 1) * L.h;
+    gw1_finalize_kernel<<<(total + 255) / 256, 256, 0, H->stream>>>(L.h, L.Hd, splits, H->gw1_part, H->d_deg,
+                                                                     H->G + L.off_w1t, H->G + L.off_b1);
     LAUNCH_CHECK();
-    H->launches++;
+    H->launches += 2;
   }
 }
 

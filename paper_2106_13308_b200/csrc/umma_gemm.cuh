@@ -135,16 +135,22 @@ __global__ void __launch_bounds__(256, 1)
       }
       ptx::mma_commit(tfull);  // accumulator complete
     }
-  } else if (warp >= 4) {  // ---------------- epilogue ----------------
-    const int q = warp - 4;
+  }
+  // ---------------- epilogue: all 8 warps ----------------
+  // warp w reads TMEM lanes 32 (w % 4) .. +31 (its row quarter); warps 4-7 take the even
+  // 32-column chunks and warps 0-3 (done with TMA / MMA / allocation) the odd ones.
+  __syncwarp();
+  {
+    const int q = warp & 3, part = warp < 4 ? 1 : 0;
     const int row = m0 + 32 * q + lane;
     ptx::mbar_wait(tfull, 0);
     ptx::tc_fence_after();
     Epi e = epi;
+    e.part = part;
     e.begin_row(row, args);
     const bool has_k = kb1 > kb0;
 #pragma unroll 1
-    for (int c = 0; c < BN; c += 32) {
+    for (int c = 32 * part; c < BN; c += 64) {
       if (n0 + c >= args.N) break;
       float v[32];
       if (has_k) {
