@@ -83,14 +83,17 @@ static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, cons
     attr = true;
   }
   const int nkb = (K + kUmmaBK - 1) / kUmmaBK;
-  UmmaArgs args{M, N, K, (nkb + splits - 1) / splits};
-  dim3 grid((N + BN - 1) / BN, (M + kUmmaBM - 1) / kUmmaBM, splits);
+  UmmaArgs args{M, N, K, (nkb + splits - 1) / splits, (N + BN - 1) / BN, (M + kUmmaBM - 1) / kUmmaBM, splits};
+  const int ntiles = args.tiles_n * args.tiles_m * splits;
+  static int sms = 0;
+  if (!sms) VQMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int grid = std::min(ntiles, sms);
   if (H) {
     KScope ks(H, name);
-    kern<<<grid, 256, Cfg::kSmem, stream>>>(ah, al, bh, bl, args, epi);
+    kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(ah, al, bh, bl, args, epi);
     H->launches++;
   } else {
-    kern<<<grid, 256, Cfg::kSmem, stream>>>(ah, al, bh, bl, args, epi);
+    kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(ah, al, bh, bl, args, epi);
   }
   VQMC_CUDA(cudaGetLastError());
 }
@@ -102,6 +105,7 @@ struct StoreEpi {  // test: C[row][col] = acc
   float* C;
   int ldc;
   int part;
+  UmmaTile tile;
   __device__ void begin_row(int, const UmmaArgs&) {}
   __device__ void chunk(int row, int col0, const float (&v)[32], const UmmaArgs& a) {
     if (row >= a.M) return;
@@ -125,6 +129,7 @@ struct TailSampleEpi {
   float* Dlo;
   double* lp_part;
   int part;
+  UmmaTile tile;
   double lps;
   __device__ void begin_row(int, const UmmaArgs&) { lps = 0.0; }
   __device__ void chunk(int b, int col0, const float (&v)[32], const UmmaArgs&) {
@@ -179,7 +184,7 @@ struct TailSampleEpi {
     if (word) atomicOr(&X[(size_t)b * W + (cb >> 5)], word);
   }
   __device__ void end_row(int b, const UmmaArgs&) {
-    if (b < B) lp_part[(size_t)(2 * blockIdx.x + part) * B + b] = lps;
+    if (b < B) lp_part[(size_t)(2 * tile.tn + part) * B + b] = lps;
   }
 };
 
@@ -187,10 +192,11 @@ struct PartialEpi {  // split-K partial: out[z][row][col]
   float* out;
   int rows, cols;
   int part;
+  UmmaTile tile;
   __device__ void begin_row(int, const UmmaArgs&) {}
   __device__ void chunk(int row, int col0, const float (&v)[32], const UmmaArgs&) {
     if (row >= rows) return;
-    float* o = out + ((size_t)blockIdx.z * rows + row) * cols;
+    float* o = out + ((size_t)tile.z * rows + row) * cols;
 #pragma unroll
     for (int j = 0; j < 32; ++j)
       if (col0 + j < cols) o[col0 + j] = v[j];
@@ -201,6 +207,7 @@ struct PartialEpi {  // split-K partial: out[z][row][col]
 struct Gw2Epi {  // rows = outputs i, columns = hidden k (k == h: bias column -> gb2)
   int n, h;
   int part;
+  UmmaTile tile;
   const int32_t* deg;
   float* gW2;
   float* gb2;
@@ -271,7 +278,7 @@ void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng) {
   const CUtensorMap al = tmap_kmajor(H->G1lo, L.h, B, H->hp, kUmmaBM);
   const CUtensorMap bh = tmap_kmajor(H->W2hi + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
   const CUtensorMap bl = tmap_kmajor(H->W2lo + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
-  TailSampleEpi e{B, L.n, H->np, L.W, colbase, L.Hd, H->P + L.off_b2, uni, rng, H->X, H->Dhi, H->Dlo, H->lp_part, 0, 0.0};
+  TailSampleEpi e{B, L.n, H->np, L.W, colbase, L.Hd, H->P + L.off_b2, uni, rng, H->X, H->Dhi, H->Dlo, H->lp_part, 0, {}, 0.0};
   H->tail_tiles = 2 * ((ncols + BN - 1) / BN);  // two epilogue partials per column tile
   launch_umma<BN, false, false>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols, L.h, 1, e, H->stream);
 }
@@ -281,7 +288,7 @@ void launch_dg1_umma(Handle* H, int B) {
   constexpr int BN = 256;
   const int mt = (B + kUmmaBM - 1) / kUmmaBM, nt = (L.h + BN - 1) / BN;
   const int nkb = (L.n + kUmmaBK - 1) / kUmmaBK;
-  int splits = std::max(1, std::min(nkb, (148 + mt * nt - 1) / (mt * nt)));
+  int splits = std::max(1, std::min(nkb, 148 / (mt * nt)));  // one tile per SM
   splits = std::min(splits, H->max_splits);
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
@@ -290,7 +297,7 @@ void launch_dg1_umma(Handle* H, int B) {
   const CUtensorMap al = tmap_kmajor(H->Dlo, L.n, B, H->np, kUmmaBM);
   const CUtensorMap bh = tmap_mnmajor(H->W2hi, L.h, L.n, H->hp, BN);
   const CUtensorMap bl = tmap_mnmajor(H->W2lo, L.h, L.n, H->hp, BN);
-  PartialEpi e{H->Epart, B, L.h, 0};
+  PartialEpi e{H->Epart, B, L.h, 0, {}};
   launch_umma<BN, false, true>(H, "bw_dg1_umma", ah, al, bh, bl, B, L.h, L.n, splits, e, H->stream);
 }
 
@@ -309,7 +316,7 @@ void launch_gw2_umma(Handle* H, int B) {
   const CUtensorMap al = tmap_mnmajor(H->Dlo, L.n, B, H->np, kUmmaBM);
   const CUtensorMap bh = tmap_mnmajor(H->wG1hi, L.h + 1, B, H->hp1, BN);
   const CUtensorMap bl = tmap_mnmajor(H->wG1lo, L.h + 1, B, H->hp1, BN);
-  Gw2Epi e{L.n, L.h, 0, H->d_deg, H->G + L.off_w2, H->G + L.off_b2};
+  Gw2Epi e{L.n, L.h, 0, {}, H->d_deg, H->G + L.off_w2, H->G + L.off_b2};
   launch_umma<BN, true, true>(H, "bw_gw2_umma", ah, al, bh, bl, L.n, L.h + 1, B, 1, e, H->stream);
 }
 
@@ -353,7 +360,7 @@ extern "C" int vqmc_test_umma_gemm(int M, int N, int K, int a_mn, int b_mn, int 
     else { ah = tmap_kmajor(dAh, K, M, lda, kUmmaBM); al = tmap_kmajor(dAl, K, M, lda, kUmmaBM); }
     if (b_mn) { bh = tmap_mnmajor(dBh, N, K, ldb, bnv); bl = tmap_mnmajor(dBl, N, K, ldb, bnv); }
     else { bh = tmap_kmajor(dBh, K, N, ldb, bnv); bl = tmap_kmajor(dBl, K, N, ldb, bnv); }
-    PartialEpi e{dC, M, N, 0};
+    PartialEpi e{dC, M, N, 0, {}};
 #define GO(BNV, AM, BM_)                                                                       \
   launch_umma<BNV, AM, BM_>(nullptr, "test", ah, al, bh, bl, M, N, K, splits, e, (cudaStream_t)0)
     if (bnv == 128) {

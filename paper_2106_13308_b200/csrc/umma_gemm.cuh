@@ -33,17 +33,30 @@ struct UmmaCfg {
   static constexpr int kABytes = kUmmaBM * kUmmaBK * 4;  // 16 KB
   static constexpr int kBBytes = BN * kUmmaBK * 4;
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
-  static constexpr int kTmemCols = BN <= 32 ? 32 : BN <= 64 ? 64 : BN <= 128 ? 128 : 256;
+  static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
+  static constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
   static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256;
 };
 
 struct UmmaArgs {
   int M, N, K;
   int kblk_per_split;  // k-blocks (of 32) per split
+  int tiles_n, tiles_m, splits;
 };
 
+// Tile coordinates handed to the epilogue functor.
+struct UmmaTile {
+  int tn, tm, z;
+};
+
+// Persistent: CTA b processes tiles b, b + grid, ...; tile t -> (n = t % tiles_n,
+// m = (t / tiles_n) % tiles_m, split = t / (tiles_n tiles_m)).  The accumulator is
+// double-buffered in TMEM (2 x BN columns) so the epilogue of tile j overlaps the
+// mainloop of tile j + 1.
+//   warp 0  TMA producer     warp 1  MMA issuer     warp 2  TMEM allocator
+//   warps 4-11  epilogue (two sets of 4 warps, alternate 32-column chunks)
 template <int BN, bool A_MN, bool B_MN, class Epi>
-__global__ void __launch_bounds__(256, 1)
+__global__ void __launch_bounds__(384, 1)
     umma_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                        const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
                        UmmaArgs args, Epi epi) {
@@ -53,14 +66,20 @@ __global__ void __launch_bounds__(256, 1)
       (reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
   uint64_t* full = reinterpret_cast<uint64_t*>(base + (size_t)Cfg::kStages * Cfg::kStageBytes);
   uint64_t* empty = full + Cfg::kStages;
-  uint64_t* tfull = empty + Cfg::kStages;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tfull + 1);
+  uint64_t* tfull = empty + Cfg::kStages;  // [2]
+  uint64_t* tempty = tfull + 2;            // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int m0 = blockIdx.y * kUmmaBM, n0 = blockIdx.x * BN;
   const int nkb = (args.K + kUmmaBK - 1) / kUmmaBK;
-  const int kb0 = blockIdx.z * args.kblk_per_split;
-  const int kb1 = min(nkb, kb0 + args.kblk_per_split);
+  const int ntiles = args.tiles_n * args.tiles_m * args.splits;
+  auto tile_of = [&](int t) {
+    UmmaTile c;
+    c.tn = t % args.tiles_n;
+    c.tm = (t / args.tiles_n) % args.tiles_m;
+    c.z = t / (args.tiles_n * args.tiles_m);
+    return c;
+  };
 
   if (warp == 0 && lane == 0) {
     ptx::prefetch_tmap(&tA_hi);
@@ -71,7 +90,10 @@ __global__ void __launch_bounds__(256, 1)
       ptx::mbar_init(&full[s], 1);
       ptx::mbar_init(&empty[s], 1);
     }
-    ptx::mbar_init(tfull, 1);
+    for (int b = 0; b < 2; ++b) {
+      ptx::mbar_init(&tfull[b], 1);
+      ptx::mbar_init(&tempty[b], 8);  // one arrive per epilogue warp
+    }
     ptx::fence_mbar_init();
   }
   if (warp == 2) ptx::tmem_alloc<Cfg::kTmemCols>(tmem_slot);
@@ -82,86 +104,112 @@ __global__ void __launch_bounds__(256, 1)
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer ----------------
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const int it = kb - kb0, s = it % Cfg::kStages, use = it / Cfg::kStages;
-        if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
-        unsigned char* st = base + (size_t)s * Cfg::kStageBytes;
-        ptx::mbar_expect_tx(&full[s], Cfg::kStageBytes);
-        const int kc = kb * kUmmaBK;
-        if (A_MN) {
-          ptx::tma_load_3d(st, &tA_hi, &full[s], 0, kc, m0 / 32);
-          ptx::tma_load_3d(st + Cfg::kABytes, &tA_lo, &full[s], 0, kc, m0 / 32);
-        } else {
-          ptx::tma_load_2d(st, &tA_hi, &full[s], kc, m0);
-          ptx::tma_load_2d(st + Cfg::kABytes, &tA_lo, &full[s], kc, m0);
-        }
-        unsigned char* sb = st + 2 * Cfg::kABytes;
-        if (B_MN) {
-          ptx::tma_load_3d(sb, &tB_hi, &full[s], 0, kc, n0 / 32);
-          ptx::tma_load_3d(sb + Cfg::kBBytes, &tB_lo, &full[s], 0, kc, n0 / 32);
-        } else {
-          ptx::tma_load_2d(sb, &tB_hi, &full[s], kc, n0);
-          ptx::tma_load_2d(sb + Cfg::kBBytes, &tB_lo, &full[s], kc, n0);
+      int s = 0, use = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x) {
+        const UmmaTile c = tile_of(t);
+        const int m0 = c.tm * kUmmaBM, n0 = c.tn * BN;
+        const int kb0 = c.z * args.kblk_per_split, kb1 = min(nkb, kb0 + args.kblk_per_split);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
+          unsigned char* st = base + (size_t)s * Cfg::kStageBytes;
+          ptx::mbar_expect_tx(&full[s], Cfg::kStageBytes);
+          const int kc = kb * kUmmaBK;
+          if (A_MN) {
+            ptx::tma_load_3d(st, &tA_hi, &full[s], 0, kc, m0 / 32);
+            ptx::tma_load_3d(st + Cfg::kABytes, &tA_lo, &full[s], 0, kc, m0 / 32);
+          } else {
+            ptx::tma_load_2d(st, &tA_hi, &full[s], kc, m0);
+            ptx::tma_load_2d(st + Cfg::kABytes, &tA_lo, &full[s], kc, m0);
+          }
+          unsigned char* sb = st + 2 * Cfg::kABytes;
+          if (B_MN) {
+            ptx::tma_load_3d(sb, &tB_hi, &full[s], 0, kc, n0 / 32);
+            ptx::tma_load_3d(sb + Cfg::kBBytes, &tB_lo, &full[s], 0, kc, n0 / 32);
+          } else {
+            ptx::tma_load_2d(sb, &tB_hi, &full[s], kc, n0);
+            ptx::tma_load_2d(sb + Cfg::kBBytes, &tB_lo, &full[s], kc, n0);
+          }
+          if (++s == Cfg::kStages) {
+            s = 0;
+            ++use;
+          }
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer ----------------
       constexpr uint32_t idesc = ptx::idesc_tf32(BN, A_MN, B_MN);
-      // descriptor geometry (bytes): LBO / SBO and the per-MMA (K = 8) start advance
       constexpr uint32_t a_lbo = A_MN ? 32 * 128 : 16, a_sbo = A_MN ? 512 : 1024, a_step = A_MN ? 1024 : 32;
       constexpr uint32_t b_lbo = B_MN ? 32 * 128 : 16, b_sbo = B_MN ? 512 : 1024, b_step = B_MN ? 1024 : 32;
       constexpr uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
-      for (int kb = kb0; kb < kb1; ++kb) {
-        const int it = kb - kb0, s = it % Cfg::kStages, use = it / Cfg::kStages;
-        ptx::mbar_wait(&full[s], use & 1);
+      int s = 0, use = 0, j = 0;
+      for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+        const UmmaTile c = tile_of(t);
+        const int kb0 = c.z * args.kblk_per_split, kb1 = min(nkb, kb0 + args.kblk_per_split);
+        const int buf = j & 1;
+        if (j >= 2) ptx::mbar_wait(&tempty[buf], ((j >> 1) - 1) & 1);  // epilogue drained this buffer
         ptx::tc_fence_after();
-        const uint32_t sa = ptx::smem_u32(base + (size_t)s * Cfg::kStageBytes);
-        const uint32_t sal = sa + Cfg::kABytes;
-        const uint32_t sb = sa + 2 * Cfg::kABytes;
-        const uint32_t sbl = sb + Cfg::kBBytes;
+        const uint32_t acc = tmem + (uint32_t)(buf * BN);
+        for (int kb = kb0; kb < kb1; ++kb) {
+          ptx::mbar_wait(&full[s], use & 1);
+          ptx::tc_fence_after();
+          const uint32_t sa = ptx::smem_u32(base + (size_t)s * Cfg::kStageBytes);
+          const uint32_t sal = sa + Cfg::kABytes;
+          const uint32_t sb = sa + 2 * Cfg::kABytes;
+          const uint32_t sbl = sb + Cfg::kBBytes;
 #pragma unroll
-        for (int k = 0; k < kUmmaBK / 8; ++k) {
-          const uint64_t ah = ptx::sdesc(sa + k * a_step, a_lbo, a_sbo, a_lay);
-          const uint64_t al = ptx::sdesc(sal + k * a_step, a_lbo, a_sbo, a_lay);
-          const uint64_t bh = ptx::sdesc(sb + k * b_step, b_lbo, b_sbo, b_lay);
-          const uint64_t bl = ptx::sdesc(sbl + k * b_step, b_lbo, b_sbo, b_lay);
-          const uint32_t acc0 = (kb > kb0 || k > 0) ? 1u : 0u;
-          ptx::mma_tf32(tmem, ah, bh, idesc, acc0);
-          ptx::mma_tf32(tmem, ah, bl, idesc, 1u);
-          ptx::mma_tf32(tmem, al, bh, idesc, 1u);
+          for (int k = 0; k < kUmmaBK / 8; ++k) {
+            const uint64_t ah = ptx::sdesc(sa + k * a_step, a_lbo, a_sbo, a_lay);
+            const uint64_t al = ptx::sdesc(sal + k * a_step, a_lbo, a_sbo, a_lay);
+            const uint64_t bh = ptx::sdesc(sb + k * b_step, b_lbo, b_sbo, b_lay);
+            const uint64_t bl = ptx::sdesc(sbl + k * b_step, b_lbo, b_sbo, b_lay);
+            const uint32_t acc0 = (kb > kb0 || k > 0) ? 1u : 0u;
+            ptx::mma_tf32(acc, ah, bh, idesc, acc0);
+            ptx::mma_tf32(acc, ah, bl, idesc, 1u);
+            ptx::mma_tf32(acc, al, bh, idesc, 1u);
+          }
+          ptx::mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+          if (++s == Cfg::kStages) {
+            s = 0;
+            ++use;
+          }
         }
-        ptx::mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
+        ptx::mma_commit(&tfull[buf]);  // accumulator of this tile complete
       }
-      ptx::mma_commit(tfull);  // accumulator complete
     }
-  }
-  // ---------------- epilogue: all 8 warps ----------------
-  // warp w reads TMEM lanes 32 (w % 4) .. +31 (its row quarter); warps 4-7 take the even
-  // 32-column chunks and warps 0-3 (done with TMA / MMA / allocation) the odd ones.
-  __syncwarp();
-  {
-    const int q = warp & 3, part = warp < 4 ? 1 : 0;
-    const int row = m0 + 32 * q + lane;
-    ptx::mbar_wait(tfull, 0);
-    ptx::tc_fence_after();
-    Epi e = epi;
-    e.part = part;
-    e.begin_row(row, args);
-    const bool has_k = kb1 > kb0;
+  } else if (warp >= 4) {  // ---------------- epilogue (8 warps) ----------------
+    const int q = warp & 3, part = warp < 8 ? 0 : 1;
+    int j = 0;
+    for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
+      const UmmaTile c = tile_of(t);
+      const int m0 = c.tm * kUmmaBM, n0 = c.tn * BN;
+      const int kb0 = c.z * args.kblk_per_split, kb1 = min(nkb, kb0 + args.kblk_per_split);
+      const int buf = j & 1;
+      const int row = m0 + 32 * q + lane;
+      ptx::mbar_wait(&tfull[buf], (j >> 1) & 1);
+      ptx::tc_fence_after();
+      Epi e = epi;
+      e.part = part;
+      e.tile = c;
+      e.begin_row(row, args);
+      const bool has_k = kb1 > kb0;
 #pragma unroll 1
-    for (int c = 32 * part; c < BN; c += 64) {
-      if (n0 + c >= args.N) break;
-      float v[32];
-      if (has_k) {
-        ptx::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)c, v);
-      } else {
+      for (int cc = 32 * part; cc < BN; cc += 64) {
+        if (n0 + cc >= args.N) break;
+        float v[32];
+        if (has_k) {
+          ptx::tmem_ld32(tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN + cc), v);
+        } else {
 #pragma unroll
-        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        e.chunk(row, n0 + cc, v, args);
       }
-      e.chunk(row, n0 + c, v, args);
+      e.end_row(row, args);
+      ptx::tc_fence_before();
+      __syncwarp();
+      if (lane == 0) ptx::mbar_arrive(&tempty[buf]);
     }
-    e.end_row(row, args);
   }
   ptx::tc_fence_before();
   __syncthreads();
