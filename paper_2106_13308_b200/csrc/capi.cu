@@ -83,7 +83,7 @@ static void dalloc(T** p, size_t count) {
 void Handle::ensure_batch(int B) {
   if (B <= cap_B) return;
   const int n = L.n, h = L.h;
-  const int max_tiles = 2 * ((n + 127) / 128 + 2);  // two epilogue partials per tail tile
+  const int max_tiles = 4 * ((n + 127) / 128 + 2);  // up to 4 epilogue partials per tail tile
   dalloc(&X, (size_t)B * L.W);
   dalloc(&G1, (size_t)B * h);
   dalloc(&Dhi, (size_t)B * np + 64);
@@ -102,6 +102,12 @@ void Handle::ensure_batch(int B) {
   dalloc(&w, (size_t)B);
   dalloc(&Epart, (size_t)max_splits * B * h);
   dalloc(&dz1, (size_t)B * h);
+  dalloc(&dz1hi, (size_t)B * hp + 64);
+  dalloc(&dz1lo, (size_t)B * hp + 64);
+  dalloc(&Xf, (size_t)B * hd1p + 64);
+  VQMC_CUDA(cudaMemset(dz1hi, 0, ((size_t)B * hp + 64) * sizeof(float)));
+  VQMC_CUDA(cudaMemset(dz1lo, 0, ((size_t)B * hp + 64) * sizeof(float)));
+  VQMC_CUDA(cudaMemset(Xf, 0, ((size_t)B * hd1p + 64) * sizeof(float)));
   cap_B = B;
 }
 
@@ -136,7 +142,7 @@ static void upload_params(Handle* H, const double* theta) {
   VQMC_CUDA(cudaMemcpyAsync(H->P, P.data(), P.size() * sizeof(float), cudaMemcpyHostToDevice, H->stream));
   VQMC_CUDA(cudaStreamSynchronize(H->stream));
   H->theta_host.assign(theta, theta + H->d);
-  launch_refresh_w2ht(H);
+  launch_params_refresh(H);
 }
 
 // live fp32 layout (device) -> reference order fp64; masked entries from `base`
@@ -312,6 +318,7 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   H->hp = (h + 3) & ~3;
   H->hp1 = (h + 1 + 3) & ~3;
   H->np = (n + 3) & ~3;
+  H->hd1p = (Hd + 1 + 3) & ~3;
   H->d = 2LL * h * n + h + n;
   H->degrees.assign(degrees, degrees + h);
   H->num_edges = num_edges;
@@ -322,7 +329,6 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   VQMC_CUDA(cudaMemsetAsync(H->G, 0, H->L.total * sizeof(float), H->stream));
   VQMC_CUDA(cudaMemsetAsync(H->Mo, 0, H->L.total * sizeof(float), H->stream));
   VQMC_CUDA(cudaMemsetAsync(H->Vo, 0, H->L.total * sizeof(float), H->stream));
-  dalloc(&H->W2hT, (size_t)h * Hd);
   dalloc(&H->gw1_part, (size_t)kGw1MaxSplits * (Hd + 1) * h);
   dalloc(&H->W2hi, (size_t)n * H->hp + 64);
   dalloc(&H->W2lo, (size_t)n * H->hp + 64);
@@ -387,9 +393,9 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   DeviceGuard dg(H->device);
   cudaStreamSynchronize(H->stream);
   if (H->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy(H->nccl_comm);
-  void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W2hT, H->W1Tp, H->W2cp, H->W2hi, H->W2lo, H->d_deg, H->d_comp_k,
+  void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2hi, H->W2lo, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1hi, H->G1lo, H->wG1hi, H->wG1lo, H->Dhi, H->Dlo, H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w,
-                  H->Epart, H->dz1, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart};
+                  H->Epart, H->dz1, H->dz1hi, H->dz1lo, H->Xf, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (H->h_scal) cudaFreeHost(H->h_scal);

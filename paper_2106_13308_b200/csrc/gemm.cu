@@ -71,12 +71,12 @@ CUtensorMap tmap_mnmajor(const float* ptr, int64_t MN, int64_t K, int64_t ld, in
   return m;
 }
 
-template <int BN, bool A_MN, bool B_MN, class Epi>
+template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false>
 static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, const CUtensorMap& al,
                         const CUtensorMap& bh, const CUtensorMap& bl, int M, int N, int K, int splits, Epi epi,
                         cudaStream_t stream) {
   using Cfg = UmmaCfg<BN>;
-  auto kern = umma_tf32x3_kernel<BN, A_MN, B_MN, Epi>;
+  auto kern = umma_tf32x3_kernel<BN, A_MN, B_MN, Epi, A_EXACT>;
   static bool attr = false;
   if (!attr) {
     VQMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
@@ -136,56 +136,54 @@ struct TailSampleEpi {
     if (b >= B) return;
     const int cb = colbase + col0;
     const size_t rowD = (size_t)b * np;
-    float dh[32], dl[32];
+    const bool full = cb >= col_lo && cb + 32 <= n;
     uint32_t word = 0;
+    float lsum = 0.f;  // 32 log terms in fp32, then one fp64 add
 #pragma unroll
     for (int j = 0; j < 32; j += 4) {
-      double u[4];
-      if (uni == nullptr) {
-        uint32_t r[4];
-        rng.quad(b, cb + j, r);  // one Philox call covers these 4 bits
-#pragma unroll
-        for (int t = 0; t < 4; ++t) u[t] = u32_to_uniform(r[t]);
-      } else {
-#pragma unroll
-        for (int t = 0; t < 4; ++t) u[t] = (cb + j + t < n) ? uni[(size_t)(cb + j + t) * B + b] : 1.0;
-      }
+      float thr[4];  // draw x = [u < p]: u = (r + 1/2) 2^-32 < p  <=>  r + 1/2 < p 2^32
+      uint32_t r[4];
+      if (uni == nullptr) rng.quad(b, cb + j, r);
+      float hi4[4], lo4[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int c = cb + j + t;
         const bool valid = c >= col_lo && c < n;
         const float z = v[j + t] + (valid ? b2[c] : 0.f);
         const UnitPre q = unit_pre(z);
-        const int x = (valid && u[t] < q.p()) ? 1 : 0;
+        int x;
+        if (uni == nullptr) {
+          thr[t] = (float)(q.p() * 4294967296.0);
+          x = (valid && (float)r[t] + 0.5f < thr[t]) ? 1 : 0;
+        } else {
+          x = (valid && uni[(size_t)c * B + b] < q.p()) ? 1 : 0;
+        }
         word |= (uint32_t)x << (j + t);
         const Unit o = unit_post(q, x);
-        ptx::split_tf32(o.D, dh[j + t], dl[j + t]);
-        if (valid) lps += (double)o.logt;
+        ptx::split_tf32(o.D, hi4[t], lo4[t]);
+        if (valid) lsum += o.logt;
       }
-    }
-    if (cb >= col_lo && cb + 32 <= n) {
-      float4* ph = reinterpret_cast<float4*>(Dhi + rowD + cb);
-      float4* pl = reinterpret_cast<float4*>(Dlo + rowD + cb);
+      if (full) {
+        *reinterpret_cast<float4*>(Dhi + rowD + cb + j) = make_float4(hi4[0], hi4[1], hi4[2], hi4[3]);
+        *reinterpret_cast<float4*>(Dlo + rowD + cb + j) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
+      } else {
 #pragma unroll
-      for (int j = 0; j < 8; ++j) {
-        ph[j] = make_float4(dh[4 * j], dh[4 * j + 1], dh[4 * j + 2], dh[4 * j + 3]);
-        pl[j] = make_float4(dl[4 * j], dl[4 * j + 1], dl[4 * j + 2], dl[4 * j + 3]);
-      }
-    } else {
-#pragma unroll
-      for (int j = 0; j < 32; ++j) {
-        const int c = cb + j;
-        if (c >= col_lo && c < n) {
-          Dhi[rowD + c] = dh[j];
-          Dlo[rowD + c] = dl[j];
+        for (int t = 0; t < 4; ++t) {
+          const int c = cb + j + t;
+          if (c >= col_lo && c < n) {
+            Dhi[rowD + c] = hi4[t];
+            Dlo[rowD + c] = lo4[t];
+          }
         }
       }
     }
+    lps += (double)lsum;
     if (word) atomicOr(&X[(size_t)b * W + (cb >> 5)], word);
   }
   __device__ void end_row(int b, const UmmaArgs&) {
-    if (b < B) lp_part[(size_t)(2 * tile.tn + part) * B + b] = lps;
+    if (b < B) lp_part[(size_t)(kParts * tile.tn + part) * B + b] = lps;
   }
+  static constexpr int kParts = UmmaCfg<128>::kEpiSets;
 };
 
 struct PartialEpi {  // split-K partial: out[z][row][col]
@@ -279,7 +277,7 @@ void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng) {
   const CUtensorMap bh = tmap_kmajor(H->W2hi + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
   const CUtensorMap bl = tmap_kmajor(H->W2lo + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
   TailSampleEpi e{B, L.n, H->np, L.W, colbase, L.Hd, H->P + L.off_b2, uni, rng, H->X, H->Dhi, H->Dlo, H->lp_part, 0, {}, 0.0};
-  H->tail_tiles = 2 * ((ncols + BN - 1) / BN);  // two epilogue partials per column tile
+  H->tail_tiles = TailSampleEpi::kParts * ((ncols + BN - 1) / BN);  // one partial per epilogue set
   launch_umma<BN, false, false>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols, L.h, 1, e, H->stream);
 }
 
@@ -318,6 +316,26 @@ void launch_gw2_umma(Handle* H, int B) {
   const CUtensorMap bl = tmap_mnmajor(H->wG1lo, L.h + 1, B, H->hp1, BN);
   Gw2Epi e{L.n, L.h, 0, {}, H->d_deg, H->G + L.off_w2, H->G + L.off_b2};
   launch_umma<BN, true, true>(H, "bw_gw2_umma", ah, al, bh, bl, L.n, L.h + 1, B, 1, e, H->stream);
+}
+
+// gW1T[j][k] = sum_b X[b][j] dz1[b][k] (j < Hd) and gb1[k] (the ones column j = Hd):
+// split-K partials into gw1_part, reduced and masked by gw1_finalize_kernel.  The spins
+// are exact in tf32, so A is single (two MMA passes).
+void launch_gw1_umma(Handle* H, int B, int& splits_out) {
+  const Layout& L = H->L;
+  constexpr int BN = 128;
+  const int mt = (L.Hd + 1 + kUmmaBM - 1) / kUmmaBM, nt = (L.h + BN - 1) / BN;
+  const int nkb = (B + kUmmaBK - 1) / kUmmaBK;
+  int splits = std::max(1, std::min(std::min(nkb, kGw1MaxSplits), 148 / (mt * nt)));
+  const int per = (nkb + splits - 1) / splits;
+  splits = (nkb + per - 1) / per;
+  splits_out = splits;
+  const CUtensorMap a = tmap_mnmajor(H->Xf, L.Hd + 1, B, H->hd1p, kUmmaBM);
+  const CUtensorMap bh = tmap_mnmajor(H->dz1hi, L.h, B, H->hp, BN);
+  const CUtensorMap bl = tmap_mnmajor(H->dz1lo, L.h, B, H->hp, BN);
+  PartialEpi e{H->gw1_part, L.Hd + 1, L.h, 0, {}};
+  launch_umma<BN, true, true, PartialEpi, true>(H, "bw_gw1_umma", a, a, bh, bl, L.Hd + 1, L.h, B, splits, e,
+                                                 H->stream);
 }
 
 }  // namespace vqmc_b200

@@ -79,7 +79,7 @@ struct KScope {
 };
 
 // Kernel launchers (kernels.cu).  All enqueue on h->stream.
-void launch_refresh_w2ht(Handle* h);
+void launch_params_refresh(Handle* h);
 void launch_head_pack(Handle* h);
 void launch_head_v2(Handle* h, int B, const double* d_uniforms, RngSpec rng, bool given_bits,
                     double* d_cond);
@@ -93,6 +93,7 @@ void launch_tail_umma(Handle* h, int B, const double* d_uniforms, RngSpec rng);
 void launch_dg1_umma(Handle* h, int B);
 void launch_gw2_umma(Handle* h, int B);
 void launch_split_w2(Handle* h);
+void launch_gw1_umma(Handle* h, int B, int& splits_out);
 void set_error(const std::string& msg);
 int status_of(const std::exception& ex);
 void launch_adam(Handle* h, float grad_scale, double lr, double b1, double b2, double eps,
@@ -112,10 +113,9 @@ struct Handle {
   float* G = nullptr;      // live grads
   float* Mo = nullptr;     // Adam m
   float* Vo = nullptr;     // Adam v
-  float* W2hT = nullptr;   // [h][Hd] transposed head block of W2 (masked)
   float* W2hi = nullptr;   // [n][hp] tf32 split of W2m (GEMM operand), refreshed after updates
   float* W2lo = nullptr;
-  int hp = 0, hp1 = 0, np = 0;  // padded row strides: h, h + 1, n rounded up to 4 floats
+  int hp = 0, hp1 = 0, np = 0, hd1p = 0;  // padded row strides: h, h + 1, n rounded up to 4 floats
   int max_splits = 16;
   float* W1Tp = nullptr;   // [Hd][hp] padded head block of W1^T (head sampler staging)
   float* W2cp = nullptr;   // [h][Hdp] W2 head columns in completion order (padded)
@@ -145,6 +145,9 @@ struct Handle {
   float* w = nullptr;        // [B]
   float* Epart = nullptr;    // [splits][B][h]
   float* dz1 = nullptr;      // [B][h]
+  float* dz1hi = nullptr;    // [B][hp] tf32 split of dz1 (gW1 operand)
+  float* dz1lo = nullptr;
+  float* Xf = nullptr;       // [B][hd1p] spins 0/1 of the head inputs + a ones column (gW1 operand)
   float* gw1_part = nullptr; // [kGw1MaxSplits][Hd + 1][h]
   double* cond = nullptr;    // [B][n] optional (log_psi with conditionals)
   double* uni = nullptr;     // [n][B] injected uniforms

@@ -16,6 +16,7 @@
 
 #include "device_common.cuh"
 #include "internal.cuh"
+#include "ptx.cuh"
 
 namespace vqmc_b200 {
 
@@ -82,14 +83,18 @@ __global__ void __launch_bounds__(z2cfg::T::NT) z2_given_kernel(
   }
 }
 
+// log_psi = (head + sum of tail partials) / 2, one warp per sample (fixed reduction order).
 __global__ void finalize_logpsi_kernel(int B, int tiles, const double* __restrict__ lp_head,
                                        const double* __restrict__ lp_part,
                                        double* __restrict__ log_psi) {
-  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
   if (b >= B) return;
-  double s = lp_head[b];
-  for (int t = 0; t < tiles; ++t) s += lp_part[(size_t)t * B + b];
-  log_psi[b] = 0.5 * s;  // sampler.cpp:56 / models.cpp:122-124
+  double s = 0.0;
+  for (int t = lane; t < tiles; t += 32) s += lp_part[(size_t)t * B + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0) log_psi[b] = 0.5 * (lp_head[b] + s);  // sampler.cpp:56 / models.cpp:122-124
 }
 
 // ===========================================================================
@@ -205,58 +210,21 @@ constexpr int BK = 16, TM = 8, TN = 8;
 constexpr int QM = 64, QN = 64;  // gW1
 }  // namespace bwcfg
 
-__global__ void dz1_kernel(int B, int h, int splits, const float* __restrict__ Epart,
+__global__ void dz1_kernel(int B, int h, int hp, int splits, const float* __restrict__ Epart,
                            const float* __restrict__ w, const float* __restrict__ G1,
-                           float* __restrict__ dz1) {
+                           float* __restrict__ dz1, float* __restrict__ dz1hi, float* __restrict__ dz1lo) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t total = (size_t)B * h;
   if (t >= total) return;
   float s = 0.f;
   for (int z = 0; z < splits; ++z) s += Epart[(size_t)z * total + t];
-  const int b = (int)(t / h);
-  dz1[t] = G1[t] > 0.f ? s * w[b] : 0.f;
-}
-
-struct LoadXT {  // A(m = input j (Hd = ones row), k = sample b) = x_bj
-  static constexpr bool kMMajor = true;
-  const uint32_t* X;
-  int W, Hd;
-  __device__ float operator()(int m, int k) const {
-    if (m > Hd) return 0.f;
-    if (m == Hd) return 1.f;
-    return (float)((X[(size_t)k * W + (m >> 5)] >> (m & 31)) & 1u);
-  }
-};
-struct LoadDz1 {  // B(n = hidden k, k = sample b) = dz1[b][k]
-  static constexpr bool kMMajor = true;
-  const float* dz1;
-  int h;
-  __device__ float operator()(int c, int k) const { return c < h ? dz1[(size_t)k * h + c] : 0.f; }
-};
-
-// gW1 partial sums over a chunk of samples (split-K over the batch; deterministic reduction below).
-__global__ void __launch_bounds__(SimtTile<bwcfg::QM, bwcfg::QN, bwcfg::BK, 8, 8>::NT)
-    gw1_kernel(int B, int h, int Hd, int W, int chunk, const uint32_t* __restrict__ X,
-               const float* __restrict__ dz1, float* __restrict__ part) {
-  using namespace bwcfg;
-  using T = SimtTile<QM, QN, BK, TM, TN>;
-  __shared__ __align__(16) float smem[BK * (QM + QN)];
-  const int m0 = blockIdx.y * QM, n0 = blockIdx.x * QN;
-  const int kb = blockIdx.z * chunk, ke = min(B, kb + chunk);
-  float acc[TM][TN];
-  simt_mainloop<QM, QN, BK, TM, TN>(acc, m0, n0, kb, ke, LoadXT{X, W, Hd}, LoadDz1{dz1, h}, smem);
-  const int tx = threadIdx.x % T::NTX, ty = threadIdx.x / T::NTX;
-  float* out = part + (size_t)blockIdx.z * (Hd + 1) * h;
-#pragma unroll
-  for (int r = 0; r < TM; ++r) {
-    const int j = m0 + T::row(ty, r);
-    if (j > Hd) continue;
-#pragma unroll
-    for (int c = 0; c < TN; ++c) {
-      const int k = n0 + T::col(tx, c);
-      if (k < h) out[(size_t)j * h + k] = acc[r][c];
-    }
-  }
+  const int b = (int)(t / h), k = (int)(t % h);
+  const float d = G1[t] > 0.f ? s * w[b] : 0.f;  // relu'(z1) = [z1 > 0] (models.cpp:181)
+  dz1[t] = d;
+  float hi, lo;
+  ptx::split_tf32(d, hi, lo);
+  dz1hi[(size_t)b * hp + k] = hi;
+  dz1lo[(size_t)b * hp + k] = lo;
 }
 
 // gW1T = (sum of partials) (.) M1^T, gb1 = the ones row (j == Hd).
@@ -282,7 +250,9 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, f
                                                    float b2, float eps, float bc1, float bc2,
                                                    float* __restrict__ P, const float* __restrict__ G,
                                                    float* __restrict__ M, float* __restrict__ V,
-                                                   double* __restrict__ gpart) {
+                                                   double* __restrict__ gpart, int64_t w2_off, int64_t w2_len,
+                                                   int h, int hp, float* __restrict__ W2hi,
+                                                   float* __restrict__ W2lo) {
   double sq = 0.0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
@@ -293,7 +263,16 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, f
     M[t] = m;
     V[t] = v;
     const float mh = m / bc1, vh = v / bc2;
-    P[t] = P[t] - lr * (mh / (sqrtf(vh) + eps));
+    const float p = P[t] - lr * (mh / (sqrtf(vh) + eps));
+    P[t] = p;
+    const int64_t u = t - w2_off;
+    if (u >= 0 && u < w2_len) {  // W2 segment: refresh the tf32 split used by the GEMMs
+      const int64_t o = hp == h ? u : (u / h) * hp + (u % h);
+      float hi, lo;
+      ptx::split_tf32(p, hi, lo);
+      W2hi[o] = hi;
+      W2lo[o] = lo;
+    }
   }
   __shared__ double red[8];
 #pragma unroll
@@ -322,22 +301,6 @@ __global__ void sum_partials_kernel(int cnt, const double* __restrict__ part, do
   }
 }
 
-// W2hT[k][i] = W2m[i][k] for head outputs i < Hd (coalesced rows for the head sampler).
-__global__ void refresh_w2ht_kernel(int h, int Hd, const float* __restrict__ W2,
-                                    float* __restrict__ W2hT) {
-  __shared__ float tile[32][33];
-  const int i0 = blockIdx.y * 32, k0 = blockIdx.x * 32;
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int i = i0 + r, k = k0 + threadIdx.x;
-    tile[r][threadIdx.x] = (i < Hd && k < h) ? W2[(size_t)i * h + k] : 0.f;
-  }
-  __syncthreads();
-  for (int r = threadIdx.y; r < 32; r += blockDim.y) {
-    const int k = k0 + r, i = i0 + threadIdx.x;
-    if (k < h && i < Hd) W2hT[(size_t)k * Hd + i] = tile[threadIdx.x][r];
-  }
-}
-
 // ===========================================================================
 // Launchers
 // ===========================================================================
@@ -353,15 +316,11 @@ KScope::~KScope() {
   if (slot >= 0) cudaEventRecord(H->kt_end[slot], H->stream);
 }
 
-void launch_refresh_w2ht(Handle* H) {
+// Derived device copies of the parameters (after set_params): the head sampler's staged
+// head blocks and the tf32 split of W2 (Adam refreshes both itself).
+void launch_params_refresh(Handle* H) {
   launch_head_pack(H);
   launch_split_w2(H);
-  const Layout& L = H->L;
-  dim3 grid((L.h + 31) / 32, (L.Hd + 31) / 32), block(32, 8);
-  KScope ks(H, "refresh_w2ht");
-  refresh_w2ht_kernel<<<grid, block, 0, H->stream>>>(L.h, L.Hd, H->P + L.off_w2, H->W2hT);
-  LAUNCH_CHECK();
-  H->launches++;
 }
 
 void launch_z2(Handle* H, int B, int col0, const double* uni, RngSpec rng, bool given, double* cond) {
@@ -385,14 +344,13 @@ void launch_z2(Handle* H, int B, int col0, const double* uni, RngSpec rng, bool 
 
 void launch_finalize_logpsi(Handle* H, int B, int tiles) {
   KScope ks(H, "finalize_logpsi");
-  finalize_logpsi_kernel<<<(B + 255) / 256, 256, 0, H->stream>>>(B, tiles, H->lp_head, H->lp_part,
-                                                                 H->log_psi);
+  finalize_logpsi_kernel<<<(B + 7) / 8, 256, 0, H->stream>>>(B, tiles, H->lp_head, H->lp_part, H->log_psi);
   LAUNCH_CHECK();
   H->launches++;
 }
 
 void launch_energy(Handle* H, int B) {
-  constexpr int S = 8;
+  constexpr int S = 4;
   const int W = H->L.W;
   const size_t smem = (size_t)S * W * sizeof(uint32_t);
   if (smem > 48 * 1024)
@@ -419,31 +377,21 @@ void launch_backward(Handle* H, int B) {
   {
     KScope ks(H, "bw_dz1");
     const size_t total = (size_t)B * L.h;
-    dz1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->splits, H->Epart, H->w, H->G1,
-                                                                       H->dz1);
+    dz1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp, H->splits, H->Epart, H->w,
+                                                                       H->G1, H->dz1, H->dz1hi, H->dz1lo);
     LAUNCH_CHECK();
     H->launches++;
   }
   launch_gw2_umma(H, B);  // gW2 (.) M2 and gb2
   {
-    const int tiles = ((L.h + QN - 1) / QN) * ((L.Hd + 1 + QM - 1) / QM);
-    int splits = std::max(1, std::min(kGw1MaxSplits, (4 * 148 + tiles - 1) / tiles));
-    int chunk = (B + splits - 1) / splits;
-    chunk = ((chunk + BK - 1) / BK) * BK;
-    splits = (B + chunk - 1) / chunk;
-    dim3 grid((L.h + QN - 1) / QN, (L.Hd + 1 + QM - 1) / QM, splits);
-    {
-      KScope ks(H, "bw_gw1");
-      gw1_kernel<<<grid, SimtTile<QM, QN, BK, TM, TN>::NT, 0, H->stream>>>(B, L.h, L.Hd, L.W, chunk, H->X, H->dz1,
-                                                                           H->gw1_part);
-      LAUNCH_CHECK();
-    }
+    int splits = 1;
+    launch_gw1_umma(H, B, splits);  // gW1 partials (tcgen05)
     KScope ks(H, "bw_gw1_finalize");
     const int total = (L.Hd + 1) * L.h;
     gw1_finalize_kernel<<<(total + 255) / 256, 256, 0, H->stream>>>(L.h, L.Hd, splits, H->gw1_part, H->d_deg,
                                                                      H->G + L.off_w1t, H->G + L.off_b1);
     LAUNCH_CHECK();
-    H->launches += 2;
+    H->launches++;
   }
 }
 
@@ -456,7 +404,8 @@ void launch_adam(Handle* H, float grad_scale, double lr, double b1, double b2, d
   KScope ks(H, "adam");
   adam_kernel<<<blocks, 256, 0, H->stream>>>(H->L.total, grad_scale, (float)lr, (float)b1,
                                              (float)b2, (float)eps, (float)bc1, (float)bc2, H->P,
-                                             H->G, H->Mo, H->Vo, H->d_gpart);
+                                             H->G, H->Mo, H->Vo, H->d_gpart, H->L.off_w2,
+                                             (int64_t)H->L.n * H->L.h, H->L.h, H->hp, H->W2hi, H->W2lo);
   LAUNCH_CHECK();
   }
   {
@@ -465,7 +414,7 @@ void launch_adam(Handle* H, float grad_scale, double lr, double b1, double b2, d
     LAUNCH_CHECK();
   }
   H->launches += 2;
-  launch_refresh_w2ht(H);
+  launch_head_pack(H);  // the W2 tf32 split is fused into adam_kernel
 }
 
 }  // namespace vqmc_b200

@@ -34,7 +34,8 @@ struct UmmaCfg {
   static constexpr int kBBytes = BN * kUmmaBK * 4;
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  static constexpr int kThreads = 384;  // 4 control warps + 8 epilogue warps
+  static constexpr int kEpiSets = BN >= 128 ? 3 : 2;     // epilogue warp sets (4 warps each)
+  static constexpr int kThreads = 128 + 128 * kEpiSets;  // 4 control warps + epilogue warps
   static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256;
 };
 
@@ -54,9 +55,10 @@ struct UmmaTile {
 // double-buffered in TMEM (2 x BN columns) so the epilogue of tile j overlaps the
 // mainloop of tile j + 1.
 //   warp 0  TMA producer     warp 1  MMA issuer     warp 2  TMEM allocator
-//   warps 4-11  epilogue (two sets of 4 warps, alternate 32-column chunks)
-template <int BN, bool A_MN, bool B_MN, class Epi>
-__global__ void __launch_bounds__(384, 1)
+//   warps 4..  epilogue (kEpiSets sets of 4 warps; set s takes 32-column chunks s, s + kEpiSets, ...)
+// A_EXACT: A is exactly representable in tf32 (e.g. 0/1 spins): A_lo is neither loaded nor used.
+template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false>
+__global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
     umma_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                        const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
                        UmmaArgs args, Epi epi) {
@@ -92,7 +94,7 @@ __global__ void __launch_bounds__(384, 1)
     }
     for (int b = 0; b < 2; ++b) {
       ptx::mbar_init(&tfull[b], 1);
-      ptx::mbar_init(&tempty[b], 8);  // one arrive per epilogue warp
+      ptx::mbar_init(&tempty[b], 4 * Cfg::kEpiSets);  // one arrive per epilogue warp
     }
     ptx::fence_mbar_init();
   }
@@ -112,14 +114,14 @@ __global__ void __launch_bounds__(384, 1)
         for (int kb = kb0; kb < kb1; ++kb) {
           if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
           unsigned char* st = base + (size_t)s * Cfg::kStageBytes;
-          ptx::mbar_expect_tx(&full[s], Cfg::kStageBytes);
+          ptx::mbar_expect_tx(&full[s], A_EXACT ? Cfg::kStageBytes - Cfg::kABytes : Cfg::kStageBytes);
           const int kc = kb * kUmmaBK;
           if (A_MN) {
             ptx::tma_load_3d(st, &tA_hi, &full[s], 0, kc, m0 / 32);
-            ptx::tma_load_3d(st + Cfg::kABytes, &tA_lo, &full[s], 0, kc, m0 / 32);
+            if (!A_EXACT) ptx::tma_load_3d(st + Cfg::kABytes, &tA_lo, &full[s], 0, kc, m0 / 32);
           } else {
             ptx::tma_load_2d(st, &tA_hi, &full[s], kc, m0);
-            ptx::tma_load_2d(st + Cfg::kABytes, &tA_lo, &full[s], kc, m0);
+            if (!A_EXACT) ptx::tma_load_2d(st + Cfg::kABytes, &tA_lo, &full[s], kc, m0);
           }
           unsigned char* sb = st + 2 * Cfg::kABytes;
           if (B_MN) {
@@ -166,7 +168,7 @@ __global__ void __launch_bounds__(384, 1)
             const uint32_t acc0 = (kb > kb0 || k > 0) ? 1u : 0u;
             ptx::mma_tf32(acc, ah, bh, idesc, acc0);
             ptx::mma_tf32(acc, ah, bl, idesc, 1u);
-            ptx::mma_tf32(acc, al, bh, idesc, 1u);
+            if (!A_EXACT) ptx::mma_tf32(acc, al, bh, idesc, 1u);
           }
           ptx::mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
           if (++s == Cfg::kStages) {
@@ -177,8 +179,8 @@ __global__ void __launch_bounds__(384, 1)
         ptx::mma_commit(&tfull[buf]);  // accumulator of this tile complete
       }
     }
-  } else if (warp >= 4) {  // ---------------- epilogue (8 warps) ----------------
-    const int q = warp & 3, part = warp < 8 ? 0 : 1;
+  } else if (warp >= 4) {  // ---------------- epilogue ----------------
+    const int q = warp & 3, part = (warp - 4) >> 2;
     int j = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
       const UmmaTile c = tile_of(t);
@@ -194,7 +196,7 @@ __global__ void __launch_bounds__(384, 1)
       e.begin_row(row, args);
       const bool has_k = kb1 > kb0;
 #pragma unroll 1
-      for (int cc = 32 * part; cc < BN; cc += 64) {
+      for (int cc = 32 * part; cc < BN; cc += 32 * Cfg::kEpiSets) {
         if (n0 + cc >= args.N) break;
         float v[32];
         if (has_k) {
