@@ -200,7 +200,8 @@ def run_ours(args):
         K.check(K.lib.vqmc_gpu_comm_init(hd, uid, world, rank))
     K.check(K.lib.vqmc_gpu_adam_reset(hd))
     lr, b1, b2, eps = 0.01, 0.9, 0.999, 1e-8
-    stream0 = 1 + rank  # worker w = rank uses make_stream(seed, w + 1)'s Philox key
+    from paper_2106_13308_b200 import dp
+    stream0 = dp.RankPlan(rank, world, 1).stream0  # worker w = rank -> stream (seed, w + 1)
     step = [0]
 
     def one_step(stats=None):

@@ -299,7 +299,7 @@ void launch_dg1_umma(Handle* H, int B) {
   launch_umma<BN, false, true>(H, "bw_dg1_umma", ah, al, bh, bl, B, L.h, L.n, splits, e, H->stream);
 }
 
-void launch_gw2_umma(Handle* H, int B) {
+void launch_gw2_umma(Handle* H, int B) {  // BN = 128: 3-stage ring, 4 column tiles of h + 1
   const Layout& L = H->L;
   {
     const int64_t total = (int64_t)B * H->hp1;
@@ -309,7 +309,7 @@ void launch_gw2_umma(Handle* H, int B) {
     VQMC_CUDA(cudaGetLastError());
     H->launches++;
   }
-  constexpr int BN = 256;
+  constexpr int BN = 128;
   const CUtensorMap ah = tmap_mnmajor(H->Dhi, L.n, B, H->np, kUmmaBM);
   const CUtensorMap al = tmap_mnmajor(H->Dlo, L.n, B, H->np, kUmmaBM);
   const CUtensorMap bh = tmap_mnmajor(H->wG1hi, L.h + 1, B, H->hp1, BN);
