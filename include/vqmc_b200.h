@@ -147,11 +147,15 @@ int vqmc_gpu_synchronize(vqmc_gpu_t* g);
 /* Number of kernel launches the handle has issued (for the bench's gpu_launches). */
 int64_t vqmc_gpu_launch_count(const vqmc_gpu_t* g);
 
-/* Device-side timing of the last train step's phases (ms): sample, energy,
- * backward, allreduce, update. */
+/* Device-side timing of the last train step (ms): level 2 gives the phases sample,
+ * energy+weights, backward, allreduce, update; level 1 gives the whole step in out_ms[0]. */
 int vqmc_gpu_phase_times(vqmc_gpu_t* g, float out_ms[5]);
-/* Enable/disable CUDA-event phase timing inside train_step (default off). */
-int vqmc_gpu_set_phase_timing(vqmc_gpu_t* g, int enable);
+/* CUDA-event timing inside train_step: 0 off (default), 1 whole step, 2 per phase. */
+int vqmc_gpu_set_phase_timing(vqmc_gpu_t* g, int level);
+
+/* Replay the training step as a captured CUDA graph (default on; the first step of a
+ * configuration runs eagerly, the second is captured). */
+int vqmc_gpu_set_graph(vqmc_gpu_t* g, int enable);
 
 /* Per-kernel CUDA-event timing of the last train step (roofline evidence):
  * names_out = count slots of 32 chars, ms_out = count durations. */

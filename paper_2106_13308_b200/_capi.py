@@ -53,6 +53,7 @@ _SIGS = {
     "vqmc_gpu_evaluate": [_vp, C.c_int, _vp, _u64, _u64, _u64, _vp],
     "vqmc_gpu_synchronize": [_vp],
     "vqmc_gpu_set_phase_timing": [_vp, C.c_int],
+    "vqmc_gpu_set_graph": [_vp, C.c_int],
     "vqmc_gpu_phase_times": [_vp, _vp],
     "vqmc_gpu_set_kernel_timing": [_vp, C.c_int],
     "vqmc_gpu_kernel_times": [_vp, _vp, _vp, C.c_int, C.POINTER(C.c_int)],

@@ -82,6 +82,7 @@ static void dalloc(T** p, size_t count) {
 
 void Handle::ensure_batch(int B) {
   if (B <= cap_B) return;
+  invalidate_graph();
   const int n = L.n, h = L.h;
   const int max_tiles = 4 * ((n + 127) / 128 + 2);  // up to 4 epilogue partials per tail tile
   dalloc(&X, (size_t)B * L.W);
@@ -199,7 +200,7 @@ static void upload_bits(Handle* H, const uint32_t* bits, int B) {
 // `workers` segments of B / workers rows; segment s draws from stream
 // (stream0 + s) (trainer.cpp:126: worker w uses make_stream(seed, w + 1)).
 static void sample_into(Handle* H, int B, int workers, const double* uniforms_host, uint64_t seed,
-                        uint64_t stream0, uint64_t call) {
+                        uint64_t stream0, uint64_t call, bool device_call = false, bool want_log_psi = true) {
   H->ensure_batch(B);
   const double* du = nullptr;
   if (uniforms_host) {
@@ -208,16 +209,16 @@ static void sample_into(Handle* H, int B, int workers, const double* uniforms_ho
                               cudaMemcpyHostToDevice, H->stream));
     du = H->uni;
   }
-  RngSpec rng{seed, stream0, call, B / workers};
+  RngSpec rng{seed, stream0, call, B / workers, device_call ? H->d_step : nullptr};
   VQMC_CUDA(cudaMemsetAsync(H->X, 0, (size_t)B * H->L.W * sizeof(uint32_t), H->stream));
   launch_head_v2(H, B, du, rng, false, nullptr);
   launch_z2(H, B, H->L.Hd, du, rng, false, nullptr);
-  launch_finalize_logpsi(H, B, H->tail_tiles);
+  if (want_log_psi) launch_finalize_logpsi(H, B, H->tail_tiles);  // the training step never reads log psi
 }
 
 // Forward from configurations already in H->X.
 static void forward_given(Handle* H, int B, double* cond) {
-  RngSpec none{0, 0, 0, 1};
+  RngSpec none{0, 0, 0, 1, nullptr};
   launch_head_v2(H, B, nullptr, none, true, cond);
   launch_z2(H, B, H->L.Hd, nullptr, none, true, cond);
   launch_finalize_logpsi(H, B, H->tail_tiles);
@@ -315,6 +316,7 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   DeviceGuard dg(device);
   VQMC_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
   H->L.init(n, h, Hd);
+  if (H->L.total >= (int64_t(1) << 31)) throw std::invalid_argument("model too large for the device layout (> 2^31 live parameters)");
   H->hp = (h + 3) & ~3;
   H->hp1 = (h + 1 + 3) & ~3;
   H->np = (n + 3) & ~3;
@@ -360,9 +362,20 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
                         : (h + 31) / 32 <= 8 ? 8 : (h + 31) / 32 <= 16 ? 16 : 32);
     dalloc(&H->W1Tp, (size_t)Hd * kp);
     dalloc(&H->W2cp, (size_t)h * kp);
+    VQMC_CUDA(cudaMemset(H->W1Tp, 0, (size_t)Hd * kp * sizeof(float)));
+    VQMC_CUDA(cudaMemset(H->W2cp, 0, (size_t)h * kp * sizeof(float)));
+    H->head_hpk = kp;
+    H->head_Hdp = H->head_fast ? kp : 32 * ((Hd + 31) / 32);
+    std::vector<int32_t> cpos(h);
+    for (int c = 0; c < h; ++c) cpos[ks[c]] = c;
+    dalloc(&H->d_comp_pos, (size_t)h);
+    VQMC_CUDA(cudaMemcpy(H->d_comp_pos, cpos.data(), h * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
   upload_edges(H, edges, num_edges);
   dalloc(&H->d_scal, 16);
+  dalloc(&H->d_step, 1);
+  dalloc(&H->d_done, 1);
+  VQMC_CUDA(cudaMemset(H->d_done, 0, sizeof(unsigned)));
   ensure_istat(H, 64);
   H->gpart_n = 148 * 4;
   dalloc(&H->d_gpart, (size_t)H->gpart_n);
@@ -392,10 +405,11 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   if (!H) return VQMC_OK;
   DeviceGuard dg(H->device);
   cudaStreamSynchronize(H->stream);
+  H->invalidate_graph();
   if (H->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy(H->nccl_comm);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2hi, H->W2lo, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1hi, H->G1lo, H->wG1hi, H->wG1lo, H->Dhi, H->Dlo, H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w,
-                  H->Epart, H->dz1, H->dz1hi, H->dz1lo, H->Xf, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart};
+                  H->Epart, H->dz1, H->dz1hi, H->dz1lo, H->Xf, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart, H->d_step, H->d_done, H->d_comp_pos};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (H->h_scal) cudaFreeHost(H->h_scal);
@@ -417,6 +431,7 @@ int vqmc_gpu_set_edges(vqmc_gpu_t* g, const int32_t* edges, int64_t num_edges) {
   DeviceGuard dg(H->device);
   validate_edges(H->L.n, edges, num_edges);
   VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  H->invalidate_graph();
   upload_edges(H, edges, num_edges);
   API_CATCH
 }
@@ -555,7 +570,9 @@ int vqmc_gpu_adam_step(vqmc_gpu_t* g, const double* grad, double lr, double beta
     for (int i = 0; i < n; ++i) G[L.off_b2 + i] = (float)gb2[i];
     VQMC_CUDA(cudaMemcpyAsync(H->G, G.data(), G.size() * sizeof(float), cudaMemcpyHostToDevice, H->stream));
   }
-  launch_adam(H, 1.0f, lr, beta1, beta2, eps, t);
+  launch_set_step(H, 0, t, lr, beta1, beta2, eps);
+  H->next_call = ~0ull;  // the next train step must re-seed the device counters
+  launch_adam(H, 1.0f);
   VQMC_CUDA(cudaStreamSynchronize(H->stream));
   API_CATCH
 }
@@ -593,8 +610,51 @@ int vqmc_gpu_comm_init(vqmc_gpu_t* g, const uint8_t id[128], int nranks, int ran
   ncclComm_t comm = nullptr;
   nccl_check(g_nccl.CommInitRank(&comm, nranks, uid, rank), "ncclCommInitRank");
   H->nccl_comm = comm;
+  H->invalidate_graph();
   API_CATCH
 }
+
+}  // extern "C"
+
+namespace vqmc_b200 {
+
+void Handle::invalidate_graph() {
+  if (gexec) cudaGraphExecDestroy(gexec);
+  gexec = nullptr;
+  gkey = -1;
+  graph_warm = false;
+}
+
+// The work of one training step (worker_body, trainer.cpp:150-282) on the handle's stream.
+// The Philox counter and the Adam step are taken from H->d_step, which the first kernel
+// advances, so the same sequence can be captured once and replayed as a CUDA graph.
+static void enqueue_train_step(Handle* H, int minibatch, int workers, const double* uniforms, uint64_t seed,
+                               uint64_t stream0) {
+  const int B = minibatch * workers;
+  H->kt_count = 0;
+  const bool tm = H->phase_timing >= 2, t0 = H->phase_timing >= 1;
+  if (t0) record_event(H, H->ev[0]);
+  launch_step_advance(H);
+  sample_into(H, B, workers, uniforms, seed, stream0, 0, /*device_call=*/true, /*want_log_psi=*/false);
+  if (tm) record_event(H, H->ev[1]);
+  launch_energy(H, B);                          // local_energy_batch (:161)
+  launch_weights_from_locals(H, B, minibatch);  // gradient_from_locals weights (:164)
+  if (tm) record_event(H, H->ev[2]);
+  launch_backward(H, B);  // weighted_grad_log_psi
+  if (tm) record_event(H, H->ev[3]);
+  if (H->nccl_comm) {  // allreduce_mean (:187): sum here, / L in Adam
+    KScope ks(H, "nccl_allreduce");
+    nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)H->L.total, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
+               "ncclAllReduce");
+  }
+  if (tm) record_event(H, H->ev[4]);
+  launch_adam(H, 1.0f / (float)(workers * H->nranks));  // adam_step (:221)
+  if (t0) record_event(H, H->ev[5]);
+}
+
+}  // namespace vqmc_b200
+
+extern "C" {
 
 int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double* uniforms, uint64_t seed,
                         uint64_t stream0, uint64_t call, double lr, double beta1, double beta2, double eps,
@@ -606,26 +666,55 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
   if (workers < 1) throw std::invalid_argument("workers must be >= 1");
   if (t < 1) throw std::invalid_argument("adam step count must be >= 1");
   const int B = minibatch * workers;
+  if (B > H->cap_B) H->invalidate_graph();
   H->ensure_batch(B);
+  if (workers > H->istat_cap) H->invalidate_graph();
   ensure_istat(H, workers);
-  H->kt_count = 0;
-  const bool tm = H->phase_timing;
-  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[0], H->stream));
-  sample_into(H, B, workers, uniforms, seed, stream0, call);  // draw (trainer.cpp:157)
-  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[1], H->stream));
-  launch_energy(H, B);                                        // local_energy_batch (:161)
-  launch_weights_from_locals(H, B, minibatch);                // gradient_from_locals weights (:164)
-  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[2], H->stream));
-  launch_backward(H, B);                                      // weighted_grad_log_psi
-  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[3], H->stream));
-  if (H->nccl_comm) {                                         // allreduce_mean (:187): sum, /L in Adam
-    KScope ks(H, "nccl_allreduce");
-    nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)H->L.total, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
-               "ncclAllReduce");
+  // device step counters: the step's first kernel turns (call - 1, t - 1) into (call, t)
+  if (call != H->next_call || t != H->next_t || lr != H->cur_lr || beta1 != H->cur_b1 || beta2 != H->cur_b2 ||
+      eps != H->cur_eps) {
+    launch_set_step(H, call - 1, t - 1, lr, beta1, beta2, eps);
+    H->cur_lr = lr;
+    H->cur_b1 = beta1;
+    H->cur_b2 = beta2;
+    H->cur_eps = eps;
   }
-  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[4], H->stream));
-  launch_adam(H, 1.0f / (float)(workers * H->nranks), lr, beta1, beta2, eps, t);  // adam_step (:221)
-  if (tm) VQMC_CUDA(cudaEventRecord(H->ev[5], H->stream));
+  const bool graphable = H->graph_enabled && uniforms == nullptr;
+  const long long key = ((long long)minibatch << 24) ^ ((long long)workers << 4) ^ (H->ktimer ? 1 : 0) ^
+                        ((long long)H->phase_timing << 1) ^ ((long long)(seed & 0xFFFF) << 44) ^ ((long long)stream0 << 40);
+  if (!graphable) {
+    enqueue_train_step(H, minibatch, workers, uniforms, seed, stream0);
+  } else if (H->gexec && H->gkey == key) {
+    VQMC_CUDA(cudaGraphLaunch(H->gexec, H->stream));  // replay the captured step
+  } else if (!H->graph_warm || H->gkey != key) {
+    if (H->gexec) {
+      cudaGraphExecDestroy(H->gexec);
+      H->gexec = nullptr;
+    }
+    enqueue_train_step(H, minibatch, workers, uniforms, seed, stream0);  // eager warm-up step
+    H->graph_warm = true;
+    H->gkey = key;
+  } else {
+    cudaGraph_t graph = nullptr;
+    VQMC_CUDA(cudaStreamBeginCapture(H->stream, cudaStreamCaptureModeThreadLocal));
+    H->capturing = true;
+    try {
+      enqueue_train_step(H, minibatch, workers, uniforms, seed, stream0);
+      H->capturing = false;
+    } catch (...) {
+      H->capturing = false;
+      cudaStreamEndCapture(H->stream, &graph);
+      if (graph) cudaGraphDestroy(graph);
+      throw;
+    }
+    VQMC_CUDA(cudaStreamEndCapture(H->stream, &graph));
+    VQMC_CUDA(cudaGraphInstantiate(&H->gexec, graph, 0));
+    cudaGraphDestroy(graph);
+    H->gkey = key;
+    VQMC_CUDA(cudaGraphLaunch(H->gexec, H->stream));
+  }
+  H->next_call = call + 1;
+  H->next_t = t + 1;
   if (stats_out) {
     VQMC_CUDA(cudaMemcpyAsync(H->h_scal, H->d_scal, sizeof(double), cudaMemcpyDeviceToHost, H->stream));
     VQMC_CUDA(cudaMemcpyAsync(H->h_istat, H->d_istat, 3 * workers * sizeof(int64_t), cudaMemcpyDeviceToHost,
@@ -694,9 +783,18 @@ int vqmc_gpu_synchronize(vqmc_gpu_t* g) {
 
 int64_t vqmc_gpu_launch_count(const vqmc_gpu_t* g) { return reinterpret_cast<const Handle*>(g)->launches; }
 
+int vqmc_gpu_set_graph(vqmc_gpu_t* g, int enable) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  H->graph_enabled = enable != 0;
+  H->invalidate_graph();
+  API_CATCH
+}
+
 int vqmc_gpu_set_phase_timing(vqmc_gpu_t* g, int enable) {
   API_TRY
-  reinterpret_cast<Handle*>(g)->phase_timing = enable != 0;
+  Handle* H = reinterpret_cast<Handle*>(g);
+  H->phase_timing = enable < 0 ? 0 : enable > 2 ? 2 : enable;
   API_CATCH
 }
 
@@ -724,7 +822,12 @@ int vqmc_gpu_phase_times(vqmc_gpu_t* g, float out_ms[5]) {
   API_TRY
   Handle* H = reinterpret_cast<Handle*>(g);
   VQMC_CUDA(cudaStreamSynchronize(H->stream));
-  for (int i = 0; i < 5; ++i) VQMC_CUDA(cudaEventElapsedTime(&out_ms[i], H->ev[i], H->ev[i + 1]));
+  if (H->phase_timing >= 2) {
+    for (int i = 0; i < 5; ++i) VQMC_CUDA(cudaEventElapsedTime(&out_ms[i], H->ev[i], H->ev[i + 1]));
+  } else {
+    VQMC_CUDA(cudaEventElapsedTime(&out_ms[0], H->ev[0], H->ev[5]));  // level 1: whole step only
+    for (int i = 1; i < 5; ++i) out_ms[i] = 0.f;
+  }
   API_CATCH
 }
 

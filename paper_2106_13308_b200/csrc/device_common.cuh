@@ -51,10 +51,12 @@ __device__ __forceinline__ uint64_t mix_seed_dev(uint64_t seed, uint64_t stream)
 struct RngSpec {
   uint64_t seed, stream0, call;
   int seg;
+  const StepParams* sp;  // when set, the call counter is read from device memory (graph replays)
+  __device__ __forceinline__ uint64_t c() const { return sp ? sp->call : call; }
   // raw outputs for bits (i & ~3) .. (i | 3) of row b
   __device__ __forceinline__ void quad(int b, int i, uint32_t (&r)[4]) const {
     const int s = b / seg;
-    philox4(mix_seed_dev(seed, stream0 + (uint64_t)s), (uint32_t)(i >> 2), (uint32_t)(b - s * seg), call, r);
+    philox4(mix_seed_dev(seed, stream0 + (uint64_t)s), (uint32_t)(i >> 2), (uint32_t)(b - s * seg), c(), r);
   }
   __device__ __forceinline__ double operator()(int b, int i) const {
     uint32_t r[4];

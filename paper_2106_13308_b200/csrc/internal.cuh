@@ -69,6 +69,18 @@ struct Layout {
 
 struct Handle;
 struct RngSpec;
+// Timing event on the handle's stream; inside a graph capture it becomes an external event
+// record node so replays still record (and can be timed).
+void record_event(Handle* h, cudaEvent_t ev);
+
+// Per-step scalars kept in device memory so a captured CUDA graph of the step can be replayed:
+// the graph's first kernel advances call/t and the Adam bias corrections.
+struct StepParams {
+  uint64_t call;  // Philox counter of this step
+  int64_t t;      // Adam step count after the increment
+  float lr, b1, b2, eps;
+  float bc1, bc2;  // 1 - beta^t
+};
 
 // RAII per-kernel event pair (active only when Handle::ktimer is set).
 struct KScope {
@@ -96,8 +108,9 @@ void launch_split_w2(Handle* h);
 void launch_gw1_umma(Handle* h, int B, int& splits_out);
 void set_error(const std::string& msg);
 int status_of(const std::exception& ex);
-void launch_adam(Handle* h, float grad_scale, double lr, double b1, double b2, double eps,
-                 int64_t t);
+void launch_adam(Handle* h, float grad_scale);  // hyper-parameters from h->d_step
+void launch_step_advance(Handle* h);
+void launch_set_step(Handle* h, uint64_t call, int64_t t, double lr, double b1, double b2, double eps);
 
 struct Handle {
   int device = 0;
@@ -119,6 +132,9 @@ struct Handle {
   int max_splits = 16;
   float* W1Tp = nullptr;   // [Hd][hp] padded head block of W1^T (head sampler staging)
   float* W2cp = nullptr;   // [h][Hdp] W2 head columns in completion order (padded)
+  int head_hpk = 0, head_Hdp = 0;  // row strides of W1Tp / W2cp
+  int32_t* d_comp_pos = nullptr;   // [h] completion slot of hidden unit k (inverse of comp_k)
+  unsigned* d_done = nullptr;      // last-block counter of the Adam grad-norm reduction
   std::vector<int32_t> comp_off_host;  // [Hd + 1]
   bool head_fast = false;  // bit i completes exactly hidden unit i
   bool w1skip = false;     // deg_k <= k + 1 for all k (W1 columns below the current word are dead)
@@ -167,12 +183,24 @@ struct Handle {
   double* h_scal = nullptr;
   int64_t* h_istat = nullptr;  // pinned, istat_cap entries
 
+  // per-step scalars and the captured step graph
+  StepParams* d_step = nullptr;
+  cudaGraphExec_t gexec = nullptr;
+  long long gkey = -1;          // (minibatch, workers, timers) the graph was captured for
+  bool graph_enabled = true;
+  bool graph_warm = false;      // one eager step runs before the first capture
+  bool capturing = false;       // inside cudaStreamBeginCapture on this handle's stream
+  uint64_t next_call = ~0ull;   // (call, t) the device counters will produce next
+  int64_t next_t = -1;
+  double cur_lr = -1, cur_b1 = -1, cur_b2 = -1, cur_eps = -1;
+  void invalidate_graph();
+
   // comm
   void* nccl_comm = nullptr;
   int nranks = 1, rank = 0;
 
   // timing
-  bool phase_timing = false;
+  int phase_timing = 0;  // 0 off, 1 whole-step events, 2 per-phase events
   cudaEvent_t ev[6] = {};
   float phase_ms[5] = {0, 0, 0, 0, 0};
 

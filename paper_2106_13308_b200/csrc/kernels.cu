@@ -246,43 +246,99 @@ __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __re
 // weights, gradient scaled by 1/L (allreduce_mean's division, trainer.cpp:334).
 // Also the squared-norm partials of the reduced gradient (trainer.cpp:253).
 // ===========================================================================
-__global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, float lr, float b1,
-                                                   float b2, float eps, float bc1, float bc2,
+// Adam over the live parameter buffer (optimizer.cpp:21-35), fp32 master weights, gradient
+// scaled by 1/L (allreduce_mean's division, trainer.cpp:334), fused with everything that
+// derives from the updated parameters: the squared norm of the reduced gradient (last-block
+// reduction, fixed order; trainer.cpp:253), the tf32 split of W2 for the GEMMs and the head
+// sampler's padded / completion-ordered copies of the head blocks.
+struct AdamOut {
+  int h, hp, Hd, hpk, Hdp;
+  int64_t off_b1, off_w2, off_b2;
+  const int* comp_pos;  // completion slot of hidden unit k
+  float* W1Tp;
+  float* W2cp;
+  float* W2hi;
+  float* W2lo;
+};
+
+__device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, float p) {
+  // (32-bit index math: the live buffer is < 2^31 entries, checked at handle creation)
+  if (t < o.off_b1) {  // W1T[j][k]
+    const unsigned tt = (unsigned)t, j = tt / (unsigned)o.h, k = tt - j * (unsigned)o.h;
+    o.W1Tp[(size_t)j * o.hpk + k] = p;
+  } else if (t >= o.off_w2 && t < o.off_b2) {  // W2[i][k]
+    const unsigned u = (unsigned)(t - o.off_w2), i = u / (unsigned)o.h, k = u - i * (unsigned)o.h;
+    float hi, lo;
+    ptx::split_tf32(p, hi, lo);
+    o.W2hi[(size_t)i * o.hp + k] = hi;
+    o.W2lo[(size_t)i * o.hp + k] = lo;
+    if ((int)i < o.Hd) o.W2cp[(size_t)o.comp_pos[k] * o.Hdp + i] = p;
+  }
+}
+
+__global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, const StepParams* __restrict__ sp,
                                                    float* __restrict__ P, const float* __restrict__ G,
                                                    float* __restrict__ M, float* __restrict__ V,
-                                                   double* __restrict__ gpart, int64_t w2_off, int64_t w2_len,
-                                                   int h, int hp, float* __restrict__ W2hi,
-                                                   float* __restrict__ W2lo) {
+                                                   double* __restrict__ gpart, unsigned* __restrict__ done,
+                                                   double* __restrict__ gnorm2, AdamOut o) {
+  const float lr = sp->lr, b1 = sp->b1, b2 = sp->b2, eps = sp->eps, bc1 = sp->bc1, bc2 = sp->bc2;
   double sq = 0.0;
-  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
-    const float g = G[t] * scale;
+  auto upd = [&](float g, float& m, float& v, float& p) {
+    g *= scale;
     sq += (double)g * (double)g;
-    const float m = b1 * M[t] + (1.f - b1) * g;
-    const float v = b2 * V[t] + (1.f - b2) * (g * g);
+    m = b1 * m + (1.f - b1) * g;
+    v = b2 * v + (1.f - b2) * (g * g);
+    const float mh = m / bc1, vh = v / bc2;
+    p = p - lr * (mh / (sqrtf(vh) + eps));
+  };
+  const int64_t nq = total / 4;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
+    float4 g4 = reinterpret_cast<const float4*>(G)[q];
+    float4 m4 = reinterpret_cast<float4*>(M)[q];
+    float4 v4 = reinterpret_cast<float4*>(V)[q];
+    float4 p4 = reinterpret_cast<float4*>(P)[q];
+    upd(g4.x, m4.x, v4.x, p4.x);
+    upd(g4.y, m4.y, v4.y, p4.y);
+    upd(g4.z, m4.z, v4.z, p4.z);
+    upd(g4.w, m4.w, v4.w, p4.w);
+    reinterpret_cast<float4*>(M)[q] = m4;
+    reinterpret_cast<float4*>(V)[q] = v4;
+    reinterpret_cast<float4*>(P)[q] = p4;
+    const int64_t t = 4 * q;
+    adam_side_writes(o, t, p4.x);
+    adam_side_writes(o, t + 1, p4.y);
+    adam_side_writes(o, t + 2, p4.z);
+    adam_side_writes(o, t + 3, p4.w);
+  }
+  for (int64_t t = 4 * nq + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+    float g = G[t], m = M[t], v = V[t], p = P[t];
+    upd(g, m, v, p);
     M[t] = m;
     V[t] = v;
-    const float mh = m / bc1, vh = v / bc2;
-    const float p = P[t] - lr * (mh / (sqrtf(vh) + eps));
     P[t] = p;
-    const int64_t u = t - w2_off;
-    if (u >= 0 && u < w2_len) {  // W2 segment: refresh the tf32 split used by the GEMMs
-      const int64_t o = hp == h ? u : (u / h) * hp + (u % h);
-      float hi, lo;
-      ptx::split_tf32(p, hi, lo);
-      W2hi[o] = hi;
-      W2lo[o] = lo;
-    }
+    adam_side_writes(o, t, p);
   }
   __shared__ double red[8];
+  __shared__ bool last;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(kFull, sq, o);
+  for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(kFull, sq, off);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
   __syncthreads();
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
     gpart[blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(done, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (last && threadIdx.x == 0) {  // fixed-order final sum by the last block
+    __threadfence();
+    double s = 0.0;
+    for (unsigned i = 0; i < gridDim.x; ++i) s += ((volatile double*)gpart)[i];
+    *gnorm2 = s;
+    *done = 0u;
   }
 }
 
@@ -306,14 +362,19 @@ __global__ void sum_partials_kernel(int cnt, const double* __restrict__ part, do
 // ===========================================================================
 #define LAUNCH_CHECK() VQMC_CUDA(cudaGetLastError())
 
+void record_event(Handle* H, cudaEvent_t ev) {
+  if (H->capturing) VQMC_CUDA(cudaEventRecordWithFlags(ev, H->stream, cudaEventRecordExternal));
+  else VQMC_CUDA(cudaEventRecord(ev, H->stream));
+}
+
 KScope::KScope(Handle* h, const char* name) : H(h), slot(-1) {
   if (!H->ktimer || H->kt_count >= Handle::kKtPool) return;
   slot = H->kt_count++;
   H->kt_name[slot] = name;
-  cudaEventRecord(H->kt_start[slot], H->stream);
+  record_event(H, H->kt_start[slot]);
 }
 KScope::~KScope() {
-  if (slot >= 0) cudaEventRecord(H->kt_end[slot], H->stream);
+  if (slot >= 0) record_event(H, H->kt_end[slot]);
 }
 
 // Derived device copies of the parameters (after set_params): the head sampler's staged
@@ -395,26 +456,46 @@ void launch_backward(Handle* H, int B) {
   }
 }
 
-void launch_adam(Handle* H, float grad_scale, double lr, double b1, double b2, double eps,
-                 int64_t t) {
-  const double bc1 = 1.0 - std::pow(b1, (double)t);
-  const double bc2 = 1.0 - std::pow(b2, (double)t);
-  const int blocks = H->gpart_n;
-  {
-  KScope ks(H, "adam");
-  adam_kernel<<<blocks, 256, 0, H->stream>>>(H->L.total, grad_scale, (float)lr, (float)b1,
-                                             (float)b2, (float)eps, (float)bc1, (float)bc2, H->P,
-                                             H->G, H->Mo, H->Vo, H->d_gpart, H->L.off_w2,
-                                             (int64_t)H->L.n * H->L.h, H->L.h, H->hp, H->W2hi, H->W2lo);
+__global__ void step_advance_kernel(StepParams* sp) {
+  sp->call += 1;
+  sp->t += 1;
+  sp->bc1 = (float)(1.0 - pow((double)sp->b1, (double)sp->t));  // optimizer.cpp:28-29
+  sp->bc2 = (float)(1.0 - pow((double)sp->b2, (double)sp->t));
+}
+
+__global__ void set_step_kernel(StepParams* sp, uint64_t call, int64_t t, float lr, float b1, float b2,
+                                float eps) {
+  sp->call = call;
+  sp->t = t;
+  sp->lr = lr;
+  sp->b1 = b1;
+  sp->b2 = b2;
+  sp->eps = eps;
+  sp->bc1 = (float)(1.0 - pow((double)b1, (double)t));
+  sp->bc2 = (float)(1.0 - pow((double)b2, (double)t));
+}
+
+void launch_step_advance(Handle* H) {
+  step_advance_kernel<<<1, 1, 0, H->stream>>>(H->d_step);
   LAUNCH_CHECK();
-  }
-  {
-    KScope ks(H, "grad_norm");
-    sum_partials_kernel<<<1, 256, 0, H->stream>>>(blocks, H->d_gpart, H->d_scal);
-    LAUNCH_CHECK();
-  }
-  H->launches += 2;
-  launch_head_pack(H);  // the W2 tf32 split is fused into adam_kernel
+  H->launches++;
+}
+
+void launch_set_step(Handle* H, uint64_t call, int64_t t, double lr, double b1, double b2, double eps) {
+  set_step_kernel<<<1, 1, 0, H->stream>>>(H->d_step, call, t, (float)lr, (float)b1, (float)b2, (float)eps);
+  LAUNCH_CHECK();
+  H->launches++;
+}
+
+void launch_adam(Handle* H, float grad_scale) {
+  const Layout& L = H->L;
+  AdamOut o{L.h, H->hp, L.Hd, H->head_hpk, H->head_Hdp, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
+            H->W1Tp, H->W2cp, H->W2hi, H->W2lo};
+  KScope ks(H, "adam");
+  adam_kernel<<<H->gpart_n, 256, 0, H->stream>>>(L.total, grad_scale, H->d_step, H->P, H->G, H->Mo, H->Vo,
+                                                 H->d_gpart, H->d_done, H->d_scal, o);
+  LAUNCH_CHECK();
+  H->launches++;
 }
 
 }  // namespace vqmc_b200
