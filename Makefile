@@ -9,7 +9,9 @@ LIB := paper_2106_13308_b200/lib/libvqmc_b200.so
 OBJDIR := build/obj
 OBJS := $(patsubst paper_2106_13308_b200/csrc/%.cu,$(OBJDIR)/%.o,$(SRC)) $(OBJDIR)/host.o
 
-all: $(LIB) oracle
+CLI := paper_2106_13308_b200/bin/vqmc
+
+all: $(LIB) $(CLI) oracle
 
 $(OBJDIR)/%.o: paper_2106_13308_b200/csrc/%.cu $(HDRS)
 	@mkdir -p $(OBJDIR)
@@ -23,10 +25,14 @@ $(LIB): $(OBJS)
 	@mkdir -p paper_2106_13308_b200/lib
 	$(NVCC) $(ARCH) -shared -o $@ $(OBJS) -ldl -lpthread
 
+$(CLI): tools/vqmc_cli.cpp include/vqmc_b200/vqmc.hpp include/vqmc_b200.h $(LIB)
+	@mkdir -p paper_2106_13308_b200/bin
+	g++ -O2 -std=c++17 -Iinclude -o $@ tools/vqmc_cli.cpp -Lpaper_2106_13308_b200/lib -lvqmc_b200 -Wl,-rpath,'$$ORIGIN/../lib'
+
 oracle:
 	$(MAKE) -s -C oracle
 
 clean:
-	rm -rf build paper_2106_13308_b200/lib oracle/_build
+	rm -rf build paper_2106_13308_b200/lib paper_2106_13308_b200/bin oracle/_build
 
 .PHONY: all oracle clean

@@ -1,0 +1,107 @@
+"""The `vqmc` command-line drop-in (tools/vqmc_cli.cpp) against the reference CLI contract
+(proj/tools/vqmc.cpp, proj/tests/cli_test.sh): subcommands, flag precedence with --config,
+output files, pairing rejection and exit codes.  The solve / sample-test runs need a GPU."""
+import json
+import os
+import subprocess
+
+import numpy as np
+import pytest
+
+import pyoracle as O
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+BIN = os.path.join(ROOT, "paper_2106_13308_b200", "bin", "vqmc")
+
+
+def run(*args, env=None, cwd=None):
+    e = dict(os.environ)
+    if env:
+        e.update(env)
+    return subprocess.run([BIN, *map(str, args)], capture_output=True, text=True, env=e, cwd=cwd)
+
+
+def test_gen_instance_matches_reference_generator(tmp_path):
+    p = tmp_path / "g6.txt"
+    r = run("gen-instance", "--problem", "maxcut", "--n", 6, "--seed", 1, "--out", p)
+    assert r.returncode == 0 and "wrote" in r.stdout
+    lines = p.read_text().split("\n")
+    assert lines[0] == "graph 6"
+    edges = [tuple(int(t) - 1 for t in ln.split()[1:]) for ln in lines[1:] if ln]
+    assert np.array_equal(np.array(edges), O.random_maxcut_graph(6, 1))
+
+
+def test_oracle_subcommand(tmp_path):  # cli_test.sh:27-29
+    p = tmp_path / "g10.txt"
+    run("gen-instance", "--problem", "maxcut", "--n", 10, "--seed", 3, "--out", p)
+    r = run("oracle", "--instance", p)
+    assert r.returncode == 0
+    assert int(r.stdout.split("\n")[0].split()[-1]) == O.brute_force_maxcut(10, O.random_maxcut_graph(10, 3))[0]
+
+
+def test_config_precedence_and_parsing(tmp_path):  # cli_test.sh:49-63
+    g = tmp_path / "g.txt"
+    run("gen-instance", "--problem", "maxcut", "--n", 8, "--seed", 0, "--out", g)
+    cfg = tmp_path / "cfg.ini"
+    cfg.write_text("iterations=3\nminibatch=16\neval-batch=32\nseed=7  # comment\n\n")
+    dry = {"VQMC_CLI_DRYRUN": "1"}
+    r = run("solve", "--instance", g, "--config", cfg, env=dry)
+    assert r.returncode == 0 and "iterations 3 " in r.stdout and "seed 7 " in r.stdout and "minibatch 16 " in r.stdout
+    r = run("solve", "--instance", g, "--config", cfg, "--iterations", 2, "--seed=5", env=dry)
+    assert "iterations 2 " in r.stdout and "seed 5 " in r.stdout
+    r = run("solve", "--instance", g, "--iterations", 2, "--iterations", 9, env=dry)  # TakeLast
+    assert "iterations 9 " in r.stdout
+
+
+@pytest.mark.parametrize("args", [
+    ["solve", "--no-such-flag"],                                     # unknown flag
+    ["solve"],                                                       # missing instance
+    ["solve", "--problem", "maxcut", "--n", 6, "--model", "made", "--sampler", "mcmc"],  # pairing
+    ["solve", "--problem", "maxcut", "--n", 6, "--model", "rbm", "--sampler", "auto"],
+    ["solve", "--problem", "maxcut", "--n", 6, "--iterations", "abc"],
+    ["gen-instance", "--problem", "tim", "--n", 4, "--out", "/tmp/x.txt"],  # outside the path
+    ["bogus"],
+])
+def test_usage_errors_exit_1(args):  # cli_test.sh:65-78
+    assert run(*args).returncode == 1
+
+
+def test_tim_instance_rejected(tmp_path):
+    p = tmp_path / "t.txt"
+    p.write_text("tim 3\nalpha 1 0.5\n")
+    r = run("solve", "--instance", p, "--iterations", 2)
+    assert r.returncode == 1 and "TIM" in r.stderr
+
+
+@pytest.mark.gpu
+def test_solve_outputs_and_checkpoint_roundtrip(tmp_path):  # cli_test.sh:31-47, 96-99
+    g = tmp_path / "g.txt"
+    run("gen-instance", "--problem", "maxcut", "--n", 12, "--seed", 1, "--out", g)
+    out = tmp_path / "run"
+    r = run("solve", "--instance", g, "--iterations", 5, "--minibatch", 32, "--eval-batch", 64, "--seed", 1,
+            "--out", out, "--save-model", tmp_path / "model.txt")
+    assert r.returncode == 0, r.stderr
+    rows = (out / "curve.csv").read_text().strip().split("\n")
+    assert rows[0] == "iter,energy_mean,energy_std,grad_norm,time_s" and len(rows) == 6
+    s = json.loads((out / "summary.json").read_text())
+    assert s["config"]["seed"] == 1 and s["iterations_run"] == 5 and s["best_cut"] >= s["mean_cut"]
+    assert '"seed": 1' in (out / "summary.json").read_text()
+    r = run("sample-test", "--checkpoint", tmp_path / "model.txt", "--samples", 20000)
+    assert r.returncode == 0 and "tv_distance" in r.stdout and "PASS" in r.stdout
+    r = run("sample-test", "--model", "made", "--n", 5, "--seed", 3, "--samples", 20000)
+    assert r.returncode == 0
+
+
+@pytest.mark.gpu
+def test_solve_reference_streams_reaches_near_optimum(tmp_path):
+    """MADE + AUTO + ADAM on n=20 through the CLI with the reference's streams
+    (acceptance.cpp:239-272: ADAM >= 0.95 x the brute-force optimum)."""
+    g = tmp_path / "g20.txt"
+    run("gen-instance", "--problem", "maxcut", "--n", 20, "--seed", 0, "--out", g)
+    out = tmp_path / "run"
+    r = run("solve", "--instance", g, "--iterations", 300, "--minibatch", 1024, "--seed", 0, "--reference-streams",
+            "--out", out)
+    assert r.returncode == 0, r.stderr
+    best = json.loads((out / "summary.json").read_text())["best_cut"]
+    opt, _ = O.brute_force_maxcut(20, O.random_maxcut_graph(20, 0))
+    assert best >= 0.95 * opt
