@@ -76,7 +76,7 @@ def test_tim_instance_rejected(tmp_path):
 @pytest.mark.gpu
 def test_solve_outputs_and_checkpoint_roundtrip(tmp_path):  # cli_test.sh:31-47, 96-99
     g = tmp_path / "g.txt"
-    run("gen-instance", "--problem", "maxcut", "--n", 12, "--seed", 1, "--out", g)
+    run("gen-instance", "--problem", "maxcut", "--n", 5, "--seed", 1, "--out", g)  # small: TV needs few bins
     out = tmp_path / "run"
     r = run("solve", "--instance", g, "--iterations", 5, "--minibatch", 32, "--eval-batch", 64, "--seed", 1,
             "--out", out, "--save-model", tmp_path / "model.txt")
