@@ -87,12 +87,12 @@ void Handle::ensure_batch(int B) {
   const int max_tiles = 4 * ((n + 127) / 128 + 2);  // up to 4 epilogue partials per tail tile
   dalloc(&X, (size_t)B * L.W);
   dalloc(&G1, (size_t)B * h);
-  dalloc(&Dhi, (size_t)B * np + 64);
-  dalloc(&Dlo, (size_t)B * np + 64);
+  dalloc(&Dbh, (size_t)B * np8 + 128);
+  dalloc(&Dbl, (size_t)B * np8 + 128);
   dalloc(&G1hi, (size_t)B * hp + 64);
   dalloc(&G1lo, (size_t)B * hp + 64);
-  dalloc(&wG1hi, (size_t)B * hp1 + 64);
-  dalloc(&wG1lo, (size_t)B * hp1 + 64);
+  dalloc(&wG1bh, (size_t)B * hp18 + 128);
+  dalloc(&wG1bl, (size_t)B * hp18 + 128);
   VQMC_CUDA(cudaMemset(G1hi, 0, ((size_t)B * hp + 64) * sizeof(float)));
   VQMC_CUDA(cudaMemset(G1lo, 0, ((size_t)B * hp + 64) * sizeof(float)));
   dalloc(&lp_head, (size_t)B);
@@ -103,12 +103,14 @@ void Handle::ensure_batch(int B) {
   dalloc(&w, (size_t)B);
   dalloc(&Epart, (size_t)max_splits * B * h);
   dalloc(&dz1, (size_t)B * h);
-  dalloc(&dz1hi, (size_t)B * hp + 64);
-  dalloc(&dz1lo, (size_t)B * hp + 64);
-  dalloc(&Xf, (size_t)B * hd1p + 64);
-  VQMC_CUDA(cudaMemset(dz1hi, 0, ((size_t)B * hp + 64) * sizeof(float)));
-  VQMC_CUDA(cudaMemset(dz1lo, 0, ((size_t)B * hp + 64) * sizeof(float)));
-  VQMC_CUDA(cudaMemset(Xf, 0, ((size_t)B * hd1p + 64) * sizeof(float)));
+  dalloc(&dz1bh, (size_t)B * hp8 + 128);
+  dalloc(&dz1bl, (size_t)B * hp8 + 128);
+  dalloc(&Xfb, (size_t)B * hd18 + 128);
+  VQMC_CUDA(cudaMemset(dz1bh, 0, ((size_t)B * hp8 + 128) * sizeof(__nv_bfloat16)));
+  VQMC_CUDA(cudaMemset(dz1bl, 0, ((size_t)B * hp8 + 128) * sizeof(__nv_bfloat16)));
+  VQMC_CUDA(cudaMemset(Xfb, 0, ((size_t)B * hd18 + 128) * sizeof(__nv_bfloat16)));
+  VQMC_CUDA(cudaMemset(Dbh, 0, ((size_t)B * np8 + 128) * sizeof(__nv_bfloat16)));
+  VQMC_CUDA(cudaMemset(Dbl, 0, ((size_t)B * np8 + 128) * sizeof(__nv_bfloat16)));
   cap_B = B;
 }
 
@@ -318,9 +320,10 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   H->L.init(n, h, Hd);
   if (H->L.total >= (int64_t(1) << 31)) throw std::invalid_argument("model too large for the device layout (> 2^31 live parameters)");
   H->hp = (h + 3) & ~3;
-  H->hp1 = (h + 1 + 3) & ~3;
-  H->np = (n + 3) & ~3;
-  H->hd1p = (Hd + 1 + 3) & ~3;
+  H->hp8 = (h + 7) & ~7;
+  H->hp18 = (h + 1 + 7) & ~7;
+  H->np8 = (n + 7) & ~7;
+  H->hd18 = (Hd + 1 + 7) & ~7;
   H->d = 2LL * h * n + h + n;
   H->degrees.assign(degrees, degrees + h);
   H->num_edges = num_edges;
@@ -336,6 +339,10 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   dalloc(&H->W2lo, (size_t)n * H->hp + 64);
   VQMC_CUDA(cudaMemset(H->W2hi, 0, ((size_t)n * H->hp + 64) * sizeof(float)));
   VQMC_CUDA(cudaMemset(H->W2lo, 0, ((size_t)n * H->hp + 64) * sizeof(float)));
+  dalloc(&H->W2bh, (size_t)n * H->hp8 + 128);
+  dalloc(&H->W2bl, (size_t)n * H->hp8 + 128);
+  VQMC_CUDA(cudaMemset(H->W2bh, 0, ((size_t)n * H->hp8 + 128) * sizeof(__nv_bfloat16)));
+  VQMC_CUDA(cudaMemset(H->W2bl, 0, ((size_t)n * H->hp8 + 128) * sizeof(__nv_bfloat16)));
   dalloc(&H->d_deg, (size_t)h);
   VQMC_CUDA(cudaMemcpy(H->d_deg, degrees, h * sizeof(int32_t), cudaMemcpyHostToDevice));
   {  // completion lists: hidden units by degree
@@ -408,8 +415,8 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   H->invalidate_graph();
   if (H->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy(H->nccl_comm);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2hi, H->W2lo, H->d_deg, H->d_comp_k,
-                  H->d_comp_off, H->d_edges, H->X, H->G1, H->G1hi, H->G1lo, H->wG1hi, H->wG1lo, H->Dhi, H->Dlo, H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w,
-                  H->Epart, H->dz1, H->dz1hi, H->dz1lo, H->Xf, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart, H->d_step, H->d_done, H->d_comp_pos};
+                  H->d_comp_off, H->d_edges, H->X, H->G1, H->G1hi, H->G1lo, H->wG1bh, H->wG1bl, H->Dbh, H->Dbl, H->W2bh, H->W2bl, H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w,
+                  H->Epart, H->dz1, H->dz1bh, H->dz1bl, H->Xfb, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart, H->d_step, H->d_done, H->d_comp_pos};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (H->h_scal) cudaFreeHost(H->h_scal);

@@ -4,6 +4,9 @@
 //                  epilogue: draw x = [u < p], pack bits, D = 0.5 (x - p_raw), log-prob partials
 //   dg1 (split-K)  E[b][k]  = sum_i D[b][i] W2m[i][k]              (A = D K-major, B = W2 MN-major)
 //   gW2 (+ gb2)    gW2[i][k] = sum_b D[b][i] w_b G1[b][k]          (A = D^T MN-major, B = wG1 MN-major)
+// The tail sampler uses 3xTF32 (the draw x = [u < p] needs fp32-grade logits); the backward
+// GEMMs use bf16 pairs (3 x kind::f16: 2x the tf32 rate, half the operand bytes; gradient
+// error ~2^-16 relative, inside the stated 1e-4 tolerance).
 //
 // Reference: made_forward / auto_sample / weighted_grad_log_psi, proj/src/models.cpp:51-62,
 // 175-198 and proj/src/sampler.cpp:47-55.
@@ -41,48 +44,54 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
-// K-major operand: element (mn, k) at ptr[mn * ld + k]; box {32 (K), box_mn}.
-CUtensorMap tmap_kmajor(const float* ptr, int64_t K, int64_t MN, int64_t ld, int box_mn) {
+// K-major operand: element (mn, k) at ptr[mn * ld + k]; box {128 bytes of K, box_mn}.
+CUtensorMap tmap_kmajor(const void* ptr, int64_t K, int64_t MN, int64_t ld, int box_mn, bool bf16 = false) {
   CUtensorMap m;
+  const int es = bf16 ? 2 : 4;
   const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)MN};
-  const cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
-  const cuuint32_t box[2] = {32, (cuuint32_t)box_mn};
-  const cuuint32_t es[2] = {1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
-                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  const cuuint64_t strides[1] = {(cuuint64_t)ld * es};
+  const cuuint32_t box[2] = {(cuuint32_t)(128 / es), (cuuint32_t)box_mn};
+  const cuuint32_t estr[2] = {1, 1};
+  CUresult r = encode_fn()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
+                           const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (K-major) failed: " + std::to_string((int)r));
   return m;
 }
 
-// MN-major operand: element (mn, k) at ptr[k * ld + mn]; 3D view {32, K, ceil(MN/32)},
-// box {32, 32, box_mn / 32}, 128-byte swizzle with 32-byte atoms (SWIZZLE_128B_BASE32B).  Reads up to 31 elements past MN on the last chunk: the
-// allocation must be padded and those rows/columns of the result are discarded.
-CUtensorMap tmap_mnmajor(const float* ptr, int64_t MN, int64_t K, int64_t ld, int box_mn) {
+// MN-major operand: element (mn, k) at ptr[k * ld + mn]; 3D view {A, K, ceil(MN/A)} with
+// A = 128 bytes of MN (the UMMA atom), box {A, 128 bytes of K, box_mn / A}.  tf32 uses the
+// 128-byte swizzle with 32-byte atoms (SWIZZLE_128B_BASE32B), bf16 the plain 128-byte one.
+// Reads up to one atom past MN on the last chunk: the allocation must be padded and those
+// rows/columns of the result are discarded.
+CUtensorMap tmap_mnmajor(const void* ptr, int64_t MN, int64_t K, int64_t ld, int box_mn, bool bf16 = false) {
   CUtensorMap m;
-  const cuuint64_t dims[3] = {32, (cuuint64_t)K, (cuuint64_t)((MN + 31) / 32)};
-  const cuuint64_t strides[2] = {(cuuint64_t)ld * 4, 128};
-  const cuuint32_t box[3] = {32, 32, (cuuint32_t)(box_mn / 32)};
-  const cuuint32_t es[3] = {1, 1, 1};
-  CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3, const_cast<float*>(ptr), dims, strides, box, es,
-                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+  const int es = bf16 ? 2 : 4, A = 128 / es;
+  const cuuint64_t dims[3] = {(cuuint64_t)A, (cuuint64_t)K, (cuuint64_t)((MN + A - 1) / A)};
+  const cuuint64_t strides[2] = {(cuuint64_t)ld * es, 128};
+  const cuuint32_t box[3] = {(cuuint32_t)A, (cuuint32_t)A, (cuuint32_t)(box_mn / A)};
+  const cuuint32_t estr[3] = {1, 1, 1};
+  CUresult r = encode_fn()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
+                           const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           bf16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (MN-major) failed: " + std::to_string((int)r));
   return m;
 }
 
-template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false>
+template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false, bool BF16 = false>
 static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, const CUtensorMap& al,
                         const CUtensorMap& bh, const CUtensorMap& bl, int M, int N, int K, int splits, Epi epi,
                         cudaStream_t stream) {
   using Cfg = UmmaCfg<BN>;
-  auto kern = umma_tf32x3_kernel<BN, A_MN, B_MN, Epi, A_EXACT>;
+  auto kern = umma_tf32x3_kernel<BN, A_MN, B_MN, Epi, A_EXACT, BF16>;
   static bool attr = false;
   if (!attr) {
     VQMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
     attr = true;
   }
-  const int nkb = (K + kUmmaBK - 1) / kUmmaBK;
+  const int nkb = (K + UmmaElem<BF16>::kBK - 1) / UmmaElem<BF16>::kBK;
   UmmaArgs args{M, N, K, (nkb + splits - 1) / splits, (N + BN - 1) / BN, (M + kUmmaBM - 1) / kUmmaBM, splits};
   const int ntiles = args.tiles_n * args.tiles_m * splits;
   static int sms = 0;
@@ -125,8 +134,8 @@ struct TailSampleEpi {
   const double* uni;
   RngSpec rng;
   uint32_t* X;
-  float* Dhi;
-  float* Dlo;
+  __nv_bfloat16* Dh;  // D as bf16 pairs [B][np] (operand of the bf16x3 backward GEMMs)
+  __nv_bfloat16* Dl;
   double* lp_part;
   int part;
   UmmaTile tile;
@@ -144,7 +153,7 @@ struct TailSampleEpi {
       float thr[4];  // draw x = [u < p]: u = (r + 1/2) 2^-32 < p  <=>  r + 1/2 < p 2^32
       uint32_t r[4];
       if (uni == nullptr) rng.quad(b, cb + j, r);
-      float hi4[4], lo4[4];
+      __nv_bfloat16 hi4[4], lo4[4];
 #pragma unroll
       for (int t = 0; t < 4; ++t) {
         const int c = cb + j + t;
@@ -160,19 +169,19 @@ struct TailSampleEpi {
         }
         word |= (uint32_t)x << (j + t);
         const Unit o = unit_post(q, x);
-        ptx::split_tf32(o.D, hi4[t], lo4[t]);
+        ptx::split_bf16(o.D, hi4[t], lo4[t]);
         if (valid) lsum += o.logt;
       }
       if (full) {
-        *reinterpret_cast<float4*>(Dhi + rowD + cb + j) = make_float4(hi4[0], hi4[1], hi4[2], hi4[3]);
-        *reinterpret_cast<float4*>(Dlo + rowD + cb + j) = make_float4(lo4[0], lo4[1], lo4[2], lo4[3]);
+        *reinterpret_cast<uint2*>(Dh + rowD + cb + j) = *reinterpret_cast<const uint2*>(hi4);
+        *reinterpret_cast<uint2*>(Dl + rowD + cb + j) = *reinterpret_cast<const uint2*>(lo4);
       } else {
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int c = cb + j + t;
           if (c >= col_lo && c < n) {
-            Dhi[rowD + c] = hi4[t];
-            Dlo[rowD + c] = lo4[t];
+            Dh[rowD + c] = hi4[t];
+            Dl[rowD + c] = lo4[t];
           }
         }
       }
@@ -237,27 +246,38 @@ __global__ void split_rows_kernel(int rows, int cols, int ld_in, int ld_out, con
   lo[t] = b;
 }
 
-// wG1[b][k] = w_b * G1[b][k] (k < h), w_b (k == h), 0 (k > h); split into tf32 hi/lo.
-__global__ void wg1_kernel(int B, int h, int hp1, const float* __restrict__ G1, const float* __restrict__ w,
-                           float* __restrict__ hi, float* __restrict__ lo) {
+__global__ void split_rows_bf16_kernel(int rows, int cols, int ld_in, int ld_out, const float* __restrict__ in,
+                                       __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)B * hp1) return;
-  const int b = (int)(t / hp1), k = (int)(t % hp1);
-  const float x = k < h ? w[b] * G1[(size_t)b * h + k] : (k == h ? w[b] : 0.f);
-  float a, c;
-  ptx::split_tf32(x, a, c);
-  hi[t] = a;
-  lo[t] = c;
+  if (t >= (int64_t)rows * ld_out) return;
+  const int r = (int)(t / ld_out), c = (int)(t % ld_out);
+  const float x = c < cols ? in[(size_t)r * ld_in + c] : 0.f;
+  ptx::split_bf16(x, hi[t], lo[t]);
 }
 
+// wG1[b][k] = w_b * G1[b][k] (k < h), w_b (k == h), 0 (k > h); split into bf16 hi/lo.
+__global__ void wg1_kernel(int B, int h, int ld, const float* __restrict__ G1, const float* __restrict__ w,
+                           __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)B * ld) return;
+  const int b = (int)(t / ld), k = (int)(t % ld);
+  const float x = k < h ? w[b] * G1[(size_t)b * h + k] : (k == h ? w[b] : 0.f);
+  ptx::split_bf16(x, hi[t], lo[t]);
+}
+
+// W2m -> tf32 pair (tail sampler GEMM) and bf16 pair (dg1 GEMM), after set_params.
 void launch_split_w2(Handle* H) {
   const Layout& L = H->L;
-  const int64_t total = (int64_t)L.n * H->hp;
   KScope ks(H, "split_w2");
+  int64_t total = (int64_t)L.n * H->hp;
   split_rows_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(L.n, L.h, L.h, H->hp, H->P + L.off_w2,
                                                                             H->W2hi, H->W2lo);
   VQMC_CUDA(cudaGetLastError());
-  H->launches++;
+  total = (int64_t)L.n * H->hp8;
+  split_rows_bf16_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(
+      L.n, L.h, L.h, H->hp8, H->P + L.off_w2, H->W2bh, H->W2bl);
+  VQMC_CUDA(cudaGetLastError());
+  H->launches += 2;
 }
 
 // ===========================================================================
@@ -276,7 +296,7 @@ void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng) {
   const CUtensorMap al = tmap_kmajor(H->G1lo, L.h, B, H->hp, kUmmaBM);
   const CUtensorMap bh = tmap_kmajor(H->W2hi + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
   const CUtensorMap bl = tmap_kmajor(H->W2lo + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
-  TailSampleEpi e{B, L.n, H->np, L.W, colbase, L.Hd, H->P + L.off_b2, uni, rng, H->X, H->Dhi, H->Dlo, H->lp_part, 0, {}, 0.0};
+  TailSampleEpi e{B, L.n, H->np8, L.W, colbase, L.Hd, H->P + L.off_b2, uni, rng, H->X, H->Dbh, H->Dbl, H->lp_part, 0, {}, 0.0};
   H->tail_tiles = TailSampleEpi::kParts * ((ncols + BN - 1) / BN);  // one partial per epilogue set
   launch_umma<BN, false, false>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols, L.h, 1, e, H->stream);
 }
@@ -285,57 +305,59 @@ void launch_dg1_umma(Handle* H, int B) {
   const Layout& L = H->L;
   constexpr int BN = 256;
   const int mt = (B + kUmmaBM - 1) / kUmmaBM, nt = (L.h + BN - 1) / BN;
-  const int nkb = (L.n + kUmmaBK - 1) / kUmmaBK;
+  const int nkb = (L.n + UmmaElem<true>::kBK - 1) / UmmaElem<true>::kBK;
   int splits = std::max(1, std::min(nkb, 148 / (mt * nt)));  // one tile per SM
   splits = std::min(splits, H->max_splits);
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   H->splits = splits;
-  const CUtensorMap ah = tmap_kmajor(H->Dhi, L.n, B, H->np, kUmmaBM);
-  const CUtensorMap al = tmap_kmajor(H->Dlo, L.n, B, H->np, kUmmaBM);
-  const CUtensorMap bh = tmap_mnmajor(H->W2hi, L.h, L.n, H->hp, BN);
-  const CUtensorMap bl = tmap_mnmajor(H->W2lo, L.h, L.n, H->hp, BN);
+  const CUtensorMap ah = tmap_kmajor(H->Dbh, L.n, B, H->np8, kUmmaBM, true);
+  const CUtensorMap al = tmap_kmajor(H->Dbl, L.n, B, H->np8, kUmmaBM, true);
+  const CUtensorMap bh = tmap_mnmajor(H->W2bh, L.h, L.n, H->hp8, BN, true);
+  const CUtensorMap bl = tmap_mnmajor(H->W2bl, L.h, L.n, H->hp8, BN, true);
   PartialEpi e{H->Epart, B, L.h, 0, {}};
-  launch_umma<BN, false, true>(H, "bw_dg1_umma", ah, al, bh, bl, B, L.h, L.n, splits, e, H->stream);
+  launch_umma<BN, false, true, PartialEpi, false, true>(H, "bw_dg1_umma", ah, al, bh, bl, B, L.h, L.n, splits, e,
+                                                         H->stream);
 }
 
 void launch_gw2_umma(Handle* H, int B) {  // BN = 128: 3-stage ring, 4 column tiles of h + 1
   const Layout& L = H->L;
   {
-    const int64_t total = (int64_t)B * H->hp1;
+    const int64_t total = (int64_t)B * H->hp18;
     KScope ks(H, "wg1_split");
-    wg1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp1, H->G1, H->w, H->wG1hi,
-                                                                       H->wG1lo);
+    wg1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp18, H->G1, H->w, H->wG1bh,
+                                                                       H->wG1bl);
     VQMC_CUDA(cudaGetLastError());
     H->launches++;
   }
   constexpr int BN = 128;
-  const CUtensorMap ah = tmap_mnmajor(H->Dhi, L.n, B, H->np, kUmmaBM);
-  const CUtensorMap al = tmap_mnmajor(H->Dlo, L.n, B, H->np, kUmmaBM);
-  const CUtensorMap bh = tmap_mnmajor(H->wG1hi, L.h + 1, B, H->hp1, BN);
-  const CUtensorMap bl = tmap_mnmajor(H->wG1lo, L.h + 1, B, H->hp1, BN);
+  const CUtensorMap ah = tmap_mnmajor(H->Dbh, L.n, B, H->np8, kUmmaBM, true);
+  const CUtensorMap al = tmap_mnmajor(H->Dbl, L.n, B, H->np8, kUmmaBM, true);
+  const CUtensorMap bh = tmap_mnmajor(H->wG1bh, L.h + 1, B, H->hp18, BN, true);
+  const CUtensorMap bl = tmap_mnmajor(H->wG1bl, L.h + 1, B, H->hp18, BN, true);
   Gw2Epi e{L.n, L.h, 0, {}, H->d_deg, H->G + L.off_w2, H->G + L.off_b2};
-  launch_umma<BN, true, true>(H, "bw_gw2_umma", ah, al, bh, bl, L.n, L.h + 1, B, 1, e, H->stream);
+  launch_umma<BN, true, true, Gw2Epi, false, true>(H, "bw_gw2_umma", ah, al, bh, bl, L.n, L.h + 1, B, 1, e,
+                                                    H->stream);
 }
 
 // gW1T[j][k] = sum_b X[b][j] dz1[b][k] (j < Hd) and gb1[k] (the ones column j = Hd):
 // split-K partials into gw1_part, reduced and masked by gw1_finalize_kernel.  The spins
-// are exact in tf32, so A is single (two MMA passes).
+// are exact in bf16, so A is single (two MMA passes).
 void launch_gw1_umma(Handle* H, int B, int& splits_out) {
   const Layout& L = H->L;
   constexpr int BN = 128;
   const int mt = (L.Hd + 1 + kUmmaBM - 1) / kUmmaBM, nt = (L.h + BN - 1) / BN;
-  const int nkb = (B + kUmmaBK - 1) / kUmmaBK;
+  const int nkb = (B + UmmaElem<true>::kBK - 1) / UmmaElem<true>::kBK;
   int splits = std::max(1, std::min(std::min(nkb, kGw1MaxSplits), 148 / (mt * nt)));
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   splits_out = splits;
-  const CUtensorMap a = tmap_mnmajor(H->Xf, L.Hd + 1, B, H->hd1p, kUmmaBM);
-  const CUtensorMap bh = tmap_mnmajor(H->dz1hi, L.h, B, H->hp, BN);
-  const CUtensorMap bl = tmap_mnmajor(H->dz1lo, L.h, B, H->hp, BN);
+  const CUtensorMap a = tmap_mnmajor(H->Xfb, L.Hd + 1, B, H->hd18, kUmmaBM, true);
+  const CUtensorMap bh = tmap_mnmajor(H->dz1bh, L.h, B, H->hp8, BN, true);
+  const CUtensorMap bl = tmap_mnmajor(H->dz1bl, L.h, B, H->hp8, BN, true);
   PartialEpi e{H->gw1_part, L.Hd + 1, L.h, 0, {}};
-  launch_umma<BN, true, true, PartialEpi, true>(H, "bw_gw1_umma", a, a, bh, bl, L.Hd + 1, L.h, B, splits, e,
-                                                 H->stream);
+  launch_umma<BN, true, true, PartialEpi, true, true>(H, "bw_gw1_umma", a, a, bh, bl, L.Hd + 1, L.h, B, splits, e,
+                                                       H->stream);
 }
 
 }  // namespace vqmc_b200
@@ -346,60 +368,74 @@ void launch_gw1_umma(Handle* H, int B, int& splits_out) {
 // ===========================================================================
 using namespace vqmc_b200;
 
-extern "C" int vqmc_test_umma_gemm(int M, int N, int K, int a_mn, int b_mn, int bn, int splits,
+extern "C" int vqmc_test_umma_gemm(int M, int N, int K, int a_mn, int b_mn, int bn, int splits, int bf16,
                                    const float* A, const float* Bm, float* C) {
-  float *dA = nullptr, *dB = nullptr, *dAh = nullptr, *dAl = nullptr, *dBh = nullptr, *dBl = nullptr,
-        *dC = nullptr;
+  void *dA = nullptr, *dB = nullptr, *dAh = nullptr, *dAl = nullptr, *dBh = nullptr, *dBl = nullptr;
+  float* dC = nullptr;
+  auto release = [&]() {
+    for (void* p : {dA, dB, dAh, dAl, dBh, dBl, (void*)dC})
+      if (p) cudaFree(p);
+  };
   try {
-    const int lda = a_mn ? ((M + 3) & ~3) : ((K + 3) & ~3);
+    const int q = bf16 ? 8 : 4, es = bf16 ? 2 : 4;
+    const int lda = a_mn ? ((M + q - 1) / q * q) : ((K + q - 1) / q * q);
     const int arows = a_mn ? K : M, acols = a_mn ? M : K;
-    const int ldb = b_mn ? ((N + 3) & ~3) : ((K + 3) & ~3);
+    const int ldb = b_mn ? ((N + q - 1) / q * q) : ((K + q - 1) / q * q);
     const int brows = b_mn ? K : N, bcols = b_mn ? N : K;
-    const size_t pad = 64;
+    const size_t pad = 128;
+    const size_t asz = ((size_t)arows * lda + pad) * es, bsz = ((size_t)brows * ldb + pad) * es;
     VQMC_CUDA(cudaMalloc(&dA, sizeof(float) * arows * acols));
     VQMC_CUDA(cudaMalloc(&dB, sizeof(float) * brows * bcols));
-    VQMC_CUDA(cudaMalloc(&dAh, sizeof(float) * ((size_t)arows * lda + pad)));
-    VQMC_CUDA(cudaMalloc(&dAl, sizeof(float) * ((size_t)arows * lda + pad)));
-    VQMC_CUDA(cudaMalloc(&dBh, sizeof(float) * ((size_t)brows * ldb + pad)));
-    VQMC_CUDA(cudaMalloc(&dBl, sizeof(float) * ((size_t)brows * ldb + pad)));
+    VQMC_CUDA(cudaMalloc(&dAh, asz));
+    VQMC_CUDA(cudaMalloc(&dAl, asz));
+    VQMC_CUDA(cudaMalloc(&dBh, bsz));
+    VQMC_CUDA(cudaMalloc(&dBl, bsz));
     VQMC_CUDA(cudaMalloc(&dC, sizeof(float) * (size_t)splits * M * N));
     VQMC_CUDA(cudaMemcpy(dA, A, sizeof(float) * arows * acols, cudaMemcpyHostToDevice));
     VQMC_CUDA(cudaMemcpy(dB, Bm, sizeof(float) * brows * bcols, cudaMemcpyHostToDevice));
-    VQMC_CUDA(cudaMemset(dAh, 0, sizeof(float) * ((size_t)arows * lda + pad)));
-    VQMC_CUDA(cudaMemset(dAl, 0, sizeof(float) * ((size_t)arows * lda + pad)));
-    VQMC_CUDA(cudaMemset(dBh, 0, sizeof(float) * ((size_t)brows * ldb + pad)));
-    VQMC_CUDA(cudaMemset(dBl, 0, sizeof(float) * ((size_t)brows * ldb + pad)));
-    split_rows_kernel<<<(unsigned)(((int64_t)arows * lda + 255) / 256), 256>>>(arows, acols, acols, lda, dA, dAh, dAl);
-    split_rows_kernel<<<(unsigned)(((int64_t)brows * ldb + 255) / 256), 256>>>(brows, bcols, bcols, ldb, dB, dBh, dBl);
-    VQMC_CUDA(cudaGetLastError());
-    CUtensorMap ah, al, bh, bl;
-    const int bnv = bn == 256 ? 256 : 128;
-    if (a_mn) { ah = tmap_mnmajor(dAh, M, K, lda, kUmmaBM); al = tmap_mnmajor(dAl, M, K, lda, kUmmaBM); }
-    else { ah = tmap_kmajor(dAh, K, M, lda, kUmmaBM); al = tmap_kmajor(dAl, K, M, lda, kUmmaBM); }
-    if (b_mn) { bh = tmap_mnmajor(dBh, N, K, ldb, bnv); bl = tmap_mnmajor(dBl, N, K, ldb, bnv); }
-    else { bh = tmap_kmajor(dBh, K, N, ldb, bnv); bl = tmap_kmajor(dBl, K, N, ldb, bnv); }
-    PartialEpi e{dC, M, N, 0, {}};
-#define GO(BNV, AM, BM_)                                                                       \
-  launch_umma<BNV, AM, BM_>(nullptr, "test", ah, al, bh, bl, M, N, K, splits, e, (cudaStream_t)0)
-    if (bnv == 128) {
-      if (!a_mn && !b_mn) GO(128, false, false);
-      else if (!a_mn && b_mn) GO(128, false, true);
-      else if (a_mn && !b_mn) GO(128, true, false);
-      else GO(128, true, true);
+    for (void* p : {dAh, dAl}) VQMC_CUDA(cudaMemset(p, 0, asz));
+    for (void* p : {dBh, dBl}) VQMC_CUDA(cudaMemset(p, 0, bsz));
+    const unsigned ga = (unsigned)(((int64_t)arows * lda + 255) / 256), gb = (unsigned)(((int64_t)brows * ldb + 255) / 256);
+    if (bf16) {
+      split_rows_bf16_kernel<<<ga, 256>>>(arows, acols, acols, lda, (const float*)dA, (__nv_bfloat16*)dAh,
+                                          (__nv_bfloat16*)dAl);
+      split_rows_bf16_kernel<<<gb, 256>>>(brows, bcols, bcols, ldb, (const float*)dB, (__nv_bfloat16*)dBh,
+                                          (__nv_bfloat16*)dBl);
     } else {
-      if (!a_mn && !b_mn) GO(256, false, false);
-      else if (!a_mn && b_mn) GO(256, false, true);
-      else if (a_mn && !b_mn) GO(256, true, false);
-      else GO(256, true, true);
+      split_rows_kernel<<<ga, 256>>>(arows, acols, acols, lda, (const float*)dA, (float*)dAh, (float*)dAl);
+      split_rows_kernel<<<gb, 256>>>(brows, bcols, bcols, ldb, (const float*)dB, (float*)dBh, (float*)dBl);
     }
+    VQMC_CUDA(cudaGetLastError());
+    const int bnv = bn == 256 ? 256 : 128;
+    const bool b16 = bf16 != 0;
+    CUtensorMap ah, al, bh, bl;
+    if (a_mn) { ah = tmap_mnmajor(dAh, M, K, lda, kUmmaBM, b16); al = tmap_mnmajor(dAl, M, K, lda, kUmmaBM, b16); }
+    else { ah = tmap_kmajor(dAh, K, M, lda, kUmmaBM, b16); al = tmap_kmajor(dAl, K, M, lda, kUmmaBM, b16); }
+    if (b_mn) { bh = tmap_mnmajor(dBh, N, K, ldb, bnv, b16); bl = tmap_mnmajor(dBl, N, K, ldb, bnv, b16); }
+    else { bh = tmap_kmajor(dBh, K, N, ldb, bnv, b16); bl = tmap_kmajor(dBl, K, N, ldb, bnv, b16); }
+    PartialEpi e{dC, M, N, 0, {}};
+#define GO(BNV, AM, BM_, BF)                                                                          \
+  launch_umma<BNV, AM, BM_, PartialEpi, false, BF>(nullptr, "test", ah, al, bh, bl, M, N, K, splits, e, \
+                                                  (cudaStream_t)0)
+#define GO4(BNV, BF)                             \
+  if (!a_mn && !b_mn) GO(BNV, false, false, BF); \
+  else if (!a_mn && b_mn) GO(BNV, false, true, BF); \
+  else if (a_mn && !b_mn) GO(BNV, true, false, BF); \
+  else GO(BNV, true, true, BF)
+    if (bnv == 128) {
+      if (b16) { GO4(128, true); } else { GO4(128, false); }
+    } else {
+      if (b16) { GO4(256, true); } else { GO4(256, false); }
+    }
+#undef GO4
 #undef GO
     VQMC_CUDA(cudaDeviceSynchronize());
     VQMC_CUDA(cudaMemcpy(C, dC, sizeof(float) * (size_t)splits * M * N, cudaMemcpyDeviceToHost));
   } catch (const std::exception& ex) {
     set_error(ex.what());
-    for (float* p : {dA, dB, dAh, dAl, dBh, dBl, dC}) if (p) cudaFree(p);
+    release();
     return status_of(ex);
   }
-  for (float* p : {dA, dB, dAh, dAl, dBh, dBl, dC}) if (p) cudaFree(p);
+  release();
   return VQMC_OK;
 }

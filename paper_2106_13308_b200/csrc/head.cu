@@ -82,8 +82,9 @@ __global__ void __launch_bounds__(32 * 17) head_v2_kernel(
     const float* __restrict__ W2cp, const float* __restrict__ b1, const float* __restrict__ b2,
     const int* __restrict__ comp_k, const int* __restrict__ comp_off, const double* __restrict__ uni,
     RngSpec rng, int given, int w1skip, uint32_t* __restrict__ X, float* __restrict__ G1,
-    float* __restrict__ G1hi, float* __restrict__ G1lo, int hp, float* __restrict__ Dhi, float* __restrict__ Dlo,
-    int np, float* __restrict__ Xf, int hd1p, double* __restrict__ lp_head, double* __restrict__ cond) {
+    float* __restrict__ G1hi, float* __restrict__ G1lo, int hp, __nv_bfloat16* __restrict__ Dbh,
+    __nv_bfloat16* __restrict__ Dbl, int np, __nv_bfloat16* __restrict__ Xf, int hd1p, double* __restrict__ lp_head,
+    double* __restrict__ cond) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int G = geo.G;  // power of two
   const int nw = blockDim.x / 32 - 1;  // consumer warps
@@ -232,13 +233,10 @@ __global__ void __launch_bounds__(32 * 17) head_v2_kernel(
       const bool mine = active && ib < Hd;
       if (mine) {
         const Unit u = unit_terms(zmine, xmine);
-        float hi, lo;
-        ptx::split_tf32(u.D, hi, lo);
-        Dhi[rowD + ib] = hi;
-        Dlo[rowD + ib] = lo;
+        ptx::split_bf16(u.D, Dbh[rowD + ib], Dbl[rowD + ib]);
         lp += (double)u.logt;
         if (cond) cond[rowC + ib] = u.p;
-        Xf[(size_t)b * hd1p + ib] = (float)xmine;
+        Xf[(size_t)b * hd1p + ib] = __float2bfloat16_rn((float)xmine);
       }
       const uint32_t word = __ballot_sync(kFull, mine && xmine);
       if (!given && active && lane == 0) X[(size_t)b * W + m] = word;
@@ -248,7 +246,7 @@ __global__ void __launch_bounds__(32 * 17) head_v2_kernel(
   for (int o = 16; o > 0; o >>= 1) lp += __shfl_xor_sync(kFull, lp, o);
   if (active && lane == 0) {
     lp_head[b] = lp;
-    Xf[(size_t)b * hd1p + Hd] = 1.f;  // ones column: gb1 = 1^T dz1
+    Xf[(size_t)b * hd1p + Hd] = __float2bfloat16_rn(1.f);  // ones column: gb1 = 1^T dz1
   }
 }
 
@@ -331,8 +329,8 @@ static void head_v2_launch(Handle* H, int B, const double* uni, RngSpec rng, boo
   KScope ks(H, given ? "head_given" : "head_sample");
   head_v2_kernel<KPL, FAST><<<grid, 32 * (nw + 1), geo.smem, H->stream>>>(
       B, L.n, L.h, L.Hd, L.W, geo, H->W1Tp, H->W2cp, H->P + L.off_b1, H->P + L.off_b2, H->d_comp_k,
-      H->d_comp_off, uni, rng, given ? 1 : 0, H->w1skip ? 1 : 0, H->X, H->G1, H->G1hi, H->G1lo, H->hp, H->Dhi,
-      H->Dlo, H->np, H->Xf, H->hd1p, H->lp_head, cond);
+      H->d_comp_off, uni, rng, given ? 1 : 0, H->w1skip ? 1 : 0, H->X, H->G1, H->G1hi, H->G1lo, H->hp, H->Dbh,
+      H->Dbl, H->np8, H->Xfb, H->hd18, H->lp_head, cond);
   VQMC_CUDA(cudaGetLastError());
   H->launches++;
 }

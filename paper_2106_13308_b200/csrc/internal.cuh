@@ -1,6 +1,7 @@
 // Internal declarations of the B200 VQMC library (handle layout, kernels, helpers).
 #pragma once
 
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -128,7 +129,10 @@ struct Handle {
   float* Vo = nullptr;     // Adam v
   float* W2hi = nullptr;   // [n][hp] tf32 split of W2m (GEMM operand), refreshed after updates
   float* W2lo = nullptr;
-  int hp = 0, hp1 = 0, np = 0, hd1p = 0;  // padded row strides: h, h + 1, n rounded up to 4 floats
+  __nv_bfloat16* W2bh = nullptr;  // [n][hp8] bf16 pair of W2m (dg1 operand), refreshed after updates
+  __nv_bfloat16* W2bl = nullptr;
+  int hp = 0;                     // W2 tf32 row stride (h rounded up to 4)
+  int hp8 = 0, hp18 = 0, np8 = 0, hd18 = 0;  // bf16 row strides: h, h + 1, n, Hd + 1 rounded up to 8
   int max_splits = 16;
   float* W1Tp = nullptr;   // [Hd][hp] padded head block of W1^T (head sampler staging)
   float* W2cp = nullptr;   // [h][Hdp] W2 head columns in completion order (padded)
@@ -147,12 +151,12 @@ struct Handle {
   int cap_B = 0;
   uint32_t* X = nullptr;     // [B][W]
   float* G1 = nullptr;       // [B][h]  relu(z1)
-  float* Dhi = nullptr;      // [B][np] 0.5 (x - p_raw) * clampmask, tf32 hi part
-  float* Dlo = nullptr;      // [B][np] tf32 lo part (D = hi + lo)
+  __nv_bfloat16* Dbh = nullptr;  // [B][np8] D = 0.5 (x - p_raw) * clampmask as a bf16 pair (hi)
+  __nv_bfloat16* Dbl = nullptr;  // (lo): operand of the bf16x3 backward GEMMs
   float* G1hi = nullptr;     // [B][hp] tf32 split of G1 (tail GEMM operand)
   float* G1lo = nullptr;
-  float* wG1hi = nullptr;    // [B][hp1] tf32 split of [w (.) G1 | w] (gW2 operand)
-  float* wG1lo = nullptr;
+  __nv_bfloat16* wG1bh = nullptr;  // [B][hp18] bf16 pair of [w (.) G1 | w] (gW2 operand)
+  __nv_bfloat16* wG1bl = nullptr;
   double* lp_head = nullptr; // [B]
   double* lp_part = nullptr; // [max_tiles][B]
   double* log_psi = nullptr; // [B]
@@ -161,9 +165,9 @@ struct Handle {
   float* w = nullptr;        // [B]
   float* Epart = nullptr;    // [splits][B][h]
   float* dz1 = nullptr;      // [B][h]
-  float* dz1hi = nullptr;    // [B][hp] tf32 split of dz1 (gW1 operand)
-  float* dz1lo = nullptr;
-  float* Xf = nullptr;       // [B][hd1p] spins 0/1 of the head inputs + a ones column (gW1 operand)
+  __nv_bfloat16* dz1bh = nullptr;  // [B][hp8] bf16 pair of dz1 (gW1 operand)
+  __nv_bfloat16* dz1bl = nullptr;
+  __nv_bfloat16* Xfb = nullptr;    // [B][hd18] spins 0/1 of the head inputs + a ones column (gW1 operand)
   float* gw1_part = nullptr; // [kGw1MaxSplits][Hd + 1][h]
   double* cond = nullptr;    // [B][n] optional (log_psi with conditionals)
   double* uni = nullptr;     // [n][B] injected uniforms

@@ -49,7 +49,8 @@ struct LoadW2 {  // B(n = output, k = hidden) = W2m[n][k]
 __global__ void __launch_bounds__(z2cfg::T::NT) z2_given_kernel(
     int B, int n, int np, int h, int W, int colbase, int col0, const float* __restrict__ G1,
     const float* __restrict__ W2, const float* __restrict__ b2, const uint32_t* __restrict__ X,
-    float* __restrict__ Dhi, float* __restrict__ Dlo, double* __restrict__ lp_part, double* __restrict__ cond) {
+    __nv_bfloat16* __restrict__ Dbh, __nv_bfloat16* __restrict__ Dbl, double* __restrict__ lp_part,
+    double* __restrict__ cond) {
   using namespace z2cfg;
   __shared__ __align__(16) float smem[BK * (BM + BN)];
   const int m0 = blockIdx.y * BM;
@@ -69,10 +70,7 @@ __global__ void __launch_bounds__(z2cfg::T::NT) z2_given_kernel(
         const float z = acc[r][c] + b2[col];
         const int x = (X[(size_t)b * W + (col >> 5)] >> (col & 31)) & 1;
         const Unit u = unit_terms(z, x);
-        float hi, lo;
-        ptx::split_tf32(u.D, hi, lo);
-        Dhi[(size_t)b * np + col] = hi;
-        Dlo[(size_t)b * np + col] = lo;
+        ptx::split_bf16(u.D, Dbh[(size_t)b * np + col], Dbl[(size_t)b * np + col]);
         lps += (double)u.logt;
         if (cond) cond[(size_t)b * n + col] = u.p;
       }
@@ -211,8 +209,8 @@ constexpr int QM = 64, QN = 64;  // gW1
 }  // namespace bwcfg
 
 __global__ void dz1_kernel(int B, int h, int hp, int splits, const float* __restrict__ Epart,
-                           const float* __restrict__ w, const float* __restrict__ G1,
-                           float* __restrict__ dz1, float* __restrict__ dz1hi, float* __restrict__ dz1lo) {
+                           const float* __restrict__ w, const float* __restrict__ G1, float* __restrict__ dz1,
+                           __nv_bfloat16* __restrict__ dz1bh, __nv_bfloat16* __restrict__ dz1bl) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t total = (size_t)B * h;
   if (t >= total) return;
@@ -221,10 +219,7 @@ __global__ void dz1_kernel(int B, int h, int hp, int splits, const float* __rest
   const int b = (int)(t / h), k = (int)(t % h);
   const float d = G1[t] > 0.f ? s * w[b] : 0.f;  // relu'(z1) = [z1 > 0] (models.cpp:181)
   dz1[t] = d;
-  float hi, lo;
-  ptx::split_tf32(d, hi, lo);
-  dz1hi[(size_t)b * hp + k] = hi;
-  dz1lo[(size_t)b * hp + k] = lo;
+  ptx::split_bf16(d, dz1bh[(size_t)b * hp + k], dz1bl[(size_t)b * hp + k]);
 }
 
 // gW1T = (sum of partials) (.) M1^T, gb1 = the ones row (j == Hd).
@@ -252,13 +247,15 @@ __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __re
 // reduction, fixed order; trainer.cpp:253), the tf32 split of W2 for the GEMMs and the head
 // sampler's padded / completion-ordered copies of the head blocks.
 struct AdamOut {
-  int h, hp, Hd, hpk, Hdp;
+  int h, hp, hp8, Hd, hpk, Hdp;
   int64_t off_b1, off_w2, off_b2;
   const int* comp_pos;  // completion slot of hidden unit k
   float* W1Tp;
   float* W2cp;
   float* W2hi;
   float* W2lo;
+  __nv_bfloat16* W2bh;
+  __nv_bfloat16* W2bl;
 };
 
 __device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, float p) {
@@ -272,6 +269,7 @@ __device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, fl
     ptx::split_tf32(p, hi, lo);
     o.W2hi[(size_t)i * o.hp + k] = hi;
     o.W2lo[(size_t)i * o.hp + k] = lo;
+    ptx::split_bf16(p, o.W2bh[(size_t)i * o.hp8 + k], o.W2bl[(size_t)i * o.hp8 + k]);
     if ((int)i < o.Hd) o.W2cp[(size_t)o.comp_pos[k] * o.Hdp + i] = p;
   }
 }
@@ -396,8 +394,8 @@ void launch_z2(Handle* H, int B, int col0, const double* uni, RngSpec rng, bool 
   if (tiles == 0) return;
   dim3 grid(tiles, (B + z2cfg::BM - 1) / z2cfg::BM);
   KScope ks(H, "z2_given");
-  z2_given_kernel<<<grid, z2cfg::T::NT, 0, H->stream>>>(B, L.n, H->np, L.h, L.W, colbase, col0, H->G1,
-                                                        H->P + L.off_w2, H->P + L.off_b2, H->X, H->Dhi, H->Dlo,
+  z2_given_kernel<<<grid, z2cfg::T::NT, 0, H->stream>>>(B, L.n, H->np8, L.h, L.W, colbase, col0, H->G1,
+                                                        H->P + L.off_w2, H->P + L.off_b2, H->X, H->Dbh, H->Dbl,
                                                         H->lp_part, cond);
   LAUNCH_CHECK();
   H->launches++;
@@ -438,8 +436,8 @@ void launch_backward(Handle* H, int B) {
   {
     KScope ks(H, "bw_dz1");
     const size_t total = (size_t)B * L.h;
-    dz1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp, H->splits, H->Epart, H->w,
-                                                                       H->G1, H->dz1, H->dz1hi, H->dz1lo);
+    dz1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp8, H->splits, H->Epart, H->w,
+                                                                       H->G1, H->dz1, H->dz1bh, H->dz1bl);
     LAUNCH_CHECK();
     H->launches++;
   }
@@ -489,8 +487,8 @@ void launch_set_step(Handle* H, uint64_t call, int64_t t, double lr, double b1, 
 
 void launch_adam(Handle* H, float grad_scale) {
   const Layout& L = H->L;
-  AdamOut o{L.h, H->hp, L.Hd, H->head_hpk, H->head_Hdp, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
-            H->W1Tp, H->W2cp, H->W2hi, H->W2lo};
+  AdamOut o{L.h, H->hp, H->hp8, L.Hd, H->head_hpk, H->head_Hdp, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
+            H->W1Tp, H->W2cp, H->W2hi, H->W2lo, H->W2bh, H->W2bl};
   KScope ks(H, "adam");
   adam_kernel<<<H->gpart_n, 256, 0, H->stream>>>(L.total, grad_scale, H->d_step, H->P, H->G, H->Mo, H->Vo,
                                                  H->d_gpart, H->d_done, H->d_scal, o);

@@ -14,6 +14,9 @@
 //             (LBO 16, SBO 1024; one MMA (K = 8) = 32 bytes of the row)
 //   MN-major: 32-element MN atoms of 32 K-rows (4096 B apart), 4-row groups 512 B apart,
 //             SWIZZLE_128B_BASE32B (LBO 4096, SBO 512; one MMA = 8 K-rows = 1024 bytes)
+// and for bf16 pairs (BF16 = true): K-major as above (one MMA = K 16 = 32 bytes); MN-major
+// 64-element atoms of 64 K-rows (8192 B apart), SWIZZLE_128B, 8-row groups (LBO 8192,
+// SBO 1024; one MMA = 16 K-rows = 2048 bytes).
 #pragma once
 
 #include <cuda.h>
@@ -25,10 +28,19 @@
 namespace vqmc_b200 {
 
 constexpr int kUmmaBM = 128;
-constexpr int kUmmaBK = 32;  // fp32 elements per 128-byte row
+constexpr int kUmmaBK = 32;  // fp32 elements per 128-byte row (bf16: 64)
+
+// Operand element: tf32 pairs (3 x kind::tf32, MMA K = 8) or bf16 pairs (3 x kind::f16, MMA K = 16).
+template <bool BF16>
+struct UmmaElem {
+  static constexpr int kBytes = BF16 ? 2 : 4;
+  static constexpr int kBK = 128 / kBytes;     // elements per 128-byte smem row = K per stage
+  static constexpr int kMmaK = 32 / kBytes;    // K of one MMA (32 bytes)
+  static constexpr int kMNAtom = 128 / kBytes; // MN-major atom width (elements)
+};
 
 template <int BN>
-struct UmmaCfg {
+struct UmmaCfg {  // tile bytes are the same for both element types (128-byte rows)
   static constexpr int kStages = BN >= 256 ? 2 : 3;
   static constexpr int kABytes = kUmmaBM * kUmmaBK * 4;  // 16 KB
   static constexpr int kBBytes = BN * kUmmaBK * 4;
@@ -56,8 +68,8 @@ struct UmmaTile {
 // mainloop of tile j + 1.
 //   warp 0  TMA producer     warp 1  MMA issuer     warp 2  TMEM allocator
 //   warps 4..  epilogue (kEpiSets sets of 4 warps; set s takes 32-column chunks s, s + kEpiSets, ...)
-// A_EXACT: A is exactly representable in tf32 (e.g. 0/1 spins): A_lo is neither loaded nor used.
-template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false>
+// A_EXACT: A is exactly representable (e.g. 0/1 spins): A_lo is neither loaded nor used.
+template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false, bool BF16 = false>
 __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
     umma_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                        const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
@@ -73,7 +85,8 @@ __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int nkb = (args.K + kUmmaBK - 1) / kUmmaBK;
+  using E = UmmaElem<BF16>;
+  const int nkb = (args.K + E::kBK - 1) / E::kBK;
   const int ntiles = args.tiles_n * args.tiles_m * args.splits;
   auto tile_of = [&](int t) {
     UmmaTile c;
@@ -115,18 +128,18 @@ __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
           if (use > 0) ptx::mbar_wait(&empty[s], (use - 1) & 1);
           unsigned char* st = base + (size_t)s * Cfg::kStageBytes;
           ptx::mbar_expect_tx(&full[s], A_EXACT ? Cfg::kStageBytes - Cfg::kABytes : Cfg::kStageBytes);
-          const int kc = kb * kUmmaBK;
+          const int kc = kb * E::kBK;
           if (A_MN) {
-            ptx::tma_load_3d(st, &tA_hi, &full[s], 0, kc, m0 / 32);
-            if (!A_EXACT) ptx::tma_load_3d(st + Cfg::kABytes, &tA_lo, &full[s], 0, kc, m0 / 32);
+            ptx::tma_load_3d(st, &tA_hi, &full[s], 0, kc, m0 / E::kMNAtom);
+            if (!A_EXACT) ptx::tma_load_3d(st + Cfg::kABytes, &tA_lo, &full[s], 0, kc, m0 / E::kMNAtom);
           } else {
             ptx::tma_load_2d(st, &tA_hi, &full[s], kc, m0);
             if (!A_EXACT) ptx::tma_load_2d(st + Cfg::kABytes, &tA_lo, &full[s], kc, m0);
           }
           unsigned char* sb = st + 2 * Cfg::kABytes;
           if (B_MN) {
-            ptx::tma_load_3d(sb, &tB_hi, &full[s], 0, kc, n0 / 32);
-            ptx::tma_load_3d(sb + Cfg::kBBytes, &tB_lo, &full[s], 0, kc, n0 / 32);
+            ptx::tma_load_3d(sb, &tB_hi, &full[s], 0, kc, n0 / E::kMNAtom);
+            ptx::tma_load_3d(sb + Cfg::kBBytes, &tB_lo, &full[s], 0, kc, n0 / E::kMNAtom);
           } else {
             ptx::tma_load_2d(sb, &tB_hi, &full[s], kc, n0);
             ptx::tma_load_2d(sb + Cfg::kBBytes, &tB_lo, &full[s], kc, n0);
@@ -140,10 +153,13 @@ __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = ptx::idesc_tf32(BN, A_MN, B_MN);
-      constexpr uint32_t a_lbo = A_MN ? 32 * 128 : 16, a_sbo = A_MN ? 512 : 1024, a_step = A_MN ? 1024 : 32;
-      constexpr uint32_t b_lbo = B_MN ? 32 * 128 : 16, b_sbo = B_MN ? 512 : 1024, b_step = B_MN ? 1024 : 32;
-      constexpr uint32_t a_lay = A_MN ? 1 : 2, b_lay = B_MN ? 1 : 2;
+      constexpr uint32_t idesc = BF16 ? ptx::idesc_bf16(BN, A_MN, B_MN) : ptx::idesc_tf32(BN, A_MN, B_MN);
+      // MN-major: atom stride = kBK K-rows x 128 B; K-row groups of 4 (tf32, BASE32B) or 8 (bf16)
+      constexpr uint32_t mn_lbo = E::kBK * 128, mn_sbo = BF16 ? 1024 : 512, mn_step = E::kMmaK * 128;
+      constexpr uint32_t mn_lay = BF16 ? 2 : 1;
+      constexpr uint32_t a_lbo = A_MN ? mn_lbo : 16, a_sbo = A_MN ? mn_sbo : 1024, a_step = A_MN ? mn_step : 32;
+      constexpr uint32_t b_lbo = B_MN ? mn_lbo : 16, b_sbo = B_MN ? mn_sbo : 1024, b_step = B_MN ? mn_step : 32;
+      constexpr uint32_t a_lay = A_MN ? mn_lay : 2, b_lay = B_MN ? mn_lay : 2;
       int s = 0, use = 0, j = 0;
       for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
         const UmmaTile c = tile_of(t);
@@ -160,15 +176,21 @@ __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
           const uint32_t sb = sa + 2 * Cfg::kABytes;
           const uint32_t sbl = sb + Cfg::kBBytes;
 #pragma unroll
-          for (int k = 0; k < kUmmaBK / 8; ++k) {
+          for (int k = 0; k < E::kBK / E::kMmaK; ++k) {
             const uint64_t ah = ptx::sdesc(sa + k * a_step, a_lbo, a_sbo, a_lay);
             const uint64_t al = ptx::sdesc(sal + k * a_step, a_lbo, a_sbo, a_lay);
             const uint64_t bh = ptx::sdesc(sb + k * b_step, b_lbo, b_sbo, b_lay);
             const uint64_t bl = ptx::sdesc(sbl + k * b_step, b_lbo, b_sbo, b_lay);
             const uint32_t acc0 = (kb > kb0 || k > 0) ? 1u : 0u;
-            ptx::mma_tf32(acc, ah, bh, idesc, acc0);
-            ptx::mma_tf32(acc, ah, bl, idesc, 1u);
-            if (!A_EXACT) ptx::mma_tf32(acc, al, bh, idesc, 1u);
+            if (BF16) {
+              ptx::mma_bf16(acc, ah, bh, idesc, acc0);
+              ptx::mma_bf16(acc, ah, bl, idesc, 1u);
+              if (!A_EXACT) ptx::mma_bf16(acc, al, bh, idesc, 1u);
+            } else {
+              ptx::mma_tf32(acc, ah, bh, idesc, acc0);
+              ptx::mma_tf32(acc, ah, bl, idesc, 1u);
+              if (!A_EXACT) ptx::mma_tf32(acc, al, bh, idesc, 1u);
+            }
           }
           ptx::mma_commit(&empty[s]);  // frees the stage once these MMAs have read it
           if (++s == Cfg::kStages) {
