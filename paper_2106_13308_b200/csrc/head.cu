@@ -76,12 +76,12 @@ __device__ __forceinline__ float logit_threshold(double u) {
   return (float)(log(u) - log1p(-u));
 }
 
-template <int KPL, bool FAST>
-__global__ void __launch_bounds__(32 * 17) head_v2_kernel(
+template <int KPL, bool FAST, bool GIVEN>
+__global__ void __launch_bounds__(32 * 9) head_v2_kernel(
     int B, int n, int h, int Hd, int W, HeadGeom geo, const float* __restrict__ W1Tp,
     const float* __restrict__ W2cp, const float* __restrict__ b1, const float* __restrict__ b2,
     const int* __restrict__ comp_k, const int* __restrict__ comp_off, const double* __restrict__ uni,
-    RngSpec rng, int given, int w1skip, uint32_t* __restrict__ X, float* __restrict__ G1,
+    RngSpec rng, int w1skip, uint32_t* __restrict__ X, float* __restrict__ G1,
     float* __restrict__ G1hi, float* __restrict__ G1lo, int hp, __nv_bfloat16* __restrict__ Dbh,
     __nv_bfloat16* __restrict__ Dbl, int np, __nv_bfloat16* __restrict__ Xf, int hd1p, double* __restrict__ lp_head,
     double* __restrict__ cond) {
@@ -155,7 +155,7 @@ __global__ void __launch_bounds__(32 * 17) head_v2_kernel(
     thr = 0.f;
     xin = 0;
     if (active && ib < Hd) {
-      if (given) xin = (X[(size_t)b * W + m] >> lane) & 1;
+      if (GIVEN) xin = (X[(size_t)b * W + m] >> lane) & 1;
       else thr = logit_threshold(uni ? uni[(size_t)ib * B + b] : rng(b, ib));
     }
   };
@@ -172,39 +172,46 @@ __global__ void __launch_bounds__(32 * 17) head_v2_kernel(
       const float thr = thr_next;
       const int xin = xin_next;
       if (32 * (m + 1) < Hd) word_input(m + 1, thr_next, xin_next);  // overlaps this word
-      float zmine = 0.f;
+      float zmine = 0.f, gmine = 0.f;
       int xmine = 0;
       const int lend = min(32, Hd - 32 * m);
+      constexpr int RS = 32 * KPL;  // FAST: row stride of the staged W1 / W2 rows (compile time)
+      const float* wr1 = w1s;
+      const float* wr2 = w2s;
       for (int l = 0; l < lend; ++l) {
         const int i = 32 * m + l;
         if ((i & (G - 1)) == 0) {
           mbar_wait(&full[slot], use & 1);
           w1s = ring + (size_t)slot * geo.slot_floats;
           w2s = w1s + G * geo.hp;
+          wr1 = w1s;
+          wr2 = w2s;
           cbase = s_off[i];
         }
         const float z = z2[m];
-        int x = given ? xin : (thr < z ? 1 : 0);
+        int x = GIVEN ? xin : (thr < z ? 1 : 0);
         if (lane == l) {
           zmine = z;
           xmine = x;
         }
         // rows are zero-padded to 32 * KPL floats: no bounds predicates below
         const float xf = (float)__shfl_sync(kFull, x, l);
-        {
+        if (FAST) {
+#pragma unroll
+          for (int mm = 0; mm < KPL; ++mm)
+            if (mm >= m) z1[mm] = fmaf(xf, wr1[lane + 32 * mm], z1[mm]);
+          const float gk = __shfl_sync(kFull, fmaxf(z1[m], 0.f), l);
+          if (lane == l) gmine = gk;  // hidden unit i = 32 m + l; stored at the end of the word
+#pragma unroll
+          for (int mm = 0; mm < KPL; ++mm)
+            if (mm >= m) z2[mm] = fmaf(wr2[lane + 32 * mm], gk, z2[mm]);
+          wr1 += RS;
+          wr2 += RS;
+        } else {
           const float* wr = w1s + (i & (G - 1)) * geo.hp;
 #pragma unroll
           for (int mm = 0; mm < KPL; ++mm)
-            if (FAST ? mm >= m : (!w1skip || mm >= m)) z1[mm] = fmaf(xf, wr[lane + 32 * mm], z1[mm]);
-        }
-        if (FAST) {
-          const float gk = __shfl_sync(kFull, fmaxf(z1[m], 0.f), l);
-          if (active && lane == l) store_g1(i, gk);
-          const float* wr = w2s + (i & (G - 1)) * geo.Hdp;
-#pragma unroll
-          for (int mm = 0; mm < KPL; ++mm)
-            if (mm >= m) z2[mm] = fmaf(wr[lane + 32 * mm], gk, z2[mm]);
-        } else {
+            if (!w1skip || mm >= m) z1[mm] = fmaf(xf, wr[lane + 32 * mm], z1[mm]);
           for (int c = s_off[i]; c < s_off[i + 1]; ++c) {
             const int k = s_ck[c];
             const int ks = k >> 5, kl = k & 31;
@@ -213,10 +220,10 @@ __global__ void __launch_bounds__(32 * 17) head_v2_kernel(
             for (int mm = 0; mm < KPL; ++mm) v = (mm == ks) ? z1[mm] : v;
             const float gk = __shfl_sync(kFull, fmaxf(v, 0.f), kl);
             if (active && lane == kl) store_g1(k, gk);
-            const float* wr = w2s + (c - cbase) * geo.Hdp;
+            const float* wr2g = w2s + (c - cbase) * geo.Hdp;
 #pragma unroll
             for (int mm = 0; mm < KPL; ++mm)
-              if (mm >= m && 32 * mm < geo.Hdp) z2[mm] = fmaf(wr[lane + 32 * mm], gk, z2[mm]);
+              if (mm >= m && 32 * mm < geo.Hdp) z2[mm] = fmaf(wr2g[lane + 32 * mm], gk, z2[mm]);
           }
         }
         if (((i + 1) & (G - 1)) == 0 || i == Hd - 1) {
@@ -228,6 +235,7 @@ __global__ void __launch_bounds__(32 * 17) head_v2_kernel(
           }
         }
       }
+      if (FAST && active && 32 * m + lane < Hd) store_g1(32 * m + lane, gmine);
       // word complete: per-lane output terms and bit packing (off the serial chain)
       const int ib = 32 * m + lane;
       const bool mine = active && ib < Hd;
@@ -239,7 +247,7 @@ __global__ void __launch_bounds__(32 * 17) head_v2_kernel(
         Xf[(size_t)b * hd1p + ib] = __float2bfloat16_rn((float)xmine);
       }
       const uint32_t word = __ballot_sync(kFull, mine && xmine);
-      if (!given && active && lane == 0) X[(size_t)b * W + m] = word;
+      if (!GIVEN && active && lane == 0) X[(size_t)b * W + m] = word;
     }
   }
 #pragma unroll
@@ -312,24 +320,24 @@ void launch_head_pack(Handle* H) {
   H->launches++;
 }
 
-template <int KPL, bool FAST>
-static void head_v2_launch(Handle* H, int B, const double* uni, RngSpec rng, bool given, double* cond) {
+template <int KPL, bool FAST, bool GIVEN>
+static void head_v2_launch(Handle* H, int B, const double* uni, RngSpec rng, double* cond) {
   const Layout& L = H->L;
   const HeadGeom geo = head_geometry(H);
-  static size_t attr_set[33][2] = {};
-  if (attr_set[KPL][FAST] < geo.smem) {
-    VQMC_CUDA(cudaFuncSetAttribute(head_v2_kernel<KPL, FAST>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+  static size_t attr_set = 0;
+  if (attr_set < geo.smem) {
+    VQMC_CUDA(cudaFuncSetAttribute(head_v2_kernel<KPL, FAST, GIVEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)geo.smem));
-    attr_set[KPL][FAST] = geo.smem;
+    attr_set = geo.smem;
   }
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, H->device);
-  const int nw = std::max(1, std::min(16, (B + dev_sms - 1) / dev_sms));
+  const int nw = std::max(1, std::min(8, (B + dev_sms - 1) / dev_sms));  // <= 8 sample warps + producer
   const int grid = (B + nw - 1) / nw;
-  KScope ks(H, given ? "head_given" : "head_sample");
-  head_v2_kernel<KPL, FAST><<<grid, 32 * (nw + 1), geo.smem, H->stream>>>(
+  KScope ks(H, GIVEN ? "head_given" : "head_sample");
+  head_v2_kernel<KPL, FAST, GIVEN><<<grid, 32 * (nw + 1), geo.smem, H->stream>>>(
       B, L.n, L.h, L.Hd, L.W, geo, H->W1Tp, H->W2cp, H->P + L.off_b1, H->P + L.off_b2, H->d_comp_k,
-      H->d_comp_off, uni, rng, given ? 1 : 0, H->w1skip ? 1 : 0, H->X, H->G1, H->G1hi, H->G1lo, H->hp, H->Dbh,
+      H->d_comp_off, uni, rng, H->w1skip ? 1 : 0, H->X, H->G1, H->G1hi, H->G1lo, H->hp, H->Dbh,
       H->Dbl, H->np8, H->Xfb, H->hd18, H->lp_head, cond);
   VQMC_CUDA(cudaGetLastError());
   H->launches++;
@@ -337,8 +345,13 @@ static void head_v2_launch(Handle* H, int B, const double* uni, RngSpec rng, boo
 
 template <int KPL>
 static void head_v2_dispatch(Handle* H, int B, const double* uni, RngSpec rng, bool given, double* cond) {
-  if (H->head_fast) head_v2_launch<KPL, true>(H, B, uni, rng, given, cond);
-  else head_v2_launch<KPL, false>(H, B, uni, rng, given, cond);
+  if (H->head_fast) {
+    if (given) head_v2_launch<KPL, true, true>(H, B, uni, rng, cond);
+    else head_v2_launch<KPL, true, false>(H, B, uni, rng, cond);
+  } else {
+    if (given) head_v2_launch<KPL, false, true>(H, B, uni, rng, cond);
+    else head_v2_launch<KPL, false, false>(H, B, uni, rng, cond);
+  }
 }
 
 void launch_head_v2(Handle* H, int B, const double* uni, RngSpec rng, bool given, double* cond) {

@@ -248,6 +248,7 @@ __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __re
 // sampler's padded / completion-ordered copies of the head blocks.
 struct AdamOut {
   int h, hp, hp8, Hd, hpk, Hdp;
+  bool dense_w2;  // hp == hp8 == h and off_w2 % 4 == 0: W2 splits are contiguous copies of P's W2
   int64_t off_b1, off_w2, off_b2;
   const int* comp_pos;  // completion slot of hidden unit k
   float* W1Tp;
@@ -304,10 +305,29 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, c
     reinterpret_cast<float4*>(V)[q] = v4;
     reinterpret_cast<float4*>(P)[q] = p4;
     const int64_t t = 4 * q;
-    adam_side_writes(o, t, p4.x);
-    adam_side_writes(o, t + 1, p4.y);
-    adam_side_writes(o, t + 2, p4.z);
-    adam_side_writes(o, t + 3, p4.w);
+    const int64_t u = t - o.off_w2;
+    if (o.dense_w2 && u >= 0 && u + 3 < o.off_b2 - o.off_w2 && (u / o.h) >= o.Hd) {
+      // bulk of W2 (rows >= Hd, row stride == h): vector stores of both splits
+      float4 hi, lo;
+      ptx::split_tf32(p4.x, hi.x, lo.x);
+      ptx::split_tf32(p4.y, hi.y, lo.y);
+      ptx::split_tf32(p4.z, hi.z, lo.z);
+      ptx::split_tf32(p4.w, hi.w, lo.w);
+      reinterpret_cast<float4*>(o.W2hi + u)[0] = hi;
+      reinterpret_cast<float4*>(o.W2lo + u)[0] = lo;
+      __nv_bfloat16 bh[4], bl[4];
+      ptx::split_bf16(p4.x, bh[0], bl[0]);
+      ptx::split_bf16(p4.y, bh[1], bl[1]);
+      ptx::split_bf16(p4.z, bh[2], bl[2]);
+      ptx::split_bf16(p4.w, bh[3], bl[3]);
+      *reinterpret_cast<uint2*>(o.W2bh + u) = *reinterpret_cast<const uint2*>(bh);
+      *reinterpret_cast<uint2*>(o.W2bl + u) = *reinterpret_cast<const uint2*>(bl);
+    } else {
+      adam_side_writes(o, t, p4.x);
+      adam_side_writes(o, t + 1, p4.y);
+      adam_side_writes(o, t + 2, p4.z);
+      adam_side_writes(o, t + 3, p4.w);
+    }
   }
   for (int64_t t = 4 * nq + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
     float g = G[t], m = M[t], v = V[t], p = P[t];
@@ -487,7 +507,8 @@ void launch_set_step(Handle* H, uint64_t call, int64_t t, double lr, double b1, 
 
 void launch_adam(Handle* H, float grad_scale) {
   const Layout& L = H->L;
-  AdamOut o{L.h, H->hp, H->hp8, L.Hd, H->head_hpk, H->head_Hdp, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
+  const bool dense = H->hp == L.h && H->hp8 == L.h && (L.off_w2 % 4) == 0;
+  AdamOut o{L.h, H->hp, H->hp8, L.Hd, H->head_hpk, H->head_Hdp, dense, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
             H->W1Tp, H->W2cp, H->W2hi, H->W2lo, H->W2bh, H->W2bl};
   KScope ks(H, "adam");
   adam_kernel<<<H->gpart_n, 256, 0, H->stream>>>(L.total, grad_scale, H->d_step, H->P, H->G, H->Mo, H->Vo,
