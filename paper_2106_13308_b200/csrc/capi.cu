@@ -214,7 +214,7 @@ static void sample_into(Handle* H, int B, int workers, const double* uniforms_ho
   RngSpec rng{seed, stream0, call, B / workers, device_call ? H->d_step : nullptr};
   VQMC_CUDA(cudaMemsetAsync(H->X, 0, (size_t)B * H->L.W * sizeof(uint32_t), H->stream));
   launch_head_v2(H, B, du, rng, false, nullptr);
-  launch_z2(H, B, H->L.Hd, du, rng, false, nullptr);
+  launch_z2(H, B, H->L.Hd, du, rng, false, nullptr, want_log_psi);
   if (want_log_psi) launch_finalize_logpsi(H, B, H->tail_tiles);  // the training step never reads log psi
 }
 

@@ -109,6 +109,19 @@ __device__ __forceinline__ UnitPre unit_pre(float z) {
   o.sp_neg = fmaxf(-z, 0.f) + L;
   return o;
 }
+// Same without the softplus terms (callers that do not accumulate the log-probability).
+__device__ __forceinline__ UnitPre unit_pre_nolog(float z) {
+  UnitPre o;
+  o.hi = z >= kLogitHi;
+  o.lo = z <= -kLogitHi;
+  const float e = __expf(-fabsf(z));
+  const float r = __frcp_rn(1.f + e);
+  o.praw = z >= 0.f ? r : e * r;
+  o.qraw = z >= 0.f ? e * r : r;
+  o.sp_pos = 0.f;
+  o.sp_neg = 0.f;
+  return o;
+}
 __device__ __forceinline__ Unit unit_post(const UnitPre& q, int x) {
   Unit o;
   if (q.hi || q.lo) {

@@ -136,7 +136,7 @@ struct TailSampleEpi {
   uint32_t* X;
   __nv_bfloat16* Dh;  // D as bf16 pairs [B][np] (operand of the bf16x3 backward GEMMs)
   __nv_bfloat16* Dl;
-  double* lp_part;
+  double* lp_part;  // nullptr: the caller does not need log psi (training step): skip the log terms
   int part;
   UmmaTile tile;
   double lps;
@@ -159,7 +159,7 @@ struct TailSampleEpi {
         const int c = cb + j + t;
         const bool valid = c >= col_lo && c < n;
         const float z = v[j + t] + (valid ? b2[c] : 0.f);
-        const UnitPre q = unit_pre(z);
+        const UnitPre q = lp_part ? unit_pre(z) : unit_pre_nolog(z);
         int x;
         if (uni == nullptr) {
           thr[t] = (float)(q.p() * 4294967296.0);
@@ -170,7 +170,7 @@ struct TailSampleEpi {
         word |= (uint32_t)x << (j + t);
         const Unit o = unit_post(q, x);
         ptx::split_bf16(o.D, hi4[t], lo4[t]);
-        if (valid) lsum += o.logt;
+        if (lp_part && valid) lsum += o.logt;
       }
       if (full) {
         *reinterpret_cast<uint2*>(Dh + rowD + cb + j) = *reinterpret_cast<const uint2*>(hi4);
@@ -190,7 +190,7 @@ struct TailSampleEpi {
     if (word) atomicOr(&X[(size_t)b * W + (cb >> 5)], word);
   }
   __device__ void end_row(int b, const UmmaArgs&) {
-    if (b < B) lp_part[(size_t)(kParts * tile.tn + part) * B + b] = lps;
+    if (lp_part && b < B) lp_part[(size_t)(kParts * tile.tn + part) * B + b] = lps;
   }
   static constexpr int kParts = UmmaCfg<128>::kEpiSets;
 };
@@ -283,7 +283,7 @@ void launch_split_w2(Handle* H) {
 // ===========================================================================
 // Production launchers
 // ===========================================================================
-void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng) {
+void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng, bool want_lp) {
   const Layout& L = H->L;
   const int colbase = (L.Hd / 32) * 32;
   const int ncols = L.n - colbase;
@@ -296,7 +296,8 @@ void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng) {
   const CUtensorMap al = tmap_kmajor(H->G1lo, L.h, B, H->hp, kUmmaBM);
   const CUtensorMap bh = tmap_kmajor(H->W2hi + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
   const CUtensorMap bl = tmap_kmajor(H->W2lo + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
-  TailSampleEpi e{B, L.n, H->np8, L.W, colbase, L.Hd, H->P + L.off_b2, uni, rng, H->X, H->Dbh, H->Dbl, H->lp_part, 0, {}, 0.0};
+  TailSampleEpi e{B, L.n, H->np8, L.W, colbase, L.Hd, H->P + L.off_b2, uni, rng, H->X, H->Dbh, H->Dbl,
+                  want_lp ? H->lp_part : nullptr, 0, {}, 0.0};
   H->tail_tiles = TailSampleEpi::kParts * ((ncols + BN - 1) / BN);  // one partial per epilogue set
   launch_umma<BN, false, false>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols, L.h, 1, e, H->stream);
 }

@@ -97,12 +97,12 @@ void launch_head_pack(Handle* h);
 void launch_head_v2(Handle* h, int B, const double* d_uniforms, RngSpec rng, bool given_bits,
                     double* d_cond);
 void launch_z2(Handle* h, int B, int col0, const double* d_uniforms, RngSpec rng,
-               bool given_bits, double* d_cond);
+               bool given_bits, double* d_cond, bool want_lp = true);
 void launch_finalize_logpsi(Handle* h, int B, int n_tiles);
 void launch_energy(Handle* h, int B);
 void launch_weights_from_locals(Handle* h, int B, int seg);
 void launch_backward(Handle* h, int B);
-void launch_tail_umma(Handle* h, int B, const double* d_uniforms, RngSpec rng);
+void launch_tail_umma(Handle* h, int B, const double* d_uniforms, RngSpec rng, bool want_lp);
 void launch_dg1_umma(Handle* h, int B);
 void launch_gw2_umma(Handle* h, int B);
 void launch_split_w2(Handle* h);

@@ -402,9 +402,10 @@ void launch_params_refresh(Handle* H) {
   launch_split_w2(H);
 }
 
-void launch_z2(Handle* H, int B, int col0, const double* uni, RngSpec rng, bool given, double* cond) {
+void launch_z2(Handle* H, int B, int col0, const double* uni, RngSpec rng, bool given, double* cond,
+               bool want_lp) {
   if (!given) {
-    launch_tail_umma(H, B, uni, rng);
+    launch_tail_umma(H, B, uni, rng, want_lp);
     return;
   }
   const Layout& L = H->L;
