@@ -46,7 +46,7 @@ struct UmmaCfg {  // tile bytes are the same for both element types (128-byte ro
   static constexpr int kBBytes = BN * kUmmaBK * 4;
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kTmemCols = 2 * BN <= 32 ? 32 : 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  static constexpr int kEpiSets = BN >= 128 ? 3 : 2;     // epilogue warp sets (4 warps each)
+  static constexpr int kEpiSets = BN / 32 < 4 ? BN / 32 : 4;  // epilogue warp sets (4 warps each)
   static constexpr int kThreads = 128 + 128 * kEpiSets;  // 4 control warps + epilogue warps
   static constexpr size_t kSmem = 1024 /*align slack*/ + (size_t)kStages * kStageBytes + 256;
 };
