@@ -87,14 +87,18 @@ void Handle::ensure_batch(int B) {
   const int max_tiles = 4 * ((n + 127) / 128 + 2);  // up to 4 epilogue partials per tail tile
   dalloc(&X, (size_t)B * L.W);
   dalloc(&G1, (size_t)B * h);
-  dalloc(&Dbh, (size_t)B * np8 + 128);
-  dalloc(&Dbl, (size_t)B * np8 + 128);
-  dalloc(&G1hi, (size_t)B * hp + 64);
-  dalloc(&G1lo, (size_t)B * hp + 64);
-  dalloc(&wG1bh, (size_t)B * hp18 + 128);
-  dalloc(&wG1bl, (size_t)B * hp18 + 128);
-  VQMC_CUDA(cudaMemset(G1hi, 0, ((size_t)B * hp + 64) * sizeof(float)));
-  VQMC_CUDA(cudaMemset(G1lo, 0, ((size_t)B * hp + 64) * sizeof(float)));
+  dalloc(&Dh, (size_t)B * np8 + 128);
+  dalloc(&Dl, (size_t)B * np8 + 128);
+  dalloc(&G1h, (size_t)B * hp18 + 128);
+  dalloc(&G1l, (size_t)B * hp18 + 128);
+  dalloc(&wG1h, (size_t)B * hp18 + 128);
+  dalloc(&wG1l, (size_t)B * hp18 + 128);
+  {  // [G1 | 1]: the ones column h multiplies b2 in the tail GEMM; padding stays zero
+    std::vector<__half> ones((size_t)B * hp18 + 128, __float2half(0.f));
+    for (int b = 0; b < B; ++b) ones[(size_t)b * hp18 + h] = __float2half(1.f);
+    VQMC_CUDA(cudaMemcpy(G1h, ones.data(), ones.size() * sizeof(__half), cudaMemcpyHostToDevice));
+    VQMC_CUDA(cudaMemset(G1l, 0, ones.size() * sizeof(__half)));
+  }
   dalloc(&lp_head, (size_t)B);
   dalloc(&lp_part, (size_t)max_tiles * B);
   dalloc(&log_psi, (size_t)B);
@@ -102,15 +106,14 @@ void Handle::ensure_batch(int B) {
   dalloc(&local, (size_t)B);
   dalloc(&w, (size_t)B);
   dalloc(&Epart, (size_t)max_splits * B * h);
-  dalloc(&dz1, (size_t)B * h);
   dalloc(&dz1bh, (size_t)B * hp8 + 128);
   dalloc(&dz1bl, (size_t)B * hp8 + 128);
   dalloc(&Xfb, (size_t)B * hd18 + 128);
   VQMC_CUDA(cudaMemset(dz1bh, 0, ((size_t)B * hp8 + 128) * sizeof(__nv_bfloat16)));
   VQMC_CUDA(cudaMemset(dz1bl, 0, ((size_t)B * hp8 + 128) * sizeof(__nv_bfloat16)));
   VQMC_CUDA(cudaMemset(Xfb, 0, ((size_t)B * hd18 + 128) * sizeof(__nv_bfloat16)));
-  VQMC_CUDA(cudaMemset(Dbh, 0, ((size_t)B * np8 + 128) * sizeof(__nv_bfloat16)));
-  VQMC_CUDA(cudaMemset(Dbl, 0, ((size_t)B * np8 + 128) * sizeof(__nv_bfloat16)));
+  VQMC_CUDA(cudaMemset(Dh, 0, ((size_t)B * np8 + 128) * sizeof(__half)));
+  VQMC_CUDA(cudaMemset(Dl, 0, ((size_t)B * np8 + 128) * sizeof(__half)));
   cap_B = B;
 }
 
@@ -189,6 +192,15 @@ struct DeviceGuard {
   }
 };
 
+// Sticky device flag: a logit of the fp16-pair GEMMs was not finite (operand overflow).  The
+// reference computes in fp64 and would not overflow here, so fail loudly (runtime_error, like
+// the reference's non-finite local-energy check, estimator.hpp:85-87) instead of drawing junk.
+static void check_flag(Handle* H, uint32_t v) {
+  if (!v) return;
+  VQMC_CUDA(cudaMemsetAsync(H->d_flag, 0, sizeof(uint32_t), H->stream));
+  throw NumericError("non-finite logit in the tail sampler (fp16 operand range exceeded)");
+}
+
 static void check_B(int B) {
   if (B < 1) throw std::invalid_argument("batch size must be >= 1");
 }
@@ -212,8 +224,7 @@ static void sample_into(Handle* H, int B, int workers, const double* uniforms_ho
     du = H->uni;
   }
   RngSpec rng{seed, stream0, call, B / workers, device_call ? H->d_step : nullptr};
-  VQMC_CUDA(cudaMemsetAsync(H->X, 0, (size_t)B * H->L.W * sizeof(uint32_t), H->stream));
-  launch_head_v2(H, B, du, rng, false, nullptr);
+  launch_head_v2(H, B, du, rng, false, nullptr);  // head and tail together write every word of X
   launch_z2(H, B, H->L.Hd, du, rng, false, nullptr, want_log_psi);
   if (want_log_psi) launch_finalize_logpsi(H, B, H->tail_tiles);  // the training step never reads log psi
 }
@@ -319,7 +330,6 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   VQMC_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
   H->L.init(n, h, Hd);
   if (H->L.total >= (int64_t(1) << 31)) throw std::invalid_argument("model too large for the device layout (> 2^31 live parameters)");
-  H->hp = (h + 3) & ~3;
   H->hp8 = (h + 7) & ~7;
   H->hp18 = (h + 1 + 7) & ~7;
   H->np8 = (n + 7) & ~7;
@@ -335,14 +345,10 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   VQMC_CUDA(cudaMemsetAsync(H->Mo, 0, H->L.total * sizeof(float), H->stream));
   VQMC_CUDA(cudaMemsetAsync(H->Vo, 0, H->L.total * sizeof(float), H->stream));
   dalloc(&H->gw1_part, (size_t)kGw1MaxSplits * (Hd + 1) * h);
-  dalloc(&H->W2hi, (size_t)n * H->hp + 64);
-  dalloc(&H->W2lo, (size_t)n * H->hp + 64);
-  VQMC_CUDA(cudaMemset(H->W2hi, 0, ((size_t)n * H->hp + 64) * sizeof(float)));
-  VQMC_CUDA(cudaMemset(H->W2lo, 0, ((size_t)n * H->hp + 64) * sizeof(float)));
-  dalloc(&H->W2bh, (size_t)n * H->hp8 + 128);
-  dalloc(&H->W2bl, (size_t)n * H->hp8 + 128);
-  VQMC_CUDA(cudaMemset(H->W2bh, 0, ((size_t)n * H->hp8 + 128) * sizeof(__nv_bfloat16)));
-  VQMC_CUDA(cudaMemset(H->W2bl, 0, ((size_t)n * H->hp8 + 128) * sizeof(__nv_bfloat16)));
+  dalloc(&H->W2h, (size_t)n * H->hp18 + 128);
+  dalloc(&H->W2l, (size_t)n * H->hp18 + 128);
+  VQMC_CUDA(cudaMemset(H->W2h, 0, ((size_t)n * H->hp18 + 128) * sizeof(__half)));
+  VQMC_CUDA(cudaMemset(H->W2l, 0, ((size_t)n * H->hp18 + 128) * sizeof(__half)));
   dalloc(&H->d_deg, (size_t)h);
   VQMC_CUDA(cudaMemcpy(H->d_deg, degrees, h * sizeof(int32_t), cudaMemcpyHostToDevice));
   {  // completion lists: hidden units by degree
@@ -383,6 +389,9 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   dalloc(&H->d_step, 1);
   dalloc(&H->d_done, 1);
   VQMC_CUDA(cudaMemset(H->d_done, 0, sizeof(unsigned)));
+  dalloc(&H->d_flag, 1);
+  VQMC_CUDA(cudaMemset(H->d_flag, 0, sizeof(uint32_t)));
+  dalloc(&H->d_wscale, 1);
   ensure_istat(H, 64);
   H->gpart_n = 148 * 4;
   dalloc(&H->d_gpart, (size_t)H->gpart_n);
@@ -414,9 +423,11 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   cudaStreamSynchronize(H->stream);
   H->invalidate_graph();
   if (H->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy(H->nccl_comm);
-  void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2hi, H->W2lo, H->d_deg, H->d_comp_k,
-                  H->d_comp_off, H->d_edges, H->X, H->G1, H->G1hi, H->G1lo, H->wG1bh, H->wG1bl, H->Dbh, H->Dbl, H->W2bh, H->W2bl, H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w,
-                  H->Epart, H->dz1, H->dz1bh, H->dz1bl, H->Xfb, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat, H->d_gpart, H->d_step, H->d_done, H->d_comp_pos};
+  void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2h, H->W2l, H->d_deg, H->d_comp_k,
+                  H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
+                  H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w, H->d_wscale, H->d_flag,
+                  H->Epart, H->dz1bh, H->dz1bl, H->Xfb, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat,
+                  H->d_gpart, H->d_step, H->d_done, H->d_comp_pos};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (H->h_scal) cudaFreeHost(H->h_scal);
@@ -480,7 +491,9 @@ int vqmc_gpu_sample(vqmc_gpu_t* g, int B, const double* uniforms, uint64_t seed,
   if (log_psi_out)
     VQMC_CUDA(cudaMemcpyAsync(log_psi_out, H->log_psi, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost,
                               H->stream));
+  VQMC_CUDA(cudaMemcpyAsync(H->h_scal + 8, H->d_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, H->stream));
   VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  check_flag(H, *reinterpret_cast<const uint32_t*>(H->h_scal + 8));
   API_CATCH
 }
 
@@ -532,8 +545,16 @@ int vqmc_gpu_weighted_grad(vqmc_gpu_t* g, const uint32_t* bits, const double* we
   check_B(B);
   H->ensure_batch(B);
   upload_bits(H, bits, B);
-  std::vector<float> wf(weights, weights + B);
+  // normalised weights w' = w / wscale, wscale = 2^e >= max |w| (as stats_weights_kernel does)
+  double wmax = 0.0;
+  for (int b = 0; b < B; ++b) wmax = std::max(wmax, std::fabs((double)(float)weights[b]));
+  int e = 0;
+  if (wmax > 0.0) std::frexp(wmax, &e);
+  const float sc = std::ldexp(1.f, e);
+  std::vector<float> wf(B);
+  for (int b = 0; b < B; ++b) wf[b] = std::ldexp((float)weights[b], -e);
   VQMC_CUDA(cudaMemcpyAsync(H->w, wf.data(), B * sizeof(float), cudaMemcpyHostToDevice, H->stream));
+  VQMC_CUDA(cudaMemcpyAsync(H->d_wscale, &sc, sizeof(float), cudaMemcpyHostToDevice, H->stream));
   forward_given(H, B, nullptr);
   launch_backward(H, B);
   grad_to_host(H, grad_out);
@@ -726,7 +747,9 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
     VQMC_CUDA(cudaMemcpyAsync(H->h_scal, H->d_scal, sizeof(double), cudaMemcpyDeviceToHost, H->stream));
     VQMC_CUDA(cudaMemcpyAsync(H->h_istat, H->d_istat, 3 * workers * sizeof(int64_t), cudaMemcpyDeviceToHost,
                               H->stream));
+    VQMC_CUDA(cudaMemcpyAsync(H->h_scal + 8, H->d_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, H->stream));
     VQMC_CUDA(cudaStreamSynchronize(H->stream));
+    check_flag(H, *reinterpret_cast<const uint32_t*>(H->h_scal + 8));
     int64_t cs = 0, cq = 0, best = 0;
     for (int s = 0; s < workers; ++s) {
       cs += H->h_istat[3 * s];

@@ -15,10 +15,8 @@ constexpr unsigned kFull = 0xffffffffu;
 // Philox4x32-10 (production-mode uniforms; restated in oracle/vqmc_oracle.cpp).
 // key = mix_seed(seed, stream); counter = (bit >> 2, sample, call_lo, call_hi); output word
 // j = bit & 3 gives u = (r_j + 1/2) * 2^-32 (32-bit resolution, never 0 or 1).
-__device__ __forceinline__ void philox4(uint64_t key, uint32_t quad, uint32_t sample, uint64_t call,
-                                        uint32_t (&r)[4]) {
-  uint32_t c0 = quad, c1 = sample, c2 = (uint32_t)call, c3 = (uint32_t)(call >> 32);
-  uint32_t k0 = (uint32_t)key, k1 = (uint32_t)(key >> 32);
+__device__ __forceinline__ void philox4_k(uint32_t k0, uint32_t k1, uint32_t c0, uint32_t c1, uint32_t c2,
+                                          uint32_t c3, uint32_t (&r)[4]) {
 #pragma unroll
   for (int i = 0; i < 10; ++i) {
     const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
@@ -35,6 +33,10 @@ __device__ __forceinline__ void philox4(uint64_t key, uint32_t quad, uint32_t sa
   r[1] = c1;
   r[2] = c2;
   r[3] = c3;
+}
+__device__ __forceinline__ void philox4(uint64_t key, uint32_t quad, uint32_t sample, uint64_t call,
+                                        uint32_t (&r)[4]) {
+  philox4_k((uint32_t)key, (uint32_t)(key >> 32), quad, sample, (uint32_t)call, (uint32_t)(call >> 32), r);
 }
 __device__ __forceinline__ double u32_to_uniform(uint32_t r) { return ((double)r + 0.5) * 0x1.0p-32; }
 

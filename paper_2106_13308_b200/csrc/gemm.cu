@@ -1,12 +1,16 @@
-// tcgen05 (3xTF32) GEMMs of the VQMC step and their fused epilogues:
+// tcgen05 3-pass (fp16-pair) GEMMs of the VQMC step and their fused epilogues:
 //
-//   tail sampler   Z[b][i]  = G1[b] . W2m[i] + b2[i], i >= Hd      (A = G1 K-major, B = W2 K-major)
+//   tail sampler   Z[b][i]  = [G1[b] 1] . [W2m[i] b2[i]], i >= Hd  (A = G1 K-major, B = W2 K-major)
 //                  epilogue: draw x = [u < p], pack bits, D = 0.5 (x - p_raw), log-prob partials
 //   dg1 (split-K)  E[b][k]  = sum_i D[b][i] W2m[i][k]              (A = D K-major, B = W2 MN-major)
 //   gW2 (+ gb2)    gW2[i][k] = sum_b D[b][i] w_b G1[b][k]          (A = D^T MN-major, B = wG1 MN-major)
-// The tail sampler uses 3xTF32 (the draw x = [u < p] needs fp32-grade logits); the backward
-// GEMMs use bf16 pairs (3 x kind::f16: 2x the tf32 rate, half the operand bytes; gradient
-// error ~2^-16 relative, inside the stated 1e-4 tolerance).
+//   gW1 (+ gb1)    gW1T[j][k] = sum_b X[b][j] dz1[b][k]            (A = X^T MN-major, B = dz1 MN-major)
+// Operands are stored as fp16 pairs x = hi + lo (22 significant bits) and every GEMM runs three
+// kind::f16 passes hi.hi + hi.lo + lo.hi with fp32 accumulation in TMEM: fp32-grade logits for
+// the draw x = [u < p] at 2x the tf32 rate and half its bytes.  fp16's range is kept safe by
+// construction: D in [-1/2, 1/2], REINFORCE weights normalised to |w'| <= 1 (the epilogues
+// multiply by the power-of-two wscale), and a sticky flag for non-finite logits.  gW1 keeps
+// bf16 pairs (dz1 is unbounded; the spins are exact).
 //
 // Reference: made_forward / auto_sample / weighted_grad_log_psi, proj/src/models.cpp:51-62,
 // 175-198 and proj/src/sampler.cpp:47-55.
@@ -44,54 +48,58 @@ static EncodeTiledFn encode_fn() {
   return fn;
 }
 
+static CUtensorMapDataType tmap_dtype(int ek) {
+  return ek == kElemTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
+                         : (ek == kElemBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+}
+
 // K-major operand: element (mn, k) at ptr[mn * ld + k]; box {128 bytes of K, box_mn}.
-CUtensorMap tmap_kmajor(const void* ptr, int64_t K, int64_t MN, int64_t ld, int box_mn, bool bf16 = false) {
+CUtensorMap tmap_kmajor(const void* ptr, int64_t K, int64_t MN, int64_t ld, int box_mn, int ek = kElemTF32) {
   CUtensorMap m;
-  const int es = bf16 ? 2 : 4;
+  const int es = ek ? 2 : 4;
   const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)MN};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * es};
   const cuuint32_t box[2] = {(cuuint32_t)(128 / es), (cuuint32_t)box_mn};
   const cuuint32_t estr[2] = {1, 1};
-  CUresult r = encode_fn()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2,
-                           const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
-                           CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  CUresult r = encode_fn()(&m, tmap_dtype(ek), 2, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B,
+                           CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (K-major) failed: " + std::to_string((int)r));
   return m;
 }
 
 // MN-major operand: element (mn, k) at ptr[k * ld + mn]; 3D view {A, K, ceil(MN/A)} with
 // A = 128 bytes of MN (the UMMA atom), box {A, 128 bytes of K, box_mn / A}.  tf32 uses the
-// 128-byte swizzle with 32-byte atoms (SWIZZLE_128B_BASE32B), bf16 the plain 128-byte one.
+// 128-byte swizzle with 32-byte atoms (SWIZZLE_128B_BASE32B), 16-bit types the plain 128-byte one.
 // Reads up to one atom past MN on the last chunk: the allocation must be padded and those
 // rows/columns of the result are discarded.
-CUtensorMap tmap_mnmajor(const void* ptr, int64_t MN, int64_t K, int64_t ld, int box_mn, bool bf16 = false) {
+CUtensorMap tmap_mnmajor(const void* ptr, int64_t MN, int64_t K, int64_t ld, int box_mn, int ek = kElemTF32) {
   CUtensorMap m;
-  const int es = bf16 ? 2 : 4, A = 128 / es;
+  const int es = ek ? 2 : 4, A = 128 / es;
   const cuuint64_t dims[3] = {(cuuint64_t)A, (cuuint64_t)K, (cuuint64_t)((MN + A - 1) / A)};
   const cuuint64_t strides[2] = {(cuuint64_t)ld * es, 128};
   const cuuint32_t box[3] = {(cuuint32_t)A, (cuuint32_t)A, (cuuint32_t)(box_mn / A)};
   const cuuint32_t estr[3] = {1, 1, 1};
-  CUresult r = encode_fn()(&m, bf16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 3,
-                           const_cast<void*>(ptr), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                           bf16 ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
+  CUresult r = encode_fn()(&m, tmap_dtype(ek), 3, const_cast<void*>(ptr), dims, strides, box, estr,
+                           CU_TENSOR_MAP_INTERLEAVE_NONE,
+                           ek ? CU_TENSOR_MAP_SWIZZLE_128B : CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B,
                            CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   if (r != CUDA_SUCCESS) throw CudaError("cuTensorMapEncodeTiled (MN-major) failed: " + std::to_string((int)r));
   return m;
 }
 
-template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false, bool BF16 = false>
+template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false, int EK = kElemTF32>
 static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, const CUtensorMap& al,
                         const CUtensorMap& bh, const CUtensorMap& bl, int M, int N, int K, int splits, Epi epi,
                         cudaStream_t stream) {
   using Cfg = UmmaCfg<BN>;
-  auto kern = umma_tf32x3_kernel<BN, A_MN, B_MN, Epi, A_EXACT, BF16>;
+  auto kern = umma_tf32x3_kernel<BN, A_MN, B_MN, Epi, A_EXACT, EK>;
   static bool attr = false;
   if (!attr) {
     VQMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
     attr = true;
   }
-  const int nkb = (K + UmmaElem<BF16>::kBK - 1) / UmmaElem<BF16>::kBK;
+  const int nkb = (K + UmmaElem<EK>::kBK - 1) / UmmaElem<EK>::kBK;
   UmmaArgs args{M, N, K, (nkb + splits - 1) / splits, (N + BN - 1) / BN, (M + kUmmaBM - 1) / kUmmaBM, splits};
   const int ntiles = args.tiles_n * args.tiles_m * splits;
   static int sms = 0;
@@ -125,69 +133,110 @@ struct StoreEpi {  // test: C[row][col] = acc
   __device__ void end_row(int, const UmmaArgs&) {}
 };
 
-// Tail sampler: rows = samples, columns = outputs colbase + col (col0 aligned to 32).
-// Two epilogue warp sets share a row (alternate 32-column chunks): each writes its own
-// log-prob partial (lp_part[2 * tile + part]), so the reduction stays deterministic.
+// Tail sampler: rows = samples, columns = outputs colbase + col (col0 aligned to 32, so a
+// chunk is exactly one word of the packed spins).  The logit arrives complete (b2 rides in the
+// GEMM as column h), so per output the epilogue is: sigmoid (ex2 + rcp), the draw, D and its fp16
+// pair; Philox keys are per row.  The epilogue warp sets take alternate 32-column chunks and
+// each writes its own log-prob partial (lp_part[kParts * tile + part]): deterministic.
 struct TailSampleEpi {
   int B, n, np, W, colbase, col_lo;  // outputs in [col_lo, n) are drawn here
-  const float* b2;
   const double* uni;
   RngSpec rng;
   uint32_t* X;
-  __nv_bfloat16* Dh;  // D as bf16 pairs [B][np] (operand of the bf16x3 backward GEMMs)
-  __nv_bfloat16* Dl;
+  __half* Dh;  // D as fp16 pairs [B][np] (operand of the backward GEMMs)
+  __half* Dl;
   double* lp_part;  // nullptr: the caller does not need log psi (training step): skip the log terms
+  uint32_t* flag;   // set when a logit is not finite (fp16 operand overflow)
   int part;
   UmmaTile tile;
   double lps;
-  __device__ void begin_row(int, const UmmaArgs&) { lps = 0.0; }
+  uint32_t k0, k1, c1, c2, c3;  // Philox key and counter words of this row (production draws)
+  __device__ void begin_row(int b, const UmmaArgs&) {
+    lps = 0.0;
+    if (uni == nullptr && b < B) {
+      const int s = b / rng.seg;
+      const uint64_t key = mix_seed_dev(rng.seed, rng.stream0 + (uint64_t)s);
+      const uint64_t call = rng.c();
+      k0 = (uint32_t)key;
+      k1 = (uint32_t)(key >> 32);
+      c1 = (uint32_t)(b - s * rng.seg);
+      c2 = (uint32_t)call;
+      c3 = (uint32_t)(call >> 32);
+    }
+  }
   __device__ void chunk(int b, int col0, const float (&v)[32], const UmmaArgs&) {
     if (b >= B) return;
     const int cb = colbase + col0;
-    const size_t rowD = (size_t)b * np;
     const bool full = cb >= col_lo && cb + 32 <= n;
+    constexpr float kThrLo = (float)(kProbEps * 4294967296.0), kThrHi = (float)((1.0 - kProbEps) * 4294967296.0);
+    const size_t rowD = (size_t)b * np;
     uint32_t word = 0;
     float lsum = 0.f;  // 32 log terms in fp32, then one fp64 add
+    bool bad = false;
 #pragma unroll
-    for (int j = 0; j < 32; j += 4) {
-      float thr[4];  // draw x = [u < p]: u = (r + 1/2) 2^-32 < p  <=>  r + 1/2 < p 2^32
-      uint32_t r[4];
-      if (uni == nullptr) rng.quad(b, cb + j, r);
-      __nv_bfloat16 hi4[4], lo4[4];
+    for (int jh = 0; jh < 32; jh += 16) {  // two halves of 16 outputs: 16-byte stores, fewer live registers
+      uint32_t dh[8], dl[8];
 #pragma unroll
-      for (int t = 0; t < 4; ++t) {
-        const int c = cb + j + t;
-        const bool valid = c >= col_lo && c < n;
-        const float z = v[j + t] + (valid ? b2[c] : 0.f);
-        const UnitPre q = lp_part ? unit_pre(z) : unit_pre_nolog(z);
-        int x;
-        if (uni == nullptr) {
-          thr[t] = (float)(q.p() * 4294967296.0);
-          x = (valid && (float)r[t] + 0.5f < thr[t]) ? 1 : 0;
-        } else {
-          x = (valid && uni[(size_t)c * B + b] < q.p()) ? 1 : 0;
-        }
-        word |= (uint32_t)x << (j + t);
-        const Unit o = unit_post(q, x);
-        ptx::split_bf16(o.D, hi4[t], lo4[t]);
-        if (lp_part && valid) lsum += o.logt;
-      }
-      if (full) {
-        *reinterpret_cast<uint2*>(Dh + rowD + cb + j) = *reinterpret_cast<const uint2*>(hi4);
-        *reinterpret_cast<uint2*>(Dl + rowD + cb + j) = *reinterpret_cast<const uint2*>(lo4);
-      } else {
+      for (int j = jh; j < jh + 16; j += 4) {
+        uint32_t r[4];
+        if (uni == nullptr) philox4_k(k0, k1, (uint32_t)((cb + j) >> 2), c1, c2, c3, r);
+        float d[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
           const int c = cb + j + t;
+          const bool valid = full || (c >= col_lo && c < n);
+          const float z = v[j + t];
+          const float a = fabsf(z);
+          bad |= !(a < INFINITY);
+          const float e = ptx::ex2_approx(a * -1.4426950408889634f);  // exp(-|z|)
+          const float rr = ptx::rcp_approx(1.f + e);
+          const float er = e * rr;
+          const float praw = z >= 0.f ? rr : er, qraw = z >= 0.f ? er : rr;  // sigmoid(z), 1 - sigmoid(z)
+          const bool clamp = a >= kLogitHi;                                     // models.hpp:26 clamp active
+          bool x;
+          if (uni == nullptr) {  // u = (r + 1/2) 2^-32 < clamp(p)
+            x = (float)r[t] + 0.5f < fminf(fmaxf(praw * 4294967296.f, kThrLo), kThrHi);
+          } else {
+            const double p = clamp ? (z > 0.f ? 1.0 - kProbEps : kProbEps) : (double)praw;
+            x = valid && uni[(size_t)c * B + b] < p;
+          }
+          x = x && valid;
+          word |= (uint32_t)x << (j + t);
+          d[t] = (clamp || !valid) ? 0.f : (x ? 0.5f * qraw : -0.5f * praw);  // made_dz2, models.cpp:163-171
+          if (lp_part && valid) {
+            const float L = log1pf(e);
+            const float lg = clamp ? ((z > 0.f) == x ? -1.00000005e-7f : -16.11809565095832f)
+                                   : -(x ? fmaxf(-z, 0.f) + L : fmaxf(z, 0.f) + L);
+            lsum += lg;
+          }
+        }
+        ptx::split_f16x2(d[0], d[1], dh[(j - jh) / 2], dl[(j - jh) / 2]);
+        ptx::split_f16x2(d[2], d[3], dh[(j - jh) / 2 + 1], dl[(j - jh) / 2 + 1]);
+      }
+      if (full) {
+        uint4* ph = reinterpret_cast<uint4*>(Dh + rowD + cb + jh);
+        uint4* pl = reinterpret_cast<uint4*>(Dl + rowD + cb + jh);
+        ph[0] = make_uint4(dh[0], dh[1], dh[2], dh[3]);
+        ph[1] = make_uint4(dh[4], dh[5], dh[6], dh[7]);
+        pl[0] = make_uint4(dl[0], dl[1], dl[2], dl[3]);
+        pl[1] = make_uint4(dl[4], dl[5], dl[6], dl[7]);
+      } else {
+        const __half* hh = reinterpret_cast<const __half*>(dh);
+        const __half* hl = reinterpret_cast<const __half*>(dl);
+#pragma unroll
+        for (int t = 0; t < 16; ++t) {
+          const int c = cb + jh + t;
           if (c >= col_lo && c < n) {
-            Dh[rowD + c] = hi4[t];
-            Dl[rowD + c] = lo4[t];
+            Dh[rowD + c] = hh[t];
+            Dl[rowD + c] = hl[t];
           }
         }
       }
     }
+    if (bad) atomicOr(flag, 1u);
+    if (cb < col_lo) atomicOr(&X[(size_t)b * W + (cb >> 5)], word);  // shares the word with the head
+    else X[(size_t)b * W + (cb >> 5)] = word;
     lps += (double)lsum;
-    if (word) atomicOr(&X[(size_t)b * W + (cb >> 5)], word);
   }
   __device__ void end_row(int b, const UmmaArgs&) {
     if (lp_part && b < B) lp_part[(size_t)(kParts * tile.tn + part) * B + b] = lps;
@@ -216,23 +265,25 @@ struct Gw2Epi {  // rows = outputs i, columns = hidden k (k == h: bias column ->
   int part;
   UmmaTile tile;
   const int32_t* deg;
+  const float* wscale;  // the B operand carries w' = w / wscale
   float* gW2;
   float* gb2;
   __device__ void begin_row(int, const UmmaArgs&) {}
   __device__ void chunk(int i, int col0, const float (&v)[32], const UmmaArgs&) {
     if (i >= n) return;
+    const float sc = *wscale;
 #pragma unroll
     for (int j = 0; j < 32; ++j) {
       const int k = col0 + j;
-      if (k < h) gW2[(size_t)i * h + k] = (deg[k] < i + 1) ? v[j] : 0.f;  // M2(i, k)
-      else if (k == h) gb2[i] = v[j];
+      if (k < h) gW2[(size_t)i * h + k] = (deg[k] < i + 1) ? v[j] * sc : 0.f;  // M2(i, k)
+      else if (k == h) gb2[i] = v[j] * sc;
     }
   }
   __device__ void end_row(int, const UmmaArgs&) {}
 };
 
 // ===========================================================================
-// Helper kernels: tf32 splits of operands
+// Helper kernels: 16-bit pairs of operands
 // ===========================================================================
 __global__ void split_rows_kernel(int rows, int cols, int ld_in, int ld_out, const float* __restrict__ in,
                                   float* __restrict__ hi, float* __restrict__ lo) {
@@ -255,29 +306,36 @@ __global__ void split_rows_bf16_kernel(int rows, int cols, int ld_in, int ld_out
   ptx::split_bf16(x, hi[t], lo[t]);
 }
 
-// wG1[b][k] = w_b * G1[b][k] (k < h), w_b (k == h), 0 (k > h); split into bf16 hi/lo.
+// rows x ld_out fp16 pair of [in | extra]: column `cols` holds extra[r] (if extra), zeros beyond.
+__global__ void split_rows_f16_kernel(int rows, int cols, int ld_in, int ld_out, const float* __restrict__ in,
+                                      const float* __restrict__ extra, __half* __restrict__ hi,
+                                      __half* __restrict__ lo) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)rows * ld_out) return;
+  const int r = (int)(t / ld_out), c = (int)(t % ld_out);
+  const float x = c < cols ? in[(size_t)r * ld_in + c] : ((c == cols && extra) ? extra[r] : 0.f);
+  ptx::split_f16(x, hi[t], lo[t]);
+}
+
+// wG1[b][k] = w'_b * G1[b][k] (k < h), w'_b (k == h), 0 (k > h); split into an fp16 pair.
 __global__ void wg1_kernel(int B, int h, int ld, const float* __restrict__ G1, const float* __restrict__ w,
-                           __nv_bfloat16* __restrict__ hi, __nv_bfloat16* __restrict__ lo) {
+                           __half* __restrict__ hi, __half* __restrict__ lo) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)B * ld) return;
   const int b = (int)(t / ld), k = (int)(t % ld);
   const float x = k < h ? w[b] * G1[(size_t)b * h + k] : (k == h ? w[b] : 0.f);
-  ptx::split_bf16(x, hi[t], lo[t]);
+  ptx::split_f16(x, hi[t], lo[t]);
 }
 
-// W2m -> tf32 pair (tail sampler GEMM) and bf16 pair (dg1 GEMM), after set_params.
+// [W2m | b2] -> fp16 pair (tail sampler and dg1 GEMMs), after set_params.
 void launch_split_w2(Handle* H) {
   const Layout& L = H->L;
   KScope ks(H, "split_w2");
-  int64_t total = (int64_t)L.n * H->hp;
-  split_rows_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(L.n, L.h, L.h, H->hp, H->P + L.off_w2,
-                                                                            H->W2hi, H->W2lo);
+  const int64_t total = (int64_t)L.n * H->hp18;
+  split_rows_f16_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(
+      L.n, L.h, L.h, H->hp18, H->P + L.off_w2, H->P + L.off_b2, H->W2h, H->W2l);
   VQMC_CUDA(cudaGetLastError());
-  total = (int64_t)L.n * H->hp8;
-  split_rows_bf16_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(
-      L.n, L.h, L.h, H->hp8, H->P + L.off_w2, H->W2bh, H->W2bl);
-  VQMC_CUDA(cudaGetLastError());
-  H->launches += 2;
+  H->launches++;
 }
 
 // ===========================================================================
@@ -292,33 +350,35 @@ void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng, bool wan
     return;
   }
   constexpr int BN = 128;
-  const CUtensorMap ah = tmap_kmajor(H->G1hi, L.h, B, H->hp, kUmmaBM);
-  const CUtensorMap al = tmap_kmajor(H->G1lo, L.h, B, H->hp, kUmmaBM);
-  const CUtensorMap bh = tmap_kmajor(H->W2hi + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
-  const CUtensorMap bl = tmap_kmajor(H->W2lo + (size_t)colbase * H->hp, L.h, ncols, H->hp, BN);
-  TailSampleEpi e{B, L.n, H->np8, L.W, colbase, L.Hd, H->P + L.off_b2, uni, rng, H->X, H->Dbh, H->Dbl,
-                  want_lp ? H->lp_part : nullptr, 0, {}, 0.0};
+  const int K = L.h + 1;  // [G1 | 1] . [W2 | b2]
+  const CUtensorMap ah = tmap_kmajor(H->G1h, K, B, H->hp18, kUmmaBM, kElemF16);
+  const CUtensorMap al = tmap_kmajor(H->G1l, K, B, H->hp18, kUmmaBM, kElemF16);
+  const CUtensorMap bh = tmap_kmajor(H->W2h + (size_t)colbase * H->hp18, K, ncols, H->hp18, BN, kElemF16);
+  const CUtensorMap bl = tmap_kmajor(H->W2l + (size_t)colbase * H->hp18, K, ncols, H->hp18, BN, kElemF16);
+  TailSampleEpi e{B,   L.n, H->np8, L.W, colbase, L.Hd, uni, rng, H->X, H->Dh, H->Dl, want_lp ? H->lp_part : nullptr,
+                  H->d_flag, 0, {}, 0.0, 0, 0, 0, 0, 0};
   H->tail_tiles = TailSampleEpi::kParts * ((ncols + BN - 1) / BN);  // one partial per epilogue set
-  launch_umma<BN, false, false>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols, L.h, 1, e, H->stream);
+  launch_umma<BN, false, false, TailSampleEpi, false, kElemF16>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols, K, 1,
+                                                                e, H->stream);
 }
 
 void launch_dg1_umma(Handle* H, int B) {
   const Layout& L = H->L;
   constexpr int BN = 256;
   const int mt = (B + kUmmaBM - 1) / kUmmaBM, nt = (L.h + BN - 1) / BN;
-  const int nkb = (L.n + UmmaElem<true>::kBK - 1) / UmmaElem<true>::kBK;
+  const int nkb = (L.n + UmmaElem<kElemF16>::kBK - 1) / UmmaElem<kElemF16>::kBK;
   int splits = std::max(1, std::min(nkb, 148 / (mt * nt)));  // one tile per SM
   splits = std::min(splits, H->max_splits);
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   H->splits = splits;
-  const CUtensorMap ah = tmap_kmajor(H->Dbh, L.n, B, H->np8, kUmmaBM, true);
-  const CUtensorMap al = tmap_kmajor(H->Dbl, L.n, B, H->np8, kUmmaBM, true);
-  const CUtensorMap bh = tmap_mnmajor(H->W2bh, L.h, L.n, H->hp8, BN, true);
-  const CUtensorMap bl = tmap_mnmajor(H->W2bl, L.h, L.n, H->hp8, BN, true);
+  const CUtensorMap ah = tmap_kmajor(H->Dh, L.n, B, H->np8, kUmmaBM, kElemF16);
+  const CUtensorMap al = tmap_kmajor(H->Dl, L.n, B, H->np8, kUmmaBM, kElemF16);
+  const CUtensorMap bh = tmap_mnmajor(H->W2h, L.h, L.n, H->hp18, BN, kElemF16);
+  const CUtensorMap bl = tmap_mnmajor(H->W2l, L.h, L.n, H->hp18, BN, kElemF16);
   PartialEpi e{H->Epart, B, L.h, 0, {}};
-  launch_umma<BN, false, true, PartialEpi, false, true>(H, "bw_dg1_umma", ah, al, bh, bl, B, L.h, L.n, splits, e,
-                                                         H->stream);
+  launch_umma<BN, false, true, PartialEpi, false, kElemF16>(H, "bw_dg1_umma", ah, al, bh, bl, B, L.h, L.n, splits,
+                                                            e, H->stream);
 }
 
 void launch_gw2_umma(Handle* H, int B) {  // BN = 128: 3-stage ring, 4 column tiles of h + 1
@@ -326,19 +386,19 @@ void launch_gw2_umma(Handle* H, int B) {  // BN = 128: 3-stage ring, 4 column ti
   {
     const int64_t total = (int64_t)B * H->hp18;
     KScope ks(H, "wg1_split");
-    wg1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp18, H->G1, H->w, H->wG1bh,
-                                                                       H->wG1bl);
+    wg1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp18, H->G1, H->w, H->wG1h,
+                                                                       H->wG1l);
     VQMC_CUDA(cudaGetLastError());
     H->launches++;
   }
   constexpr int BN = 128;
-  const CUtensorMap ah = tmap_mnmajor(H->Dbh, L.n, B, H->np8, kUmmaBM, true);
-  const CUtensorMap al = tmap_mnmajor(H->Dbl, L.n, B, H->np8, kUmmaBM, true);
-  const CUtensorMap bh = tmap_mnmajor(H->wG1bh, L.h + 1, B, H->hp18, BN, true);
-  const CUtensorMap bl = tmap_mnmajor(H->wG1bl, L.h + 1, B, H->hp18, BN, true);
-  Gw2Epi e{L.n, L.h, 0, {}, H->d_deg, H->G + L.off_w2, H->G + L.off_b2};
-  launch_umma<BN, true, true, Gw2Epi, false, true>(H, "bw_gw2_umma", ah, al, bh, bl, L.n, L.h + 1, B, 1, e,
-                                                    H->stream);
+  const CUtensorMap ah = tmap_mnmajor(H->Dh, L.n, B, H->np8, kUmmaBM, kElemF16);
+  const CUtensorMap al = tmap_mnmajor(H->Dl, L.n, B, H->np8, kUmmaBM, kElemF16);
+  const CUtensorMap bh = tmap_mnmajor(H->wG1h, L.h + 1, B, H->hp18, BN, kElemF16);
+  const CUtensorMap bl = tmap_mnmajor(H->wG1l, L.h + 1, B, H->hp18, BN, kElemF16);
+  Gw2Epi e{L.n, L.h, 0, {}, H->d_deg, H->d_wscale, H->G + L.off_w2, H->G + L.off_b2};
+  launch_umma<BN, true, true, Gw2Epi, false, kElemF16>(H, "bw_gw2_umma", ah, al, bh, bl, L.n, L.h + 1, B, 1, e,
+                                                       H->stream);
 }
 
 // gW1T[j][k] = sum_b X[b][j] dz1[b][k] (j < Hd) and gb1[k] (the ones column j = Hd):
@@ -353,23 +413,24 @@ void launch_gw1_umma(Handle* H, int B, int& splits_out) {
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   splits_out = splits;
-  const CUtensorMap a = tmap_mnmajor(H->Xfb, L.Hd + 1, B, H->hd18, kUmmaBM, true);
-  const CUtensorMap bh = tmap_mnmajor(H->dz1bh, L.h, B, H->hp8, BN, true);
-  const CUtensorMap bl = tmap_mnmajor(H->dz1bl, L.h, B, H->hp8, BN, true);
+  const CUtensorMap a = tmap_mnmajor(H->Xfb, L.Hd + 1, B, H->hd18, kUmmaBM, kElemBF16);
+  const CUtensorMap bh = tmap_mnmajor(H->dz1bh, L.h, B, H->hp8, BN, kElemBF16);
+  const CUtensorMap bl = tmap_mnmajor(H->dz1bl, L.h, B, H->hp8, BN, kElemBF16);
   PartialEpi e{H->gw1_part, L.Hd + 1, L.h, 0, {}};
-  launch_umma<BN, true, true, PartialEpi, true, true>(H, "bw_gw1_umma", a, a, bh, bl, L.Hd + 1, L.h, B, splits, e,
-                                                       H->stream);
+  launch_umma<BN, true, true, PartialEpi, true, kElemBF16>(H, "bw_gw1_umma", a, a, bh, bl, L.Hd + 1, L.h, B, splits,
+                                                           e, H->stream);
 }
 
 }  // namespace vqmc_b200
 
 // ===========================================================================
-// Test hook: C = A B^T through the 3xTF32 tcgen05 kernel on host fp32 arrays.
+// Test hook: C = A B^T through the 3-pass tcgen05 kernel on host fp32 arrays.
 //   a_mn = 0: A is [M][K] (K-major); 1: A is [K][M] (MN-major).  Same for B with N.
+//   ek: operand pairs 0 = tf32, 1 = bf16, 2 = fp16.
 // ===========================================================================
 using namespace vqmc_b200;
 
-extern "C" int vqmc_test_umma_gemm(int M, int N, int K, int a_mn, int b_mn, int bn, int splits, int bf16,
+extern "C" int vqmc_test_umma_gemm(int M, int N, int K, int a_mn, int b_mn, int bn, int splits, int ek,
                                    const float* A, const float* Bm, float* C) {
   void *dA = nullptr, *dB = nullptr, *dAh = nullptr, *dAl = nullptr, *dBh = nullptr, *dBl = nullptr;
   float* dC = nullptr;
@@ -378,7 +439,8 @@ extern "C" int vqmc_test_umma_gemm(int M, int N, int K, int a_mn, int b_mn, int 
       if (p) cudaFree(p);
   };
   try {
-    const int q = bf16 ? 8 : 4, es = bf16 ? 2 : 4;
+    if (ek < 0 || ek > 2) throw InvalidArgument("element kind must be 0 (tf32), 1 (bf16) or 2 (fp16)");
+    const int q = ek ? 8 : 4, es = ek ? 2 : 4;
     const int lda = a_mn ? ((M + q - 1) / q * q) : ((K + q - 1) / q * q);
     const int arows = a_mn ? K : M, acols = a_mn ? M : K;
     const int ldb = b_mn ? ((N + q - 1) / q * q) : ((K + q - 1) / q * q);
@@ -397,37 +459,46 @@ extern "C" int vqmc_test_umma_gemm(int M, int N, int K, int a_mn, int b_mn, int 
     for (void* p : {dAh, dAl}) VQMC_CUDA(cudaMemset(p, 0, asz));
     for (void* p : {dBh, dBl}) VQMC_CUDA(cudaMemset(p, 0, bsz));
     const unsigned ga = (unsigned)(((int64_t)arows * lda + 255) / 256), gb = (unsigned)(((int64_t)brows * ldb + 255) / 256);
-    if (bf16) {
+    if (ek == kElemBF16) {
       split_rows_bf16_kernel<<<ga, 256>>>(arows, acols, acols, lda, (const float*)dA, (__nv_bfloat16*)dAh,
                                           (__nv_bfloat16*)dAl);
       split_rows_bf16_kernel<<<gb, 256>>>(brows, bcols, bcols, ldb, (const float*)dB, (__nv_bfloat16*)dBh,
                                           (__nv_bfloat16*)dBl);
+    } else if (ek == kElemF16) {
+      split_rows_f16_kernel<<<ga, 256>>>(arows, acols, acols, lda, (const float*)dA, nullptr, (__half*)dAh,
+                                         (__half*)dAl);
+      split_rows_f16_kernel<<<gb, 256>>>(brows, bcols, bcols, ldb, (const float*)dB, nullptr, (__half*)dBh,
+                                         (__half*)dBl);
     } else {
       split_rows_kernel<<<ga, 256>>>(arows, acols, acols, lda, (const float*)dA, (float*)dAh, (float*)dAl);
       split_rows_kernel<<<gb, 256>>>(brows, bcols, bcols, ldb, (const float*)dB, (float*)dBh, (float*)dBl);
     }
     VQMC_CUDA(cudaGetLastError());
     const int bnv = bn == 256 ? 256 : 128;
-    const bool b16 = bf16 != 0;
     CUtensorMap ah, al, bh, bl;
-    if (a_mn) { ah = tmap_mnmajor(dAh, M, K, lda, kUmmaBM, b16); al = tmap_mnmajor(dAl, M, K, lda, kUmmaBM, b16); }
-    else { ah = tmap_kmajor(dAh, K, M, lda, kUmmaBM, b16); al = tmap_kmajor(dAl, K, M, lda, kUmmaBM, b16); }
-    if (b_mn) { bh = tmap_mnmajor(dBh, N, K, ldb, bnv, b16); bl = tmap_mnmajor(dBl, N, K, ldb, bnv, b16); }
-    else { bh = tmap_kmajor(dBh, K, N, ldb, bnv, b16); bl = tmap_kmajor(dBl, K, N, ldb, bnv, b16); }
+    if (a_mn) { ah = tmap_mnmajor(dAh, M, K, lda, kUmmaBM, ek); al = tmap_mnmajor(dAl, M, K, lda, kUmmaBM, ek); }
+    else { ah = tmap_kmajor(dAh, K, M, lda, kUmmaBM, ek); al = tmap_kmajor(dAl, K, M, lda, kUmmaBM, ek); }
+    if (b_mn) { bh = tmap_mnmajor(dBh, N, K, ldb, bnv, ek); bl = tmap_mnmajor(dBl, N, K, ldb, bnv, ek); }
+    else { bh = tmap_kmajor(dBh, K, N, ldb, bnv, ek); bl = tmap_kmajor(dBl, K, N, ldb, bnv, ek); }
     PartialEpi e{dC, M, N, 0, {}};
-#define GO(BNV, AM, BM_, BF)                                                                          \
-  launch_umma<BNV, AM, BM_, PartialEpi, false, BF>(nullptr, "test", ah, al, bh, bl, M, N, K, splits, e, \
-                                                  (cudaStream_t)0)
-#define GO4(BNV, BF)                             \
-  if (!a_mn && !b_mn) GO(BNV, false, false, BF); \
-  else if (!a_mn && b_mn) GO(BNV, false, true, BF); \
-  else if (a_mn && !b_mn) GO(BNV, true, false, BF); \
-  else GO(BNV, true, true, BF)
+#define GO(BNV, AM, BM_, EKV)                                                                          \
+  launch_umma<BNV, AM, BM_, PartialEpi, false, EKV>(nullptr, "test", ah, al, bh, bl, M, N, K, splits, e, \
+                                                   (cudaStream_t)0)
+#define GO4(BNV, EKV)                                \
+  if (!a_mn && !b_mn) GO(BNV, false, false, EKV);     \
+  else if (!a_mn && b_mn) GO(BNV, false, true, EKV);  \
+  else if (a_mn && !b_mn) GO(BNV, true, false, EKV);  \
+  else GO(BNV, true, true, EKV)
+#define GO_EK(BNV)                                       \
+  if (ek == kElemBF16) { GO4(BNV, kElemBF16); }          \
+  else if (ek == kElemF16) { GO4(BNV, kElemF16); }       \
+  else { GO4(BNV, kElemTF32); }
     if (bnv == 128) {
-      if (b16) { GO4(128, true); } else { GO4(128, false); }
+      GO_EK(128)
     } else {
-      if (b16) { GO4(256, true); } else { GO4(256, false); }
+      GO_EK(256)
     }
+#undef GO_EK
 #undef GO4
 #undef GO
     VQMC_CUDA(cudaDeviceSynchronize());

@@ -82,8 +82,8 @@ __global__ void __launch_bounds__(32 * 9) head_v2_kernel(
     const float* __restrict__ W2cp, const float* __restrict__ b1, const float* __restrict__ b2,
     const int* __restrict__ comp_k, const int* __restrict__ comp_off, const double* __restrict__ uni,
     RngSpec rng, int w1skip, uint32_t* __restrict__ X, float* __restrict__ G1,
-    float* __restrict__ G1hi, float* __restrict__ G1lo, int hp, __nv_bfloat16* __restrict__ Dbh,
-    __nv_bfloat16* __restrict__ Dbl, int np, __nv_bfloat16* __restrict__ Xf, int hd1p, double* __restrict__ lp_head,
+    __half* __restrict__ G1h, __half* __restrict__ G1l, int hp, __half* __restrict__ Dh,
+    __half* __restrict__ Dl, int np, __nv_bfloat16* __restrict__ Xf, int hd1p, double* __restrict__ lp_head,
     double* __restrict__ cond) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int G = geo.G;  // power of two
@@ -145,10 +145,7 @@ __global__ void __launch_bounds__(32 * 9) head_v2_kernel(
   const size_t rowD = (size_t)b * np, rowC = (size_t)b * n;
   auto store_g1 = [&](int k, float g) {
     G1[(size_t)b * h + k] = g;
-    float hi, lo;
-    ptx::split_tf32(g, hi, lo);
-    G1hi[(size_t)b * hp + k] = hi;
-    G1lo[(size_t)b * hp + k] = lo;
+    ptx::split_f16(g, G1h[(size_t)b * hp + k], G1l[(size_t)b * hp + k]);
   };
   auto word_input = [&](int m, float& thr, int& xin) {
     const int ib = 32 * m + lane;
@@ -241,7 +238,7 @@ __global__ void __launch_bounds__(32 * 9) head_v2_kernel(
       const bool mine = active && ib < Hd;
       if (mine) {
         const Unit u = unit_terms(zmine, xmine);
-        ptx::split_bf16(u.D, Dbh[rowD + ib], Dbl[rowD + ib]);
+        ptx::split_f16(u.D, Dh[rowD + ib], Dl[rowD + ib]);
         lp += (double)u.logt;
         if (cond) cond[rowC + ib] = u.p;
         Xf[(size_t)b * hd1p + ib] = __float2bfloat16_rn((float)xmine);
@@ -337,8 +334,8 @@ static void head_v2_launch(Handle* H, int B, const double* uni, RngSpec rng, dou
   KScope ks(H, GIVEN ? "head_given" : "head_sample");
   head_v2_kernel<KPL, FAST, GIVEN><<<grid, 32 * (nw + 1), geo.smem, H->stream>>>(
       B, L.n, L.h, L.Hd, L.W, geo, H->W1Tp, H->W2cp, H->P + L.off_b1, H->P + L.off_b2, H->d_comp_k,
-      H->d_comp_off, uni, rng, H->w1skip ? 1 : 0, H->X, H->G1, H->G1hi, H->G1lo, H->hp, H->Dbh,
-      H->Dbl, H->np8, H->Xfb, H->hd18, H->lp_head, cond);
+      H->d_comp_off, uni, rng, H->w1skip ? 1 : 0, H->X, H->G1, H->G1h, H->G1l, H->hp18, H->Dh,
+      H->Dl, H->np8, H->Xfb, H->hd18, H->lp_head, cond);
   VQMC_CUDA(cudaGetLastError());
   H->launches++;
 }

@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cuda_bf16.h>
+#include <cuda_fp16.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -127,12 +128,12 @@ struct Handle {
   float* G = nullptr;      // live grads
   float* Mo = nullptr;     // Adam m
   float* Vo = nullptr;     // Adam v
-  float* W2hi = nullptr;   // [n][hp] tf32 split of W2m (GEMM operand), refreshed after updates
-  float* W2lo = nullptr;
-  __nv_bfloat16* W2bh = nullptr;  // [n][hp8] bf16 pair of W2m (dg1 operand), refreshed after updates
-  __nv_bfloat16* W2bl = nullptr;
-  int hp = 0;                     // W2 tf32 row stride (h rounded up to 4)
-  int hp8 = 0, hp18 = 0, np8 = 0, hd18 = 0;  // bf16 row strides: h, h + 1, n, Hd + 1 rounded up to 8
+  // fp16 pair of [W2m | b2] ([n][hp18], column h = b2, zero padding): the B operand of the tail
+  // GEMM (K-major, the bias rides along as column h against G1's ones column) and of dg1
+  // (MN-major).  Refreshed by Adam after every update.
+  __half* W2h = nullptr;
+  __half* W2l = nullptr;
+  int hp8 = 0, hp18 = 0, np8 = 0, hd18 = 0;  // 16-bit row strides: h, h + 1, n, Hd + 1 rounded up to 8
   int max_splits = 16;
   float* W1Tp = nullptr;   // [Hd][hp] padded head block of W1^T (head sampler staging)
   float* W2cp = nullptr;   // [h][Hdp] W2 head columns in completion order (padded)
@@ -151,20 +152,20 @@ struct Handle {
   int cap_B = 0;
   uint32_t* X = nullptr;     // [B][W]
   float* G1 = nullptr;       // [B][h]  relu(z1)
-  __nv_bfloat16* Dbh = nullptr;  // [B][np8] D = 0.5 (x - p_raw) * clampmask as a bf16 pair (hi)
-  __nv_bfloat16* Dbl = nullptr;  // (lo): operand of the bf16x3 backward GEMMs
-  float* G1hi = nullptr;     // [B][hp] tf32 split of G1 (tail GEMM operand)
-  float* G1lo = nullptr;
-  __nv_bfloat16* wG1bh = nullptr;  // [B][hp18] bf16 pair of [w (.) G1 | w] (gW2 operand)
-  __nv_bfloat16* wG1bl = nullptr;
+  __half* Dh = nullptr;      // [B][np8] D = 0.5 (x - p_raw) * clampmask as an fp16 pair (hi)
+  __half* Dl = nullptr;      // (lo): A operand of dg1 (K-major) and gW2 (MN-major)
+  __half* G1h = nullptr;     // [B][hp18] fp16 pair of [G1 | 1] (tail GEMM A operand; column h = 1)
+  __half* G1l = nullptr;
+  __half* wG1h = nullptr;    // [B][hp18] fp16 pair of [w' (.) G1 | w'] (gW2 B operand)
+  __half* wG1l = nullptr;
   double* lp_head = nullptr; // [B]
   double* lp_part = nullptr; // [max_tiles][B]
   double* log_psi = nullptr; // [B]
   int32_t* cut = nullptr;    // [B]
   double* local = nullptr;   // [B]
-  float* w = nullptr;        // [B]
+  float* w = nullptr;        // [B] REINFORCE weights w' = w / wscale (|w'| <= 1, fp16-safe)
+  float* d_wscale = nullptr; // [1] wscale: power of two >= max |w| (the backward epilogues multiply by it)
   float* Epart = nullptr;    // [splits][B][h]
-  float* dz1 = nullptr;      // [B][h]
   __nv_bfloat16* dz1bh = nullptr;  // [B][hp8] bf16 pair of dz1 (gW1 operand)
   __nv_bfloat16* dz1bl = nullptr;
   __nv_bfloat16* Xfb = nullptr;    // [B][hd18] spins 0/1 of the head inputs + a ones column (gW1 operand)
@@ -180,7 +181,7 @@ struct Handle {
   int istat_cap = 0;
   double* d_gpart = nullptr;   // grad-norm partials
   int gpart_n = 0;
-  uint32_t* d_flag = nullptr;  // non-finite flag
+  uint32_t* d_flag = nullptr;  // sticky non-finite flag (logit overflow in the fp16-pair GEMMs)
   double* d_host_stage = nullptr;
 
   // pinned host staging for stats

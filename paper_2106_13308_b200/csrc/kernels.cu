@@ -49,7 +49,7 @@ struct LoadW2 {  // B(n = output, k = hidden) = W2m[n][k]
 __global__ void __launch_bounds__(z2cfg::T::NT) z2_given_kernel(
     int B, int n, int np, int h, int W, int colbase, int col0, const float* __restrict__ G1,
     const float* __restrict__ W2, const float* __restrict__ b2, const uint32_t* __restrict__ X,
-    __nv_bfloat16* __restrict__ Dbh, __nv_bfloat16* __restrict__ Dbl, double* __restrict__ lp_part,
+    __half* __restrict__ Dh, __half* __restrict__ Dl, double* __restrict__ lp_part,
     double* __restrict__ cond) {
   using namespace z2cfg;
   __shared__ __align__(16) float smem[BK * (BM + BN)];
@@ -70,7 +70,7 @@ __global__ void __launch_bounds__(z2cfg::T::NT) z2_given_kernel(
         const float z = acc[r][c] + b2[col];
         const int x = (X[(size_t)b * W + (col >> 5)] >> (col & 31)) & 1;
         const Unit u = unit_terms(z, x);
-        ptx::split_bf16(u.D, Dbh[(size_t)b * np + col], Dbl[(size_t)b * np + col]);
+        ptx::split_f16(u.D, Dh[(size_t)b * np + col], Dl[(size_t)b * np + col]);
         lps += (double)u.logt;
         if (cond) cond[(size_t)b * n + col] = u.p;
       }
@@ -145,55 +145,80 @@ __global__ void __launch_bounds__(256) energy_kernel(int B, int W, int64_t nE,
 }
 
 // ===========================================================================
-// In-batch statistics and REINFORCE weights, one CTA per worker segment of
-// `seg` rows (deterministic order): mean over the segment (estimator.hpp:
-// 115, the per-worker baseline), w_b = 2 (l_b - mean) / seg (estimator.hpp:
-// 116-117), and the segment's exact cut sums (pooled statistics are formed
-// from these integers on the host, trainer.cpp:246-248).
+// In-batch statistics and REINFORCE weights, one CTA looping over the worker
+// segments of `seg` rows (deterministic order): mean over the segment
+// (estimator.hpp:115, the per-worker baseline), w_b = 2 (l_b - mean) / seg
+// (estimator.hpp:116-117), and the segment's exact cut sums (pooled statistics
+// are formed from these integers on the host, trainer.cpp:246-248).  The weights
+// are stored normalised, w' = w / wscale with wscale the power of two >= max |w|
+// (exact), so the fp16-pair backward operands w' G1 cannot overflow; the
+// backward epilogues multiply by wscale.
 // ===========================================================================
-__global__ void __launch_bounds__(1024) stats_weights_kernel(int seg, const double* __restrict__ local,
+__global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, const double* __restrict__ local,
                                                              const int32_t* __restrict__ cut,
-                                                             float* __restrict__ w,
+                                                             float* __restrict__ w, float* __restrict__ wscale,
                                                              int64_t* __restrict__ istat) {
   __shared__ double sd[32];
   __shared__ long long si[32], sq[32];
   __shared__ int sm[32];
+  __shared__ float sw[32];
   __shared__ double smean;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
-  const int base = blockIdx.x * seg;
-  double s = 0.0;
-  long long cs = 0, cq = 0;
-  int cm = 0;
-  for (int b = tid; b < seg; b += blockDim.x) {
-    s += local[base + b];
-    const long long c = cut[base + b];
-    cs += c;
-    cq += c * c;
-    cm = max(cm, (int)c);
+  float wmax = 0.f;
+  for (int sgi = 0; sgi < segs; ++sgi) {
+    const int base = sgi * seg;
+    double s = 0.0;
+    long long cs = 0, cq = 0;
+    int cm = 0;
+    for (int b = tid; b < seg; b += blockDim.x) {
+      s += local[base + b];
+      const long long c = cut[base + b];
+      cs += c;
+      cq += c * c;
+      cm = max(cm, (int)c);
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      s += __shfl_xor_sync(kFull, s, o);
+      cs += __shfl_xor_sync(kFull, cs, o);
+      cq += __shfl_xor_sync(kFull, cq, o);
+      cm = max(cm, __shfl_xor_sync(kFull, cm, o));
+    }
+    if (lane == 0) { sd[warp] = s; si[warp] = cs; sq[warp] = cq; sm[warp] = cm; }
+    __syncthreads();
+    if (tid == 0) {
+      double t = 0.0;
+      long long a = 0, q = 0;
+      int mx = 0;
+      for (int i = 0; i < nw; ++i) { t += sd[i]; a += si[i]; q += sq[i]; mx = max(mx, sm[i]); }
+      smean = t / (double)seg;
+      istat[3 * sgi + 0] = a;
+      istat[3 * sgi + 1] = q;
+      istat[3 * sgi + 2] = mx;
+    }
+    __syncthreads();
+    const double mean = smean;
+    for (int b = tid; b < seg; b += blockDim.x) {
+      const float wb = (float)(2.0 * (local[base + b] - mean) / (double)seg);
+      w[base + b] = wb;
+      wmax = fmaxf(wmax, fabsf(wb));
+    }
+    __syncthreads();  // smean / partials are reused by the next segment
   }
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    s += __shfl_xor_sync(kFull, s, o);
-    cs += __shfl_xor_sync(kFull, cs, o);
-    cq += __shfl_xor_sync(kFull, cq, o);
-    cm = max(cm, __shfl_xor_sync(kFull, cm, o));
-  }
-  if (lane == 0) { sd[warp] = s; si[warp] = cs; sq[warp] = cq; sm[warp] = cm; }
+  for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(kFull, wmax, o));
+  if (lane == 0) sw[warp] = wmax;
   __syncthreads();
-  if (tid == 0) {
-    double t = 0.0;
-    long long a = 0, q = 0;
-    int mx = 0;
-    for (int i = 0; i < nw; ++i) { t += sd[i]; a += si[i]; q += sq[i]; mx = max(mx, sm[i]); }
-    smean = t / (double)seg;
-    istat[3 * blockIdx.x + 0] = a;
-    istat[3 * blockIdx.x + 1] = q;
-    istat[3 * blockIdx.x + 2] = mx;
+  float m = 0.f;
+  for (int i = 0; i < nw; ++i) m = fmaxf(m, sw[i]);
+  // wscale = 2^e >= m (1 when every weight is 0); w' = w * 2^-e exactly
+  int e = 0;
+  if (m > 0.f) {
+    frexpf(m, &e);  // m = f 2^e, f in [0.5, 1)
   }
-  __syncthreads();
-  const double mean = smean;
-  for (int b = tid; b < seg; b += blockDim.x)
-    w[base + b] = (float)(2.0 * (local[base + b] - mean) / (double)seg);
+  const float sc = ldexpf(1.f, e), inv = ldexpf(1.f, -e);
+  if (tid == 0) *wscale = sc;
+  for (int b = tid; b < segs * seg; b += blockDim.x) w[b] *= inv;
 }
 
 // ===========================================================================
@@ -208,8 +233,9 @@ constexpr int BK = 16, TM = 8, TN = 8;
 constexpr int QM = 64, QN = 64;  // gW1
 }  // namespace bwcfg
 
+// dz1' = w'_b E_bk [z1_bk > 0] as a bf16 pair (gW1 operand; gw1_finalize multiplies by wscale).
 __global__ void dz1_kernel(int B, int h, int hp, int splits, const float* __restrict__ Epart,
-                           const float* __restrict__ w, const float* __restrict__ G1, float* __restrict__ dz1,
+                           const float* __restrict__ w, const float* __restrict__ G1,
                            __nv_bfloat16* __restrict__ dz1bh, __nv_bfloat16* __restrict__ dz1bl) {
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t total = (size_t)B * h;
@@ -218,19 +244,19 @@ __global__ void dz1_kernel(int B, int h, int hp, int splits, const float* __rest
   for (int z = 0; z < splits; ++z) s += Epart[(size_t)z * total + t];
   const int b = (int)(t / h), k = (int)(t % h);
   const float d = G1[t] > 0.f ? s * w[b] : 0.f;  // relu'(z1) = [z1 > 0] (models.cpp:181)
-  dz1[t] = d;
   ptx::split_bf16(d, dz1bh[(size_t)b * hp + k], dz1bl[(size_t)b * hp + k]);
 }
 
 // gW1T = (sum of partials) (.) M1^T, gb1 = the ones row (j == Hd).
 __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __restrict__ part,
-                                    const int32_t* __restrict__ deg, float* __restrict__ gW1T,
-                                    float* __restrict__ gb1) {
+                                    const int32_t* __restrict__ deg, const float* __restrict__ wscale,
+                                    float* __restrict__ gW1T, float* __restrict__ gb1) {
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int total = (Hd + 1) * h;
   if (t >= total) return;
   float s = 0.f;
   for (int z = 0; z < splits; ++z) s += part[(size_t)z * total + t];
+  s *= *wscale;
   const int j = t / h, k = t % h;
   if (j < Hd) gW1T[(size_t)j * h + k] = (j + 1 <= deg[k]) ? s : 0.f;  // M1(k, j)
   else gb1[k] = s;
@@ -247,16 +273,14 @@ __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __re
 // reduction, fixed order; trainer.cpp:253), the tf32 split of W2 for the GEMMs and the head
 // sampler's padded / completion-ordered copies of the head blocks.
 struct AdamOut {
-  int h, hp, hp8, Hd, hpk, Hdp;
-  bool dense_w2;  // hp == hp8 == h and off_w2 % 4 == 0: W2 splits are contiguous copies of P's W2
+  int h, hp18, Hd, hpk, Hdp;
+  bool vec_w2;  // h % 4 == 0 and off_w2 % 4 == 0: a group of 4 never straddles two W2 rows
   int64_t off_b1, off_w2, off_b2;
   const int* comp_pos;  // completion slot of hidden unit k
   float* W1Tp;
   float* W2cp;
-  float* W2hi;
-  float* W2lo;
-  __nv_bfloat16* W2bh;
-  __nv_bfloat16* W2bl;
+  __half* W2h;  // fp16 pair of [W2m | b2], row stride hp18
+  __half* W2l;
 };
 
 __device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, float p) {
@@ -266,12 +290,11 @@ __device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, fl
     o.W1Tp[(size_t)j * o.hpk + k] = p;
   } else if (t >= o.off_w2 && t < o.off_b2) {  // W2[i][k]
     const unsigned u = (unsigned)(t - o.off_w2), i = u / (unsigned)o.h, k = u - i * (unsigned)o.h;
-    float hi, lo;
-    ptx::split_tf32(p, hi, lo);
-    o.W2hi[(size_t)i * o.hp + k] = hi;
-    o.W2lo[(size_t)i * o.hp + k] = lo;
-    ptx::split_bf16(p, o.W2bh[(size_t)i * o.hp8 + k], o.W2bl[(size_t)i * o.hp8 + k]);
+    ptx::split_f16(p, o.W2h[(size_t)i * o.hp18 + k], o.W2l[(size_t)i * o.hp18 + k]);
     if ((int)i < o.Hd) o.W2cp[(size_t)o.comp_pos[k] * o.Hdp + i] = p;
+  } else if (t >= o.off_b2) {  // b2[i]: column h of the W2 pair (the tail GEMM's bias column)
+    const size_t i = (size_t)(t - o.off_b2);
+    ptx::split_f16(p, o.W2h[i * o.hp18 + o.h], o.W2l[i * o.hp18 + o.h]);
   }
 }
 
@@ -306,22 +329,14 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, c
     reinterpret_cast<float4*>(P)[q] = p4;
     const int64_t t = 4 * q;
     const int64_t u = t - o.off_w2;
-    if (o.dense_w2 && u >= 0 && u + 3 < o.off_b2 - o.off_w2 && (u / o.h) >= o.Hd) {
-      // bulk of W2 (rows >= Hd, row stride == h): vector stores of both splits
-      float4 hi, lo;
-      ptx::split_tf32(p4.x, hi.x, lo.x);
-      ptx::split_tf32(p4.y, hi.y, lo.y);
-      ptx::split_tf32(p4.z, hi.z, lo.z);
-      ptx::split_tf32(p4.w, hi.w, lo.w);
-      reinterpret_cast<float4*>(o.W2hi + u)[0] = hi;
-      reinterpret_cast<float4*>(o.W2lo + u)[0] = lo;
-      __nv_bfloat16 bh[4], bl[4];
-      ptx::split_bf16(p4.x, bh[0], bl[0]);
-      ptx::split_bf16(p4.y, bh[1], bl[1]);
-      ptx::split_bf16(p4.z, bh[2], bl[2]);
-      ptx::split_bf16(p4.w, bh[3], bl[3]);
-      *reinterpret_cast<uint2*>(o.W2bh + u) = *reinterpret_cast<const uint2*>(bh);
-      *reinterpret_cast<uint2*>(o.W2bl + u) = *reinterpret_cast<const uint2*>(bl);
+    if (o.vec_w2 && u >= 0 && u < o.off_b2 - o.off_w2 && (u / o.h) >= o.Hd) {
+      // bulk of W2 (rows >= Hd): 4 consecutive entries of one row -> 8-byte stores of both halves
+      const unsigned i = (unsigned)u / (unsigned)o.h, k = (unsigned)u - i * (unsigned)o.h;
+      uint2 hi, lo;
+      ptx::split_f16x2(p4.x, p4.y, hi.x, lo.x);
+      ptx::split_f16x2(p4.z, p4.w, hi.y, lo.y);
+      *reinterpret_cast<uint2*>(o.W2h + (size_t)i * o.hp18 + k) = hi;
+      *reinterpret_cast<uint2*>(o.W2l + (size_t)i * o.hp18 + k) = lo;
     } else {
       adam_side_writes(o, t, p4.x);
       adam_side_writes(o, t + 1, p4.y);
@@ -416,7 +431,7 @@ void launch_z2(Handle* H, int B, int col0, const double* uni, RngSpec rng, bool 
   dim3 grid(tiles, (B + z2cfg::BM - 1) / z2cfg::BM);
   KScope ks(H, "z2_given");
   z2_given_kernel<<<grid, z2cfg::T::NT, 0, H->stream>>>(B, L.n, H->np8, L.h, L.W, colbase, col0, H->G1,
-                                                        H->P + L.off_w2, H->P + L.off_b2, H->X, H->Dbh, H->Dbl,
+                                                        H->P + L.off_w2, H->P + L.off_b2, H->X, H->Dh, H->Dl,
                                                         H->lp_part, cond);
   LAUNCH_CHECK();
   H->launches++;
@@ -445,7 +460,7 @@ void launch_energy(Handle* H, int B) {
 
 void launch_weights_from_locals(Handle* H, int B, int seg) {
   KScope ks(H, "stats_weights");
-  stats_weights_kernel<<<B / seg, 1024, 0, H->stream>>>(seg, H->local, H->cut, H->w, H->d_istat);
+  stats_weights_kernel<<<1, 1024, 0, H->stream>>>(B / seg, seg, H->local, H->cut, H->w, H->d_wscale, H->d_istat);
   LAUNCH_CHECK();
   H->launches++;
 }
@@ -458,7 +473,7 @@ void launch_backward(Handle* H, int B) {
     KScope ks(H, "bw_dz1");
     const size_t total = (size_t)B * L.h;
     dz1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp8, H->splits, H->Epart, H->w,
-                                                                       H->G1, H->dz1, H->dz1bh, H->dz1bl);
+                                                                       H->G1, H->dz1bh, H->dz1bl);
     LAUNCH_CHECK();
     H->launches++;
   }
@@ -469,7 +484,7 @@ void launch_backward(Handle* H, int B) {
     KScope ks(H, "bw_gw1_finalize");
     const int total = (L.Hd + 1) * L.h;
     gw1_finalize_kernel<<<(total + 255) / 256, 256, 0, H->stream>>>(L.h, L.Hd, splits, H->gw1_part, H->d_deg,
-                                                                     H->G + L.off_w1t, H->G + L.off_b1);
+                                                                     H->d_wscale, H->G + L.off_w1t, H->G + L.off_b1);
     LAUNCH_CHECK();
     H->launches++;
   }
@@ -508,9 +523,9 @@ void launch_set_step(Handle* H, uint64_t call, int64_t t, double lr, double b1, 
 
 void launch_adam(Handle* H, float grad_scale) {
   const Layout& L = H->L;
-  const bool dense = H->hp == L.h && H->hp8 == L.h && (L.off_w2 % 4) == 0;
-  AdamOut o{L.h, H->hp, H->hp8, L.Hd, H->head_hpk, H->head_Hdp, dense, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
-            H->W1Tp, H->W2cp, H->W2hi, H->W2lo, H->W2bh, H->W2bl};
+  const bool vec = (L.h % 4) == 0 && (L.off_w2 % 4) == 0;
+  AdamOut o{L.h, H->hp18, L.Hd, H->head_hpk, H->head_Hdp, vec, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
+            H->W1Tp, H->W2cp, H->W2h, H->W2l};
   KScope ks(H, "adam");
   adam_kernel<<<H->gpart_n, 256, 0, H->stream>>>(L.total, grad_scale, H->d_step, H->P, H->G, H->Mo, H->Vo,
                                                  H->d_gpart, H->d_done, H->d_scal, o);

@@ -14,7 +14,7 @@
 //             (LBO 16, SBO 1024; one MMA (K = 8) = 32 bytes of the row)
 //   MN-major: 32-element MN atoms of 32 K-rows (4096 B apart), 4-row groups 512 B apart,
 //             SWIZZLE_128B_BASE32B (LBO 4096, SBO 512; one MMA = 8 K-rows = 1024 bytes)
-// and for bf16 pairs (BF16 = true): K-major as above (one MMA = K 16 = 32 bytes); MN-major
+// and for 16-bit pairs (EK = bf16 / fp16): K-major as above (one MMA = K 16 = 32 bytes); MN-major
 // 64-element atoms of 64 K-rows (8192 B apart), SWIZZLE_128B, 8-row groups (LBO 8192,
 // SBO 1024; one MMA = 16 K-rows = 2048 bytes).
 #pragma once
@@ -30,10 +30,12 @@ namespace vqmc_b200 {
 constexpr int kUmmaBM = 128;
 constexpr int kUmmaBK = 32;  // fp32 elements per 128-byte row (bf16: 64)
 
-// Operand element: tf32 pairs (3 x kind::tf32, MMA K = 8) or bf16 pairs (3 x kind::f16, MMA K = 16).
-template <bool BF16>
+// Operand element kind EK: 0 = tf32 pairs (3 x kind::tf32, MMA K = 8); 1 = bf16 pairs, 2 = fp16
+// pairs (3 x kind::f16, MMA K = 16).
+enum : int { kElemTF32 = 0, kElemBF16 = 1, kElemF16 = 2 };
+template <int EK>
 struct UmmaElem {
-  static constexpr int kBytes = BF16 ? 2 : 4;
+  static constexpr int kBytes = EK ? 2 : 4;
   static constexpr int kBK = 128 / kBytes;     // elements per 128-byte smem row = K per stage
   static constexpr int kMmaK = 32 / kBytes;    // K of one MMA (32 bytes)
   static constexpr int kMNAtom = 128 / kBytes; // MN-major atom width (elements)
@@ -69,7 +71,7 @@ struct UmmaTile {
 //   warp 0  TMA producer     warp 1  MMA issuer     warp 2  TMEM allocator
 //   warps 4..  epilogue (kEpiSets sets of 4 warps; set s takes 32-column chunks s, s + kEpiSets, ...)
 // A_EXACT: A is exactly representable (e.g. 0/1 spins): A_lo is neither loaded nor used.
-template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false, bool BF16 = false>
+template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false, int EK = kElemTF32>
 __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
     umma_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                        const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
@@ -85,7 +87,7 @@ __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tempty + 2);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  using E = UmmaElem<BF16>;
+  using E = UmmaElem<EK>;
   const int nkb = (args.K + E::kBK - 1) / E::kBK;
   const int ntiles = args.tiles_n * args.tiles_m * args.splits;
   auto tile_of = [&](int t) {
@@ -153,10 +155,10 @@ __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---------------- MMA issuer ----------------
-      constexpr uint32_t idesc = BF16 ? ptx::idesc_bf16(BN, A_MN, B_MN) : ptx::idesc_tf32(BN, A_MN, B_MN);
+      constexpr uint32_t idesc = EK ? ptx::idesc_f16(BN, A_MN, B_MN, EK == kElemBF16) : ptx::idesc_tf32(BN, A_MN, B_MN);
       // MN-major: atom stride = kBK K-rows x 128 B; K-row groups of 4 (tf32, BASE32B) or 8 (bf16)
-      constexpr uint32_t mn_lbo = E::kBK * 128, mn_sbo = BF16 ? 1024 : 512, mn_step = E::kMmaK * 128;
-      constexpr uint32_t mn_lay = BF16 ? 2 : 1;
+      constexpr uint32_t mn_lbo = E::kBK * 128, mn_sbo = EK ? 1024 : 512, mn_step = E::kMmaK * 128;
+      constexpr uint32_t mn_lay = EK ? 2 : 1;
       constexpr uint32_t a_lbo = A_MN ? mn_lbo : 16, a_sbo = A_MN ? mn_sbo : 1024, a_step = A_MN ? mn_step : 32;
       constexpr uint32_t b_lbo = B_MN ? mn_lbo : 16, b_sbo = B_MN ? mn_sbo : 1024, b_step = B_MN ? mn_step : 32;
       constexpr uint32_t a_lay = A_MN ? mn_lay : 2, b_lay = B_MN ? mn_lay : 2;
@@ -182,10 +184,10 @@ __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
             const uint64_t bh = ptx::sdesc(sb + k * b_step, b_lbo, b_sbo, b_lay);
             const uint64_t bl = ptx::sdesc(sbl + k * b_step, b_lbo, b_sbo, b_lay);
             const uint32_t acc0 = (kb > kb0 || k > 0) ? 1u : 0u;
-            if (BF16) {
-              ptx::mma_bf16(acc, ah, bh, idesc, acc0);
-              ptx::mma_bf16(acc, ah, bl, idesc, 1u);
-              if (!A_EXACT) ptx::mma_bf16(acc, al, bh, idesc, 1u);
+            if (EK) {
+              ptx::mma_f16(acc, ah, bh, idesc, acc0);
+              ptx::mma_f16(acc, ah, bl, idesc, 1u);
+              if (!A_EXACT) ptx::mma_f16(acc, al, bh, idesc, 1u);
             } else {
               ptx::mma_tf32(acc, ah, bh, idesc, acc0);
               ptx::mma_tf32(acc, ah, bl, idesc, 1u);
