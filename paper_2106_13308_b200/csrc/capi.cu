@@ -371,8 +371,10 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
     for (int k = 0; k < h; ++k) H->w1skip = H->w1skip && degrees[k] <= k + 1;
     H->head_fast = true;
     for (int i = 0; i < Hd; ++i) H->head_fast = H->head_fast && off[i + 1] - off[i] == 1 && ks[off[i]] == i;
-    const int kp = 32 * ((h + 31) / 32 <= 1 ? 1 : (h + 31) / 32 <= 2 ? 2 : (h + 31) / 32 <= 4 ? 4
-                        : (h + 31) / 32 <= 8 ? 8 : (h + 31) / 32 <= 16 ? 16 : 32);
+    // staged head rows: v3 (fast structure) uses 128-float lane groups, v2 a power-of-two word count
+    const int kp = H->head_fast ? 128 * ((h + 127) / 128)
+                                : 32 * ((h + 31) / 32 <= 1 ? 1 : (h + 31) / 32 <= 2 ? 2 : (h + 31) / 32 <= 4 ? 4
+                                        : (h + 31) / 32 <= 8 ? 8 : (h + 31) / 32 <= 16 ? 16 : 32);
     dalloc(&H->W1Tp, (size_t)Hd * kp);
     dalloc(&H->W2cp, (size_t)h * kp);
     VQMC_CUDA(cudaMemset(H->W1Tp, 0, (size_t)Hd * kp * sizeof(float)));

@@ -50,6 +50,17 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+// Same with a suspend-time hint: the waiting thread sleeps instead of re-polling (producer warps
+// share an SM sub-partition with a consumer warp, so their polling would steal its issue slots).
+__device__ __forceinline__ void mbar_wait_sleep(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1, %2;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity), "r"(1000000u)
+      : "memory");
+}
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
@@ -255,21 +266,450 @@ __global__ void __launch_bounds__(32 * 9) head_v2_kernel(
   }
 }
 
+// ===========================================================================
+// Head sampler v3: the "fast" MADE structure (bit i completes exactly hidden unit i:
+// the reference's cyclic degrees deg_k = k + 1 when h <= n - 1, models.cpp:91), two
+// samples per warp.
+//
+// Lane l owns units / outputs 32 m + l (word slot m).  While word m is sampled, only slots
+// >= m still change, so the registers hold RELATIVE slots t = slot - m (shifted down by one
+// after every word) and the staged rows of the bits of word m are stored in the same
+// relative, lane-interleaved order: row i (word m = i / 32) keeps unit 32 (m + t) + l at
+// position 128 (t >> 2) + 4 l + (t & 3), so one LDS.128 gives a lane four consecutive
+// relative slots and the rows shrink word by word (triangular staging).  The code of a bit
+// is therefore the same for every word (a compact loop, no per-word unrolling).
+//
+// Bit i = 32 m + l is owned by lane l: it has the logit z2[0] and z1[0] of unit i (and the
+// diagonal weight W1T[i][i] in its own float4), so it computes x_i and g_i = relu(z1_i +
+// x_i W1T[i][i]) without communication and sends both in ONE shuffle (x in the sign bit of
+// g >= 0).  Every lane then applies the two rank-1 updates.  Serial chain per bit: compare,
+// select, max, select, shuffle, fma.  The rows of bit i + 1 are loaded while bit i is
+// processed (ping-pong registers); the two samples share every shared-memory load.
+// ===========================================================================
+__host__ __device__ __forceinline__ int head_rel_pos(int t, int l) { return 128 * (t >> 2) + 4 * l + (t & 3); }
+// staged floats of a row of word m (KPL word slots per lane)
+__host__ __device__ __forceinline__ int head_row_floats(int KPL, int m) { return 128 * ((KPL - m + 3) >> 2); }
+
+// Per-lane input of word m (this lane's bit 32 m + lane): the logit threshold of its uniform.
+// Production draws: u = (r + 1/2) 2^-32 from a 32-bit Philox word r, so logit(u) =
+// log((r + 1/2) / (~r + 1/2)) in fp32 (the ratio is exact up to fp32 rounding: the threshold
+// is within ~2e-7 of the fp64 value, far inside the 1e-5 flip tolerance), with the
+// clamp folded in: u < 1e-7 <=> r <= 428, u >= 1 - 1e-7 <=> ~r <= 428.  Parity mode (given
+// fp64 uniforms) keeps the fp64 threshold.
+__device__ __noinline__ float head_threshold(const double* __restrict__ uni, RngSpec rng, int B, int b, int ib) {
+  if (uni) return logit_threshold(uni[(size_t)ib * B + b]);
+  uint32_t r4[4];
+  rng.quad(b, ib, r4);
+  const uint32_t r = r4[ib & 3], nr = ~r;
+  if (r <= 428u) return -INFINITY;
+  if (nr <= 428u) return INFINITY;
+  return logf(((float)r + 0.5f) / ((float)nr + 0.5f));  // one log of the ratio: ~1e-7 absolute
+}
+
+// Outputs of one completed bit (sample b, bit ib; off the serial chain).
+__device__ __noinline__ double head_emit(int b, int ib, float z, float z1, int x, int n, int h, int hp, int np,
+                                         int hd1p, float* __restrict__ G1, __half* __restrict__ G1h,
+                                         __half* __restrict__ G1l, __half* __restrict__ Dh, __half* __restrict__ Dl,
+                                         __nv_bfloat16* __restrict__ Xf, double* __restrict__ cond) {
+  const float g = fmaxf(z1, 0.f);
+  G1[(size_t)b * h + ib] = g;
+  ptx::split_f16(g, G1h[(size_t)b * hp + ib], G1l[(size_t)b * hp + ib]);
+  const Unit u = unit_terms(z, x);
+  ptx::split_f16(u.D, Dh[(size_t)b * np + ib], Dl[(size_t)b * np + ib]);
+  if (cond) cond[(size_t)b * n + ib] = u.p;
+  Xf[(size_t)b * hd1p + ib] = __float2bfloat16_rn((float)x);
+  return (double)u.logt;
+}
+
+struct HeadV3Args {
+  int B, n, h, W;
+  HeadGeom geo;
+  const float* W1Tq;
+  const float* W2cq;
+  const float* b1;
+  const float* b2;
+  const double* uni;
+  RngSpec rng;
+  uint32_t* X;
+  float* G1;
+  __half* G1h;
+  __half* G1l;
+  int hp;
+  __half* Dh;
+  __half* Dl;
+  int np;
+  __nv_bfloat16* Xf;
+  int hd1p;
+  double* lp_head;
+  double* cond;
+};
+
+// Consumer state of one warp (two samples): relative slots and the ping-pong row buffers.
+template <int KG>
+struct HeadV3State {
+  static constexpr int KPL = 4 * KG;
+  float z1[2][KPL], z2[2][KPL];
+  float4 wa1[KG], wa2[KG], wb1[KG], wb2[KG];
+  float thr[2], thr_next[2];
+  int xin[2], xin_next[2];
+  double lp[2];
+  float vp[2];  // shuffled (x, g) of the pending bit
+#ifdef VQMC_HEAD_PROF
+  long long wait_cycles = 0;
+#endif
+  int slot, use;
+  const float* rows;
+};
+
+// Rank-1 updates of one bit (shuffled value v: x in the sign bit, g = |v|) to relative slots
+// [T0, T1) with that bit's rows (w1, w2).
+template <int KG, int T0, int T1>
+__device__ __forceinline__ void head_v3_update(HeadV3State<KG>& S, const float (&v)[2], const float4 (&w1)[KG],
+                                               const float4 (&w2)[KG]) {
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const float xf = (__float_as_uint(v[a]) >> 31) ? 1.f : 0.f;
+    const float ga = fabsf(v[a]);
+#pragma unroll
+    for (int t = T0; t < T1; ++t) {
+      const float4& r1 = w1[t >> 2];
+      const float4& r2 = w2[t >> 2];
+      const float c1 = (t & 3) == 0 ? r1.x : (t & 3) == 1 ? r1.y : (t & 3) == 2 ? r1.z : r1.w;
+      const float c2 = (t & 3) == 0 ? r2.x : (t & 3) == 1 ? r2.y : (t & 3) == 2 ? r2.z : r2.w;
+      S.z1[a][t] = fmaf(xf, c1, S.z1[a][t]);
+      S.z2[a][t] = fmaf(ga, c2, S.z2[a][t]);
+    }
+  }
+}
+
+// Ring geometry in registers (the bit loop must not reload kernel parameters).
+struct HeadRing {
+  uint64_t* full;
+  uint64_t* empty;
+  float* ring;
+  int G, R, slot_floats, Hd;
+};
+
+// One bit i = 32 m + l, software-pipelined: the update of bit i - 1 (rows in P, shuffled values
+// in S.vp; a zero value at the start of a word, making it a no-op) is split so that only its
+// slot-0 part (the next owner's logit and pre-activation) precedes the serial chain of bit i;
+// the bulk of it is issued after bit i's shuffle, hiding the shuffle latency.  Then the rows of
+// bit i + 1 are loaded into P.  EDGE: bit i + 1 may start a new ring slot or not exist (only
+// odd l can end a slot: G is even).
+template <int KG, int NQ, bool GIVEN, bool EDGE>
+__device__ __forceinline__ void head_v3_bit(HeadV3State<KG>& S, const HeadRing& Rg, int lane, int i, int l,
+                                            float4 (&P1)[KG], float4 (&P2)[KG], const float4 (&C1)[KG],
+                                            const float4 (&C2)[KG]) {
+  constexpr int RS = 128 * KG;
+  head_v3_update<KG, 0, 1>(S, S.vp, P1, P2);  // slot 0 of bit i - 1: on the serial chain
+  // owner (lane l) draws bit i and completes unit i; everyone evaluates it, lane l's value wins
+  float v[2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const bool x = GIVEN ? (S.xin[a] != 0) : (S.thr[a] < S.z2[a][0]);
+    const float z1u = x ? S.z1[a][0] + C1[0].x : S.z1[a][0];  // + x_i W1T[i][i] (relative slot 0)
+    const float g = fmaxf(z1u, 0.f);
+    v[a] = x ? -g : g;  // g >= 0: x rides in the sign bit (-0.0 when g == 0)
+    v[a] = __shfl_sync(kFull, v[a], l);
+  }
+  head_v3_update<KG, 1, 4 * NQ>(S, S.vp, P1, P2);  // the rest of bit i - 1
+#pragma unroll
+  for (int a = 0; a < 2; ++a) S.vp[a] = v[a];
+  if (EDGE) {
+    if (i + 1 >= Rg.Hd) return;
+    if (((i + 1) & (Rg.G - 1)) == 0) {
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&Rg.empty[S.slot]);  // rows of this slot are all in registers
+      if (++S.slot == Rg.R) {
+        S.slot = 0;
+        ++S.use;
+      }
+#ifdef VQMC_HEAD_PROF
+      const long long t0 = clock64();
+#endif
+      mbar_wait(&Rg.full[S.slot], S.use & 1);
+#ifdef VQMC_HEAD_PROF
+      S.wait_cycles += clock64() - t0;
+#endif
+      S.rows = Rg.ring + (size_t)S.slot * Rg.slot_floats;
+    }
+  }
+  // rows of bit i + 1 into P (free now; the next bit may start the next word, whose rows are
+  // never longer)
+  const float* r1 = S.rows + ((i + 1) & (Rg.G - 1)) * RS + 4 * lane;
+#if defined(VQMC_HEAD_EXP) && VQMC_HEAD_EXP == 1
+  if (i < 1)
+#endif
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    P1[q] = *reinterpret_cast<const float4*>(r1 + 128 * q);
+    P2[q] = *reinterpret_cast<const float4*>(r1 + Rg.G * RS + 128 * q);
+  }
+}
+
+// Eight bits i0 .. i0 + 7 = one ring slot (G == 8, i0 slot-aligned), unrolled: static row
+// buffers, static shuffle lanes l0 + k, and a single slot handover after the eighth bit.
+template <int KG, int NQ, bool GIVEN, int K>
+__device__ __forceinline__ void head_v3_bit8(HeadV3State<KG>& S, const HeadRing& Rg, int lane, int i0, int l0,
+                                             float4 (&P1)[KG], float4 (&P2)[KG], const float4 (&C1)[KG],
+                                             const float4 (&C2)[KG]) {
+  constexpr int RS = 128 * KG;
+  head_v3_update<KG, 0, 1>(S, S.vp, P1, P2);  // slot 0 of bit i - 1: on the serial chain
+  float v[2];
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    const bool x = GIVEN ? (S.xin[a] != 0) : (S.thr[a] < S.z2[a][0]);
+    const float z1u = x ? S.z1[a][0] + C1[0].x : S.z1[a][0];
+    const float g = fmaxf(z1u, 0.f);
+    v[a] = x ? -g : g;
+    v[a] = __shfl_sync(kFull, v[a], l0 + K);
+  }
+  head_v3_update<KG, 1, 4 * NQ>(S, S.vp, P1, P2);
+#pragma unroll
+  for (int a = 0; a < 2; ++a) S.vp[a] = v[a];
+  const float* r1;
+  if (K < 7) {
+    r1 = S.rows + (K + 1) * RS + 4 * lane;
+  } else {
+    if (i0 + 8 >= Rg.Hd) return;
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&Rg.empty[S.slot]);  // rows of this slot are all in registers
+    if (++S.slot == Rg.R) {
+      S.slot = 0;
+      ++S.use;
+    }
+    mbar_wait(&Rg.full[S.slot], S.use & 1);
+    S.rows = Rg.ring + (size_t)S.slot * Rg.slot_floats;
+    r1 = S.rows + 4 * lane;
+  }
+#pragma unroll
+  for (int q = 0; q < NQ; ++q) {
+    P1[q] = *reinterpret_cast<const float4*>(r1 + 128 * q);
+    P2[q] = *reinterpret_cast<const float4*>(r1 + 8 * RS + 128 * q);
+  }
+}
+
+template <int KG, int NQ, bool GIVEN>
+__device__ __forceinline__ void head_v3_group8(HeadV3State<KG>& S, const HeadRing& Rg, int lane, int i0, int l0) {
+  head_v3_bit8<KG, NQ, GIVEN, 0>(S, Rg, lane, i0, l0, S.wb1, S.wb2, S.wa1, S.wa2);
+  head_v3_bit8<KG, NQ, GIVEN, 1>(S, Rg, lane, i0, l0, S.wa1, S.wa2, S.wb1, S.wb2);
+  head_v3_bit8<KG, NQ, GIVEN, 2>(S, Rg, lane, i0, l0, S.wb1, S.wb2, S.wa1, S.wa2);
+  head_v3_bit8<KG, NQ, GIVEN, 3>(S, Rg, lane, i0, l0, S.wa1, S.wa2, S.wb1, S.wb2);
+  head_v3_bit8<KG, NQ, GIVEN, 4>(S, Rg, lane, i0, l0, S.wb1, S.wb2, S.wa1, S.wa2);
+  head_v3_bit8<KG, NQ, GIVEN, 5>(S, Rg, lane, i0, l0, S.wa1, S.wa2, S.wb1, S.wb2);
+  head_v3_bit8<KG, NQ, GIVEN, 6>(S, Rg, lane, i0, l0, S.wb1, S.wb2, S.wa1, S.wa2);
+  head_v3_bit8<KG, NQ, GIVEN, 7>(S, Rg, lane, i0, l0, S.wa1, S.wa2, S.wb1, S.wb2);
+}
+
+// Words [m0, m1), all with NQ live groups of relative slots (NQ = KG - m0 / 4).
+template <int KG, int NQ, bool GIVEN>
+__device__ __forceinline__ void head_v3_words(HeadV3State<KG>& S, const HeadV3Args& A, const HeadRing& Rg, int lane,
+                                              const int (&bs)[2], const bool (&act)[2], int m0, int m1) {
+  constexpr int KPL = 4 * KG;
+  const int Hd = Rg.Hd;
+  const int nwords = (Hd + 31) >> 5;
+#pragma unroll 1
+  for (int m = m0; m < m1; ++m) {
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      S.thr[a] = S.thr_next[a];
+      S.xin[a] = S.xin_next[a];
+      S.vp[a] = 0.f;  // nothing pending at a word start
+    }
+    if (m + 1 < nwords) {  // next word's inputs (overlaps this word)
+      const int ib = 32 * (m + 1) + lane;
+#pragma unroll
+      for (int a = 0; a < 2; ++a) {
+        S.thr_next[a] = 0.f;
+        S.xin_next[a] = 0;
+        if (act[a] && ib < Hd) {
+          if (GIVEN) S.xin_next[a] = (A.X[(size_t)bs[a] * A.W + m + 1] >> lane) & 1;
+          else S.thr_next[a] = head_threshold(A.uni, A.rng, A.B, bs[a], ib);
+        }
+      }
+    }
+    const int lend = min(32, Hd - 32 * m);
+    // bit l's rows are in wa when l is even, wb when odd; the pending bit's rows in the other
+    const int i0 = 32 * m;
+    // whole ring slots of 8 bits run unrolled; anything else (G != 8, a ragged last word) per pair
+    const int l8 = Rg.G == 8 ? (lend & ~7) : 0;
+#pragma unroll 1
+    for (int l = 0; l < l8; l += 8) head_v3_group8<KG, NQ, GIVEN>(S, Rg, lane, i0 + l, l);
+#pragma unroll 1
+    for (int l = l8; l < lend; l += 2) {  // lend is even except on the last word
+      if (l + 1 < lend) {
+        head_v3_bit<KG, NQ, GIVEN, false>(S, Rg, lane, i0 + l, l, S.wb1, S.wb2, S.wa1, S.wa2);
+        head_v3_bit<KG, NQ, GIVEN, true>(S, Rg, lane, i0 + l + 1, l + 1, S.wa1, S.wa2, S.wb1, S.wb2);
+      } else {
+        head_v3_bit<KG, NQ, GIVEN, true>(S, Rg, lane, i0 + l, l, S.wb1, S.wb2, S.wa1, S.wa2);
+      }
+    }
+    // flush the last bit's update (its rows are where bit lend - 1 kept them)
+    if ((lend - 1) & 1) head_v3_update<KG, 0, 4 * NQ>(S, S.vp, S.wb1, S.wb2);
+    else head_v3_update<KG, 0, 4 * NQ>(S, S.vp, S.wa1, S.wa2);
+    // word complete: this lane's bit 32 m + lane.  Later bits only add masked (exactly zero)
+    // terms to slot 0, so z2[0] is the final logit and z1[0] the final pre-activation.
+    const int ib = 32 * m + lane;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      const bool mine = act[a] && ib < Hd;
+      const float z = S.z2[a][0];
+      const int x = GIVEN ? S.xin[a] : (S.thr[a] < z ? 1 : 0);
+      if (mine)
+        S.lp[a] += head_emit(bs[a], ib, z, S.z1[a][0], x, A.n, A.h, A.hp, A.np, A.hd1p, A.G1, A.G1h, A.G1l, A.Dh,
+                             A.Dl, A.Xf, A.cond);
+      const uint32_t word = __ballot_sync(kFull, mine && x);
+      if (!GIVEN && act[a] && lane == 0) A.X[(size_t)bs[a] * A.W + m] = word;
+#pragma unroll
+      for (int t = 0; t + 1 < KPL; ++t) {  // shift the relative slots: slot m is complete
+        S.z1[a][t] = S.z1[a][t + 1];
+        S.z2[a][t] = S.z2[a][t + 1];
+      }
+      S.z1[a][KPL - 1] = 0.f;
+      S.z2[a][KPL - 1] = 0.f;
+    }
+  }
+}
+
+template <int KG, int P, bool GIVEN>
+__device__ __forceinline__ void head_v3_phases(HeadV3State<KG>& S, const HeadV3Args& A, const HeadRing& Rg, int lane,
+                                               const int (&bs)[2], const bool (&act)[2], int nwords) {
+  if constexpr (P < KG) {
+    const int m0 = 4 * P, m1 = min(nwords, 4 * P + 4);
+    if (m0 < m1) head_v3_words<KG, KG - P, GIVEN>(S, A, Rg, lane, bs, act, m0, m1);
+    head_v3_phases<KG, P + 1, GIVEN>(S, A, Rg, lane, bs, act, nwords);
+  }
+}
+
+template <int KG, bool GIVEN>
+__global__ void __launch_bounds__(32 * 5) head_v3_kernel(const __grid_constant__ HeadV3Args A) {
+  constexpr int KPL = 4 * KG;  // word slots per lane
+  constexpr int RS = 128 * KG; // staged row stride (floats), both matrices
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  const int Hd = A.h;          // fast structure: Hd == h
+  const int G = A.geo.G;       // bits per ring slot (power of two, divides 32)
+  const int nw = blockDim.x / 32 - 1;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + A.geo.R;
+  float* ring = reinterpret_cast<float*>(smem_raw + 256);
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < A.geo.R; ++r) {
+      mbar_init(&full[r], 1);
+      mbar_init(&empty[r], nw);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+
+  if (warp == nw) {  // ---------------- producer warp ----------------
+    if (lane == 0) {
+      int slot = 0, use = 0;
+      for (int g = 0; g < A.geo.ngroups; ++g) {
+        if (use > 0) mbar_wait_sleep(&empty[slot], (use - 1) & 1);
+        const int i0 = g * G, i1 = min(Hd, i0 + G);
+        // every row of the slot belongs to word i0 / 32 (G divides 32): copy its staged length only
+        const uint32_t rb = (uint32_t)head_row_floats(KPL, i0 >> 5) * 4u;
+        float* dst = ring + (size_t)slot * A.geo.slot_floats;
+        mbar_expect_tx(&full[slot], 2u * (uint32_t)(i1 - i0) * rb);
+        for (int r = 0; r < i1 - i0; ++r) {
+          bulk_g2s(dst + r * RS, A.W1Tq + (size_t)(i0 + r) * RS, rb, &full[slot]);
+          bulk_g2s(dst + (G + r) * RS, A.W2cq + (size_t)(i0 + r) * RS, rb, &full[slot]);
+        }
+        if (++slot == A.geo.R) {
+          slot = 0;
+          ++use;
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warps: samples 2 w and 2 w + 1 ----------------
+  const int bw = 2 * (blockIdx.x * nw + warp);
+  const int bs[2] = {bw, bw + 1};
+  const bool act[2] = {bw < A.B, bw + 1 < A.B};
+  HeadV3State<KG> S;
+#pragma unroll
+  for (int t = 0; t < KPL; ++t) {
+    const int k = 32 * t + lane;
+#pragma unroll
+    for (int a = 0; a < 2; ++a) {
+      S.z1[a][t] = k < A.h ? A.b1[k] : 0.f;
+      S.z2[a][t] = k < Hd ? A.b2[k] : 0.f;
+    }
+  }
+  const int nwords = (Hd + 31) >> 5;
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+    S.lp[a] = 0.0;
+    S.thr_next[a] = 0.f;
+    S.xin_next[a] = 0;
+    if (act[a] && lane < Hd) {
+      if (GIVEN) S.xin_next[a] = (A.X[(size_t)bs[a] * A.W] >> lane) & 1;
+      else S.thr_next[a] = head_threshold(A.uni, A.rng, A.B, bs[a], lane);
+    }
+  }
+  S.slot = 0;
+  S.use = 0;
+  S.rows = ring;
+  mbar_wait(&full[0], 0);
+#pragma unroll
+  for (int q = 0; q < KG; ++q) {
+    S.wa1[q] = *reinterpret_cast<const float4*>(S.rows + 128 * q + 4 * lane);
+    S.wa2[q] = *reinterpret_cast<const float4*>(S.rows + G * RS + 128 * q + 4 * lane);
+    S.wb1[q] = make_float4(0.f, 0.f, 0.f, 0.f);  // "pending" rows of the first bit (0 x 0, never NaN)
+    S.wb2[q] = make_float4(0.f, 0.f, 0.f, 0.f);
+  }
+  const HeadRing Rg{full, empty, ring, G, A.geo.R, A.geo.slot_floats, Hd};
+#ifdef VQMC_HEAD_PROF
+  const long long tstart = clock64();
+#endif
+  head_v3_phases<KG, 0, GIVEN>(S, A, Rg, lane, bs, act, nwords);
+#ifdef VQMC_HEAD_PROF
+  if (lane == 0 && (blockIdx.x % 32) == 0)
+    printf("HEADPROF block %d warp %d total %lld wait_full %lld\n", blockIdx.x, warp, clock64() - tstart, S.wait_cycles);
+#endif
+  // the last slot
+  __syncwarp();
+  if (lane == 0) mbar_arrive(&empty[S.slot]);
+#pragma unroll
+  for (int a = 0; a < 2; ++a) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) S.lp[a] += __shfl_xor_sync(kFull, S.lp[a], o);
+    if (act[a] && lane == 0) {
+      A.lp_head[bs[a]] = S.lp[a];
+      A.Xf[(size_t)bs[a] * A.hd1p + Hd] = __float2bfloat16_rn(1.f);  // ones column: gb1 = 1^T dz1
+    }
+  }
+}
+
 // Padded, completion-ordered copies of the head blocks (refreshed after every update):
 //   W1Tp[j][k] = W1m[k][j]           j < Hd, k < h (row stride hp)
 //   W2cp[c][i] = W2m[i][comp_k[c]]   c < h,  i < Hd (row stride Hdp)
-__global__ void head_pack_kernel(int h, int Hd, int hp, int Hdp, const float* __restrict__ W1T,
+// perm: the v3 relative staging order (head_rel_pos) when the fast structure holds, else identity.
+__global__ void head_pack_kernel(int h, int Hd, int hp, int Hdp, int perm, const float* __restrict__ W1T,
                                  const float* __restrict__ W2, const int* __restrict__ comp_k,
                                  float* __restrict__ W1Tp, float* __restrict__ W2cp) {
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n1 = (int64_t)Hd * hp, n2 = (int64_t)h * Hdp;
   if (t < n1) {
     const int j = (int)(t / hp), k = (int)(t % hp);
-    W1Tp[t] = k < h ? W1T[(size_t)j * h + k] : 0.f;
+    if (!perm) {
+      W1Tp[t] = k < h ? W1T[(size_t)j * h + k] : 0.f;
+    } else {  // v3: row j in the relative order of word j / 32; units of earlier words are not staged
+      const int m = j >> 5, tt = (k >> 5) - m;
+      if (tt >= 0) W1Tp[(size_t)j * hp + head_rel_pos(tt, k & 31)] = k < h ? W1T[(size_t)j * h + k] : 0.f;
+    }
   } else if (t < n1 + n2) {
     const int64_t u = t - n1;
     const int c = (int)(u / Hdp), i = (int)(u % Hdp);
-    W2cp[u] = i < Hd ? W2[(size_t)i * h + comp_k[c]] : 0.f;
+    if (!perm) {
+      W2cp[u] = i < Hd ? W2[(size_t)i * h + comp_k[c]] : 0.f;
+    } else {  // v3: row c (= bit c, fast structure) in the relative order of word c / 32
+      const int m = c >> 5, tt = (i >> 5) - m;
+      if (tt >= 0) W2cp[(size_t)c * Hdp + head_rel_pos(tt, i & 31)] = i < Hd ? W2[(size_t)i * h + comp_k[c]] : 0.f;
+    }
   }
 }
 
@@ -308,11 +748,11 @@ static HeadGeom head_geometry(const Handle* H) {
 
 void launch_head_pack(Handle* H) {
   const Layout& L = H->L;
-  const int hp = 32 * head_kpl(L.h), Hdp = H->head_fast ? hp : 32 * ((L.Hd + 31) / 32);
+  const int hp = H->head_hpk, Hdp = H->head_Hdp;
   const int64_t total = (int64_t)L.Hd * hp + (int64_t)L.h * Hdp;
   KScope ks(H, "head_pack");
   head_pack_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(
-      L.h, L.Hd, hp, Hdp, H->P + L.off_w1t, H->P + L.off_w2, H->d_comp_k, H->W1Tp, H->W2cp);
+      L.h, L.Hd, hp, Hdp, H->head_fast ? 1 : 0, H->P + L.off_w1t, H->P + L.off_w2, H->d_comp_k, H->W1Tp, H->W2cp);
   VQMC_CUDA(cudaGetLastError());
   H->launches++;
 }
@@ -351,7 +791,70 @@ static void head_v2_dispatch(Handle* H, int B, const double* uni, RngSpec rng, b
   }
 }
 
+// v3 geometry: slot = G bits x (W1 row + W2 row) of 128 KG floats each.
+static HeadGeom head_v3_geometry(const Handle* H) {
+  const Layout& L = H->L;
+  HeadGeom g{};
+  const int RS = H->head_hpk;  // 128 * KG
+  g.R = 6;
+  g.hp = RS;
+  g.Hdp = RS;
+  g.cmax = 1;
+  for (int G = 8; G >= 1; G >>= 1) {
+    g.G = G;
+    g.slot_floats = 2 * G * RS;
+    g.smem = 256 + (size_t)g.R * g.slot_floats * 4;
+    if (g.smem <= 225 * 1024) break;
+    if (G == 1) throw InvalidArgument("head sampler shared-memory ring does not fit (hidden width too large)");
+  }
+  g.ngroups = (L.Hd + g.G - 1) / g.G;
+  return g;
+}
+
+template <int KG, bool GIVEN>
+static void head_v3_launch(Handle* H, int B, const double* uni, RngSpec rng, double* cond) {
+  const Layout& L = H->L;
+  const HeadGeom geo = head_v3_geometry(H);
+  static size_t attr_set = 0;
+  if (attr_set < geo.smem) {
+    VQMC_CUDA(cudaFuncSetAttribute(head_v3_kernel<KG, GIVEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                   (int)geo.smem));
+    attr_set = geo.smem;
+  }
+  int dev_sms = 148;
+  cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, H->device);
+  const int pairs = (B + 1) / 2;
+  const int nw = std::max(1, std::min(4, (pairs + dev_sms - 1) / dev_sms));  // <= 4 sample-pair warps + producer
+  const int grid = (pairs + nw - 1) / nw;
+  KScope ks(H, GIVEN ? "head_given" : "head_sample");
+  const HeadV3Args args{B,      L.n,     L.h,    L.W,    geo,     H->W1Tp,  H->W2cp, H->P + L.off_b1,
+                        H->P + L.off_b2, uni, rng, H->X, H->G1, H->G1h, H->G1l, H->hp18, H->Dh, H->Dl, H->np8,
+                        H->Xfb, H->hd18, H->lp_head, cond};
+  head_v3_kernel<KG, GIVEN><<<grid, 32 * (nw + 1), geo.smem, H->stream>>>(args);
+  VQMC_CUDA(cudaGetLastError());
+  H->launches++;
+}
+
+template <int KG>
+static void head_v3_dispatch(Handle* H, int B, const double* uni, RngSpec rng, bool given, double* cond) {
+  if (given) head_v3_launch<KG, true>(H, B, uni, rng, cond);
+  else head_v3_launch<KG, false>(H, B, uni, rng, cond);
+}
+
 void launch_head_v2(Handle* H, int B, const double* uni, RngSpec rng, bool given, double* cond) {
+  if (H->head_fast) {
+    switch (H->head_hpk / 128) {
+      case 1: head_v3_dispatch<1>(H, B, uni, rng, given, cond); return;
+      case 2: head_v3_dispatch<2>(H, B, uni, rng, given, cond); return;
+      case 3: head_v3_dispatch<3>(H, B, uni, rng, given, cond); return;
+      case 4: head_v3_dispatch<4>(H, B, uni, rng, given, cond); return;
+      case 5: head_v3_dispatch<5>(H, B, uni, rng, given, cond); return;
+      case 6: head_v3_dispatch<6>(H, B, uni, rng, given, cond); return;
+      case 7: head_v3_dispatch<7>(H, B, uni, rng, given, cond); return;
+      case 8: head_v3_dispatch<8>(H, B, uni, rng, given, cond); return;
+      default: throw InvalidArgument("head sampler: hidden width > 1024 is not supported");
+    }
+  }
   const int kpl = (H->L.h + 31) / 32;
   if (kpl <= 1) head_v2_dispatch<1>(H, B, uni, rng, given, cond);
   else if (kpl <= 2) head_v2_dispatch<2>(H, B, uni, rng, given, cond);

@@ -141,7 +141,7 @@ struct Handle {
   int32_t* d_comp_pos = nullptr;   // [h] completion slot of hidden unit k (inverse of comp_k)
   unsigned* d_done = nullptr;      // last-block counter of the Adam grad-norm reduction
   std::vector<int32_t> comp_off_host;  // [Hd + 1]
-  bool head_fast = false;  // bit i completes exactly hidden unit i
+  bool head_fast = false;  // bit i completes exactly hidden unit i (head v3, lane-permuted staging)
   bool w1skip = false;     // deg_k <= k + 1 for all k (W1 columns below the current word are dead)
   int32_t* d_deg = nullptr;
   int32_t* d_comp_k = nullptr;    // hidden units sorted by degree

@@ -272,8 +272,16 @@ __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __re
 // derives from the updated parameters: the squared norm of the reduced gradient (last-block
 // reduction, fixed order; trainer.cpp:253), the tf32 split of W2 for the GEMMs and the head
 // sampler's padded / completion-ordered copies of the head blocks.
+// head v3 staging order (head.cu): row r of word m = r / 32 keeps entry k (k >= 32 m) at
+// 128 (t >> 2) + 4 (k & 31) + (t & 3), t = k / 32 - m; entries of earlier words are not staged.
+__device__ __forceinline__ int head_rel_pos_dev(int r, int k) {
+  const int t = (k >> 5) - (r >> 5);
+  return t < 0 ? -1 : 128 * (t >> 2) + 4 * (k & 31) + (t & 3);
+}
+
 struct AdamOut {
   int h, hp18, Hd, hpk, Hdp;
+  bool perm;  // head staging copies are lane-permuted (head v3)
   bool vec_w2;  // h % 4 == 0 and off_w2 % 4 == 0: a group of 4 never straddles two W2 rows
   int64_t off_b1, off_w2, off_b2;
   const int* comp_pos;  // completion slot of hidden unit k
@@ -287,11 +295,24 @@ __device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, fl
   // (32-bit index math: the live buffer is < 2^31 entries, checked at handle creation)
   if (t < o.off_b1) {  // W1T[j][k]
     const unsigned tt = (unsigned)t, j = tt / (unsigned)o.h, k = tt - j * (unsigned)o.h;
-    o.W1Tp[(size_t)j * o.hpk + k] = p;
+    if (!o.perm) {
+      o.W1Tp[(size_t)j * o.hpk + k] = p;
+    } else {
+      const int pos = head_rel_pos_dev((int)j, (int)k);
+      if (pos >= 0) o.W1Tp[(size_t)j * o.hpk + pos] = p;
+    }
   } else if (t >= o.off_w2 && t < o.off_b2) {  // W2[i][k]
     const unsigned u = (unsigned)(t - o.off_w2), i = u / (unsigned)o.h, k = u - i * (unsigned)o.h;
     ptx::split_f16(p, o.W2h[(size_t)i * o.hp18 + k], o.W2l[(size_t)i * o.hp18 + k]);
-    if ((int)i < o.Hd) o.W2cp[(size_t)o.comp_pos[k] * o.Hdp + i] = p;
+    if ((int)i < o.Hd) {
+      const int c = o.comp_pos[k];
+      if (!o.perm) {
+        o.W2cp[(size_t)c * o.Hdp + i] = p;
+      } else {
+        const int pos = head_rel_pos_dev(c, (int)i);
+        if (pos >= 0) o.W2cp[(size_t)c * o.Hdp + pos] = p;
+      }
+    }
   } else if (t >= o.off_b2) {  // b2[i]: column h of the W2 pair (the tail GEMM's bias column)
     const size_t i = (size_t)(t - o.off_b2);
     ptx::split_f16(p, o.W2h[i * o.hp18 + o.h], o.W2l[i * o.hp18 + o.h]);
@@ -524,7 +545,7 @@ void launch_set_step(Handle* H, uint64_t call, int64_t t, double lr, double b1, 
 void launch_adam(Handle* H, float grad_scale) {
   const Layout& L = H->L;
   const bool vec = (L.h % 4) == 0 && (L.off_w2 % 4) == 0;
-  AdamOut o{L.h, H->hp18, L.Hd, H->head_hpk, H->head_Hdp, vec, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
+  AdamOut o{L.h, H->hp18, L.Hd, H->head_hpk, H->head_Hdp, H->head_fast, vec, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
             H->W1Tp, H->W2cp, H->W2h, H->W2l};
   KScope ks(H, "adam");
   adam_kernel<<<H->gpart_n, 256, 0, H->stream>>>(L.total, grad_scale, H->d_step, H->P, H->G, H->Mo, H->Vo,
