@@ -100,6 +100,7 @@ void Handle::ensure_batch(int B) {
     VQMC_CUDA(cudaMemset(G1l, 0, ones.size() * sizeof(__half)));
   }
   dalloc(&lp_head, (size_t)B);
+  dalloc(&thr, (size_t)B * ((L.Hd + 7) & ~7));
   dalloc(&lp_part, (size_t)max_tiles * B);
   dalloc(&log_psi, (size_t)B);
   dalloc(&cut, (size_t)B);
@@ -375,10 +376,12 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
     const int kp = H->head_fast ? 128 * ((h + 127) / 128)
                                 : 32 * ((h + 31) / 32 <= 1 ? 1 : (h + 31) / 32 <= 2 ? 2 : (h + 31) / 32 <= 4 ? 4
                                         : (h + 31) / 32 <= 8 ? 8 : (h + 31) / 32 <= 16 ? 16 : 32);
-    dalloc(&H->W1Tp, (size_t)Hd * kp);
-    dalloc(&H->W2cp, (size_t)h * kp);
-    VQMC_CUDA(cudaMemset(H->W1Tp, 0, (size_t)Hd * kp * sizeof(float)));
-    VQMC_CUDA(cudaMemset(H->W2cp, 0, (size_t)h * kp * sizeof(float)));
+    // rows padded to a multiple of 8 with zero rows (the v3 head runs whole 8-bit ring slots)
+    const size_t r1 = (size_t)((Hd + 7) & ~7), r2 = (size_t)((h + 7) & ~7);
+    dalloc(&H->W1Tp, r1 * kp);
+    dalloc(&H->W2cp, r2 * kp);
+    VQMC_CUDA(cudaMemset(H->W1Tp, 0, r1 * kp * sizeof(float)));
+    VQMC_CUDA(cudaMemset(H->W2cp, 0, r2 * kp * sizeof(float)));
     H->head_hpk = kp;
     H->head_Hdp = H->head_fast ? kp : 32 * ((Hd + 31) / 32);
     std::vector<int32_t> cpos(h);
@@ -427,7 +430,7 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   if (H->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy(H->nccl_comm);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2h, H->W2l, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
-                  H->lp_head, H->lp_part, H->log_psi, H->cut, H->local, H->w, H->d_wscale, H->d_flag,
+                  H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->local, H->w, H->d_wscale, H->d_flag,
                   H->Epart, H->dz1bh, H->dz1bl, H->Xfb, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat,
                   H->d_gpart, H->d_step, H->d_done, H->d_comp_pos};
   for (void* p : ptrs)

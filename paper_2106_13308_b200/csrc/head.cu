@@ -77,6 +77,7 @@ struct HeadGeom {
   int cmax;    // max completions in one group of G bits
   int ngroups;
   int slot_floats;
+  int ring_off;  // v3: byte offset of the row ring (after the mbarriers)
   size_t smem;
 };
 
@@ -296,7 +297,7 @@ __host__ __device__ __forceinline__ int head_row_floats(int KPL, int m) { return
 // is within ~2e-7 of the fp64 value, far inside the 1e-5 flip tolerance), with the
 // clamp folded in: u < 1e-7 <=> r <= 428, u >= 1 - 1e-7 <=> ~r <= 428.  Parity mode (given
 // fp64 uniforms) keeps the fp64 threshold.
-__device__ __noinline__ float head_threshold(const double* __restrict__ uni, RngSpec rng, int B, int b, int ib) {
+__device__ __forceinline__ float head_threshold(const double* __restrict__ uni, RngSpec rng, int B, int b, int ib) {
   if (uni) return logit_threshold(uni[(size_t)ib * B + b]);
   uint32_t r4[4];
   rng.quad(b, ib, r4);
@@ -306,8 +307,40 @@ __device__ __noinline__ float head_threshold(const double* __restrict__ uni, Rng
   return logf(((float)r + 0.5f) / ((float)nr + 0.5f));  // one log of the ratio: ~1e-7 absolute
 }
 
+// Logit thresholds of the head bits, thr[b][i] for i < Hd8 (bits >= Hd: +inf, they draw 0).
+// Given configurations (made_forward) become -inf / +inf, so the head draws exactly those bits.
+// One thread per (sample, 4 consecutive bits): one Philox call serves all four.
+__global__ void head_thresholds_kernel(int B, int Hd, int Hd8, int W, const double* __restrict__ uni, RngSpec rng,
+                                       const uint32_t* __restrict__ X, int given, float* __restrict__ thr) {
+  const int q4 = Hd8 >> 2;
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)B * q4) return;
+  const int b = (int)(t / q4), i0 = 4 * (int)(t % q4);
+  float out[4];
+  if (given) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int i = i0 + k;
+      out[k] = (i < Hd && ((X[(size_t)b * W + (i >> 5)] >> (i & 31)) & 1)) ? -INFINITY : INFINITY;
+    }
+  } else if (uni) {
+#pragma unroll
+    for (int k = 0; k < 4; ++k) out[k] = i0 + k < Hd ? logit_threshold(uni[(size_t)(i0 + k) * B + b]) : INFINITY;
+  } else {
+    uint32_t r4[4];
+    rng.quad(b, i0, r4);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const uint32_t r = r4[k], nr = ~r;
+      float v = r <= 428u ? -INFINITY : (nr <= 428u ? INFINITY : logf(((float)r + 0.5f) / ((float)nr + 0.5f)));
+      out[k] = i0 + k < Hd ? v : INFINITY;
+    }
+  }
+  *reinterpret_cast<float4*>(thr + (size_t)b * Hd8 + i0) = make_float4(out[0], out[1], out[2], out[3]);
+}
+
 // Outputs of one completed bit (sample b, bit ib; off the serial chain).
-__device__ __noinline__ double head_emit(int b, int ib, float z, float z1, int x, int n, int h, int hp, int np,
+__device__ __forceinline__ double head_emit(int b, int ib, float z, float z1, int x, int n, int h, int hp, int np,
                                          int hd1p, float* __restrict__ G1, __half* __restrict__ G1h,
                                          __half* __restrict__ G1l, __half* __restrict__ Dh, __half* __restrict__ Dl,
                                          __nv_bfloat16* __restrict__ Xf, double* __restrict__ cond) {
@@ -342,6 +375,7 @@ struct HeadV3Args {
   int hd1p;
   double* lp_head;
   double* cond;
+  const float* thr;  // [B][Hd8] logit thresholds (head_thresholds_kernel)
 };
 
 // Consumer state of one warp (two samples): relative slots and the ping-pong row buffers.
@@ -350,10 +384,9 @@ struct HeadV3State {
   static constexpr int KPL = 4 * KG;
   float z1[2][KPL], z2[2][KPL];
   float4 wa1[KG], wa2[KG], wb1[KG], wb2[KG];
-  float thr[2], thr_next[2];
-  int xin[2], xin_next[2];
-  double lp[2];
-  float vp[2];  // shuffled (x, g) of the pending bit
+  float thr[2];       // this lane's logit threshold of the current word (given bits: -inf / +inf)
+  float thr_next[2];  // the next word's (prefetched)
+  float vp[2];   // shuffled (x, g) of the pending bit
 #ifdef VQMC_HEAD_PROF
   long long wait_cycles = 0;
 #endif
@@ -388,64 +421,8 @@ struct HeadRing {
   uint64_t* empty;
   float* ring;
   int G, R, slot_floats, Hd;
+  int Hd8;  // bits rounded up to the 8-bit slot (staged rows padded with zero rows)
 };
-
-// One bit i = 32 m + l, software-pipelined: the update of bit i - 1 (rows in P, shuffled values
-// in S.vp; a zero value at the start of a word, making it a no-op) is split so that only its
-// slot-0 part (the next owner's logit and pre-activation) precedes the serial chain of bit i;
-// the bulk of it is issued after bit i's shuffle, hiding the shuffle latency.  Then the rows of
-// bit i + 1 are loaded into P.  EDGE: bit i + 1 may start a new ring slot or not exist (only
-// odd l can end a slot: G is even).
-template <int KG, int NQ, bool GIVEN, bool EDGE>
-__device__ __forceinline__ void head_v3_bit(HeadV3State<KG>& S, const HeadRing& Rg, int lane, int i, int l,
-                                            float4 (&P1)[KG], float4 (&P2)[KG], const float4 (&C1)[KG],
-                                            const float4 (&C2)[KG]) {
-  constexpr int RS = 128 * KG;
-  head_v3_update<KG, 0, 1>(S, S.vp, P1, P2);  // slot 0 of bit i - 1: on the serial chain
-  // owner (lane l) draws bit i and completes unit i; everyone evaluates it, lane l's value wins
-  float v[2];
-#pragma unroll
-  for (int a = 0; a < 2; ++a) {
-    const bool x = GIVEN ? (S.xin[a] != 0) : (S.thr[a] < S.z2[a][0]);
-    const float z1u = x ? S.z1[a][0] + C1[0].x : S.z1[a][0];  // + x_i W1T[i][i] (relative slot 0)
-    const float g = fmaxf(z1u, 0.f);
-    v[a] = x ? -g : g;  // g >= 0: x rides in the sign bit (-0.0 when g == 0)
-    v[a] = __shfl_sync(kFull, v[a], l);
-  }
-  head_v3_update<KG, 1, 4 * NQ>(S, S.vp, P1, P2);  // the rest of bit i - 1
-#pragma unroll
-  for (int a = 0; a < 2; ++a) S.vp[a] = v[a];
-  if (EDGE) {
-    if (i + 1 >= Rg.Hd) return;
-    if (((i + 1) & (Rg.G - 1)) == 0) {
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&Rg.empty[S.slot]);  // rows of this slot are all in registers
-      if (++S.slot == Rg.R) {
-        S.slot = 0;
-        ++S.use;
-      }
-#ifdef VQMC_HEAD_PROF
-      const long long t0 = clock64();
-#endif
-      mbar_wait(&Rg.full[S.slot], S.use & 1);
-#ifdef VQMC_HEAD_PROF
-      S.wait_cycles += clock64() - t0;
-#endif
-      S.rows = Rg.ring + (size_t)S.slot * Rg.slot_floats;
-    }
-  }
-  // rows of bit i + 1 into P (free now; the next bit may start the next word, whose rows are
-  // never longer)
-  const float* r1 = S.rows + ((i + 1) & (Rg.G - 1)) * RS + 4 * lane;
-#if defined(VQMC_HEAD_EXP) && VQMC_HEAD_EXP == 1
-  if (i < 1)
-#endif
-#pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    P1[q] = *reinterpret_cast<const float4*>(r1 + 128 * q);
-    P2[q] = *reinterpret_cast<const float4*>(r1 + Rg.G * RS + 128 * q);
-  }
-}
 
 // Eight bits i0 .. i0 + 7 = one ring slot (G == 8, i0 slot-aligned), unrolled: static row
 // buffers, static shuffle lanes l0 + k, and a single slot handover after the eighth bit.
@@ -458,30 +435,41 @@ __device__ __forceinline__ void head_v3_bit8(HeadV3State<KG>& S, const HeadRing&
   float v[2];
 #pragma unroll
   for (int a = 0; a < 2; ++a) {
-    const bool x = GIVEN ? (S.xin[a] != 0) : (S.thr[a] < S.z2[a][0]);
+    const bool x = S.thr[a] < S.z2[a][0];
     const float z1u = x ? S.z1[a][0] + C1[0].x : S.z1[a][0];
     const float g = fmaxf(z1u, 0.f);
     v[a] = x ? -g : g;
+#if !(defined(VQMC_HEAD_EXP) && VQMC_HEAD_EXP == 2)
     v[a] = __shfl_sync(kFull, v[a], l0 + K);
+#endif
   }
+#if !(defined(VQMC_HEAD_EXP) && VQMC_HEAD_EXP == 3)
   head_v3_update<KG, 1, 4 * NQ>(S, S.vp, P1, P2);
+#endif
 #pragma unroll
   for (int a = 0; a < 2; ++a) S.vp[a] = v[a];
   const float* r1;
   if (K < 7) {
     r1 = S.rows + (K + 1) * RS + 4 * lane;
   } else {
-    if (i0 + 8 >= Rg.Hd) return;
+    if (i0 + 8 >= Rg.Hd8) return;
+#if !defined(VQMC_HEAD_EXP5)
     __syncwarp();
     if (lane == 0) mbar_arrive(&Rg.empty[S.slot]);  // rows of this slot are all in registers
+#endif
     if (++S.slot == Rg.R) {
       S.slot = 0;
       ++S.use;
     }
+#if !defined(VQMC_HEAD_EXP5)
     mbar_wait(&Rg.full[S.slot], S.use & 1);
+#endif
     S.rows = Rg.ring + (size_t)S.slot * Rg.slot_floats;
     r1 = S.rows + 4 * lane;
   }
+#if defined(VQMC_HEAD_EXP4)
+  if (i0 < 0)
+#endif
 #pragma unroll
   for (int q = 0; q < NQ; ++q) {
     P1[q] = *reinterpret_cast<const float4*>(r1 + 128 * q);
@@ -501,65 +489,54 @@ __device__ __forceinline__ void head_v3_group8(HeadV3State<KG>& S, const HeadRin
   head_v3_bit8<KG, NQ, GIVEN, 7>(S, Rg, lane, i0, l0, S.wa1, S.wa2, S.wb1, S.wb2);
 }
 
+// Side channels of a head CTA (besides the row ring):
+//   thr (global)       logit thresholds [B][Hd8] from head_thresholds_kernel (consumers prefetch a word ahead)
+//   zb[p][s][2][32]    final (z2, z1) of this lane's bit of word m, p = m & 1 (consumers -> emit warps)
+struct HeadSide {
+  uint64_t* zdone;      // [2]: all consumers wrote zb[p] (count nw)
+  uint64_t* zfree;      // [2]: the emit warps consumed zb[p] (count kHeadEmitWarps)
+  const float* thr;     // global [B][Hd8]
+  float* zb;            // [2][8][2][32]
+  int Hd8, b0;          // threshold row stride; first sample of the CTA
+};
+constexpr int kHeadEmitWarps = 2;
+
 // Words [m0, m1), all with NQ live groups of relative slots (NQ = KG - m0 / 4).
 template <int KG, int NQ, bool GIVEN>
-__device__ __forceinline__ void head_v3_words(HeadV3State<KG>& S, const HeadV3Args& A, const HeadRing& Rg, int lane,
-                                              const int (&bs)[2], const bool (&act)[2], int m0, int m1) {
+__device__ __forceinline__ void head_v3_words(HeadV3State<KG>& S, const HeadRing& Rg, const HeadSide& Sd, int lane,
+                                              int warp, int m0, int m1) {
   constexpr int KPL = 4 * KG;
   const int Hd = Rg.Hd;
-  const int nwords = (Hd + 31) >> 5;
+  const int nwords = (Sd.Hd8 + 31) >> 5;
 #pragma unroll 1
   for (int m = m0; m < m1; ++m) {
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
       S.thr[a] = S.thr_next[a];
-      S.xin[a] = S.xin_next[a];
       S.vp[a] = 0.f;  // nothing pending at a word start
-    }
-    if (m + 1 < nwords) {  // next word's inputs (overlaps this word)
+      // next word's thresholds (global, coalesced; hidden behind this word)
       const int ib = 32 * (m + 1) + lane;
-#pragma unroll
-      for (int a = 0; a < 2; ++a) {
-        S.thr_next[a] = 0.f;
-        S.xin_next[a] = 0;
-        if (act[a] && ib < Hd) {
-          if (GIVEN) S.xin_next[a] = (A.X[(size_t)bs[a] * A.W + m + 1] >> lane) & 1;
-          else S.thr_next[a] = head_threshold(A.uni, A.rng, A.B, bs[a], ib);
-        }
-      }
+      if (m + 1 < nwords && ib < Sd.Hd8) S.thr_next[a] = Sd.thr[(size_t)(Sd.b0 + 2 * warp + a) * Sd.Hd8 + ib];
     }
-    const int lend = min(32, Hd - 32 * m);
-    // bit l's rows are in wa when l is even, wb when odd; the pending bit's rows in the other
+    const int lend = min(32, Rg.Hd8 - 32 * m);
     const int i0 = 32 * m;
-    // whole ring slots of 8 bits run unrolled; anything else (G != 8, a ragged last word) per pair
-    const int l8 = Rg.G == 8 ? (lend & ~7) : 0;
+    // ring slots of 8 bits, unrolled (the bit count is padded to a multiple of 8 with dummy bits:
+    // zero rows, threshold +inf, so they draw 0 and change nothing)
 #pragma unroll 1
-    for (int l = 0; l < l8; l += 8) head_v3_group8<KG, NQ, GIVEN>(S, Rg, lane, i0 + l, l);
-#pragma unroll 1
-    for (int l = l8; l < lend; l += 2) {  // lend is even except on the last word
-      if (l + 1 < lend) {
-        head_v3_bit<KG, NQ, GIVEN, false>(S, Rg, lane, i0 + l, l, S.wb1, S.wb2, S.wa1, S.wa2);
-        head_v3_bit<KG, NQ, GIVEN, true>(S, Rg, lane, i0 + l + 1, l + 1, S.wa1, S.wa2, S.wb1, S.wb2);
-      } else {
-        head_v3_bit<KG, NQ, GIVEN, true>(S, Rg, lane, i0 + l, l, S.wb1, S.wb2, S.wa1, S.wa2);
-      }
-    }
-    // flush the last bit's update (its rows are where bit lend - 1 kept them)
-    if ((lend - 1) & 1) head_v3_update<KG, 0, 4 * NQ>(S, S.vp, S.wb1, S.wb2);
-    else head_v3_update<KG, 0, 4 * NQ>(S, S.vp, S.wa1, S.wa2);
+    for (int l = 0; l < lend; l += 8) head_v3_group8<KG, NQ, GIVEN>(S, Rg, lane, i0 + l, l);
+    // flush the last bit's update (an 8-bit group ends with its rows in wb)
+    head_v3_update<KG, 0, 4 * NQ>(S, S.vp, S.wb1, S.wb2);
     // word complete: this lane's bit 32 m + lane.  Later bits only add masked (exactly zero)
-    // terms to slot 0, so z2[0] is the final logit and z1[0] the final pre-activation.
-    const int ib = 32 * m + lane;
+    // terms to slot 0, so z2[0] is the final logit and z1[0] the final pre-activation: hand
+    // them to the emit warp (double-buffered by word parity).
+    const int p = m & 1;
+    if (m >= 2) mbar_wait(&Sd.zfree[p], ((m >> 1) - 1) & 1);
 #pragma unroll
     for (int a = 0; a < 2; ++a) {
-      const bool mine = act[a] && ib < Hd;
-      const float z = S.z2[a][0];
-      const int x = GIVEN ? S.xin[a] : (S.thr[a] < z ? 1 : 0);
-      if (mine)
-        S.lp[a] += head_emit(bs[a], ib, z, S.z1[a][0], x, A.n, A.h, A.hp, A.np, A.hd1p, A.G1, A.G1h, A.G1l, A.Dh,
-                             A.Dl, A.Xf, A.cond);
-      const uint32_t word = __ballot_sync(kFull, mine && x);
-      if (!GIVEN && act[a] && lane == 0) A.X[(size_t)bs[a] * A.W + m] = word;
+      const int sidx = 2 * warp + a;
+      float* zrow = Sd.zb + ((size_t)(p * 8 + sidx) * 2) * 32;
+      zrow[lane] = S.z2[a][0];
+      zrow[32 + lane] = S.z1[a][0];
 #pragma unroll
       for (int t = 0; t + 1 < KPL; ++t) {  // shift the relative slots: slot m is complete
         S.z1[a][t] = S.z1[a][t + 1];
@@ -568,46 +545,65 @@ __device__ __forceinline__ void head_v3_words(HeadV3State<KG>& S, const HeadV3Ar
       S.z1[a][KPL - 1] = 0.f;
       S.z2[a][KPL - 1] = 0.f;
     }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&Sd.zdone[p]);
   }
 }
 
 template <int KG, int P, bool GIVEN>
-__device__ __forceinline__ void head_v3_phases(HeadV3State<KG>& S, const HeadV3Args& A, const HeadRing& Rg, int lane,
-                                               const int (&bs)[2], const bool (&act)[2], int nwords) {
+__device__ __forceinline__ void head_v3_phases(HeadV3State<KG>& S, const HeadRing& Rg, const HeadSide& Sd, int lane,
+                                               int warp, int nwords) {
   if constexpr (P < KG) {
     const int m0 = 4 * P, m1 = min(nwords, 4 * P + 4);
-    if (m0 < m1) head_v3_words<KG, KG - P, GIVEN>(S, A, Rg, lane, bs, act, m0, m1);
-    head_v3_phases<KG, P + 1, GIVEN>(S, A, Rg, lane, bs, act, nwords);
+    if (m0 < m1) head_v3_words<KG, KG - P, GIVEN>(S, Rg, Sd, lane, warp, m0, m1);
+    head_v3_phases<KG, P + 1, GIVEN>(S, Rg, Sd, lane, warp, nwords);
   }
 }
 
+// CTA layout: warps [0, nw) consumers (two samples each), warp nw the row producer (TMA),
+// warps nw + 1 .. nw + kHeadEmitWarps the emit warps (per completed word: G1 and its fp16
+// pair, D pair, spins, log-probability, packed X words).  The consumers only run the serial
+// chain and the rank-1 updates; thresholds come precomputed (head_thresholds_kernel).
 template <int KG, bool GIVEN>
-__global__ void __launch_bounds__(32 * 5) head_v3_kernel(const __grid_constant__ HeadV3Args A) {
+__global__ void __launch_bounds__(32 * (5 + kHeadEmitWarps)) head_v3_kernel(const __grid_constant__ HeadV3Args A) {
   constexpr int KPL = 4 * KG;  // word slots per lane
   constexpr int RS = 128 * KG; // staged row stride (floats), both matrices
   extern __shared__ __align__(128) unsigned char smem_raw[];
   const int Hd = A.h;          // fast structure: Hd == h
-  const int G = A.geo.G;       // bits per ring slot (power of two, divides 32)
-  const int nw = blockDim.x / 32 - 1;
+  const int G = A.geo.G;       // bits per ring slot (= 8)
+  const int nw = blockDim.x / 32 - 1 - kHeadEmitWarps;
+  const int nwords = (Hd + 31) >> 5;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
   uint64_t* empty = full + A.geo.R;
-  float* ring = reinterpret_cast<float*>(smem_raw + 256);
+  HeadSide Sd;
+  Sd.zdone = empty + A.geo.R;
+  Sd.zfree = Sd.zdone + 2;
+  Sd.Hd8 = (Hd + 7) & ~7;
+  Sd.thr = A.thr;
+  Sd.b0 = 2 * nw * blockIdx.x;  // first sample of this CTA
+  float* ring = reinterpret_cast<float*>(smem_raw + A.geo.ring_off);
+  Sd.zb = ring + (size_t)A.geo.R * A.geo.slot_floats;
   if (threadIdx.x == 0) {
     for (int r = 0; r < A.geo.R; ++r) {
       mbar_init(&full[r], 1);
       mbar_init(&empty[r], nw);
     }
+    for (int p = 0; p < 2; ++p) {
+      mbar_init(&Sd.zdone[p], nw);
+      mbar_init(&Sd.zfree[p], kHeadEmitWarps);
+    }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  const int cta_b0 = Sd.b0;
 
   if (warp == nw) {  // ---------------- producer warp ----------------
     if (lane == 0) {
       int slot = 0, use = 0;
       for (int g = 0; g < A.geo.ngroups; ++g) {
         if (use > 0) mbar_wait_sleep(&empty[slot], (use - 1) & 1);
-        const int i0 = g * G, i1 = min(Hd, i0 + G);
+        const int i0 = g * G, i1 = i0 + G;  // rows are padded to a multiple of G = 8 (zero rows)
         // every row of the slot belongs to word i0 / 32 (G divides 32): copy its staged length only
         const uint32_t rb = (uint32_t)head_row_floats(KPL, i0 >> 5) * 4u;
         float* dst = ring + (size_t)slot * A.geo.slot_floats;
@@ -624,11 +620,53 @@ __global__ void __launch_bounds__(32 * 5) head_v3_kernel(const __grid_constant__
     }
     return;
   }
+  if (warp > nw) {  // ---------------- emit warps ----------------
+    const int e = warp - nw - 1;
+    double lp[8 / kHeadEmitWarps];
+#pragma unroll
+    for (int j = 0; j < 8 / kHeadEmitWarps; ++j) lp[j] = 0.0;
+    for (int m = 0; m < nwords; ++m) {
+      const int p = m & 1;
+      mbar_wait_sleep(&Sd.zdone[p], (m >> 1) & 1);
+      const int ib = 32 * m + lane;
+#pragma unroll
+      for (int j = 0; j < 8 / kHeadEmitWarps; ++j) {
+        const int sidx = e + kHeadEmitWarps * j;
+        if (sidx < 2 * nw) {
+          const int b = cta_b0 + sidx;
+          const float* zrow = Sd.zb + ((size_t)(p * 8 + sidx) * 2) * 32;
+          const float z = zrow[lane], z1 = zrow[32 + lane];
+          const bool mine = b < A.B && ib < Hd;
+          const float t = mine ? A.thr[(size_t)b * Sd.Hd8 + ib] : INFINITY;
+          const int x = (t < z) ? 1 : 0;  // the consumer's draw, recomputed exactly
+          if (mine)
+            lp[j] += head_emit(b, ib, z, z1, x, A.n, A.h, A.hp, A.np, A.hd1p, A.G1, A.G1h, A.G1l, A.Dh, A.Dl, A.Xf,
+                               A.cond);
+          const uint32_t word = __ballot_sync(kFull, mine && x);
+          if (!GIVEN && b < A.B && lane == 0) A.X[(size_t)b * A.W + m] = word;
+        }
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&Sd.zfree[p]);
+    }
+#pragma unroll
+    for (int j = 0; j < 8 / kHeadEmitWarps; ++j) {
+      const int sidx = e + kHeadEmitWarps * j;
+      if (sidx < 2 * nw) {
+        double v = lp[j];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        const int b = cta_b0 + sidx;
+        if (b < A.B && lane == 0) {
+          A.lp_head[b] = v;
+          A.Xf[(size_t)b * A.hd1p + Hd] = __float2bfloat16_rn(1.f);  // ones column: gb1 = 1^T dz1
+        }
+      }
+    }
+    return;
+  }
 
   // ---------------- consumer warps: samples 2 w and 2 w + 1 ----------------
-  const int bw = 2 * (blockIdx.x * nw + warp);
-  const int bs[2] = {bw, bw + 1};
-  const bool act[2] = {bw < A.B, bw + 1 < A.B};
   HeadV3State<KG> S;
 #pragma unroll
   for (int t = 0; t < KPL; ++t) {
@@ -637,17 +675,6 @@ __global__ void __launch_bounds__(32 * 5) head_v3_kernel(const __grid_constant__
     for (int a = 0; a < 2; ++a) {
       S.z1[a][t] = k < A.h ? A.b1[k] : 0.f;
       S.z2[a][t] = k < Hd ? A.b2[k] : 0.f;
-    }
-  }
-  const int nwords = (Hd + 31) >> 5;
-#pragma unroll
-  for (int a = 0; a < 2; ++a) {
-    S.lp[a] = 0.0;
-    S.thr_next[a] = 0.f;
-    S.xin_next[a] = 0;
-    if (act[a] && lane < Hd) {
-      if (GIVEN) S.xin_next[a] = (A.X[(size_t)bs[a] * A.W] >> lane) & 1;
-      else S.thr_next[a] = head_threshold(A.uni, A.rng, A.B, bs[a], lane);
     }
   }
   S.slot = 0;
@@ -661,27 +688,20 @@ __global__ void __launch_bounds__(32 * 5) head_v3_kernel(const __grid_constant__
     S.wb1[q] = make_float4(0.f, 0.f, 0.f, 0.f);  // "pending" rows of the first bit (0 x 0, never NaN)
     S.wb2[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
-  const HeadRing Rg{full, empty, ring, G, A.geo.R, A.geo.slot_floats, Hd};
+#pragma unroll
+  for (int a = 0; a < 2; ++a) S.thr_next[a] = A.thr[(size_t)(cta_b0 + 2 * warp + a) * Sd.Hd8 + lane];
+  const HeadRing Rg{full, empty, ring, G, A.geo.R, A.geo.slot_floats, Hd, (Hd + 7) & ~7};
 #ifdef VQMC_HEAD_PROF
   const long long tstart = clock64();
 #endif
-  head_v3_phases<KG, 0, GIVEN>(S, A, Rg, lane, bs, act, nwords);
+  head_v3_phases<KG, 0, GIVEN>(S, Rg, Sd, lane, warp, nwords);
 #ifdef VQMC_HEAD_PROF
-  if (lane == 0 && (blockIdx.x % 32) == 0)
-    printf("HEADPROF block %d warp %d total %lld wait_full %lld\n", blockIdx.x, warp, clock64() - tstart, S.wait_cycles);
+  if (lane == 0 && (blockIdx.x % 64) == 0 && warp == 0)
+    printf("HEADPROF block %d warp %d total %lld\n", blockIdx.x, warp, clock64() - tstart);
 #endif
   // the last slot
   __syncwarp();
   if (lane == 0) mbar_arrive(&empty[S.slot]);
-#pragma unroll
-  for (int a = 0; a < 2; ++a) {
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) S.lp[a] += __shfl_xor_sync(kFull, S.lp[a], o);
-    if (act[a] && lane == 0) {
-      A.lp_head[bs[a]] = S.lp[a];
-      A.Xf[(size_t)bs[a] * A.hd1p + Hd] = __float2bfloat16_rn(1.f);  // ones column: gb1 = 1^T dz1
-    }
-  }
 }
 
 // Padded, completion-ordered copies of the head blocks (refreshed after every update):
@@ -796,18 +816,26 @@ static HeadGeom head_v3_geometry(const Handle* H) {
   const Layout& L = H->L;
   HeadGeom g{};
   const int RS = H->head_hpk;  // 128 * KG
-  g.R = 6;
+  const int nwords = (L.Hd + 31) / 32;
   g.hp = RS;
   g.Hdp = RS;
   g.cmax = 1;
-  for (int G = 8; G >= 1; G >>= 1) {
-    g.G = G;
-    g.slot_floats = 2 * G * RS;
-    g.smem = 256 + (size_t)g.R * g.slot_floats * 4;
-    if (g.smem <= 225 * 1024) break;
-    if (G == 1) throw InvalidArgument("head sampler shared-memory ring does not fit (hidden width too large)");
+  g.G = 8;  // one ring slot = 8 bits (the unrolled group)
+  g.slot_floats = 2 * g.G * RS;
+  g.ring_off = 256;  // full[R] + empty[R] + zdone[2] + zfree[2] mbarriers (<= 16)
+  const size_t side = (size_t)2 * 8 * 2 * 32 * 4;  // (z2, z1) hand-off to the emit warps
+  (void)nwords;
+  const size_t limit = 227 * 1024;
+  g.R = 0;
+  for (int R = 6; R >= 2; --R) {
+    g.smem = g.ring_off + (size_t)R * g.slot_floats * 4 + side;
+    if (g.smem <= limit) {
+      g.R = R;
+      break;
+    }
   }
-  g.ngroups = (L.Hd + g.G - 1) / g.G;
+  if (!g.R) throw InvalidArgument("head sampler shared-memory ring does not fit (hidden width too large)");
+  g.ngroups = (L.Hd + g.G - 1) / g.G;  // rows padded to Hd8 = 8 ngroups
   return g;
 }
 
@@ -824,13 +852,23 @@ static void head_v3_launch(Handle* H, int B, const double* uni, RngSpec rng, dou
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, H->device);
   const int pairs = (B + 1) / 2;
-  const int nw = std::max(1, std::min(4, (pairs + dev_sms - 1) / dev_sms));  // <= 4 sample-pair warps + producer
+  // <= 4 sample-pair warps + producer + threshold + emit warps
+  const int nw = std::max(1, std::min(4, (pairs + dev_sms - 1) / dev_sms));
   const int grid = (pairs + nw - 1) / nw;
+  const int Hd8 = (L.Hd + 7) & ~7;
+  {
+    KScope ks(H, "head_thresholds");
+    const int64_t total = (int64_t)B * (Hd8 / 4);
+    head_thresholds_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.Hd, Hd8, L.W, uni, rng, H->X,
+                                                                                   GIVEN ? 1 : 0, H->thr);
+    VQMC_CUDA(cudaGetLastError());
+    H->launches++;
+  }
   KScope ks(H, GIVEN ? "head_given" : "head_sample");
   const HeadV3Args args{B,      L.n,     L.h,    L.W,    geo,     H->W1Tp,  H->W2cp, H->P + L.off_b1,
                         H->P + L.off_b2, uni, rng, H->X, H->G1, H->G1h, H->G1l, H->hp18, H->Dh, H->Dl, H->np8,
-                        H->Xfb, H->hd18, H->lp_head, cond};
-  head_v3_kernel<KG, GIVEN><<<grid, 32 * (nw + 1), geo.smem, H->stream>>>(args);
+                        H->Xfb, H->hd18, H->lp_head, cond, H->thr};
+  head_v3_kernel<KG, GIVEN><<<grid, 32 * (nw + 1 + kHeadEmitWarps), geo.smem, H->stream>>>(args);
   VQMC_CUDA(cudaGetLastError());
   H->launches++;
 }

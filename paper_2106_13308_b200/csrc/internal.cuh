@@ -159,6 +159,7 @@ struct Handle {
   __half* wG1h = nullptr;    // [B][hp18] fp16 pair of [w' (.) G1 | w'] (gW2 B operand)
   __half* wG1l = nullptr;
   double* lp_head = nullptr; // [B]
+  float* thr = nullptr;      // [B][Hd8] logit thresholds of the head bits (head v3)
   double* lp_part = nullptr; // [max_tiles][B]
   double* log_psi = nullptr; // [B]
   int32_t* cut = nullptr;    // [B]
