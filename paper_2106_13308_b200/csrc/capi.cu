@@ -281,7 +281,9 @@ static void upload_edges(Handle* H, const int32_t* edges, int64_t num_edges) {
   H->d_edges = nullptr;
   H->num_edges = num_edges;
   if (num_edges > 0) {
-    VQMC_CUDA(cudaMalloc((void**)&H->d_edges, num_edges * sizeof(int2)));
+    // (+2 entries: the energy kernel's bulk copies round a chunk up to an even edge count)
+    VQMC_CUDA(cudaMalloc((void**)&H->d_edges, (num_edges + 2) * sizeof(int2)));
+    VQMC_CUDA(cudaMemset(H->d_edges, 0, (num_edges + 2) * sizeof(int2)));
     VQMC_CUDA(cudaMemcpy(H->d_edges, edges, num_edges * sizeof(int2), cudaMemcpyHostToDevice));
   }
 }
@@ -533,12 +535,12 @@ int vqmc_gpu_maxcut_energy(vqmc_gpu_t* g, const uint32_t* bits, int B, int32_t* 
   H->ensure_batch(B);
   upload_bits(H, bits, B);
   launch_energy(H, B);
-  if (cut_out)
-    VQMC_CUDA(cudaMemcpyAsync(cut_out, H->cut, (size_t)B * sizeof(int32_t), cudaMemcpyDeviceToHost, H->stream));
-  if (local_out)
-    VQMC_CUDA(cudaMemcpyAsync(local_out, H->local, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost,
-                              H->stream));
+  std::vector<int32_t> cuts((size_t)B);
+  VQMC_CUDA(cudaMemcpyAsync(cuts.data(), H->cut, (size_t)B * sizeof(int32_t), cudaMemcpyDeviceToHost, H->stream));
   VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  if (cut_out) std::memcpy(cut_out, cuts.data(), (size_t)B * sizeof(int32_t));
+  if (local_out)  // l_b = (|E| - 2 cut_b) / 4 (exact in fp64), as the device statistics use it
+    for (int b = 0; b < B; ++b) local_out[b] = 0.25 * ((double)H->num_edges - 2.0 * (double)cuts[b]);
   API_CATCH
 }
 

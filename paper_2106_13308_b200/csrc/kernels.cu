@@ -145,6 +145,96 @@ __global__ void __launch_bounds__(256) energy_kernel(int B, int W, int64_t nE,
 }
 
 // ===========================================================================
+// Max-Cut cuts, bit-sliced over samples (the default path).  A CTA takes 32 samples and a
+// chunk of the edge list.  It transposes the samples' packed spins in shared memory so that
+// T[i] holds node i of all 32 samples (bit s = x_{s,i}); an edge then costs one XOR of two
+// words, a 32-sample mask of "cut" bits, added into 8 bit-sliced counter planes (a ripple
+// carry over the planes: <= 255 edges per thread).  Per-sample counts come back with one
+// 32 x 32 bit transpose per plane and popc; CTAs add them to cut[] with integer atomics
+// (exact and order-independent).  hamiltonian.cpp:61-69,121-124 with beta_ij = -1/4.
+// ===========================================================================
+__device__ __forceinline__ uint32_t transpose32_lane(uint32_t v, int lane) {
+  // lane r holds row r (bit c = M[r][c]); returns column `lane` (bit r = M[r][lane])
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const int j = 16 >> t;
+    const uint32_t m = masks[t];
+    const uint32_t o = __shfl_xor_sync(kFull, v, j);
+    v = (lane & j) ? ((v & ~m) | ((o & ~m) >> j)) : ((v & m) | ((o & m) << j));
+  }
+  return v;
+}
+
+// Shared memory: T [32 W] transposed words | S [32 W] staged rows | E [per_chunk + 1] edges.
+// The rows and the edge chunk arrive by bulk copies (TMA) on two mbarriers; the transpose
+// overlaps the edge copy.
+__global__ void __launch_bounds__(256) maxcut_cut_kernel(int B, int n, int W, int64_t nE, int64_t per_chunk,
+                                                         const int2* __restrict__ edges,
+                                                         const uint32_t* __restrict__ X, int32_t* __restrict__ cut) {
+  extern __shared__ __align__(16) uint32_t smem_words[];
+  uint32_t* T = smem_words;               // [32 W]: node-major words of the CTA's 32 samples
+  uint32_t* S = smem_words + 32 * W;      // [32][W]: the samples' packed rows (staging)
+  int2* E = reinterpret_cast<int2*>(smem_words + ((64 * W + 3) & ~3));  // the edge chunk
+  __shared__ int scnt[32];
+  __shared__ __align__(8) uint64_t bar[2];
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
+  const int s0 = 32 * blockIdx.y;
+  const int rows = min(32, B - s0);
+  const int64_t e0 = (int64_t)blockIdx.x * per_chunk, e1 = min(nE, e0 + per_chunk);
+  const int ne = (int)(e1 - e0);
+  if (threadIdx.x == 0) {
+    ptx::mbar_init(&bar[0], 1);
+    ptx::mbar_init(&bar[1], 1);
+    ptx::fence_mbar_init();
+  }
+  if (threadIdx.x < 32) scnt[threadIdx.x] = 0;
+  __syncthreads();
+  const bool bulk_rows = rows == 32;  // whole group: 128 W bytes, 16-byte aligned
+  if (threadIdx.x == 0) {
+    if (bulk_rows) {
+      ptx::mbar_expect_tx(&bar[0], 128u * (uint32_t)W);
+      ptx::bulk_g2s(S, X + (size_t)s0 * W, 128u * (uint32_t)W, &bar[0]);
+    }
+    if (ne > 0) {
+      const uint32_t eb = (uint32_t)((ne + 1) & ~1) * 8u;  // even count: 16-byte multiple (array padded)
+      ptx::mbar_expect_tx(&bar[1], eb);
+      ptx::bulk_g2s(E, edges + e0, eb, &bar[1]);
+    }
+  }
+  if (!bulk_rows) {  // ragged last group
+    for (int t = threadIdx.x; t < 32 * W; t += blockDim.x) S[t] = t < rows * W ? X[(size_t)s0 * W + t] : 0u;
+    __syncthreads();
+  } else {
+    ptx::mbar_wait(&bar[0], 0);
+  }
+  for (int w = warp; w < W; w += nwarps)  // (row stride W: odd W reads conflict-free columns)
+    T[32 * w + lane] = transpose32_lane(S[lane * W + w], lane);  // node 32 w + lane
+  __syncthreads();
+  uint32_t c[8];
+#pragma unroll
+  for (int k = 0; k < 8; ++k) c[k] = 0u;
+  if (ne > 0) ptx::mbar_wait(&bar[1], 0);
+  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
+    const int2 ed = E[e];
+    uint32_t carry = T[ed.x] ^ T[ed.y];  // samples in which edge (i, j) is cut
+#pragma unroll
+    for (int k = 0; k < 8; ++k) {
+      const uint32_t t = c[k] & carry;
+      c[k] ^= carry;
+      carry = t;
+    }
+  }
+  // per-sample counts of this warp: transpose each plane (lane s <- sample s), popc, weight 2^k
+  int cnt = 0;
+#pragma unroll
+  for (int k = 0; k < 8; ++k) cnt += __popc(transpose32_lane(c[k], lane)) << k;
+  atomicAdd(&scnt[lane], cnt);
+  __syncthreads();
+  if (threadIdx.x < 32 && s0 + threadIdx.x < B && scnt[threadIdx.x]) atomicAdd(&cut[s0 + threadIdx.x], scnt[threadIdx.x]);
+}
+
+// ===========================================================================
 // In-batch statistics and REINFORCE weights, one CTA looping over the worker
 // segments of `seg` rows (deterministic order): mean over the segment
 // (estimator.hpp:115, the per-worker baseline), w_b = 2 (l_b - mean) / seg
@@ -154,7 +244,7 @@ __global__ void __launch_bounds__(256) energy_kernel(int B, int W, int64_t nE,
 // (exact), so the fp16-pair backward operands w' G1 cannot overflow; the
 // backward epilogues multiply by wscale.
 // ===========================================================================
-__global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, const double* __restrict__ local,
+__global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, int64_t nE, double* __restrict__ local,
                                                              const int32_t* __restrict__ cut,
                                                              float* __restrict__ w, float* __restrict__ wscale,
                                                              int64_t* __restrict__ istat) {
@@ -171,7 +261,9 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
     long long cs = 0, cq = 0;
     int cm = 0;
     for (int b = tid; b < seg; b += blockDim.x) {
-      s += local[base + b];
+      const double lb = 0.25 * ((double)nE - 2.0 * (double)cut[base + b]);  // l_b = (|E| - 2 cut_b) / 4, exact
+      local[base + b] = lb;
+      s += lb;
       const long long c = cut[base + b];
       cs += c;
       cq += c * c;
@@ -466,8 +558,35 @@ void launch_finalize_logpsi(Handle* H, int B, int tiles) {
 }
 
 void launch_energy(Handle* H, int B) {
-  constexpr int S = 4;
   const int W = H->L.W;
+  const size_t tsm = (size_t)((64 * W + 3) & ~3) * sizeof(uint32_t);  // T + S
+  const size_t cap = 200 * 1024;
+  if (tsm + 256 * 8 <= cap) {  // bit-sliced path (n <= ~25,000)
+    const int groups = (B + 31) / 32;
+    const int64_t nE = H->num_edges;
+    // chunk: fits the remaining shared memory, <= 255 edges per thread (8 counter planes);
+    // split further while there are fewer than ~148 CTAs and >= 8 edges per thread remain
+    const int64_t per_max = std::min<int64_t>(255 * 256, (int64_t)((cap - tsm) / 8) - 2);
+    int64_t chunks = std::max<int64_t>(1, (nE + per_max - 1) / per_max);
+    while (chunks * groups < 148 && (nE + 2 * chunks - 1) / (2 * chunks) >= 256 * 8) chunks *= 2;
+    int64_t per = std::max<int64_t>(2, (nE + chunks - 1) / chunks);
+    per = (per + 1) & ~int64_t(1);  // even: the bulk copies start 16-byte aligned
+    chunks = std::max<int64_t>(1, (nE + per - 1) / per);
+    const size_t smem = tsm + (size_t)(per + 2) * 8;
+    static size_t attr = 0;
+    if (smem > 48 * 1024 && attr < smem) {
+      VQMC_CUDA(cudaFuncSetAttribute(maxcut_cut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
+      attr = cap;
+    }
+    KScope ks(H, "maxcut_energy");
+    VQMC_CUDA(cudaMemsetAsync(H->cut, 0, (size_t)B * sizeof(int32_t), H->stream));
+    maxcut_cut_kernel<<<dim3((unsigned)chunks, (unsigned)groups), 256, smem, H->stream>>>(B, H->L.n, W, nE, per,
+                                                                                         H->d_edges, H->X, H->cut);
+    LAUNCH_CHECK();
+    H->launches++;
+    return;
+  }
+  constexpr int S = 4;
   const size_t smem = (size_t)S * W * sizeof(uint32_t);
   if (smem > 48 * 1024)
     VQMC_CUDA(cudaFuncSetAttribute(energy_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -481,7 +600,8 @@ void launch_energy(Handle* H, int B) {
 
 void launch_weights_from_locals(Handle* H, int B, int seg) {
   KScope ks(H, "stats_weights");
-  stats_weights_kernel<<<1, 1024, 0, H->stream>>>(B / seg, seg, H->local, H->cut, H->w, H->d_wscale, H->d_istat);
+  stats_weights_kernel<<<1, 1024, 0, H->stream>>>(B / seg, seg, H->num_edges, H->local, H->cut, H->w, H->d_wscale,
+                                                   H->d_istat);
   LAUNCH_CHECK();
   H->launches++;
 }
