@@ -124,6 +124,14 @@ void Handle::ensure_uniforms(int64_t count) {
   uni_cap = count;
 }
 
+void Handle::ensure_cpart(int64_t count) {
+  if (count <= cpart_cap) return;
+  if (capturing) throw std::runtime_error("cpart reallocation during graph capture");
+  invalidate_graph();
+  dalloc(&cpart, (size_t)count);
+  cpart_cap = count;
+}
+
 void Handle::ensure_cond(int64_t count) {
   if (count <= cond_cap) return;
   dalloc(&cond, (size_t)count);
@@ -432,7 +440,7 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   if (H->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy(H->nccl_comm);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2h, H->W2l, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
-                  H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->local, H->w, H->d_wscale, H->d_flag,
+                  H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->cpart, H->local, H->w, H->d_wscale, H->d_flag,
                   H->Epart, H->dz1bh, H->dz1bl, H->Xfb, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat,
                   H->d_gpart, H->d_step, H->d_done, H->d_comp_pos};
   for (void* p : ptrs)
@@ -535,6 +543,7 @@ int vqmc_gpu_maxcut_energy(vqmc_gpu_t* g, const uint32_t* bits, int B, int32_t* 
   H->ensure_batch(B);
   upload_bits(H, bits, B);
   launch_energy(H, B);
+  launch_cuts_reduce(H, B);
   std::vector<int32_t> cuts((size_t)B);
   VQMC_CUDA(cudaMemcpyAsync(cuts.data(), H->cut, (size_t)B * sizeof(int32_t), cudaMemcpyDeviceToHost, H->stream));
   VQMC_CUDA(cudaStreamSynchronize(H->stream));
@@ -669,13 +678,12 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
   H->kt_count = 0;
   const bool tm = H->phase_timing >= 2, t0 = H->phase_timing >= 1;
   if (t0) record_event(H, H->ev[0]);
-  launch_step_advance(H);
   sample_into(H, B, workers, uniforms, seed, stream0, 0, /*device_call=*/true, /*want_log_psi=*/false);
   if (tm) record_event(H, H->ev[1]);
-  launch_energy(H, B);                          // local_energy_batch (:161)
-  launch_weights_from_locals(H, B, minibatch);  // gradient_from_locals weights (:164)
+  launch_energy(H, B);                                // local_energy_batch (:161)
+  launch_weights_from_locals(H, B, minibatch, true);  // gradient_from_locals weights (:164) + w' G1 operand
   if (tm) record_event(H, H->ev[2]);
-  launch_backward(H, B);  // weighted_grad_log_psi
+  launch_backward(H, B, /*wg1_done=*/true);  // weighted_grad_log_psi
   if (tm) record_event(H, H->ev[3]);
   if (H->nccl_comm) {  // allreduce_mean (:187): sum here, / L in Adam
     KScope ks(H, "nccl_allreduce");
@@ -705,10 +713,10 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
   H->ensure_batch(B);
   if (workers > H->istat_cap) H->invalidate_graph();
   ensure_istat(H, workers);
-  // device step counters: the step's first kernel turns (call - 1, t - 1) into (call, t)
+  // device step counters describe the step about to run; Adam advances them at the step's end
   if (call != H->next_call || t != H->next_t || lr != H->cur_lr || beta1 != H->cur_b1 || beta2 != H->cur_b2 ||
       eps != H->cur_eps) {
-    launch_set_step(H, call - 1, t - 1, lr, beta1, beta2, eps);
+    launch_set_step(H, call, t, lr, beta1, beta2, eps);
     H->cur_lr = lr;
     H->cur_b1 = beta1;
     H->cur_b2 = beta2;

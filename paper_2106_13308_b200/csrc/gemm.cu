@@ -381,9 +381,9 @@ void launch_dg1_umma(Handle* H, int B) {
                                                             e, H->stream);
 }
 
-void launch_gw2_umma(Handle* H, int B) {  // BN = 128: 3-stage ring, 4 column tiles of h + 1
+void launch_gw2_umma(Handle* H, int B, bool wg1_done) {  // BN = 128: 3-stage ring, 4 column tiles of h + 1
   const Layout& L = H->L;
-  {
+  if (!wg1_done) {  // (the training step fuses this split into the statistics kernel)
     const int64_t total = (int64_t)B * H->hp18;
     KScope ks(H, "wg1_split");
     wg1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp18, H->G1, H->w, H->wG1h,

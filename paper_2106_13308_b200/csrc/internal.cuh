@@ -76,10 +76,11 @@ struct RngSpec;
 void record_event(Handle* h, cudaEvent_t ev);
 
 // Per-step scalars kept in device memory so a captured CUDA graph of the step can be replayed:
-// the graph's first kernel advances call/t and the Adam bias corrections.
+// they describe the step about to run; the step's last kernel (Adam) advances call / t and the
+// Adam bias corrections for the next one.
 struct StepParams {
   uint64_t call;  // Philox counter of this step
-  int64_t t;      // Adam step count after the increment
+  int64_t t;      // Adam step count of this step (1-based)
   float lr, b1, b2, eps;
   float bc1, bc2;  // 1 - beta^t
 };
@@ -101,17 +102,17 @@ void launch_z2(Handle* h, int B, int col0, const double* d_uniforms, RngSpec rng
                bool given_bits, double* d_cond, bool want_lp = true);
 void launch_finalize_logpsi(Handle* h, int B, int n_tiles);
 void launch_energy(Handle* h, int B);
-void launch_weights_from_locals(Handle* h, int B, int seg);
-void launch_backward(Handle* h, int B);
+void launch_weights_from_locals(Handle* h, int B, int seg, bool with_wg1 = false);
+void launch_cuts_reduce(Handle* h, int B);
+void launch_backward(Handle* h, int B, bool wg1_done = false);
 void launch_tail_umma(Handle* h, int B, const double* d_uniforms, RngSpec rng, bool want_lp);
 void launch_dg1_umma(Handle* h, int B);
-void launch_gw2_umma(Handle* h, int B);
+void launch_gw2_umma(Handle* h, int B, bool wg1_done = false);
 void launch_split_w2(Handle* h);
 void launch_gw1_umma(Handle* h, int B, int& splits_out);
 void set_error(const std::string& msg);
 int status_of(const std::exception& ex);
 void launch_adam(Handle* h, float grad_scale);  // hyper-parameters from h->d_step
-void launch_step_advance(Handle* h);
 void launch_set_step(Handle* h, uint64_t call, int64_t t, double lr, double b1, double b2, double eps);
 
 struct Handle {
@@ -163,6 +164,9 @@ struct Handle {
   double* lp_part = nullptr; // [max_tiles][B]
   double* log_psi = nullptr; // [B]
   int32_t* cut = nullptr;    // [B]
+  int32_t* cpart = nullptr;  // [cut_chunks][B] per-edge-chunk partial cut counts (energy kernel)
+  int cut_chunks = 1;
+  int64_t cpart_cap = 0;
   double* local = nullptr;   // [B]
   float* w = nullptr;        // [B] REINFORCE weights w' = w / wscale (|w'| <= 1, fp16-safe)
   float* d_wscale = nullptr; // [1] wscale: power of two >= max |w| (the backward epilogues multiply by it)
@@ -224,6 +228,7 @@ struct Handle {
   void ensure_batch(int B);
   void ensure_uniforms(int64_t count);
   void ensure_cond(int64_t count);
+  void ensure_cpart(int64_t count);
 };
 
 }  // namespace vqmc_b200

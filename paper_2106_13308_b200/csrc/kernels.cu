@@ -171,7 +171,7 @@ __device__ __forceinline__ uint32_t transpose32_lane(uint32_t v, int lane) {
 // overlaps the edge copy.
 __global__ void __launch_bounds__(256) maxcut_cut_kernel(int B, int n, int W, int64_t nE, int64_t per_chunk,
                                                          const int2* __restrict__ edges,
-                                                         const uint32_t* __restrict__ X, int32_t* __restrict__ cut) {
+                                                         const uint32_t* __restrict__ X, int32_t* __restrict__ cpart) {
   extern __shared__ __align__(16) uint32_t smem_words[];
   uint32_t* T = smem_words;               // [32 W]: node-major words of the CTA's 32 samples
   uint32_t* S = smem_words + 32 * W;      // [32][W]: the samples' packed rows (staging)
@@ -231,29 +231,36 @@ __global__ void __launch_bounds__(256) maxcut_cut_kernel(int B, int n, int W, in
   for (int k = 0; k < 8; ++k) cnt += __popc(transpose32_lane(c[k], lane)) << k;
   atomicAdd(&scnt[lane], cnt);
   __syncthreads();
-  if (threadIdx.x < 32 && s0 + threadIdx.x < B && scnt[threadIdx.x]) atomicAdd(&cut[s0 + threadIdx.x], scnt[threadIdx.x]);
+  if (threadIdx.x < 32 && s0 + threadIdx.x < B) cpart[(size_t)blockIdx.x * B + s0 + threadIdx.x] = scnt[threadIdx.x];
 }
 
 // ===========================================================================
-// In-batch statistics and REINFORCE weights, one CTA looping over the worker
-// segments of `seg` rows (deterministic order): mean over the segment
-// (estimator.hpp:115, the per-worker baseline), w_b = 2 (l_b - mean) / seg
-// (estimator.hpp:116-117), and the segment's exact cut sums (pooled statistics
-// are formed from these integers on the host, trainer.cpp:246-248).  The weights
-// are stored normalised, w' = w / wscale with wscale the power of two >= max |w|
-// (exact), so the fp16-pair backward operands w' G1 cannot overflow; the
-// backward epilogues multiply by wscale.
+// In-batch statistics and REINFORCE weights, fused with the wG1 operand of the gW2 GEMM.
+// Every CTA computes, over the worker segments of `seg` rows in a fixed order: cut_b (the sum
+// of the energy kernel's per-chunk partial counts), l_b = (|E| - 2 cut_b) / 4 (exact), the
+// segment mean (estimator.hpp:115, the per-worker baseline) and w_b = 2 (l_b - mean) / seg
+// (estimator.hpp:116-117), stored normalised as w' = w / wscale with wscale the power of two
+// >= max |w| (exact), so the fp16-pair operand w' G1 cannot overflow (the backward epilogues
+// multiply by wscale).  CTA 0 also writes cut, l, w', wscale and the segments' exact integer
+// cut sums (pooled statistics are formed from these on the host, trainer.cpp:246-248).  Then
+// the grid writes wG1 = fp16 pair of [w' G1 | w'] (skipped when G1 is null).
 // ===========================================================================
-__global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, int64_t nE, double* __restrict__ local,
-                                                             const int32_t* __restrict__ cut,
+__global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, int chunks, int64_t nE,
+                                                             const int32_t* __restrict__ cpart,
+                                                             int32_t* __restrict__ cut, double* __restrict__ local,
                                                              float* __restrict__ w, float* __restrict__ wscale,
-                                                             int64_t* __restrict__ istat) {
+                                                             int64_t* __restrict__ istat, int h, int ld,
+                                                             const float* __restrict__ G1, __half* __restrict__ wgh,
+                                                             __half* __restrict__ wgl) {
+  extern __shared__ float sw[];  // [B] weights of the whole batch (per CTA)
   __shared__ double sd[32];
   __shared__ long long si[32], sq[32];
   __shared__ int sm[32];
-  __shared__ float sw[32];
+  __shared__ float smax[32];
   __shared__ double smean;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  const int B = segs * seg;
+  const bool lead = blockIdx.x == 0;
   float wmax = 0.f;
   for (int sgi = 0; sgi < segs; ++sgi) {
     const int base = sgi * seg;
@@ -261,13 +268,17 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
     long long cs = 0, cq = 0;
     int cm = 0;
     for (int b = tid; b < seg; b += blockDim.x) {
-      const double lb = 0.25 * ((double)nE - 2.0 * (double)cut[base + b]);  // l_b = (|E| - 2 cut_b) / 4, exact
-      local[base + b] = lb;
+      int c = 0;
+      for (int k = 0; k < chunks; ++k) c += cpart[(size_t)k * B + base + b];
+      const double lb = 0.25 * ((double)nE - 2.0 * (double)c);  // l_b = (|E| - 2 cut_b) / 4, exact
+      if (lead) {
+        cut[base + b] = c;
+        local[base + b] = lb;
+      }
       s += lb;
-      const long long c = cut[base + b];
       cs += c;
-      cq += c * c;
-      cm = max(cm, (int)c);
+      cq += (long long)c * c;
+      cm = max(cm, c);
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -284,33 +295,49 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
       int mx = 0;
       for (int i = 0; i < nw; ++i) { t += sd[i]; a += si[i]; q += sq[i]; mx = max(mx, sm[i]); }
       smean = t / (double)seg;
-      istat[3 * sgi + 0] = a;
-      istat[3 * sgi + 1] = q;
-      istat[3 * sgi + 2] = mx;
+      if (lead) {
+        istat[3 * sgi + 0] = a;
+        istat[3 * sgi + 1] = q;
+        istat[3 * sgi + 2] = mx;
+      }
     }
     __syncthreads();
     const double mean = smean;
     for (int b = tid; b < seg; b += blockDim.x) {
-      const float wb = (float)(2.0 * (local[base + b] - mean) / (double)seg);
-      w[base + b] = wb;
+      int c = 0;
+      for (int k = 0; k < chunks; ++k) c += cpart[(size_t)k * B + base + b];
+      const double lb = 0.25 * ((double)nE - 2.0 * (double)c);
+      const float wb = (float)(2.0 * (lb - mean) / (double)seg);
+      sw[base + b] = wb;
       wmax = fmaxf(wmax, fabsf(wb));
     }
     __syncthreads();  // smean / partials are reused by the next segment
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(kFull, wmax, o));
-  if (lane == 0) sw[warp] = wmax;
+  if (lane == 0) smax[warp] = wmax;
   __syncthreads();
   float m = 0.f;
-  for (int i = 0; i < nw; ++i) m = fmaxf(m, sw[i]);
+  for (int i = 0; i < nw; ++i) m = fmaxf(m, smax[i]);
   // wscale = 2^e >= m (1 when every weight is 0); w' = w * 2^-e exactly
   int e = 0;
-  if (m > 0.f) {
-    frexpf(m, &e);  // m = f 2^e, f in [0.5, 1)
-  }
+  if (m > 0.f) frexpf(m, &e);  // m = f 2^e, f in [0.5, 1)
   const float sc = ldexpf(1.f, e), inv = ldexpf(1.f, -e);
-  if (tid == 0) *wscale = sc;
-  for (int b = tid; b < segs * seg; b += blockDim.x) w[b] *= inv;
+  for (int b = tid; b < B; b += blockDim.x) {
+    const float wn = sw[b] * inv;
+    sw[b] = wn;
+    if (lead) w[b] = wn;
+  }
+  if (lead && tid == 0) *wscale = sc;
+  if (G1 == nullptr) return;
+  __syncthreads();
+  // wG1[b][k] = w'_b G1[b][k] (k < h), w'_b (k == h), 0 beyond; fp16 pair (gW2 B operand)
+  const int64_t total = (int64_t)B * ld;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + tid; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const int b = (int)(t / ld), k = (int)(t % ld);
+    const float x = k < h ? sw[b] * G1[(size_t)b * h + k] : (k == h ? sw[b] : 0.f);
+    ptx::split_f16(x, wgh[t], wgl[t]);
+  }
 }
 
 // ===========================================================================
@@ -485,6 +512,13 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, c
     for (unsigned i = 0; i < gridDim.x; ++i) s += ((volatile double*)gpart)[i];
     *gnorm2 = s;
     *done = 0u;
+    // advance the device step counters for the next step (every other block has read them):
+    // Philox call + 1, Adam t + 1 and its bias corrections (optimizer.cpp:28-29)
+    StepParams* w = const_cast<StepParams*>(sp);
+    w->call += 1;
+    w->t += 1;
+    w->bc1 = (float)(1.0 - pow((double)w->b1, (double)w->t));
+    w->bc2 = (float)(1.0 - pow((double)w->b2, (double)w->t));
   }
 }
 
@@ -578,10 +612,11 @@ void launch_energy(Handle* H, int B) {
       VQMC_CUDA(cudaFuncSetAttribute(maxcut_cut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
       attr = cap;
     }
+    H->ensure_cpart((int)chunks * B);
+    H->cut_chunks = (int)chunks;
     KScope ks(H, "maxcut_energy");
-    VQMC_CUDA(cudaMemsetAsync(H->cut, 0, (size_t)B * sizeof(int32_t), H->stream));
     maxcut_cut_kernel<<<dim3((unsigned)chunks, (unsigned)groups), 256, smem, H->stream>>>(B, H->L.n, W, nE, per,
-                                                                                         H->d_edges, H->X, H->cut);
+                                                                                         H->d_edges, H->X, H->cpart);
     LAUNCH_CHECK();
     H->launches++;
     return;
@@ -591,22 +626,48 @@ void launch_energy(Handle* H, int B) {
   if (smem > 48 * 1024)
     VQMC_CUDA(cudaFuncSetAttribute(energy_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                    (int)smem));
+  H->ensure_cpart(B);
+  H->cut_chunks = 1;
   KScope ks(H, "maxcut_energy");
   energy_kernel<S><<<(B + S - 1) / S, 256, smem, H->stream>>>(B, W, H->num_edges, H->d_edges, H->X,
-                                                              H->cut, H->local);
+                                                              H->cpart, H->local);
   LAUNCH_CHECK();
   H->launches++;
 }
 
-void launch_weights_from_locals(Handle* H, int B, int seg) {
-  KScope ks(H, "stats_weights");
-  stats_weights_kernel<<<1, 1024, 0, H->stream>>>(B / seg, seg, H->num_edges, H->local, H->cut, H->w, H->d_wscale,
-                                                   H->d_istat);
+__global__ void cuts_reduce_kernel(int B, int chunks, const int32_t* __restrict__ cpart, int32_t* __restrict__ cut) {
+  const int b = blockIdx.x * blockDim.x + threadIdx.x;
+  if (b >= B) return;
+  int c = 0;
+  for (int k = 0; k < chunks; ++k) c += cpart[(size_t)k * B + b];
+  cut[b] = c;
+}
+
+void launch_cuts_reduce(Handle* H, int B) {
+  cuts_reduce_kernel<<<(B + 255) / 256, 256, 0, H->stream>>>(B, H->cut_chunks, H->cpart, H->cut);
   LAUNCH_CHECK();
   H->launches++;
 }
 
-void launch_backward(Handle* H, int B) {
+void launch_weights_from_locals(Handle* H, int B, int seg, bool with_wg1) {
+  const Layout& L = H->L;
+  const size_t smem = (size_t)B * sizeof(float);
+  static size_t attr = 0;
+  if (smem > 48 * 1024 && attr < smem) {
+    VQMC_CUDA(cudaFuncSetAttribute(stats_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    attr = smem;
+  }
+  const int64_t total = (int64_t)B * H->hp18;
+  const int grid = with_wg1 ? (int)std::max<int64_t>(1, std::min<int64_t>(148, (total + 4095) / 4096)) : 1;
+  KScope ks(H, with_wg1 ? "stats_weights_wg1" : "stats_weights");
+  stats_weights_kernel<<<grid, 1024, smem, H->stream>>>(B / seg, seg, H->cut_chunks, H->num_edges, H->cpart, H->cut,
+                                                       H->local, H->w, H->d_wscale, H->d_istat, L.h, H->hp18,
+                                                       with_wg1 ? H->G1 : nullptr, H->wG1h, H->wG1l);
+  LAUNCH_CHECK();
+  H->launches++;
+}
+
+void launch_backward(Handle* H, int B, bool wg1_done) {
   using namespace bwcfg;
   const Layout& L = H->L;
   launch_dg1_umma(H, B);  // E = D . W2m (split-K partials)
@@ -618,7 +679,7 @@ void launch_backward(Handle* H, int B) {
     LAUNCH_CHECK();
     H->launches++;
   }
-  launch_gw2_umma(H, B);  // gW2 (.) M2 and gb2
+  launch_gw2_umma(H, B, wg1_done);  // gW2 (.) M2 and gb2
   {
     int splits = 1;
     launch_gw1_umma(H, B, splits);  // gW1 partials (tcgen05)
@@ -631,13 +692,6 @@ void launch_backward(Handle* H, int B) {
   }
 }
 
-__global__ void step_advance_kernel(StepParams* sp) {
-  sp->call += 1;
-  sp->t += 1;
-  sp->bc1 = (float)(1.0 - pow((double)sp->b1, (double)sp->t));  // optimizer.cpp:28-29
-  sp->bc2 = (float)(1.0 - pow((double)sp->b2, (double)sp->t));
-}
-
 __global__ void set_step_kernel(StepParams* sp, uint64_t call, int64_t t, float lr, float b1, float b2,
                                 float eps) {
   sp->call = call;
@@ -648,12 +702,6 @@ __global__ void set_step_kernel(StepParams* sp, uint64_t call, int64_t t, float 
   sp->eps = eps;
   sp->bc1 = (float)(1.0 - pow((double)b1, (double)t));
   sp->bc2 = (float)(1.0 - pow((double)b2, (double)t));
-}
-
-void launch_step_advance(Handle* H) {
-  step_advance_kernel<<<1, 1, 0, H->stream>>>(H->d_step);
-  LAUNCH_CHECK();
-  H->launches++;
 }
 
 void launch_set_step(Handle* H, uint64_t call, int64_t t, double lr, double b1, double b2, double eps) {
