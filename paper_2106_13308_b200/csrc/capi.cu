@@ -339,6 +339,7 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   H->device = device;
   DeviceGuard dg(device);
   VQMC_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
+  if (const char* e = std::getenv("VQMC_PDL")) H->pdl = e[0] == '1';
   H->L.init(n, h, Hd);
   if (H->L.total >= (int64_t(1) << 31)) throw std::invalid_argument("model too large for the device layout (> 2^31 live parameters)");
   H->hp8 = (h + 7) & ~7;

@@ -107,7 +107,7 @@ static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, cons
   const int grid = std::min(ntiles, sms);
   if (H) {
     KScope ks(H, name);
-    kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(ah, al, bh, bl, args, epi);
+    launch_k(H, kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, ah, al, bh, bl, args, epi);
     H->launches++;
   } else {
     kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(ah, al, bh, bl, args, epi);

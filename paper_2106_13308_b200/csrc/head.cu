@@ -312,6 +312,8 @@ __device__ __forceinline__ float head_threshold(const double* __restrict__ uni, 
 // One thread per (sample, 4 consecutive bits): one Philox call serves all four.
 __global__ void head_thresholds_kernel(int B, int Hd, int Hd8, int W, const double* __restrict__ uni, RngSpec rng,
                                        const uint32_t* __restrict__ X, int given, float* __restrict__ thr) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int q4 = Hd8 >> 2;
   const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   if (t >= (int64_t)B * q4) return;
@@ -596,6 +598,8 @@ __global__ void __launch_bounds__(32 * (5 + kHeadEmitWarps)) head_v3_kernel(cons
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
+  ptx::pdl_trigger();
+  ptx::pdl_wait();  // thresholds (previous kernel) complete
   const int cta_b0 = Sd.b0;
 
   if (warp == nw) {  // ---------------- producer warp ----------------
@@ -859,8 +863,8 @@ static void head_v3_launch(Handle* H, int B, const double* uni, RngSpec rng, dou
   {
     KScope ks(H, "head_thresholds");
     const int64_t total = (int64_t)B * (Hd8 / 4);
-    head_thresholds_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.Hd, Hd8, L.W, uni, rng, H->X,
-                                                                                   GIVEN ? 1 : 0, H->thr);
+    launch_k(H, head_thresholds_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, B, L.Hd, Hd8, L.W, uni,
+             rng, H->X, GIVEN ? 1 : 0, H->thr);
     VQMC_CUDA(cudaGetLastError());
     H->launches++;
   }
@@ -868,7 +872,7 @@ static void head_v3_launch(Handle* H, int B, const double* uni, RngSpec rng, dou
   const HeadV3Args args{B,      L.n,     L.h,    L.W,    geo,     H->W1Tp,  H->W2cp, H->P + L.off_b1,
                         H->P + L.off_b2, uni, rng, H->X, H->G1, H->G1h, H->G1l, H->hp18, H->Dh, H->Dl, H->np8,
                         H->Xfb, H->hd18, H->lp_head, cond, H->thr};
-  head_v3_kernel<KG, GIVEN><<<grid, 32 * (nw + 1 + kHeadEmitWarps), geo.smem, H->stream>>>(args);
+  launch_k(H, head_v3_kernel<KG, GIVEN>, dim3(grid), dim3(32 * (nw + 1 + kHeadEmitWarps)), geo.smem, args);
   VQMC_CUDA(cudaGetLastError());
   H->launches++;
 }

@@ -115,6 +115,12 @@ int status_of(const std::exception& ex);
 void launch_adam(Handle* h, float grad_scale);  // hyper-parameters from h->d_step
 void launch_set_step(Handle* h, uint64_t call, int64_t t, double lr, double b1, double b2, double eps);
 
+// Kernel launch on the handle's stream; with Handle::pdl the launch carries the programmatic
+// stream serialization attribute, so the kernel's prologue overlaps the previous kernel's tail
+// (every step kernel calls ptx::pdl_wait() before touching global memory).
+template <typename... KArgs, typename... Args>
+void launch_k(Handle* H, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args);
+
 struct Handle {
   int device = 0;
   cudaStream_t stream = nullptr;
@@ -222,6 +228,7 @@ struct Handle {
   int kt_count = 0;
 
   int64_t launches = 0;
+  bool pdl = false;  // programmatic dependent launch for the step kernels (VQMC_PDL=1 enables; measured neutral)
   int tail_tiles = 0;  // column tiles of the last z2 launch (lp partials)
   int splits = 0;      // split-K factor of the dg1 GEMM
 
@@ -230,5 +237,22 @@ struct Handle {
   void ensure_cond(int64_t count);
   void ensure_cpart(int64_t count);
 };
+
+template <typename... KArgs, typename... Args>
+void launch_k(Handle* H, void (*kern)(KArgs...), dim3 grid, dim3 block, size_t smem, Args&&... args) {
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = H->stream;
+  cudaLaunchAttribute at[1];
+  if (H->pdl) {
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
+  VQMC_CUDA(cudaLaunchKernelEx(&cfg, kern, static_cast<KArgs>(args)...));
+}
 
 }  // namespace vqmc_b200

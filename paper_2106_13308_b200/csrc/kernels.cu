@@ -183,6 +183,8 @@ __global__ void __launch_bounds__(256) maxcut_cut_kernel(int B, int n, int W, in
   const int rows = min(32, B - s0);
   const int64_t e0 = (int64_t)blockIdx.x * per_chunk, e1 = min(nE, e0 + per_chunk);
   const int ne = (int)(e1 - e0);
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   if (threadIdx.x == 0) {
     ptx::mbar_init(&bar[0], 1);
     ptx::mbar_init(&bar[1], 1);
@@ -261,6 +263,8 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   const int B = segs * seg;
   const bool lead = blockIdx.x == 0;
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   float wmax = 0.f;
   for (int sgi = 0; sgi < segs; ++sgi) {
     const int base = sgi * seg;
@@ -356,6 +360,8 @@ constexpr int QM = 64, QN = 64;  // gW1
 __global__ void dz1_kernel(int B, int h, int hp, int splits, const float* __restrict__ Epart,
                            const float* __restrict__ w, const float* __restrict__ G1,
                            __nv_bfloat16* __restrict__ dz1bh, __nv_bfloat16* __restrict__ dz1bl) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
   const size_t total = (size_t)B * h;
   if (t >= total) return;
@@ -370,6 +376,8 @@ __global__ void dz1_kernel(int B, int h, int hp, int splits, const float* __rest
 __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __restrict__ part,
                                     const int32_t* __restrict__ deg, const float* __restrict__ wscale,
                                     float* __restrict__ gW1T, float* __restrict__ gb1) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int total = (Hd + 1) * h;
   if (t >= total) return;
@@ -443,6 +451,8 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, c
                                                    float* __restrict__ M, float* __restrict__ V,
                                                    double* __restrict__ gpart, unsigned* __restrict__ done,
                                                    double* __restrict__ gnorm2, AdamOut o) {
+  ptx::pdl_trigger();
+  ptx::pdl_wait();
   const float lr = sp->lr, b1 = sp->b1, b2 = sp->b2, eps = sp->eps, bc1 = sp->bc1, bc2 = sp->bc2;
   double sq = 0.0;
   auto upd = [&](float g, float& m, float& v, float& p) {
@@ -615,8 +625,8 @@ void launch_energy(Handle* H, int B) {
     H->ensure_cpart((int)chunks * B);
     H->cut_chunks = (int)chunks;
     KScope ks(H, "maxcut_energy");
-    maxcut_cut_kernel<<<dim3((unsigned)chunks, (unsigned)groups), 256, smem, H->stream>>>(B, H->L.n, W, nE, per,
-                                                                                         H->d_edges, H->X, H->cpart);
+    launch_k(H, maxcut_cut_kernel, dim3((unsigned)chunks, (unsigned)groups), dim3(256), smem, B, H->L.n, W, nE, per,
+             (const int2*)H->d_edges, (const uint32_t*)H->X, H->cpart);
     LAUNCH_CHECK();
     H->launches++;
     return;
@@ -660,9 +670,9 @@ void launch_weights_from_locals(Handle* H, int B, int seg, bool with_wg1) {
   const int64_t total = (int64_t)B * H->hp18;
   const int grid = with_wg1 ? (int)std::max<int64_t>(1, std::min<int64_t>(148, (total + 4095) / 4096)) : 1;
   KScope ks(H, with_wg1 ? "stats_weights_wg1" : "stats_weights");
-  stats_weights_kernel<<<grid, 1024, smem, H->stream>>>(B / seg, seg, H->cut_chunks, H->num_edges, H->cpart, H->cut,
-                                                       H->local, H->w, H->d_wscale, H->d_istat, L.h, H->hp18,
-                                                       with_wg1 ? H->G1 : nullptr, H->wG1h, H->wG1l);
+  launch_k(H, stats_weights_kernel, dim3(grid), dim3(1024), smem, B / seg, seg, H->cut_chunks, H->num_edges,
+           (const int32_t*)H->cpart, H->cut, H->local, H->w, H->d_wscale, H->d_istat, L.h, (int)H->hp18,
+           (const float*)(with_wg1 ? H->G1 : nullptr), H->wG1h, H->wG1l);
   LAUNCH_CHECK();
   H->launches++;
 }
@@ -674,8 +684,8 @@ void launch_backward(Handle* H, int B, bool wg1_done) {
   {
     KScope ks(H, "bw_dz1");
     const size_t total = (size_t)B * L.h;
-    dz1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp8, H->splits, H->Epart, H->w,
-                                                                       H->G1, H->dz1bh, H->dz1bl);
+    launch_k(H, dz1_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, B, L.h, H->hp8, H->splits,
+             (const float*)H->Epart, (const float*)H->w, (const float*)H->G1, H->dz1bh, H->dz1bl);
     LAUNCH_CHECK();
     H->launches++;
   }
@@ -685,8 +695,9 @@ void launch_backward(Handle* H, int B, bool wg1_done) {
     launch_gw1_umma(H, B, splits);  // gW1 partials (tcgen05)
     KScope ks(H, "bw_gw1_finalize");
     const int total = (L.Hd + 1) * L.h;
-    gw1_finalize_kernel<<<(total + 255) / 256, 256, 0, H->stream>>>(L.h, L.Hd, splits, H->gw1_part, H->d_deg,
-                                                                     H->d_wscale, H->G + L.off_w1t, H->G + L.off_b1);
+    launch_k(H, gw1_finalize_kernel, dim3((total + 255) / 256), dim3(256), 0, L.h, L.Hd, splits,
+             (const float*)H->gw1_part, (const int32_t*)H->d_deg, (const float*)H->d_wscale, H->G + L.off_w1t,
+             H->G + L.off_b1);
     LAUNCH_CHECK();
     H->launches++;
   }
@@ -716,8 +727,8 @@ void launch_adam(Handle* H, float grad_scale) {
   AdamOut o{L.h, H->hp18, L.Hd, H->head_hpk, H->head_Hdp, H->head_fast, vec, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
             H->W1Tp, H->W2cp, H->W2h, H->W2l};
   KScope ks(H, "adam");
-  adam_kernel<<<H->gpart_n, 256, 0, H->stream>>>(L.total, grad_scale, H->d_step, H->P, H->G, H->Mo, H->Vo,
-                                                 H->d_gpart, H->d_done, H->d_scal, o);
+  launch_k(H, adam_kernel, dim3(H->gpart_n), dim3(256), 0, L.total, grad_scale, (const StepParams*)H->d_step, H->P,
+           (const float*)H->G, H->Mo, H->Vo, H->d_gpart, H->d_done, H->d_scal, o);
   LAUNCH_CHECK();
   H->launches++;
 }

@@ -39,6 +39,13 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       : "memory");
 }
 
+// ---- programmatic dependent launch ------------------------------------------------
+// wait: block until the preceding kernel of the stream has completed and its writes are
+// visible (no-op when launched without the PDL attribute); trigger: allow the next kernel
+// to be scheduled (its CTAs then run their prologue and park in `wait`).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
 // ---- bulk / tensor copies (TMA) ------------------------------------------------
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(

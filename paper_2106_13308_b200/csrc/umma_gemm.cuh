@@ -118,6 +118,8 @@ __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
   __syncthreads();
   ptx::tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  ptx::pdl_trigger();
+  ptx::pdl_wait();  // predecessor's outputs (the operands) are complete from here on
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer ----------------
