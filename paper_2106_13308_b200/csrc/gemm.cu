@@ -26,6 +26,7 @@
 #include "internal.cuh"
 #include "ptx.cuh"
 #include "umma_gemm.cuh"
+#include "umma2_gemm.cuh"
 
 namespace vqmc_b200 {
 
@@ -111,6 +112,52 @@ static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, cons
     H->launches++;
   } else {
     kern<<<grid, Cfg::kThreads, Cfg::kSmem, stream>>>(ah, al, bh, bl, args, epi);
+  }
+  VQMC_CUDA(cudaGetLastError());
+}
+
+// CTA-pair launch: clusters of 2, one pair per 2 SMs (persistent over pair tiles of 256 x BN).
+template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT, int EK>
+static void launch_umma2(Handle* H, const char* name, const CUtensorMap& ah, const CUtensorMap& al,
+                         const CUtensorMap& bh, const CUtensorMap& bl, int M, int N, int K, int splits, Epi epi,
+                         cudaStream_t stream) {
+  using Cfg = Umma2Cfg<BN>;
+  auto kern = umma2_kernel<BN, A_MN, B_MN, Epi, A_EXACT, EK>;
+  static bool attr = false;
+  if (!attr) {
+    VQMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
+    attr = true;
+  }
+  const int nkb = (K + Cfg::kBK - 1) / Cfg::kBK;
+  UmmaArgs args{M, N, K, (nkb + splits - 1) / splits, (N + BN - 1) / BN, (M + 2 * kUmmaBM - 1) / (2 * kUmmaBM), splits};
+  const int ntiles = args.tiles_n * args.tiles_m * splits;
+  static int sms = 0;
+  if (!sms) VQMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  const int pairs = std::min(ntiles, sms / 2);
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(2 * pairs);
+  cfg.blockDim = dim3(Cfg::kThreads);
+  cfg.dynamicSmemBytes = Cfg::kSmem;
+  cfg.stream = stream;
+  cudaLaunchAttribute at[2];
+  at[0].id = cudaLaunchAttributeClusterDimension;
+  at[0].val.clusterDim.x = 2;
+  at[0].val.clusterDim.y = 1;
+  at[0].val.clusterDim.z = 1;
+  int na = 1;
+  if (H && H->pdl) {
+    at[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[1].val.programmaticStreamSerializationAllowed = 1;
+    na = 2;
+  }
+  cfg.attrs = at;
+  cfg.numAttrs = na;
+  if (H) {
+    KScope ks(H, name);
+    VQMC_CUDA(cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, args, epi));
+    H->launches++;
+  } else {
+    VQMC_CUDA(cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, args, epi));
   }
   VQMC_CUDA(cudaGetLastError());
 }
@@ -282,6 +329,35 @@ struct Gw2Epi {  // rows = outputs i, columns = hidden k (k == h: bias column ->
   __device__ void end_row(int, const UmmaArgs&) {}
 };
 
+// gW2 computed transposed (pair kernel): rows = hidden k (k == h: the bias row -> gb2), columns =
+// outputs i.  For a fixed column the 32 lanes (consecutive k) store 128 contiguous bytes.
+struct Gw2TEpi {
+  int n, h;
+  int part;
+  UmmaTile tile;
+  const int32_t* deg;
+  const float* wscale;  // the A operand carries w' = w / wscale
+  float* gW2;
+  float* gb2;
+  float sc;
+  int dk;
+  __device__ void begin_row(int k, const UmmaArgs&) {
+    sc = *wscale;
+    dk = k < h ? deg[k] : 0;
+  }
+  __device__ void chunk(int k, int col0, const float (&v)[32], const UmmaArgs&) {
+    if (k > h) return;
+#pragma unroll
+    for (int j = 0; j < 32; ++j) {
+      const int i = col0 + j;
+      if (i >= n) break;
+      if (k < h) gW2[(size_t)i * h + k] = (dk < i + 1) ? v[j] * sc : 0.f;  // M2(i, k)
+      else gb2[i] = v[j] * sc;
+    }
+  }
+  __device__ void end_row(int, const UmmaArgs&) {}
+};
+
 // ===========================================================================
 // Helper kernels: 16-bit pairs of operands
 // ===========================================================================
@@ -349,36 +425,36 @@ void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng, bool wan
     H->tail_tiles = 0;
     return;
   }
-  constexpr int BN = 128;
-  const int K = L.h + 1;  // [G1 | 1] . [W2 | b2]
+  constexpr int BN = 192;  // CTA pairs: 256 samples x 192 outputs per tile (96 outputs per CTA's B half)
+  const int K = L.h + 1;   // [G1 | 1] . [W2 | b2]
   const CUtensorMap ah = tmap_kmajor(H->G1h, K, B, H->hp18, kUmmaBM, kElemF16);
   const CUtensorMap al = tmap_kmajor(H->G1l, K, B, H->hp18, kUmmaBM, kElemF16);
-  const CUtensorMap bh = tmap_kmajor(H->W2h + (size_t)colbase * H->hp18, K, ncols, H->hp18, BN, kElemF16);
-  const CUtensorMap bl = tmap_kmajor(H->W2l + (size_t)colbase * H->hp18, K, ncols, H->hp18, BN, kElemF16);
+  const CUtensorMap bh = tmap_kmajor(H->W2h + (size_t)colbase * H->hp18, K, ncols, H->hp18, BN / 2, kElemF16);
+  const CUtensorMap bl = tmap_kmajor(H->W2l + (size_t)colbase * H->hp18, K, ncols, H->hp18, BN / 2, kElemF16);
   TailSampleEpi e{B,   L.n, H->np8, L.W, colbase, L.Hd, uni, rng, H->X, H->Dh, H->Dl, want_lp ? H->lp_part : nullptr,
                   H->d_flag, 0, {}, 0.0, 0, 0, 0, 0, 0};
   H->tail_tiles = TailSampleEpi::kParts * ((ncols + BN - 1) / BN);  // one partial per epilogue set
-  launch_umma<BN, false, false, TailSampleEpi, false, kElemF16>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols, K, 1,
-                                                                e, H->stream);
+  launch_umma2<BN, false, false, TailSampleEpi, false, kElemF16>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols, K, 1,
+                                                                 e, H->stream);
 }
 
 void launch_dg1_umma(Handle* H, int B) {
   const Layout& L = H->L;
-  constexpr int BN = 256;
-  const int mt = (B + kUmmaBM - 1) / kUmmaBM, nt = (L.h + BN - 1) / BN;
-  const int nkb = (L.n + UmmaElem<kElemF16>::kBK - 1) / UmmaElem<kElemF16>::kBK;
-  int splits = std::max(1, std::min(nkb, 148 / (mt * nt)));  // one tile per SM
+  constexpr int BN = 256;  // CTA pairs: 256 samples x 256 hidden units, split-K over the outputs
+  const int mt = (B + 2 * kUmmaBM - 1) / (2 * kUmmaBM), nt = (L.h + BN - 1) / BN;
+  const int nkb = (L.n + Umma2Cfg<BN>::kBK - 1) / Umma2Cfg<BN>::kBK;
+  int splits = std::max(1, std::min(nkb, 74 / (mt * nt)));  // one pair tile per SM pair
   splits = std::min(splits, H->max_splits);
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   H->splits = splits;
   const CUtensorMap ah = tmap_kmajor(H->Dh, L.n, B, H->np8, kUmmaBM, kElemF16);
   const CUtensorMap al = tmap_kmajor(H->Dl, L.n, B, H->np8, kUmmaBM, kElemF16);
-  const CUtensorMap bh = tmap_mnmajor(H->W2h, L.h, L.n, H->hp18, BN, kElemF16);
-  const CUtensorMap bl = tmap_mnmajor(H->W2l, L.h, L.n, H->hp18, BN, kElemF16);
+  const CUtensorMap bh = tmap_mnmajor(H->W2h, L.h, L.n, H->hp18, BN / 2, kElemF16);
+  const CUtensorMap bl = tmap_mnmajor(H->W2l, L.h, L.n, H->hp18, BN / 2, kElemF16);
   PartialEpi e{H->Epart, B, L.h, 0, {}};
-  launch_umma<BN, false, true, PartialEpi, false, kElemF16>(H, "bw_dg1_umma", ah, al, bh, bl, B, L.h, L.n, splits,
-                                                            e, H->stream);
+  launch_umma2<BN, false, true, PartialEpi, false, kElemF16>(H, "bw_dg1_umma", ah, al, bh, bl, B, L.h, L.n, splits,
+                                                             e, H->stream);
 }
 
 void launch_gw2_umma(Handle* H, int B, bool wg1_done) {  // BN = 128: 3-stage ring, 4 column tiles of h + 1
@@ -391,14 +467,16 @@ void launch_gw2_umma(Handle* H, int B, bool wg1_done) {  // BN = 128: 3-stage ri
     VQMC_CUDA(cudaGetLastError());
     H->launches++;
   }
-  constexpr int BN = 128;
-  const CUtensorMap ah = tmap_mnmajor(H->Dh, L.n, B, H->np8, kUmmaBM, kElemF16);
-  const CUtensorMap al = tmap_mnmajor(H->Dl, L.n, B, H->np8, kUmmaBM, kElemF16);
-  const CUtensorMap bh = tmap_mnmajor(H->wG1h, L.h + 1, B, H->hp18, BN, kElemF16);
-  const CUtensorMap bl = tmap_mnmajor(H->wG1l, L.h + 1, B, H->hp18, BN, kElemF16);
-  Gw2Epi e{L.n, L.h, 0, {}, H->d_deg, H->d_wscale, H->G + L.off_w2, H->G + L.off_b2};
-  launch_umma<BN, true, true, Gw2Epi, false, kElemF16>(H, "bw_gw2_umma", ah, al, bh, bl, L.n, L.h + 1, B, 1, e,
-                                                       H->stream);
+  // gW2^T = [w' G1 | w']^T D on CTA pairs: 256 hidden units x 256 outputs per tile (M = h + 1
+  // rows: the bias row h gives gb2), K = batch
+  constexpr int BN = 256;
+  const CUtensorMap ah = tmap_mnmajor(H->wG1h, L.h + 1, B, H->hp18, kUmmaBM, kElemF16);
+  const CUtensorMap al = tmap_mnmajor(H->wG1l, L.h + 1, B, H->hp18, kUmmaBM, kElemF16);
+  const CUtensorMap bh = tmap_mnmajor(H->Dh, L.n, B, H->np8, BN / 2, kElemF16);
+  const CUtensorMap bl = tmap_mnmajor(H->Dl, L.n, B, H->np8, BN / 2, kElemF16);
+  Gw2TEpi e{L.n, L.h, 0, {}, H->d_deg, H->d_wscale, H->G + L.off_w2, H->G + L.off_b2, 1.f, 0};
+  launch_umma2<BN, true, true, Gw2TEpi, false, kElemF16>(H, "bw_gw2_umma", ah, al, bh, bl, L.h + 1, L.n, B, 1, e,
+                                                         H->stream);
 }
 
 // gW1T[j][k] = sum_b X[b][j] dz1[b][k] (j < Hd) and gb1[k] (the ones column j = Hd):
@@ -499,6 +577,93 @@ extern "C" int vqmc_test_umma_gemm(int M, int N, int K, int a_mn, int b_mn, int 
       GO_EK(256)
     }
 #undef GO_EK
+#undef GO2K
+#undef GO4
+#undef GO
+    VQMC_CUDA(cudaDeviceSynchronize());
+    VQMC_CUDA(cudaMemcpy(C, dC, sizeof(float) * (size_t)splits * M * N, cudaMemcpyDeviceToHost));
+  } catch (const std::exception& ex) {
+    set_error(ex.what());
+    release();
+    return status_of(ex);
+  }
+  release();
+  return VQMC_OK;
+}
+
+// Test hook: the CTA-pair kernel (16-bit pairs only), same conventions as vqmc_test_umma_gemm;
+// bn in {128, 192, 256}.
+extern "C" int vqmc_test_umma2_gemm(int M, int N, int K, int a_mn, int b_mn, int bn, int splits, int ek,
+                                    const float* A, const float* Bm, float* C) {
+  void *dA = nullptr, *dB = nullptr, *dAh = nullptr, *dAl = nullptr, *dBh = nullptr, *dBl = nullptr;
+  float* dC = nullptr;
+  auto release = [&]() {
+    for (void* p : {dA, dB, dAh, dAl, dBh, dBl, (void*)dC})
+      if (p) cudaFree(p);
+  };
+  try {
+    if (ek != kElemBF16 && ek != kElemF16) throw InvalidArgument("pair kernel: element kind must be 1 or 2");
+    const int q = 8;
+    const int lda = a_mn ? ((M + q - 1) / q * q) : ((K + q - 1) / q * q);
+    const int arows = a_mn ? K : M, acols = a_mn ? M : K;
+    const int ldb = b_mn ? ((N + q - 1) / q * q) : ((K + q - 1) / q * q);
+    const int brows = b_mn ? K : N, bcols = b_mn ? N : K;
+    const size_t pad = 512;
+    const size_t asz = ((size_t)arows * lda + pad) * 2, bsz = ((size_t)brows * ldb + pad) * 2;
+    VQMC_CUDA(cudaMalloc(&dA, sizeof(float) * arows * acols));
+    VQMC_CUDA(cudaMalloc(&dB, sizeof(float) * brows * bcols));
+    VQMC_CUDA(cudaMalloc(&dAh, asz));
+    VQMC_CUDA(cudaMalloc(&dAl, asz));
+    VQMC_CUDA(cudaMalloc(&dBh, bsz));
+    VQMC_CUDA(cudaMalloc(&dBl, bsz));
+    VQMC_CUDA(cudaMalloc(&dC, sizeof(float) * (size_t)splits * M * N));
+    VQMC_CUDA(cudaMemcpy(dA, A, sizeof(float) * arows * acols, cudaMemcpyHostToDevice));
+    VQMC_CUDA(cudaMemcpy(dB, Bm, sizeof(float) * brows * bcols, cudaMemcpyHostToDevice));
+    for (void* p : {dAh, dAl}) VQMC_CUDA(cudaMemset(p, 0, asz));
+    for (void* p : {dBh, dBl}) VQMC_CUDA(cudaMemset(p, 0, bsz));
+    const unsigned ga = (unsigned)(((int64_t)arows * lda + 255) / 256), gb = (unsigned)(((int64_t)brows * ldb + 255) / 256);
+    if (ek == kElemBF16) {
+      split_rows_bf16_kernel<<<ga, 256>>>(arows, acols, acols, lda, (const float*)dA, (__nv_bfloat16*)dAh,
+                                          (__nv_bfloat16*)dAl);
+      split_rows_bf16_kernel<<<gb, 256>>>(brows, bcols, bcols, ldb, (const float*)dB, (__nv_bfloat16*)dBh,
+                                          (__nv_bfloat16*)dBl);
+    } else {
+      split_rows_f16_kernel<<<ga, 256>>>(arows, acols, acols, lda, (const float*)dA, nullptr, (__half*)dAh,
+                                         (__half*)dAl);
+      split_rows_f16_kernel<<<gb, 256>>>(brows, bcols, bcols, ldb, (const float*)dB, nullptr, (__half*)dBh,
+                                         (__half*)dBl);
+    }
+    VQMC_CUDA(cudaGetLastError());
+    const int half = bn / 2;
+    CUtensorMap ah, al, bh, bl;
+    if (a_mn) { ah = tmap_mnmajor(dAh, M, K, lda, kUmmaBM, ek); al = tmap_mnmajor(dAl, M, K, lda, kUmmaBM, ek); }
+    else { ah = tmap_kmajor(dAh, K, M, lda, kUmmaBM, ek); al = tmap_kmajor(dAl, K, M, lda, kUmmaBM, ek); }
+    if (b_mn) { bh = tmap_mnmajor(dBh, N, K, ldb, half, ek); bl = tmap_mnmajor(dBl, N, K, ldb, half, ek); }
+    else { bh = tmap_kmajor(dBh, K, N, ldb, half, ek); bl = tmap_kmajor(dBl, K, N, ldb, half, ek); }
+    PartialEpi e{dC, M, N, 0, {}};
+#define GO(BNV, AM, BM_, EKV)                                                                            \
+  launch_umma2<BNV, AM, BM_, PartialEpi, false, EKV>(nullptr, "test", ah, al, bh, bl, M, N, K, splits, e, \
+                                                    (cudaStream_t)0)
+#define GO4(BNV, EKV)                                \
+  if (!a_mn && !b_mn) GO(BNV, false, false, EKV);     \
+  else if (!a_mn && b_mn) GO(BNV, false, true, EKV);  \
+  else if (a_mn && !b_mn) GO(BNV, true, false, EKV);  \
+  else GO(BNV, true, true, EKV)
+#define GO2K(BNV, EKV)                               \
+  if (b_mn) throw InvalidArgument("pair kernel: bn 192 needs a K-major B"); \
+  else if (!a_mn) GO(BNV, false, false, EKV);         \
+  else GO(BNV, true, false, EKV)
+#define GO_EK(BNV)                                 \
+  if (ek == kElemBF16) { GO4(BNV, kElemBF16); }    \
+  else { GO4(BNV, kElemF16); }
+    if (bn == 128) { GO_EK(128) }
+    else if (bn == 192) {
+      if (ek == kElemBF16) { GO2K(192, kElemBF16); } else { GO2K(192, kElemF16); }
+    }
+    else if (bn == 256) { GO_EK(256) }
+    else throw InvalidArgument("pair kernel: bn must be 128, 192 or 256");
+#undef GO_EK
+#undef GO2K
 #undef GO4
 #undef GO
     VQMC_CUDA(cudaDeviceSynchronize());
