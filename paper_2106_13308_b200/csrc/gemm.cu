@@ -170,6 +170,7 @@ struct StoreEpi {  // test: C[row][col] = acc
   int ldc;
   int part;
   UmmaTile tile;
+  __device__ void init() {}
   __device__ void begin_row(int, const UmmaArgs&) {}
   __device__ void chunk(int row, int col0, const float (&v)[32], const UmmaArgs& a) {
     if (row >= a.M) return;
@@ -185,7 +186,9 @@ struct StoreEpi {  // test: C[row][col] = acc
 // GEMM as column h), so per output the epilogue is: sigmoid (ex2 + rcp), the draw, D and its fp16
 // pair; Philox keys are per row.  The epilogue warp sets take alternate 32-column chunks and
 // each writes its own log-prob partial (lp_part[kParts * tile + part]): deterministic.
-struct TailSampleEpi {
+constexpr int kTailBN = 192;  // tail sampler pair tile: 256 samples x 192 outputs
+template <bool PROD>  // PROD: production draws (Philox) and no log-probabilities (the training step)
+struct TailSampleEpiT {
   int B, n, np, W, colbase, col_lo;  // outputs in [col_lo, n) are drawn here
   const double* uni;
   RngSpec rng;
@@ -198,17 +201,21 @@ struct TailSampleEpi {
   UmmaTile tile;
   double lps;
   uint32_t k0, k1, c1, c2, c3;  // Philox key and counter words of this row (production draws)
+  __device__ void init() {
+    if (PROD || uni == nullptr) {
+      const uint64_t call = rng.c();  // (device step counter: loaded once per thread)
+      c2 = (uint32_t)call;
+      c3 = (uint32_t)(call >> 32);
+    }
+  }
   __device__ void begin_row(int b, const UmmaArgs&) {
-    lps = 0.0;
-    if (uni == nullptr && b < B) {
+    if (!PROD) lps = 0.0;
+    if ((PROD || uni == nullptr) && b < B) {
       const int s = b / rng.seg;
       const uint64_t key = mix_seed_dev(rng.seed, rng.stream0 + (uint64_t)s);
-      const uint64_t call = rng.c();
       k0 = (uint32_t)key;
       k1 = (uint32_t)(key >> 32);
       c1 = (uint32_t)(b - s * rng.seg);
-      c2 = (uint32_t)call;
-      c3 = (uint32_t)(call >> 32);
     }
   }
   __device__ void chunk(int b, int col0, const float (&v)[32], const UmmaArgs&) {
@@ -226,7 +233,7 @@ struct TailSampleEpi {
 #pragma unroll
       for (int j = jh; j < jh + 16; j += 4) {
         uint32_t r[4];
-        if (uni == nullptr) philox4_k(k0, k1, (uint32_t)((cb + j) >> 2), c1, c2, c3, r);
+        if (PROD || uni == nullptr) philox4_k(k0, k1, (uint32_t)((cb + j) >> 2), c1, c2, c3, r);
         float d[4];
 #pragma unroll
         for (int t = 0; t < 4; ++t) {
@@ -241,7 +248,7 @@ struct TailSampleEpi {
           const float praw = z >= 0.f ? rr : er, qraw = z >= 0.f ? er : rr;  // sigmoid(z), 1 - sigmoid(z)
           const bool clamp = a >= kLogitHi;                                     // models.hpp:26 clamp active
           bool x;
-          if (uni == nullptr) {  // u = (r + 1/2) 2^-32 < clamp(p)
+          if (PROD || uni == nullptr) {  // u = (r + 1/2) 2^-32 < clamp(p)
             x = (float)r[t] + 0.5f < fminf(fmaxf(praw * 4294967296.f, kThrLo), kThrHi);
           } else {
             const double p = clamp ? (z > 0.f ? 1.0 - kProbEps : kProbEps) : (double)praw;
@@ -250,7 +257,7 @@ struct TailSampleEpi {
           x = x && valid;
           word |= (uint32_t)x << (j + t);
           d[t] = (clamp || !valid) ? 0.f : (x ? 0.5f * qraw : -0.5f * praw);  // made_dz2, models.cpp:163-171
-          if (lp_part && valid) {
+          if (!PROD && lp_part && valid) {
             const float L = log1pf(e);
             const float lg = clamp ? ((z > 0.f) == x ? -1.00000005e-7f : -16.11809565095832f)
                                    : -(x ? fmaxf(-z, 0.f) + L : fmaxf(z, 0.f) + L);
@@ -283,12 +290,12 @@ struct TailSampleEpi {
     if (bad) atomicOr(flag, 1u);
     if (cb < col_lo) atomicOr(&X[(size_t)b * W + (cb >> 5)], word);  // shares the word with the head
     else X[(size_t)b * W + (cb >> 5)] = word;
-    lps += (double)lsum;
+    if (!PROD) lps += (double)lsum;
   }
   __device__ void end_row(int b, const UmmaArgs&) {
-    if (lp_part && b < B) lp_part[(size_t)(kParts * tile.tn + part) * B + b] = lps;
+    if (!PROD && lp_part && b < B) lp_part[(size_t)(kParts * tile.tn + part) * B + b] = lps;
   }
-  static constexpr int kParts = UmmaCfg<128>::kEpiSets;
+  static constexpr int kParts = Umma2Cfg<kTailBN>::kEpiSets;  // one log-prob partial per epilogue set
 };
 
 struct PartialEpi {  // split-K partial: out[z][row][col]
@@ -296,6 +303,7 @@ struct PartialEpi {  // split-K partial: out[z][row][col]
   int rows, cols;
   int part;
   UmmaTile tile;
+  __device__ void init() {}
   __device__ void begin_row(int, const UmmaArgs&) {}
   __device__ void chunk(int row, int col0, const float (&v)[32], const UmmaArgs&) {
     if (row >= rows) return;
@@ -315,6 +323,7 @@ struct Gw2Epi {  // rows = outputs i, columns = hidden k (k == h: bias column ->
   const float* wscale;  // the B operand carries w' = w / wscale
   float* gW2;
   float* gb2;
+  __device__ void init() {}
   __device__ void begin_row(int, const UmmaArgs&) {}
   __device__ void chunk(int i, int col0, const float (&v)[32], const UmmaArgs&) {
     if (i >= n) return;
@@ -341,6 +350,7 @@ struct Gw2TEpi {
   float* gb2;
   float sc;
   int dk;
+  __device__ void init() {}
   __device__ void begin_row(int k, const UmmaArgs&) {
     sc = *wscale;
     dk = k < h ? deg[k] : 0;
@@ -425,17 +435,24 @@ void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng, bool wan
     H->tail_tiles = 0;
     return;
   }
-  constexpr int BN = 192;  // CTA pairs: 256 samples x 192 outputs per tile (96 outputs per CTA's B half)
+  constexpr int BN = kTailBN;  // CTA pairs: 256 samples x 192 outputs per tile (96 outputs per CTA's B half)
   const int K = L.h + 1;   // [G1 | 1] . [W2 | b2]
   const CUtensorMap ah = tmap_kmajor(H->G1h, K, B, H->hp18, kUmmaBM, kElemF16);
   const CUtensorMap al = tmap_kmajor(H->G1l, K, B, H->hp18, kUmmaBM, kElemF16);
   const CUtensorMap bh = tmap_kmajor(H->W2h + (size_t)colbase * H->hp18, K, ncols, H->hp18, BN / 2, kElemF16);
   const CUtensorMap bl = tmap_kmajor(H->W2l + (size_t)colbase * H->hp18, K, ncols, H->hp18, BN / 2, kElemF16);
-  TailSampleEpi e{B,   L.n, H->np8, L.W, colbase, L.Hd, uni, rng, H->X, H->Dh, H->Dl, want_lp ? H->lp_part : nullptr,
-                  H->d_flag, 0, {}, 0.0, 0, 0, 0, 0, 0};
-  H->tail_tiles = TailSampleEpi::kParts * ((ncols + BN - 1) / BN);  // one partial per epilogue set
-  launch_umma2<BN, false, false, TailSampleEpi, false, kElemF16>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols, K, 1,
-                                                                 e, H->stream);
+  H->tail_tiles = TailSampleEpiT<false>::kParts * ((ncols + BN - 1) / BN);  // one partial per epilogue set
+  if (uni == nullptr && !want_lp) {  // training step: Philox draws, no log-probabilities
+    TailSampleEpiT<true> e{B, L.n, H->np8, L.W, colbase, L.Hd, nullptr, rng, H->X, H->Dh, H->Dl, nullptr,
+                           H->d_flag, 0, {}, 0.0, 0, 0, 0, 0, 0};
+    launch_umma2<BN, false, false, TailSampleEpiT<true>, false, kElemF16>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols,
+                                                                          K, 1, e, H->stream);
+  } else {
+    TailSampleEpiT<false> e{B,   L.n, H->np8, L.W, colbase, L.Hd, uni, rng, H->X, H->Dh, H->Dl,
+                            want_lp ? H->lp_part : nullptr, H->d_flag, 0, {}, 0.0, 0, 0, 0, 0, 0};
+    launch_umma2<BN, false, false, TailSampleEpiT<false>, false, kElemF16>(H, "z2_tail_umma", ah, al, bh, bl, B,
+                                                                           ncols, K, 1, e, H->stream);
+  }
 }
 
 void launch_dg1_umma(Handle* H, int B) {

@@ -102,7 +102,8 @@ struct Umma2Cfg {  // 16-bit operand pairs only; per CTA: A 128 rows, B BN / 2 r
   static constexpr int kStages = (200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
   static constexpr int kChunks = BN / 32;
-  static constexpr int kEpiSets = kChunks < 4 ? kChunks : 4;
+  // epilogue warp sets of 4 warps, each taking whole 32-column chunks (balanced: 6 chunks -> 3 sets)
+  static constexpr int kEpiSets = kChunks % 4 == 0 ? 4 : (kChunks % 3 == 0 ? 3 : (kChunks < 4 ? kChunks : 4));
   static constexpr int kThreads = 128 + 128 * kEpiSets;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256;
   static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "pair tile N");
@@ -246,6 +247,8 @@ __global__ void __launch_bounds__(Umma2Cfg<BN>::kThreads, 1)
     const int q = warp & 3, part = (warp - 4) >> 2;
     const uint32_t tempty_leader0 = ptx::mapa_shared(ptx::smem_u32(&tempty[0]), 0);
     const uint32_t tempty_leader1 = ptx::mapa_shared(ptx::smem_u32(&tempty[1]), 0);
+    Epi e = epi;
+    e.init();  // per-thread state that does not change between tiles
     int j = 0;
     for (int t = pair; t < ntiles; t += npairs, ++j) {
       UmmaTile c = tile_of(t);
@@ -256,7 +259,6 @@ __global__ void __launch_bounds__(Umma2Cfg<BN>::kThreads, 1)
       const int row = m0 + 32 * q + lane;
       ptx::mbar_wait(&tfull[buf], (j >> 1) & 1);
       ptx::tc_fence_after();
-      Epi e = epi;
       e.part = part;
       e.tile = c;
       e.begin_row(row, args);

@@ -207,6 +207,8 @@ __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
     }
   } else if (warp >= 4) {  // ---------------- epilogue ----------------
     const int q = warp & 3, part = (warp - 4) >> 2;
+    Epi e = epi;
+    e.init();  // per-thread state that does not change between tiles
     int j = 0;
     for (int t = blockIdx.x; t < ntiles; t += gridDim.x, ++j) {
       const UmmaTile c = tile_of(t);
@@ -216,7 +218,6 @@ __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
       const int row = m0 + 32 * q + lane;
       ptx::mbar_wait(&tfull[buf], (j >> 1) & 1);
       ptx::tc_fence_after();
-      Epi e = epi;
       e.part = part;
       e.tile = c;
       e.begin_row(row, args);
