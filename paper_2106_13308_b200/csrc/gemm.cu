@@ -19,6 +19,7 @@
 #include <stdint.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -486,7 +487,7 @@ void launch_gw2_umma(Handle* H, int B, bool wg1_done) {  // BN = 128: 3-stage ri
   }
   // gW2^T = [w' G1 | w']^T D on CTA pairs: 256 hidden units x 256 outputs per tile (M = h + 1
   // rows: the bias row h gives gb2), K = batch
-  constexpr int BN = 256;
+  constexpr int BN = 128;  // 2 x 79 pair tiles at N = 10k: 2.1 waves of 74 pairs (BN 256: 80 tiles, 2 full waves)
   const CUtensorMap ah = tmap_mnmajor(H->wG1h, L.h + 1, B, H->hp18, kUmmaBM, kElemF16);
   const CUtensorMap al = tmap_mnmajor(H->wG1l, L.h + 1, B, H->hp18, kUmmaBM, kElemF16);
   const CUtensorMap bh = tmap_mnmajor(H->Dh, L.n, B, H->np8, BN / 2, kElemF16);
@@ -524,6 +525,13 @@ void launch_gw1_umma(Handle* H, int B, int& splits_out) {
 //   ek: operand pairs 0 = tf32, 1 = bf16, 2 = fp16.
 // ===========================================================================
 using namespace vqmc_b200;
+
+static float g_test_ms = 0.f;  // average kernel time of the last test-hook GEMM (VQMC_TEST_REPS launches)
+extern "C" float vqmc_test_last_ms(void) { return g_test_ms; }
+static int test_reps() {
+  const char* e = std::getenv("VQMC_TEST_REPS");
+  return e ? std::max(1, atoi(e)) : 1;
+}
 
 extern "C" int vqmc_test_umma_gemm(int M, int N, int K, int a_mn, int b_mn, int bn, int splits, int ek,
                                    const float* A, const float* Bm, float* C) {
@@ -673,12 +681,26 @@ extern "C" int vqmc_test_umma2_gemm(int M, int N, int K, int a_mn, int b_mn, int
 #define GO_EK(BNV)                                 \
   if (ek == kElemBF16) { GO4(BNV, kElemBF16); }    \
   else { GO4(BNV, kElemF16); }
-    if (bn == 128) { GO_EK(128) }
-    else if (bn == 192) {
-      if (ek == kElemBF16) { GO2K(192, kElemBF16); } else { GO2K(192, kElemF16); }
+    const int reps = test_reps();
+    cudaEvent_t e0, e1;
+    VQMC_CUDA(cudaEventCreate(&e0));
+    VQMC_CUDA(cudaEventCreate(&e1));
+    for (int rep = 0; rep <= reps; ++rep) {  // rep 0: warm-up
+      if (rep == 1) VQMC_CUDA(cudaEventRecord(e0));
+      if (bn == 128) { GO_EK(128) }
+      else if (bn == 192) {
+        if (ek == kElemBF16) { GO2K(192, kElemBF16); } else { GO2K(192, kElemF16); }
+      }
+      else if (bn == 256) { GO_EK(256) }
+      else throw InvalidArgument("pair kernel: bn must be 128, 192 or 256");
     }
-    else if (bn == 256) { GO_EK(256) }
-    else throw InvalidArgument("pair kernel: bn must be 128, 192 or 256");
+    VQMC_CUDA(cudaEventRecord(e1));
+    VQMC_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    VQMC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    g_test_ms = reps > 0 ? ms / reps : 0.f;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
 #undef GO_EK
 #undef GO2K
 #undef GO4
