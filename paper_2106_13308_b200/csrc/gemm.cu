@@ -219,10 +219,15 @@ struct TailSampleEpiT {
       c1 = (uint32_t)(b - s * rng.seg);
     }
   }
-  __device__ void chunk(int b, int col0, const float (&v)[32], const UmmaArgs&) {
+  __device__ void chunk(int b, int col0, const float (&v)[32], const UmmaArgs& a) {
     if (b >= B) return;
     const int cb = colbase + col0;
-    const bool full = cb >= col_lo && cb + 32 <= n;
+    if (cb >= col_lo && cb + 32 <= n) chunk_t<true>(b, cb, v);  // every output of the chunk is drawn here
+    else chunk_t<false>(b, cb, v);
+  }
+  template <bool FULL>
+  __device__ __forceinline__ void chunk_t(int b, int cb, const float (&v)[32]) {
+    constexpr bool full = FULL;
     constexpr float kThrLo = (float)(kProbEps * 4294967296.0), kThrHi = (float)((1.0 - kProbEps) * 4294967296.0);
     const size_t rowD = (size_t)b * np;
     uint32_t word = 0;

@@ -267,33 +267,17 @@ __global__ void __launch_bounds__(Umma2Cfg<BN>::kThreads, 1)
       e.begin_row(row, args);
       const bool has_k = kb1 > kb0;
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN);
-      if constexpr (Cfg::kChunks == 2 * Cfg::kEpiSets) {
-        // two chunks per warp set: both TMEM loads in flight before the first wait
-        const int c0 = 32 * part, c1 = 32 * (part + Cfg::kEpiSets);
-        float v0[32], v1[32];
+#pragma unroll 1
+      for (int cc = 32 * part; cc < BN; cc += 32 * Cfg::kEpiSets) {
+        if (n0 + cc >= args.N) break;
+        float v[32];
         if (has_k) {
-          ptx::tmem_ld32_nowait(trow + (uint32_t)c0, v0);
-          ptx::tmem_ld32_nowait(trow + (uint32_t)c1, v1);
-          ptx::tmem_wait_ld(v0, v1);
+          ptx::tmem_ld32(trow + (uint32_t)cc, v);
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v0[i] = v1[i] = 0.f;
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
         }
-        if (n0 + c0 < args.N) e.chunk(row, n0 + c0, v0, args);
-        if (n0 + c1 < args.N) e.chunk(row, n0 + c1, v1, args);
-      } else {
-#pragma unroll 1
-        for (int cc = 32 * part; cc < BN; cc += 32 * Cfg::kEpiSets) {
-          if (n0 + cc >= args.N) break;
-          float v[32];
-          if (has_k) {
-            ptx::tmem_ld32(trow + (uint32_t)cc, v);
-          } else {
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] = 0.f;
-          }
-          e.chunk(row, n0 + cc, v, args);
-        }
+        e.chunk(row, n0 + cc, v, args);
       }
       e.end_row(row, args);
       ptx::tc_fence_before();
