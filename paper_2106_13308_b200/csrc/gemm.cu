@@ -314,6 +314,12 @@ struct PartialEpi {  // split-K partial: out[z][row][col]
   __device__ void chunk(int row, int col0, const float (&v)[32], const UmmaArgs&) {
     if (row >= rows) return;
     float* o = out + ((size_t)tile.z * rows + row) * cols;
+    if ((cols & 3) == 0 && col0 + 32 <= cols) {  // 16-byte stores (row stride and col0 are multiples of 4)
+      float4* o4 = reinterpret_cast<float4*>(o + col0);
+#pragma unroll
+      for (int j = 0; j < 8; ++j) o4[j] = make_float4(v[4 * j], v[4 * j + 1], v[4 * j + 2], v[4 * j + 3]);
+      return;
+    }
 #pragma unroll
     for (int j = 0; j < 32; ++j)
       if (col0 + j < cols) o[col0 + j] = v[j];
