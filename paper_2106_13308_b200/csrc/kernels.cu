@@ -446,53 +446,70 @@ __device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, fl
   }
 }
 
-__global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, const StepParams* __restrict__ sp,
+__global__ void __launch_bounds__(256, 4) adam_kernel(int64_t total, float scale, const StepParams* __restrict__ sp,
                                                    float* __restrict__ P, const float* __restrict__ G,
                                                    float* __restrict__ M, float* __restrict__ V,
                                                    double* __restrict__ gpart, unsigned* __restrict__ done,
                                                    double* __restrict__ gnorm2, AdamOut o) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  const float lr = sp->lr, b1 = sp->b1, b2 = sp->b2, eps = sp->eps, bc1 = sp->bc1, bc2 = sp->bc2;
+  const float lr = sp->lr, b1 = sp->b1, b2 = sp->b2, eps = sp->eps, ibc1 = 1.f / sp->bc1, ibc2 = 1.f / sp->bc2;
+  float sqf = 0.f;  // fp32 partial of ||g||^2 per element group, summed into fp64 per thread
   double sq = 0.0;
   auto upd = [&](float g, float& m, float& v, float& p) {
     g *= scale;
-    sq += (double)g * (double)g;
+    sqf = fmaf(g, g, sqf);
     m = b1 * m + (1.f - b1) * g;
     v = b2 * v + (1.f - b2) * (g * g);
-    const float mh = m / bc1, vh = v / bc2;
+    const float mh = m * ibc1, vh = v * ibc2;
     p = p - lr * (mh / (sqrtf(vh) + eps));
   };
   const int64_t nq = total / 4;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-  for (int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q < nq; q += stride) {
-    float4 g4 = reinterpret_cast<const float4*>(G)[q];
-    float4 m4 = reinterpret_cast<float4*>(M)[q];
-    float4 v4 = reinterpret_cast<float4*>(V)[q];
-    float4 p4 = reinterpret_cast<float4*>(P)[q];
-    upd(g4.x, m4.x, v4.x, p4.x);
-    upd(g4.y, m4.y, v4.y, p4.y);
-    upd(g4.z, m4.z, v4.z, p4.z);
-    upd(g4.w, m4.w, v4.w, p4.w);
-    reinterpret_cast<float4*>(M)[q] = m4;
-    reinterpret_cast<float4*>(V)[q] = v4;
-    reinterpret_cast<float4*>(P)[q] = p4;
-    const int64_t t = 4 * q;
-    const int64_t u = t - o.off_w2;
-    if (o.vec_w2 && u >= 0 && u < o.off_b2 - o.off_w2 && (u / o.h) >= o.Hd) {
-      // bulk of W2 (rows >= Hd): 4 consecutive entries of one row -> 8-byte stores of both halves
-      const unsigned i = (unsigned)u / (unsigned)o.h, k = (unsigned)u - i * (unsigned)o.h;
-      uint2 hi, lo;
-      ptx::split_f16x2(p4.x, p4.y, hi.x, lo.x);
-      ptx::split_f16x2(p4.z, p4.w, hi.y, lo.y);
-      *reinterpret_cast<uint2*>(o.W2h + (size_t)i * o.hp18 + k) = hi;
-      *reinterpret_cast<uint2*>(o.W2l + (size_t)i * o.hp18 + k) = lo;
-    } else {
-      adam_side_writes(o, t, p4.x);
-      adam_side_writes(o, t + 1, p4.y);
-      adam_side_writes(o, t + 2, p4.z);
-      adam_side_writes(o, t + 3, p4.w);
+  const int64_t w2_bulk0 = (int64_t)o.Hd * o.h, w2_end = o.off_b2 - o.off_w2;  // W2 rows >= Hd
+  constexpr int U = 2;  // float4 groups per thread per iteration: all loads in flight before any math
+  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < nq; q0 += U * stride) {
+    float4 g4[U], m4[U], v4[U], p4[U];
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * stride;
+      if (q < nq) {
+        g4[u] = reinterpret_cast<const float4*>(G)[q];
+        m4[u] = reinterpret_cast<float4*>(M)[q];
+        v4[u] = reinterpret_cast<float4*>(V)[q];
+        p4[u] = reinterpret_cast<float4*>(P)[q];
+      }
     }
+#pragma unroll
+    for (int u = 0; u < U; ++u) {
+      const int64_t q = q0 + u * stride;
+      if (q >= nq) break;
+      upd(g4[u].x, m4[u].x, v4[u].x, p4[u].x);
+      upd(g4[u].y, m4[u].y, v4[u].y, p4[u].y);
+      upd(g4[u].z, m4[u].z, v4[u].z, p4[u].z);
+      upd(g4[u].w, m4[u].w, v4[u].w, p4[u].w);
+      reinterpret_cast<float4*>(M)[q] = m4[u];
+      reinterpret_cast<float4*>(V)[q] = v4[u];
+      reinterpret_cast<float4*>(P)[q] = p4[u];
+      const int64_t t = 4 * q;
+      const int64_t w = t - o.off_w2;
+      if (o.vec_w2 && w >= w2_bulk0 && w < w2_end) {
+        // bulk of W2 (rows >= Hd): 4 consecutive entries of one row -> 8-byte stores of both halves
+        const unsigned i = (unsigned)w / (unsigned)o.h, k = (unsigned)w - i * (unsigned)o.h;
+        uint2 hi, lo;
+        ptx::split_f16x2(p4[u].x, p4[u].y, hi.x, lo.x);
+        ptx::split_f16x2(p4[u].z, p4[u].w, hi.y, lo.y);
+        *reinterpret_cast<uint2*>(o.W2h + (size_t)i * o.hp18 + k) = hi;
+        *reinterpret_cast<uint2*>(o.W2l + (size_t)i * o.hp18 + k) = lo;
+      } else {
+        adam_side_writes(o, t, p4[u].x);
+        adam_side_writes(o, t + 1, p4[u].y);
+        adam_side_writes(o, t + 2, p4[u].z);
+        adam_side_writes(o, t + 3, p4[u].w);
+      }
+    }
+    sq += (double)sqf;  // (at most 8 fp32 terms per partial: ||g||^2 keeps ~fp32-grade relative error)
+    sqf = 0.f;
   }
   for (int64_t t = 4 * nq + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
     float g = G[t], m = M[t], v = V[t], p = P[t];
@@ -502,6 +519,7 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, c
     P[t] = p;
     adam_side_writes(o, t, p);
   }
+  sq += (double)sqf;
   __shared__ double red[8];
   __shared__ bool last;
 #pragma unroll
@@ -516,10 +534,19 @@ __global__ void __launch_bounds__(256) adam_kernel(int64_t total, float scale, c
     last = atomicAdd(done, 1u) == gridDim.x - 1;
   }
   __syncthreads();
-  if (last && threadIdx.x == 0) {  // fixed-order final sum by the last block
+  if (!last) return;
+  {  // fixed-order final sum by the last block: strided thread sums, then a fixed shuffle tree
     __threadfence();
     double s = 0.0;
-    for (unsigned i = 0; i < gridDim.x; ++i) s += ((volatile double*)gpart)[i];
+    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) s += ((volatile double*)gpart)[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
     *gnorm2 = s;
     *done = 0u;
     // advance the device step counters for the next step (every other block has read them):
