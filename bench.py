@@ -94,8 +94,40 @@ class ClockSampler:
     def __init__(self):
         self.proc = None
         self.path = os.path.join(ROOT, "gpurun_out", "clocks.csv")
+        self.nvml = None
+
+    # NVML sampler (every 2 ms in a thread, so even a few-ms timed region is covered); nvidia-smi
+    # (-lms 100) is the fallback.
+    def _nvml_loop(self):
+        import pynvml as nv
+        while not self._stop.is_set():
+            try:
+                sm = nv.nvmlDeviceGetClockInfo(self._h, nv.NVML_CLOCK_SM)
+                mx = nv.nvmlDeviceGetMaxClockInfo(self._h, nv.NVML_CLOCK_SM)
+                rs = nv.nvmlDeviceGetCurrentClocksEventReasons(self._h)
+                self._samples.append((sm, mx, rs))
+            except Exception:
+                pass
+            self._first.set()
+            self._stop.wait(0.002)
 
     def start(self):
+        try:
+            import pynvml as nv
+            nv.nvmlInit()
+            idx = int(os.environ.get("LOCAL_RANK", "0"))
+            vis = os.environ.get("CUDA_VISIBLE_DEVICES")
+            if vis:
+                idx = int(vis.split(",")[idx])
+            self._h = nv.nvmlDeviceGetHandleByIndex(idx)
+            self._samples, self._stop, self._first = [], threading.Event(), threading.Event()
+            self._t = threading.Thread(target=self._nvml_loop, daemon=True)
+            self._t.start()
+            self._first.wait(1.0)
+            self.nvml = nv
+            return
+        except Exception:
+            self.nvml = None
         try:
             os.makedirs(os.path.dirname(self.path), exist_ok=True)
             self.f = open(self.path, "w")
@@ -105,6 +137,18 @@ class ClockSampler:
             self.proc = None
 
     def stop(self):
+        if self.nvml is not None:
+            nv = self.nvml
+            self._stop.set()
+            self._t.join(timeout=2)
+            bits = {"hw_slowdown": 0x8, "hw_thermal_slowdown": 0x40, "sw_thermal_slowdown": 0x20,
+                    "sw_power_cap": 0x4}
+            if not self._samples:
+                return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["no samples"]}
+            reasons = sorted({nm for (_, _, r) in self._samples for nm, b in bits.items() if r & b})
+            return {"sm_mhz": float(np.median([x[0] for x in self._samples])),
+                    "sm_max_mhz": float(max(x[1] for x in self._samples)), "reasons": reasons,
+                    "samples": len(self._samples), "source": "nvml (2 ms)"}
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
         self.proc.terminate()
@@ -160,11 +204,12 @@ def kernel_work(name, n, h, Hd, B, E):
         return "tensor", 2.0 * B * n * h, "FLOP"
     if name in ("bw_gw2", "bw_gw2_umma"):
         return "tensor", 2.0 * B * n * (h + 1), "FLOP"
-    if name == "bw_gw1":
+    if name in ("bw_gw1", "bw_gw1_umma"):
         return "tensor", 2.0 * B * (Hd + 1) * h, "FLOP"
     if name == "adam":
         total = Hd * h + h + n * h + n
-        return "hbm", 28.0 * total, "B"
+        # read g, m, v, theta; write m, v, theta (28 B per live param) + the fp16 pair of [W2 | b2] (4 B)
+        return "hbm", 28.0 * total + 4.0 * n * (h + 1), "B"
     if name == "maxcut_energy":
         W = (n + 31) // 32
         return "hbm", 4.0 * B * W + 8.0 * E + 12.0 * B, "B"
@@ -294,32 +339,34 @@ def run_ours(args):
     peaks = measured_peaks()
     avg = {k: ktimes[k] / kcount[k] for k in ktimes}
     share = {k: ktimes[k] / max(1e-9, sum(ktimes.values())) for k in ktimes}
-    dom = max(ktimes, key=lambda k: ktimes[k])
+    # the roofline object describes the largest kernel with a tensor or HBM bound (the head sampler,
+    # a serial dependency chain, is reported beside it under "kernels" / "head_latency")
+    modelled = [k for k in ktimes if kernel_work(k, n, h, Hd, B, len(e))[0] in ("tensor", "hbm")]
+    dom = max(modelled, key=lambda k: ktimes[k])
     bound, work, wunit = kernel_work(dom, n, h, Hd, B, len(e))
-    if bound is None:  # dominant kernel without a roofline model: report the largest modelled one
-        modelled = [k for k in ktimes if kernel_work(k, n, h, Hd, B, len(e))[0] in ("tensor", "hbm")]
-        dom = max(modelled, key=lambda k: ktimes[k])
-        bound, work, wunit = kernel_work(dom, n, h, Hd, B, len(e))
+    traffic = None  # dram bytes per launch of that kernel from the committed ncu --set full capture
+    tpath = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(tpath):
+        try:
+            traffic = json.load(open(tpath)).get(dom)
+        except (OSError, ValueError):
+            traffic = None
     roof = None
     if bound == "tensor":
         ach = work / (avg[dom] * 1e-3) / 1e12
         pk = peaks["bf16_tflops_sustained"] if peaks else 1400.0
         roof = {"bound": "tensor", "kernel": dom, "achieved": ach, "peak": pk, "unit": "TFLOP/s", "frac": ach / pk,
-                "traffic": None, "peak_src": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
+                "traffic": traffic, "peak_src": "MEASURED_PEAKS.json bf16_tflops_sustained" if peaks else "fallback",
                 "algorithmic_per_launch": work, "launch_ms": avg[dom],
-                "note": "achieved = algorithmic (useful) FLOPs / launch time; the kernel issues 3x that as "
-                        "tcgen05 kind::tf32 MMAs (3xTF32 split for fp32-grade parity), and tf32 runs at half "
-                        "the bf16 rate, so the tf32-pipe ceiling for this kernel is peak / 6"}
-    elif bound == "hbm":
+                "note": "achieved = algorithmic (useful, single-pass) FLOPs / launch time.  Every operand is an "
+                        "fp16 pair and the kernel issues 3 tcgen05 kind::f16 MMA passes (hi.hi + hi.lo + lo.hi, "
+                        "fp32-grade), so its tensor-pipe ceiling for useful FLOPs is peak / 3; traffic = "
+                        "dram read+write bytes per launch from profiles/traffic.json (ncu --set full)"}
+    else:
         ach = work / (avg[dom] * 1e-3) / 1e9
         pk = peaks["hbm_gbs"] if peaks else 6650.0
         roof = {"bound": "hbm", "kernel": dom, "achieved": ach, "peak": pk, "unit": "GB/s", "frac": ach / pk,
-                "traffic": None, "algorithmic_per_launch": work, "launch_ms": avg[dom]}
-    else:
-        ach = work / (avg[dom] * 1e-3) / 1e12
-        pk = 148 * 128 * 2 * 1.965e9 / 1e12
-        roof = {"bound": "latency", "kernel": dom, "achieved": ach, "peak": pk, "unit": "TFLOP/s (fp32 FMA pipe)",
-                "frac": ach / pk, "traffic": None, "algorithmic_per_launch": work, "launch_ms": avg[dom]}
+                "traffic": traffic, "algorithmic_per_launch": work, "launch_ms": avg[dom]}
     # all tensor/hbm kernels for context
     kernels = {}
     for k in sorted(ktimes, key=lambda k: -ktimes[k]):
@@ -329,6 +376,13 @@ def run_ours(args):
             ent["achieved"] = w_ / (avg[k] * 1e-3) / (1e12 if u_ == "FLOP" else 1e9)
             ent["unit"] = "TFLOP/s" if u_ == "FLOP" else "GB/s"
         kernels[k] = ent
+    head_lat = None
+    if "head_sample" in avg:  # the head's serial chain: cycles per sampled bit at the measured clock
+        hz = (clk or {}).get("sm_mhz") or 1965.0
+        head_lat = {"kernel": "head_sample", "launch_ms": avg["head_sample"], "bits": Hd,
+                    "cycles_per_bit": avg["head_sample"] * 1e-3 * hz * 1e6 / max(Hd, 1),
+                    "fp32_tflops": kernel_work("head_sample", n, h, Hd, B, len(e))[1] / (avg["head_sample"] * 1e-3) / 1e12,
+                    "note": "latency-bound dependency chain over the first Hd bits; reported beside the roofline"}
 
     cpu = None
     if world == 1 and not args.no_cpu_baseline and not args.profile:
@@ -357,6 +411,7 @@ def run_ours(args):
         "phase_ms_note": "phase and kernel events come from a second K-step pass (event nodes between kernels "
                          "add overhead); ms_per_step uses whole-step events only",
         "kernels": kernels,
+        "head_latency": head_lat,
         "roofline": roof,
         "final_cut": {"best_cut": ev[2], "mean_cut": ev[3], "energy": ev[0], "note": "eval batch 1024 after "
                       f"{args.warmup + 2 * args.steps} training steps"},
