@@ -236,7 +236,7 @@ def run_ours(args):
     e = np.ascontiguousarray(g.edges, np.int32)
     K.check(K.lib.vqmc_gpu_create(local, n, h, K.ptr(model.degrees), K.ptr(model.parameters()), K.ptr(e), len(e),
                                   B, C.byref(hd)))
-    if world > 1:
+    if world > 1 or os.environ.get("VQMC_NCCL_SELF") == "1":  # (1 rank: exercises the overlapped path)
         uid = (C.c_uint8 * 128)()
         if rank == 0:
             K.check(K.lib.vqmc_gpu_comm_unique_id(uid))

@@ -439,6 +439,9 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   cudaStreamSynchronize(H->stream);
   H->invalidate_graph();
   if (H->nccl_comm && g_nccl.CommDestroy) g_nccl.CommDestroy(H->nccl_comm);
+  if (H->cstream) cudaStreamDestroy(H->cstream);
+  if (H->ev_fork) cudaEventDestroy(H->ev_fork);
+  if (H->ev_join) cudaEventDestroy(H->ev_join);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2h, H->W2l, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
                   H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->cpart, H->local, H->w, H->d_wscale, H->d_flag,
@@ -648,13 +651,24 @@ int vqmc_gpu_comm_init(vqmc_gpu_t* g, const uint8_t id[128], int nranks, int ran
   if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad nranks/rank");
   H->nranks = nranks;
   H->rank = rank;
-  if (nranks == 1) return VQMC_OK;
+  // nranks == 1 needs no communicator; VQMC_NCCL_SELF=1 still creates one (a one-rank NCCL
+  // all-reduce) so the overlapped-collective path can be exercised on a single GPU
+  const char* self = std::getenv("VQMC_NCCL_SELF");
+  if (nranks == 1 && !(self && self[0] == '1')) return VQMC_OK;
   load_nccl();
   NcclUniqueId uid;
   std::memcpy(uid.internal, id, 128);
   ncclComm_t comm = nullptr;
   nccl_check(g_nccl.CommInitRank(&comm, nranks, uid, rank), "ncclCommInitRank");
   H->nccl_comm = comm;
+  if (!H->cstream) {
+    int lo = 0, hi = 0;
+    VQMC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+    VQMC_CUDA(cudaStreamCreateWithPriority(&H->cstream, cudaStreamNonBlocking, hi));  // comm first
+    VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
+    VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_join, cudaEventDisableTiming));
+  }
+  H->gemm_sm_reserve = 16;  // SMs left to NCCL while the backward GEMMs overlap the all-reduce
   H->invalidate_graph();
   API_CATCH
 }
@@ -684,14 +698,29 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
   launch_energy(H, B);                                // local_energy_batch (:161)
   launch_weights_from_locals(H, B, minibatch, true);  // gradient_from_locals weights (:164) + w' G1 operand
   if (tm) record_event(H, H->ev[2]);
-  launch_backward(H, B, /*wg1_done=*/true);  // weighted_grad_log_psi
-  if (tm) record_event(H, H->ev[3]);
-  if (H->nccl_comm) {  // allreduce_mean (:187): sum here, / L in Adam
-    KScope ks(H, "nccl_allreduce");
-    nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)H->L.total, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
-               "ncclAllReduce");
+  if (!H->nccl_comm) {
+    launch_backward(H, B, /*wg1_done=*/true);  // weighted_grad_log_psi
+    if (tm) record_event(H, H->ev[3]);
+    if (tm) record_event(H, H->ev[4]);
+  } else {
+    // allreduce_mean (:187), summed here and divided by L in Adam, overlapped with the backward:
+    // gW2 / gb2 first, then their all-reduce (99% of the bytes) on cstream while dg1 -> dz1 -> gW1
+    // run on the main stream; then the small W1 / b1 all-reduce and the join.
+    const Layout& L = H->L;
+    launch_gw2_umma(H, B, /*wg1_done=*/true);
+    VQMC_CUDA(cudaEventRecord(H->ev_fork, H->stream));
+    VQMC_CUDA(cudaStreamWaitEvent(H->cstream, H->ev_fork, 0));
+    nccl_check(g_nccl.AllReduce(H->G + L.off_w2, H->G + L.off_w2, (size_t)(L.total - L.off_w2), ncclFloat32, ncclSum,
+                                H->nccl_comm, H->cstream),
+               "ncclAllReduce (W2, b2)");
+    VQMC_CUDA(cudaEventRecord(H->ev_join, H->cstream));
+    launch_backward_tail(H, B);
+    if (tm) record_event(H, H->ev[3]);
+    nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)L.off_w2, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
+               "ncclAllReduce (W1, b1)");
+    VQMC_CUDA(cudaStreamWaitEvent(H->stream, H->ev_join, 0));
+    if (tm) record_event(H, H->ev[4]);
   }
-  if (tm) record_event(H, H->ev[4]);
   launch_adam(H, 1.0f / (float)(workers * H->nranks));  // adam_step (:221)
   if (t0) record_event(H, H->ev[5]);
 }

@@ -90,6 +90,12 @@ CUtensorMap tmap_mnmajor(const void* ptr, int64_t MN, int64_t K, int64_t ld, int
   return m;
 }
 
+int gemm_sms(const Handle* H) {
+  static int sms = 0;
+  if (!sms) VQMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
+  return H ? std::max(2, sms - H->gemm_sm_reserve) : sms;
+}
+
 template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false, int EK = kElemTF32>
 static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, const CUtensorMap& al,
                         const CUtensorMap& bh, const CUtensorMap& bl, int M, int N, int K, int splits, Epi epi,
@@ -104,9 +110,7 @@ static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, cons
   const int nkb = (K + UmmaElem<EK>::kBK - 1) / UmmaElem<EK>::kBK;
   UmmaArgs args{M, N, K, (nkb + splits - 1) / splits, (N + BN - 1) / BN, (M + kUmmaBM - 1) / kUmmaBM, splits};
   const int ntiles = args.tiles_n * args.tiles_m * splits;
-  static int sms = 0;
-  if (!sms) VQMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  const int grid = std::min(ntiles, sms);
+  const int grid = std::min(ntiles, gemm_sms(H));
   if (H) {
     KScope ks(H, name);
     launch_k(H, kern, dim3(grid), dim3(Cfg::kThreads), Cfg::kSmem, ah, al, bh, bl, args, epi);
@@ -132,9 +136,7 @@ static void launch_umma2(Handle* H, const char* name, const CUtensorMap& ah, con
   const int nkb = (K + Cfg::kBK - 1) / Cfg::kBK;
   UmmaArgs args{M, N, K, (nkb + splits - 1) / splits, (N + BN - 1) / BN, (M + 2 * kUmmaBM - 1) / (2 * kUmmaBM), splits};
   const int ntiles = args.tiles_n * args.tiles_m * splits;
-  static int sms = 0;
-  if (!sms) VQMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  const int pairs = std::min(ntiles, sms / 2);
+  const int pairs = std::min(ntiles, gemm_sms(H) / 2);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(2 * pairs);
   cfg.blockDim = dim3(Cfg::kThreads);
@@ -472,7 +474,7 @@ void launch_dg1_umma(Handle* H, int B) {
   constexpr int BN = 256;  // CTA pairs: 256 samples x 256 hidden units, split-K over the outputs
   const int mt = (B + 2 * kUmmaBM - 1) / (2 * kUmmaBM), nt = (L.h + BN - 1) / BN;
   const int nkb = (L.n + Umma2Cfg<BN>::kBK - 1) / Umma2Cfg<BN>::kBK;
-  int splits = std::max(1, std::min(nkb, 74 / (mt * nt)));  // one pair tile per SM pair
+  int splits = std::max(1, std::min(nkb, (gemm_sms(H) / 2) / (mt * nt)));  // one pair tile per SM pair
   splits = std::min(splits, H->max_splits);
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
@@ -516,7 +518,7 @@ void launch_gw1_umma(Handle* H, int B, int& splits_out) {
   constexpr int BN = 128;
   const int mt = (L.Hd + 1 + kUmmaBM - 1) / kUmmaBM, nt = (L.h + BN - 1) / BN;
   const int nkb = (B + UmmaElem<true>::kBK - 1) / UmmaElem<true>::kBK;
-  int splits = std::max(1, std::min(std::min(nkb, kGw1MaxSplits), 148 / (mt * nt)));
+  int splits = std::max(1, std::min(std::min(nkb, kGw1MaxSplits), gemm_sms(H) / (mt * nt)));
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   splits_out = splits;

@@ -105,6 +105,8 @@ void launch_energy(Handle* h, int B);
 void launch_weights_from_locals(Handle* h, int B, int seg, bool with_wg1 = false);
 void launch_cuts_reduce(Handle* h, int B);
 void launch_backward(Handle* h, int B, bool wg1_done = false);
+void launch_backward_tail(Handle* h, int B);  // dg1, dz1, gW1 (+ finalize)
+int gemm_sms(const Handle* h);  // SMs the persistent GEMMs may use
 void launch_tail_umma(Handle* h, int B, const double* d_uniforms, RngSpec rng, bool want_lp);
 void launch_dg1_umma(Handle* h, int B);
 void launch_gw2_umma(Handle* h, int B, bool wg1_done = false);
@@ -211,9 +213,13 @@ struct Handle {
   double cur_lr = -1, cur_b1 = -1, cur_b2 = -1, cur_eps = -1;
   void invalidate_graph();
 
-  // comm
+  // comm: the [W2 | b2] part of the gradient (99% of the bytes) is all-reduced on cstream while dg1,
+  // dz1 and gW1 run; the GEMMs then leave gemm_sm_reserve SMs free for NCCL's kernels
   void* nccl_comm = nullptr;
   int nranks = 1, rank = 0;
+  cudaStream_t cstream = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  int gemm_sm_reserve = 0;
 
   // timing
   int phase_timing = 0;  // 0 off, 1 whole-step events, 2 per-phase events

@@ -705,6 +705,12 @@ void launch_weights_from_locals(Handle* H, int B, int seg, bool with_wg1) {
 }
 
 void launch_backward(Handle* H, int B, bool wg1_done) {
+  launch_gw2_umma(H, B, wg1_done);  // gW2 (.) M2 and gb2
+  launch_backward_tail(H, B);
+}
+
+// dg1 -> dz1 -> gW1: the W1 / b1 part of the gradient (independent of gW2)
+void launch_backward_tail(Handle* H, int B) {
   using namespace bwcfg;
   const Layout& L = H->L;
   launch_dg1_umma(H, B);  // E = D . W2m (split-K partials)
@@ -716,7 +722,6 @@ void launch_backward(Handle* H, int B, bool wg1_done) {
     LAUNCH_CHECK();
     H->launches++;
   }
-  launch_gw2_umma(H, B, wg1_done);  // gW2 (.) M2 and gb2
   {
     int splits = 1;
     launch_gw1_umma(H, B, splits);  // gW1 partials (tcgen05)

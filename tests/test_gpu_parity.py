@@ -324,3 +324,27 @@ def test_production_train_n10000_smoke():
     res = api.train(cfg)
     assert len(res.stats) == 3 and all(np.isfinite([s.energy_mean, s.grad_norm]).all() for s in res.stats)
     assert 0 < res.best_cut <= 15000 and res.best_cut >= res.mean_cut
+
+
+def test_overlapped_allreduce_path_matches_single_gpu(monkeypatch):
+    """The multi-GPU step (gW2 all-reduce on a comm stream overlapped with dg1/dz1/gW1, GEMMs leaving
+    SMs to NCCL) run through a one-rank NCCL communicator (VQMC_NCCL_SELF=1) gives bitwise the same
+    parameters as the plain single-GPU step over eager, captured and replayed steps."""
+    n, B = 1000, 256
+    m = _model(n, 4, perturb=False)
+    e = _graph(n, 4, "regular")
+    devs = [Dev(n, m.h, m.degrees, m.theta, e, B), Dev(n, m.h, m.degrees, m.theta, e, B)]
+    monkeypatch.setenv("VQMC_NCCL_SELF", "1")
+    uid = (C.c_uint8 * 128)()
+    K.check(K.lib.vqmc_gpu_comm_unique_id(uid))
+    K.check(K.lib.vqmc_gpu_comm_init(devs[1].h_, uid, 1, 0))
+    for d in devs:
+        K.check(K.lib.vqmc_gpu_adam_reset(d.h_))
+    stats = [[], []]
+    for t in range(1, 5):
+        for k, d in enumerate(devs):
+            st = K.StepStats()
+            K.check(K.lib.vqmc_gpu_train_step(d.h_, B, 1, None, 4, 1, t, 0.01, 0.9, 0.999, 1e-8, t, C.byref(st)))
+            stats[k].append((st.energy_mean, st.grad_norm))
+    assert stats[0] == stats[1]
+    assert np.array_equal(devs[0].get_params(), devs[1].get_params())
