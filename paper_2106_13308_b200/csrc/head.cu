@@ -380,15 +380,17 @@ struct HeadV3Args {
   const float* thr;  // [B][Hd8] logit thresholds (head_thresholds_kernel)
 };
 
-// Consumer state of one warp (two samples): relative slots and the ping-pong row buffers.
+constexpr int kHeadS = 2;  // samples per consumer warp (they share every shared-memory row load)
+
+// Consumer state of one warp (kHeadS samples): relative slots and the ping-pong row buffers.
 template <int KG>
 struct HeadV3State {
   static constexpr int KPL = 4 * KG;
-  float z1[2][KPL], z2[2][KPL];
+  float z1[kHeadS][KPL], z2[kHeadS][KPL];
   float4 wa1[KG], wa2[KG], wb1[KG], wb2[KG];
-  float thr[2];       // this lane's logit threshold of the current word (given bits: -inf / +inf)
-  float thr_next[2];  // the next word's (prefetched)
-  float vp[2];   // shuffled (x, g) of the pending bit
+  float thr[kHeadS];       // this lane's logit threshold of the current word (given bits: -inf / +inf)
+  float thr_next[kHeadS];  // the next word's (prefetched)
+  float vp[kHeadS];   // shuffled (x, g) of the pending bit
 #ifdef VQMC_HEAD_PROF
   long long wait_cycles = 0;
 #endif
@@ -399,10 +401,10 @@ struct HeadV3State {
 // Rank-1 updates of one bit (shuffled value v: x in the sign bit, g = |v|) to relative slots
 // [T0, T1) with that bit's rows (w1, w2).
 template <int KG, int T0, int T1>
-__device__ __forceinline__ void head_v3_update(HeadV3State<KG>& S, const float (&v)[2], const float4 (&w1)[KG],
+__device__ __forceinline__ void head_v3_update(HeadV3State<KG>& S, const float (&v)[kHeadS], const float4 (&w1)[KG],
                                                const float4 (&w2)[KG]) {
 #pragma unroll
-  for (int a = 0; a < 2; ++a) {
+  for (int a = 0; a < kHeadS; ++a) {
     const float xf = (__float_as_uint(v[a]) >> 31) ? 1.f : 0.f;
     const float ga = fabsf(v[a]);
 #pragma unroll
@@ -434,9 +436,9 @@ __device__ __forceinline__ void head_v3_bit8(HeadV3State<KG>& S, const HeadRing&
                                              const float4 (&C2)[KG]) {
   constexpr int RS = 128 * KG;
   head_v3_update<KG, 0, 1>(S, S.vp, P1, P2);  // slot 0 of bit i - 1: on the serial chain
-  float v[2];
+  float v[kHeadS];
 #pragma unroll
-  for (int a = 0; a < 2; ++a) {
+  for (int a = 0; a < kHeadS; ++a) {
     const bool x = S.thr[a] < S.z2[a][0];
     const float z1u = x ? S.z1[a][0] + C1[0].x : S.z1[a][0];
     const float g = fmaxf(z1u, 0.f);
@@ -449,7 +451,7 @@ __device__ __forceinline__ void head_v3_bit8(HeadV3State<KG>& S, const HeadRing&
   head_v3_update<KG, 1, 4 * NQ>(S, S.vp, P1, P2);
 #endif
 #pragma unroll
-  for (int a = 0; a < 2; ++a) S.vp[a] = v[a];
+  for (int a = 0; a < kHeadS; ++a) S.vp[a] = v[a];
   const float* r1;
   if (K < 7) {
     r1 = S.rows + (K + 1) * RS + 4 * lane;
@@ -513,12 +515,12 @@ __device__ __forceinline__ void head_v3_words(HeadV3State<KG>& S, const HeadRing
 #pragma unroll 1
   for (int m = m0; m < m1; ++m) {
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < kHeadS; ++a) {
       S.thr[a] = S.thr_next[a];
       S.vp[a] = 0.f;  // nothing pending at a word start
       // next word's thresholds (global, coalesced; hidden behind this word)
       const int ib = 32 * (m + 1) + lane;
-      if (m + 1 < nwords && ib < Sd.Hd8) S.thr_next[a] = Sd.thr[(size_t)(Sd.b0 + 2 * warp + a) * Sd.Hd8 + ib];
+      if (m + 1 < nwords && ib < Sd.Hd8) S.thr_next[a] = Sd.thr[(size_t)(Sd.b0 + kHeadS * warp + a) * Sd.Hd8 + ib];
     }
     const int lend = min(32, Rg.Hd8 - 32 * m);
     const int i0 = 32 * m;
@@ -534,8 +536,8 @@ __device__ __forceinline__ void head_v3_words(HeadV3State<KG>& S, const HeadRing
     const int p = m & 1;
     if (m >= 2) mbar_wait(&Sd.zfree[p], ((m >> 1) - 1) & 1);
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
-      const int sidx = 2 * warp + a;
+    for (int a = 0; a < kHeadS; ++a) {
+      const int sidx = kHeadS * warp + a;
       float* zrow = Sd.zb + ((size_t)(p * 8 + sidx) * 2) * 32;
       zrow[lane] = S.z2[a][0];
       zrow[32 + lane] = S.z1[a][0];
@@ -583,7 +585,7 @@ __global__ void __launch_bounds__(32 * (5 + kHeadEmitWarps)) head_v3_kernel(cons
   Sd.zfree = Sd.zdone + 2;
   Sd.Hd8 = (Hd + 7) & ~7;
   Sd.thr = A.thr;
-  Sd.b0 = 2 * nw * blockIdx.x;  // first sample of this CTA
+  Sd.b0 = kHeadS * nw * blockIdx.x;  // first sample of this CTA
   float* ring = reinterpret_cast<float*>(smem_raw + A.geo.ring_off);
   Sd.zb = ring + (size_t)A.geo.R * A.geo.slot_floats;
   if (threadIdx.x == 0) {
@@ -636,7 +638,7 @@ __global__ void __launch_bounds__(32 * (5 + kHeadEmitWarps)) head_v3_kernel(cons
 #pragma unroll
       for (int j = 0; j < 8 / kHeadEmitWarps; ++j) {
         const int sidx = e + kHeadEmitWarps * j;
-        if (sidx < 2 * nw) {
+        if (sidx < kHeadS * nw) {
           const int b = cta_b0 + sidx;
           const float* zrow = Sd.zb + ((size_t)(p * 8 + sidx) * 2) * 32;
           const float z = zrow[lane], z1 = zrow[32 + lane];
@@ -656,7 +658,7 @@ __global__ void __launch_bounds__(32 * (5 + kHeadEmitWarps)) head_v3_kernel(cons
 #pragma unroll
     for (int j = 0; j < 8 / kHeadEmitWarps; ++j) {
       const int sidx = e + kHeadEmitWarps * j;
-      if (sidx < 2 * nw) {
+      if (sidx < kHeadS * nw) {
         double v = lp[j];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
@@ -670,13 +672,13 @@ __global__ void __launch_bounds__(32 * (5 + kHeadEmitWarps)) head_v3_kernel(cons
     return;
   }
 
-  // ---------------- consumer warps: samples 2 w and 2 w + 1 ----------------
+  // ---------------- consumer warps: samples kHeadS w .. kHeadS w + kHeadS - 1 ----------------
   HeadV3State<KG> S;
 #pragma unroll
   for (int t = 0; t < KPL; ++t) {
     const int k = 32 * t + lane;
 #pragma unroll
-    for (int a = 0; a < 2; ++a) {
+    for (int a = 0; a < kHeadS; ++a) {
       S.z1[a][t] = k < A.h ? A.b1[k] : 0.f;
       S.z2[a][t] = k < Hd ? A.b2[k] : 0.f;
     }
@@ -693,7 +695,7 @@ __global__ void __launch_bounds__(32 * (5 + kHeadEmitWarps)) head_v3_kernel(cons
     S.wb2[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
 #pragma unroll
-  for (int a = 0; a < 2; ++a) S.thr_next[a] = A.thr[(size_t)(cta_b0 + 2 * warp + a) * Sd.Hd8 + lane];
+  for (int a = 0; a < kHeadS; ++a) S.thr_next[a] = A.thr[(size_t)(cta_b0 + kHeadS * warp + a) * Sd.Hd8 + lane];
   const HeadRing Rg{full, empty, ring, G, A.geo.R, A.geo.slot_floats, Hd, (Hd + 7) & ~7};
 #ifdef VQMC_HEAD_PROF
   const long long tstart = clock64();
@@ -855,10 +857,10 @@ static void head_v3_launch(Handle* H, int B, const double* uni, RngSpec rng, dou
   }
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, H->device);
-  const int pairs = (B + 1) / 2;
-  // <= 4 sample-pair warps + producer + threshold + emit warps
-  const int nw = std::max(1, std::min(4, (pairs + dev_sms - 1) / dev_sms));
-  const int grid = (pairs + nw - 1) / nw;
+  const int groups = (B + kHeadS - 1) / kHeadS;  // consumer warps needed
+  // <= 8 / kHeadS consumer warps (8 samples per CTA: the emit hand-off buffer) + producer + emit warps
+  const int nw = std::max(1, std::min(8 / kHeadS, (groups + dev_sms - 1) / dev_sms));
+  const int grid = (groups + nw - 1) / nw;
   const int Hd8 = (L.Hd + 7) & ~7;
   {
     KScope ks(H, "head_thresholds");
