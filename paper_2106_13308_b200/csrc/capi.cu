@@ -210,6 +210,16 @@ static void check_flag(Handle* H, uint32_t v) {
   throw NumericError("non-finite logit in the tail sampler (fp16 operand range exceeded)");
 }
 
+// Side stream of the concurrent backward / gradient all-reduce (high priority) and its events.
+static void ensure_side_stream(Handle* H) {
+  if (H->cstream) return;
+  int lo = 0, hi = 0;
+  VQMC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+  VQMC_CUDA(cudaStreamCreateWithPriority(&H->cstream, cudaStreamNonBlocking, hi));
+  VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
+  VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_join, cudaEventDisableTiming));
+}
+
 static void check_B(int B) {
   if (B < 1) throw std::invalid_argument("batch size must be >= 1");
 }
@@ -340,6 +350,8 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   DeviceGuard dg(device);
   VQMC_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
   if (const char* e = std::getenv("VQMC_PDL")) H->pdl = e[0] == '1';
+  if (const char* e = std::getenv("VQMC_SERIAL_BW")) H->concurrent_bw = e[0] != '1';
+  if (const char* e = std::getenv("VQMC_GW2_SMS")) H->gw2_sms = std::max(2, atoi(e));
   H->L.init(n, h, Hd);
   if (H->L.total >= (int64_t(1) << 31)) throw std::invalid_argument("model too large for the device layout (> 2^31 live parameters)");
   H->hp8 = (h + 7) & ~7;
@@ -661,13 +673,7 @@ int vqmc_gpu_comm_init(vqmc_gpu_t* g, const uint8_t id[128], int nranks, int ran
   ncclComm_t comm = nullptr;
   nccl_check(g_nccl.CommInitRank(&comm, nranks, uid, rank), "ncclCommInitRank");
   H->nccl_comm = comm;
-  if (!H->cstream) {
-    int lo = 0, hi = 0;
-    VQMC_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
-    VQMC_CUDA(cudaStreamCreateWithPriority(&H->cstream, cudaStreamNonBlocking, hi));  // comm first
-    VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
-    VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_join, cudaEventDisableTiming));
-  }
+  ensure_side_stream(H);
   H->gemm_sm_reserve = 16;  // SMs left to NCCL while the backward GEMMs overlap the all-reduce
   H->invalidate_graph();
   API_CATCH
@@ -698,27 +704,38 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
   launch_energy(H, B);                                // local_energy_batch (:161)
   launch_weights_from_locals(H, B, minibatch, true);  // gradient_from_locals weights (:164) + w' G1 operand
   if (tm) record_event(H, H->ev[2]);
-  if (!H->nccl_comm) {
-    launch_backward(H, B, /*wg1_done=*/true);  // weighted_grad_log_psi
-    if (tm) record_event(H, H->ev[3]);
-    if (tm) record_event(H, H->ev[4]);
-  } else {
-    // allreduce_mean (:187), summed here and divided by L in Adam, overlapped with the backward:
-    // gW2 / gb2 first, then their all-reduce (99% of the bytes) on cstream while dg1 -> dz1 -> gW1
-    // run on the main stream; then the small W1 / b1 all-reduce and the join.
-    const Layout& L = H->L;
-    launch_gw2_umma(H, B, /*wg1_done=*/true);
+  const Layout& L = H->L;
+  if (H->concurrent_bw && !H->ktimer) {
+    // weighted_grad_log_psi with its two independent halves concurrent: gW2 / gb2 (and, multi-GPU,
+    // their all-reduce: 99% of the gradient bytes) on cstream with gw2_sms SMs, dg1 -> dz1 -> gW1
+    // on the main stream with the rest; then the small W1 / b1 all-reduce and the join.
+    // allreduce_mean (:187) is summed here and divided by L in Adam.
+    ensure_side_stream(H);
+    const int avail = gemm_sms(nullptr) - H->gemm_sm_reserve;
     VQMC_CUDA(cudaEventRecord(H->ev_fork, H->stream));
     VQMC_CUDA(cudaStreamWaitEvent(H->cstream, H->ev_fork, 0));
-    nccl_check(g_nccl.AllReduce(H->G + L.off_w2, H->G + L.off_w2, (size_t)(L.total - L.off_w2), ncclFloat32, ncclSum,
-                                H->nccl_comm, H->cstream),
-               "ncclAllReduce (W2, b2)");
+    H->gemm_sm_cap = std::min(H->gw2_sms, avail - 16);
+    launch_gw2_umma(H, B, /*wg1_done=*/true, H->cstream);
+    if (H->nccl_comm)
+      nccl_check(g_nccl.AllReduce(H->G + L.off_w2, H->G + L.off_w2, (size_t)(L.total - L.off_w2), ncclFloat32,
+                                  ncclSum, H->nccl_comm, H->cstream),
+                 "ncclAllReduce (W2, b2)");
     VQMC_CUDA(cudaEventRecord(H->ev_join, H->cstream));
+    H->gemm_sm_cap = avail - std::min(H->gw2_sms, avail - 16);
     launch_backward_tail(H, B);
+    H->gemm_sm_cap = 0;
     if (tm) record_event(H, H->ev[3]);
-    nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)L.off_w2, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
-               "ncclAllReduce (W1, b1)");
+    if (H->nccl_comm)
+      nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)L.off_w2, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
+                 "ncclAllReduce (W1, b1)");
     VQMC_CUDA(cudaStreamWaitEvent(H->stream, H->ev_join, 0));
+    if (tm) record_event(H, H->ev[4]);
+  } else {
+    launch_backward(H, B, /*wg1_done=*/true);  // weighted_grad_log_psi (serial; per-kernel timing)
+    if (tm) record_event(H, H->ev[3]);
+    if (H->nccl_comm)
+      nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)L.total, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
+                 "ncclAllReduce");
     if (tm) record_event(H, H->ev[4]);
   }
   launch_adam(H, 1.0f / (float)(workers * H->nranks));  // adam_step (:221)

@@ -93,7 +93,10 @@ CUtensorMap tmap_mnmajor(const void* ptr, int64_t MN, int64_t K, int64_t ld, int
 int gemm_sms(const Handle* H) {
   static int sms = 0;
   if (!sms) VQMC_CUDA(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0));
-  return H ? std::max(2, sms - H->gemm_sm_reserve) : sms;
+  if (!H) return sms;
+  int n = sms - H->gemm_sm_reserve;
+  if (H->gemm_sm_cap > 0) n = std::min(n, H->gemm_sm_cap);
+  return std::max(2, n & ~1);
 }
 
 template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false, int EK = kElemTF32>
@@ -155,12 +158,13 @@ static void launch_umma2(Handle* H, const char* name, const CUtensorMap& ah, con
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  if (H) {
+  if (H && stream == H->stream) {  // (kernel timing events live on the handle's main stream)
     KScope ks(H, name);
     VQMC_CUDA(cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, args, epi));
     H->launches++;
   } else {
     VQMC_CUDA(cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, args, epi));
+    if (H) H->launches++;
   }
   VQMC_CUDA(cudaGetLastError());
 }
@@ -474,7 +478,8 @@ void launch_dg1_umma(Handle* H, int B) {
   constexpr int BN = 256;  // CTA pairs: 256 samples x 256 hidden units, split-K over the outputs
   const int mt = (B + 2 * kUmmaBM - 1) / (2 * kUmmaBM), nt = (L.h + BN - 1) / BN;
   const int nkb = (L.n + Umma2Cfg<BN>::kBK - 1) / Umma2Cfg<BN>::kBK;
-  int splits = std::max(1, std::min(nkb, (gemm_sms(H) / 2) / (mt * nt)));  // one pair tile per SM pair
+  // (split count from the whole GPU, not the current SM partition: results independent of it)
+  int splits = std::max(1, std::min(nkb, (gemm_sms(nullptr) / 2) / (mt * nt)));  // one pair tile per SM pair
   splits = std::min(splits, H->max_splits);
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
@@ -488,12 +493,13 @@ void launch_dg1_umma(Handle* H, int B) {
                                                              e, H->stream);
 }
 
-void launch_gw2_umma(Handle* H, int B, bool wg1_done) {  // BN = 128: 3-stage ring, 4 column tiles of h + 1
+void launch_gw2_umma(Handle* H, int B, bool wg1_done, cudaStream_t stream) {
   const Layout& L = H->L;
+  if (!stream) stream = H->stream;
   if (!wg1_done) {  // (the training step fuses this split into the statistics kernel)
     const int64_t total = (int64_t)B * H->hp18;
     KScope ks(H, "wg1_split");
-    wg1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->hp18, H->G1, H->w, H->wG1h,
+    wg1_kernel<<<(unsigned)((total + 255) / 256), 256, 0, stream>>>(B, L.h, H->hp18, H->G1, H->w, H->wG1h,
                                                                        H->wG1l);
     VQMC_CUDA(cudaGetLastError());
     H->launches++;
@@ -507,7 +513,7 @@ void launch_gw2_umma(Handle* H, int B, bool wg1_done) {  // BN = 128: 3-stage ri
   const CUtensorMap bl = tmap_mnmajor(H->Dl, L.n, B, H->np8, BN / 2, kElemF16);
   Gw2TEpi e{L.n, L.h, 0, {}, H->d_deg, H->d_wscale, H->G + L.off_w2, H->G + L.off_b2, 1.f, 0};
   launch_umma2<BN, true, true, Gw2TEpi, false, kElemF16>(H, "bw_gw2_umma", ah, al, bh, bl, L.h + 1, L.n, B, 1, e,
-                                                         H->stream);
+                                                         stream);
 }
 
 // gW1T[j][k] = sum_b X[b][j] dz1[b][k] (j < Hd) and gb1[k] (the ones column j = Hd):
@@ -518,7 +524,7 @@ void launch_gw1_umma(Handle* H, int B, int& splits_out) {
   constexpr int BN = 128;
   const int mt = (L.Hd + 1 + kUmmaBM - 1) / kUmmaBM, nt = (L.h + BN - 1) / BN;
   const int nkb = (B + UmmaElem<true>::kBK - 1) / UmmaElem<true>::kBK;
-  int splits = std::max(1, std::min(std::min(nkb, kGw1MaxSplits), gemm_sms(H) / (mt * nt)));
+  int splits = std::max(1, std::min(std::min(nkb, kGw1MaxSplits), gemm_sms(nullptr) / (mt * nt)));
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   splits_out = splits;

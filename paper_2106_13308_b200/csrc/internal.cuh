@@ -109,7 +109,7 @@ void launch_backward_tail(Handle* h, int B);  // dg1, dz1, gW1 (+ finalize)
 int gemm_sms(const Handle* h);  // SMs the persistent GEMMs may use
 void launch_tail_umma(Handle* h, int B, const double* d_uniforms, RngSpec rng, bool want_lp);
 void launch_dg1_umma(Handle* h, int B);
-void launch_gw2_umma(Handle* h, int B, bool wg1_done = false);
+void launch_gw2_umma(Handle* h, int B, bool wg1_done = false, cudaStream_t stream = nullptr);
 void launch_split_w2(Handle* h);
 void launch_gw1_umma(Handle* h, int B, int& splits_out);
 void set_error(const std::string& msg);
@@ -220,6 +220,11 @@ struct Handle {
   cudaStream_t cstream = nullptr;
   cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
   int gemm_sm_reserve = 0;
+  // concurrent backward: gW2 (and its all-reduce) on cstream with gw2_sms SMs while dg1 -> dz1 ->
+  // gW1 use the rest (gemm_sm_cap limits the persistent GEMM grids; 0 = no cap)
+  bool concurrent_bw = true;
+  int gw2_sms = 72;
+  int gemm_sm_cap = 0;
 
   // timing
   int phase_timing = 0;  // 0 off, 1 whole-step events, 2 per-phase events
