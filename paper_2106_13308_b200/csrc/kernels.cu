@@ -362,14 +362,38 @@ __global__ void dz1_kernel(int B, int h, int hp, int splits, const float* __rest
                            __nv_bfloat16* __restrict__ dz1bh, __nv_bfloat16* __restrict__ dz1bl) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  const size_t t = (size_t)blockIdx.x * blockDim.x + threadIdx.x;
+  // 4 consecutive k per thread (h % 4 == 0: 16-byte loads of every partial; else scalar)
   const size_t total = (size_t)B * h;
-  if (t >= total) return;
-  float s = 0.f;
-  for (int z = 0; z < splits; ++z) s += Epart[(size_t)z * total + t];
-  const int b = (int)(t / h), k = (int)(t % h);
-  const float d = G1[t] > 0.f ? s * w[b] : 0.f;  // relu'(z1) = [z1 > 0] (models.cpp:181)
-  ptx::split_bf16(d, dz1bh[(size_t)b * hp + k], dz1bl[(size_t)b * hp + k]);
+  const size_t t4 = 4 * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);
+  if (t4 >= total) return;
+  if ((h & 3) == 0) {
+    float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
+    for (int z = 0; z < splits; ++z) {
+      const float4 p = *reinterpret_cast<const float4*>(Epart + (size_t)z * total + t4);
+      s.x += p.x;
+      s.y += p.y;
+      s.z += p.z;
+      s.w += p.w;
+    }
+    const int b = (int)(t4 / h), k = (int)(t4 % h);
+    const float4 g = *reinterpret_cast<const float4*>(G1 + t4);
+    const float wb = w[b];
+    const float d[4] = {g.x > 0.f ? s.x * wb : 0.f, g.y > 0.f ? s.y * wb : 0.f, g.z > 0.f ? s.z * wb : 0.f,
+                        g.w > 0.f ? s.w * wb : 0.f};  // relu'(z1) = [z1 > 0] (models.cpp:181)
+    __nv_bfloat16 hi[4], lo[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) ptx::split_bf16(d[u], hi[u], lo[u]);
+    *reinterpret_cast<uint2*>(dz1bh + (size_t)b * hp + k) = *reinterpret_cast<const uint2*>(hi);
+    *reinterpret_cast<uint2*>(dz1bl + (size_t)b * hp + k) = *reinterpret_cast<const uint2*>(lo);
+    return;
+  }
+  for (size_t t = t4; t < t4 + 4 && t < total; ++t) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += Epart[(size_t)z * total + t];
+    const int b = (int)(t / h), k = (int)(t % h);
+    const float d = G1[t] > 0.f ? s * w[b] : 0.f;
+    ptx::split_bf16(d, dz1bh[(size_t)b * hp + k], dz1bl[(size_t)b * hp + k]);
+  }
 }
 
 // gW1T = (sum of partials) (.) M1^T, gb1 = the ones row (j == Hd).
@@ -378,15 +402,31 @@ __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __re
                                     float* __restrict__ gW1T, float* __restrict__ gb1) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
   const int total = (Hd + 1) * h;
-  if (t >= total) return;
-  float s = 0.f;
-  for (int z = 0; z < splits; ++z) s += part[(size_t)z * total + t];
-  s *= *wscale;
-  const int j = t / h, k = t % h;
-  if (j < Hd) gW1T[(size_t)j * h + k] = (j + 1 <= deg[k]) ? s : 0.f;  // M1(k, j)
-  else gb1[k] = s;
+  const int t4 = 4 * (blockIdx.x * blockDim.x + threadIdx.x);  // 4 consecutive k (h % 4 == 0) or scalar
+  if (t4 >= total) return;
+  const float sc = *wscale;
+  const int n4 = (h & 3) == 0 ? 4 : 1;
+  for (int t = t4; t < t4 + 4 && t < total; t += n4) {
+    float s[4] = {0.f, 0.f, 0.f, 0.f};
+    if (n4 == 4) {
+      for (int z = 0; z < splits; ++z) {
+        const float4 p = *reinterpret_cast<const float4*>(part + (size_t)z * total + t);
+        s[0] += p.x;
+        s[1] += p.y;
+        s[2] += p.z;
+        s[3] += p.w;
+      }
+    } else {
+      for (int z = 0; z < splits; ++z) s[0] += part[(size_t)z * total + t];
+    }
+    for (int u = 0; u < n4; ++u) {
+      const int j = (t + u) / h, k = (t + u) % h;
+      const float v = s[u] * sc;
+      if (j < Hd) gW1T[(size_t)j * h + k] = (j + 1 <= deg[k]) ? v : 0.f;  // M1(k, j)
+      else gb1[k] = v;
+    }
+  }
 }
 
 // ===========================================================================
@@ -716,7 +756,7 @@ void launch_backward_tail(Handle* H, int B) {
   launch_dg1_umma(H, B);  // E = D . W2m (split-K partials)
   {
     KScope ks(H, "bw_dz1");
-    const size_t total = (size_t)B * L.h;
+    const size_t total = ((size_t)B * L.h + 3) / 4;  // (4 entries per thread)
     launch_k(H, dz1_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, B, L.h, H->hp8, H->splits,
              (const float*)H->Epart, (const float*)H->w, (const float*)H->G1, H->dz1bh, H->dz1bl);
     LAUNCH_CHECK();
@@ -726,7 +766,7 @@ void launch_backward_tail(Handle* H, int B) {
     int splits = 1;
     launch_gw1_umma(H, B, splits);  // gW1 partials (tcgen05)
     KScope ks(H, "bw_gw1_finalize");
-    const int total = (L.Hd + 1) * L.h;
+    const int total = ((L.Hd + 1) * L.h + 3) / 4;  // (4 entries per thread)
     launch_k(H, gw1_finalize_kernel, dim3((total + 255) / 256), dim3(256), 0, L.h, L.Hd, splits,
              (const float*)H->gw1_part, (const int32_t*)H->d_deg, (const float*)H->d_wscale, H->G + L.off_w1t,
              H->G + L.off_b1);
