@@ -391,6 +391,7 @@ struct HeadV3State {
   float thr[kHeadS];       // this lane's logit threshold of the current word (given bits: -inf / +inf)
   float thr_next[kHeadS];  // the next word's (prefetched)
   float vp[kHeadS];   // shuffled (x, g) of the pending bit
+  float dg;           // this lane's diagonal weight W1T[i][i] of the current bit (row of bit i, slot 0)
 #ifdef VQMC_HEAD_PROF
   long long wait_cycles = 0;
 #endif
@@ -440,44 +441,37 @@ __device__ __forceinline__ void head_v3_bit8(HeadV3State<KG>& S, const HeadRing&
 #pragma unroll
   for (int a = 0; a < kHeadS; ++a) {
     const bool x = S.thr[a] < S.z2[a][0];
-    const float z1u = x ? S.z1[a][0] + C1[0].x : S.z1[a][0];
+    const float z1u = x ? S.z1[a][0] + S.dg : S.z1[a][0];  // + x_i W1T[i][i] (prefetched diagonal)
     const float g = fmaxf(z1u, 0.f);
     v[a] = x ? -g : g;
-#if !(defined(VQMC_HEAD_EXP) && VQMC_HEAD_EXP == 2)
     v[a] = __shfl_sync(kFull, v[a], l0 + K);
-#endif
   }
-#if !(defined(VQMC_HEAD_EXP) && VQMC_HEAD_EXP == 3)
-  head_v3_update<KG, 1, 4 * NQ>(S, S.vp, P1, P2);
-#endif
-#pragma unroll
-  for (int a = 0; a < kHeadS; ++a) S.vp[a] = v[a];
-  const float* r1;
+  // rows of bit i + 1 (slot handover after the eighth bit); its diagonal weight is fetched now,
+  // ahead of the bulk update, so the next bit's serial chain does not wait on shared memory
+  const float* r1 = nullptr;
   if (K < 7) {
     r1 = S.rows + (K + 1) * RS + 4 * lane;
-  } else {
-    if (i0 + 8 >= Rg.Hd8) return;
-#if !defined(VQMC_HEAD_EXP5)
+  } else if (i0 + 8 < Rg.Hd8) {
     __syncwarp();
     if (lane == 0) mbar_arrive(&Rg.empty[S.slot]);  // rows of this slot are all in registers
-#endif
     if (++S.slot == Rg.R) {
       S.slot = 0;
       ++S.use;
     }
-#if !defined(VQMC_HEAD_EXP5)
     mbar_wait(&Rg.full[S.slot], S.use & 1);
-#endif
     S.rows = Rg.ring + (size_t)S.slot * Rg.slot_floats;
     r1 = S.rows + 4 * lane;
   }
-#if defined(VQMC_HEAD_EXP4)
-  if (i0 < 0)
-#endif
+  if (r1) S.dg = r1[0];
+  head_v3_update<KG, 1, 4 * NQ>(S, S.vp, P1, P2);  // the rest of bit i - 1
 #pragma unroll
-  for (int q = 0; q < NQ; ++q) {
-    P1[q] = *reinterpret_cast<const float4*>(r1 + 128 * q);
-    P2[q] = *reinterpret_cast<const float4*>(r1 + 8 * RS + 128 * q);
+  for (int a = 0; a < kHeadS; ++a) S.vp[a] = v[a];
+  if (r1) {
+#pragma unroll
+    for (int q = 0; q < NQ; ++q) {
+      P1[q] = *reinterpret_cast<const float4*>(r1 + 128 * q);
+      P2[q] = *reinterpret_cast<const float4*>(r1 + 8 * RS + 128 * q);
+    }
   }
 }
 
@@ -694,6 +688,7 @@ __global__ void __launch_bounds__(32 * (5 + kHeadEmitWarps)) head_v3_kernel(cons
     S.wb1[q] = make_float4(0.f, 0.f, 0.f, 0.f);  // "pending" rows of the first bit (0 x 0, never NaN)
     S.wb2[q] = make_float4(0.f, 0.f, 0.f, 0.f);
   }
+  S.dg = S.wa1[0].x;
 #pragma unroll
   for (int a = 0; a < kHeadS; ++a) S.thr_next[a] = A.thr[(size_t)(cta_b0 + kHeadS * warp + a) * Sd.Hd8 + lane];
   const HeadRing Rg{full, empty, ring, G, A.geo.R, A.geo.slot_floats, Hd, (Hd + 7) & ~7};
