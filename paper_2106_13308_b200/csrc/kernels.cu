@@ -210,8 +210,18 @@ __global__ void __launch_bounds__(256) maxcut_cut_kernel(int B, int n, int W, in
   } else {
     ptx::mbar_wait(&bar[0], 0);
   }
-  for (int w = warp; w < W; w += nwarps)  // (row stride W: odd W reads conflict-free columns)
-    T[32 * w + lane] = transpose32_lane(S[lane * W + w], lane);  // node 32 w + lane
+  // (row stride W: odd W reads conflict-free columns); four independent transposes per iteration
+  int w = warp;
+  for (; w + 3 * nwarps < W; w += 4 * nwarps) {
+    uint32_t v[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = S[lane * W + w + u * nwarps];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) v[u] = transpose32_lane(v[u], lane);
+#pragma unroll
+    for (int u = 0; u < 4; ++u) T[32 * (w + u * nwarps) + lane] = v[u];  // node 32 w' + lane
+  }
+  for (; w < W; w += nwarps) T[32 * w + lane] = transpose32_lane(S[lane * W + w], lane);
   __syncthreads();
   uint32_t c[8];
 #pragma unroll
@@ -265,6 +275,20 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
   const bool lead = blockIdx.x == 0;
   ptx::pdl_trigger();
   ptx::pdl_wait();
+  // the wG1 part's G1 values do not depend on the statistics: load them first (<= 4 per thread)
+  constexpr int kPre = 4;
+  const int64_t wtotal = G1 ? (int64_t)B * ld : 0;
+  const int64_t wstride = (int64_t)gridDim.x * blockDim.x;
+  float g1pre[kPre];
+#pragma unroll
+  for (int u = 0; u < kPre; ++u) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + tid + u * wstride;
+    g1pre[u] = 0.f;
+    if (t < wtotal) {
+      const int b = (int)(t / ld), k = (int)(t % ld);
+      if (k < h) g1pre[u] = G1[(size_t)b * h + k];
+    }
+  }
   float wmax = 0.f;
   for (int sgi = 0; sgi < segs; ++sgi) {
     const int base = sgi * seg;
@@ -336,8 +360,16 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
   if (G1 == nullptr) return;
   __syncthreads();
   // wG1[b][k] = w'_b G1[b][k] (k < h), w'_b (k == h), 0 beyond; fp16 pair (gW2 B operand)
-  const int64_t total = (int64_t)B * ld;
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + tid; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+#pragma unroll
+  for (int u = 0; u < kPre; ++u) {
+    const int64_t t = (int64_t)blockIdx.x * blockDim.x + tid + u * wstride;
+    if (t < wtotal) {
+      const int b = (int)(t / ld), k = (int)(t % ld);
+      const float x = k < h ? sw[b] * g1pre[u] : (k == h ? sw[b] : 0.f);
+      ptx::split_f16(x, wgh[t], wgl[t]);
+    }
+  }
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + tid + kPre * wstride; t < wtotal; t += wstride) {
     const int b = (int)(t / ld), k = (int)(t % ld);
     const float x = k < h ? sw[b] * G1[(size_t)b * h + k] : (k == h ? sw[b] : 0.f);
     ptx::split_f16(x, wgh[t], wgl[t]);
