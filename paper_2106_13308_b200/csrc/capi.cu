@@ -352,6 +352,7 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   if (const char* e = std::getenv("VQMC_PDL")) H->pdl = e[0] == '1';
   if (const char* e = std::getenv("VQMC_SERIAL_BW")) H->concurrent_bw = e[0] != '1';
   if (const char* e = std::getenv("VQMC_GW2_SMS")) H->gw2_sms = std::max(2, atoi(e));
+  if (const char* e = std::getenv("VQMC_GW1_SPLITS")) H->gw1_splits = atoi(e);
   H->L.init(n, h, Hd);
   if (H->L.total >= (int64_t(1) << 31)) throw std::invalid_argument("model too large for the device layout (> 2^31 live parameters)");
   H->hp8 = (h + 7) & ~7;

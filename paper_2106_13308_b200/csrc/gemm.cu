@@ -333,6 +333,46 @@ struct PartialEpi {  // split-K partial: out[z][row][col]
   __device__ void end_row(int, const UmmaArgs&) {}
 };
 
+// gW1 without split-K: rows j (j == Hd: the ones row -> gb1), columns k; (.) M1^T and x wscale.
+struct Gw1Epi {
+  int h, Hd;
+  int part;
+  UmmaTile tile;
+  const int32_t* deg;
+  const float* wscale;
+  float* gW1T;
+  float* gb1;
+  float sc;
+  __device__ void init() { sc = *wscale; }
+  __device__ void begin_row(int, const UmmaArgs&) {}
+  __device__ void chunk(int j, int col0, const float (&v)[32], const UmmaArgs&) {
+    if (j > Hd) return;
+    if (j == Hd) {
+#pragma unroll
+      for (int t = 0; t < 32; ++t)
+        if (col0 + t < h) gb1[col0 + t] = v[t] * sc;
+      return;
+    }
+    float* o = gW1T + (size_t)j * h + col0;
+    if ((h & 3) == 0 && col0 + 32 <= h) {
+#pragma unroll
+      for (int q = 0; q < 8; ++q) {
+        float4 r;
+        r.x = (j + 1 <= deg[col0 + 4 * q + 0]) ? v[4 * q + 0] * sc : 0.f;  // M1(k, j)
+        r.y = (j + 1 <= deg[col0 + 4 * q + 1]) ? v[4 * q + 1] * sc : 0.f;
+        r.z = (j + 1 <= deg[col0 + 4 * q + 2]) ? v[4 * q + 2] * sc : 0.f;
+        r.w = (j + 1 <= deg[col0 + 4 * q + 3]) ? v[4 * q + 3] * sc : 0.f;
+        reinterpret_cast<float4*>(o)[q] = r;
+      }
+      return;
+    }
+#pragma unroll
+    for (int t = 0; t < 32; ++t)
+      if (col0 + t < h) o[t] = (j + 1 <= deg[col0 + t]) ? v[t] * sc : 0.f;
+  }
+  __device__ void end_row(int, const UmmaArgs&) {}
+};
+
 struct Gw2Epi {  // rows = outputs i, columns = hidden k (k == h: bias column -> gb2)
   int n, h;
   int part;
@@ -525,12 +565,19 @@ void launch_gw1_umma(Handle* H, int B, int& splits_out) {
   const int mt = (L.Hd + 1 + kUmmaBM - 1) / kUmmaBM, nt = (L.h + BN - 1) / BN;
   const int nkb = (B + UmmaElem<true>::kBK - 1) / UmmaElem<true>::kBK;
   int splits = std::max(1, std::min(std::min(nkb, kGw1MaxSplits), gemm_sms(nullptr) / (mt * nt)));
+  if (H->gw1_splits > 0) splits = std::min(splits, H->gw1_splits);
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
   splits_out = splits;
   const CUtensorMap a = tmap_mnmajor(H->Xfb, L.Hd + 1, B, H->hd18, kUmmaBM, kElemBF16);
   const CUtensorMap bh = tmap_mnmajor(H->dz1bh, L.h, B, H->hp8, BN, kElemBF16);
   const CUtensorMap bl = tmap_mnmajor(H->dz1bl, L.h, B, H->hp8, BN, kElemBF16);
+  if (splits == 1) {  // whole K per tile: the epilogue writes gW1T / gb1 directly (no finalize pass)
+    Gw1Epi e{L.h, L.Hd, 0, {}, H->d_deg, H->d_wscale, H->G + L.off_w1t, H->G + L.off_b1, 1.f};
+    launch_umma<BN, true, true, Gw1Epi, true, kElemBF16>(H, "bw_gw1_umma", a, a, bh, bl, L.Hd + 1, L.h, B, 1, e,
+                                                         H->stream);
+    return;
+  }
   PartialEpi e{H->gw1_part, L.Hd + 1, L.h, 0, {}};
   launch_umma<BN, true, true, PartialEpi, true, kElemBF16>(H, "bw_gw1_umma", a, a, bh, bl, L.Hd + 1, L.h, B, splits,
                                                            e, H->stream);

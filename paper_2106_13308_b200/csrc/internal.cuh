@@ -225,6 +225,7 @@ struct Handle {
   bool concurrent_bw = true;
   int gw2_sms = 72;
   int gemm_sm_cap = 0;
+  int gw1_splits = 4;  // max split-K of the gW1 GEMM (1: direct epilogue, no finalize; VQMC_GW1_SPLITS; 4 measured best)
 
   // timing
   int phase_timing = 0;  // 0 off, 1 whole-step events, 2 per-phase events

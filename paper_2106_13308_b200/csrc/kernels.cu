@@ -796,7 +796,8 @@ void launch_backward_tail(Handle* H, int B) {
   }
   {
     int splits = 1;
-    launch_gw1_umma(H, B, splits);  // gW1 partials (tcgen05)
+    launch_gw1_umma(H, B, splits);  // gW1 (tcgen05): direct epilogue, or split-K partials
+    if (splits == 1) return;
     KScope ks(H, "bw_gw1_finalize");
     const int total = ((L.Hd + 1) * L.h + 3) / 4;  // (4 entries per thread)
     launch_k(H, gw1_finalize_kernel, dim3((total + 255) / 256), dim3(256), 0, L.h, L.Hd, splits,
