@@ -104,7 +104,7 @@ static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, cons
                         const CUtensorMap& bh, const CUtensorMap& bl, int M, int N, int K, int splits, Epi epi,
                         cudaStream_t stream) {
   using Cfg = UmmaCfg<BN>;
-  auto kern = umma_tf32x3_kernel<BN, A_MN, B_MN, Epi, A_EXACT, EK>;
+  auto kern = umma3p_kernel<BN, A_MN, B_MN, Epi, A_EXACT, EK>;
   static bool attr = false;
   if (!attr) {
     VQMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));

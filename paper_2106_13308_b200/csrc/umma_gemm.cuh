@@ -1,4 +1,4 @@
-// tcgen05 GEMM for sm_100a with a 3xTF32 split ("fp32-grade" tensor-core GEMM):
+// tcgen05 3-pass GEMM for sm_100a ("fp32-grade" tensor-core GEMM on split operands: tf32, bf16 or fp16 pairs):
 //
 //   C[M x N] (fp32, TMEM) = sum_k A(m, k) B(n, k),  computed as
 //   A_hi B_hi + A_hi B_lo + A_lo B_hi          (operands stored as tf32 hi/lo pairs)
@@ -73,7 +73,7 @@ struct UmmaTile {
 // A_EXACT: A is exactly representable (e.g. 0/1 spins): A_lo is neither loaded nor used.
 template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT = false, int EK = kElemTF32>
 __global__ void __launch_bounds__(UmmaCfg<BN>::kThreads, 1)
-    umma_tf32x3_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
+    umma3p_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                        const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo,
                        UmmaArgs args, Epi epi) {
   using Cfg = UmmaCfg<BN>;

@@ -9,7 +9,7 @@ import sys
 
 # kernel-name substring -> the bench's kernel key (KScope names)
 MAP = [("TailSampleEpiT", "z2_tail_umma"), ("Gw2TEpi", "bw_gw2_umma"), ("umma2_kernel<256, 0, 1, PartialEpi", "bw_dg1_umma"),
-       ("umma_tf32x3_kernel<128, 1, 1, PartialEpi, 1", "bw_gw1_umma"), ("adam_kernel", "adam"),
+       ("umma3p_kernel<128, 1, 1, PartialEpi, 1", "bw_gw1_umma"), ("adam_kernel", "adam"),
        ("maxcut_cut_kernel", "maxcut_energy"), ("head_v3_kernel", "head_sample"), ("dz1_kernel", "bw_dz1"),
        ("stats_weights_kernel", "stats_weights_wg1"), ("head_thresholds_kernel", "head_thresholds")]
 out = {}
