@@ -218,6 +218,7 @@ static void ensure_side_stream(Handle* H) {
   VQMC_CUDA(cudaStreamCreateWithPriority(&H->cstream, cudaStreamNonBlocking, hi));
   VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
   VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_join, cudaEventDisableTiming));
+  VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_dg1, cudaEventDisableTiming));
 }
 
 static void check_B(int B) {
@@ -353,6 +354,7 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   if (const char* e = std::getenv("VQMC_SERIAL_BW")) H->concurrent_bw = e[0] != '1';
   if (const char* e = std::getenv("VQMC_GW2_SMS")) H->gw2_sms = std::max(2, atoi(e));
   if (const char* e = std::getenv("VQMC_GW1_SPLITS")) H->gw1_splits = atoi(e);
+  if (const char* e = std::getenv("VQMC_ADAM_SMS")) H->adam_w2_sms = std::max(2, atoi(e));
   H->L.init(n, h, Hd);
   if (H->L.total >= (int64_t(1) << 31)) throw std::invalid_argument("model too large for the device layout (> 2^31 live parameters)");
   H->hp8 = (h + 7) & ~7;
@@ -455,6 +457,7 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   if (H->cstream) cudaStreamDestroy(H->cstream);
   if (H->ev_fork) cudaEventDestroy(H->ev_fork);
   if (H->ev_join) cudaEventDestroy(H->ev_join);
+  if (H->ev_dg1) cudaEventDestroy(H->ev_dg1);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2h, H->W2l, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
                   H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->cpart, H->local, H->w, H->d_wscale, H->d_flag,
@@ -721,16 +724,25 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
       nccl_check(g_nccl.AllReduce(H->G + L.off_w2, H->G + L.off_w2, (size_t)(L.total - L.off_w2), ncclFloat32,
                                   ncclSum, H->nccl_comm, H->cstream),
                  "ncclAllReduce (W2, b2)");
-    VQMC_CUDA(cudaEventRecord(H->ev_join, H->cstream));
     H->gemm_sm_cap = avail - std::min(H->gw2_sms, avail - 16);
-    launch_backward_tail(H, B);
+    launch_dg1_umma(H, B);  // the step's last read of the W2 operand pairs
+    VQMC_CUDA(cudaEventRecord(H->ev_dg1, H->stream));
+    // adam_step (:221) on [W2 | b2] as soon as its gradient is reduced and dg1 is done: it overlaps
+    // dz1 -> gW1 on the main stream
+    VQMC_CUDA(cudaStreamWaitEvent(H->cstream, H->ev_dg1, 0));
+    launch_adam_part(H, 1.0f / (float)(workers * H->nranks), 0, H->cstream);
+    VQMC_CUDA(cudaEventRecord(H->ev_join, H->cstream));
+    launch_backward_after_dg1(H, B);
     H->gemm_sm_cap = 0;
     if (tm) record_event(H, H->ev[3]);
     if (H->nccl_comm)
       nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)L.off_w2, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
                  "ncclAllReduce (W1, b1)");
-    VQMC_CUDA(cudaStreamWaitEvent(H->stream, H->ev_join, 0));
     if (tm) record_event(H, H->ev[4]);
+    launch_adam_part(H, 1.0f / (float)(workers * H->nranks), 1, H->stream);  // [W1T | b1]
+    VQMC_CUDA(cudaStreamWaitEvent(H->stream, H->ev_join, 0));
+    if (t0) record_event(H, H->ev[5]);
+    return;
   } else {
     launch_backward(H, B, /*wg1_done=*/true);  // weighted_grad_log_psi (serial; per-kernel timing)
     if (tm) record_event(H, H->ev[3]);

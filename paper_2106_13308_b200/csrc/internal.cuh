@@ -106,6 +106,8 @@ void launch_weights_from_locals(Handle* h, int B, int seg, bool with_wg1 = false
 void launch_cuts_reduce(Handle* h, int B);
 void launch_backward(Handle* h, int B, bool wg1_done = false);
 void launch_backward_tail(Handle* h, int B);  // dg1, dz1, gW1 (+ finalize)
+void launch_backward_after_dg1(Handle* h, int B);  // dz1, gW1 (+ finalize)
+void launch_dg1_umma(Handle* h, int B);
 int gemm_sms(const Handle* h);  // SMs the persistent GEMMs may use
 void launch_tail_umma(Handle* h, int B, const double* d_uniforms, RngSpec rng, bool want_lp);
 void launch_dg1_umma(Handle* h, int B);
@@ -115,6 +117,7 @@ void launch_gw1_umma(Handle* h, int B, int& splits_out);
 void set_error(const std::string& msg);
 int status_of(const std::exception& ex);
 void launch_adam(Handle* h, float grad_scale);  // hyper-parameters from h->d_step
+void launch_adam_part(Handle* h, float grad_scale, int part, cudaStream_t stream);  // 0: [W2|b2], 1: [W1T|b1]
 void launch_set_step(Handle* h, uint64_t call, int64_t t, double lr, double b1, double b2, double eps);
 
 // Kernel launch on the handle's stream; with Handle::pdl the launch carries the programmatic
@@ -218,12 +221,13 @@ struct Handle {
   void* nccl_comm = nullptr;
   int nranks = 1, rank = 0;
   cudaStream_t cstream = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_dg1 = nullptr;
   int gemm_sm_reserve = 0;
   // concurrent backward: gW2 (and its all-reduce) on cstream with gw2_sms SMs while dg1 -> dz1 ->
   // gW1 use the rest (gemm_sm_cap limits the persistent GEMM grids; 0 = no cap)
   bool concurrent_bw = true;
   int gw2_sms = 72;
+  int adam_w2_sms = 100;  // SMs' worth of blocks for the [W2 | b2] Adam beside dz1 -> gW1 (VQMC_ADAM_SMS)
   int gemm_sm_cap = 0;
   int gw1_splits = 4;  // max split-K of the gW1 GEMM (1: direct epilogue, no finalize; VQMC_GW1_SPLITS; 4 measured best)
 

@@ -518,10 +518,16 @@ __device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, fl
   }
 }
 
-__global__ void __launch_bounds__(256, 4) adam_kernel(int64_t total, float scale, const StepParams* __restrict__ sp,
-                                                   float* __restrict__ P, const float* __restrict__ G,
-                                                   float* __restrict__ M, float* __restrict__ V,
-                                                   double* __restrict__ gpart, unsigned* __restrict__ done,
+// Adam over the element range [lo, hi) of the live buffer.  The training step runs it as up to
+// two launches (the [W2 | b2] range right after its gradient and the W1 GEMM's last read of W2,
+// concurrently with the rest of the backward; then the [W1T | b1] range): every launch writes
+// its per-block ||g||^2 partials at gpart[block_base + block], and the last block of ALL launches
+// (a shared counter up to total_blocks) sums them in block order and advances the step counters.
+__global__ void __launch_bounds__(256, 4) adam_kernel(int64_t lo, int64_t hi, float scale,
+                                                   const StepParams* __restrict__ sp, float* __restrict__ P,
+                                                   const float* __restrict__ G, float* __restrict__ M,
+                                                   float* __restrict__ V, double* __restrict__ gpart,
+                                                   int block_base, int total_blocks, unsigned* __restrict__ done,
                                                    double* __restrict__ gnorm2, AdamOut o) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
@@ -536,8 +542,15 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t total, float scale
     const float mh = m * ibc1, vh = v * ibc2;
     p = p - lr * (mh / (sqrtf(vh) + eps));
   };
-  const int64_t nq = total / 4;
+  // float4 groups inside [lo, hi); scalar heads / tails
+  const int64_t q_lo = (lo + 3) / 4, q_hi = hi / 4;
+  const int64_t nq = q_hi > q_lo ? q_hi - q_lo : 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  G += 4 * q_lo;
+  M += 4 * q_lo;
+  V += 4 * q_lo;
+  P += 4 * q_lo;
+  const int64_t t_off = 4 * q_lo;  // element index of the shifted base
   const int64_t w2_bulk0 = (int64_t)o.Hd * o.h, w2_end = o.off_b2 - o.off_w2;  // W2 rows >= Hd
   constexpr int U = 2;  // float4 groups per thread per iteration: all loads in flight before any math
   for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < nq; q0 += U * stride) {
@@ -563,7 +576,7 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t total, float scale
       reinterpret_cast<float4*>(M)[q] = m4[u];
       reinterpret_cast<float4*>(V)[q] = v4[u];
       reinterpret_cast<float4*>(P)[q] = p4[u];
-      const int64_t t = 4 * q;
+      const int64_t t = t_off + 4 * q;
       const int64_t w = t - o.off_w2;
       if (o.vec_w2 && w >= w2_bulk0 && w < w2_end) {
         // bulk of W2 (rows >= Hd): 4 consecutive entries of one row -> 8-byte stores of both halves
@@ -583,7 +596,14 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t total, float scale
     sq += (double)sqf;  // (at most 8 fp32 terms per partial: ||g||^2 keeps ~fp32-grade relative error)
     sqf = 0.f;
   }
-  for (int64_t t = 4 * nq + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += stride) {
+  G -= t_off;
+  M -= t_off;
+  V -= t_off;
+  P -= t_off;
+  const int64_t e_head = nq > 0 ? 4 * q_lo : hi;  // scalar elements: [lo, 4 q_lo) and [4 q_hi, hi)
+  const int64_t n_head = e_head - lo, n_tail = nq > 0 ? hi - 4 * q_hi : 0;
+  for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n_head + n_tail; x += stride) {
+    const int64_t t = x < n_head ? lo + x : 4 * q_hi + (x - n_head);
     float g = G[t], m = M[t], v = V[t], p = P[t];
     upd(g, m, v, p);
     M[t] = m;
@@ -601,16 +621,16 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t total, float scale
   if (threadIdx.x == 0) {
     double s = 0.0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-    gpart[blockIdx.x] = s;
+    gpart[block_base + blockIdx.x] = s;
     __threadfence();
-    last = atomicAdd(done, 1u) == gridDim.x - 1;
+    last = atomicAdd(done, 1u) == (unsigned)total_blocks - 1;
   }
   __syncthreads();
   if (!last) return;
   {  // fixed-order final sum by the last block: strided thread sums, then a fixed shuffle tree
     __threadfence();
     double s = 0.0;
-    for (unsigned i = threadIdx.x; i < gridDim.x; i += blockDim.x) s += ((volatile double*)gpart)[i];
+    for (int i = threadIdx.x; i < total_blocks; i += blockDim.x) s += ((volatile double*)gpart)[i];
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -783,9 +803,14 @@ void launch_backward(Handle* H, int B, bool wg1_done) {
 
 // dg1 -> dz1 -> gW1: the W1 / b1 part of the gradient (independent of gW2)
 void launch_backward_tail(Handle* H, int B) {
+  launch_dg1_umma(H, B);  // E = D . W2m (split-K partials): the step's last read of the W2 pairs
+  launch_backward_after_dg1(H, B);
+}
+
+// dz1 -> gW1 (+ finalize)
+void launch_backward_after_dg1(Handle* H, int B) {
   using namespace bwcfg;
   const Layout& L = H->L;
-  launch_dg1_umma(H, B);  // E = D . W2m (split-K partials)
   {
     KScope ks(H, "bw_dz1");
     const size_t total = ((size_t)B * L.h + 3) / 4;  // (4 entries per thread)
@@ -826,14 +851,38 @@ void launch_set_step(Handle* H, uint64_t call, int64_t t, double lr, double b1, 
   H->launches++;
 }
 
-void launch_adam(Handle* H, float grad_scale) {
+static AdamOut adam_out(const Handle* H) {
   const Layout& L = H->L;
   const bool vec = (L.h % 4) == 0 && (L.off_w2 % 4) == 0;
-  AdamOut o{L.h, H->hp18, L.Hd, H->head_hpk, H->head_Hdp, H->head_fast, vec, L.off_b1, L.off_w2, L.off_b2, H->d_comp_pos,
-            H->W1Tp, H->W2cp, H->W2h, H->W2l};
+  return AdamOut{L.h, H->hp18, L.Hd, H->head_hpk, H->head_Hdp, H->head_fast, vec, L.off_b1, L.off_w2, L.off_b2,
+                 H->d_comp_pos, H->W1Tp, H->W2cp, H->W2h, H->W2l};
+}
+
+void launch_adam(Handle* H, float grad_scale) {  // the whole live buffer in one launch
   KScope ks(H, "adam");
-  launch_k(H, adam_kernel, dim3(H->gpart_n), dim3(256), 0, L.total, grad_scale, (const StepParams*)H->d_step, H->P,
-           (const float*)H->G, H->Mo, H->Vo, H->d_gpart, H->d_done, H->d_scal, o);
+  launch_k(H, adam_kernel, dim3(H->gpart_n), dim3(256), 0, (int64_t)0, H->L.total, grad_scale,
+           (const StepParams*)H->d_step, H->P, (const float*)H->G, H->Mo, H->Vo, H->d_gpart, 0, H->gpart_n, H->d_done,
+           H->d_scal, adam_out(H));
+  LAUNCH_CHECK();
+  H->launches++;
+}
+
+// Adam split at off_w2: part 0 = [off_w2, total) ([W2 | b2]: ~99% of the parameters) with
+// blocks0 blocks on `stream0`, part 1 = [0, off_w2) ([W1T | b1]) on the handle's stream.
+void launch_adam_part(Handle* H, float grad_scale, int part, cudaStream_t stream) {
+  const Layout& L = H->L;
+  // part 0 runs beside dz1 -> gW1: 4 blocks on each of the SMs gW2 used (4 x 256 threads fill an SM)
+  const int blocks0 = std::min(H->gpart_n - H->gpart_n / 16, 4 * std::max(2, H->adam_w2_sms));
+  const int blocks1 = H->gpart_n / 16;
+  const int64_t lo = part == 0 ? L.off_w2 : 0, hi = part == 0 ? L.total : L.off_w2;
+  const int nb = part == 0 ? blocks0 : blocks1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = dim3(nb);
+  cfg.blockDim = dim3(256);
+  cfg.stream = stream;
+  VQMC_CUDA(cudaLaunchKernelEx(&cfg, adam_kernel, lo, hi, grad_scale, (const StepParams*)H->d_step, H->P,
+                               (const float*)H->G, H->Mo, H->Vo, H->d_gpart, part == 0 ? 0 : blocks0, blocks0 + blocks1,
+                               H->d_done, H->d_scal, adam_out(H)));
   LAUNCH_CHECK();
   H->launches++;
 }
