@@ -15,6 +15,7 @@
 #include <cmath>
 
 #include "device_common.cuh"
+#include "adam.cuh"
 #include "internal.cuh"
 #include "ptx.cuh"
 
@@ -471,53 +472,6 @@ __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __re
 // derives from the updated parameters: the squared norm of the reduced gradient (last-block
 // reduction, fixed order; trainer.cpp:253), the tf32 split of W2 for the GEMMs and the head
 // sampler's padded / completion-ordered copies of the head blocks.
-// head v3 staging order (head.cu): row r of word m = r / 32 keeps entry k (k >= 32 m) at
-// 128 (t >> 2) + 4 (k & 31) + (t & 3), t = k / 32 - m; entries of earlier words are not staged.
-__device__ __forceinline__ int head_rel_pos_dev(int r, int k) {
-  const int t = (k >> 5) - (r >> 5);
-  return t < 0 ? -1 : 128 * (t >> 2) + 4 * (k & 31) + (t & 3);
-}
-
-struct AdamOut {
-  int h, hp18, Hd, hpk, Hdp;
-  bool perm;  // head staging copies are lane-permuted (head v3)
-  bool vec_w2;  // h % 4 == 0 and off_w2 % 4 == 0: a group of 4 never straddles two W2 rows
-  int64_t off_b1, off_w2, off_b2;
-  const int* comp_pos;  // completion slot of hidden unit k
-  float* W1Tp;
-  float* W2cp;
-  __half* W2h;  // fp16 pair of [W2m | b2], row stride hp18
-  __half* W2l;
-};
-
-__device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, float p) {
-  // (32-bit index math: the live buffer is < 2^31 entries, checked at handle creation)
-  if (t < o.off_b1) {  // W1T[j][k]
-    const unsigned tt = (unsigned)t, j = tt / (unsigned)o.h, k = tt - j * (unsigned)o.h;
-    if (!o.perm) {
-      o.W1Tp[(size_t)j * o.hpk + k] = p;
-    } else {
-      const int pos = head_rel_pos_dev((int)j, (int)k);
-      if (pos >= 0) o.W1Tp[(size_t)j * o.hpk + pos] = p;
-    }
-  } else if (t >= o.off_w2 && t < o.off_b2) {  // W2[i][k]
-    const unsigned u = (unsigned)(t - o.off_w2), i = u / (unsigned)o.h, k = u - i * (unsigned)o.h;
-    ptx::split_f16(p, o.W2h[(size_t)i * o.hp18 + k], o.W2l[(size_t)i * o.hp18 + k]);
-    if ((int)i < o.Hd) {
-      const int c = o.comp_pos[k];
-      if (!o.perm) {
-        o.W2cp[(size_t)c * o.Hdp + i] = p;
-      } else {
-        const int pos = head_rel_pos_dev(c, (int)i);
-        if (pos >= 0) o.W2cp[(size_t)c * o.Hdp + pos] = p;
-      }
-    }
-  } else if (t >= o.off_b2) {  // b2[i]: column h of the W2 pair (the tail GEMM's bias column)
-    const size_t i = (size_t)(t - o.off_b2);
-    ptx::split_f16(p, o.W2h[i * o.hp18 + o.h], o.W2l[i * o.hp18 + o.h]);
-  }
-}
-
 // Adam over the element range [lo, hi) of the live buffer.  The training step runs it as up to
 // two launches (the [W2 | b2] range right after its gradient and the W1 GEMM's last read of W2,
 // concurrently with the rest of the backward; then the [W1T | b1] range): every launch writes
@@ -531,16 +485,14 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t lo, int64_t hi, fl
                                                    double* __restrict__ gnorm2, AdamOut o) {
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  const float lr = sp->lr, b1 = sp->b1, b2 = sp->b2, eps = sp->eps, ibc1 = 1.f / sp->bc1, ibc2 = 1.f / sp->bc2;
+  AdamHyper hp;
+  hp.load(sp);
   float sqf = 0.f;  // fp32 partial of ||g||^2 per element group, summed into fp64 per thread
   double sq = 0.0;
   auto upd = [&](float g, float& m, float& v, float& p) {
     g *= scale;
     sqf = fmaf(g, g, sqf);
-    m = b1 * m + (1.f - b1) * g;
-    v = b2 * v + (1.f - b2) * (g * g);
-    const float mh = m * ibc1, vh = v * ibc2;
-    p = p - lr * (mh / (sqrtf(vh) + eps));
+    hp.update(g, m, v, p);
   };
   // float4 groups inside [lo, hi); scalar heads / tails
   const int64_t q_lo = (lo + 3) / 4, q_hi = hi / 4;
