@@ -40,6 +40,7 @@ extern "C" {
 #define VQMC_ERR_NUMERIC 2 /* std::runtime_error (numerical) in the reference */
 #define VQMC_ERR_CUDA 3
 #define VQMC_ERR_NCCL 4
+#define VQMC_ERR_SR 5 /* SrSolveError (optimizer.hpp:46-55): SR CG missed its residual contract */
 
 typedef struct vqmc_gpu vqmc_gpu_t;
 
@@ -114,6 +115,26 @@ int vqmc_gpu_adam_reset(vqmc_gpu_t* g);
  * std::barrier phases :174-279): one NCCL communicator per rank. */
 int vqmc_gpu_comm_unique_id(uint8_t id_out[128]);
 int vqmc_gpu_comm_init(vqmc_gpu_t* g, const uint8_t id[128], int nranks, int rank);
+
+/* sr_direction (optimizer.cpp:64-82) with the Fisher estimate of the configurations `bits`
+ * (FisherEstimate over score_matrix rows, estimator.hpp:146-168, models.cpp:221-244; centred
+ * unless centered == 0): solves (F + lambda I) delta = grad by conjugate gradient on the GPU
+ * (the scores are never materialised), accepting the solution only if
+ * ||(F + lambda I) delta - grad|| <= tol ||grad|| (else VQMC_ERR_SR, with iterations_out /
+ * residual_out set).  grad and delta_out: d entries, reference order. */
+int vqmc_gpu_sr_direction(vqmc_gpu_t* g, const uint32_t* bits, int B, const double* grad, double lambda, double tol,
+                          int max_iterations, int centered, double* delta_out, int* iterations_out,
+                          double* residual_out);
+
+/* One SGD + SR iteration (OptimizerKind::kSgdSr; trainer.cpp:150-282 with :165-168, :189-199,
+ * :223-225) on this GPU: sampling, local energies, REINFORCE gradient, the mean over the
+ * `workers` segments, the SR direction over the pooled scores of all workers*minibatch samples,
+ * and params -= lr * direction.  fallback != 0: a CG failure applies the raw gradient instead
+ * (SrConfig::fallback); otherwise VQMC_ERR_SR and the parameters are unchanged.  Single GPU. */
+int vqmc_gpu_train_step_sr(vqmc_gpu_t* g, int minibatch, int workers, const double* uniforms, uint64_t seed,
+                           uint64_t stream0, uint64_t call, double lr, double lambda, double tol, int max_iterations,
+                           int fallback, int centered, vqmc_step_stats_t* stats_out, int* iterations_out,
+                           double* residual_out);
 
 /* One fused VQMC iteration (worker_body, trainer.cpp:150-282) for `workers`
  * data-parallel workers of `minibatch` samples each on this GPU (worker s of

@@ -66,6 +66,10 @@ def lib():
     L.oracle_time_reference_step.argtypes = [C.c_int, C.c_int, _ip, C.c_int64, C.c_int, C.c_int, C.c_uint64,
                                              C.c_int, _dp]
     L.oracle_goodness_of_fit.argtypes = [C.c_int, _dp, C.c_int64, _u8, _dp]
+    L.oracle_set_train_sr.argtypes = [C.c_double, C.c_double, C.c_int, C.c_int, C.c_int]
+    L.oracle_score_matrix.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_int, _u8, _dp]
+    L.oracle_sr_direction.argtypes = [C.c_int64, C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_double, C.c_int,
+                                      _dp, C.POINTER(C.c_int), C.POINTER(C.c_double)]
     _lib = L
     return L
 
@@ -237,15 +241,50 @@ def brute_force_maxcut(n, edges):
     return int(v), int(am.value)
 
 
+class SrSolveError(RuntimeError):
+    """SR conjugate gradient did not converge (optimizer.hpp:46-55)."""
+
+    def __init__(self, msg, residual, iterations):
+        super().__init__(msg)
+        self.residual, self.iterations = residual, iterations
+
+
+def score_matrix(m: Made, x):
+    """score_matrix (models.cpp:221-244): B x d rows 2 grad log psi, reference flatten order."""
+    x = np.ascontiguousarray(x, np.uint8)
+    out = np.empty((x.shape[0], m.d))
+    _check(lib().oracle_score_matrix(m.n, m.h, m.degrees, m.theta, x.shape[0], x, out))
+    return out
+
+
+def sr_direction(scores, grad, lam=1e-3, tol=1e-6, max_iterations=200, centered=True):
+    """sr_direction (optimizer.cpp:64-82) over explicit score rows; returns (delta, iters, resid)."""
+    S = np.ascontiguousarray(scores, np.float64)
+    g = np.ascontiguousarray(grad, np.float64)
+    out = np.empty(S.shape[1]); it = C.c_int(0); res = C.c_double(0.0)
+    rc = lib().oracle_sr_direction(S.shape[1], S.shape[0], S, 1 if centered else 0, g, lam, tol, max_iterations,
+                                   out, C.byref(it), C.byref(res))
+    if rc == -3:
+        raise SrSolveError(lib().oracle_last_error().decode(), res.value, it.value)
+    _check(rc)
+    return out, it.value, res.value
+
+
+_OPT = {"sgd": 0, "adam": 1, "sgd_sr": 2}
+
+
 def train(n, edges, h=0, optimizer="adam", lr=0.0, iterations=300, workers=1, minibatch=1024,
-          eval_batch=1024, seed=0, sampler_mode=0, threads=True, want_first_grad=False):
+          eval_batch=1024, seed=0, sampler_mode=0, threads=True, want_first_grad=False,
+          sr_lambda=1e-3, sr_tol=1e-6, sr_max_iterations=200, sr_fallback=False, sr_centered=True):
     """Restated vqmc::train for MADE+AUTO on a Max-Cut instance (trainer.cpp:111-322)."""
     e = np.ascontiguousarray(edges, np.int32).reshape(-1)
     hh = h if h > 0 else default_made_hidden(n)
     d = 2 * hh * n + hh + n
     stats = np.empty((iterations, 4)); ev = np.empty(4); theta = np.empty(d)
     g0 = np.empty(d) if want_first_grad else None
-    _check(lib().oracle_train(n, hh, e, e.size // 2, 1 if optimizer == "adam" else 0, lr, iterations,
+    _check(lib().oracle_set_train_sr(sr_lambda, sr_tol, sr_max_iterations, 1 if sr_fallback else 0,
+                                     1 if sr_centered else 0))
+    _check(lib().oracle_train(n, hh, e, e.size // 2, _OPT[optimizer], lr, iterations,
                               workers, minibatch, eval_batch, seed, sampler_mode, 1 if threads else 0,
                               _ptr(stats), _ptr(ev), _ptr(theta), _ptr(g0)))
     out = dict(stats=stats, final_energy=ev[0], final_energy_std=ev[1], best_cut=ev[2], mean_cut=ev[3],

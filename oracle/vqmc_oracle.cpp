@@ -47,6 +47,10 @@ using dgemm_fn = void (*)(int, int, int, int, int, int, double, const double*, i
                           const double*, int, double, double*, int);
 using setthreads_fn = void (*)(int);
 dgemm_fn g_dgemm = nullptr;
+using potrf_fn = int (*)(int, char, int, double*, int);
+using potrs_fn = int (*)(int, char, int, int, const double*, int, double*, int);
+potrf_fn g_potrf = nullptr;  // LAPACKE Cholesky (SR's dense solve), same library
+potrs_fn g_potrs = nullptr;
 bool g_blas_probed = false;
 std::string g_blas_path;
 
@@ -73,6 +77,8 @@ void probe_blas() {
       if (st) st(1);
       g_dgemm = f;
       g_blas_path = p;
+      g_potrf = reinterpret_cast<potrf_fn>(dlsym(h, "scipy_LAPACKE_dpotrf"));
+      g_potrs = reinterpret_cast<potrs_fn>(dlsym(h, "scipy_LAPACKE_dpotrs"));
       return;
     }
   }
@@ -543,6 +549,189 @@ void adam_step(Adam& st, std::vector<double>& p, const std::vector<double>& g) {
 }
 
 // ---------------------------------------------------------------------------
+// SR: score_matrix (proj/src/models.cpp:221-244), FisherEstimate
+// (proj/include/vqmc/estimator.hpp:146-168), sr_direction / conjugate_gradient
+// (proj/src/optimizer.cpp:36-92), SrConfig defaults (proj/include/vqmc/optimizer.hpp:38-45).
+// ---------------------------------------------------------------------------
+struct SrSolveError : std::runtime_error {
+  SrSolveError(double residual, int iterations)
+      : std::runtime_error("SR conjugate gradient did not converge (relative residual " +
+                           std::to_string(residual) + " after " + std::to_string(iterations) +
+                           " iterations)"),
+        residual(residual),
+        iterations(iterations) {}
+  double residual;
+  int iterations;
+};
+
+// models.cpp:221-244: row b = 2 * grad_theta log psi(x_b) in the flatten order of get_theta.
+std::vector<double> score_matrix(const Made& m, const double* X, int B) {
+  const int n = m.n, h = m.h;
+  const long d = m.d();
+  const Fwd f = made_forward(m, X, B);
+  std::vector<double> dz2((size_t)B * n);
+  for (int b = 0; b < B; ++b)
+    for (int i = 0; i < n; ++i) {  // made_dz2 (models.cpp:163-171), unweighted
+      const size_t t = (size_t)b * n + i;
+      double v = 0.5 * (X[t] - f.p_raw[t]);
+      if (f.p_raw[t] <= kProbEps || f.p_raw[t] >= 1.0 - kProbEps) v = 0.0;
+      dz2[t] = v;
+    }
+  std::vector<double> A2((size_t)n * h);
+  for (size_t t = 0; t < A2.size(); ++t) A2[t] = m.M2[t] * m.W2[t];
+  std::vector<double> dz1((size_t)B * h, 0.0);
+  gemm(false, false, B, h, n, dz2.data(), n, A2.data(), h, 0.0, dz1.data(), h);  // dg1_b = a2^T dz2_b
+  for (size_t t = 0; t < dz1.size(); ++t) dz1[t] = f.z1[t] > 0.0 ? dz1[t] : 0.0;
+  std::vector<double> S((size_t)B * d, 0.0);
+  for (int b = 0; b < B; ++b) {
+    double* row = &S[(size_t)b * d];
+    double* sW1 = row;
+    double* sb1 = sW1 + (size_t)h * n;
+    double* sW2 = sb1 + h;
+    double* sb2 = sW2 + (size_t)n * h;
+    const double* x = X + (size_t)b * n;
+    for (int k = 0; k < h; ++k) {
+      const double g = dz1[(size_t)b * h + k];
+      for (int j = 0; j < n; ++j) sW1[(size_t)k * n + j] = 2.0 * g * x[j] * m.M1[(size_t)k * n + j];
+      sb1[k] = 2.0 * g;
+    }
+    for (int i = 0; i < n; ++i) {
+      const double g = dz2[(size_t)b * n + i];
+      for (int k = 0; k < h; ++k)
+        sW2[(size_t)i * h + k] = 2.0 * g * f.g1[(size_t)b * h + k] * m.M2[(size_t)i * h + k];
+      sb2[i] = 2.0 * g;
+    }
+  }
+  return S;
+}
+
+// estimator.hpp:146-168: centred (by default) score rows; F v = S^T (S v) / B.
+struct Fisher {
+  std::vector<double> S;
+  int B = 0;
+  long d = 0;
+  Fisher(std::vector<double> scores, int B_, long d_, bool centered) : S(std::move(scores)), B(B_), d(d_) {
+    if (B < 2) throw std::invalid_argument("Fisher needs at least two samples");
+    if (!centered) return;
+    for (long p = 0; p < d; ++p) {
+      double s = 0.0;
+      for (int b = 0; b < B; ++b) s += S[(size_t)b * d + p];
+      const double mean = s / static_cast<double>(B);
+      for (int b = 0; b < B; ++b) S[(size_t)b * d + p] -= mean;
+    }
+  }
+  std::vector<double> apply(const std::vector<double>& v) const {
+    std::vector<double> t(B, 0.0), out(d, 0.0);
+    gemm(false, false, B, 1, (int)d, S.data(), (int)d, v.data(), 1, 0.0, t.data(), 1);
+    gemm(true, false, (int)d, 1, B, S.data(), (int)d, t.data(), 1, 0.0, out.data(), 1);
+    for (double& x : out) x /= static_cast<double>(B);
+    return out;
+  }
+  std::vector<double> dense() const {
+    std::vector<double> F((size_t)d * d, 0.0);
+    gemm(true, false, (int)d, (int)d, B, S.data(), (int)d, S.data(), (int)d, 0.0, F.data(), (int)d);
+    for (double& x : F) x /= static_cast<double>(B);
+    return F;
+  }
+};
+
+double dot(const std::vector<double>& a, const std::vector<double>& b) {
+  double s = 0.0;
+  for (size_t i = 0; i < a.size(); ++i) s += a[i] * b[i];
+  return s;
+}
+
+// Cholesky solve of the SPD system (Eigen's LDLT in the reference; same solution for SPD input).
+std::vector<double> spd_solve(std::vector<double> A, long d, const std::vector<double>& rhs) {
+  std::vector<double> x = rhs;
+  probe_blas();
+  if (g_potrf && g_potrs) {
+    if (g_potrf(kRowMajor, 'L', (int)d, A.data(), (int)d) != 0) throw std::runtime_error("SR system not SPD");
+    g_potrs(kRowMajor, 'L', (int)d, 1, A.data(), (int)d, x.data(), 1);
+    return x;
+  }
+  for (long j = 0; j < d; ++j) {  // plain lower Cholesky
+    double s = A[(size_t)j * d + j];
+    for (long k = 0; k < j; ++k) s -= A[(size_t)j * d + k] * A[(size_t)j * d + k];
+    if (!(s > 0.0)) throw std::runtime_error("SR system not SPD");
+    const double l = std::sqrt(s);
+    A[(size_t)j * d + j] = l;
+    for (long i = j + 1; i < d; ++i) {
+      double t = A[(size_t)i * d + j];
+      for (long k = 0; k < j; ++k) t -= A[(size_t)i * d + k] * A[(size_t)j * d + k];
+      A[(size_t)i * d + j] = t / l;
+    }
+  }
+  for (long i = 0; i < d; ++i) {
+    double t = x[i];
+    for (long k = 0; k < i; ++k) t -= A[(size_t)i * d + k] * x[k];
+    x[i] = t / A[(size_t)i * d + i];
+  }
+  for (long i = d - 1; i >= 0; --i) {
+    double t = x[i];
+    for (long k = i + 1; k < d; ++k) t -= A[(size_t)k * d + i] * x[k];
+    x[i] = t / A[(size_t)i * d + i];
+  }
+  return x;
+}
+
+struct SrCfg {
+  double lambda = 1e-3, tol = 1e-6;
+  int max_iterations = 200;
+};
+
+// optimizer.cpp:46-92.  `iters` / `resid` report the solve (0 iterations for the dense path).
+std::vector<double> sr_direction(const SrCfg& cfg, const std::vector<double>& grad, const Fisher& F,
+                                 int* iters, double* resid) {
+  const long d = (long)grad.size();
+  const double gnorm = std::sqrt(dot(grad, grad));
+  if (d <= 2000) {
+    std::vector<double> A = F.dense();
+    for (long i = 0; i < d; ++i) A[(size_t)i * d + i] += cfg.lambda;
+    const std::vector<double> delta = spd_solve(A, d, grad);
+    double r2 = 0.0;
+    for (long i = 0; i < d; ++i) {
+      double t = -grad[i];
+      for (long k = 0; k < d; ++k) t += A[(size_t)i * d + k] * delta[k];
+      r2 += t * t;
+    }
+    const double residual = std::sqrt(r2);
+    if (iters) *iters = 0;
+    if (resid) *resid = gnorm > 0.0 ? residual / gnorm : 0.0;
+    if (residual > cfg.tol * gnorm && gnorm > 0.0) throw SrSolveError(residual / gnorm, 0);
+    return delta;
+  }
+  std::vector<double> x(d, 0.0);
+  int it_done = 0;
+  double rel = 0.0;
+  if (gnorm != 0.0) {
+    std::vector<double> r = grad, p = r;
+    double rs = dot(r, r);
+    for (int it = 0; it < cfg.max_iterations; ++it) {
+      std::vector<double> ap = F.apply(p);
+      for (long i = 0; i < d; ++i) ap[i] += cfg.lambda * p[i];
+      const double alpha = rs / dot(p, ap);
+      for (long i = 0; i < d; ++i) x[i] += alpha * p[i];
+      for (long i = 0; i < d; ++i) r[i] -= alpha * ap[i];
+      it_done = it + 1;
+      const double rs_next = dot(r, r);
+      if (std::sqrt(rs_next) <= cfg.tol * gnorm) {
+        rs = rs_next;
+        break;
+      }
+      const double beta = rs_next / rs;
+      for (long i = 0; i < d; ++i) p[i] = r[i] + beta * p[i];
+      rs = rs_next;
+    }
+    rel = std::sqrt(rs) / gnorm;
+  }
+  if (iters) *iters = it_done;
+  if (resid) *resid = rel;
+  if (rel > cfg.tol) throw SrSolveError(rel, it_done);
+  return x;
+}
+
+// ---------------------------------------------------------------------------
 // L6 trainer: proj/src/trainer.cpp:324-335 (allreduce_mean), :111-306 (train_impl)
 // ---------------------------------------------------------------------------
 std::vector<double> allreduce_mean(const std::vector<std::vector<double>>& vs) {
@@ -642,6 +831,10 @@ const char* oracle_blas_path() {
 
 #define ORACLE_TRY try {
 #define ORACLE_CATCH                 \
+  }                                  \
+  catch (const SrSolveError& ex) {   \
+    g_error = ex.what();             \
+    return -3;                       \
   }                                  \
   catch (const std::exception& ex) { \
     g_error = ex.what();             \
@@ -836,6 +1029,55 @@ int64_t oracle_brute_force_maxcut(int n, const int32_t* edges, int64_t E, uint64
 // the incremental sampler (same uniforms, fp64 order differs), 0 the n-forward
 // reference sampler.  `first_grad_out` (d, optional) receives iteration 0's
 // reduced gradient (the gradient_observer hook, trainer.hpp:57).
+// SR settings used by oracle_train with optimizer 2 (SGD + SR; SrConfig, optimizer.hpp:38-45).
+static SrCfg g_train_sr;
+static bool g_train_sr_fallback = false, g_train_sr_centered = true;
+int oracle_set_train_sr(double lambda, double tol, int max_iterations, int fallback, int centered) {
+  g_train_sr.lambda = lambda;
+  g_train_sr.tol = tol;
+  g_train_sr.max_iterations = max_iterations;
+  g_train_sr_fallback = fallback != 0;
+  g_train_sr_centered = centered != 0;
+  return 0;
+}
+
+// score_matrix rows (B x d) of 0/1 configurations.
+int oracle_score_matrix(int n, int h, const int* deg, const double* theta, int B, const uint8_t* x,
+                        double* scores_out) {
+  ORACLE_TRY
+  const Made m = made_from(n, h, deg, theta);
+  const auto X = to_double(x, (size_t)B * n);
+  const auto S = score_matrix(m, X.data(), B);
+  std::copy(S.begin(), S.end(), scores_out);
+  ORACLE_CATCH
+}
+
+// sr_direction over explicit score rows (B x d).  Returns -3 on SrSolveError (iters / resid
+// still written).
+int oracle_sr_direction(int64_t d, int B, const double* scores, int centered, const double* grad,
+                        double lambda, double tol, int max_iterations, double* delta_out, int* iters_out,
+                        double* resid_out) {
+  int it = 0;
+  double res = 0.0;
+  try {
+    Fisher F(std::vector<double>(scores, scores + (size_t)B * d), B, (long)d, centered != 0);
+    SrCfg cfg{lambda, tol, max_iterations};
+    const auto delta = sr_direction(cfg, std::vector<double>(grad, grad + d), F, &it, &res);
+    std::copy(delta.begin(), delta.end(), delta_out);
+  } catch (const SrSolveError& ex) {
+    g_error = ex.what();
+    if (iters_out) *iters_out = ex.iterations;
+    if (resid_out) *resid_out = ex.residual;
+    return -3;
+  } catch (const std::exception& ex) {
+    g_error = ex.what();
+    return -1;
+  }
+  if (iters_out) *iters_out = it;
+  if (resid_out) *resid_out = res;
+  return 0;
+}
+
 int oracle_train(int n, int h, const int32_t* edges, int64_t E, int optimizer, double lr,
                  int iterations, int workers, int minibatch, int eval_batch, uint64_t seed,
                  int sampler_mode, int use_threads, double* stats_out, double* eval_out,
@@ -859,6 +1101,9 @@ int oracle_train(int n, int h, const int32_t* edges, int64_t E, int optimizer, d
   for (int w = 0; w < L; ++w) rngs.push_back(make_stream(seed, w + 1));
   auto eval_rng = make_stream(seed, kEvalStream);
   std::vector<std::vector<double>> grads(L), locals(L);
+  const bool use_sr = optimizer == 2;
+  const long d = model.d();
+  std::vector<double> shared_scores(use_sr ? (size_t)L * mbs * d : 0);
   for (int it = 0; it < iterations; ++it) {
     const double t0 = now_s();
     auto work = [&](int w) {
@@ -867,6 +1112,10 @@ int oracle_train(int n, int h, const int32_t* edges, int64_t E, int optimizer, d
                            : auto_sample(model, mbs, &rngs[w], nullptr, nullptr);
       locals[w] = local_energy_maxcut(n, e, s.X.data(), mbs);
       grads[w] = gradient_from_locals(model, s.X.data(), mbs, locals[w]);
+      if (use_sr) {  // trainer.cpp:165-168: rows w * mbs .. of the shared score matrix
+        const auto S = score_matrix(model, s.X.data(), mbs);
+        std::copy(S.begin(), S.end(), shared_scores.begin() + (size_t)w * mbs * d);
+      }
     };
     if (use_threads && L > 1) {
       std::vector<std::thread> th;
@@ -879,6 +1128,16 @@ int oracle_train(int n, int h, const int32_t* edges, int64_t E, int optimizer, d
     if (it == 0 && first_grad_out) std::copy(reduced.begin(), reduced.end(), first_grad_out);
     if (optimizer == 1) {
       adam_step(adam, params, reduced);
+    } else if (use_sr) {  // trainer.cpp:189-199 (natural-gradient direction), :223-225 (SGD step)
+      std::vector<double> update;
+      try {
+        Fisher F(shared_scores, L * mbs, d, g_train_sr_centered);
+        update = sr_direction(g_train_sr, reduced, F, nullptr, nullptr);
+      } catch (const SrSolveError&) {
+        if (!g_train_sr_fallback) throw;
+        update = reduced;
+      }
+      for (size_t t = 0; t < params.size(); ++t) params[t] = params[t] - lr * update[t];
     } else {
       for (size_t t = 0; t < params.size(); ++t) params[t] = params[t] - lr * reduced[t];
     }

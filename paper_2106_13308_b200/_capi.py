@@ -17,7 +17,7 @@ if not os.path.exists(LIB_PATH):
 
 lib = C.CDLL(LIB_PATH)
 
-VQMC_OK, VQMC_ERR_INVALID, VQMC_ERR_NUMERIC, VQMC_ERR_CUDA, VQMC_ERR_NCCL = 0, 1, 2, 3, 4
+VQMC_OK, VQMC_ERR_INVALID, VQMC_ERR_NUMERIC, VQMC_ERR_CUDA, VQMC_ERR_NCCL, VQMC_ERR_SR = 0, 1, 2, 3, 4, 5
 
 _vp = C.c_void_p
 _i32, _i64, _u64, _dbl = C.c_int32, C.c_int64, C.c_uint64, C.c_double
@@ -48,6 +48,10 @@ _SIGS = {
     "vqmc_gpu_comm_init": [_vp, _vp, C.c_int, C.c_int],
     "vqmc_gpu_train_step": [_vp, C.c_int, C.c_int, _vp, _u64, _u64, _u64, _dbl, _dbl, _dbl, _dbl, _i64,
                             C.POINTER(StepStats)],
+    "vqmc_gpu_sr_direction": [_vp, _vp, C.c_int, _vp, _dbl, _dbl, C.c_int, C.c_int, _vp, C.POINTER(C.c_int),
+                              C.POINTER(_dbl)],
+    "vqmc_gpu_train_step_sr": [_vp, C.c_int, C.c_int, _vp, _u64, _u64, _u64, _dbl, _dbl, _dbl, C.c_int, C.c_int,
+                               C.c_int, C.POINTER(StepStats), C.POINTER(C.c_int), C.POINTER(_dbl)],
     "vqmc_pooled_stats": [_i64, _i64, _i64, _i64, C.POINTER(_dbl), C.POINTER(_dbl)],
     "vqmc_gpu_last_cuts": [_vp, _vp, C.c_int],
     "vqmc_gpu_evaluate": [_vp, C.c_int, _vp, _u64, _u64, _u64, _vp],
@@ -87,6 +91,10 @@ class VqmcError(RuntimeError):
         self.code = code
 
 
+class SrSolveError(VqmcError):
+    """SR conjugate gradient missed its residual contract (optimizer.hpp:46-55)."""
+
+
 def check(rc: int) -> None:
     """Map a status code to the reference's exception types (ValueError ~ std::invalid_argument)."""
     if rc == VQMC_OK:
@@ -94,6 +102,8 @@ def check(rc: int) -> None:
     msg = lib.vqmc_last_error().decode()
     if rc == VQMC_ERR_INVALID:
         raise ValueError(msg)
+    if rc == VQMC_ERR_SR:
+        raise SrSolveError(rc, msg)
     raise VqmcError(rc, msg)
 
 

@@ -391,6 +391,67 @@ def sgd_step(params, grad, lr):  # optimizer.hpp:57-59
     return np.asarray(params) - lr * np.asarray(grad)
 
 
+@dataclasses.dataclass
+class SrConfig:  # optimizer.hpp:38-45
+    lr: float = 0.1
+    lam: float = 1e-3           # diagonal regularization (SrConfig::lambda)
+    tol: float = 1e-6           # relative residual
+    max_iterations: int = 200   # CG budget
+    fallback: bool = False      # on CG failure, continue with the raw gradient
+    centered: bool = True       # subtract the mean score before forming F
+
+
+SrSolveError = K.SrSolveError
+
+
+class FisherEstimate:
+    """fisher_estimate(model, configs, centered) (estimator.hpp:146-174).  The B x d score matrix
+    is never formed: the device applies F v = S^T (S v) / B through the model's structure."""
+
+    def __init__(self, model: "MadeModel", configs, centered: bool = True):
+        self.model = model
+        self.bits, self.B = _bits(model, configs)
+        if self.B < 2:
+            raise ValueError("Fisher needs at least two samples")
+        self.centered = centered
+
+    def samples(self) -> int:
+        return self.B
+
+    def dim(self) -> int:
+        return self.model.param_count()
+
+
+def fisher_estimate(model: "MadeModel", configs, centered: bool = True) -> FisherEstimate:
+    return FisherEstimate(model, configs, centered)
+
+
+def sr_direction(cfg: SrConfig, grad, fisher: FisherEstimate, info: Optional[dict] = None) -> np.ndarray:
+    """sr_direction (optimizer.cpp:64-82): solves (F + lambda I) delta = grad (CG on the GPU);
+    raises SrSolveError unless ||(F + lambda I) delta - grad|| <= tol ||grad||."""
+    g = np.ascontiguousarray(grad, np.float64)
+    if g.shape != (fisher.dim(),):
+        raise ValueError("gradient length mismatch")
+    out = np.empty_like(g)
+    it, res = C.c_int(0), C.c_double(0.0)
+    rc = K.lib.vqmc_gpu_sr_direction(fisher.model.device().h, ptr(fisher.bits), fisher.B, ptr(g), cfg.lam, cfg.tol,
+                                     cfg.max_iterations, 1 if fisher.centered else 0, ptr(out), C.byref(it),
+                                     C.byref(res))
+    if info is not None:
+        info.update(iterations=it.value, residual=res.value)
+    check(rc)
+    return out
+
+
+def sr_step(cfg: SrConfig, params, grad, fisher: FisherEstimate) -> np.ndarray:  # optimizer.cpp:84-92
+    try:
+        return np.asarray(params) - cfg.lr * sr_direction(cfg, grad, fisher)
+    except SrSolveError:
+        if not cfg.fallback:
+            raise
+        return np.asarray(params) - cfg.lr * np.asarray(grad)
+
+
 # ---------------------------------------------------------------------------
 # L6 trainer (trainer.hpp)
 # ---------------------------------------------------------------------------
@@ -416,7 +477,7 @@ class StepStats:
 
 @dataclasses.dataclass
 class RunConfig:
-    """The Max-Cut / MADE / AUTO / ADAM slice of RunConfig (trainer.hpp:31-58)."""
+    """The Max-Cut / MADE / AUTO / {ADAM, SGD + SR} slice of RunConfig (trainer.hpp:31-58)."""
     problem: Optional[MaxCutProblem] = None
     hidden: int = 0
     optimizer: str = "adam"
@@ -428,6 +489,7 @@ class RunConfig:
     seed: int = 0
     target: Optional[float] = None
     uniforms: str = "philox"    # "philox" (production) or "mt19937" (reference streams, parity)
+    sr: SrConfig = dataclasses.field(default_factory=SrConfig)
     gradient_observer: Optional[Callable[[int, np.ndarray], None]] = None
     device: int = 0
 
@@ -462,8 +524,8 @@ def _mt_uniforms(streams: List[Stream], n: int, mbs: int) -> np.ndarray:
 
 
 def train(cfg: RunConfig, comm=None) -> RunResult:
-    """vqmc::train for MADE + AUTO + ADAM on a Max-Cut instance (trainer.cpp:111-322), one
-    fused device step per iteration.  `comm` (optional) = (rank, world) of an initialised
+    """vqmc::train for MADE + AUTO + ADAM or SGD + SR on a Max-Cut instance (trainer.cpp:111-322),
+    one fused device step per iteration.  `comm` (optional) = (rank, world) of an initialised
     NCCL communicator on the model's handle; stats are then pooled by the caller."""
     if cfg.problem is None:
         raise ValueError("a Max-Cut problem is required")
@@ -473,8 +535,10 @@ def train(cfg: RunConfig, comm=None) -> RunResult:
         raise ValueError("iterations must be >= 1")
     if cfg.minibatch < 2:
         raise ValueError("minibatch must be >= 2")
-    if cfg.optimizer != "adam":
-        raise ValueError("the B200 path implements the ADAM optimizer (north-star path)")
+    if cfg.optimizer not in ("adam", "sgd_sr"):
+        raise ValueError("the B200 path implements the ADAM and SGD + SR optimizers")
+    if cfg.optimizer == "sgd_sr" and comm is not None and comm[1] > 1:
+        raise ValueError("the SR step runs on one GPU")
     n = cfg.problem.graph.n
     h = cfg.hidden if cfg.hidden > 0 else default_made_hidden(n)
     model = made_init(n, h, cfg.seed)
@@ -494,8 +558,15 @@ def train(cfg: RunConfig, comm=None) -> RunResult:
     for it in range(cfg.iterations):
         t0 = time.perf_counter()
         u = _mt_uniforms(streams, n, mbs) if cfg.uniforms == "mt19937" else None
-        check(K.lib.vqmc_gpu_train_step(dev.h, mbs, L, ptr(u), cfg.seed, stream0, it, lr, 0.9, 0.999, 1e-8,
-                                        it + 1, C.byref(st)))
+        if cfg.optimizer == "sgd_sr":  # trainer.cpp:165-168, 189-199, 223-225
+            cg_it, cg_res = C.c_int(0), C.c_double(0.0)
+            check(K.lib.vqmc_gpu_train_step_sr(dev.h, mbs, L, ptr(u), cfg.seed, stream0, it, lr, cfg.sr.lam,
+                                               cfg.sr.tol, cfg.sr.max_iterations, 1 if cfg.sr.fallback else 0,
+                                               1 if cfg.sr.centered else 0, C.byref(st), C.byref(cg_it),
+                                               C.byref(cg_res)))
+        else:
+            check(K.lib.vqmc_gpu_train_step(dev.h, mbs, L, ptr(u), cfg.seed, stream0, it, lr, 0.9, 0.999, 1e-8,
+                                            it + 1, C.byref(st)))
         dev.device_newer = True
         wall = time.perf_counter() - t0
         result.stats.append(StepStats(st.energy_mean, math.sqrt(st.energy_var), st.grad_norm, wall))

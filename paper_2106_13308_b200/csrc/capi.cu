@@ -22,6 +22,7 @@ void set_error(const std::string& msg) { g_error = msg; }
 
 int status_of(const std::exception& ex) {
   if (dynamic_cast<const CudaError*>(&ex)) return VQMC_ERR_CUDA;
+  if (dynamic_cast<const SrSolveError*>(&ex)) return VQMC_ERR_SR;
   if (dynamic_cast<const std::invalid_argument*>(&ex)) return VQMC_ERR_INVALID;
   return VQMC_ERR_NUMERIC;
 }
@@ -167,6 +168,45 @@ static void live_to_reference(const Handle* H, const std::vector<float>& P, cons
   const int n = L.n, h = L.h, Hd = L.Hd;
   if (base) std::memcpy(out, base, sizeof(double) * H->d);
   else std::memset(out, 0, sizeof(double) * H->d);
+  double* W1 = out;
+  double* b1 = W1 + (size_t)h * n;
+  double* W2 = b1 + h;
+  double* b2 = W2 + (size_t)n * h;
+  for (int j = 0; j < Hd; ++j)
+    for (int k = 0; k < h; ++k)
+      if (j + 1 <= H->degrees[k]) W1[(size_t)k * n + j] = P[L.off_w1t + (size_t)j * h + k];
+  for (int k = 0; k < h; ++k) b1[k] = P[L.off_b1 + k];
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < h; ++k)
+      if (H->degrees[k] < i + 1) W2[(size_t)i * h + k] = P[L.off_w2 + (size_t)i * h + k];
+  for (int i = 0; i < n; ++i) b2[i] = P[L.off_b2 + i];
+}
+
+// reference order fp64 -> live layout fp64 (masked entries dropped)
+static std::vector<double> reference_to_live(const Handle* H, const double* theta) {
+  const Layout& L = H->L;
+  const int n = L.n, h = L.h, Hd = L.Hd;
+  std::vector<double> P((size_t)L.total, 0.0);
+  const double* W1 = theta;
+  const double* b1 = W1 + (size_t)h * n;
+  const double* W2 = b1 + h;
+  const double* b2 = W2 + (size_t)n * h;
+  for (int j = 0; j < Hd; ++j)
+    for (int k = 0; k < h; ++k)
+      P[L.off_w1t + (size_t)j * h + k] = (j + 1 <= H->degrees[k]) ? W1[(size_t)k * n + j] : 0.0;
+  for (int k = 0; k < h; ++k) P[L.off_b1 + k] = b1[k];
+  for (int i = 0; i < n; ++i)
+    for (int k = 0; k < h; ++k)
+      P[L.off_w2 + (size_t)i * h + k] = (H->degrees[k] < i + 1) ? W2[(size_t)i * h + k] : 0.0;
+  for (int i = 0; i < n; ++i) P[L.off_b2 + i] = b2[i];
+  return P;
+}
+
+// live layout fp64 -> reference order fp64 (masked entries 0)
+static void live_to_reference_d(const Handle* H, const std::vector<double>& P, double* out) {
+  const Layout& L = H->L;
+  const int n = L.n, h = L.h, Hd = L.Hd;
+  std::memset(out, 0, sizeof(double) * H->d);
   double* W1 = out;
   double* b1 = W1 + (size_t)h * n;
   double* W2 = b1 + h;
@@ -458,6 +498,7 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   if (H->ev_fork) cudaEventDestroy(H->ev_fork);
   if (H->ev_join) cudaEventDestroy(H->ev_join);
   if (H->ev_dg1) cudaEventDestroy(H->ev_dg1);
+  free_sr(H);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2h, H->W2l, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
                   H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->cpart, H->local, H->w, H->d_wscale, H->d_flag,
@@ -838,6 +879,120 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
     stats_out->best_cut = (int32_t)best;
     stats_out->batch = B;
   }
+  API_CATCH
+}
+
+int vqmc_gpu_sr_direction(vqmc_gpu_t* g, const uint32_t* bits, int B, const double* grad, double lambda, double tol,
+                          int max_iterations, int centered, double* delta_out, int* iterations_out,
+                          double* residual_out) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  if (B < 2) throw std::invalid_argument("Fisher needs at least two samples");  // estimator.hpp:153
+  if (max_iterations < 0) throw std::invalid_argument("max_iterations must be >= 0");
+  H->ensure_batch(B);
+  ensure_sr(H, B);
+  upload_bits(H, bits, B);
+  forward_given(H, B, nullptr);  // G1, D of the configurations
+  launch_dg1_umma(H, B);         // D . W2m partials (dz1 of the scores)
+  const std::vector<double> gl = reference_to_live(H, grad);
+  VQMC_CUDA(cudaMemcpyAsync(H->cg_g, gl.data(), gl.size() * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+  int it = 0;
+  double res = 0.0;
+  const bool ok = sr_solve(H, B, lambda, tol, max_iterations, centered != 0, &it, &res, nullptr);
+  if (iterations_out) *iterations_out = it;
+  if (residual_out) *residual_out = res;
+  if (!ok)
+    throw SrSolveError("SR conjugate gradient did not converge (relative residual " + std::to_string(res) +
+                       " after " + std::to_string(it) + " iterations)");
+  std::vector<double> x((size_t)H->L.total);
+  VQMC_CUDA(cudaMemcpyAsync(x.data(), H->cg_x, x.size() * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  live_to_reference_d(H, x, delta_out);
+  API_CATCH
+}
+
+// Test hook: the explicit fp64 score rows of the small-model SR path (d <= 2000), uncentred,
+// reference order [B][d]: forward + dg1 of `bits`, then the score kernel.
+int vqmc_test_sr_scores(vqmc_gpu_t* g, const uint32_t* bits, int B, double* out) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  if (H->d > 2000) throw std::invalid_argument("explicit scores only for d <= 2000");
+  H->ensure_batch(B);
+  ensure_sr(H, B);
+  upload_bits(H, bits, B);
+  forward_given(H, B, nullptr);
+  launch_dg1_umma(H, B);
+  sr_build_scores(H, B, false);
+  const int64_t total = H->L.total;
+  std::vector<double> S((size_t)B * total);
+  VQMC_CUDA(cudaMemcpyAsync(S.data(), H->sr_S, S.size() * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  for (int b = 0; b < B; ++b) {
+    std::vector<double> row(S.begin() + (size_t)b * total, S.begin() + (size_t)(b + 1) * total);
+    live_to_reference_d(H, row, out + (size_t)b * H->d);
+  }
+  API_CATCH
+}
+
+int vqmc_gpu_train_step_sr(vqmc_gpu_t* g, int minibatch, int workers, const double* uniforms, uint64_t seed,
+                           uint64_t stream0, uint64_t call, double lr, double lambda, double tol, int max_iterations,
+                           int fallback, int centered, vqmc_step_stats_t* stats_out, int* iterations_out,
+                           double* residual_out) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  if (minibatch < 2) throw std::invalid_argument("minibatch must be >= 2");
+  if (workers < 1) throw std::invalid_argument("workers must be >= 1");
+  if (max_iterations < 0) throw std::invalid_argument("max_iterations must be >= 0");
+  if (H->nranks > 1) throw std::invalid_argument("the SR step runs on one GPU (workers = segments of its batch)");
+  const int B = minibatch * workers;
+  H->ensure_batch(B);
+  ensure_istat(H, workers);
+  ensure_sr(H, B);
+  launch_set_step(H, call, 1, lr, 0.9, 0.999, 1e-8);  // (the sampler's Philox call; t / Adam unused)
+  H->next_call = ~uint64_t(0);                         // an ADAM step after this one resets the counters
+  // phase 1: sample, local energies, REINFORCE weights, gradient (trainer.cpp:155-168)
+  sample_into(H, B, workers, uniforms, seed, stream0, 0, /*device_call=*/true, /*want_log_psi=*/false);
+  launch_energy(H, B);
+  launch_weights_from_locals(H, B, minibatch, true);
+  launch_backward(H, B, /*wg1_done=*/true);
+  int64_t cs = 0, cq = 0, best = 0;
+  VQMC_CUDA(cudaMemcpyAsync(H->h_istat, H->d_istat, 3 * workers * sizeof(int64_t), cudaMemcpyDeviceToHost,
+                            H->stream));
+  VQMC_CUDA(cudaMemcpyAsync(H->h_scal + 8, H->d_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  check_flag(H, *reinterpret_cast<const uint32_t*>(H->h_scal + 8));
+  for (int s = 0; s < workers; ++s) {
+    cs += H->h_istat[3 * s];
+    cq += H->h_istat[3 * s + 1];
+    best = std::max(best, H->h_istat[3 * s + 2]);
+  }
+  // phase 2: allreduce_mean (the segments' summed gradient / L) and the natural-gradient solve
+  // over the pooled scores (trainer.cpp:187-199)
+  launch_sr_grad_from_G(H, 1.0 / (double)workers);
+  int it = 0;
+  double res = 0.0, gnorm = 0.0;
+  const bool ok = sr_solve(H, B, lambda, tol, max_iterations, centered != 0, &it, &res, &gnorm);
+  if (iterations_out) *iterations_out = it;
+  if (residual_out) *residual_out = res;
+  if (!ok && !fallback)
+    throw SrSolveError("SR conjugate gradient did not converge (relative residual " + std::to_string(res) +
+                       " after " + std::to_string(it) + " iterations)");
+  // phase 3: sgd_step with the natural direction (or the raw gradient on a tolerated failure)
+  launch_sr_apply(H, lr, ok ? H->cg_x : H->cg_g);
+  launch_params_refresh(H);
+  H->invalidate_graph();
+  if (stats_out) {
+    pooled_stats(H->num_edges, B, cs, cq, &stats_out->energy_mean, &stats_out->energy_var);
+    stats_out->grad_norm = gnorm;
+    stats_out->cut_sum = cs;
+    stats_out->cut_sq_sum = cq;
+    stats_out->best_cut = (int32_t)best;
+    stats_out->batch = B;
+  }
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
   API_CATCH
 }
 

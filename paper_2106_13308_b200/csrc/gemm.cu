@@ -193,7 +193,7 @@ struct StoreEpi {  // test: C[row][col] = acc
 // GEMM as column h), so per output the epilogue is: sigmoid (ex2 + rcp), the draw, D and its fp16
 // pair; Philox keys are per row.  The epilogue warp sets take alternate 32-column chunks and
 // each writes its own log-prob partial (lp_part[kParts * tile + part]): deterministic.
-constexpr int kTailBN = 192;  // tail sampler pair tile: 256 samples x 192 outputs
+// (kTailBN: internal.cuh)
 template <bool PROD>  // PROD: production draws (Philox) and no log-probabilities (the training step)
 struct TailSampleEpiT {
   int B, n, np, W, colbase, col_lo;  // outputs in [col_lo, n) are drawn here
@@ -426,6 +426,48 @@ struct Gw2TEpi {
   __device__ void end_row(int, const UmmaArgs&) {}
 };
 
+// SR operator (stochastic reconfiguration, optimizer.cpp:46-92): the W2 | b2 half of S p,
+// sum_i D[b][i] Z[b][i] with Z = [G1 | 1] . [P2 | p2]^T the logits of the direction p.  Rows b,
+// columns i over all n outputs; one fp64 partial per row and epilogue set per column tile.
+struct SpDotEpi {
+  int B, n, np;
+  const __half* Dh;  // D (unweighted made_dz2) as an fp16 pair, [B][np]
+  const __half* Dl;
+  double* out;  // [kParts * tiles_n][B]
+  int part;
+  UmmaTile tile;
+  double acc;
+  static constexpr int kParts = Umma2Cfg<kTailBN>::kEpiSets;
+  __device__ void init() {}
+  __device__ void begin_row(int, const UmmaArgs&) { acc = 0.0; }
+  __device__ void chunk(int b, int col0, const float (&v)[32], const UmmaArgs&) {
+    if (b >= B) return;
+    const __half* dh = Dh + (size_t)b * np + col0;
+    const __half* dl = Dl + (size_t)b * np + col0;
+    float s = 0.f;
+    if (col0 + 32 <= n) {  // (np % 8 == 0 and col0 % 32 == 0: 16-byte loads)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const uint4 hv = reinterpret_cast<const uint4*>(dh)[q], lv = reinterpret_cast<const uint4*>(dl)[q];
+        const __half2* h2 = reinterpret_cast<const __half2*>(&hv);
+        const __half2* l2 = reinterpret_cast<const __half2*>(&lv);
+#pragma unroll
+        for (int t = 0; t < 4; ++t) {
+          const float2 a = __half22float2(h2[t]), c = __half22float2(l2[t]);
+          s = fmaf(a.x + c.x, v[8 * q + 2 * t], s);
+          s = fmaf(a.y + c.y, v[8 * q + 2 * t + 1], s);
+        }
+      }
+    } else {
+      for (int j = 0; j < 32 && col0 + j < n; ++j) s = fmaf(__half2float(dh[j]) + __half2float(dl[j]), v[j], s);
+    }
+    acc += (double)s;
+  }
+  __device__ void end_row(int b, const UmmaArgs&) {
+    if (b < B) out[(size_t)(kParts * tile.tn + part) * B + b] = acc;
+  }
+};
+
 // ===========================================================================
 // Helper kernels: 16-bit pairs of operands
 // ===========================================================================
@@ -554,6 +596,22 @@ void launch_gw2_umma(Handle* H, int B, bool wg1_done, cudaStream_t stream) {
   Gw2TEpi e{L.n, L.h, 0, {}, H->d_deg, H->d_wscale, H->G + L.off_w2, H->G + L.off_b2, 1.f, 0};
   launch_umma2<BN, true, true, Gw2TEpi, false, kElemF16>(H, "bw_gw2_umma", ah, al, bh, bl, L.h + 1, L.n, B, 1, e,
                                                          stream);
+}
+
+// S p (W2 | b2 half): [G1 | 1] . [P2 | p2]^T on CTA pairs with the D-dot epilogue; returns the
+// number of partials per row (SpDotEpi::kParts x column tiles).
+int launch_sp_umma(Handle* H, int B) {
+  const Layout& L = H->L;
+  constexpr int BN = kTailBN;
+  const int K = L.h + 1;
+  const CUtensorMap ah = tmap_kmajor(H->G1h, K, B, H->hp18, kUmmaBM, kElemF16);
+  const CUtensorMap al = tmap_kmajor(H->G1l, K, B, H->hp18, kUmmaBM, kElemF16);
+  const CUtensorMap bh = tmap_kmajor(H->SRh, K, L.n, H->hp18, BN / 2, kElemF16);
+  const CUtensorMap bl = tmap_kmajor(H->SRl, K, L.n, H->hp18, BN / 2, kElemF16);
+  SpDotEpi e{B, L.n, H->np8, H->Dh, H->Dl, H->sp_part, 0, {}, 0.0};
+  launch_umma2<BN, false, false, SpDotEpi, false, kElemF16>(H, "sr_sp_umma", ah, al, bh, bl, B, L.n, K, 1, e,
+                                                           H->stream);
+  return SpDotEpi::kParts * ((L.n + BN - 1) / BN);
 }
 
 // gW1T[j][k] = sum_b X[b][j] dz1[b][k] (j < Hd) and gb1[k] (the ones column j = Hd):

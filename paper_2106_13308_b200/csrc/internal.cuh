@@ -26,6 +26,10 @@ struct NumericError : std::runtime_error {
 struct CudaError : std::runtime_error {
   using std::runtime_error::runtime_error;
 };
+// SR conjugate gradient did not meet its residual contract (optimizer.hpp:46-55)
+struct SrSolveError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 #define VQMC_CUDA(expr)                                                                  \
   do {                                                                                   \
@@ -39,6 +43,7 @@ constexpr double kProbEps = 1e-7;  // proj/include/vqmc/models.hpp:26
 // logit(1 - 1e-7) = ln((1 - 1e-7) / 1e-7): p_raw >= 1 - eps  <=>  z >= kLogitHi.
 constexpr float kLogitHi = 16.118095650958319f;
 constexpr int kMaxHidden = 1024;
+constexpr int kTailBN = 192;  // tail sampler / S p pair tile: 256 samples x 192 outputs
 constexpr int kGw1MaxSplits = 16;  // split-K of the gW1 GEMM over the batch  // head sampler register tiling limit (32 lanes x 32)
 
 // ---------------------------------------------------------------------------
@@ -114,6 +119,15 @@ void launch_dg1_umma(Handle* h, int B);
 void launch_gw2_umma(Handle* h, int B, bool wg1_done = false, cudaStream_t stream = nullptr);
 void launch_split_w2(Handle* h);
 void launch_gw1_umma(Handle* h, int B, int& splits_out);
+// SR (sr.cu, gemm.cu)
+int launch_sp_umma(Handle* h, int B);
+void ensure_sr(Handle* h, int B);
+void sr_build_scores(Handle* h, int B, bool centered);  // small models: explicit fp64 score rows
+void free_sr(Handle* h);
+void launch_sr_grad_from_G(Handle* h, double scale);
+void launch_sr_apply(Handle* h, double lr, const double* delta);
+bool sr_solve(Handle* h, int B, double lambda, double tol, int max_iterations, bool centered, int* iterations,
+              double* residual, double* gnorm_out);
 void set_error(const std::string& msg);
 int status_of(const std::exception& ex);
 void launch_adam(Handle* h, float grad_scale);  // hyper-parameters from h->d_step
@@ -196,6 +210,16 @@ struct Handle {
   int64_t* d_istat = nullptr;  // per worker segment s: [3s] cut_sum [3s+1] cut_sq_sum [3s+2] best
   int istat_cap = 0;
   double* d_gpart = nullptr;   // grad-norm partials
+  // SR (sr.cu; allocated on first use): fp64 CG vectors in the live layout, the fp16 pair of the
+  // CG direction's [W2 | b2] block, per-sample products q = grad log psi . p and their partials
+  double *cg_x = nullptr, *cg_r = nullptr, *cg_p = nullptr, *cg_g = nullptr, *cg_ap = nullptr, *cg_part = nullptr;
+  double* sr_S = nullptr;  // small models (d <= 2000): explicit fp64 score rows [B][total]
+  double* sr_C = nullptr;  // and the Cholesky factor of the dense system (min(B, total)^2)
+  size_t sr_S_cap = 0, sr_C_cap = 0;
+  __half *SRh = nullptr, *SRl = nullptr;
+  double *sr_q = nullptr, *sp_part = nullptr, *d_sr_scal = nullptr, *h_sr_scal = nullptr;
+  unsigned* d_pmax = nullptr;
+  int sr_cap_B = 0;
   int gpart_n = 0;
   uint32_t* d_flag = nullptr;  // sticky non-finite flag (logit overflow in the fp16-pair GEMMs)
   double* d_host_stage = nullptr;

@@ -229,3 +229,54 @@ def test_invalid_configs_rejected():  # trainer_test.cpp:191-201
     for kw in (dict(workers=0), dict(iterations=0), dict(minibatch=1)):
         with pytest.raises(RuntimeError):
             O.train(4, e, **kw)
+
+
+# --- SR: optimizer_test.cpp:64-150, models_test.cpp:211-218 ---------------
+def test_score_rows_are_twice_single_sample_gradients():  # models_test.cpp:211-218
+    m = O.made_init(6, 10, 1)
+    x, _ = O.auto_sample(m, 5, seed=1, stream=1)
+    S = O.score_matrix(m, x)
+    for b in range(5):
+        w = np.zeros(5)
+        w[b] = 1.0
+        assert np.abs(S[b] - 2.0 * O.weighted_grad(m, x, w)).max() <= 1e-12
+
+
+def test_sr_zero_fisher_is_grad_over_lambda():  # optimizer_test.cpp:64-71
+    g = np.linspace(1.0, 6.0, 6)
+    d, _, _ = O.sr_direction(np.zeros((4, 6)), g, lam=0.001)
+    assert np.abs(d - g / 0.001).max() <= 1e-6 * np.linalg.norm(g)
+
+
+def test_sr_identity_fisher_rescales():  # optimizer_test.cpp:73-82 (centred=False: S^T S / B = I)
+    S = np.eye(5) * np.sqrt(5.0)
+    g = np.linspace(-2.0, 2.0, 5)
+    d, _, _ = O.sr_direction(S, g, lam=0.5, centered=False)
+    assert np.abs(d - g / 1.5).max() <= 1e-10
+
+
+def test_sr_large_lambda_monotone_angle():  # optimizer_test.cpp:84-106
+    rng = np.random.default_rng(1)
+    S, g = rng.standard_normal((16, 8)), rng.standard_normal(8)
+    prev = 1e9
+    for lam in (0.01, 1.0, 100.0, 10000.0):
+        d, _, _ = O.sr_direction(S, g, lam=lam)
+        ang = np.arccos(d @ g / (np.linalg.norm(d) * np.linalg.norm(g)))
+        assert ang <= prev + 1e-12
+        prev = ang
+
+
+def test_sr_cg_path_residual_contract():  # optimizer_test.cpp:108-126 (d > 2000: CG)
+    rng = np.random.default_rng(2)
+    S, g = rng.standard_normal((6, 2100)), rng.standard_normal(2100)
+    d, it, res = O.sr_direction(S, g, lam=0.001, tol=1e-6)
+    Sc = S - S.mean(0)
+    r = Sc.T @ (Sc @ d) / 6 + 0.001 * d - g
+    assert np.linalg.norm(r) <= 1e-6 * np.linalg.norm(g) and it > 0 and res <= 1e-6
+
+
+def test_sr_cg_failure_raises():  # optimizer_test.cpp:128-142
+    S = np.zeros((4, 2100))
+    S[0, 0] = 1.0
+    with pytest.raises(O.SrSolveError):
+        O.sr_direction(S, np.ones(2100), max_iterations=0)

@@ -10,10 +10,14 @@
   n=20, 5 seeds, MADE+AUTO+ADAM, 300 iterations, batch 1024 (acceptance.cpp:239-272).
   This is a 300-step trajectory of the whole north-star path (sampler, Max-Cut
   local energy, REINFORCE gradient, tree all-reduce, Adam, final evaluation).
+  Its SR half, "sr optimal 5/5 (worst ratio 1.000)" — SGD + SR, 150 iterations, batch 256
+  (acceptance.cpp:246-257) — pins the SR restatement (score_matrix, FisherEstimate, the dense
+  sr_direction at d = 1865).
 
 The CPU-generated golden fixtures (tests/golden/) are checked here too.
 """
 import os
+from concurrent.futures import ThreadPoolExecutor
 
 import numpy as np
 
@@ -44,6 +48,21 @@ def test_pin_criterion6_maxcut_adam_ratio():
                     sampler_mode=0)
         worst = min(worst, r["best_cut"] / opt)
     assert "%.3f" % worst == "0.956"
+
+
+def test_pin_criterion6_maxcut_sr_optimal():
+    def run(s):  # (ctypes releases the GIL: the five seeds run on five host threads)
+        e = O.random_maxcut_graph(20, s)
+        opt, _ = O.brute_force_maxcut(20, e)
+        r = O.train(20, e, optimizer="sgd_sr", iterations=150, minibatch=256, eval_batch=1024, seed=s,
+                    sampler_mode=1)
+        return r["best_cut"], opt
+
+    with ThreadPoolExecutor(5) as ex:
+        res = list(ex.map(run, range(5)))
+    optimal = sum(c >= o for c, o in res)
+    worst = min(c / o for c, o in res)
+    assert optimal == 5 and "%.3f" % worst == "1.000"
 
 
 def test_golden_fixtures_reproduce():
