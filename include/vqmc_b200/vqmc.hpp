@@ -30,9 +30,15 @@ namespace vqmc {
 
 using Vector = std::vector<double>;
 
+/// SR conjugate gradient did not converge (optimizer.hpp:46-55).
+struct SrSolveError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
 inline void check(int rc) {
   if (rc == VQMC_OK) return;
   if (rc == VQMC_ERR_INVALID) throw std::invalid_argument(vqmc_last_error());
+  if (rc == VQMC_ERR_SR) throw SrSolveError(vqmc_last_error());
   throw std::runtime_error(vqmc_last_error());
 }
 
@@ -332,9 +338,22 @@ inline Vector allreduce_mean(const std::vector<Vector>& vs) {  // trainer.cpp:32
   return out;
 }
 
-struct RunConfig {  // the Max-Cut / MADE / AUTO / ADAM slice of trainer.hpp:31-58
+enum class OptimizerKind { kAdam, kSgdSr };  // (kSgd and RBM/MCMC are outside the B200 path)
+
+struct SrConfig {  // optimizer.hpp:38-45
+  double lr = 0.1;
+  double lambda = 1e-3;
+  double tol = 1e-6;
+  int max_iterations = 200;
+  bool fallback = false;
+  bool centered = true;
+};
+
+struct RunConfig {  // the Max-Cut / MADE / AUTO / {ADAM, SGD + SR} slice of trainer.hpp:31-58
   std::optional<MaxCutProblem> maxcut;
   int hidden = 0;
+  OptimizerKind optimizer = OptimizerKind::kAdam;
+  SrConfig sr;
   double lr = 0.0;
   int iterations = 300;
   int workers = 1;
@@ -365,9 +384,11 @@ struct RunResult {
 
 constexpr uint64_t kEvalStream = 1'000'000'007ULL;  // trainer.cpp:48
 
-inline double resolve_lr(const RunConfig& c) { return c.lr > 0.0 ? c.lr : 0.01; }  // trainer.cpp:35-46 (ADAM)
+inline double resolve_lr(const RunConfig& c) {  // trainer.cpp:35-46
+  return c.lr > 0.0 ? c.lr : (c.optimizer == OptimizerKind::kAdam ? 0.01 : 0.1);
+}
 
-/// train (trainer.cpp:111-322) for MADE + AUTO + ADAM on a Max-Cut instance: one fused
+/// train (trainer.cpp:111-322) for MADE + AUTO + ADAM or SGD + SR on a Max-Cut instance: one fused
 /// device step per iteration; `workers` reference workers are segments of the device batch.
 inline RunResult train(const RunConfig& cfg) {
   if (!cfg.maxcut) throw std::invalid_argument("the B200 path trains Max-Cut instances");
@@ -412,7 +433,15 @@ inline RunResult train(const RunConfig& cfg) {
       up = u.data();
     }
     vqmc_step_stats_t st{};
-    check(vqmc_gpu_train_step(r.get(), mbs, L, up, cfg.seed, 1, (uint64_t)it, lr, 0.9, 0.999, 1e-8, it + 1, &st));
+    if (cfg.optimizer == OptimizerKind::kSgdSr) {  // trainer.cpp:165-168, 189-199, 223-225
+      int cg_it = 0;
+      double cg_res = 0.0;
+      check(vqmc_gpu_train_step_sr(r.get(), mbs, L, up, cfg.seed, 1, (uint64_t)it, lr, cfg.sr.lambda, cfg.sr.tol,
+                                   cfg.sr.max_iterations, cfg.sr.fallback ? 1 : 0, cfg.sr.centered ? 1 : 0, &st,
+                                   &cg_it, &cg_res));
+    } else {
+      check(vqmc_gpu_train_step(r.get(), mbs, L, up, cfg.seed, 1, (uint64_t)it, lr, 0.9, 0.999, 1e-8, it + 1, &st));
+    }
     StepStats s;
     s.energy_mean = st.energy_mean;
     s.energy_std = std::sqrt(st.energy_var);

@@ -105,3 +105,27 @@ def test_solve_reference_streams_reaches_near_optimum(tmp_path):
     best = json.loads((out / "summary.json").read_text())["best_cut"]
     opt, _ = O.brute_force_maxcut(20, O.random_maxcut_graph(20, 0))
     assert best >= 0.95 * opt
+
+
+@pytest.mark.gpu
+def test_solve_sgd_sr(tmp_path):
+    """--optimizer sgd_sr (vqmc.cpp:416-425): SGD + SR on n=20 with the reference's streams
+    reaches the optimum (acceptance.cpp:246-257); the summary echoes the SR settings
+    (vqmc.cpp:170-176); a CG budget of 0 without --sr-fallback is a numerical failure (exit 2)."""
+    g = tmp_path / "g20.txt"
+    run("gen-instance", "--problem", "maxcut", "--n", 20, "--seed", 1, "--out", g)
+    out = tmp_path / "run"
+    r = run("solve", "--instance", g, "--optimizer", "sgd_sr", "--iterations", 150, "--minibatch", 256, "--seed", 1,
+            "--reference-streams", "--out", out)
+    assert r.returncode == 0, r.stderr
+    s = json.loads((out / "summary.json").read_text())
+    assert s["config"]["optimizer"] == "sgd_sr" and s["config"]["lr"] == 0.1
+    assert s["config"]["sr_lambda"] == 0.001 and s["config"]["sr_centered"] is True
+    opt, _ = O.brute_force_maxcut(20, O.random_maxcut_graph(20, 1))
+    assert s["best_cut"] >= 0.97 * opt
+    r = run("solve", "--problem", "maxcut", "--n", 30, "--optimizer", "sgd_sr", "--iterations", 1, "--minibatch",
+            64, "--sr-maxiter", 0, "--out", tmp_path / "fail")
+    assert r.returncode == 2 and "did not converge" in r.stderr
+    r = run("solve", "--problem", "maxcut", "--n", 30, "--optimizer", "sgd_sr", "--iterations", 1, "--minibatch",
+            64, "--sr-maxiter", 0, "--sr-fallback", "--out", tmp_path / "fb")
+    assert r.returncode == 0, r.stderr

@@ -202,7 +202,7 @@ int run_solve(const Args& a) {
                        " (made pairs with auto, rbm with mcmc)");
   }
   if (model != "made") throw UsageError("the B200 path implements MADE + AUTO (RBM/MCMC is out of scope)");
-  if (optimizer != "adam") throw UsageError("the B200 path implements ADAM (" + optimizer + " is out of scope)");
+  if (optimizer == "sgd") throw UsageError("the B200 path implements ADAM and SGD + SR (plain sgd is out of scope)");
 
   vqmc::RunConfig cfg;
   cfg.seed = (uint64_t)a.geti("seed", 0);
@@ -214,6 +214,14 @@ int run_solve(const Args& a) {
   cfg.workers = (int)a.geti("workers", 1);
   cfg.device = (int)a.geti("device", 0);
   cfg.reference_streams = a.flags.count("reference-streams") > 0;
+  if (optimizer == "sgd_sr") {  // vqmc.cpp:416-425
+    cfg.optimizer = vqmc::OptimizerKind::kSgdSr;
+    cfg.sr.lambda = a.getd("sr-lambda", cfg.sr.lambda);
+    cfg.sr.tol = a.getd("sr-tol", cfg.sr.tol);
+    cfg.sr.max_iterations = (int)a.geti("sr-maxiter", cfg.sr.max_iterations);
+    cfg.sr.fallback = a.flags.count("sr-fallback") > 0;
+    cfg.sr.centered = a.flags.count("sr-uncentered") == 0;
+  }
   if (a.has("target")) cfg.target = a.getd("target", 0.0);
   const std::string instance = a.get("instance", "");
   const int n = (int)a.geti("n", 0);
@@ -279,12 +287,19 @@ int run_solve(const Args& a) {
   c.kv["model"] = jstr("made");
   c.kv["sampler"] = jstr("auto");
   c.kv["hidden"] = std::to_string(cfg.hidden > 0 ? cfg.hidden : vqmc::default_made_hidden(g.n));
-  c.kv["optimizer"] = jstr("adam");
+  c.kv["optimizer"] = jstr(optimizer);
   c.kv["lr"] = jnum(vqmc::resolve_lr(cfg));
   c.kv["iterations"] = std::to_string(cfg.iterations);
   c.kv["workers"] = std::to_string(cfg.workers);
   c.kv["minibatch"] = std::to_string(cfg.minibatch);
   c.kv["eval_batch"] = std::to_string(cfg.eval_batch);
+  if (cfg.optimizer == vqmc::OptimizerKind::kSgdSr) {  // config_echo (vqmc.cpp:170-176)
+    c.kv["sr_lambda"] = jnum(cfg.sr.lambda);
+    c.kv["sr_tol"] = jnum(cfg.sr.tol);
+    c.kv["sr_maxiter"] = std::to_string(cfg.sr.max_iterations);
+    c.kv["sr_fallback"] = cfg.sr.fallback ? "true" : "false";
+    c.kv["sr_centered"] = cfg.sr.centered ? "true" : "false";
+  }
   if (cfg.target) c.kv["target"] = jnum(*cfg.target);
   JObj ph;
   ph.kv["sample"] = jnum(res.phases.sample);
