@@ -43,6 +43,7 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-seconds", type=float, default=15.0, help="budget of the bounded CPU sample")
     ap.add_argument("--profile", action="store_true", help="short run for ncu (no clocks / e2e / cpu)")
+    ap.add_argument("--no-sr", action="store_true", help="skip the SGD + SR step measurement")
     return ap.parse_args()
 
 
@@ -315,6 +316,8 @@ def run_ours(args):
     e2e = None
     if not args.profile:
         st = K.StepStats()
+        for _ in range(2):  # untimed: the timing modes changed, so the step graph is re-captured
+            one_step(C.byref(st))
         D.barrier()
         t0 = time.perf_counter()
         for _ in range(args.steps):
@@ -388,6 +391,33 @@ def run_ours(args):
     if world == 1 and not args.no_cpu_baseline and not args.profile:
         cpu = cpu_baseline(args, g, B)
 
+    # SGD + SR step (the reference cannot form S at this size: B x d fp64 = 70 GB)
+    sr = None
+    if world == 1 and not args.profile and not args.no_sr:
+        st = K.StepStats()
+        cg_it, cg_res = C.c_int(0), C.c_double(0.0)
+        iters = []
+
+        def sr_step(i):
+            K.check(K.lib.vqmc_gpu_train_step_sr(hd, B, 1, None, args.seed, stream0, 10_000 + i, 0.1, 1e-3, 1e-6, 200,
+                                                 1, 1, C.byref(st), C.byref(cg_it), C.byref(cg_res)))
+            iters.append(cg_it.value)
+
+        sr_step(0)  # (first use allocates the CG buffers)
+        K.check(K.lib.vqmc_gpu_synchronize(hd))
+        iters.clear()
+        t0 = time.perf_counter()
+        for i in range(3):
+            sr_step(1 + i)
+        K.check(K.lib.vqmc_gpu_synchronize(hd))
+        sr_ms = (time.perf_counter() - t0) * 1e3 / 3
+        sr = {"ms_per_step": sr_ms, "samples_per_s": B * 1000.0 / sr_ms, "cg_iterations": iters,
+              "ms_per_cg_iteration": sr_ms / max(1.0, float(np.mean(iters))),
+              "workload": "SGD + SR (lambda 1e-3, tol 1e-6, centred), same instance and batch; CG on the "
+                          "structured Fisher operator (the scores are never formed)",
+              "timing": "host wall clock around 3 blocking vqmc_gpu_train_step_sr calls (the CG loop reads one "
+                        "scalar per iteration)"}
+
     K.lib.vqmc_gpu_destroy(hd)
     line = {
         "metric": "samples/sec (VQMC training step, N=10k Max-Cut MADE)",
@@ -421,6 +451,7 @@ def run_ours(args):
         "gpu_launches_per_step": launches / args.steps,
         "graph": "each step is one captured CUDA graph replayed per iteration (vqmc_gpu_set_graph)",
         "cpu_baseline": cpu,
+        "sr": sr,
     }
     return line
 

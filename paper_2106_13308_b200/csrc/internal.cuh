@@ -217,7 +217,8 @@ struct Handle {
   double* sr_C = nullptr;  // and the Cholesky factor of the dense system (min(B, total)^2)
   size_t sr_S_cap = 0, sr_C_cap = 0;
   __half *SRh = nullptr, *SRl = nullptr;
-  double *sr_q = nullptr, *sp_part = nullptr, *d_sr_scal = nullptr, *h_sr_scal = nullptr;
+  double *sr_q = nullptr, *sp_part = nullptr, *d_sr_scal = nullptr, *h_sr_scal = nullptr, *sr_q1 = nullptr;
+  float *sr_dz1 = nullptr, *sr_p1f = nullptr;
   unsigned* d_pmax = nullptr;
   int sr_cap_B = 0;
   int gpart_n = 0;

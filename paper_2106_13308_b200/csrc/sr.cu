@@ -77,27 +77,37 @@ __global__ void __launch_bounds__(kVecThreads) cg_init_kernel(int64_t total, con
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-// p . (F p + lambda p)
-__global__ void __launch_bounds__(kVecThreads) cg_pap_kernel(int64_t total, const double* __restrict__ G,
+// p . (F p + lambda p), F p in G (fp32, the backward's output)
+__global__ void __launch_bounds__(kVecThreads) cg_pap_kernel(int64_t total, const float* __restrict__ G,
                                                             const double* __restrict__ p, double lambda,
                                                             double* __restrict__ part) {
   double s = 0.0;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
     const double pv = p[t];
-    s += pv * (G[t] + lambda * pv);
+    s += pv * ((double)G[t] + lambda * pv);
   }
   s = block_sum256(s);
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
+// alpha = rs / (p . A p) on the device (scal[0] = rs, scal[1] = alpha): no host round trip
+__global__ void __launch_bounds__(kVecThreads) cg_alpha_kernel(int cnt, const double* __restrict__ part,
+                                                              double* __restrict__ scal) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) s += part[i];
+  s = block_sum256(s);
+  if (threadIdx.x == 0) scal[1] = scal[0] / s;
+}
+
 // x += alpha p; r -= alpha (F p + lambda p); partial sums of r.r
-__global__ void __launch_bounds__(kVecThreads) cg_xr_kernel(int64_t total, double alpha, const double* __restrict__ G,
-                                                           const double* __restrict__ p, double lambda,
-                                                           double* __restrict__ x, double* __restrict__ r,
-                                                           double* __restrict__ part) {
+__global__ void __launch_bounds__(kVecThreads) cg_xr_kernel(int64_t total, const double* __restrict__ scal,
+                                                           const float* __restrict__ G, const double* __restrict__ p,
+                                                           double lambda, double* __restrict__ x,
+                                                           double* __restrict__ r, double* __restrict__ part) {
+  const double alpha = scal[1];
   double s = 0.0;
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
-    const double pv = p[t], ap = G[t] + lambda * pv;
+    const double pv = p[t], ap = (double)G[t] + lambda * pv;
     x[t] += alpha * pv;
     const double rv = r[t] - alpha * ap;
     r[t] = rv;
@@ -107,9 +117,19 @@ __global__ void __launch_bounds__(kVecThreads) cg_xr_kernel(int64_t total, doubl
   if (threadIdx.x == 0) part[blockIdx.x] = s;
 }
 
-__global__ void cg_p_kernel(int64_t total, double beta, const double* __restrict__ r, double* __restrict__ p) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
-    p[t] = r[t] + beta * p[t];
+// p = r + beta p, and max |p| over the [W2 | b2] range [lo, total) for the next operand split
+__global__ void __launch_bounds__(kVecThreads) cg_p_kernel(int64_t total, int64_t lo, double beta,
+                                                          const double* __restrict__ r, double* __restrict__ p,
+                                                          unsigned* __restrict__ pmax) {
+  float m = 0.f;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = r[t] + beta * p[t];
+    p[t] = v;
+    if (t >= lo) m = fmaxf(m, (float)fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(pmax, __float_as_uint(m));
 }
 
 // params - lr * delta (sgd_step, optimizer.hpp:57-59) on the fp32 master copy
@@ -149,60 +169,112 @@ __global__ void sr_split_kernel(int n, int h, int ld, const double* __restrict__
   ptx::split_f16((float)ldexp(x, -e), hi[t], lo[t]);
 }
 
-// q_b = grad log psi(x_b) . p: the W1 | b1 half here (dz1 = (D W2m) relu'(z1) from the step's
-// split-K partials), plus the W2 | b2 half from the GEMM partials.  One CTA per sample.
-constexpr int kQThreads = 128, kQPer = kMaxHidden / kQThreads;
-__global__ void __launch_bounds__(kQThreads) sr_q_kernel(int B, int h, int Hd, int W, const uint32_t* __restrict__ X,
-                                                         const float* __restrict__ G1, const float* __restrict__ Epart,
-                                                         int splits, const int32_t* __restrict__ deg,
-                                                         const double* __restrict__ p, int64_t off_w1t, int64_t off_b1,
-                                                         const double* __restrict__ sp_part, int nparts,
-                                                         const unsigned* __restrict__ pmax, double* __restrict__ q) {
+// dz1 = (D W2m) relu'(z1) of the batch (unweighted; fixed during a solve), from dg1's split-K partials
+__global__ void sr_dz1_kernel(int B, int h, int splits, const float* __restrict__ Epart, const float* __restrict__ G1,
+                              float* __restrict__ dz1) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)B * h) return;
+  float e = 0.f;
+  for (int z = 0; z < splits; ++z) e += Epart[(size_t)z * B * h + t];
+  dz1[t] = G1[t] > 0.f ? e : 0.f;  // relu'(z1) = [g1 > 0]
+}
+
+// The W1 block of the direction as masked fp32 rows P1f[j][k] = P1[k][j] M1(k, j) (row stride ld)
+__global__ void sr_p1f_kernel(int Hd, int h, int ld, const double* __restrict__ p1, const int32_t* __restrict__ deg,
+                              float* __restrict__ out) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= (int64_t)Hd * ld) return;
+  const int j = (int)(t / ld), k = (int)(t % ld);
+  out[t] = (k < h && j + 1 <= deg[k]) ? (float)p1[(size_t)j * h + k] : 0.f;
+}
+
+// W1 half of q without the bias term: sum_k dz1_b[k] sum_{j: x_b[j] = 1} P1f[j][k], one CTA per
+// sample, 16-byte row loads, four set bits in flight.  part[b] (one partial per sample).
+constexpr int kQ1Threads = 128, kQ1Per = kMaxHidden / (4 * kQ1Threads);
+__global__ void __launch_bounds__(kQ1Threads) sr_q1_kernel(int B, int h, int Hd, int W, int ld,
+                                                           const uint32_t* __restrict__ X, const float* __restrict__ dz1,
+                                                           const float* __restrict__ P1f, double* __restrict__ part) {
   const int b = blockIdx.x;
-  double dz[kQPer], acc[kQPer];
-  int dg[kQPer];
+  float4 acc[kQ1Per];
 #pragma unroll
-  for (int u = 0; u < kQPer; ++u) {
-    const int k = threadIdx.x + kQThreads * u;
-    dz[u] = 0.0;
-    acc[u] = 0.0;
-    dg[u] = 0;
-    if (k < h) {
-      float e = 0.f;
-      for (int z = 0; z < splits; ++z) e += Epart[((size_t)z * B + b) * h + k];
-      dz[u] = G1[(size_t)b * h + k] > 0.f ? (double)e : 0.0;  // relu'(z1) = [g1 > 0]
-      acc[u] = p[off_b1 + k];
-      dg[u] = deg[k];
-    }
-  }
+  for (int u = 0; u < kQ1Per; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  const int nq = ld / 4;  // float4 columns per row
+  int jl[4];
+  int cnt = 0;
+  auto flush = [&](int n) {
+    float4 v[4][kQ1Per];
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int u = 0; u < kQ1Per; ++u) {
+        const int c = threadIdx.x + kQ1Threads * u;
+        v[r][u] = (r < n && c < nq) ? reinterpret_cast<const float4*>(P1f + (size_t)jl[r] * ld)[c]
+                                    : make_float4(0.f, 0.f, 0.f, 0.f);
+      }
+#pragma unroll
+    for (int r = 0; r < 4; ++r)
+#pragma unroll
+      for (int u = 0; u < kQ1Per; ++u) {
+        acc[u].x += v[r][u].x;
+        acc[u].y += v[r][u].y;
+        acc[u].z += v[r][u].z;
+        acc[u].w += v[r][u].w;
+      }
+  };
   for (int w = 0; w * 32 < Hd; ++w) {
     uint32_t bits = X[(size_t)b * W + w];
     if (Hd - 32 * w < 32) bits &= (1u << (Hd - 32 * w)) - 1u;
     while (bits) {
-      const int j = 32 * w + __ffs(bits) - 1;
+      jl[cnt++] = 32 * w + __ffs(bits) - 1;
       bits &= bits - 1u;
-      const double* row = p + off_w1t + (int64_t)j * h;  // W1T[j][k]
-#pragma unroll
-      for (int u = 0; u < kQPer; ++u) {
-        const int k = threadIdx.x + kQThreads * u;
-        if (k < h && j + 1 <= dg[u]) acc[u] += row[k];  // M1(k, j)
+      if (cnt == 4) {
+        flush(4);
+        cnt = 0;
       }
     }
   }
+  if (cnt) flush(cnt);
   double s = 0.0;
 #pragma unroll
-  for (int u = 0; u < kQPer; ++u) s += dz[u] * acc[u];
-  __shared__ double red[kQThreads / 32];
+  for (int u = 0; u < kQ1Per; ++u) {
+    const int c = threadIdx.x + kQ1Threads * u;
+    if (c < nq) {
+      const float* d = dz1 + (size_t)b * h + 4 * c;  // (rows of h floats: not 16-byte aligned in general)
+      const float a[4] = {acc[u].x, acc[u].y, acc[u].z, acc[u].w};
+#pragma unroll
+      for (int i = 0; i < 4; ++i)
+        if (4 * c + i < h) s += (double)d[i] * a[i];
+    }
+  }
+  __shared__ double red[kQ1Threads / 32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
   if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
-    double t1 = 0.0;
-    for (int i = 0; i < kQThreads / 32; ++i) t1 += red[i];
+    double t = 0.0;
+    for (int i = 0; i < kQ1Threads / 32; ++i) t += red[i];
+    part[b] = t;
+  }
+}
+
+// q_b = grad log psi(x_b) . p = (W1 half: q1 partials + dz1_b . p_b1) + (W2 half: GEMM partials
+// x 2^e).  One warp per sample.
+__global__ void sr_q_kernel(int B, int h, const float* __restrict__ dz1, const double* __restrict__ pb1,
+                            const double* __restrict__ q1_part, int q1_tiles, const double* __restrict__ sp_part,
+                            int nparts, const unsigned* __restrict__ pmax, double* __restrict__ q) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  double s = 0.0;
+  for (int k = lane; k < h; k += 32) s += (double)dz1[(size_t)b * h + k] * pb1[k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0) {
+    for (int t = 0; t < q1_tiles; ++t) s += q1_part[(size_t)t * B + b];
     double t2 = 0.0;
     for (int t = 0; t < nparts; ++t) t2 += sp_part[(size_t)t * B + b];
-    q[b] = t1 + ldexp(t2, pmax_exp(pmax));
+    q[b] = s + ldexp(t2, pmax_exp(pmax));
   }
 }
 
@@ -245,10 +317,6 @@ __global__ void __launch_bounds__(1024) sr_weights_kernel(int B, const double* _
   if (threadIdx.x == 0) *wscale = ldexpf(1.f, e);
 }
 
-__global__ void sr_widen_kernel(int64_t total, const float* __restrict__ G, double* __restrict__ out) {
-  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
-    out[t] = (double)G[t];
-}
 
 // ---- small models (reference d <= 2000, where sr_direction solves the dense system exactly):
 // the score rows are materialised in fp64 (live layout) and F is applied exactly, so CG is a
@@ -419,21 +487,25 @@ double sum_parts(Handle* H, const double* part, int cnt) {
   return *H->h_sr_scal;
 }
 
-// G = F p (without lambda), p = H->cg_p.  Needs the batch's G1 / D / X and dg1 partials.
+// G = F p (without lambda), p = H->cg_p with max |p| over [W2 | b2] in H->d_pmax.  Needs the
+// batch's G1 / D / X and dg1 partials.
 void apply_fisher(Handle* H, int B, bool centered) {
   const Layout& L = H->L;
-  VQMC_CUDA(cudaMemsetAsync(H->d_pmax, 0, sizeof(unsigned), H->stream));
-  sr_pmax_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(L.off_w2, L.total, H->cg_p, H->d_pmax);
-  SR_CHECK();
   const int64_t tot = (int64_t)L.n * H->hp18;
   sr_split_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, H->stream>>>(L.n, L.h, H->hp18, H->cg_p, L.off_w2,
                                                                          L.off_b2, H->d_deg, H->d_pmax, H->SRh,
                                                                          H->SRl);
   SR_CHECK();
   const int nparts = launch_sp_umma(H, B);
-  sr_q_kernel<<<B, kQThreads, 0, H->stream>>>(B, L.h, L.Hd, L.W, H->X, H->G1, H->Epart, H->splits, H->d_deg,
-                                               H->cg_p, L.off_w1t, L.off_b1, H->sp_part, nparts, H->d_pmax,
-                                               H->sr_q);
+  {
+    const int ld = 4 * ((L.h + 3) / 4);
+    const int64_t tp = (int64_t)L.Hd * ld;
+    sr_p1f_kernel<<<(unsigned)((tp + 255) / 256), 256, 0, H->stream>>>(L.Hd, L.h, ld, H->cg_p + L.off_w1t, H->d_deg,
+                                                                       H->sr_p1f);
+    sr_q1_kernel<<<B, kQ1Threads, 0, H->stream>>>(B, L.h, L.Hd, L.W, ld, H->X, H->sr_dz1, H->sr_p1f, H->sr_q1);
+    sr_q_kernel<<<(B + 7) / 8, 256, 0, H->stream>>>(B, L.h, H->sr_dz1, H->cg_p + L.off_b1, H->sr_q1, 1, H->sp_part,
+                                                    nparts, H->d_pmax, H->sr_q);
+  }
   SR_CHECK();
   // F p = S~^T S~ p / B with S = 2 grad log psi: weights 4 (q - mean q) / B on grad log psi
   sr_weights_kernel<<<1, 1024, 0, H->stream>>>(B, H->sr_q, 4.0 / (double)B, centered ? 1 : 0, H->w, H->d_wscale);
@@ -441,9 +513,6 @@ void apply_fisher(Handle* H, int B, bool centered) {
   H->launches += 5;
   launch_gw2_umma(H, B, /*wg1_done=*/false);  // w' [G1 | 1] pair, then gW2 / gb2
   launch_backward_after_dg1(H, B);            // dz1 (the batch's dg1 partials), gW1 / gb1
-  sr_widen_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(L.total, H->G, H->cg_ap);
-  SR_CHECK();
-  H->launches++;
 }
 
 void apply_fisher_dense(Handle* H, int B) {
@@ -493,6 +562,7 @@ void ensure_sr(Handle* H, int B) {
     alloc(&H->SRh, (size_t)L.n * H->hp18);
     alloc(&H->SRl, (size_t)L.n * H->hp18);
     alloc(&H->cg_part, (size_t)kVecBlocks);
+    alloc(&H->sr_p1f, (size_t)L.Hd * 4 * ((L.h + 3) / 4));
     alloc(&H->d_sr_scal, (size_t)4);
     alloc(&H->d_pmax, (size_t)1);
     VQMC_CUDA(cudaMallocHost((void**)&H->h_sr_scal, 4 * sizeof(double)));
@@ -501,6 +571,10 @@ void ensure_sr(Handle* H, int B) {
     if (H->sr_q) cudaFree(H->sr_q);
     if (H->sp_part) cudaFree(H->sp_part);
     alloc(&H->sr_q, (size_t)B);
+    if (H->sr_dz1) cudaFree(H->sr_dz1);
+    if (H->sr_q1) cudaFree(H->sr_q1);
+    alloc(&H->sr_dz1, (size_t)B * L.h);
+    alloc(&H->sr_q1, (size_t)B);
     const int nparts = Umma2Cfg<kTailBN>::kEpiSets * ((L.n + kTailBN - 1) / kTailBN);
     alloc(&H->sp_part, (size_t)nparts * B);
     H->sr_cap_B = B;
@@ -509,7 +583,7 @@ void ensure_sr(Handle* H, int B) {
 
 void free_sr(Handle* H) {
   void* ptrs[] = {H->cg_x, H->cg_r, H->cg_p, H->cg_g, H->cg_ap, H->sr_S, H->sr_C, H->SRh, H->SRl, H->cg_part, H->d_sr_scal, H->d_pmax,
-                  H->sr_q, H->sp_part};
+                  H->sr_q, H->sp_part, H->sr_dz1, H->sr_q1, H->sr_p1f};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (H->h_sr_scal) cudaFreeHost(H->h_sr_scal);
@@ -607,7 +681,7 @@ bool sr_solve(Handle* H, int B, double lambda, double tol, int max_iterations, b
   cg_init_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, H->cg_g, H->cg_x, H->cg_r, H->cg_p, H->cg_part);
   SR_CHECK();
   H->launches++;
-  double rs = sum_parts(H, H->cg_part, kVecBlocks);
+  double rs = sum_parts(H, H->cg_part, kVecBlocks);  // (also leaves rs in d_sr_scal[0])
   const double rhs_norm = std::sqrt(rs);
   if (gnorm_out) *gnorm_out = rhs_norm;
   int it_done = 0;
@@ -616,24 +690,29 @@ bool sr_solve(Handle* H, int B, double lambda, double tol, int max_iterations, b
     *residual = 0.0;
     return true;
   }
+  sr_dz1_kernel<<<(unsigned)(((int64_t)B * L.h + 255) / 256), 256, 0, H->stream>>>(B, L.h, H->splits, H->Epart,
+                                                                                      H->G1, H->sr_dz1);
+  VQMC_CUDA(cudaMemsetAsync(H->d_pmax, 0, sizeof(unsigned), H->stream));
+  sr_pmax_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(L.off_w2, L.total, H->cg_p, H->d_pmax);
+  SR_CHECK();
+  H->launches++;
   for (int it = 0; it < max_iterations; ++it) {
     apply_fisher(H, B, centered);
-    cg_pap_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, H->cg_ap, H->cg_p, lambda, H->cg_part);
+    cg_pap_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, H->G, H->cg_p, lambda, H->cg_part);
+    cg_alpha_kernel<<<1, kVecThreads, 0, H->stream>>>(kVecBlocks, H->cg_part, H->d_sr_scal);
+    cg_xr_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, H->d_sr_scal, H->G, H->cg_p, lambda, H->cg_x,
+                                                             H->cg_r, H->cg_part);
     SR_CHECK();
-    H->launches++;
-    const double pap = sum_parts(H, H->cg_part, kVecBlocks);
-    const double alpha = rs / pap;
-    cg_xr_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, alpha, H->cg_ap, H->cg_p, lambda, H->cg_x, H->cg_r,
-                                                             H->cg_part);
-    SR_CHECK();
-    H->launches++;
+    H->launches += 3;
     it_done = it + 1;
-    const double rs_next = sum_parts(H, H->cg_part, kVecBlocks);
+    const double rs_next = sum_parts(H, H->cg_part, kVecBlocks);  // the convergence test (host)
     if (std::sqrt(rs_next) <= tol * rhs_norm) {
       rs = rs_next;
       break;
     }
-    cg_p_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, rs_next / rs, H->cg_r, H->cg_p);
+    VQMC_CUDA(cudaMemsetAsync(H->d_pmax, 0, sizeof(unsigned), H->stream));
+    cg_p_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, L.off_w2, rs_next / rs, H->cg_r, H->cg_p,
+                                                            H->d_pmax);
     SR_CHECK();
     H->launches++;
     rs = rs_next;
