@@ -297,12 +297,28 @@ static void forward_given(Handle* H, int B, double* cond) {
   launch_finalize_logpsi(H, B, H->tail_tiles);
 }
 
+// The step's host-visible results live in one device block (read back with one copy):
+// [0] ||g||^2 (double), [8] the non-finite-logit flag (uint32), [16 ...] per-segment integer cut
+// statistics (3 int64 per segment); mirrored by a pinned host block of the same layout.
 static void ensure_istat(Handle* H, int segs) {
   if (segs <= H->istat_cap) return;
-  dalloc(&H->d_istat, (size_t)3 * segs);
-  if (H->h_istat) VQMC_CUDA(cudaFreeHost(H->h_istat));
-  VQMC_CUDA(cudaMallocHost((void**)&H->h_istat, (size_t)3 * segs * sizeof(int64_t)));
+  const size_t words = 16 + (size_t)3 * segs;  // 8-byte words
+  if (H->d_scal) VQMC_CUDA(cudaFree(H->d_scal));
+  VQMC_CUDA(cudaMalloc((void**)&H->d_scal, words * 8));
+  VQMC_CUDA(cudaMemset(H->d_scal, 0, words * 8));
+  H->d_flag = reinterpret_cast<uint32_t*>(H->d_scal + 8);
+  H->d_istat = reinterpret_cast<int64_t*>(H->d_scal + 16);
+  if (H->h_scal) VQMC_CUDA(cudaFreeHost(H->h_scal));
+  VQMC_CUDA(cudaMallocHost((void**)&H->h_scal, words * 8));
+  H->h_istat = reinterpret_cast<int64_t*>(H->h_scal + 16);
   H->istat_cap = segs;
+}
+
+// one copy of the step's results (||g||^2, flag, cut statistics of `segs` segments); blocks
+static void read_step_results(Handle* H, int segs) {
+  VQMC_CUDA(cudaMemcpyAsync(H->h_scal, H->d_scal, (16 + (size_t)3 * segs) * 8, cudaMemcpyDeviceToHost, H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  check_flag(H, *reinterpret_cast<const uint32_t*>(H->h_scal + 8));
 }
 
 // Pooled mean / unbiased variance of N Max-Cut local energies l = (E - 2c)/4
@@ -456,17 +472,13 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
     VQMC_CUDA(cudaMemcpy(H->d_comp_pos, cpos.data(), h * sizeof(int32_t), cudaMemcpyHostToDevice));
   }
   upload_edges(H, edges, num_edges);
-  dalloc(&H->d_scal, 16);
   dalloc(&H->d_step, 1);
   dalloc(&H->d_done, 1);
   VQMC_CUDA(cudaMemset(H->d_done, 0, sizeof(unsigned)));
-  dalloc(&H->d_flag, 1);
-  VQMC_CUDA(cudaMemset(H->d_flag, 0, sizeof(uint32_t)));
   dalloc(&H->d_wscale, 1);
-  ensure_istat(H, 64);
+  ensure_istat(H, 64);  // (d_scal, d_flag, d_istat and their host mirror)
   H->gpart_n = 148 * 4;
   dalloc(&H->d_gpart, (size_t)H->gpart_n);
-  VQMC_CUDA(cudaMallocHost((void**)&H->h_scal, 16 * sizeof(double)));
   for (auto& e : H->ev) VQMC_CUDA(cudaEventCreate(&e));
   for (int i = 0; i < Handle::kKtPool; ++i) {
     VQMC_CUDA(cudaEventCreate(&H->kt_start[i]));
@@ -501,13 +513,12 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   free_sr(H);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2h, H->W2l, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
-                  H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->cpart, H->local, H->w, H->d_wscale, H->d_flag,
-                  H->Epart, H->dz1bh, H->dz1bl, H->Xfb, H->gw1_part, H->cond, H->uni, H->d_scal, H->d_istat,
+                  H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->cpart, H->local, H->w, H->d_wscale,
+                  H->Epart, H->dz1bh, H->dz1bl, H->Xfb, H->gw1_part, H->cond, H->uni, H->d_scal,
                   H->d_gpart, H->d_step, H->d_done, H->d_comp_pos};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (H->h_scal) cudaFreeHost(H->h_scal);
-  if (H->h_istat) cudaFreeHost(H->h_istat);
   for (auto& e : H->ev)
     if (e) cudaEventDestroy(e);
   for (int i = 0; i < Handle::kKtPool; ++i) {
@@ -860,12 +871,7 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
   H->next_call = call + 1;
   H->next_t = t + 1;
   if (stats_out) {
-    VQMC_CUDA(cudaMemcpyAsync(H->h_scal, H->d_scal, sizeof(double), cudaMemcpyDeviceToHost, H->stream));
-    VQMC_CUDA(cudaMemcpyAsync(H->h_istat, H->d_istat, 3 * workers * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                              H->stream));
-    VQMC_CUDA(cudaMemcpyAsync(H->h_scal + 8, H->d_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, H->stream));
-    VQMC_CUDA(cudaStreamSynchronize(H->stream));
-    check_flag(H, *reinterpret_cast<const uint32_t*>(H->h_scal + 8));
+    read_step_results(H, workers);
     int64_t cs = 0, cq = 0, best = 0;
     for (int s = 0; s < workers; ++s) {
       cs += H->h_istat[3 * s];
@@ -959,11 +965,7 @@ int vqmc_gpu_train_step_sr(vqmc_gpu_t* g, int minibatch, int workers, const doub
   launch_weights_from_locals(H, B, minibatch, true);
   launch_backward(H, B, /*wg1_done=*/true);
   int64_t cs = 0, cq = 0, best = 0;
-  VQMC_CUDA(cudaMemcpyAsync(H->h_istat, H->d_istat, 3 * workers * sizeof(int64_t), cudaMemcpyDeviceToHost,
-                            H->stream));
-  VQMC_CUDA(cudaMemcpyAsync(H->h_scal + 8, H->d_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, H->stream));
-  VQMC_CUDA(cudaStreamSynchronize(H->stream));
-  check_flag(H, *reinterpret_cast<const uint32_t*>(H->h_scal + 8));
+  read_step_results(H, workers);
   for (int s = 0; s < workers; ++s) {
     cs += H->h_istat[3 * s];
     cq += H->h_istat[3 * s + 1];
