@@ -130,7 +130,9 @@ int vqmc_gpu_sr_direction(vqmc_gpu_t* g, const uint32_t* bits, int B, const doub
  * :223-225) on this GPU: sampling, local energies, REINFORCE gradient, the mean over the
  * `workers` segments, the SR direction over the pooled scores of all workers*minibatch samples,
  * and params -= lr * direction.  fallback != 0: a CG failure applies the raw gradient instead
- * (SrConfig::fallback); otherwise VQMC_ERR_SR and the parameters are unchanged.  Single GPU. */
+ * (SrConfig::fallback); otherwise VQMC_ERR_SR and the parameters are unchanged.  With a
+ * communicator (vqmc_gpu_comm_init) the Fisher estimate pools every rank's samples: the gradient,
+ * the centring sum and F p are all-reduced inside each CG iteration (CG path, d > 2000). */
 int vqmc_gpu_train_step_sr(vqmc_gpu_t* g, int minibatch, int workers, const double* uniforms, uint64_t seed,
                            uint64_t stream0, uint64_t call, double lr, double lambda, double tol, int max_iterations,
                            int fallback, int centered, vqmc_step_stats_t* stats_out, int* iterations_out,

@@ -537,8 +537,6 @@ def train(cfg: RunConfig, comm=None) -> RunResult:
         raise ValueError("minibatch must be >= 2")
     if cfg.optimizer not in ("adam", "sgd_sr"):
         raise ValueError("the B200 path implements the ADAM and SGD + SR optimizers")
-    if cfg.optimizer == "sgd_sr" and comm is not None and comm[1] > 1:
-        raise ValueError("the SR step runs on one GPU")
     n = cfg.problem.graph.n
     h = cfg.hidden if cfg.hidden > 0 else default_made_hidden(n)
     model = made_init(n, h, cfg.seed)

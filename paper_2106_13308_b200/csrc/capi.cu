@@ -32,7 +32,7 @@ int status_of(const std::exception& ex) {
 // ---------------------------------------------------------------------------
 struct NcclUniqueId { char internal[128]; };
 using ncclComm_t = void*;
-enum { ncclFloat32 = 7, ncclSum = 0 };
+enum { ncclFloat32 = 7, ncclFloat64 = 8, ncclSum = 0 };
 struct NcclApi {
   bool loaded = false;
   int (*GetUniqueId)(NcclUniqueId*) = nullptr;
@@ -69,6 +69,13 @@ static void nccl_check(int rc, const char* what) {
   if (rc != 0)
     throw std::runtime_error(std::string(what) + ": " +
                              (g_nccl.GetErrorString ? g_nccl.GetErrorString(rc) : "nccl error"));
+}
+
+// Sum over the ranks of the handle's communicator (no-op without one), on the handle's stream.
+void comm_allreduce_sum(Handle* H, void* buf, size_t count, bool f64) {
+  if (!H->nccl_comm) return;
+  nccl_check(g_nccl.AllReduce(buf, buf, count, f64 ? ncclFloat64 : ncclFloat32, ncclSum, H->nccl_comm, H->stream),
+             "ncclAllReduce (SR)");
 }
 
 // ---------------------------------------------------------------------------
@@ -952,7 +959,8 @@ int vqmc_gpu_train_step_sr(vqmc_gpu_t* g, int minibatch, int workers, const doub
   if (minibatch < 2) throw std::invalid_argument("minibatch must be >= 2");
   if (workers < 1) throw std::invalid_argument("workers must be >= 1");
   if (max_iterations < 0) throw std::invalid_argument("max_iterations must be >= 0");
-  if (H->nranks > 1) throw std::invalid_argument("the SR step runs on one GPU (workers = segments of its batch)");
+  if (H->nranks > 1 && H->d <= 2000)
+    throw std::invalid_argument("multi-GPU SR needs the CG path (reference d > 2000)");
   const int B = minibatch * workers;
   H->ensure_batch(B);
   ensure_istat(H, workers);
@@ -971,9 +979,10 @@ int vqmc_gpu_train_step_sr(vqmc_gpu_t* g, int minibatch, int workers, const doub
     cq += H->h_istat[3 * s + 1];
     best = std::max(best, H->h_istat[3 * s + 2]);
   }
-  // phase 2: allreduce_mean (the segments' summed gradient / L) and the natural-gradient solve
-  // over the pooled scores (trainer.cpp:187-199)
-  launch_sr_grad_from_G(H, 1.0 / (double)workers);
+  // phase 2: allreduce_mean (the segments' and ranks' summed gradient / L) and the natural-gradient
+  // solve over the pooled scores of every rank (trainer.cpp:187-199)
+  comm_allreduce_sum(H, H->G, (size_t)H->L.total, false);
+  launch_sr_grad_from_G(H, 1.0 / ((double)workers * H->nranks));
   int it = 0;
   double res = 0.0, gnorm = 0.0;
   const bool ok = sr_solve(H, B, lambda, tol, max_iterations, centered != 0, &it, &res, &gnorm);

@@ -122,6 +122,7 @@ void launch_gw1_umma(Handle* h, int B, int& splits_out);
 // SR (sr.cu, gemm.cu)
 int launch_sp_umma(Handle* h, int B);
 void ensure_sr(Handle* h, int B);
+void comm_allreduce_sum(Handle* h, void* buf, size_t count, bool f64);  // capi.cu (NCCL; no-op alone)
 void sr_build_scores(Handle* h, int B, bool centered);  // small models: explicit fp64 score rows
 void free_sr(Handle* h);
 void launch_sr_grad_from_G(Handle* h, double scale);

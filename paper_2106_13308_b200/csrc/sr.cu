@@ -280,12 +280,9 @@ __global__ void sr_q_kernel(int B, int h, const float* __restrict__ dz1, const d
 
 // REINFORCE-style weights of F p: y = coef (q - mean q) (centred) or coef q, normalised to
 // w' = y / wscale with wscale = 2^e >= max |y| (the backward's fp16 operand range).  One block.
-__global__ void __launch_bounds__(1024) sr_weights_kernel(int B, const double* __restrict__ q, double coef,
-                                                          int centered, float* __restrict__ w,
-                                                          float* __restrict__ wscale) {
+// sum of q over this rank's samples (fixed order) -> *out; summed over ranks before the weights
+__global__ void __launch_bounds__(1024) sr_qsum_kernel(int B, const double* __restrict__ q, double* __restrict__ out) {
   __shared__ double red[32];
-  __shared__ double s_mean;
-  __shared__ float s_max[32];
   double s = 0.0;
   for (int b = threadIdx.x; b < B; b += blockDim.x) s += q[b];
 #pragma unroll
@@ -295,10 +292,16 @@ __global__ void __launch_bounds__(1024) sr_weights_kernel(int B, const double* _
   if (threadIdx.x == 0) {
     double t = 0.0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) t += red[i];
-    s_mean = centered ? t / (double)B : 0.0;
+    *out = t;
   }
-  __syncthreads();
-  const double mean = s_mean;
+}
+
+// (qsum: the sum of q over every rank's samples; N: their number)
+__global__ void __launch_bounds__(1024) sr_weights_kernel(int B, const double* __restrict__ q, double coef,
+                                                          int centered, const double* __restrict__ qsum, double N,
+                                                          float* __restrict__ w, float* __restrict__ wscale) {
+  __shared__ float s_max[32];
+  const double mean = centered ? *qsum / N : 0.0;
   float m = 0.f;
   for (int b = threadIdx.x; b < B; b += blockDim.x) m = fmaxf(m, (float)fabs(coef * (q[b] - mean)));
 #pragma unroll
@@ -507,12 +510,19 @@ void apply_fisher(Handle* H, int B, bool centered) {
                                                     nparts, H->d_pmax, H->sr_q);
   }
   SR_CHECK();
-  // F p = S~^T S~ p / B with S = 2 grad log psi: weights 4 (q - mean q) / B on grad log psi
-  sr_weights_kernel<<<1, 1024, 0, H->stream>>>(B, H->sr_q, 4.0 / (double)B, centered ? 1 : 0, H->w, H->d_wscale);
+  // F p = S~^T S~ p / N with S = 2 grad log psi over all N = B x ranks samples (the reference's
+  // shared_scores): weights 4 (q - mean q) / N on grad log psi, then the gradient all-reduce
+  const double N = (double)B * H->nranks;
+  sr_qsum_kernel<<<1, 1024, 0, H->stream>>>(B, H->sr_q, H->d_sr_scal + 2);
   SR_CHECK();
-  H->launches += 5;
+  comm_allreduce_sum(H, H->d_sr_scal + 2, 1, true);
+  sr_weights_kernel<<<1, 1024, 0, H->stream>>>(B, H->sr_q, 4.0 / N, centered ? 1 : 0, H->d_sr_scal + 2, N, H->w,
+                                               H->d_wscale);
+  SR_CHECK();
+  H->launches += 6;
   launch_gw2_umma(H, B, /*wg1_done=*/false);  // w' [G1 | 1] pair, then gW2 / gb2
   launch_backward_after_dg1(H, B);            // dz1 (the batch's dg1 partials), gW1 / gb1
+  comm_allreduce_sum(H, H->G, (size_t)H->L.total, false);
 }
 
 void apply_fisher_dense(Handle* H, int B) {
@@ -677,7 +687,10 @@ bool sr_solve(Handle* H, int B, double lambda, double tol, int max_iterations, b
   const Layout& L = H->L;
   const int64_t total = L.total;
   // optimizer.cpp:66: the reference solves the dense system when d <= 2000
-  if (H->d <= 2000) return sr_dense_solve(H, B, lambda, tol, centered, iterations, residual, gnorm_out);
+  if (H->d <= 2000) {
+    if (H->nranks > 1) throw InvalidArgument("multi-GPU SR needs the CG path (reference d > 2000)");
+    return sr_dense_solve(H, B, lambda, tol, centered, iterations, residual, gnorm_out);
+  }
   cg_init_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, H->cg_g, H->cg_x, H->cg_r, H->cg_p, H->cg_part);
   SR_CHECK();
   H->launches++;

@@ -166,3 +166,39 @@ def test_sr_dense_cholesky(mdim):
     assert np.abs(x - np.linalg.solve(A, b)).max() <= 1e-9 * np.abs(np.linalg.solve(A, b)).max()
     A[0, 0] = -1.0  # not positive definite -> flagged
     assert f(mdim, K.ptr(A), K.ptr(b), K.ptr(x)) == 1
+
+
+def test_sr_step_through_nccl_matches_single_gpu(monkeypatch):
+    """The multi-GPU SR step (gradient, q-sum and F p all-reduced over the ranks' NCCL communicator
+    inside every CG iteration) run through a one-rank communicator (VQMC_NCCL_SELF=1) gives bitwise
+    the single-GPU result over three SGD + SR steps (CG path, d > 2000)."""
+    n, B = 100, 256
+    h = O.default_made_hidden(n)
+    m = O.made_init(n, h, 7)
+    e = np.ascontiguousarray(O.random_maxcut_graph(n, 7), np.int32).reshape(-1, 2)
+    monkeypatch.setenv("VQMC_NCCL_SELF", "1")
+    hs = []
+    for _ in range(2):
+        hd = C.c_void_p()
+        K.check(K.lib.vqmc_gpu_create(0, n, h, K.ptr(m.degrees), K.ptr(m.theta), K.ptr(e), len(e), B, C.byref(hd)))
+        hs.append(hd)
+    uid = (C.c_uint8 * 128)()
+    K.check(K.lib.vqmc_gpu_comm_unique_id(uid))
+    K.check(K.lib.vqmc_gpu_comm_init(hs[1], uid, 1, 0))
+    out = [[], []]
+    try:
+        for t in range(3):
+            for k, hd in enumerate(hs):
+                st, it, res = K.StepStats(), C.c_int(0), C.c_double(0.0)
+                K.check(K.lib.vqmc_gpu_train_step_sr(hd, B, 1, None, 7, 1, t, 0.1, 1e-3, 1e-6, 200, 0, 1, C.byref(st),
+                                                     C.byref(it), C.byref(res)))
+                out[k].append((st.energy_mean, st.grad_norm, it.value, res.value))
+        assert out[0] == out[1]
+        d = 2 * h * n + h + n
+        th = [np.empty(d), np.empty(d)]
+        for k, hd in enumerate(hs):
+            K.check(K.lib.vqmc_gpu_get_params(hd, K.ptr(th[k])))
+        assert np.array_equal(th[0], th[1])
+    finally:
+        for hd in hs:
+            K.lib.vqmc_gpu_destroy(hd)
