@@ -129,3 +129,13 @@ def test_solve_sgd_sr(tmp_path):
     r = run("solve", "--problem", "maxcut", "--n", 30, "--optimizer", "sgd_sr", "--iterations", 1, "--minibatch",
             64, "--sr-maxiter", 0, "--sr-fallback", "--out", tmp_path / "fb")
     assert r.returncode == 0, r.stderr
+
+
+@pytest.mark.gpu
+def test_solve_target_reports_hit(tmp_path):  # vqmc.cpp:240-243 (hitting-time mode)
+    out = tmp_path / "run"
+    r = run("solve", "--problem", "maxcut", "--n", 12, "--iterations", 20, "--minibatch", 64, "--eval-batch", 64,
+            "--target", 1, "--out", out)
+    assert r.returncode == 0, r.stderr
+    s = json.loads((out / "summary.json").read_text())
+    assert s["hit_iteration"] == 1 and s["hit_time_s"] > 0 and s["iterations_run"] == 1

@@ -348,3 +348,21 @@ def test_overlapped_allreduce_path_matches_single_gpu(monkeypatch):
             stats[k].append((st.energy_mean, st.grad_norm))
     assert stats[0] == stats[1]
     assert np.array_equal(devs[0].get_params(), devs[1].get_params())
+
+
+def test_hitting_time_mode():
+    """trainer_test.cpp:146-158 / trainer.cpp:265-274: with a target the run evaluates after every
+    iteration (outside the timed phases) and stops at the first hit (Max-Cut: best_cut >= target)."""
+    g = api.random_maxcut_graph(20, 2)
+    cfg = api.RunConfig(problem=api.maxcut_spec(g), iterations=50, minibatch=64, eval_batch=128, seed=1, target=1.0)
+    res = api.train(cfg)
+    assert res.hit_iteration == 1 and len(res.stats) == 1 and res.hit_time is not None and res.hit_time > 0
+    opt, _ = O.brute_force_maxcut(20, g.edges)
+    cfg = api.RunConfig(problem=api.maxcut_spec(g), iterations=300, minibatch=1024, eval_batch=1024, seed=1,
+                        target=float(opt), uniforms="mt19937")
+    res = api.train(cfg)
+    assert res.hit_iteration == -1 or (res.best_cut >= opt and len(res.stats) == res.hit_iteration)
+    cfg = api.RunConfig(problem=api.maxcut_spec(g), iterations=5, minibatch=64, eval_batch=128, seed=1,
+                        target=1e9)  # unreachable: runs every iteration, no hit
+    res = api.train(cfg)
+    assert res.hit_iteration == -1 and res.hit_time is None and len(res.stats) == 5
