@@ -159,9 +159,9 @@ __device__ __forceinline__ int pmax_exp(const unsigned* pmax) {
 __global__ void sr_split_kernel(int n, int h, int ld, const double* __restrict__ p, int64_t off_w2, int64_t off_b2,
                                 const int32_t* __restrict__ deg, const unsigned* __restrict__ pmax,
                                 __half* __restrict__ hi, __half* __restrict__ lo) {
-  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= (int64_t)n * ld) return;
-  const int i = (int)(t / ld), c = (int)(t % ld);
+  const int i = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;  // row i, column c
+  if (i >= n || c >= ld) return;
+  const size_t t = (size_t)i * ld + c;
   const int e = pmax_exp(pmax);
   double x = 0.0;
   if (c < h) x = deg[c] < i + 1 ? p[off_w2 + (int64_t)i * h + c] : 0.0;  // M2(i, c)
@@ -270,10 +270,12 @@ __global__ void sr_q_kernel(int B, int h, const float* __restrict__ dz1, const d
   for (int k = lane; k < h; k += 32) s += (double)dz1[(size_t)b * h + k] * pb1[k];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  double t2 = 0.0;  // GEMM partials: lane-strided, then the same fixed shuffle tree
+  for (int t = lane; t < nparts; t += 32) t2 += sp_part[(size_t)t * B + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t2 += __shfl_xor_sync(kFull, t2, o);
   if (lane == 0) {
     for (int t = 0; t < q1_tiles; ++t) s += q1_part[(size_t)t * B + b];
-    double t2 = 0.0;
-    for (int t = 0; t < nparts; ++t) t2 += sp_part[(size_t)t * B + b];
     q[b] = s + ldexp(t2, pmax_exp(pmax));
   }
 }
@@ -494,8 +496,7 @@ double sum_parts(Handle* H, const double* part, int cnt) {
 // batch's G1 / D / X and dg1 partials.
 void apply_fisher(Handle* H, int B, bool centered) {
   const Layout& L = H->L;
-  const int64_t tot = (int64_t)L.n * H->hp18;
-  sr_split_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, H->stream>>>(L.n, L.h, H->hp18, H->cg_p, L.off_w2,
+  sr_split_kernel<<<dim3((unsigned)((H->hp18 + 127) / 128), (unsigned)L.n), 128, 0, H->stream>>>(L.n, L.h, H->hp18, H->cg_p, L.off_w2,
                                                                          L.off_b2, H->d_deg, H->d_pmax, H->SRh,
                                                                          H->SRl);
   SR_CHECK();
