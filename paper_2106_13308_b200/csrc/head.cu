@@ -563,7 +563,7 @@ __device__ __forceinline__ void head_v3_phases(HeadV3State<KG>& S, const HeadRin
 // pair, D pair, spins, log-probability, packed X words).  The consumers only run the serial
 // chain and the rank-1 updates; thresholds come precomputed (head_thresholds_kernel).
 template <int KG, bool GIVEN>
-__global__ void __launch_bounds__(32 * (5 + kHeadEmitWarps)) head_v3_kernel(const __grid_constant__ HeadV3Args A) {
+__global__ void __launch_bounds__(32 * (8 / kHeadS + 1 + kHeadEmitWarps)) head_v3_kernel(const __grid_constant__ HeadV3Args A) {
   constexpr int KPL = 4 * KG;  // word slots per lane
   constexpr int RS = 128 * KG; // staged row stride (floats), both matrices
   extern __shared__ __align__(128) unsigned char smem_raw[];
