@@ -366,3 +366,39 @@ def test_hitting_time_mode():
                         target=1e9)  # unreachable: runs every iteration, no hit
     res = api.train(cfg)
     assert res.hit_iteration == -1 and res.hit_time is None and len(res.stats) == 5
+
+
+@pytest.mark.parametrize("n,L,mbs", [(1000, 3, 77), (300, 1, 33), (20, 5, 7)])
+def test_fused_step_parity_ragged_batches(n, L, mbs):
+    """Ragged batches (B not a multiple of the 32-sample energy groups, the 256-row GEMM tiles or
+    the head's 8-sample CTAs): one fused step == oracle iteration 0, as above."""
+    seed = 5
+    e = O.random_maxcut_graph(n, seed)
+    h = O.default_made_hidden(n)
+    r = O.train(n, e, h=h, iterations=1, workers=L, minibatch=mbs, eval_batch=16, seed=seed, want_first_grad=True,
+                sampler_mode=1)
+    m0 = O.made_init(n, h, seed)
+    dev = Dev(n, h, m0.degrees, m0.theta, e, L * mbs)
+    U = np.concatenate([O.uniforms(seed, w + 1, n * mbs).reshape(n, mbs) for w in range(L)], axis=1)
+    st = _train_step(dev, mbs, L, np.ascontiguousarray(U), seed, 1, 0, 1)
+    assert st.energy_mean == r["stats"][0, 0]
+    # std: the device forms the variance exactly from integer cut sums and rounds once; the oracle's
+    # two-pass fp64 sum (like Eigen's, whose SIMD reduction order the oracle does not reproduce
+    # either) rounds per term, so for N not a power of two they may differ in the last bits
+    assert np.sqrt(st.energy_var) == pytest.approx(r["stats"][0, 1], rel=1e-15, abs=0)
+    assert st.grad_norm == pytest.approx(r["stats"][0, 2], rel=1e-4)
+    g = r["first_grad"]
+    sel = np.abs(g) > 1e-6 * np.abs(g).max()
+    d_ref, d_got = r["theta"] - m0.theta, dev.get_params() - m0.theta
+    assert np.all(np.abs(d_got[sel] - d_ref[sel]) <= 1e-6 + 1e-4 * np.abs(d_ref[sel]))
+
+
+@pytest.mark.parametrize("n,B", [(1000, 100), (300, 37), (10000, 5)])
+def test_sampler_parity_production_philox_ragged(n, B):
+    m = _model(n, 6, perturb=n < 10000)
+    dev = Dev(n, m.h, m.degrees, m.theta, _graph(n, 6, "regular"), B)
+    xg, lp = dev.sample(B, None, seed=3, stream=2, call=5)
+    U = O.philox_uniforms(3, 2, 5, n, B)
+    xo, lo, po = O.auto_sample(m, B, uniforms=U, mode=1, want_p=True)
+    flips, clean = check_samples(xg, xo, U, po)
+    assert clean >= 0.8 * B
