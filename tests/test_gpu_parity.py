@@ -402,3 +402,28 @@ def test_sampler_parity_production_philox_ragged(n, B):
     xo, lo, po = O.auto_sample(m, B, uniforms=U, mode=1, want_p=True)
     flips, clean = check_samples(xg, xo, U, po)
     assert clean >= 0.8 * B
+
+
+@pytest.mark.parametrize("n", [2, 3, 33])
+def test_edge_cases_tiny_models_and_empty_graphs(n):
+    """Smallest models (n = 2: h = 2, one head bit) and graphs without edges: sampling parity,
+    exact zero energies, and a training step whose zero-variance batch gives a zero gradient
+    (a zero Adam update), like the reference (estimator.hpp:111-119, optimizer.cpp:21-35)."""
+    h = O.default_made_hidden(n)
+    m = O.made_init(n, h, 2)
+    B = 64
+    for edges in (np.zeros((0, 2), np.int32), O.random_maxcut_graph(n, 2)):
+        dev = Dev(n, h, m.degrees, m.theta, edges, B)
+        U = O.uniforms(2, 1, n * B).reshape(n, B)
+        xg, lp = dev.sample(B, U)
+        xo, lo, po = O.auto_sample(m, B, uniforms=U, mode=0, want_p=True)
+        check_samples(xg, xo, U, po)
+        cut, le = dev.energy(xo)
+        lo_ref, _ = O.local_energy(n, edges, xo)
+        assert np.array_equal(le, lo_ref)
+        if len(np.asarray(edges).reshape(-1, 2)) == 0:
+            assert np.all(cut == 0) and np.all(le == 0.0)
+            p0 = dev.get_params()  # (the device master copy is fp32)
+            st = _train_step(dev, B, 1, np.ascontiguousarray(U), 2, 1, 0, 1)
+            assert st.energy_mean == 0.0 and st.energy_var == 0.0 and st.grad_norm == 0.0
+            assert np.array_equal(dev.get_params(), p0)

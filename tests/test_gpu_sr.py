@@ -26,7 +26,7 @@ def _setup(n, B, seed):
     r = O.auto_sample(m, B, seed=seed, stream=1, mode=1)
     x = np.ascontiguousarray(r[0] if isinstance(r, tuple) else r, np.uint8)
     e = O.random_maxcut_graph(n, seed)
-    g = O.gradient_from_locals(m, x, O.local_energy(n, e, x))
+    g = O.gradient_from_locals(m, x, O.local_energy(n, e, x)[0])
     return m, e, x, g
 
 
