@@ -427,3 +427,28 @@ def test_edge_cases_tiny_models_and_empty_graphs(n):
             st = _train_step(dev, B, 1, np.ascontiguousarray(U), 2, 1, 0, 1)
             assert st.energy_mean == 0.0 and st.energy_var == 0.0 and st.grad_norm == 0.0
             assert np.array_equal(dev.get_params(), p0)
+
+
+@pytest.mark.parametrize("n,h", [(1200, 1000), (3000, 1024)])
+def test_maximum_hidden_width(n, h):
+    """The widest supported hidden layer (kMaxHidden = 1024: the head sampler's 8 register slots
+    per lane and its largest shared-memory ring): sampling parity and a finite training step."""
+    m = _model(n, 4, perturb=False, h=h)
+    m.theta = m.theta + (O.uniforms(4, 98, m.d) * 0.2 - 0.1)
+    B = 64
+    dev = Dev(n, h, m.degrees, m.theta, _graph(n, 4, "regular"), B)
+    U = O.uniforms(4, 1, n * B).reshape(n, B)
+    xg, lp = dev.sample(B, U)
+    xo, lo, po = O.auto_sample(m, B, uniforms=U, mode=1, want_p=True)
+    flips, clean = check_samples(xg, xo, U, po)
+    assert clean >= 0.5 * B
+    st = _train_step(dev, B, 1, None, 4, 1, 0, 1)
+    assert np.isfinite(st.energy_mean) and np.isfinite(st.grad_norm) and st.grad_norm > 0
+
+
+def test_hidden_width_above_maximum_is_rejected():
+    n, h = 1200, 1100
+    m = _model(n, 4, perturb=False, h=h)
+    with pytest.raises(ValueError):
+        dev = Dev(n, h, m.degrees, m.theta, _graph(n, 4, "regular"), 64)
+        dev.sample(64, O.uniforms(4, 1, n * 64).reshape(n, 64))
