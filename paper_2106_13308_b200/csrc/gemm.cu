@@ -105,11 +105,7 @@ static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, cons
                         cudaStream_t stream) {
   using Cfg = UmmaCfg<BN>;
   auto kern = umma3p_kernel<BN, A_MN, B_MN, Epi, A_EXACT, EK>;
-  static bool attr = false;
-  if (!attr) {
-    VQMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
-    attr = true;
-  }
+  ensure_smem_attr((const void*)kern, Cfg::kSmem);
   const int nkb = (K + UmmaElem<EK>::kBK - 1) / UmmaElem<EK>::kBK;
   UmmaArgs args{M, N, K, (nkb + splits - 1) / splits, (N + BN - 1) / BN, (M + kUmmaBM - 1) / kUmmaBM, splits};
   const int ntiles = args.tiles_n * args.tiles_m * splits;
@@ -131,11 +127,7 @@ static void launch_umma2(Handle* H, const char* name, const CUtensorMap& ah, con
                          cudaStream_t stream) {
   using Cfg = Umma2Cfg<BN>;
   auto kern = umma2_kernel<BN, A_MN, B_MN, Epi, A_EXACT, EK>;
-  static bool attr = false;
-  if (!attr) {
-    VQMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)Cfg::kSmem));
-    attr = true;
-  }
+  ensure_smem_attr((const void*)kern, Cfg::kSmem);
   const int nkb = (K + Cfg::kBK - 1) / Cfg::kBK;
   UmmaArgs args{M, N, K, (nkb + splits - 1) / splits, (N + BN - 1) / BN, (M + 2 * kUmmaBM - 1) / (2 * kUmmaBM), splits};
   const int ntiles = args.tiles_n * args.tiles_m * splits;

@@ -782,12 +782,7 @@ template <int KPL, bool FAST, bool GIVEN>
 static void head_v2_launch(Handle* H, int B, const double* uni, RngSpec rng, double* cond) {
   const Layout& L = H->L;
   const HeadGeom geo = head_geometry(H);
-  static size_t attr_set = 0;
-  if (attr_set < geo.smem) {
-    VQMC_CUDA(cudaFuncSetAttribute(head_v2_kernel<KPL, FAST, GIVEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)geo.smem));
-    attr_set = geo.smem;
-  }
+  ensure_smem_attr((const void*)head_v2_kernel<KPL, FAST, GIVEN>, geo.smem);
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, H->device);
   const int nw = std::max(1, std::min(8, (B + dev_sms - 1) / dev_sms));  // <= 8 sample warps + producer
@@ -844,12 +839,7 @@ template <int KG, bool GIVEN>
 static void head_v3_launch(Handle* H, int B, const double* uni, RngSpec rng, double* cond) {
   const Layout& L = H->L;
   const HeadGeom geo = head_v3_geometry(H);
-  static size_t attr_set = 0;
-  if (attr_set < geo.smem) {
-    VQMC_CUDA(cudaFuncSetAttribute(head_v3_kernel<KG, GIVEN>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)geo.smem));
-    attr_set = geo.smem;
-  }
+  ensure_smem_attr((const void*)head_v3_kernel<KG, GIVEN>, geo.smem);
   int dev_sms = 148;
   cudaDeviceGetAttribute(&dev_sms, cudaDevAttrMultiProcessorCount, H->device);
   const int groups = (B + kHeadS - 1) / kHeadS;  // consumer warps needed

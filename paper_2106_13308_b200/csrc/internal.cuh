@@ -100,6 +100,10 @@ struct KScope {
 
 // Kernel launchers (kernels.cu).  All enqueue on h->stream.
 void launch_params_refresh(Handle* h);
+// cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `kern` on the current device, once per
+// (kernel, device, size): function attributes are per device, and handles on different devices
+// may share a process (thread-safe).
+void ensure_smem_attr(const void* kern, size_t bytes);
 void launch_head_pack(Handle* h);
 void launch_head_v2(Handle* h, int B, const double* d_uniforms, RngSpec rng, bool given_bits,
                     double* d_cond);

@@ -13,6 +13,9 @@
 
 #include <algorithm>
 #include <cmath>
+#include <map>
+#include <mutex>
+#include <utility>
 
 #include "device_common.cuh"
 #include "adam.cuh"
@@ -623,6 +626,19 @@ __global__ void sum_partials_kernel(int cnt, const double* __restrict__ part, do
 // ===========================================================================
 #define LAUNCH_CHECK() VQMC_CUDA(cudaGetLastError())
 
+void ensure_smem_attr(const void* kern, size_t bytes) {
+  if (bytes <= 48 * 1024) return;
+  int dev = 0;
+  VQMC_CUDA(cudaGetDevice(&dev));
+  static std::mutex mu;
+  static std::map<std::pair<const void*, int>, size_t> done;
+  std::lock_guard<std::mutex> lock(mu);
+  size_t& have = done[{kern, dev}];
+  if (have >= bytes) return;
+  VQMC_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  have = bytes;
+}
+
 void record_event(Handle* H, cudaEvent_t ev) {
   if (H->capturing) VQMC_CUDA(cudaEventRecordWithFlags(ev, H->stream, cudaEventRecordExternal));
   else VQMC_CUDA(cudaEventRecord(ev, H->stream));
@@ -688,11 +704,7 @@ void launch_energy(Handle* H, int B) {
     per = (per + 1) & ~int64_t(1);  // even: the bulk copies start 16-byte aligned
     chunks = std::max<int64_t>(1, (nE + per - 1) / per);
     const size_t smem = tsm + (size_t)(per + 2) * 8;
-    static size_t attr = 0;
-    if (smem > 48 * 1024 && attr < smem) {
-      VQMC_CUDA(cudaFuncSetAttribute(maxcut_cut_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)cap));
-      attr = cap;
-    }
+    if (smem > 48 * 1024) ensure_smem_attr((const void*)maxcut_cut_kernel, cap);
     H->ensure_cpart((int)chunks * B);
     H->cut_chunks = (int)chunks;
     KScope ks(H, "maxcut_energy");
@@ -704,9 +716,7 @@ void launch_energy(Handle* H, int B) {
   }
   constexpr int S = 4;
   const size_t smem = (size_t)S * W * sizeof(uint32_t);
-  if (smem > 48 * 1024)
-    VQMC_CUDA(cudaFuncSetAttribute(energy_kernel<S>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                   (int)smem));
+  ensure_smem_attr((const void*)energy_kernel<S>, smem);
   H->ensure_cpart(B);
   H->cut_chunks = 1;
   KScope ks(H, "maxcut_energy");
@@ -733,11 +743,7 @@ void launch_cuts_reduce(Handle* H, int B) {
 void launch_weights_from_locals(Handle* H, int B, int seg, bool with_wg1) {
   const Layout& L = H->L;
   const size_t smem = (size_t)B * sizeof(float);
-  static size_t attr = 0;
-  if (smem > 48 * 1024 && attr < smem) {
-    VQMC_CUDA(cudaFuncSetAttribute(stats_weights_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    attr = smem;
-  }
+  ensure_smem_attr((const void*)stats_weights_kernel, smem);
   const int64_t total = (int64_t)B * H->hp18;
   const int grid = with_wg1 ? (int)std::max<int64_t>(1, std::min<int64_t>(148, (total + 4095) / 4096)) : 1;
   KScope ks(H, with_wg1 ? "stats_weights_wg1" : "stats_weights");
