@@ -473,7 +473,7 @@ __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __re
 // Adam over the live parameter buffer (optimizer.cpp:21-35), fp32 master weights, gradient
 // scaled by 1/L (allreduce_mean's division, trainer.cpp:334), fused with everything that
 // derives from the updated parameters: the squared norm of the reduced gradient (last-block
-// reduction, fixed order; trainer.cpp:253), the tf32 split of W2 for the GEMMs and the head
+// reduction, fixed order; trainer.cpp:253), the fp16 pair of W2 for the GEMMs and the head
 // sampler's padded / completion-ordered copies of the head blocks.
 // Adam over the element range [lo, hi) of the live buffer.  The training step runs it as up to
 // two launches (the [W2 | b2] range right after its gradient and the W1 GEMM's last read of W2,
@@ -655,7 +655,7 @@ KScope::~KScope() {
 }
 
 // Derived device copies of the parameters (after set_params): the head sampler's staged
-// head blocks and the tf32 split of W2 (Adam refreshes both itself).
+// head blocks and the fp16 pair of W2 (Adam refreshes both itself).
 void launch_params_refresh(Handle* H) {
   launch_head_pack(H);
   launch_split_w2(H);
