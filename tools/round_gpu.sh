@@ -15,6 +15,10 @@ timeout 900 ncu --set full --clock-control none --import-source on -k regex:'hea
 python tools/ncu_summary.py report gpurun_out/${TAG}_umma.ncu-rep gpurun_out/profiles/${TAG}_umma_full.txt > /dev/null
 python tools/ncu_summary.py report gpurun_out/${TAG}_misc.ncu-rep gpurun_out/profiles/${TAG}_misc_full.txt > /dev/null
 python tools/traffic_json.py gpurun_out/profiles/traffic.json gpurun_out/${TAG}_umma.ncu-rep gpurun_out/${TAG}_misc.ncu-rep > /dev/null
+# SR (natural gradient) step: launch list of one solve and the step rate at N = 10k
+timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none --csv --log-file gpurun_out/${TAG}_sr_launches.csv python scripts/sr_rate.py 10000 0 > gpurun_out/${TAG}_sr_ncu.log 2>&1
+python tools/ncu_summary.py launches gpurun_out/${TAG}_sr_launches.csv gpurun_out/profiles/${TAG}_sr_launches.txt > /dev/null
+timeout 300 python scripts/sr_rate.py 10000 3 > gpurun_out/profiles/${TAG}_sr_rate.txt 2>&1
 cp gpurun_out/${TAG}_bench.json gpurun_out/profiles/${TAG}_bench.json; cp gpurun_out/${TAG}_bench_ref.json gpurun_out/profiles/${TAG}_bench_ref.json
 head -24 gpurun_out/profiles/${TAG}_launches.txt
 ls gpurun_out/profiles
