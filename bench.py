@@ -473,7 +473,8 @@ def cpu_baseline(args, g, B, steps=1, budget_s=None):
             for _ in range(steps)]
     step_s = float(np.mean([r["step_s"] for r in runs]))
     return {"value": workers * mbs / step_s, "unit": "samples/s", "cores": workers, "kind": "port",
-            "steps_per_s": 1.0 / step_s,
+            "steps_per_s": 1.0 / step_s, "extrapolated": bits < args.n, "bits_timed": bits,
+            "cpu_model": cpu_model(), "nproc": cores,
             "sample": f"one reference iteration, {workers} worker threads x minibatch {mbs} (batch {workers * mbs}); "
                       f"sampler timed for the first {bits} of {args.n} bits (each bit is one full two-GEMM forward "
                       f"pass, sampler.cpp:47-48) and extrapolated x{args.n / bits:.1f}; energy, gradient, tree "
@@ -482,38 +483,86 @@ def cpu_baseline(args, g, B, steps=1, budget_s=None):
             "update_s": runs[0]["update_s"], "oracle": "oracle/vqmc_oracle.cpp (restated reference; Eigen absent)"}
 
 
+def cpu_model():
+    try:
+        for line in open("/proc/cpuinfo"):
+            if line.startswith("model name"):
+                return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return "unknown"
+
+
+def oracle_instance(args):
+    """The same synthetic instance as make_instance, generated by the oracle (the reference arm
+    must not load the repo's own library)."""
+    sys.path.insert(0, os.path.join(ROOT, "oracle"))
+    import pyoracle as O
+    if args.graph == "regular3":
+        e = O.random_regular_graph(args.n, 3, args.seed)
+        return e, f"random 3-regular, |E|={len(e)}"
+    e = O.random_maxcut_graph(args.n, args.seed)
+    return e, f"reference G(n,3/4), |E|={len(e)}"
+
+
+def validate_extrapolation(O, workers, mbs, seed, n=1000, bits=40):
+    """One FULL reference iteration (all n sampler bits timed) against the per-bit extrapolation
+    used at N = 10k (sampler timed for `bits` bits, x n / bits; every bit is one identical full
+    two-GEMM forward pass, sampler.cpp:47-48; trainer.cpp:254 times the whole iteration)."""
+    e = O.random_regular_graph(n, 3, seed)
+    O.time_reference_step(n, e, workers, mbs, seed=seed, bits_limit=4)  # (warm the BLAS / threads)
+    t0 = time.perf_counter()
+    full = O.time_reference_step(n, e, workers, mbs, seed=seed, bits_limit=n)
+    wall = time.perf_counter() - t0
+    ext = O.time_reference_step(n, e, workers, mbs, seed=seed, bits_limit=bits)
+    return {"n": n, "graph": "random 3-regular", "measured_step_s": full["step_s"], "measured_wall_s": wall,
+            "extrapolated_step_s": ext["step_s"], "bits_timed_in_extrapolation": bits,
+            "measured_over_extrapolated": full["step_s"] / ext["step_s"]}
+
+
 def run_reference(args):
+    """The reference algorithm (the oracle's restatement of proj/src/{sampler,models,trainer}.cpp,
+    fp64, n full forward passes per sampling call; Eigen is absent so the reference itself cannot be
+    built) on all host cores.  Imports only oracle/ (never the repo's package or its .so)."""
     world, rank, local = dist_env()
     if rank != 0:
         return None
-    g, gdesc = make_instance(args)
+    e, gdesc = oracle_instance(args)
     B = args.minibatch
     K_, W_ = max(1, args.steps), max(0, args.warmup)
     budget = max(2.0, min(20.0, 150.0 / (K_ + W_)))
-    sys.path.insert(0, os.path.join(ROOT, "oracle"))
     import pyoracle as O
     cores = os.cpu_count() or 1
     workers = max(1, min(cores, B // 2))
     mbs = max(2, B // workers)
-    cal = O.time_reference_step(args.n, g.edges, workers, mbs, seed=args.seed, bits_limit=1)
+    t_start = time.perf_counter()
+    cal = O.time_reference_step(args.n, e, workers, mbs, seed=args.seed, bits_limit=1)
     per_bit = cal["sample_s"] / args.n
     bits = int(max(1, min(args.n, budget / max(per_bit, 1e-9))))
     for _ in range(W_):
-        O.time_reference_step(args.n, g.edges, workers, mbs, seed=args.seed, bits_limit=max(1, bits // 4))
-    steps = [O.time_reference_step(args.n, g.edges, workers, mbs, seed=args.seed, bits_limit=bits)["step_s"]
-             for _ in range(K_)]
-    step_s = float(np.mean(steps))
+        O.time_reference_step(args.n, e, workers, mbs, seed=args.seed, bits_limit=max(1, bits // 4))
+    t_timed = time.perf_counter()
+    runs = [O.time_reference_step(args.n, e, workers, mbs, seed=args.seed, bits_limit=bits) for _ in range(K_)]
+    timed_wall = time.perf_counter() - t_timed
+    step_s = float(np.mean([r["step_s"] for r in runs]))
     value = workers * mbs / step_s
+    val = validate_extrapolation(O, workers, mbs, args.seed) if args.n > 1000 else None
     h = O.default_made_hidden(args.n)
+    extrap = bits < args.n
     sample = (f"{workers} worker threads x minibatch {mbs}; per step the reference sampler runs the first {bits} of "
-              f"{args.n} bits (one full forward pass each) and is extrapolated; energy/gradient/all-reduce/Adam in full")
+              f"{args.n} bits (one full forward pass each)" + (" and is extrapolated x n/bits" if extrap else "") +
+              "; energy/gradient/all-reduce/Adam timed in full")
     return {"impl": "reference", "metric": "samples/sec (VQMC training step, N=10k Max-Cut MADE)", "value": value,
             "unit": "samples/s", "n_gpus": 0, "steps": K_, "warmup": W_, "ms_per_step": step_s * 1000.0,
             "steps_per_s": 1.0 / step_s, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
             "dtype": "f64", "data": "synthetic",
             "config": {"workload": f"Max-Cut N={args.n} ({gdesc}), MADE h={h}, AUTO sampler, ADAM lr=0.01",
                        "samples_per_step": workers * mbs, "parallelism": f"{workers} host threads"},
-            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": workers, "kind": "port", "sample": sample},
+            "extrapolated": extrap, "bits_timed": bits, "bits_total": args.n,
+            "timed_region_wall_s": timed_wall, "run_wall_s": time.perf_counter() - t_start,
+            "extrapolation_check": val, "nproc": cores, "cpu_model": cpu_model(),
+            "cpu_baseline": {"value": value, "unit": "samples/s", "cores": workers, "kind": "port", "sample": sample,
+                             "cpu_model": cpu_model()},
             "e2e": {"value": value, "unit": "samples/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
 
 

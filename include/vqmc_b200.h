@@ -153,6 +153,15 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
 
 /* Copy the last step's cut values (B int32) to the host. */
 int vqmc_gpu_last_cuts(vqmc_gpu_t* g, int32_t* cuts_out, int B);
+/* Copy the configurations of the handle's last batch (the last train step's samples, or the
+ * last vqmc_gpu_evaluate / sample / log_psi batch) to the host: B x W packed words.  The
+ * reference keeps them in SampleBatch::configs (sampler.hpp:24-30); the parity tests compare
+ * them with the oracle's draws and feed them to the oracle's downstream functions. */
+int vqmc_gpu_last_samples(vqmc_gpu_t* g, uint32_t* bits_out, int B);
+/* The reduced gradient of the last vqmc_gpu_train_step (allreduce_mean over every worker and
+ * rank, i.e. what Adam consumed), d entries in the reference order: the value the reference
+ * hands to RunConfig::gradient_observer (trainer.hpp:57, trainer.cpp:187-188). */
+int vqmc_gpu_last_gradient(vqmc_gpu_t* g, double* grad_out);
 
 /* evaluate (trainer.cpp:91-108): fresh batch, out = {energy_mean, energy_std,
  * best_cut, mean_cut}.  uniforms as in vqmc_gpu_sample. */

@@ -62,6 +62,8 @@ def lib():
     L.oracle_train.argtypes = [C.c_int, C.c_int, _ip, C.c_int64, C.c_int, C.c_double, C.c_int, C.c_int,
                                C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int, C.c_void_p, C.c_void_p,
                                C.c_void_p, C.c_void_p]
+    L.oracle_evaluate.argtypes = [C.c_int, C.c_int, _ip, _dp, _ip, C.c_int64, C.c_int, C.c_uint64, C.c_uint64,
+                                  C.c_void_p, C.c_int, _dp]
     L.oracle_enumerate_distribution.argtypes = [C.c_int, C.c_int, _ip, _dp, _dp]
     L.oracle_time_reference_step.argtypes = [C.c_int, C.c_int, _ip, C.c_int64, C.c_int, C.c_int, C.c_uint64,
                                              C.c_int, _dp]
@@ -291,6 +293,15 @@ def train(n, edges, h=0, optimizer="adam", lr=0.0, iterations=300, workers=1, mi
                theta=theta, h=hh)
     if want_first_grad:
         out["first_grad"] = g0
+    return out
+
+
+def evaluate(m: Made, edges, B, seed=0, stream=1_000_000_007, uniforms=None, mode=0):
+    """evaluate (trainer.cpp:91-108): {energy, energy_std, best_cut, mean_cut} of B samples."""
+    e = np.ascontiguousarray(edges, np.int32).reshape(-1)
+    u = None if uniforms is None else np.ascontiguousarray(uniforms, np.float64)
+    out = np.empty(4)
+    _check(lib().oracle_evaluate(m.n, m.h, m.degrees, m.theta, e, e.size // 2, B, seed, stream, _ptr(u), mode, out))
     return out
 
 

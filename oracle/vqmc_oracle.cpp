@@ -767,10 +767,11 @@ struct EvalOut {
 };
 
 // proj/src/trainer.cpp:91-108
+// (uniforms: optional [n][eval_batch] draws replacing rng's, as the GPU parity tests feed them)
 EvalOut evaluate(int n, const std::vector<Edge>& e, const Made& m, int eval_batch,
-                 std::mt19937_64& rng, bool incremental) {
-  const Sample s = incremental ? auto_sample_incremental(m, eval_batch, &rng, nullptr, nullptr)
-                               : auto_sample(m, eval_batch, &rng, nullptr, nullptr);
+                 std::mt19937_64& rng, bool incremental, const double* uniforms = nullptr) {
+  const Sample s = incremental ? auto_sample_incremental(m, eval_batch, &rng, uniforms, nullptr)
+                               : auto_sample(m, eval_batch, &rng, uniforms, nullptr);
   const auto l = local_energy_maxcut(n, e, s.X.data(), eval_batch);
   const auto mv = energy_and_variance(l);
   EvalOut o{mv.first, std::sqrt(mv.second), 0.0, 0.0};
@@ -1160,6 +1161,24 @@ int oracle_train(int n, int h, const int32_t* edges, int64_t E, int optimizer, d
     eval_out[3] = ev.mean_cut;
   }
   if (theta_out) get_theta(model, theta_out);
+  ORACLE_CATCH
+}
+
+// evaluate (proj/src/trainer.cpp:91-108) of a given model on make_stream(seed, stream) (or the
+// given [n][B] uniforms): out = {energy, energy_std, best_cut, mean_cut}.
+int oracle_evaluate(int n, int h, const int* deg, const double* theta, const int32_t* edges, int64_t E, int B,
+                    uint64_t seed, uint64_t stream, const double* uniforms, int mode, double* out) {
+  ORACLE_TRY
+  if (B < 2) throw std::invalid_argument("variance needs at least two samples");
+  std::vector<Edge> e((size_t)E);
+  for (int64_t t = 0; t < E; ++t) e[t] = {edges[2 * t], edges[2 * t + 1]};
+  const Made m = made_from(n, h, deg, theta);
+  auto rng = make_stream(seed, stream);
+  const EvalOut ev = evaluate(n, e, m, B, rng, mode == 1, uniforms);
+  out[0] = ev.energy;
+  out[1] = ev.energy_std;
+  out[2] = ev.best_cut;
+  out[3] = ev.mean_cut;
   ORACLE_CATCH
 }
 

@@ -54,6 +54,8 @@ _SIGS = {
                                C.c_int, C.POINTER(StepStats), C.POINTER(C.c_int), C.POINTER(_dbl)],
     "vqmc_pooled_stats": [_i64, _i64, _i64, _i64, C.POINTER(_dbl), C.POINTER(_dbl)],
     "vqmc_gpu_last_cuts": [_vp, _vp, C.c_int],
+    "vqmc_gpu_last_samples": [_vp, _vp, C.c_int],
+    "vqmc_gpu_last_gradient": [_vp, _vp],
     "vqmc_gpu_evaluate": [_vp, C.c_int, _vp, _u64, _u64, _u64, _vp],
     "vqmc_gpu_synchronize": [_vp],
     "vqmc_gpu_set_phase_timing": [_vp, C.c_int],

@@ -165,10 +165,12 @@ class MadeModel:
             raise ValueError("parameter vector length mismatch")
         self._theta = theta.copy()
         self._version += 1
+        if self._dev is not None:  # the host copy is now the newer one: the next sync uploads it
+            self._dev.device_newer = False
 
-    def device(self) -> "DeviceReplica":
+    def device(self, device: int = 0) -> "DeviceReplica":
         if self._dev is None:
-            self._dev = DeviceReplica(self)
+            self._dev = DeviceReplica(self, device)
         self._dev.sync()
         return self._dev
 
@@ -525,8 +527,14 @@ def _mt_uniforms(streams: List[Stream], n: int, mbs: int) -> np.ndarray:
 
 def train(cfg: RunConfig, comm=None) -> RunResult:
     """vqmc::train for MADE + AUTO + ADAM or SGD + SR on a Max-Cut instance (trainer.cpp:111-322),
-    one fused device step per iteration.  `comm` (optional) = (rank, world) of an initialised
-    NCCL communicator on the model's handle; stats are then pooled by the caller."""
+    one fused device step per iteration.
+
+    `comm` (optional, one process per GPU): a ``dp.Communicator`` or a tuple (rank, world,
+    nccl_unique_id) with rank 0's ``vqmc_gpu_comm_unique_id`` shared by every rank (see
+    ``dp.make_communicator``).  This rank then plays reference workers rank*L .. rank*L + L - 1,
+    its handle joins the NCCL communicator (one all-reduce per step: the gradient and the exact
+    cut statistics), and the returned StepStats are pooled over all world*L*minibatch samples,
+    like the reference's (trainer.cpp:246-256)."""
     if cfg.problem is None:
         raise ValueError("a Max-Cut problem is required")
     if cfg.workers < 1:
@@ -541,11 +549,14 @@ def train(cfg: RunConfig, comm=None) -> RunResult:
     h = cfg.hidden if cfg.hidden > 0 else default_made_hidden(n)
     model = made_init(n, h, cfg.seed)
     lr = resolve_lr(cfg)
-    dev = model.device()
+    rank, world, uid = _comm_parts(comm)
+    dev = model.device(cfg.device)
     dev.set_problem(cfg.problem)
+    if uid is not None:
+        ub = (C.c_uint8 * 128).from_buffer_copy(bytes(uid))
+        check(K.lib.vqmc_gpu_comm_init(dev.h, ub, world, rank))
     check(K.lib.vqmc_gpu_adam_reset(dev.h))
     L, mbs = cfg.workers, cfg.minibatch
-    rank, world = comm if comm else (0, 1)
     stream0 = 1 + rank * L
     streams = [Stream(cfg.seed, stream0 + w) for w in range(L)]
     eval_stream = Stream(cfg.seed, kEvalStream)
@@ -567,6 +578,10 @@ def train(cfg: RunConfig, comm=None) -> RunResult:
                                             it + 1, C.byref(st)))
         dev.device_newer = True
         wall = time.perf_counter() - t0
+        if cfg.gradient_observer is not None:  # trainer.cpp:187-188 (worker 0, outside the timing)
+            g = np.empty(model.param_count())
+            check(K.lib.vqmc_gpu_last_gradient(dev.h, ptr(g)))
+            cfg.gradient_observer(it, g)
         result.stats.append(StepStats(st.energy_mean, math.sqrt(st.energy_var), st.grad_norm, wall))
         acc_time += wall
         if cfg.target is not None:
@@ -580,6 +595,26 @@ def train(cfg: RunConfig, comm=None) -> RunResult:
     result.total_time = time.perf_counter() - t_run
     result.made = model
     return result
+
+
+def _comm_parts(comm):
+    """(rank, world, unique_id or None) of train()'s `comm` argument."""
+    if comm is None:
+        return 0, 1, None
+    if hasattr(comm, "rank"):
+        rank, world, uid = comm.rank, comm.world, getattr(comm, "unique_id", None)
+    else:
+        if len(comm) != 3:
+            raise ValueError("comm must be (rank, world, nccl_unique_id)")
+        rank, world, uid = comm
+    rank, world = int(rank), int(world)
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("bad (rank, world)")
+    if world > 1 and uid is None:
+        raise ValueError("a multi-rank run needs the NCCL unique id of rank 0 (dp.make_communicator)")
+    if uid is not None and len(bytes(uid)) != 128:
+        raise ValueError("the NCCL unique id has 128 bytes")
+    return rank, world, uid
 
 
 def evaluate(cfg: RunConfig, model: MadeModel, eval_stream) -> tuple:  # trainer.cpp:91-108

@@ -47,6 +47,10 @@ struct AdamOut {
   float* W2cp;
   __half* W2h;  // fp16 pair of [W2m | b2], row stride hp18
   __half* W2l;
+  // sticky non-finite-logit flag of the step's sampler: when set, Adam leaves P / M / V (and the
+  // derived copies) untouched, so a failed step does not poison the parameters (the reference
+  // aborts in phase 1, before any update: trainer.cpp:170-179)
+  const uint32_t* flag;
 };
 
 __device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, float p) {

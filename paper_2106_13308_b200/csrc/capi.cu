@@ -254,6 +254,7 @@ struct DeviceGuard {
 static void check_flag(Handle* H, uint32_t v) {
   if (!v) return;
   VQMC_CUDA(cudaMemsetAsync(H->d_flag, 0, sizeof(uint32_t), H->stream));
+  H->next_call = ~0ull;  // (the device step counters are re-seeded from the caller's next call)
   throw NumericError("non-finite logit in the tail sampler (fp16 operand range exceeded)");
 }
 
@@ -270,6 +271,19 @@ static void ensure_side_stream(Handle* H) {
 
 static void check_B(int B) {
   if (B < 1) throw std::invalid_argument("batch size must be >= 1");
+}
+
+// The statistics / REINFORCE-weights kernel keeps the whole batch's weights in shared memory
+// (4 bytes per sample per CTA): the fused step and evaluate accept batches up to that limit
+// (~56K samples per GPU handle; the reference has no cap, so fail with a clear message).
+static void check_stats_batch(int B) {
+  int dev = 0, optin = 0;
+  VQMC_CUDA(cudaGetDevice(&dev));
+  VQMC_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+  const int64_t cap = (optin - 4096) / (int64_t)sizeof(float);  // (the kernel's static shared memory)
+  if ((int64_t)B > cap)
+    throw std::invalid_argument("batch of " + std::to_string(B) + " samples exceeds the per-GPU statistics limit of " +
+                                std::to_string(cap) + " (split the batch over more workers' handles or GPUs)");
 }
 
 static void upload_bits(Handle* H, const uint32_t* bits, int B) {
@@ -321,11 +335,43 @@ static void ensure_istat(Handle* H, int segs) {
   H->istat_cap = segs;
 }
 
-// one copy of the step's results (||g||^2, flag, cut statistics of `segs` segments); blocks
+// one copy of the step's results (||g||^2, flag, cut statistics of `segs` segments, and with a
+// communicator the reduced statistics limbs of all ranks); blocks
 static void read_step_results(Handle* H, int segs) {
   VQMC_CUDA(cudaMemcpyAsync(H->h_scal, H->d_scal, (16 + (size_t)3 * segs) * 8, cudaMemcpyDeviceToHost, H->stream));
+  if (H->nccl_comm)
+    VQMC_CUDA(cudaMemcpyAsync(H->h_rstat, H->G + H->L.total, rstat_count(H->nranks) * sizeof(float),
+                              cudaMemcpyDeviceToHost, H->stream));
   VQMC_CUDA(cudaStreamSynchronize(H->stream));
   check_flag(H, *reinterpret_cast<const uint32_t*>(H->h_scal + 8));
+}
+
+// Pooled cut statistics of the step: this rank's segments, or (communicator) every rank's, decoded
+// from the all-reduced limbs (sums exact; best = max over the ranks' slots).
+struct CutTotals {
+  int64_t cs = 0, cq = 0, best = 0, N = 0;
+};
+static CutTotals step_totals(const Handle* H, int segs, int B) {
+  CutTotals t;
+  if (H->nccl_comm) {
+    auto limbs = [&](int off, int cnt) {
+      uint64_t v = 0;
+      for (int k = 0; k < cnt; ++k) v += (uint64_t)llrintf(H->h_rstat[off + k]) << (16 * k);
+      return v;
+    };
+    t.cs = (int64_t)limbs(0, 3);
+    t.cq = (int64_t)limbs(3, 4);
+    for (int r = 0; r < H->nranks; ++r) t.best = std::max(t.best, (int64_t)limbs(7 + 2 * r, 2));
+    t.N = (int64_t)B * H->nranks;
+    return t;
+  }
+  for (int s = 0; s < segs; ++s) {
+    t.cs += H->h_istat[3 * s];
+    t.cq += H->h_istat[3 * s + 1];
+    t.best = std::max(t.best, H->h_istat[3 * s + 2]);
+  }
+  t.N = B;
+  return t;
 }
 
 // Pooled mean / unbiased variance of N Max-Cut local energies l = (E - 2c)/4
@@ -428,10 +474,11 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   H->degrees.assign(degrees, degrees + h);
   H->num_edges = num_edges;
   dalloc(&H->P, (size_t)H->L.total);
-  dalloc(&H->G, (size_t)H->L.total);
+  dalloc(&H->G, (size_t)H->L.total + rstat_count(kMaxRanks));
   dalloc(&H->Mo, (size_t)H->L.total);
   dalloc(&H->Vo, (size_t)H->L.total);
-  VQMC_CUDA(cudaMemsetAsync(H->G, 0, H->L.total * sizeof(float), H->stream));
+  VQMC_CUDA(cudaMemsetAsync(H->G, 0, (H->L.total + rstat_count(kMaxRanks)) * sizeof(float), H->stream));
+  VQMC_CUDA(cudaMallocHost((void**)&H->h_rstat, rstat_count(kMaxRanks) * sizeof(float)));
   VQMC_CUDA(cudaMemsetAsync(H->Mo, 0, H->L.total * sizeof(float), H->stream));
   VQMC_CUDA(cudaMemsetAsync(H->Vo, 0, H->L.total * sizeof(float), H->stream));
   dalloc(&H->gw1_part, (size_t)kGw1MaxSplits * (Hd + 1) * h);
@@ -526,6 +573,7 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (H->h_scal) cudaFreeHost(H->h_scal);
+  if (H->h_rstat) cudaFreeHost(H->h_rstat);
   for (auto& e : H->ev)
     if (e) cudaEventDestroy(e);
   for (int i = 0; i < Handle::kKtPool; ++i) {
@@ -695,7 +743,7 @@ int vqmc_gpu_adam_step(vqmc_gpu_t* g, const double* grad, double lr, double beta
   }
   launch_set_step(H, 0, t, lr, beta1, beta2, eps);
   H->next_call = ~0ull;  // the next train step must re-seed the device counters
-  launch_adam(H, 1.0f);
+  launch_adam(H, 1.0f, /*gated=*/false);
   VQMC_CUDA(cudaStreamSynchronize(H->stream));
   API_CATCH
 }
@@ -724,6 +772,7 @@ int vqmc_gpu_comm_init(vqmc_gpu_t* g, const uint8_t id[128], int nranks, int ran
   Handle* H = reinterpret_cast<Handle*>(g);
   DeviceGuard dg(H->device);
   if (nranks < 1 || rank < 0 || rank >= nranks) throw std::invalid_argument("bad nranks/rank");
+  if (nranks > kMaxRanks) throw std::invalid_argument("at most 256 ranks (exact fp32 statistics limbs)");
   H->nranks = nranks;
   H->rank = rank;
   // nranks == 1 needs no communicator; VQMC_NCCL_SELF=1 still creates one (a one-rank NCCL
@@ -749,7 +798,7 @@ namespace vqmc_b200 {
 void Handle::invalidate_graph() {
   if (gexec) cudaGraphExecDestroy(gexec);
   gexec = nullptr;
-  gkey = -1;
+  gkey = GraphKey{};
   graph_warm = false;
 }
 
@@ -780,9 +829,10 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
     H->gemm_sm_cap = std::min(H->gw2_sms, avail - 16);
     launch_gw2_umma(H, B, /*wg1_done=*/true, H->cstream);
     if (H->nccl_comm)
-      nccl_check(g_nccl.AllReduce(H->G + L.off_w2, H->G + L.off_w2, (size_t)(L.total - L.off_w2), ncclFloat32,
-                                  ncclSum, H->nccl_comm, H->cstream),
-                 "ncclAllReduce (W2, b2)");
+      nccl_check(g_nccl.AllReduce(H->G + L.off_w2, H->G + L.off_w2,
+                                  (size_t)(L.total - L.off_w2) + rstat_count(H->nranks), ncclFloat32, ncclSum,
+                                  H->nccl_comm, H->cstream),
+                 "ncclAllReduce (W2, b2, cut statistics)");
     H->gemm_sm_cap = avail - std::min(H->gw2_sms, avail - 16);
     launch_dg1_umma(H, B);  // the step's last read of the W2 operand pairs
     VQMC_CUDA(cudaEventRecord(H->ev_dg1, H->stream));
@@ -806,11 +856,12 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
     launch_backward(H, B, /*wg1_done=*/true);  // weighted_grad_log_psi (serial; per-kernel timing)
     if (tm) record_event(H, H->ev[3]);
     if (H->nccl_comm)
-      nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)L.total, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
+      nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)L.total + rstat_count(H->nranks), ncclFloat32, ncclSum,
+                                  H->nccl_comm, H->stream),
                  "ncclAllReduce");
     if (tm) record_event(H, H->ev[4]);
   }
-  launch_adam(H, 1.0f / (float)(workers * H->nranks));  // adam_step (:221)
+  launch_adam(H, 1.0f / (float)(workers * H->nranks), /*gated=*/true);  // adam_step (:221)
   if (t0) record_event(H, H->ev[5]);
 }
 
@@ -827,7 +878,11 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
   if (minibatch < 2) throw std::invalid_argument("minibatch must be >= 2");
   if (workers < 1) throw std::invalid_argument("workers must be >= 1");
   if (t < 1) throw std::invalid_argument("adam step count must be >= 1");
+  if ((int64_t)minibatch * workers > INT32_MAX) throw std::invalid_argument("batch too large");
   const int B = minibatch * workers;
+  check_stats_batch(B);
+  H->last_grad_scale = 1.0f / (float)(workers * H->nranks);
+  H->last_grad_sr = false;
   if (B > H->cap_B) H->invalidate_graph();
   H->ensure_batch(B);
   if (workers > H->istat_cap) H->invalidate_graph();
@@ -842,13 +897,19 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
     H->cur_eps = eps;
   }
   const bool graphable = H->graph_enabled && uniforms == nullptr;
-  const long long key = ((long long)minibatch << 24) ^ ((long long)workers << 4) ^ (H->ktimer ? 1 : 0) ^
-                        ((long long)H->phase_timing << 1) ^ ((long long)(seed & 0xFFFF) << 44) ^ ((long long)stream0 << 40);
+  Handle::GraphKey key;
+  key.valid = true;
+  key.minibatch = minibatch;
+  key.workers = workers;
+  key.phase_timing = H->phase_timing;
+  key.ktimer = H->ktimer;
+  key.seed = seed;
+  key.stream0 = stream0;
   if (!graphable) {
     enqueue_train_step(H, minibatch, workers, uniforms, seed, stream0);
   } else if (H->gexec && H->gkey == key) {
     VQMC_CUDA(cudaGraphLaunch(H->gexec, H->stream));  // replay the captured step
-  } else if (!H->graph_warm || H->gkey != key) {
+  } else if (!H->graph_warm || !(H->gkey == key)) {
     if (H->gexec) {
       cudaGraphExecDestroy(H->gexec);
       H->gexec = nullptr;
@@ -879,18 +940,13 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
   H->next_t = t + 1;
   if (stats_out) {
     read_step_results(H, workers);
-    int64_t cs = 0, cq = 0, best = 0;
-    for (int s = 0; s < workers; ++s) {
-      cs += H->h_istat[3 * s];
-      cq += H->h_istat[3 * s + 1];
-      best = std::max(best, H->h_istat[3 * s + 2]);
-    }
-    pooled_stats(H->num_edges, B, cs, cq, &stats_out->energy_mean, &stats_out->energy_var);
+    const CutTotals t = step_totals(H, workers, B);
+    pooled_stats(H->num_edges, t.N, t.cs, t.cq, &stats_out->energy_mean, &stats_out->energy_var);
     stats_out->grad_norm = std::sqrt(H->h_scal[0]);
-    stats_out->cut_sum = cs;
-    stats_out->cut_sq_sum = cq;
-    stats_out->best_cut = (int32_t)best;
-    stats_out->batch = B;
+    stats_out->cut_sum = t.cs;
+    stats_out->cut_sq_sum = t.cq;
+    stats_out->best_cut = (int32_t)t.best;
+    stats_out->batch = (int32_t)t.N;
   }
   API_CATCH
 }
@@ -961,7 +1017,9 @@ int vqmc_gpu_train_step_sr(vqmc_gpu_t* g, int minibatch, int workers, const doub
   if (max_iterations < 0) throw std::invalid_argument("max_iterations must be >= 0");
   if (H->nranks > 1 && H->d <= 2000)
     throw std::invalid_argument("multi-GPU SR needs the CG path (reference d > 2000)");
+  if ((int64_t)minibatch * workers > INT32_MAX) throw std::invalid_argument("batch too large");
   const int B = minibatch * workers;
+  check_stats_batch(B);
   H->ensure_batch(B);
   ensure_istat(H, workers);
   ensure_sr(H, B);
@@ -972,17 +1030,13 @@ int vqmc_gpu_train_step_sr(vqmc_gpu_t* g, int minibatch, int workers, const doub
   launch_energy(H, B);
   launch_weights_from_locals(H, B, minibatch, true);
   launch_backward(H, B, /*wg1_done=*/true);
-  int64_t cs = 0, cq = 0, best = 0;
+  // phase 2: allreduce_mean (the segments' and ranks' summed gradient / L, and the statistics limbs)
+  // and the natural-gradient solve over the pooled scores of every rank (trainer.cpp:187-199)
+  if (H->nccl_comm) comm_allreduce_sum(H, H->G, (size_t)H->L.total + rstat_count(H->nranks), false);
   read_step_results(H, workers);
-  for (int s = 0; s < workers; ++s) {
-    cs += H->h_istat[3 * s];
-    cq += H->h_istat[3 * s + 1];
-    best = std::max(best, H->h_istat[3 * s + 2]);
-  }
-  // phase 2: allreduce_mean (the segments' and ranks' summed gradient / L) and the natural-gradient
-  // solve over the pooled scores of every rank (trainer.cpp:187-199)
-  comm_allreduce_sum(H, H->G, (size_t)H->L.total, false);
+  const CutTotals tot = step_totals(H, workers, B);
   launch_sr_grad_from_G(H, 1.0 / ((double)workers * H->nranks));
+  H->last_grad_sr = true;
   int it = 0;
   double res = 0.0, gnorm = 0.0;
   const bool ok = sr_solve(H, B, lambda, tol, max_iterations, centered != 0, &it, &res, &gnorm);
@@ -996,12 +1050,12 @@ int vqmc_gpu_train_step_sr(vqmc_gpu_t* g, int minibatch, int workers, const doub
   launch_params_refresh(H);
   H->invalidate_graph();
   if (stats_out) {
-    pooled_stats(H->num_edges, B, cs, cq, &stats_out->energy_mean, &stats_out->energy_var);
+    pooled_stats(H->num_edges, tot.N, tot.cs, tot.cq, &stats_out->energy_mean, &stats_out->energy_var);
     stats_out->grad_norm = gnorm;
-    stats_out->cut_sum = cs;
-    stats_out->cut_sq_sum = cq;
-    stats_out->best_cut = (int32_t)best;
-    stats_out->batch = B;
+    stats_out->cut_sum = tot.cs;
+    stats_out->cut_sq_sum = tot.cq;
+    stats_out->best_cut = (int32_t)tot.best;
+    stats_out->batch = (int32_t)tot.N;
   }
   VQMC_CUDA(cudaStreamSynchronize(H->stream));
   API_CATCH
@@ -1017,12 +1071,41 @@ int vqmc_gpu_last_cuts(vqmc_gpu_t* g, int32_t* cuts_out, int B) {
   API_CATCH
 }
 
+int vqmc_gpu_last_samples(vqmc_gpu_t* g, uint32_t* bits_out, int B) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  if (B < 0 || B > H->cap_B) throw std::invalid_argument("B exceeds the batch capacity");
+  VQMC_CUDA(cudaMemcpyAsync(bits_out, H->X, (size_t)B * H->L.W * sizeof(uint32_t), cudaMemcpyDeviceToHost,
+                            H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  API_CATCH
+}
+
+int vqmc_gpu_last_gradient(vqmc_gpu_t* g, double* grad_out) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  if (H->last_grad_sr) {  // SGD + SR step: the reduced gradient is the CG right-hand side (fp64)
+    std::vector<double> x((size_t)H->L.total);
+    VQMC_CUDA(cudaMemcpyAsync(x.data(), H->cg_g, x.size() * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+    VQMC_CUDA(cudaStreamSynchronize(H->stream));
+    live_to_reference_d(H, x, grad_out);
+  } else {
+    auto G = download(H, H->G, H->L.total);
+    for (auto& v : G) v *= H->last_grad_scale;  // (the step keeps the sum; Adam applies 1 / L on the fly)
+    live_to_reference(H, G, nullptr, grad_out);
+  }
+  API_CATCH
+}
+
 int vqmc_gpu_evaluate(vqmc_gpu_t* g, int B, const double* uniforms, uint64_t seed, uint64_t stream,
                       uint64_t call, double out[4]) {
   API_TRY
   Handle* H = reinterpret_cast<Handle*>(g);
   DeviceGuard dg(H->device);
   if (B < 2) throw std::invalid_argument("variance needs at least two samples");
+  check_stats_batch(B);
   sample_into(H, B, 1, uniforms, seed, stream, call);
   launch_energy(H, B);
   launch_weights_from_locals(H, B, B);

@@ -44,7 +44,11 @@ constexpr double kProbEps = 1e-7;  // proj/include/vqmc/models.hpp:26
 constexpr float kLogitHi = 16.118095650958319f;
 constexpr int kMaxHidden = 1024;
 constexpr int kTailBN = 192;  // tail sampler / S p pair tile: 256 samples x 192 outputs
-constexpr int kGw1MaxSplits = 16;  // split-K of the gW1 GEMM over the batch  // head sampler register tiling limit (32 lanes x 32)
+constexpr int kGw1MaxSplits = 16;  // split-K of the gW1 GEMM over the batch
+// Exact per-rank cut statistics ride in the gradient all-reduce as fp32 16-bit limbs, stored right
+// after the live gradient (G[L.total ...]): cut sum (3), cut^2 sum (4), best cut per rank (2 each).
+constexpr int kMaxRanks = 256;  // limb sums stay < 2^24 (exact in fp32) for <= 256 ranks
+__host__ __device__ constexpr int rstat_count(int nranks) { return 7 + 2 * nranks; }
 
 // ---------------------------------------------------------------------------
 // Device-resident parameter layout ("live" layout).  One contiguous fp32
@@ -135,7 +139,8 @@ bool sr_solve(Handle* h, int B, double lambda, double tol, int max_iterations, b
               double* residual, double* gnorm_out);
 void set_error(const std::string& msg);
 int status_of(const std::exception& ex);
-void launch_adam(Handle* h, float grad_scale);  // hyper-parameters from h->d_step
+// hyper-parameters from h->d_step; gated: skip the update when the step's non-finite-logit flag is set
+void launch_adam(Handle* h, float grad_scale, bool gated);
 void launch_adam_part(Handle* h, float grad_scale, int part, cudaStream_t stream);  // 0: [W2|b2], 1: [W1T|b1]
 void launch_set_step(Handle* h, uint64_t call, int64_t t, double lr, double b1, double b2, double eps);
 
@@ -156,7 +161,10 @@ struct Handle {
 
   // model
   float* P = nullptr;      // live params [L.total]
-  float* G = nullptr;      // live grads
+  float* G = nullptr;      // live grads [L.total] + the rank statistics limbs [rstat_count(kMaxRanks)]
+  float* h_rstat = nullptr;  // pinned host copy of the reduced limbs
+  float last_grad_scale = 1.f;  // 1 / (workers * ranks) of the last train step (G holds the sum)
+  bool last_grad_sr = false;     // the last step was SGD + SR: its reduced gradient is in cg_g
   float* Mo = nullptr;     // Adam m
   float* Vo = nullptr;     // Adam v
   // fp16 pair of [W2m | b2] ([n][hp18], column h = b2, zero padding): the B operand of the tail
@@ -237,7 +245,19 @@ struct Handle {
   // per-step scalars and the captured step graph
   StepParams* d_step = nullptr;
   cudaGraphExec_t gexec = nullptr;
-  long long gkey = -1;          // (minibatch, workers, timers) the graph was captured for
+  // exact configuration the graph was captured for (seed and stream0 are baked into its kernels'
+  // arguments, so every field is compared; valid = false: no captured / warmed configuration)
+  struct GraphKey {
+    bool valid = false;
+    int minibatch = 0, workers = 0, phase_timing = 0;
+    bool ktimer = false;
+    uint64_t seed = 0, stream0 = 0;
+    bool operator==(const GraphKey& o) const {
+      return valid && o.valid && minibatch == o.minibatch && workers == o.workers && phase_timing == o.phase_timing &&
+             ktimer == o.ktimer && seed == o.seed && stream0 == o.stream0;
+    }
+  };
+  GraphKey gkey;
   bool graph_enabled = true;
   bool graph_warm = false;      // one eager step runs before the first capture
   bool capturing = false;       // inside cudaStreamBeginCapture on this handle's stream

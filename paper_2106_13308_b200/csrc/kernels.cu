@@ -1,4 +1,5 @@
-// VQMC step kernels for sm_100a (v1: SIMT fp32 GEMMs).
+// VQMC step kernels for sm_100a: energy, statistics / REINFORCE weights, the backward's elementwise
+// passes and Adam (the GEMMs are tcgen05 kernels in gemm.cu, the head sampler is head.cu).
 //
 // Reference path (arxiv/paper_2106_13308, /root/reference/proj):
 //   auto_sample            proj/src/sampler.cpp:35-59      -> head_v2_kernel (head.cu) + tail GEMM (gemm.cu)
@@ -267,7 +268,8 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
                                                              float* __restrict__ w, float* __restrict__ wscale,
                                                              int64_t* __restrict__ istat, int h, int ld,
                                                              const float* __restrict__ G1, __half* __restrict__ wgh,
-                                                             __half* __restrict__ wgl) {
+                                                             __half* __restrict__ wgl, float* __restrict__ rstat,
+                                                             int nranks, int rank) {
   extern __shared__ float sw[];  // [B] weights of the whole batch (per CTA)
   __shared__ double sd[32];
   __shared__ long long si[32], sq[32];
@@ -344,6 +346,21 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
       wmax = fmaxf(wmax, fabsf(wb));
     }
     __syncthreads();  // smean / partials are reused by the next segment
+  }
+  if (lead && tid == 0 && rstat) {
+    // this rank's exact cut statistics as 16-bit fp32 limbs riding in the gradient all-reduce (sum):
+    // [0, 3) cut sum, [3, 7) cut^2 sum, [7 + 2 r, 9 + 2 r) rank r's best cut (zero in other ranks'
+    // slots).  Every limb sum over <= 256 ranks is < 2^24: exact in fp32 (dp.stat_limbs_decode).
+    unsigned long long a = 0, q = 0, mx = 0;
+    for (int sgi = 0; sgi < segs; ++sgi) {
+      a += (unsigned long long)istat[3 * sgi];
+      q += (unsigned long long)istat[3 * sgi + 1];
+      mx = max(mx, (unsigned long long)istat[3 * sgi + 2]);
+    }
+    for (int k = 0; k < 3; ++k) rstat[k] = (float)((a >> (16 * k)) & 0xFFFFull);
+    for (int k = 0; k < 4; ++k) rstat[3 + k] = (float)((q >> (16 * k)) & 0xFFFFull);
+    for (int r = 0; r < nranks; ++r)
+      for (int k = 0; k < 2; ++k) rstat[7 + 2 * r + k] = r == rank ? (float)((mx >> (16 * k)) & 0xFFFFull) : 0.f;
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(kFull, wmax, o));
@@ -498,7 +515,8 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t lo, int64_t hi, fl
     hp.update(g, m, v, p);
   };
   // float4 groups inside [lo, hi); scalar heads / tails
-  const int64_t q_lo = (lo + 3) / 4, q_hi = hi / 4;
+  const bool skip = o.flag != nullptr && *(volatile const uint32_t*)o.flag != 0u;  // failed step: no update
+  const int64_t q_lo = (lo + 3) / 4, q_hi = skip ? q_lo : hi / 4;
   const int64_t nq = q_hi > q_lo ? q_hi - q_lo : 0;
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   G += 4 * q_lo;
@@ -556,7 +574,7 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t lo, int64_t hi, fl
   V -= t_off;
   P -= t_off;
   const int64_t e_head = nq > 0 ? 4 * q_lo : hi;  // scalar elements: [lo, 4 q_lo) and [4 q_hi, hi)
-  const int64_t n_head = e_head - lo, n_tail = nq > 0 ? hi - 4 * q_hi : 0;
+  const int64_t n_head = skip ? 0 : e_head - lo, n_tail = nq > 0 ? hi - 4 * q_hi : 0;
   for (int64_t x = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; x < n_head + n_tail; x += stride) {
     const int64_t t = x < n_head ? lo + x : 4 * q_hi + (x - n_head);
     float g = G[t], m = M[t], v = V[t], p = P[t];
@@ -749,7 +767,8 @@ void launch_weights_from_locals(Handle* H, int B, int seg, bool with_wg1) {
   KScope ks(H, with_wg1 ? "stats_weights_wg1" : "stats_weights");
   launch_k(H, stats_weights_kernel, dim3(grid), dim3(1024), smem, B / seg, seg, H->cut_chunks, H->num_edges,
            (const int32_t*)H->cpart, H->cut, H->local, H->w, H->d_wscale, H->d_istat, L.h, (int)H->hp18,
-           (const float*)(with_wg1 ? H->G1 : nullptr), H->wG1h, H->wG1l);
+           (const float*)(with_wg1 ? H->G1 : nullptr), H->wG1h, H->wG1l,
+           (float*)(with_wg1 && H->nccl_comm ? H->G + L.total : nullptr), H->nranks, H->rank);
   LAUNCH_CHECK();
   H->launches++;
 }
@@ -809,18 +828,19 @@ void launch_set_step(Handle* H, uint64_t call, int64_t t, double lr, double b1, 
   H->launches++;
 }
 
-static AdamOut adam_out(const Handle* H) {
+static AdamOut adam_out(const Handle* H, bool gated) {
   const Layout& L = H->L;
   const bool vec = (L.h % 4) == 0 && (L.off_w2 % 4) == 0;
   return AdamOut{L.h, H->hp18, L.Hd, H->head_hpk, H->head_Hdp, H->head_fast, vec, L.off_b1, L.off_w2, L.off_b2,
-                 H->d_comp_pos, H->W1Tp, H->W2cp, H->W2h, H->W2l};
+                 H->d_comp_pos, H->W1Tp, H->W2cp, H->W2h, H->W2l,
+                 gated ? H->d_flag : nullptr};
 }
 
-void launch_adam(Handle* H, float grad_scale) {  // the whole live buffer in one launch
+void launch_adam(Handle* H, float grad_scale, bool gated) {  // the whole live buffer in one launch
   KScope ks(H, "adam");
   launch_k(H, adam_kernel, dim3(H->gpart_n), dim3(256), 0, (int64_t)0, H->L.total, grad_scale,
            (const StepParams*)H->d_step, H->P, (const float*)H->G, H->Mo, H->Vo, H->d_gpart, 0, H->gpart_n, H->d_done,
-           H->d_scal, adam_out(H));
+           H->d_scal, adam_out(H, gated));
   LAUNCH_CHECK();
   H->launches++;
 }
@@ -840,7 +860,7 @@ void launch_adam_part(Handle* H, float grad_scale, int part, cudaStream_t stream
   cfg.stream = stream;
   VQMC_CUDA(cudaLaunchKernelEx(&cfg, adam_kernel, lo, hi, grad_scale, (const StepParams*)H->d_step, H->P,
                                (const float*)H->G, H->Mo, H->Vo, H->d_gpart, part == 0 ? 0 : blocks0, blocks0 + blocks1,
-                               H->d_done, H->d_scal, adam_out(H)));
+                               H->d_done, H->d_scal, adam_out(H, true)));
   LAUNCH_CHECK();
   H->launches++;
 }

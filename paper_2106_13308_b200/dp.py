@@ -70,3 +70,45 @@ def share_unique_id(uid: bytes, group=None) -> bytes:
     obj = [uid]
     dist.broadcast_object_list(obj, src=0, group=group)
     return obj[0]
+
+
+@dataclass(frozen=True)
+class Communicator:
+    """What api.train(cfg, comm) needs to put this rank's handle on the step's NCCL communicator:
+    the rank, the world size and rank 0's NCCL unique id (128 bytes)."""
+    rank: int
+    world: int
+    unique_id: bytes
+
+
+def make_communicator(rank: int, world: int, group=None) -> Communicator:
+    """Rank 0 draws the NCCL unique id (vqmc_gpu_comm_unique_id); torch.distributed (any backend,
+    already initialised) broadcasts it.  One process per GPU, as in bench.py."""
+    uid = b""
+    if rank == 0:
+        buf = (C.c_uint8 * 128)()
+        K.check(K.lib.vqmc_gpu_comm_unique_id(buf))
+        uid = bytes(buf)
+    uid = share_unique_id(uid, group)
+    if len(uid) != 128:
+        raise RuntimeError("NCCL unique id was not shared (is torch.distributed initialised?)")
+    return Communicator(rank, world, uid)
+
+
+def stat_limbs_decode(limbs) -> int:
+    """Inverse of the step's exact-integer encoding inside the fp32 gradient all-reduce: an
+    integer statistic travels as 16-bit limbs, each an exactly representable fp32 value whose
+    sum over <= 256 ranks stays below 2^24 (exact); value = sum_k limb_k * 2^(16 k)."""
+    v = 0
+    for k, x in enumerate(limbs):
+        v += int(round(float(x))) << (16 * k)
+    return v
+
+
+def stat_limbs_encode(value: int, count: int):
+    if value < 0:
+        raise ValueError("non-negative statistics only")
+    out = [float((value >> (16 * k)) & 0xFFFF) for k in range(count)]
+    if value >> (16 * count):
+        raise ValueError("statistic does not fit the limbs")
+    return out

@@ -1,0 +1,196 @@
+"""GPU parity at the benchmarked configurations (BASELINE.json configs[3-4]: N = 5,000 and
+N = 10,000, h = 363 / 424, B = 1024 per GPU) and for the reference's own dense generator at the
+headline size (G(10^4, 3/4), ~3.75e7 edges), through the C ABI against the CPU oracle.
+
+Per-step parity contract (tolerances as in tests/test_gpu_parity.py):
+* samples: bit-exact except where |u - p_ref| < 1e-5 (flips counted and written to the parity
+  log; a sample is compared only up to its first flip);
+* downstream quantities are compared on the SAME sample bits (the device's, read back with
+  vqmc_gpu_last_samples and fed to the oracle): cuts, local energies, pooled energy mean and
+  variance and evaluate's {energy, std, best_cut, mean_cut} bit-exact; the reduced gradient
+  (vqmc_gpu_last_gradient, the reference's gradient_observer value) norm-wise <= 1e-4 and
+  element-wise |g - g_ref| <= 1e-4 |g_ref| + 1e-5 ||g_ref||_inf, masked entries exactly 0; the
+  Adam update <= 1e-6 + 1e-4 |dtheta_ref| where |g_ref| > 1e-6 ||g_ref||_inf.
+References: proj/src/trainer.cpp:91-108 (evaluate), :150-282 (the step), proj/src/models.cpp:175-198
+(weighted_grad_log_psi), proj/src/hamiltonian.cpp:144-160 (the dense generator).
+"""
+import ctypes as C
+
+import numpy as np
+import pytest
+
+import pyoracle as O
+from paper_2106_13308_b200 import _capi as K
+
+from test_gpu_parity import TOL_FLIP, Dev, check_grad, check_samples
+
+pytestmark = pytest.mark.gpu
+kEval = 1_000_000_007
+
+
+def _last_samples(dev, B):
+    bits = np.empty((B, dev.W), np.uint32)
+    K.check(K.lib.vqmc_gpu_last_samples(dev.h_, K.ptr(bits), B))
+    return K.unpack_bits(bits, dev.n)
+
+
+def _last_gradient(dev):
+    g = np.empty(2 * dev.h * dev.n + dev.h + dev.n)
+    K.check(K.lib.vqmc_gpu_last_gradient(dev.h_, K.ptr(g)))
+    return g
+
+
+def _flip_count_with_gaps(xg, xo, U, p):
+    mism = xg != xo
+    gaps = []
+    for b in np.nonzero(mism.any(axis=1))[0]:
+        i = int(np.argmax(mism[b]))
+        gaps.append(float(abs(U[i, b] - p[b, i])))
+    return gaps
+
+
+@pytest.mark.parametrize("n", [5000, 10000])
+def test_fused_step_parity_headline(n, parity_log):
+    """One fused vqmc_gpu_train_step at the headline shape with the reference's mt19937 uniforms
+    (worker 0 = stream (seed, 1)) == the oracle's iteration 0 on the same sample bits."""
+    seed, B = 7, 1024
+    e = O.random_regular_graph(n, 3, seed)
+    h = O.default_made_hidden(n)
+    m0 = O.made_init(n, h, seed)
+    dev = Dev(n, h, m0.degrees, m0.theta, e, B)
+    K.check(K.lib.vqmc_gpu_adam_reset(dev.h_))
+    U = np.ascontiguousarray(O.uniforms(seed, 1, n * B).reshape(n, B))
+    st = K.StepStats()
+    K.check(K.lib.vqmc_gpu_train_step(dev.h_, B, 1, K.ptr(U), seed, 1, 0, 0.01, 0.9, 0.999, 1e-8, 1, C.byref(st)))
+    xg = _last_samples(dev, B)
+    xo, lo, po = O.auto_sample(m0, B, uniforms=U, mode=1, want_p=True)
+    flips, clean = check_samples(xg, xo, U, po)
+    parity_log.append({"test": "fused_step", "n": n, "h": h, "B": B, "rows_with_flip": flips,
+                       "bits_drawn": n * B, "gaps": _flip_count_with_gaps(xg, xo, U, po)})
+    assert clean >= 0.95 * B
+    # pooled statistics on the device's samples: bit-exact
+    le, cut = O.local_energy(n, e, xg)
+    mean, var = O.energy_and_variance(le)
+    assert st.energy_mean == mean and st.energy_var == var
+    assert st.cut_sum == int(cut.sum()) and st.best_cut == int(cut.max()) and st.batch == B
+    # reduced gradient (gradient_observer value) and the Adam update vs the oracle on the same bits
+    g_ref = O.gradient_from_locals(m0, xg, le)
+    g = _last_gradient(dev)
+    nr = check_grad(g, g_ref, m0)
+    assert st.grad_norm == pytest.approx(np.linalg.norm(g_ref), rel=1e-4)
+    ad = O.AdamState(m0.d)
+    p = m0.theta.copy()
+    O.adam_step(ad, p, g_ref)
+    got = dev.get_params()
+    sel = np.abs(g_ref) > 1e-6 * np.abs(g_ref).max()
+    d_ref, d_got = p - m0.theta, got - m0.theta
+    assert np.all(np.abs(d_got[sel] - d_ref[sel]) <= 1e-6 + 1e-4 * np.abs(d_ref[sel]))
+    zero = g_ref == 0.0
+    assert np.all(np.abs(got[zero] - m0.theta[zero]) <= 1e-7 * np.abs(m0.theta[zero]))
+    parity_log[-1].update(grad_norm_rel_err=float(nr), adam_entries_checked=int(sel.sum()))
+
+
+@pytest.mark.parametrize("n,scale", [(5000, 0.25), (10000, 0.25)])
+def test_gradient_parity_headline(n, scale, parity_log):
+    """gradient_from_locals (estimator.hpp:111-119 -> models.cpp:175-198) at N = 5k / 10k, B = 1024,
+    on the oracle's samples of a perturbed model: the dg1 split-K over K = n and gW2 over K = B."""
+    seed, B = 4, 1024
+    h = O.default_made_hidden(n)
+    m = O.made_init(n, h, seed)
+    m.theta = m.theta + (O.uniforms(seed, 98, m.d) * 2 * scale - scale)
+    e = O.random_regular_graph(n, 3, seed)
+    dev = Dev(n, h, m.degrees, m.theta, e, B)
+    xo, _ = O.auto_sample(m, B, seed=seed, stream=1, mode=1)
+    leo, _ = O.local_energy(n, e, xo)
+    g = dev.grad_from_locals(xo, leo)
+    nr = check_grad(g, O.gradient_from_locals(m, xo, leo), m)
+    parity_log.append({"test": "gradient_from_locals", "n": n, "B": B, "perturbation": scale,
+                       "grad_norm_rel_err": float(nr)})
+
+
+@pytest.mark.parametrize("n,B", [(20, 1024), (1000, 1024), (10000, 1024)])
+def test_evaluate_parity(n, B, parity_log):
+    """evaluate (trainer.cpp:91-108): eval batch from the eval stream (seed, 1e9+7); {energy, std,
+    best_cut = max(0, cuts), mean_cut} bit-exact vs the oracle's evaluate on the same bits."""
+    seed = 3
+    e = O.random_maxcut_graph(n, seed) if n <= 1000 else O.random_regular_graph(n, 3, seed)
+    h = O.default_made_hidden(n)
+    m = O.made_init(n, h, seed)
+    m.theta = m.theta + (O.uniforms(seed, 98, m.d) * 0.5 - 0.25)
+    dev = Dev(n, h, m.degrees, m.theta, e, B)
+    U = np.ascontiguousarray(O.uniforms(seed, kEval, n * B).reshape(n, B))
+    out = np.empty(4)
+    K.check(K.lib.vqmc_gpu_evaluate(dev.h_, B, K.ptr(U), 0, 0, 0, K.ptr(out)))
+    xg = _last_samples(dev, B)
+    xo, lo, po = O.auto_sample(m, B, uniforms=U, mode=1, want_p=True)
+    flips, clean = check_samples(xg, xo, U, po)
+    parity_log.append({"test": "evaluate", "n": n, "B": B, "rows_with_flip": flips, "bits_drawn": n * B,
+                       "gaps": _flip_count_with_gaps(xg, xo, U, po)})
+    assert clean >= 0.95 * B
+    ref = O.evaluate(m, e, B, uniforms=U, mode=1)  # the oracle's own draw
+    if flips == 0:
+        assert np.array_equal(out, ref), (out, ref)
+    # on the device's bits (identical to ref when there is no flip)
+    le, cut = O.local_energy(n, e, xg)
+    mean, var = O.energy_and_variance(le)
+    assert out[0] == mean and out[1] == np.sqrt(var)
+    assert out[2] == max(0.0, cut.max()) and out[3] == cut.sum() / B
+
+
+def test_energy_bit_exact_dense_headline(parity_log):
+    """The reference generator's dense instance at the headline size, G(10^4, 3/4) (|E| ~ 3.75e7,
+    hamiltonian.cpp:144-160): cuts and local energies bit-exact on random and sampled spins."""
+    n, B = 10000, 96
+    e = O.random_maxcut_graph(n, 0)
+    assert len(e) == 37498967  # probed |E| of the reference generator at seed 0
+    h = O.default_made_hidden(n)
+    m = O.made_init(n, h, 0)
+    dev = Dev(n, h, m.degrees, m.theta, e, B)
+    rng = np.random.default_rng(11)
+    x = rng.integers(0, 2, (B, n)).astype(np.uint8)
+    x[0] = 0
+    x[1] = 1
+    x[2, : n // 2] = 1  # (a balanced cut)
+    cut, le = dev.energy(x)
+    leo, cuto = O.local_energy(n, e, x)
+    assert cut[0] == 0 and cut[1] == 0
+    assert np.array_equal(le, leo) and np.array_equal(cut.astype(float), cuto)
+    parity_log.append({"test": "energy_dense_g_n_3_4", "n": n, "edges": int(len(e)), "B": B, "bit_exact": True})
+
+
+def test_energy_bit_exact_regular_headline_large_batch():
+    """N = 10k 3-regular, a batch of 4096 random spin rows (every 32-sample energy group and the
+    per-edge-chunk partial counts): bit-exact."""
+    n, B = 10000, 4096
+    e = O.random_regular_graph(n, 3, 2)
+    h = O.default_made_hidden(n)
+    m = O.made_init(n, h, 2)
+    dev = Dev(n, h, m.degrees, m.theta, e, B)
+    x = np.random.default_rng(5).integers(0, 2, (B, n)).astype(np.uint8)
+    cut, le = dev.energy(x)
+    leo, cuto = O.local_energy(n, e, x)
+    assert np.array_equal(le, leo) and np.array_equal(cut.astype(float), cuto)
+
+
+def test_train_step_numeric_error_leaves_parameters_unchanged():
+    """A step whose fp16-pair logits overflow raises NumericError (the reference's runtime_error)
+    and Adam skips the update, so the handle's parameters are unchanged (trainer.cpp:170-179
+    aborts before any update)."""
+    n, B = 300, 256
+    h = O.default_made_hidden(n)
+    m = O.made_init(n, h, 1)
+    # a huge W2 entry: |w| far above fp16's range in the tail GEMM operand
+    th = m.theta.copy()
+    W2 = th[h * n + h: h * n + h + n * h].reshape(n, h)
+    W2[n - 1, :] = 1e6
+    e = O.random_regular_graph(n, 3, 1)
+    dev = Dev(n, h, m.degrees, th, e, B)
+    p0 = dev.get_params()
+    st = K.StepStats()
+    with pytest.raises(K.VqmcError):
+        K.check(K.lib.vqmc_gpu_train_step(dev.h_, B, 1, None, 1, 1, 0, 0.01, 0.9, 0.999, 1e-8, 1, C.byref(st)))
+    assert np.array_equal(dev.get_params(), p0)
+    # the handle recovers once the parameters are sane again
+    dev.set_params(m.theta)
+    K.check(K.lib.vqmc_gpu_train_step(dev.h_, B, 1, None, 1, 1, 1, 0.01, 0.9, 0.999, 1e-8, 1, C.byref(st)))
+    assert np.isfinite(st.energy_mean) and np.isfinite(st.grad_norm)
