@@ -414,6 +414,7 @@ static void upload_edges(Handle* H, const int32_t* edges, int64_t num_edges) {
     VQMC_CUDA(cudaMemset(H->d_edges, 0, (num_edges + 2) * sizeof(int2)));
     VQMC_CUDA(cudaMemcpy(H->d_edges, edges, num_edges * sizeof(int2), cudaMemcpyHostToDevice));
   }
+  setup_dense_energy(H);  // dense instances (e.g. the reference's G(n, 3/4)): the tensor-core quadratic form
 }
 
 }  // namespace vqmc_b200
@@ -565,6 +566,7 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   if (H->ev_join) cudaEventDestroy(H->ev_join);
   if (H->ev_dg1) cudaEventDestroy(H->ev_dg1);
   free_sr(H);
+  free_dense_energy(H);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2h, H->W2l, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
                   H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->cpart, H->local, H->w, H->d_wscale,

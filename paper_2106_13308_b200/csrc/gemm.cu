@@ -52,13 +52,16 @@ static EncodeTiledFn encode_fn() {
 
 static CUtensorMapDataType tmap_dtype(int ek) {
   return ek == kElemTF32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32
-                         : (ek == kElemBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16 : CU_TENSOR_MAP_DATA_TYPE_FLOAT16);
+                         : ek == kElemBF16 ? CU_TENSOR_MAP_DATA_TYPE_BFLOAT16
+                         : ek == kElemU8   ? CU_TENSOR_MAP_DATA_TYPE_UINT8
+                                           : CU_TENSOR_MAP_DATA_TYPE_FLOAT16;
 }
+static int tmap_esize(int ek) { return ek == kElemTF32 ? 4 : ek == kElemU8 ? 1 : 2; }
 
 // K-major operand: element (mn, k) at ptr[mn * ld + k]; box {128 bytes of K, box_mn}.
 CUtensorMap tmap_kmajor(const void* ptr, int64_t K, int64_t MN, int64_t ld, int box_mn, int ek = kElemTF32) {
   CUtensorMap m;
-  const int es = ek ? 2 : 4;
+  const int es = tmap_esize(ek);
   const cuuint64_t dims[2] = {(cuuint64_t)K, (cuuint64_t)MN};
   const cuuint64_t strides[1] = {(cuuint64_t)ld * es};
   const cuuint32_t box[2] = {(cuuint32_t)(128 / es), (cuuint32_t)box_mn};

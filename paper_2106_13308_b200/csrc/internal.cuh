@@ -3,6 +3,7 @@
 
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -102,6 +103,10 @@ struct KScope {
   ~KScope();
 };
 
+// TMA descriptors (gemm.cu): K-major operand, element (mn, k) at ptr[mn * ld + k], box {128 bytes
+// of K, box_mn}, SWIZZLE_128B; ek = umma_gemm.cuh element kind (kElemU8 for 8-bit operands).
+CUtensorMap tmap_kmajor(const void* ptr, int64_t K, int64_t MN, int64_t ld, int box_mn, int ek);
+
 // Kernel launchers (kernels.cu).  All enqueue on h->stream.
 void launch_params_refresh(Handle* h);
 // cudaFuncSetAttribute(MaxDynamicSharedMemorySize) for `kern` on the current device, once per
@@ -115,6 +120,11 @@ void launch_z2(Handle* h, int B, int col0, const double* d_uniforms, RngSpec rng
                bool given_bits, double* d_cond, bool want_lp = true);
 void launch_finalize_logpsi(Handle* h, int B, int n_tiles);
 void launch_energy(Handle* h, int B);
+// dense-graph energy (energy_dense.cu)
+bool dense_energy_preferred(int n, int64_t num_edges);
+void setup_dense_energy(Handle* h);  // after the edge list is uploaded
+void free_dense_energy(Handle* h);
+void launch_energy_dense(Handle* h, int B);
 void launch_weights_from_locals(Handle* h, int B, int seg, bool with_wg1 = false);
 void launch_cuts_reduce(Handle* h, int B);
 void launch_backward(Handle* h, int B, bool wg1_done = false);
@@ -186,6 +196,13 @@ struct Handle {
   int32_t* d_comp_k = nullptr;    // hidden units sorted by degree
   int32_t* d_comp_off = nullptr;  // [Hd + 1]: units with degree i+1 at [off[i], off[i+1])
   int2* d_edges = nullptr;
+  // dense-graph energy (energy_dense.cu): fp8 strictly-upper adjacency [n][32 W], node degrees, and
+  // the fp8 expansion of the batch's spins [B][32 W]
+  bool dense_energy = false;
+  uint8_t* Uf8 = nullptr;
+  uint8_t* Xf8 = nullptr;
+  int32_t* d_degn = nullptr;
+  int64_t xf8_cap = 0;
 
   // batch buffers (capacity cap_B)
   int cap_B = 0;

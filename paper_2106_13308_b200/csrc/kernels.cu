@@ -707,6 +707,10 @@ void launch_finalize_logpsi(Handle* H, int B, int tiles) {
 }
 
 void launch_energy(Handle* H, int B) {
+  if (H->dense_energy) {  // tensor-core quadratic form (energy_dense.cu)
+    launch_energy_dense(H, B);
+    return;
+  }
   const int W = H->L.W;
   const size_t tsm = (size_t)((64 * W + 3) & ~3) * sizeof(uint32_t);  // T + S
   const size_t cap = 200 * 1024;
@@ -866,3 +870,66 @@ void launch_adam_part(Handle* H, float grad_scale, int part, cudaStream_t stream
 }
 
 }  // namespace vqmc_b200
+
+// ===========================================================================
+// Energy-kernel throughput hook (bench / profiles): cut values of B device-resident random spin
+// rows through the production launcher (edge-list or dense path, as the handle dispatches), timed
+// with CUDA events on the handle's stream over `iters` launches after one warm-up.  The batch
+// lives in its own buffer (the handle's batch buffers are not grown to B).
+// ===========================================================================
+namespace vqmc_b200 {
+__global__ void random_bits_kernel(int64_t words, int n, int W, uint64_t seed, uint32_t* __restrict__ X) {
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < words; t += (int64_t)gridDim.x * blockDim.x) {
+    uint64_t z = seed + (uint64_t)t * 0x9E3779B97F4A7C15ull;
+    z = (z ^ (z >> 30)) * 0xBF58476D1CE4E5B9ull;
+    z = (z ^ (z >> 27)) * 0x94D049BB133111EBull;
+    z ^= z >> 31;
+    const int w = (int)(t % W);
+    const int valid = n - 32 * w;  // bits of this word inside the row
+    uint32_t v = (uint32_t)z;
+    if (valid < 32) v &= (1u << valid) - 1u;
+    X[t] = v;
+  }
+}
+}  // namespace vqmc_b200
+
+extern "C" int vqmc_test_energy_rate(vqmc_gpu_t* g, int B, int iters, float* ms_per_launch, int* chunks_out) {
+  using namespace vqmc_b200;
+  Handle* H = reinterpret_cast<Handle*>(g);
+  uint32_t* X = nullptr;
+  uint32_t* saved = H->X;
+  int saved_cap = H->cap_B;
+  try {
+    const int64_t words = (int64_t)B * H->L.W;
+    VQMC_CUDA(cudaMalloc((void**)&X, words * sizeof(uint32_t)));
+    random_bits_kernel<<<148 * 8, 256, 0, H->stream>>>(words, H->L.n, H->L.W, 12345, X);
+    VQMC_CUDA(cudaGetLastError());
+    H->invalidate_graph();
+    H->X = X;
+    H->cap_B = std::max(H->cap_B, B);  // (only the energy path runs against this buffer)
+    cudaEvent_t e0, e1;
+    VQMC_CUDA(cudaEventCreate(&e0));
+    VQMC_CUDA(cudaEventCreate(&e1));
+    launch_energy(H, B);  // warm-up (sizes cpart)
+    VQMC_CUDA(cudaEventRecord(e0, H->stream));
+    for (int i = 0; i < iters; ++i) launch_energy(H, B);
+    VQMC_CUDA(cudaEventRecord(e1, H->stream));
+    VQMC_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    VQMC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_launch = ms / std::max(1, iters);
+    *chunks_out = H->cut_chunks;
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+  } catch (const std::exception& ex) {
+    H->X = saved;
+    H->cap_B = saved_cap;
+    if (X) cudaFree(X);
+    set_error(ex.what());
+    return status_of(ex);
+  }
+  H->X = saved;
+  H->cap_B = saved_cap;
+  cudaFree(X);
+  return VQMC_OK;
+}

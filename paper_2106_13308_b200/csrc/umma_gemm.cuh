@@ -32,7 +32,7 @@ constexpr int kUmmaBK = 32;  // fp32 elements per 128-byte row (bf16: 64)
 
 // Operand element kind EK: 0 = tf32 pairs (3 x kind::tf32, MMA K = 8); 1 = bf16 pairs, 2 = fp16
 // pairs (3 x kind::f16, MMA K = 16).
-enum : int { kElemTF32 = 0, kElemBF16 = 1, kElemF16 = 2 };
+enum : int { kElemTF32 = 0, kElemBF16 = 1, kElemF16 = 2, kElemU8 = 3 /* 8-bit (fp8 / int8) single operands */ };
 template <int EK>
 struct UmmaElem {
   static constexpr int kBytes = EK ? 2 : 4;
