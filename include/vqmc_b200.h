@@ -66,7 +66,8 @@ int vqmc_gpu_device_count(int* count);
  * hamiltonian.hpp:78-84; maxcut_spec hamiltonian.cpp:109-119 incl. validate :36-54).
  * degrees: h entries in [1, n-1] (models.cpp:91 for made_init, or a checkpoint's).
  * edges: num_edges pairs (i, j), 0-based, i < j, no duplicates.
- * max_batch: initial batch capacity (buffers grow on demand outside the step). */
+ * max_batch: initial batch capacity (buffers grow on demand outside the step).  Every call takes
+ * at most 49152 samples (B = minibatch * workers); larger batches return VQMC_ERR_INVALID. */
 int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const double* theta,
                     const int32_t* edges, int64_t num_edges, int max_batch, vqmc_gpu_t** out);
 int vqmc_gpu_destroy(vqmc_gpu_t* g);

@@ -90,6 +90,10 @@ static void dalloc(T** p, size_t count) {
 
 void Handle::ensure_batch(int B) {
   if (B <= cap_B) return;
+  // stats_weights_kernel keeps the whole batch's weights in one CTA's shared memory
+  if (B > kMaxBatch)
+    throw std::invalid_argument("batch of " + std::to_string(B) + " samples exceeds the per-call maximum of " +
+                                std::to_string(kMaxBatch) + " (split it over calls or GPUs)");
   invalidate_graph();
   const int n = L.n, h = L.h;
   const int max_tiles = 4 * ((n + 127) / 128 + 2);  // up to 4 epilogue partials per tail tile

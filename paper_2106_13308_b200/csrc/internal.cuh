@@ -44,6 +44,7 @@ constexpr double kProbEps = 1e-7;  // proj/include/vqmc/models.hpp:26
 // logit(1 - 1e-7) = ln((1 - 1e-7) / 1e-7): p_raw >= 1 - eps  <=>  z >= kLogitHi.
 constexpr float kLogitHi = 16.118095650958319f;
 constexpr int kMaxHidden = 1024;
+constexpr int kMaxBatch = 49152;  // samples per call: stats_weights_kernel holds B fp32 weights in one CTA's smem
 constexpr int kTailBN = 192;  // tail sampler / S p pair tile: 256 samples x 192 outputs
 constexpr int kGw1MaxSplits = 16;  // split-K of the gW1 GEMM over the batch
 // Exact per-rank cut statistics ride in the gradient all-reduce as fp32 16-bit limbs, stored right

@@ -217,7 +217,7 @@ def test_train_step_numeric_error_leaves_parameters_unchanged():
 
 
 @pytest.mark.parametrize("n,B,kind", [(40, 33, "maxcut"), (300, 300, "maxcut"), (1000, 1000, "maxcut"),
-                                      (2100, 257, "maxcut"), (777, 64, "regular")])
+                                      (2100, 257, "maxcut"), (778, 64, "regular")])
 def test_dense_energy_path_matches_edge_list(n, B, kind, monkeypatch):
     """The fp8 tensor-core quadratic form (energy_dense.cu, forced with VQMC_ENERGY=dense) and the
     bit-sliced edge-list kernel (VQMC_ENERGY=edges) give the oracle's cuts bit-exactly, incl. ragged

@@ -1,8 +1,8 @@
 // vqmc — command-line drop-in for the reference's `vqmc` tool (proj/tools/vqmc.cpp) on the
 // B200 path.  Same subcommands, flags, config-file precedence, output files and exit codes
 // (0 ok, 1 usage, 2 numerical, 3 sample-test reject; vqmc.cpp:35-37) for the north-star
-// workload (Max-Cut, MADE, AUTO sampler, ADAM).  Configurations outside that path (TIM
-// instances, RBM/MCMC, SGD/SR) are rejected as usage errors with an explicit message.
+// workload (Max-Cut, MADE, AUTO sampler, ADAM or SGD + SR).  Configurations outside that path
+// (TIM instances, RBM/MCMC) are rejected as usage errors with an explicit message.
 //
 // CLI11 and nlohmann/json are not available in this image; the parser below implements the
 // subset of CLI11 behaviour the reference relies on: `--flag value` and `--flag=value`,
