@@ -408,10 +408,76 @@ static void validate_edges(int n, const int32_t* edges, int64_t num_edges) {
   if (std::adjacent_find(keys.begin(), keys.end()) != keys.end()) throw std::invalid_argument("duplicate pair");
 }
 
+// Edge list for the bit-sliced cut kernel: entries u | v << 16 (n <= 65536; swizzled indices, see
+// maxcut_cut_kernel) grouped into aligned batches of 32 in which the u's are pairwise distinct
+// mod 32 and so are the v's (orientation is
+// free: the cut term is symmetric), so a warp's two shared-memory lookups per edge hit 32 distinct
+// banks.  Greedy first fit over a window of open batches; unfilled slots point at two of the kernel's
+// 32 zero words (one per bank) on banks still free (XOR = 0: no contribution).  The order of the integer sum
+// does not matter (exact).
+static std::vector<uint32_t> bank_order_edges(int W, const int32_t* edges, int64_t num_edges) {
+  struct Batch {
+    uint32_t lu = 0, lv = 0;
+    uint32_t e[32];
+    int cnt = 0;
+  };
+  std::vector<Batch> batches;
+  std::vector<int> open;  // indices of batches that are not full (window)
+  constexpr size_t kWindow = 48;
+  for (int64_t t = 0; t < num_edges; ++t) {
+    // swizzled word indices of the cut kernel's transposed spins: node i at i ^ ((i >> 5) & 31)
+    const uint32_t u0 = (uint32_t)edges[2 * t], v0 = (uint32_t)edges[2 * t + 1];
+    const uint32_t u = u0 ^ ((u0 >> 5) & 31u), v = v0 ^ ((v0 >> 5) & 31u);
+    const uint32_t bu = 1u << (u & 31), bv = 1u << (v & 31);
+    bool placed = false;
+    for (size_t k = open.size(); k-- > 0 && !placed;) {
+      Batch& b = batches[open[k]];
+      if (!(b.lu & bu) && !(b.lv & bv)) {
+        b.lu |= bu, b.lv |= bv, b.e[b.cnt++] = u | v << 16;
+        placed = true;
+      } else if (!(b.lu & bv) && !(b.lv & bu)) {
+        b.lu |= bv, b.lv |= bu, b.e[b.cnt++] = v | u << 16;
+        placed = true;
+      }
+      if (placed && b.cnt == 32) open.erase(open.begin() + (long)k);
+    }
+    if (!placed) {
+      batches.emplace_back();
+      Batch& b = batches.back();
+      b.lu = bu, b.lv = bv, b.e[b.cnt++] = u | v << 16;
+      open.push_back((int)batches.size() - 1);
+      if (open.size() > kWindow) open.erase(open.begin());  // oldest leaves the window (padded later)
+    }
+  }
+  std::vector<uint32_t> out;
+  out.reserve(batches.size() * 32 + 32);
+  const uint32_t zero = 32u * (uint32_t)W;  // 32 zero words after the transposed spins (kernel)
+  for (Batch& b : batches) {
+    for (int k = b.cnt; k < 32; ++k) {  // pad: a zero word on a free bank on each side (XOR = 0)
+      const uint32_t pu = (uint32_t)__builtin_ctz(~b.lu), pv = (uint32_t)__builtin_ctz(~b.lv);
+      b.lu |= 1u << pu, b.lv |= 1u << pv;
+      b.e[k] = (zero + pu) | (zero + pv) << 16;
+    }
+    out.insert(out.end(), b.e, b.e + 32);
+  }
+  if (out.empty())  // no edges: one batch of zero pairs
+    for (uint32_t k = 0; k < 32; ++k) out.push_back((zero + k) | (zero + k) << 16);
+  return out;
+}
+
 static void upload_edges(Handle* H, const int32_t* edges, int64_t num_edges) {
   if (H->d_edges) VQMC_CUDA(cudaFree(H->d_edges));
   H->d_edges = nullptr;
+  if (H->d_edges_bank) VQMC_CUDA(cudaFree(H->d_edges_bank));
+  H->d_edges_bank = nullptr;
+  H->num_edges_bank = 0;
   H->num_edges = num_edges;
+  if (32 * H->L.W + 32 <= 65536 && !dense_energy_preferred(H->L.n, num_edges)) {
+    const std::vector<uint32_t> pk = bank_order_edges(H->L.W, edges, num_edges);
+    VQMC_CUDA(cudaMalloc((void**)&H->d_edges_bank, pk.size() * sizeof(uint32_t)));
+    VQMC_CUDA(cudaMemcpy(H->d_edges_bank, pk.data(), pk.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));
+    H->num_edges_bank = (int64_t)pk.size();
+  }
   if (num_edges > 0) {
     // (+2 entries: the energy kernel's bulk copies round a chunk up to an even edge count)
     VQMC_CUDA(cudaMalloc((void**)&H->d_edges, (num_edges + 2) * sizeof(int2)));
@@ -571,6 +637,7 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   if (H->ev_dg1) cudaEventDestroy(H->ev_dg1);
   free_sr(H);
   free_dense_energy(H);
+  if (H->d_edges_bank) cudaFree(H->d_edges_bank);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2h, H->W2l, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
                   H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->cpart, H->local, H->w, H->d_wscale,

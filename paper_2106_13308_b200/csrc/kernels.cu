@@ -150,105 +150,176 @@ __global__ void __launch_bounds__(256) energy_kernel(int B, int W, int64_t nE,
 }
 
 // ===========================================================================
-// Max-Cut cuts, bit-sliced over samples (the default path).  A CTA takes 32 samples and a
-// chunk of the edge list.  It transposes the samples' packed spins in shared memory so that
-// T[i] holds node i of all 32 samples (bit s = x_{s,i}); an edge then costs one XOR of two
-// words, a 32-sample mask of "cut" bits, added into 8 bit-sliced counter planes (a ripple
-// carry over the planes: <= 255 edges per thread).  Per-sample counts come back with one
-// 32 x 32 bit transpose per plane and popc; CTAs add them to cut[] with integer atomics
-// (exact and order-independent).  hamiltonian.cpp:61-69,121-124 with beta_ij = -1/4.
+// Max-Cut cuts, bit-sliced over samples (the default path; maxcut_cut_kernel below).
 // ===========================================================================
-__device__ __forceinline__ uint32_t transpose32_lane(uint32_t v, int lane) {
-  // lane r holds row r (bit c = M[r][c]); returns column `lane` (bit r = M[r][lane])
+// 32x32 bit transpose across a warp with one funnel rotation + one LOP3 per stage (the bits
+// that wrap around are masked away): lane r holds row r; returns column `lane`.
+__device__ __forceinline__ uint32_t transpose32_rot(uint32_t v, int lane) {
+  const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
+#pragma unroll
+  for (int t = 0; t < 5; ++t) {
+    const int j = 16 >> t;
+    const bool hi = (lane & j) != 0;
+    const uint32_t keep = hi ? ~masks[t] : masks[t];  // this lane's own bits
+    const uint32_t o = __shfl_xor_sync(kFull, v, j);
+    const uint32_t r = __funnelshift_l(o, o, hi ? 32 - j : j);  // rotl(o, j) or rotr(o, j)
+    v = (v & keep) | (r & ~keep);
+  }
+  return v;
+}
+
+// 32 x 32 bit transpose of v[r] (row r, bit c = M[r][c]) in registers: afterwards v[c] bit r =
+// M[r][c].  Five delta-swap stages of 16 register pairs.
+__device__ __forceinline__ void transpose32_regs(uint32_t (&v)[32]) {
   const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
 #pragma unroll
   for (int t = 0; t < 5; ++t) {
     const int j = 16 >> t;
     const uint32_t m = masks[t];
-    const uint32_t o = __shfl_xor_sync(kFull, v, j);
-    v = (lane & j) ? ((v & ~m) | ((o & ~m) >> j)) : ((v & m) | ((o & m) << j));
+#pragma unroll
+    for (int r = 0; r < 32; ++r) {
+      if (r & j) continue;
+      // swap the high-j bits of v[r] (columns >= j within each 2j block) with the low bits of v[r + j]
+      const uint32_t x = ((v[r] >> j) ^ v[r + j]) & m;
+      v[r + j] ^= x;
+      v[r] ^= x << j;
+    }
   }
-  return v;
 }
 
-// Shared memory: T [32 W] transposed words | S [32 W] staged rows | E [per_chunk + 1] edges.
-// The rows and the edge chunk arrive by bulk copies (TMA) on two mbarriers; the transpose
-// overlaps the edge copy.
-__global__ void __launch_bounds__(256) maxcut_cut_kernel(int B, int n, int W, int64_t nE, int64_t per_chunk,
-                                                         const int2* __restrict__ edges,
-                                                         const uint32_t* __restrict__ X, int32_t* __restrict__ cpart) {
+// Carry-save adder: (hi, lo) = a + b + c bitwise (two LOP3s).
+__device__ __forceinline__ void csa(uint32_t& hi, uint32_t& lo, uint32_t a, uint32_t b, uint32_t c) {
+  const uint32_t u = a ^ b;
+  hi = (a & b) | (u & c);
+  lo = u ^ c;
+}
+
+// Max-Cut cut counts over bit-sliced samples (local_energy_batch's diagonal branch,
+// estimator.hpp:53-57; diagonal_energy hamiltonian.cpp:61-69; cut_value :121-124).
+//
+// Edges arrive bank-ordered and packed (upload_edges): entry e = u | v << 16, and every aligned
+// batch of 32 entries has pairwise-distinct u mod 32 and pairwise-distinct v mod 32, so the two
+// shared-memory lookups T[u], T[v] of a warp are conflict-free.  A CTA keeps its edge chunk
+// resident in shared memory and walks sample groups g = blockIdx.y, += gridDim.y (32 samples per
+// group): the group's packed rows arrive by one bulk copy into T, every thread reads one word
+// column into registers, and after a barrier writes it back transposed (in place: T[swz(node)] =
+// that node's spin in all 32 samples).  One XOR per edge gives the 32-sample cut mask, and
+// Harley-Seal carry-save counters (ones, twos, fours, eights + a ripple counter of sixteens) sum
+// them at ~2 logic ops per edge (<= 63 entries per thread: 6 planes).  The planes are transposed back (lane s <- sample s)
+// and popcounted.  Shared memory stays <= ~110 KB so two CTAs share an SM (one's copy and
+// transpose overlap the other's edge pass).  Per-chunk counts are exact integers, summed in a
+// fixed order by the statistics kernel.   Shared memory: T [32 W] | zero [32] | E [chunk entries].
+constexpr int kCutThreads = 512;
+__global__ void __launch_bounds__(kCutThreads, 2) maxcut_cut_kernel(int B, int W, int64_t nEp, int64_t per_chunk,
+                                                                    const uint32_t* __restrict__ edges,
+                                                                    const uint32_t* __restrict__ X,
+                                                                    int32_t* __restrict__ cpart) {
   extern __shared__ __align__(16) uint32_t smem_words[];
-  uint32_t* T = smem_words;               // [32 W]: node-major words of the CTA's 32 samples
-  uint32_t* S = smem_words + 32 * W;      // [32][W]: the samples' packed rows (staging)
-  int2* E = reinterpret_cast<int2*>(smem_words + ((64 * W + 3) & ~3));  // the edge chunk
+  const int TW = 32 * W + 32;  // transposed spins + 32 zero words (the padding entries' targets)
+  uint32_t* T = smem_words;
+  uint32_t* E = smem_words + TW;
   __shared__ int scnt[32];
   __shared__ __align__(8) uint64_t bar[2];
-  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarps = blockDim.x >> 5;
-  const int s0 = 32 * blockIdx.y;
-  const int rows = min(32, B - s0);
-  const int64_t e0 = (int64_t)blockIdx.x * per_chunk, e1 = min(nE, e0 + per_chunk);
-  const int ne = (int)(e1 - e0);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  constexpr int nwarps = kCutThreads / 32;
+  const int groups = (B + 31) / 32;
+  const int64_t e0 = (int64_t)blockIdx.x * per_chunk, e1 = min(nEp, e0 + per_chunk);
+  const int ne = (int)(e1 - e0);  // multiple of 32
   ptx::pdl_trigger();
   ptx::pdl_wait();
-  if (threadIdx.x == 0) {
-    ptx::mbar_init(&bar[0], 1);
-    ptx::mbar_init(&bar[1], 1);
+  if (tid == 0) {
+    for (int k = 0; k < 2; ++k) ptx::mbar_init(&bar[k], 1);
     ptx::fence_mbar_init();
   }
-  if (threadIdx.x < 32) scnt[threadIdx.x] = 0;
-  __syncthreads();
-  const bool bulk_rows = rows == 32;  // whole group: 128 W bytes, 16-byte aligned
-  if (threadIdx.x == 0) {
-    if (bulk_rows) {
-      ptx::mbar_expect_tx(&bar[0], 128u * (uint32_t)W);
-      ptx::bulk_g2s(S, X + (size_t)s0 * W, 128u * (uint32_t)W, &bar[0]);
-    }
-    if (ne > 0) {
-      const uint32_t eb = (uint32_t)((ne + 1) & ~1) * 8u;  // even count: 16-byte multiple (array padded)
-      ptx::mbar_expect_tx(&bar[1], eb);
-      ptx::bulk_g2s(E, edges + e0, eb, &bar[1]);
-    }
+  if (tid < 32) {
+    scnt[tid] = 0;
+    T[32 * W + tid] = 0u;
   }
-  if (!bulk_rows) {  // ragged last group
-    for (int t = threadIdx.x; t < 32 * W; t += blockDim.x) S[t] = t < rows * W ? X[(size_t)s0 * W + t] : 0u;
+  __syncthreads();
+  if (tid == 0 && ne > 0) {
+    ptx::mbar_expect_tx(&bar[1], 4u * (uint32_t)ne);
+    ptx::bulk_g2s(E, edges + e0, 4u * (uint32_t)ne, &bar[1]);
+  }
+  bool edges_ready = false;
+  int it = 0;
+  for (int g = blockIdx.y; g < groups; g += gridDim.y, ++it) {
+    const int s0 = 32 * g, rows = min(32, B - s0);
+    if (rows == 32) {
+      if (tid == 0) {
+        ptx::mbar_expect_tx(&bar[0], 128u * (uint32_t)W);
+        ptx::bulk_g2s(T, X + (size_t)s0 * W, 128u * (uint32_t)W, &bar[0]);
+      }
+      ptx::mbar_wait(&bar[0], it & 1);
+    } else {  // ragged last group
+      for (int t = tid; t < 32 * W; t += kCutThreads) T[t] = t < rows * W ? X[(size_t)s0 * W + t] : 0u;
+      __syncthreads();
+    }
+    // in-place transpose, one 32 x 32 bit block per thread in registers (thread w takes word column w:
+    // 32 conflict-free loads, 5 delta-swap stages, 32 stores).  T is swizzled so that those stores
+    // are conflict-free: node i lives at word swz(i) = i ^ ((i >> 5) & 31); the edge entries carry
+    // swizzled indices (upload_edges).
+    uint32_t v[32];
+    const int w = tid;
+    if (w < W) {
+#pragma unroll
+      for (int r = 0; r < 32; ++r) v[r] = T[r * W + w];
+    }
     __syncthreads();
-  } else {
-    ptx::mbar_wait(&bar[0], 0);
-  }
-  // (row stride W: odd W reads conflict-free columns); four independent transposes per iteration
-  int w = warp;
-  for (; w + 3 * nwarps < W; w += 4 * nwarps) {
-    uint32_t v[4];
+    if (w < W) {
+      transpose32_regs(v);
 #pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = S[lane * W + w + u * nwarps];
-#pragma unroll
-    for (int u = 0; u < 4; ++u) v[u] = transpose32_lane(v[u], lane);
-#pragma unroll
-    for (int u = 0; u < 4; ++u) T[32 * (w + u * nwarps) + lane] = v[u];  // node 32 w' + lane
-  }
-  for (; w < W; w += nwarps) T[32 * w + lane] = transpose32_lane(S[lane * W + w], lane);
-  __syncthreads();
-  uint32_t c[8];
-#pragma unroll
-  for (int k = 0; k < 8; ++k) c[k] = 0u;
-  if (ne > 0) ptx::mbar_wait(&bar[1], 0);
-  for (int e = threadIdx.x; e < ne; e += blockDim.x) {
-    const int2 ed = E[e];
-    uint32_t carry = T[ed.x] ^ T[ed.y];  // samples in which edge (i, j) is cut
-#pragma unroll
-    for (int k = 0; k < 8; ++k) {
-      const uint32_t t = c[k] & carry;
-      c[k] ^= carry;
-      carry = t;
+      for (int j = 0; j < 32; ++j) T[32 * w + (j ^ (w & 31))] = v[j];  // node 32 w + j
     }
-  }
-  // per-sample counts of this warp: transpose each plane (lane s <- sample s), popc, weight 2^k
-  int cnt = 0;
+    if (!edges_ready) {
+      if (ne > 0) ptx::mbar_wait(&bar[1], 0);
+      edges_ready = true;
+    }
+    __syncthreads();
+    // 16 entries per thread per pass (entries tid + 512 k), Harley-Seal carry-save counting
+    uint32_t ones = 0, twos = 0, fours = 0, eights = 0, c16 = 0, c32 = 0;  // <= 63 per thread (launcher)
+    for (int base = 0; base < ne; base += 16 * kCutThreads) {
+      uint32_t c[16];
 #pragma unroll
-  for (int k = 0; k < 8; ++k) cnt += __popc(transpose32_lane(c[k], lane)) << k;
-  atomicAdd(&scnt[lane], cnt);
-  __syncthreads();
-  if (threadIdx.x < 32 && s0 + threadIdx.x < B) cpart[(size_t)blockIdx.x * B + s0 + threadIdx.x] = scnt[threadIdx.x];
+      for (int k = 0; k < 16; ++k) {
+        const int e = base + k * kCutThreads + tid;
+        uint32_t m = 0u;
+        if (e < ne) {
+          const uint32_t p = E[e];
+          m = T[p & 0xFFFFu] ^ T[p >> 16];  // samples in which this edge is cut
+        }
+        c[k] = m;
+      }
+      uint32_t tA, tB, fA, fB, eA, eB, sx;
+      csa(tA, ones, ones, c[0], c[1]);
+      csa(tB, ones, ones, c[2], c[3]);
+      csa(fA, twos, twos, tA, tB);
+      csa(tA, ones, ones, c[4], c[5]);
+      csa(tB, ones, ones, c[6], c[7]);
+      csa(fB, twos, twos, tA, tB);
+      csa(eA, fours, fours, fA, fB);
+      csa(tA, ones, ones, c[8], c[9]);
+      csa(tB, ones, ones, c[10], c[11]);
+      csa(fA, twos, twos, tA, tB);
+      csa(tA, ones, ones, c[12], c[13]);
+      csa(tB, ones, ones, c[14], c[15]);
+      csa(fB, twos, twos, tA, tB);
+      csa(eB, fours, fours, fA, fB);
+      csa(sx, eights, eights, eA, eB);
+      c32 ^= c16 & sx;  // ripple counter of sixteens (two planes)
+      c16 ^= sx;
+    }
+    // per-sample counts: transpose each plane (lane s <- sample s), popc, weight
+    const int cnt = __popc(transpose32_rot(ones, lane)) + (__popc(transpose32_rot(twos, lane)) << 1) +
+                    (__popc(transpose32_rot(fours, lane)) << 2) + (__popc(transpose32_rot(eights, lane)) << 3) +
+                    (__popc(transpose32_rot(c16, lane)) << 4) + (__popc(transpose32_rot(c32, lane)) << 5);
+    atomicAdd(&scnt[lane], cnt);
+    __syncthreads();  // counts complete; every edge lookup into T done (the next group may overwrite it)
+    if (tid < 32) {
+      if (tid < rows) cpart[(size_t)blockIdx.x * B + s0 + tid] = scnt[tid];
+      scnt[tid] = 0;
+    }
+    // (the next iteration's barriers order these resets before its atomics)
+  }
 }
 
 // ===========================================================================
@@ -712,26 +783,26 @@ void launch_energy(Handle* H, int B) {
     return;
   }
   const int W = H->L.W;
-  const size_t tsm = (size_t)((64 * W + 3) & ~3) * sizeof(uint32_t);  // T + S
-  const size_t cap = 200 * 1024;
-  if (tsm + 256 * 8 <= cap) {  // bit-sliced path (n <= ~25,000)
+  const size_t tw = (size_t)(32 * W + 32) * sizeof(uint32_t);
+  const size_t cap = 110 * 1024;  // two CTAs per SM
+  if (H->d_edges_bank && W <= kCutThreads && tw + 16 * 1024 <= cap) {  // bit-sliced path (n <= 12,288)
     const int groups = (B + 31) / 32;
-    const int64_t nE = H->num_edges;
-    // chunk: fits the remaining shared memory, <= 255 edges per thread (8 counter planes);
-    // split further while there are fewer than ~148 CTAs and >= 8 edges per thread remain
-    const int64_t per_max = std::min<int64_t>(255 * 256, (int64_t)((cap - tsm) / 8) - 2);
-    int64_t chunks = std::max<int64_t>(1, (nE + per_max - 1) / per_max);
-    while (chunks * groups < 148 && (nE + 2 * chunks - 1) / (2 * chunks) >= 256 * 8) chunks *= 2;
-    int64_t per = std::max<int64_t>(2, (nE + chunks - 1) / chunks);
-    per = (per + 1) & ~int64_t(1);  // even: the bulk copies start 16-byte aligned
-    chunks = std::max<int64_t>(1, (nE + per - 1) / per);
-    const size_t smem = tsm + (size_t)(per + 2) * 8;
-    if (smem > 48 * 1024) ensure_smem_attr((const void*)maxcut_cut_kernel, cap);
+    const int64_t nEp = H->num_edges_bank;
+    // edge chunks: fit the remaining shared memory; small batches split further (more CTAs, up to
+    // two per SM) while a chunk keeps >= 2 passes' worth of entries; groups are spread over the CTAs
+    const int64_t per_max = std::min<int64_t>(63 * kCutThreads, (int64_t)((cap - tw) / 4)) & ~int64_t(31);
+    int64_t chunks = std::max<int64_t>(1, (nEp + per_max - 1) / per_max);
+    while (chunks * groups * 2 <= 2 * 148 && nEp / (2 * chunks) >= 2 * kCutThreads) chunks *= 2;
+    int64_t per = std::max<int64_t>(32, ((nEp + chunks - 1) / chunks + 31) & ~int64_t(31));
+    chunks = std::max<int64_t>(1, (nEp + per - 1) / per);
+    const int ctas_y = (int)std::min<int64_t>(groups, std::max<int64_t>(1, (2 * 148) / chunks));
+    const size_t smem = tw + (size_t)per * 4;
+    ensure_smem_attr((const void*)maxcut_cut_kernel, cap);
     H->ensure_cpart((int)chunks * B);
     H->cut_chunks = (int)chunks;
     KScope ks(H, "maxcut_energy");
-    launch_k(H, maxcut_cut_kernel, dim3((unsigned)chunks, (unsigned)groups), dim3(256), smem, B, H->L.n, W, nE, per,
-             (const int2*)H->d_edges, (const uint32_t*)H->X, H->cpart);
+    launch_k(H, maxcut_cut_kernel, dim3((unsigned)chunks, (unsigned)ctas_y), dim3(kCutThreads), smem, B, W, nEp, per,
+             (const uint32_t*)H->d_edges_bank, (const uint32_t*)H->X, H->cpart);
     LAUNCH_CHECK();
     H->launches++;
     return;
