@@ -51,13 +51,17 @@ struct AdamOut {
   // derived copies) untouched, so a failed step does not poison the parameters (the reference
   // aborts in phase 1, before any update: trainer.cpp:170-179)
   const uint32_t* flag;
+  bool v4;        // head v4 staging (head4.cuh) instead of the v3 rows
+  Head4Stage h4;
 };
 
 __device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, float p) {
   // (32-bit index math: the live buffer is < 2^31 entries, checked at handle creation)
   if (t < o.off_b1) {  // W1T[j][k]
     const unsigned tt = (unsigned)t, j = tt / (unsigned)o.h, k = tt - j * (unsigned)o.h;
-    if (!o.perm) {
+    if (o.v4) {
+      head4_put_w1(o.h4, (int)j, (int)k, p);
+    } else if (!o.perm) {
       o.W1Tp[(size_t)j * o.hpk + k] = p;
     } else {
       const int pos = head_rel_pos_dev((int)j, (int)k);
@@ -66,7 +70,9 @@ __device__ __forceinline__ void adam_side_writes(const AdamOut& o, int64_t t, fl
   } else if (t >= o.off_w2 && t < o.off_b2) {  // W2[i][k]
     const unsigned u = (unsigned)(t - o.off_w2), i = u / (unsigned)o.h, k = u - i * (unsigned)o.h;
     ptx::split_f16(p, o.W2h[(size_t)i * o.hp18 + k], o.W2l[(size_t)i * o.hp18 + k]);
-    if ((int)i < o.Hd) {
+    if ((int)i < o.Hd && o.v4) {
+      head4_put_w2(o.h4, (int)i, (int)k, p);
+    } else if ((int)i < o.Hd) {
       const int c = o.comp_pos[k];
       if (!o.perm) {
         o.W2cp[(size_t)c * o.Hdp + i] = p;

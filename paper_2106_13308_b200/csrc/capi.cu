@@ -591,6 +591,17 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
     VQMC_CUDA(cudaMemset(H->W2cp, 0, r2 * kp * sizeof(float)));
     H->head_hpk = kp;
     H->head_Hdp = H->head_fast ? kp : 32 * ((Hd + 31) / 32);
+    const char* hv = std::getenv("VQMC_HEAD");  // "3": keep the v3 head sampler (A/B measurements)
+    H->head_v4 = H->head_fast && !(hv && hv[0] == '3');
+    if (H->head_v4) {
+      const int KG = kp / 128, nwords = (h + 31) / 32;
+      const size_t af = (size_t)nwords * KG * 2 * 8192, tri = (size_t)nwords * 32 * 64;  // halves, floats
+      dalloc(&H->h4.AF, af);
+      dalloc(&H->h4.TRI, tri);
+      VQMC_CUDA(cudaMemset(H->h4.AF, 0, af * sizeof(__half)));
+      VQMC_CUDA(cudaMemset(H->h4.TRI, 0, tri * sizeof(float)));
+      H->h4.KG = KG;
+    }
     std::vector<int32_t> cpos(h);
     for (int c = 0; c < h; ++c) cpos[ks[c]] = c;
     dalloc(&H->d_comp_pos, (size_t)h);
@@ -642,7 +653,7 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
                   H->lp_head, H->thr, H->lp_part, H->log_psi, H->cut, H->cpart, H->local, H->w, H->d_wscale,
                   H->Epart, H->dz1bh, H->dz1bl, H->Xfb, H->gw1_part, H->cond, H->uni, H->d_scal,
-                  H->d_gpart, H->d_step, H->d_done, H->d_comp_pos};
+                  H->d_gpart, H->d_step, H->d_done, H->d_comp_pos, H->h4.AF, H->h4.TRI};
   for (void* p : ptrs)
     if (p) cudaFree(p);
   if (H->h_scal) cudaFreeHost(H->h_scal);

@@ -25,6 +25,8 @@
 
 #include "device_common.cuh"
 #include "internal.cuh"
+#include "head4.cuh"
+#include "ptx.cuh"
 
 namespace vqmc_b200 {
 
@@ -705,6 +707,264 @@ __global__ void __launch_bounds__(32 * (8 / kHeadS + 1 + kHeadEmitWarps)) head_v
   if (lane == 0) mbar_arrive(&empty[S.slot]);
 }
 
+// ===========================================================================
+// Head sampler v4 (fast structure; staging layout: head4.cuh).
+//
+// One CTA = 8 consumer warps (one sample each: the N = 8 of the tensor-core updates) + a TMA
+// producer warp.  Per 32-bit word m:
+//   chain   lane l owns bit 32m + l: z1c / z2c are unit / output 32m + l; the word's own 32 x 32
+//           blocks (TRI, staged in shared memory) give the in-word rank-1 updates.  Bit l' on
+//           lane l': x = [thr < z2c], g = relu(z1c + x W1[i][i]) (both candidates precomputed),
+//           sent in one shuffle (x in the sign bit); every lane then applies 2 FMAs.  Serial
+//           chain per bit: compare, select, shuffle, fma.
+//   emit    every lane writes its own bit's outputs (G1 + fp16 pair, D pair, spins, log-prob
+//           term, conditionals) and the warp ballots the packed spin word.
+//   update  x and the fp16 pair of g of the word's 32 bits x 8 samples are staged in shared
+//           memory; every warp applies them to the accumulator tiles it owns (tile j of 16 slots
+//           -> warp j % 8): z1 += W1[s][word] X (2 MMAs per k-step: x is exact in fp16), z2 +=
+//           W2[s][word] (G_hi + G_lo) with the W2 pair (3 MMAs): mma.sync m16n8k16, fp32
+//           accumulators in registers (rows = slots, columns = the CTA's 8 samples).  The A
+//           operands stream through a ring of 16 KB chunks (TMA bulk copies issued ahead by the
+//           producer warp, which also double-buffers the TRI blocks).
+//   exchange the owners of the next word's two tiles write them (16 slots x 8 samples, z1 and
+//           z2) to shared memory; each chain warp reads its sample's 32 slots.
+// Work per bit drops from ~100 dependent FMA/LDS instructions per warp (v3) to the short chain;
+// the rank-32 updates run on the tensor cores once per word.
+// ===========================================================================
+constexpr int kH4Warps = 8;          // consumer warps = samples per CTA
+constexpr int kH4Ring = 6;           // 16 KB A-operand chunks in flight
+constexpr int kH4Chunk = 16384;
+constexpr int kH4Tri = 8192;         // bytes of one word's TRI block ([64][32] floats)
+constexpr int kH4BStride = 40;       // halves per sample row of the staged B operand (conflict-free)
+
+struct HeadV4Args {
+  int B, n, h, W, nwords, T, Hd8;  // T = 16-slot tiles of the head (ceil(h / 16))
+  const __half* AF;
+  const float* TRI;
+  const float* b1;
+  const float* b2;
+  uint32_t* X;
+  float* G1;
+  __half* G1h;
+  __half* G1l;
+  int hp;
+  __half* Dh;
+  __half* Dl;
+  int np;
+  __nv_bfloat16* Xf;
+  int hd1p;
+  double* lp_head;
+  double* cond;
+  const float* thr;  // [B][Hd8] logit thresholds (head_thresholds_kernel)
+};
+
+__device__ __forceinline__ void h4_mma(float (&d)[4], const uint4& a, uint32_t b0, uint32_t b1) {
+  asm volatile(
+      "mma.sync.aligned.m16n8k16.row.col.f32.f16.f16.f32 {%0, %1, %2, %3}, {%4, %5, %6, %7}, {%8, %9}, "
+      "{%0, %1, %2, %3};"
+      : "+f"(d[0]), "+f"(d[1]), "+f"(d[2]), "+f"(d[3])
+      : "r"(a.x), "r"(a.y), "r"(a.z), "r"(a.w), "r"(b0), "r"(b1));
+}
+__device__ __forceinline__ void h4_bar_consumers() { asm volatile("bar.sync 1, 256;" ::: "memory"); }
+
+// Shared memory: mbarriers @0 | Zx [2][32][8] f32 @128 | B staging 3 x [8][40] f16 @2176 |
+// TRI [2][64][32] f32 @4096 | ring [kH4Ring][16 KB] @20480.
+template <int KG, bool GIVEN>
+__global__ void __launch_bounds__(32 * (kH4Warps + 1), 1) head_v4_kernel(const __grid_constant__ HeadV4Args A) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);
+  uint64_t* empty = full + kH4Ring;
+  uint64_t* tfull = empty + kH4Ring;  // [2]
+  uint64_t* tempty = tfull + 2;       // [2]
+  float* Zx = reinterpret_cast<float*>(smem_raw + 128);            // [2][32][8] (2 KB)
+  __half* Bx = reinterpret_cast<__half*>(smem_raw + 2176);         // [8][40] x
+  __half* Bgh = Bx + 8 * kH4BStride;                               // [8][40] g hi
+  __half* Bgl = Bgh + 8 * kH4BStride;                              // [8][40] g lo (ends at 4096)
+  float* tri_s = reinterpret_cast<float*>(smem_raw + 4096);        // [2][64][32]
+  unsigned char* ring = smem_raw + 4096 + 2 * kH4Tri;              // [kH4Ring][16 KB]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = A.h, nwords = A.nwords, T = A.T;
+  const int cta_b0 = kH4Warps * blockIdx.x;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < kH4Ring; ++r) {
+      mbar_init(&full[r], 1);
+      mbar_init(&empty[r], kH4Warps);
+    }
+    for (int p = 0; p < 2; ++p) {
+      mbar_init(&tfull[p], 1);
+      mbar_init(&tempty[p], kH4Warps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  ptx::pdl_trigger();
+  ptx::pdl_wait();  // thresholds (previous kernel) complete
+  const int rounds = (T + 7) >> 3;
+
+  if (warp == kH4Warps) {  // ---------------- producer: TRI blocks and A-operand chunks ----------------
+    if (lane == 0) {
+      int slot = 0, use = 0;
+      auto tri_copy = [&](int m) {
+        const int p = m & 1;
+        if (m >= 2) mbar_wait_sleep(&tempty[p], ((m >> 1) - 1) & 1);
+        mbar_expect_tx(&tfull[p], kH4Tri);
+        bulk_g2s(tri_s + p * 2048, A.TRI + (size_t)m * 2048, kH4Tri, &tfull[p]);
+      };
+      tri_copy(0);
+      for (int m = 0; m + 1 < nwords; ++m) {
+        tri_copy(m + 1);
+        for (int r = (2 * m + 2) >> 3; r < rounds; ++r) {
+          for (int z = 0; z < 2; ++z) {
+            if (use > 0) mbar_wait_sleep(&empty[slot], (use - 1) & 1);
+            mbar_expect_tx(&full[slot], kH4Chunk);
+            bulk_g2s(ring + (size_t)slot * kH4Chunk, A.AF + head4_chunk_off(KG, m, r, z), kH4Chunk, &full[slot]);
+            if (++slot == kH4Ring) {
+              slot = 0;
+              ++use;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  // ---------------- consumer warp `warp`: sample b ----------------
+  const int w = warp, b = cta_b0 + w;
+  const int g = lane >> 2, t4 = lane & 3;
+  float acc1[KG][4], acc2[KG][4];  // tiles j = 8 r + w: rows g, g + 8 of the tile, columns 2 t4, 2 t4 + 1
+#pragma unroll
+  for (int r = 0; r < KG; ++r) {
+    const int s0 = 16 * (8 * r + w) + g, s1 = s0 + 8;
+    const float a0 = s0 < h ? A.b1[s0] : 0.f, a1 = s1 < h ? A.b1[s1] : 0.f;
+    const float c0 = s0 < h ? A.b2[s0] : 0.f, c1 = s1 < h ? A.b2[s1] : 0.f;
+    acc1[r][0] = acc1[r][1] = a0;
+    acc1[r][2] = acc1[r][3] = a1;
+    acc2[r][0] = acc2[r][1] = c0;
+    acc2[r][2] = acc2[r][3] = c1;
+  }
+  const bool bvalid = b < A.B;
+  float thr = (bvalid && lane < A.Hd8) ? A.thr[(size_t)b * A.Hd8 + lane] : INFINITY;
+  double lp = 0.0;
+  int slot = 0, use = 0;
+  for (int m = 0; m < nwords; ++m) {
+    // ---- exchange: the owners of tiles 2m, 2m + 1 publish word m's slots ----
+    {
+      const int r = (2 * m) >> 3;
+      const bool own0 = w == ((2 * m) & 7), own1 = w == ((2 * m + 1) & 7);
+      if (own0 || own1) {
+        const int base = own1 ? 16 : 0;
+#pragma unroll
+        for (int rr = 0; rr < KG; ++rr) {
+          if (rr == r) {
+            Zx[(base + g) * 8 + 2 * t4] = acc1[rr][0];
+            Zx[(base + g) * 8 + 2 * t4 + 1] = acc1[rr][1];
+            Zx[(base + g + 8) * 8 + 2 * t4] = acc1[rr][2];
+            Zx[(base + g + 8) * 8 + 2 * t4 + 1] = acc1[rr][3];
+            Zx[256 + (base + g) * 8 + 2 * t4] = acc2[rr][0];
+            Zx[256 + (base + g) * 8 + 2 * t4 + 1] = acc2[rr][1];
+            Zx[256 + (base + g + 8) * 8 + 2 * t4] = acc2[rr][2];
+            Zx[256 + (base + g + 8) * 8 + 2 * t4 + 1] = acc2[rr][3];
+          }
+        }
+      }
+    }
+    h4_bar_consumers();
+    float z1c = Zx[lane * 8 + w], z2c = Zx[256 + lane * 8 + w];
+    // ---- serial chain over the word's 32 bits ----
+    const int p = m & 1;
+    mbar_wait(&tfull[p], (m >> 1) & 1);
+    const float* tw = tri_s + p * 2048 + lane;  // tw[32 l] = W1[32m + lane][32m + l], tw[32 (32 + l)] = W2[...]
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const float t1 = tw[32 * l], t2 = tw[32 * (32 + l)];
+      const float g0 = fmaxf(z1c, 0.f), g1 = fmaxf(z1c + t1, 0.f);  // (on lane l: t1 = W1[i][i])
+      float v = (thr < z2c) ? -g1 : g0;                             // x in the sign bit
+      v = __shfl_sync(kFull, v, l);
+      const float xf = (__float_as_uint(v) >> 31) ? 1.f : 0.f;
+      z1c = fmaf(xf, t1, z1c);           // lanes >= l (t1 = 0 above this lane's diagonal)
+      z2c = fmaf(fabsf(v), t2, z2c);     // lanes > l
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[p]);
+    const bool x = thr < z2c;  // this lane's bit (its logit no longer changes)
+    const float gl = fmaxf(z1c, 0.f);
+    // ---- outputs of the word's bits (one per lane) ----
+    {
+      const int ib = 32 * m + lane;
+      const bool mine = bvalid && ib < h;
+      if (mine)
+        lp += head_emit(b, ib, z2c, z1c, x ? 1 : 0, A.n, h, A.hp, A.np, A.hd1p, A.G1, A.G1h, A.G1l, A.Dh, A.Dl, A.Xf,
+                        A.cond);
+      const uint32_t word = __ballot_sync(kFull, mine && x);
+      if (!GIVEN && bvalid && lane == 0) A.X[(size_t)b * A.W + m] = word;
+    }
+    if (m + 1 == nwords) break;
+    // ---- stage B = (x, g_hi, g_lo) of the word, [sample][bit] ----
+    {
+      __half gh, glo;
+      ptx::split_f16(gl, gh, glo);
+      Bx[w * kH4BStride + lane] = __float2half_rn(x ? 1.f : 0.f);
+      Bgh[w * kH4BStride + lane] = gh;
+      Bgl[w * kH4BStride + lane] = glo;
+      const int ib = 32 * (m + 1) + lane;  // next word's threshold (latency hidden by the MMAs)
+      thr = (bvalid && ib < A.Hd8) ? A.thr[(size_t)b * A.Hd8 + ib] : INFINITY;
+    }
+    h4_bar_consumers();
+    uint32_t bx[2][2], bh[2][2], bl[2][2];
+#pragma unroll
+    for (int ks = 0; ks < 2; ++ks) {
+      const int o = g * kH4BStride + 16 * ks + 2 * t4;
+      bx[ks][0] = *reinterpret_cast<const uint32_t*>(Bx + o);
+      bx[ks][1] = *reinterpret_cast<const uint32_t*>(Bx + o + 8);
+      bh[ks][0] = *reinterpret_cast<const uint32_t*>(Bgh + o);
+      bh[ks][1] = *reinterpret_cast<const uint32_t*>(Bgh + o + 8);
+      bl[ks][0] = *reinterpret_cast<const uint32_t*>(Bgl + o);
+      bl[ks][1] = *reinterpret_cast<const uint32_t*>(Bgl + o + 8);
+    }
+    // ---- rank-32 updates of the later tiles (the producer's chunk order: r, then z) ----
+    const int r0 = (2 * m + 2) >> 3;
+#pragma unroll
+    for (int r = 0; r < KG; ++r) {
+      if (r < r0 || r >= rounds) continue;
+      const int j = 8 * r + w;
+      const bool live = j >= 2 * m + 2 && j < T;
+#pragma unroll
+      for (int z = 0; z < 2; ++z) {
+        mbar_wait(&full[slot], use & 1);
+        if (live) {
+          const unsigned char* cb = ring + (size_t)slot * kH4Chunk + (size_t)w * 2048 + lane * 16;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint4 ah = *reinterpret_cast<const uint4*>(cb + ks * 1024);
+            const uint4 al = *reinterpret_cast<const uint4*>(cb + ks * 1024 + 512);
+            if (z == 0) {
+              h4_mma(acc1[r], ah, bx[ks][0], bx[ks][1]);
+              h4_mma(acc1[r], al, bx[ks][0], bx[ks][1]);
+            } else {
+              h4_mma(acc2[r], ah, bh[ks][0], bh[ks][1]);
+              h4_mma(acc2[r], ah, bl[ks][0], bl[ks][1]);
+              h4_mma(acc2[r], al, bh[ks][0], bh[ks][1]);
+            }
+          }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[slot]);
+        if (++slot == kH4Ring) {
+          slot = 0;
+          ++use;
+        }
+      }
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lp += __shfl_xor_sync(kFull, lp, o);
+  if (bvalid && lane == 0) {
+    A.lp_head[b] = lp;
+    A.Xf[(size_t)b * A.hd1p + h] = __float2bfloat16_rn(1.f);  // ones column: gb1 = 1^T dz1
+  }
+}
+
 // Padded, completion-ordered copies of the head blocks (refreshed after every update):
 //   W1Tp[j][k] = W1m[k][j]           j < Hd, k < h (row stride hp)
 //   W2cp[c][i] = W2m[i][comp_k[c]]   c < h,  i < Hd (row stride Hdp)
@@ -731,6 +991,22 @@ __global__ void head_pack_kernel(int h, int Hd, int hp, int Hdp, int perm, const
       const int m = c >> 5, tt = (i >> 5) - m;
       if (tt >= 0) W2cp[(size_t)c * Hdp + head_rel_pos(tt, i & 31)] = i < Hd ? W2[(size_t)i * h + comp_k[c]] : 0.f;
     }
+  }
+}
+
+// v4 staging (head4.cuh) from the live parameters: every W1T[j][k] (j < Hd) and head W2[i][k]
+// (i < Hd) lands in TRI or AF; masked entries (zero) and earlier-word slots are never stored.
+__global__ void head4_pack_kernel(int h, int Hd, Head4Stage S, const float* __restrict__ W1T,
+                                  const float* __restrict__ W2) {
+  const int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n1 = (int64_t)Hd * h;
+  if (t < n1) {
+    const int j = (int)(t / h), k = (int)(t % h);
+    head4_put_w1(S, j, k, W1T[t]);
+  } else if (t < 2 * n1) {
+    const int64_t u = t - n1;
+    const int i = (int)(u / h), k = (int)(u % h);
+    head4_put_w2(S, i, k, W2[u]);
   }
 }
 
@@ -769,6 +1045,15 @@ static HeadGeom head_geometry(const Handle* H) {
 
 void launch_head_pack(Handle* H) {
   const Layout& L = H->L;
+  if (H->head_v4) {
+    const int64_t total = 2 * (int64_t)L.Hd * L.h;
+    KScope ks(H, "head_pack");
+    head4_pack_kernel<<<(unsigned)((total + 255) / 256), 256, 0, H->stream>>>(L.h, L.Hd, H->h4, H->P + L.off_w1t,
+                                                                             H->P + L.off_w2);
+    VQMC_CUDA(cudaGetLastError());
+    H->launches++;
+    return;
+  }
   const int hp = H->head_hpk, Hdp = H->head_Hdp;
   const int64_t total = (int64_t)L.Hd * hp + (int64_t)L.h * Hdp;
   KScope ks(H, "head_pack");
@@ -864,6 +1149,37 @@ static void head_v3_launch(Handle* H, int B, const double* uni, RngSpec rng, dou
   H->launches++;
 }
 
+template <int KG, bool GIVEN>
+static void head_v4_launch(Handle* H, int B, const double* uni, RngSpec rng, double* cond) {
+  const Layout& L = H->L;
+  const size_t smem = 4096 + 2 * kH4Tri + (size_t)kH4Ring * kH4Chunk;
+  ensure_smem_attr((const void*)head_v4_kernel<KG, GIVEN>, smem);
+  const int grid = (B + kH4Warps - 1) / kH4Warps;
+  const int Hd8 = (L.Hd + 7) & ~7;
+  {
+    KScope ks(H, "head_thresholds");
+    const int64_t total = (int64_t)B * (Hd8 / 4);
+    launch_k(H, head_thresholds_kernel, dim3((unsigned)((total + 255) / 256)), dim3(256), 0, B, L.Hd, Hd8, L.W, uni,
+             rng, H->X, GIVEN ? 1 : 0, H->thr);
+    VQMC_CUDA(cudaGetLastError());
+    H->launches++;
+  }
+  KScope ks(H, GIVEN ? "head_given" : "head_sample");
+  const HeadV4Args args{B,        L.n,      L.h,          L.W,      (L.h + 31) / 32, (L.h + 15) / 16,
+                        Hd8,      H->h4.AF, H->h4.TRI,    H->P + L.off_b1, H->P + L.off_b2, H->X,
+                        H->G1,    H->G1h,   H->G1l,       H->hp18,  H->Dh,           H->Dl,
+                        H->np8,   H->Xfb,   H->hd18,      H->lp_head, cond,          H->thr};
+  launch_k(H, head_v4_kernel<KG, GIVEN>, dim3(grid), dim3(32 * (kH4Warps + 1)), smem, args);
+  VQMC_CUDA(cudaGetLastError());
+  H->launches++;
+}
+
+template <int KG>
+static void head_v4_dispatch(Handle* H, int B, const double* uni, RngSpec rng, bool given, double* cond) {
+  if (given) head_v4_launch<KG, true>(H, B, uni, rng, cond);
+  else head_v4_launch<KG, false>(H, B, uni, rng, cond);
+}
+
 template <int KG>
 static void head_v3_dispatch(Handle* H, int B, const double* uni, RngSpec rng, bool given, double* cond) {
   if (given) head_v3_launch<KG, true>(H, B, uni, rng, cond);
@@ -871,6 +1187,19 @@ static void head_v3_dispatch(Handle* H, int B, const double* uni, RngSpec rng, b
 }
 
 void launch_head_v2(Handle* H, int B, const double* uni, RngSpec rng, bool given, double* cond) {
+  if (H->head_v4) {
+    switch (H->h4.KG) {
+      case 1: head_v4_dispatch<1>(H, B, uni, rng, given, cond); return;
+      case 2: head_v4_dispatch<2>(H, B, uni, rng, given, cond); return;
+      case 3: head_v4_dispatch<3>(H, B, uni, rng, given, cond); return;
+      case 4: head_v4_dispatch<4>(H, B, uni, rng, given, cond); return;
+      case 5: head_v4_dispatch<5>(H, B, uni, rng, given, cond); return;
+      case 6: head_v4_dispatch<6>(H, B, uni, rng, given, cond); return;
+      case 7: head_v4_dispatch<7>(H, B, uni, rng, given, cond); return;
+      case 8: head_v4_dispatch<8>(H, B, uni, rng, given, cond); return;
+      default: throw InvalidArgument("head sampler: hidden width > 1024 is not supported");
+    }
+  }
   if (H->head_fast) {
     switch (H->head_hpk / 128) {
       case 1: head_v3_dispatch<1>(H, B, uni, rng, given, cond); return;

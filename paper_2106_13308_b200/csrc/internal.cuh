@@ -3,6 +3,7 @@
 
 #include <cuda_bf16.h>
 #include <cuda_fp16.h>
+#include "head4.cuh"
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -192,6 +193,8 @@ struct Handle {
   unsigned* d_done = nullptr;      // last-block counter of the Adam grad-norm reduction
   std::vector<int32_t> comp_off_host;  // [Hd + 1]
   bool head_fast = false;  // bit i completes exactly hidden unit i (head v3, lane-permuted staging)
+  bool head_v4 = false;    // head_fast and the v4 sampler (tensor-core word updates; VQMC_HEAD=3 keeps v3)
+  Head4Stage h4{nullptr, nullptr, 0};  // v4 staging (head4.cuh)
   bool w1skip = false;     // deg_k <= k + 1 for all k (W1 columns below the current word are dead)
   int32_t* d_deg = nullptr;
   int32_t* d_comp_k = nullptr;    // hidden units sorted by degree

@@ -908,7 +908,7 @@ static AdamOut adam_out(const Handle* H, bool gated) {
   const bool vec = (L.h % 4) == 0 && (L.off_w2 % 4) == 0;
   return AdamOut{L.h, H->hp18, L.Hd, H->head_hpk, H->head_Hdp, H->head_fast, vec, L.off_b1, L.off_w2, L.off_b2,
                  H->d_comp_pos, H->W1Tp, H->W2cp, H->W2h, H->W2l,
-                 gated ? H->d_flag : nullptr};
+                 gated ? H->d_flag : nullptr, H->head_v4, H->h4};
 }
 
 void launch_adam(Handle* H, float grad_scale, bool gated) {  // the whole live buffer in one launch
