@@ -72,6 +72,13 @@ def lib():
     L.oracle_score_matrix.argtypes = [C.c_int, C.c_int, _ip, _dp, C.c_int, _u8, _dp]
     L.oracle_sr_direction.argtypes = [C.c_int64, C.c_int, _dp, C.c_int, _dp, C.c_double, C.c_double, C.c_int,
                                       _dp, C.POINTER(C.c_int), C.POINTER(C.c_double)]
+    L.oracle_random_tim.argtypes = [C.c_int, C.c_uint64, _dp, _dp, _ip, _ip, _dp]
+    L.oracle_diagonal_energy.argtypes = [C.c_int, _dp, _dp, _ip, _ip, _dp, C.c_int64, C.c_int, _u8, _dp]
+    L.oracle_local_energy_spec.argtypes = [C.c_int, C.c_int, _ip, _dp, _dp, _dp, _ip, _ip, _dp, C.c_int64,
+                                           C.c_int, _u8, _dp, _dp]
+    L.oracle_train_spec.argtypes = [C.c_int, C.c_int, _dp, _dp, _ip, _ip, _dp, C.c_int64, C.c_int, C.c_double,
+                                    C.c_int, C.c_int, C.c_int, C.c_int, C.c_uint64, C.c_int, C.c_int,
+                                    C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p]
     _lib = L
     return L
 
@@ -326,3 +333,91 @@ def time_reference_step(n, edges, workers, minibatch, seed=0, bits_limit=None, h
     _check(lib().oracle_time_reference_step(n, h, e, e.size // 2, workers, minibatch, seed,
                                             bits_limit or n, out))
     return dict(sample_s=out[0], estimate_s=out[1], update_s=out[2], step_s=out[3], bits_timed=int(out[4]))
+
+
+# ---------------------------------------------------------------------------
+# General Ising spec (TIM): hamiltonian.hpp:26-44, hamiltonian.cpp:36-69,126-142,
+# estimator.hpp:43-90
+# ---------------------------------------------------------------------------
+class Spec:
+    """H = -sum_i (alpha_i X_i + beta_i Z_i) - sum_{i<j} beta_ij Z_i Z_j (pairs: i, j, value)."""
+
+    def __init__(self, n, alpha, beta, pi, pj, pv):
+        self.n = n
+        self.alpha = np.ascontiguousarray(alpha, np.float64)
+        self.beta = np.ascontiguousarray(beta, np.float64)
+        self.pi = np.ascontiguousarray(pi, np.int32)
+        self.pj = np.ascontiguousarray(pj, np.int32)
+        self.pv = np.ascontiguousarray(pv, np.float64)
+
+    @property
+    def npairs(self):
+        return self.pi.size
+
+    def args(self):
+        return (self.alpha, self.beta, self.pi, self.pj, self.pv, self.npairs)
+
+
+def random_tim(n, seed):
+    np_ = n * (n - 1) // 2
+    a = np.empty(n); b = np.empty(n)
+    pi = np.empty(np_, np.int32); pj = np.empty(np_, np.int32); pv = np.empty(np_)
+    _check(lib().oracle_random_tim(n, seed, a, b, pi, pj, pv))
+    return Spec(n, a, b, pi, pj, pv)
+
+
+def maxcut_spec(n, edges):
+    """maxcut_spec (hamiltonian.cpp:109-119): alpha = beta = 0, beta_ij = -1/4 per edge."""
+    e = np.asarray(edges, np.int32).reshape(-1, 2)
+    return Spec(n, np.zeros(n), np.zeros(n), e[:, 0], e[:, 1], np.full(e.shape[0], -0.25))
+
+
+def diagonal_energy(spec: Spec, x):
+    x = np.ascontiguousarray(x, np.uint8)
+    out = np.empty(x.shape[0])
+    _check(lib().oracle_diagonal_energy(spec.n, *spec.args(), x.shape[0], x, out))
+    return out
+
+
+def local_energy_spec(spec: Spec, m: Made, x, cached_log_psi):
+    """local_energy_batch (estimator.hpp:43-90) with the off-diagonal (flipped-neighbour) branch."""
+    x = np.ascontiguousarray(x, np.uint8)
+    out = np.empty(x.shape[0])
+    _check(lib().oracle_local_energy_spec(m.n, m.h, m.degrees, m.theta, *spec.args(), x.shape[0], x,
+                                          np.ascontiguousarray(cached_log_psi, np.float64), out))
+    return out
+
+
+def train_spec(spec: Spec, h=0, optimizer="adam", lr=0.0, iterations=300, workers=1, minibatch=1024,
+               eval_batch=1024, seed=0, sampler_mode=0, threads=True, want_first_grad=False,
+               sr_lambda=1e-3, sr_tol=1e-6, sr_max_iterations=200, sr_fallback=False, sr_centered=True):
+    """Restated vqmc::train for MADE+AUTO on a general spec (TIM) (trainer.cpp:111-322)."""
+    n = spec.n
+    hh = h if h > 0 else default_made_hidden(n)
+    d = 2 * hh * n + hh + n
+    stats = np.empty((iterations, 4)); ev = np.empty(4); theta = np.empty(d)
+    g0 = np.empty(d) if want_first_grad else None
+    _check(lib().oracle_set_train_sr(sr_lambda, sr_tol, sr_max_iterations, 1 if sr_fallback else 0,
+                                     1 if sr_centered else 0))
+    _check(lib().oracle_train_spec(n, hh, *spec.args(), _OPT[optimizer], lr, iterations, workers, minibatch,
+                                   eval_batch, seed, sampler_mode, 1 if threads else 0, _ptr(stats), _ptr(ev),
+                                   _ptr(theta), _ptr(g0)))
+    out = dict(stats=stats, final_energy=ev[0], final_energy_std=ev[1], theta=theta, h=hh)
+    if want_first_grad:
+        out["first_grad"] = g0
+    return out
+
+
+def dense_hamiltonian(spec: Spec):
+    """dense_matrix (oracle.cpp) in numpy for small n: H[x, y], bit 1 = MSB of the index."""
+    n = spec.n
+    N = 1 << n
+    idx = np.arange(N)
+    X = ((idx[:, None] >> (n - 1 - np.arange(n))[None, :]) & 1).astype(np.float64)
+    S = 1.0 - 2.0 * X
+    diag = -(S @ spec.beta) - np.sum(spec.pv[None, :] * S[:, spec.pi] * S[:, spec.pj], axis=1)
+    H = np.diag(diag)
+    for i in range(n):
+        if spec.alpha[i] != 0.0:
+            H[idx, idx ^ (1 << (n - 1 - i))] -= spec.alpha[i]
+    return H

@@ -525,6 +525,116 @@ std::vector<double> gradient_from_locals(const Made& m, const double* X, int B,
 }
 
 // ---------------------------------------------------------------------------
+// General Ising spec (TIM): proj/include/vqmc/hamiltonian.hpp:26-44,
+// H = -sum_i (alpha_i X_i + beta_i Z_i) - sum_{i<j} beta_ij Z_i Z_j.
+// ---------------------------------------------------------------------------
+struct PairC {
+  int i, j;
+  double v;
+};
+struct Spec {
+  int n = 0;
+  std::vector<double> alpha, beta;
+  std::vector<PairC> pairs;
+};
+
+// proj/src/hamiltonian.cpp:36-54
+void validate_spec(const Spec& s) {
+  if (s.n < 1) throw std::invalid_argument("spec requires n >= 1");
+  if ((int)s.alpha.size() != s.n || (int)s.beta.size() != s.n)
+    throw std::invalid_argument("alpha/beta length does not match n");
+  for (int i = 0; i < s.n; ++i)
+    if (s.alpha[i] < 0.0) throw std::invalid_argument("alpha must be non-negative");
+  std::set<std::pair<int, int>> seen;
+  for (const auto& p : s.pairs) {
+    if (p.i < 0 || p.j >= s.n || p.i >= p.j)
+      throw std::invalid_argument("pair indices must satisfy 0 <= i < j < n");
+    if (!seen.insert({p.i, p.j}).second) throw std::invalid_argument("duplicate pair");
+  }
+}
+
+// proj/src/hamiltonian.cpp:126-142: alpha ~ U[0,1) for every site, then beta ~ U[-1,1), then
+// every pair (i < j, row-major) ~ U[-1,1), all from make_stream(seed).
+Spec random_tim(int n, uint64_t seed) {
+  if (n < 1) throw std::invalid_argument("random_tim requires n >= 1");
+  auto rng = make_stream(seed);
+  std::uniform_real_distribution<double> unit(0.0, 1.0);
+  std::uniform_real_distribution<double> symmetric(-1.0, 1.0);
+  Spec s;
+  s.n = n;
+  s.alpha.resize(n);
+  s.beta.resize(n);
+  for (int i = 0; i < n; ++i) s.alpha[i] = unit(rng);
+  for (int i = 0; i < n; ++i) s.beta[i] = symmetric(rng);
+  s.pairs.reserve((size_t)n * (n - 1) / 2);
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j) s.pairs.push_back({i, j, symmetric(rng)});
+  return s;
+}
+
+// proj/src/hamiltonian.cpp:61-69
+double diagonal_energy(const Spec& s, const double* x) {
+  double energy = 0.0;
+  for (int i = 0; i < s.n; ++i) energy -= s.beta[i] * (1.0 - 2.0 * x[i]);
+  for (const auto& p : s.pairs) energy -= p.v * (1.0 - 2.0 * x[p.i]) * (1.0 - 2.0 * x[p.j]);
+  return energy;
+}
+
+// proj/include/vqmc/estimator.hpp:43-90 for the MADE model: diagonal part, then the flipped
+// neighbours of every site with alpha > 0 in chunks of at most 2^22 / n rows (log_psi_batch =
+// log_prob / 2, models.cpp:126-128), exponents shifted only when the largest exceeds 50.
+std::vector<double> local_energy_batch(const Spec& s, const Made& m, const double* X, int B,
+                                       const double* cached_log_psi) {
+  const int n = s.n;
+  std::vector<int> sites;
+  for (int i = 0; i < n; ++i)
+    if (s.alpha[i] > 0.0) sites.push_back(i);
+  const long S = (long)sites.size();
+  std::vector<double> local(B);
+  for (int b = 0; b < B; ++b) local[b] = diagonal_energy(s, X + (size_t)b * n);
+  if (S == 0) return local;
+  const long chunk_rows = std::max<long>(1, (1L << 22) / std::max(1, n));
+  const long per_chunk = std::max<long>(1, chunk_rows / S);
+  for (long b0 = 0; b0 < B; b0 += per_chunk) {
+    const long bc = std::min<long>(per_chunk, B - b0);
+    std::vector<double> nb((size_t)bc * S * n);
+    for (long b = 0; b < bc; ++b)
+      for (long k = 0; k < S; ++k) {
+        double* row = &nb[(size_t)(b * S + k) * n];
+        std::memcpy(row, X + (size_t)(b0 + b) * n, sizeof(double) * n);
+        row[sites[k]] = 1.0 - row[sites[k]];
+      }
+    std::vector<double> lp = log_prob(m, nb.data(), (int)(bc * S));
+    for (double& v : lp) v *= 0.5;
+    for (long b = 0; b < bc; ++b) {
+      double max_exponent = 0.0;
+      for (long k = 0; k < S; ++k)
+        max_exponent = std::max(max_exponent, lp[b * S + k] - cached_log_psi[b0 + b]);
+      const double shift = max_exponent > 50.0 ? max_exponent : 0.0;
+      double acc = 0.0;
+      for (long k = 0; k < S; ++k)
+        acc -= s.alpha[sites[k]] * std::exp(lp[b * S + k] - cached_log_psi[b0 + b] - shift);
+      local[b0 + b] += acc * std::exp(shift);
+      if (!std::isfinite(local[b0 + b]))
+        throw std::runtime_error("non-finite local energy (amplitude underflow?)");
+    }
+  }
+  return local;
+}
+
+Spec spec_from(int n, const double* alpha, const double* beta, const int32_t* pi, const int32_t* pj,
+               const double* pv, int64_t np) {
+  Spec s;
+  s.n = n;
+  s.alpha.assign(alpha, alpha + n);
+  s.beta.assign(beta, beta + n);
+  s.pairs.resize((size_t)np);
+  for (int64_t t = 0; t < np; ++t) s.pairs[t] = {pi[t], pj[t], pv[t]};
+  validate_spec(s);
+  return s;
+}
+
+// ---------------------------------------------------------------------------
 // L5 optimizer: proj/src/optimizer.cpp:21-35
 // ---------------------------------------------------------------------------
 struct Adam {
@@ -1079,14 +1189,15 @@ int oracle_sr_direction(int64_t d, int B, const double* scores, int centered, co
   return 0;
 }
 
-int oracle_train(int n, int h, const int32_t* edges, int64_t E, int optimizer, double lr,
-                 int iterations, int workers, int minibatch, int eval_batch, uint64_t seed,
-                 int sampler_mode, int use_threads, double* stats_out, double* eval_out,
-                 double* theta_out, double* first_grad_out) {
-  ORACLE_TRY
-  std::vector<Edge> e((size_t)E);
-  for (int64_t t = 0; t < E; ++t) e[t] = {edges[2 * t], edges[2 * t + 1]};
-  validate_edges(n, e);
+}  // extern "C"
+
+// The training loop over a local-energy function `local_of(model, sample) -> locals` and an
+// evaluation `eval_of(model, rng) -> EvalOut` (Max-Cut: diagonal branch + cuts; TIM: the full
+// local_energy_batch with the sampler's log psi, trainer.cpp:94).
+template <class LocalFn, class EvalFn>
+static void train_core(int n, int h, LocalFn local_of, EvalFn eval_of, int optimizer, double lr, int iterations,
+                       int workers, int minibatch, uint64_t seed, int sampler_mode, int use_threads,
+                       double* stats_out, double* eval_out, double* theta_out, double* first_grad_out) {
   if (workers < 1) throw std::invalid_argument("workers must be >= 1");
   if (iterations < 1) throw std::invalid_argument("iterations must be >= 1");
   if (minibatch < 2) throw std::invalid_argument("minibatch must be >= 2");
@@ -1111,7 +1222,7 @@ int oracle_train(int n, int h, const int32_t* edges, int64_t E, int optimizer, d
       const Sample s = sampler_mode == 1
                            ? auto_sample_incremental(model, mbs, &rngs[w], nullptr, nullptr)
                            : auto_sample(model, mbs, &rngs[w], nullptr, nullptr);
-      locals[w] = local_energy_maxcut(n, e, s.X.data(), mbs);
+      locals[w] = local_of(model, s);
       grads[w] = gradient_from_locals(model, s.X.data(), mbs, locals[w]);
       if (use_sr) {  // trainer.cpp:165-168: rows w * mbs .. of the shared score matrix
         const auto S = score_matrix(model, s.X.data(), mbs);
@@ -1153,7 +1264,7 @@ int oracle_train(int n, int h, const int32_t* edges, int64_t E, int optimizer, d
       stats_out[4 * it + 3] = now_s() - t0;
     }
   }
-  const EvalOut ev = evaluate(n, e, model, eval_batch, eval_rng, sampler_mode == 1);
+  const EvalOut ev = eval_of(model, eval_rng);
   if (eval_out) {
     eval_out[0] = ev.energy;
     eval_out[1] = ev.energy_std;
@@ -1161,6 +1272,86 @@ int oracle_train(int n, int h, const int32_t* edges, int64_t E, int optimizer, d
     eval_out[3] = ev.mean_cut;
   }
   if (theta_out) get_theta(model, theta_out);
+}
+
+extern "C" {
+
+int oracle_train(int n, int h, const int32_t* edges, int64_t E, int optimizer, double lr,
+                 int iterations, int workers, int minibatch, int eval_batch, uint64_t seed,
+                 int sampler_mode, int use_threads, double* stats_out, double* eval_out,
+                 double* theta_out, double* first_grad_out) {
+  ORACLE_TRY
+  std::vector<Edge> e((size_t)E);
+  for (int64_t t = 0; t < E; ++t) e[t] = {edges[2 * t], edges[2 * t + 1]};
+  validate_edges(n, e);
+  auto local_of = [&](const Made&, const Sample& s) {
+    return local_energy_maxcut(n, e, s.X.data(), (int)s.log_psi.size());
+  };
+  auto eval_of = [&](const Made& m, std::mt19937_64& rng) {
+    return evaluate(n, e, m, eval_batch, rng, sampler_mode == 1);
+  };
+  train_core(n, h, local_of, eval_of, optimizer, lr, iterations, workers, minibatch, seed, sampler_mode,
+             use_threads, stats_out, eval_out, theta_out, first_grad_out);
+  ORACLE_CATCH
+}
+
+// The same training run on a general Ising spec (TIM): local energies with the off-diagonal
+// branch (estimator.hpp:43-90); eval_out = {energy, std, 0, 0} (no cut, trainer.cpp:91-108).
+int oracle_train_spec(int n, int h, const double* alpha, const double* beta, const int32_t* pi,
+                      const int32_t* pj, const double* pv, int64_t np, int optimizer, double lr, int iterations,
+                      int workers, int minibatch, int eval_batch, uint64_t seed, int sampler_mode, int use_threads,
+                      double* stats_out, double* eval_out, double* theta_out, double* first_grad_out) {
+  ORACLE_TRY
+  const Spec sp = spec_from(n, alpha, beta, pi, pj, pv, np);
+  auto local_of = [&](const Made& m, const Sample& s) {
+    return local_energy_batch(sp, m, s.X.data(), (int)s.log_psi.size(), s.log_psi.data());
+  };
+  auto eval_of = [&](const Made& m, std::mt19937_64& rng) {
+    const Sample s = sampler_mode == 1 ? auto_sample_incremental(m, eval_batch, &rng, nullptr, nullptr)
+                                       : auto_sample(m, eval_batch, &rng, nullptr, nullptr);
+    const auto l = local_energy_batch(sp, m, s.X.data(), eval_batch, s.log_psi.data());
+    const auto mv = energy_and_variance(l);
+    return EvalOut{mv.first, std::sqrt(mv.second), 0.0, 0.0};
+  };
+  train_core(n, h, local_of, eval_of, optimizer, lr, iterations, workers, minibatch, seed, sampler_mode,
+             use_threads, stats_out, eval_out, theta_out, first_grad_out);
+  ORACLE_CATCH
+}
+
+// random_tim (hamiltonian.cpp:126-142): alpha[n], beta[n], and the n(n-1)/2 pairs in row-major order.
+int oracle_random_tim(int n, uint64_t seed, double* alpha, double* beta, int32_t* pi, int32_t* pj, double* pv) {
+  ORACLE_TRY
+  const Spec s = random_tim(n, seed);
+  std::copy(s.alpha.begin(), s.alpha.end(), alpha);
+  std::copy(s.beta.begin(), s.beta.end(), beta);
+  for (size_t t = 0; t < s.pairs.size(); ++t) {
+    pi[t] = s.pairs[t].i;
+    pj[t] = s.pairs[t].j;
+    pv[t] = s.pairs[t].v;
+  }
+  ORACLE_CATCH
+}
+
+// diagonal_energy (hamiltonian.cpp:61-69) of B configurations.
+int oracle_diagonal_energy(int n, const double* alpha, const double* beta, const int32_t* pi, const int32_t* pj,
+                           const double* pv, int64_t np, int B, const uint8_t* x, double* out) {
+  ORACLE_TRY
+  const Spec sp = spec_from(n, alpha, beta, pi, pj, pv, np);
+  const auto X = to_double(x, (size_t)B * n);
+  for (int b = 0; b < B; ++b) out[b] = diagonal_energy(sp, X.data() + (size_t)b * n);
+  ORACLE_CATCH
+}
+
+// local_energy_batch (estimator.hpp:43-90) of B configurations with the caller's cached log psi.
+int oracle_local_energy_spec(int n, int h, const int* deg, const double* theta, const double* alpha,
+                             const double* beta, const int32_t* pi, const int32_t* pj, const double* pv, int64_t np,
+                             int B, const uint8_t* x, const double* cached_log_psi, double* out) {
+  ORACLE_TRY
+  const Spec sp = spec_from(n, alpha, beta, pi, pj, pv, np);
+  const Made m = made_from(n, h, deg, theta);
+  const auto X = to_double(x, (size_t)B * n);
+  const auto l = local_energy_batch(sp, m, X.data(), B, cached_log_psi);
+  std::copy(l.begin(), l.end(), out);
   ORACLE_CATCH
 }
 
