@@ -2,7 +2,7 @@
 NVCC ?= /usr/local/cuda/bin/nvcc
 ARCH := -gencode arch=compute_100a,code=sm_100a
 NVFLAGS := $(ARCH) -O3 -lineinfo -std=c++17 -Xcompiler -fPIC -Iinclude -Xptxas -v
-SRC := paper_2106_13308_b200/csrc/kernels.cu paper_2106_13308_b200/csrc/head.cu paper_2106_13308_b200/csrc/gemm.cu paper_2106_13308_b200/csrc/capi.cu paper_2106_13308_b200/csrc/sr.cu paper_2106_13308_b200/csrc/energy_dense.cu
+SRC := paper_2106_13308_b200/csrc/kernels.cu paper_2106_13308_b200/csrc/head.cu paper_2106_13308_b200/csrc/gemm.cu paper_2106_13308_b200/csrc/capi.cu paper_2106_13308_b200/csrc/sr.cu paper_2106_13308_b200/csrc/energy_dense.cu paper_2106_13308_b200/csrc/spec.cu
 HOSTSRC := paper_2106_13308_b200/csrc/host.cpp
 HDRS := $(wildcard paper_2106_13308_b200/csrc/*.cuh) include/vqmc_b200.h Makefile
 LIB := paper_2106_13308_b200/lib/libvqmc_b200.so

@@ -1,5 +1,5 @@
 /*
- * vqmc_b200.h — C ABI of the B200-native VQMC Max-Cut training step.
+ * vqmc_b200.h — C ABI of the B200-native VQMC training step (Max-Cut; general Ising / TIM specs).
  *
  * Drop-in boundary for the reference's C++ free-function API
  * (arxiv/paper_2106_13308, /root/reference/proj).  The reference has no FFI;
@@ -94,6 +94,24 @@ int vqmc_gpu_log_psi(vqmc_gpu_t* g, const uint32_t* bits, int B, double* log_psi
  * cut_value (hamiltonian.cpp:121-124).  Either output may be NULL. */
 int vqmc_gpu_maxcut_energy(vqmc_gpu_t* g, const uint32_t* bits, int B, int32_t* cut_out,
                            double* local_out);
+
+/* HamiltonianSpec (hamiltonian.hpp:34-44; validate hamiltonian.cpp:36-54): a general Ising
+ * problem H = -sum_i (alpha_i X_i + beta_i Z_i) - sum_{i<j} beta_ij Z_i Z_j on the handle's n
+ * spins (the TIM instances of random_tim / load_spec).  alpha, beta: n entries (alpha >= 0);
+ * pairs: num_pairs (i, j, value), 0-based, i < j, no duplicates.  While a spec is set,
+ * vqmc_gpu_local_energy, vqmc_gpu_evaluate and vqmc_gpu_train_step use its local energy (with the
+ * off-diagonal branch); vqmc_gpu_clear_spec returns to the handle's Max-Cut instance. */
+int vqmc_gpu_set_spec(vqmc_gpu_t* g, const double* alpha, const double* beta, const int32_t* pair_i,
+                      const int32_t* pair_j, const double* pair_value, int64_t num_pairs);
+int vqmc_gpu_clear_spec(vqmc_gpu_t* g);
+
+/* local_energy_batch (estimator.hpp:43-90): l_b = H_xx - sum_{k: alpha_k > 0} alpha_k
+ * exp(log psi(x_b ^ e_k) - cached_log_psi_b) (exponents shifted by their maximum when it exceeds
+ * 50).  cached_log_psi: B entries (SampleBatch::log_psi), or NULL for the model's own log psi of
+ * the configurations.  Without a spec: the Max-Cut diagonal branch.  VQMC_ERR_NUMERIC on a
+ * non-finite result. */
+int vqmc_gpu_local_energy(vqmc_gpu_t* g, const uint32_t* bits, int B, const double* cached_log_psi,
+                          double* local_out);
 
 /* weighted_grad_log_psi (models.cpp:175-198): sum_b w_b grad log psi(x_b),
  * reference flatten order, d entries. */
@@ -215,6 +233,15 @@ int vqmc_random_regular_graph(int n, int d, uint64_t seed, int32_t* edges_out, i
                               int64_t* num_edges);
 int vqmc_erdos_renyi_graph(int n, double p, uint64_t seed, int32_t* edges_out, int64_t cap,
                            int64_t* num_edges);
+/* random_tim (hamiltonian.cpp:126-142): alpha, beta n entries; pairs n(n-1)/2 (row-major i < j). */
+int vqmc_random_tim(int n, uint64_t seed, double* alpha, double* beta, int32_t* pair_i, int32_t* pair_j,
+                    double* pair_value);
+/* load_spec / save_spec "tim" text format (hamiltonian.cpp:162-234); load with alpha == NULL first
+ * to get *n_out and *num_pairs. */
+int vqmc_load_spec(const char* path, int* n_out, double* alpha, double* beta, int32_t* pair_i,
+                   int32_t* pair_j, double* pair_value, int64_t cap, int64_t* num_pairs);
+int vqmc_save_spec(const char* path, int n, const double* alpha, const double* beta, const int32_t* pair_i,
+                   const int32_t* pair_j, const double* pair_value, int64_t num_pairs);
 /* load_graph / save_graph text format (hamiltonian.cpp:236-266). */
 int vqmc_load_graph(const char* path, int* n_out, int32_t* edges_out, int64_t cap,
                     int64_t* num_edges);

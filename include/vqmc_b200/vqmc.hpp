@@ -1,7 +1,8 @@
 // vqmc_b200/vqmc.hpp — header-only C++ facade with the reference's API names
 // (namespace vqmc, proj/include/vqmc/*.hpp) over the C ABI of libvqmc_b200.so.
 //
-// Scope: the north-star path (Max-Cut, MADE, AUTO sampler, ADAM).  Eigen is not available,
+// Scope: the north-star path (Max-Cut, MADE, AUTO sampler, ADAM / SGD + SR), general Ising (TIM)
+// specs, and one host thread per GPU for multi-GPU training.  Eigen is not available,
 // so Vector is std::vector<double> and ConfigBatch a small row-major 0/1 matrix; names,
 // argument meaning, default values and exception types follow the reference:
 // std::invalid_argument for usage errors, std::runtime_error for numerical / device errors.
@@ -18,6 +19,7 @@
 #include <memory>
 #include <optional>
 #include <random>
+#include <thread>
 #include <sstream>
 #include <stdexcept>
 #include <string>
@@ -143,6 +145,84 @@ inline MaxCutProblem maxcut_spec(const Graph& g) {  // hamiltonian.cpp:109-119 (
   return MaxCutProblem{g, g.edges.size()};
 }
 
+/// One ZZ coupling term, 0-based, i < j (hamiltonian.hpp:26-31).
+struct PairCoupling {
+  int i;
+  int j;
+  double value;
+};
+/// H = -sum_i (alpha_i X_i + beta_i Z_i) - sum_{i<j} beta_ij Z_i Z_j (hamiltonian.hpp:34-44).
+struct HamiltonianSpec {
+  int n = 0;
+  Vector alpha, beta;
+  std::vector<PairCoupling> pairs;
+  void validate() const {  // hamiltonian.cpp:36-54
+    if (n < 1) throw std::invalid_argument("spec requires n >= 1");
+    if ((int)alpha.size() != n || (int)beta.size() != n)
+      throw std::invalid_argument("alpha/beta length does not match n");
+    for (double a : alpha)
+      if (a < 0.0) throw std::invalid_argument("alpha must be non-negative");
+    std::vector<std::pair<int, int>> s;
+    for (const auto& p : pairs) {
+      if (p.i < 0 || p.j >= n || p.i >= p.j) throw std::invalid_argument("pair indices must satisfy 0 <= i < j < n");
+      s.emplace_back(p.i, p.j);
+    }
+    std::sort(s.begin(), s.end());
+    if (std::adjacent_find(s.begin(), s.end()) != s.end()) throw std::invalid_argument("duplicate pair");
+  }
+};
+
+namespace detail {
+struct SpecArrays {
+  std::vector<int32_t> pi, pj;
+  Vector pv;
+};
+inline SpecArrays arrays(const HamiltonianSpec& s) {
+  SpecArrays a;
+  for (const auto& p : s.pairs) {
+    a.pi.push_back(p.i);
+    a.pj.push_back(p.j);
+    a.pv.push_back(p.value);
+  }
+  return a;
+}
+inline HamiltonianSpec from_arrays(int n, Vector alpha, Vector beta, const std::vector<int32_t>& pi,
+                                   const std::vector<int32_t>& pj, const Vector& pv) {
+  HamiltonianSpec s;
+  s.n = n;
+  s.alpha = std::move(alpha);
+  s.beta = std::move(beta);
+  s.pairs.reserve(pi.size());
+  for (size_t t = 0; t < pi.size(); ++t) s.pairs.push_back({pi[t], pj[t], pv[t]});
+  return s;
+}
+}  // namespace detail
+
+inline HamiltonianSpec random_tim(int n, uint64_t seed) {  // hamiltonian.cpp:126-142
+  if (n < 1) throw std::invalid_argument("random_tim requires n >= 1");
+  const size_t np = (size_t)n * (n - 1) / 2;
+  Vector a((size_t)n), b((size_t)n), pv(np);
+  std::vector<int32_t> pi(np), pj(np);
+  check(vqmc_random_tim(n, seed, a.data(), b.data(), pi.data(), pj.data(), pv.data()));
+  return detail::from_arrays(n, std::move(a), std::move(b), pi, pj, pv);
+}
+inline HamiltonianSpec load_spec(const std::string& path) {  // hamiltonian.cpp:204-234
+  int n = 0;
+  int64_t np = 0;
+  check(vqmc_load_spec(path.c_str(), &n, nullptr, nullptr, nullptr, nullptr, nullptr, 0, &np));
+  Vector a((size_t)n), b((size_t)n), pv((size_t)np);
+  std::vector<int32_t> pi((size_t)np), pj((size_t)np);
+  check(vqmc_load_spec(path.c_str(), &n, a.data(), b.data(), pi.data(), pj.data(), pv.data(), np, &np));
+  HamiltonianSpec s = detail::from_arrays(n, std::move(a), std::move(b), pi, pj, pv);
+  s.validate();
+  return s;
+}
+inline void save_spec(const HamiltonianSpec& s, const std::string& path) {  // hamiltonian.cpp:162-177
+  const auto a = detail::arrays(s);
+  check(vqmc_save_spec(path.c_str(), s.n, s.alpha.data(), s.beta.data(), a.pi.data(), a.pj.data(), a.pv.data(),
+                       (int64_t)s.pairs.size()));
+}
+
 // ---- L2 model (models.hpp) --------------------------------------------------------
 class GpuReplica;
 
@@ -194,11 +274,22 @@ class GpuReplica {
     }
   }
   void set_problem(const MaxCutProblem& p) {
+    if (spec_set_) {
+      check(vqmc_gpu_clear_spec(h_));
+      spec_set_ = false;
+    }
     const auto e = detail::flat(p.graph);
     if (e != edges_) {
       check(vqmc_gpu_set_edges(h_, e.data(), (int64_t)p.graph.edges.size()));
       edges_ = e;
     }
+  }
+  void set_problem(const HamiltonianSpec& s) {
+    if (s.n != n_) throw std::invalid_argument("spec n does not match the model");
+    const auto a = detail::arrays(s);
+    check(vqmc_gpu_set_spec(h_, s.alpha.data(), s.beta.data(), a.pi.data(), a.pj.data(), a.pv.data(),
+                            (int64_t)s.pairs.size()));
+    spec_set_ = true;
   }
   Vector params(int d) const {
     Vector t((size_t)d);
@@ -212,6 +303,7 @@ class GpuReplica {
   int n_;
   Vector theta_;
   std::vector<int32_t> edges_;
+  bool spec_set_ = false;
 };
 
 inline GpuReplica& replica(const MadeModel& m) {
@@ -282,6 +374,19 @@ inline Vector local_energy_batch(const MaxCutProblem& p, const MadeModel& m, con
     if (!std::isfinite(v)) throw std::runtime_error("non-finite local energy (amplitude underflow?)");
   return out;
 }
+/// local_energy_batch (estimator.hpp:43-90) on a general spec: the diagonal plus the flipped-
+/// neighbour terms, with the sampler's cached log psi (empty: the model's own).
+inline Vector local_energy_batch(const HamiltonianSpec& s, const MadeModel& m, const ConfigBatch& c,
+                                 const Vector& cached_log_psi = {}) {
+  if (c.cols() != s.n) throw std::invalid_argument("configuration width does not match spec n");
+  auto& r = replica(m);
+  r.set_problem(s);
+  const auto bits = c.packed();
+  Vector out((size_t)c.rows());
+  check(vqmc_gpu_local_energy(r.get(), bits.data(), c.rows(), cached_log_psi.empty() ? nullptr : cached_log_psi.data(),
+                              out.data()));
+  return out;
+}
 inline std::pair<double, double> energy_and_variance(const Vector& l) {  // estimator.hpp:94-100
   if (l.size() < 2) throw std::invalid_argument("variance needs at least two samples");
   double s = 0.0;
@@ -349,8 +454,9 @@ struct SrConfig {  // optimizer.hpp:38-45
   bool centered = true;
 };
 
-struct RunConfig {  // the Max-Cut / MADE / AUTO / {ADAM, SGD + SR} slice of trainer.hpp:31-58
-  std::optional<MaxCutProblem> maxcut;
+struct RunConfig {  // the MADE / AUTO / {ADAM, SGD + SR} slice of trainer.hpp:31-58
+  std::optional<MaxCutProblem> maxcut;  // Max-Cut instance (exact cut path; best / mean cut reported)
+  std::optional<HamiltonianSpec> spec;  // otherwise a general spec (TIM), ADAM
   int hidden = 0;
   OptimizerKind optimizer = OptimizerKind::kAdam;
   SrConfig sr;
@@ -362,7 +468,9 @@ struct RunConfig {  // the Max-Cut / MADE / AUTO / {ADAM, SGD + SR} slice of tra
   uint64_t seed = 0;
   std::optional<double> target;
   bool reference_streams = false;  // true: the reference's mt19937_64 uniforms (bit parity), else Philox
-  int device = 0;
+  int device = 0;                  // first GPU
+  int gpus = 1;  // GPUs (devices device .. device + gpus - 1), one host thread and NCCL rank each;
+                 // the `workers` reference workers are split evenly over them (trainer.cpp:284-287)
 };
 
 struct PhaseTimings {
@@ -388,30 +496,51 @@ inline double resolve_lr(const RunConfig& c) {  // trainer.cpp:35-46
   return c.lr > 0.0 ? c.lr : (c.optimizer == OptimizerKind::kAdam ? 0.01 : 0.1);
 }
 
-/// train (trainer.cpp:111-322) for MADE + AUTO + ADAM or SGD + SR on a Max-Cut instance: one fused
-/// device step per iteration; `workers` reference workers are segments of the device batch.
-inline RunResult train(const RunConfig& cfg) {
-  if (!cfg.maxcut) throw std::invalid_argument("the B200 path trains Max-Cut instances");
-  if (cfg.workers < 1) throw std::invalid_argument("workers must be >= 1");
-  if (cfg.iterations < 1) throw std::invalid_argument("iterations must be >= 1");
-  if (cfg.minibatch < 2) throw std::invalid_argument("minibatch must be >= 2");
+namespace detail {
+/// Which reference workers a GPU rank plays (trainer.cpp:121-127): rank r of G runs workers
+/// r * L / G .. (r + 1) * L / G - 1 as segments of its batch; worker w draws from
+/// make_stream(seed, w + 1), so the rank's first stream is 1 + r * L / G.
+struct RankPlan {
+  int rank = 0, gpus = 1, workers = 1, device = 0;
+  uint64_t stream0 = 1;
+};
+inline RankPlan rank_plan(const RunConfig& cfg, int rank) {
+  if (cfg.gpus < 1) throw std::invalid_argument("gpus must be >= 1");
+  if (cfg.workers % cfg.gpus != 0) throw std::invalid_argument("workers must be a multiple of gpus");
+  RankPlan p;
+  p.rank = rank;
+  p.gpus = cfg.gpus;
+  p.workers = cfg.workers / cfg.gpus;
+  p.device = cfg.device + rank;
+  p.stream0 = 1 + (uint64_t)rank * (uint64_t)p.workers;
+  return p;
+}
+
+/// One rank's training loop (worker_body, trainer.cpp:150-282): with a communicator every step
+/// all-reduces the gradient and the energy statistics, so each rank sees the pooled StepStats
+/// and applies the same update (replicas stay identical).
+inline RunResult train_rank(const RunConfig& cfg, const RankPlan& plan, const uint8_t* uid) {
   const auto run0 = std::chrono::steady_clock::now();
-  const int n = cfg.maxcut->graph.n;
+  const bool maxcut = cfg.maxcut.has_value();
+  const int n = maxcut ? cfg.maxcut->graph.n : cfg.spec->n;
   const int h = cfg.hidden > 0 ? cfg.hidden : default_made_hidden(n);
   MadeModel model = made_init(n, h, cfg.seed);  // trainer.cpp:318
+  model.replica = std::make_shared<GpuReplica>(model, plan.device);
   auto& r = replica(model);
-  r.set_problem(*cfg.maxcut);
+  if (maxcut) r.set_problem(*cfg.maxcut);
+  else r.set_problem(*cfg.spec);
+  if (plan.gpus > 1) check(vqmc_gpu_comm_init(r.get(), uid, plan.gpus, plan.rank));
   check(vqmc_gpu_adam_reset(r.get()));
   const double lr = resolve_lr(cfg);
-  const int L = cfg.workers, mbs = cfg.minibatch;
+  const int L = plan.workers, mbs = cfg.minibatch;
   std::vector<std::mt19937_64> rngs;
-  for (int w = 0; w < L; ++w) rngs.push_back(make_stream(cfg.seed, w + 1));
+  for (int w = 0; w < L; ++w) rngs.push_back(make_stream(cfg.seed, plan.stream0 + w));
   auto eval_rng = make_stream(cfg.seed, kEvalStream);
   std::uniform_real_distribution<double> unit(0.0, 1.0);
   RunResult res;
   double acc_time = 0.0;
   uint64_t eval_calls = 0;
-  auto evaluate = [&](double out[4]) {  // trainer.cpp:91-108
+  auto evaluate = [&](double out[4]) {  // trainer.cpp:91-108 (every rank: identical replicas and stream)
     if (cfg.reference_streams) {
       std::vector<double> u((size_t)n * cfg.eval_batch);
       for (double& v : u) v = unit(eval_rng);
@@ -429,18 +558,18 @@ inline RunResult train(const RunConfig& cfg) {
       for (int w = 0; w < L; ++w)
         for (int i = 0; i < n; ++i)
           for (int b = 0; b < mbs; ++b) u[(size_t)i * L * mbs + (size_t)w * mbs + b] = unit(rngs[w]);
-      // (the reference draws worker w's [bit][sample] block sequentially from its own stream)
       up = u.data();
     }
     vqmc_step_stats_t st{};
     if (cfg.optimizer == OptimizerKind::kSgdSr) {  // trainer.cpp:165-168, 189-199, 223-225
       int cg_it = 0;
       double cg_res = 0.0;
-      check(vqmc_gpu_train_step_sr(r.get(), mbs, L, up, cfg.seed, 1, (uint64_t)it, lr, cfg.sr.lambda, cfg.sr.tol,
-                                   cfg.sr.max_iterations, cfg.sr.fallback ? 1 : 0, cfg.sr.centered ? 1 : 0, &st,
-                                   &cg_it, &cg_res));
+      check(vqmc_gpu_train_step_sr(r.get(), mbs, L, up, cfg.seed, plan.stream0, (uint64_t)it, lr, cfg.sr.lambda,
+                                   cfg.sr.tol, cfg.sr.max_iterations, cfg.sr.fallback ? 1 : 0,
+                                   cfg.sr.centered ? 1 : 0, &st, &cg_it, &cg_res));
     } else {
-      check(vqmc_gpu_train_step(r.get(), mbs, L, up, cfg.seed, 1, (uint64_t)it, lr, 0.9, 0.999, 1e-8, it + 1, &st));
+      check(vqmc_gpu_train_step(r.get(), mbs, L, up, cfg.seed, plan.stream0, (uint64_t)it, lr, 0.9, 0.999, 1e-8,
+                                it + 1, &st));
     }
     StepStats s;
     s.energy_mean = st.energy_mean;
@@ -449,10 +578,10 @@ inline RunResult train(const RunConfig& cfg) {
     s.wall_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
     acc_time += s.wall_time;
     res.stats.push_back(s);
-    if (cfg.target) {
+    if (cfg.target) {  // trainer.cpp:265-273
       double ev[4];
       evaluate(ev);
-      if (ev[2] >= *cfg.target) {
+      if (maxcut ? ev[2] >= *cfg.target : ev[0] <= *cfg.target) {
         res.hit_time = acc_time;
         res.hit_iteration = it + 1;
         break;
@@ -463,13 +592,60 @@ inline RunResult train(const RunConfig& cfg) {
   evaluate(ev);
   res.final_energy = ev[0];
   res.final_energy_std = ev[1];
-  res.best_cut = ev[2];
-  res.mean_cut = ev[3];
+  if (maxcut) {
+    res.best_cut = ev[2];
+    res.mean_cut = ev[3];
+  }
   model.theta = r.params(model.param_count());
   r.mark_device_updated(model.theta);
   res.final_params = model.theta;
   res.made = model;
   res.total_time = std::chrono::duration<double>(std::chrono::steady_clock::now() - run0).count();
+  return res;
+}
+}  // namespace detail
+
+/// train (trainer.cpp:111-322) for MADE + AUTO + ADAM or SGD + SR on a Max-Cut instance, or ADAM on
+/// a general spec: one fused device step per iteration.  gpus = G > 1 runs one host thread per GPU
+/// (the reference's worker threads, trainer.cpp:284-287), each an NCCL rank playing workers / G of
+/// the reference workers; replicas_identical compares the ranks' final parameters bitwise.
+inline RunResult train(const RunConfig& cfg) {
+  if (!cfg.maxcut && !cfg.spec) throw std::invalid_argument("a Max-Cut instance or a Hamiltonian spec is required");
+  if (!cfg.maxcut) {
+    cfg.spec->validate();
+    if (cfg.optimizer != OptimizerKind::kAdam)
+      throw std::invalid_argument("general (TIM) specs train with ADAM on the B200 path");
+  }
+  if (cfg.workers < 1) throw std::invalid_argument("workers must be >= 1");
+  if (cfg.iterations < 1) throw std::invalid_argument("iterations must be >= 1");
+  if (cfg.minibatch < 2) throw std::invalid_argument("minibatch must be >= 2");
+  if (cfg.gpus == 1) return detail::train_rank(cfg, detail::rank_plan(cfg, 0), nullptr);
+  std::vector<detail::RankPlan> plans;
+  for (int g = 0; g < cfg.gpus; ++g) plans.push_back(detail::rank_plan(cfg, g));
+  int visible = 0;
+  check(vqmc_gpu_device_count(&visible));
+  if (cfg.device + cfg.gpus > visible)
+    throw std::invalid_argument("gpus: " + std::to_string(cfg.gpus) + " devices from " + std::to_string(cfg.device) +
+                                " requested, " + std::to_string(visible) + " visible");
+  uint8_t uid[128];
+  check(vqmc_gpu_comm_unique_id(uid));
+  std::vector<RunResult> rs((size_t)cfg.gpus);
+  std::vector<std::exception_ptr> errs((size_t)cfg.gpus);
+  std::vector<std::thread> threads;
+  for (int g = 0; g < cfg.gpus; ++g)
+    threads.emplace_back([&, g] {
+      try {
+        rs[(size_t)g] = detail::train_rank(cfg, plans[(size_t)g], uid);
+      } catch (...) {
+        errs[(size_t)g] = std::current_exception();
+      }
+    });
+  for (auto& t : threads) t.join();
+  for (auto& e : errs)
+    if (e) std::rethrow_exception(e);
+  RunResult res = std::move(rs[0]);
+  for (int g = 1; g < cfg.gpus; ++g)
+    if (rs[(size_t)g].final_params != res.final_params) res.replicas_identical = false;
   return res;
 }
 

@@ -40,6 +40,9 @@ _SIGS = {
     "vqmc_gpu_sample": [_vp, C.c_int, _vp, _u64, _u64, _u64, _vp, _vp],
     "vqmc_gpu_log_psi": [_vp, _vp, C.c_int, _vp, _vp],
     "vqmc_gpu_maxcut_energy": [_vp, _vp, C.c_int, _vp, _vp],
+    "vqmc_gpu_set_spec": [_vp, _vp, _vp, _vp, _vp, _vp, _i64],
+    "vqmc_gpu_clear_spec": [_vp],
+    "vqmc_gpu_local_energy": [_vp, _vp, C.c_int, _vp, _vp],
     "vqmc_gpu_weighted_grad": [_vp, _vp, _vp, C.c_int, _vp],
     "vqmc_gpu_gradient_from_locals": [_vp, _vp, _vp, C.c_int, _vp],
     "vqmc_gpu_adam_step": [_vp, _vp, _dbl, _dbl, _dbl, _dbl, _i64],
@@ -69,6 +72,9 @@ _SIGS = {
     "vqmc_random_maxcut_graph": [C.c_int, _u64, _vp, _i64, C.POINTER(_i64)],
     "vqmc_random_regular_graph": [C.c_int, C.c_int, _u64, _vp, _i64, C.POINTER(_i64)],
     "vqmc_erdos_renyi_graph": [C.c_int, C.c_double, _u64, _vp, _i64, C.POINTER(_i64)],
+    "vqmc_random_tim": [C.c_int, _u64, _vp, _vp, _vp, _vp, _vp],
+    "vqmc_load_spec": [C.c_char_p, C.POINTER(C.c_int), _vp, _vp, _vp, _vp, _vp, _i64, C.POINTER(_i64)],
+    "vqmc_save_spec": [C.c_char_p, C.c_int, _vp, _vp, _vp, _vp, _vp, _i64],
     "vqmc_load_graph": [C.c_char_p, C.POINTER(C.c_int), _vp, _i64, C.POINTER(_i64)],
     "vqmc_save_graph": [C.c_char_p, C.c_int, _vp, _i64],
 }

@@ -133,6 +133,79 @@ def maxcut_spec(g: Graph) -> MaxCutProblem:  # hamiltonian.cpp:109-119 (validate
     return MaxCutProblem(Graph(g.n, e), len(e))
 
 
+@dataclasses.dataclass
+class HamiltonianSpec:
+    """HamiltonianSpec (hamiltonian.hpp:34-44): H = -sum_i (alpha_i X_i + beta_i Z_i)
+    - sum_{i<j} beta_ij Z_i Z_j; pairs as three arrays (pair_i < pair_j, 0-based, value)."""
+    n: int
+    alpha: np.ndarray
+    beta: np.ndarray
+    pair_i: np.ndarray
+    pair_j: np.ndarray
+    pair_value: np.ndarray
+
+    def __post_init__(self):
+        self.alpha = np.ascontiguousarray(self.alpha, np.float64)
+        self.beta = np.ascontiguousarray(self.beta, np.float64)
+        self.pair_i = np.ascontiguousarray(self.pair_i, np.int32)
+        self.pair_j = np.ascontiguousarray(self.pair_j, np.int32)
+        self.pair_value = np.ascontiguousarray(self.pair_value, np.float64)
+
+    def validate(self) -> None:  # hamiltonian.cpp:36-54
+        if self.n < 1:
+            raise ValueError("spec requires n >= 1")
+        if self.alpha.shape != (self.n,) or self.beta.shape != (self.n,):
+            raise ValueError("alpha/beta length does not match n")
+        if np.any(self.alpha < 0.0):
+            raise ValueError("alpha must be non-negative")
+        if len(self.pair_i):
+            if (np.any(self.pair_i < 0) or np.any(self.pair_j >= self.n) or np.any(self.pair_i >= self.pair_j)):
+                raise ValueError("pair indices must satisfy 0 <= i < j < n")
+            if len(np.unique(self.pair_i.astype(np.int64) * self.n + self.pair_j)) != len(self.pair_i):
+                raise ValueError("duplicate pair")
+
+
+def random_tim(n: int, seed: int) -> HamiltonianSpec:  # hamiltonian.cpp:126-142
+    if n < 1:
+        raise ValueError("random_tim requires n >= 1")
+    npairs = n * (n - 1) // 2
+    a, b = np.empty(n), np.empty(n)
+    pi, pj, pv = np.empty(npairs, np.int32), np.empty(npairs, np.int32), np.empty(npairs)
+    check(K.lib.vqmc_random_tim(n, seed, ptr(a), ptr(b), ptr(pi), ptr(pj), ptr(pv)))
+    return HamiltonianSpec(n, a, b, pi, pj, pv)
+
+
+def load_spec(path: str) -> HamiltonianSpec:  # hamiltonian.cpp:204-234
+    n, npairs = C.c_int(), C.c_int64()
+    check(K.lib.vqmc_load_spec(path.encode(), C.byref(n), None, None, None, None, None, 0, C.byref(npairs)))
+    a, b = np.empty(n.value), np.empty(n.value)
+    pi, pj, pv = (np.empty(npairs.value, np.int32), np.empty(npairs.value, np.int32), np.empty(npairs.value))
+    check(K.lib.vqmc_load_spec(path.encode(), C.byref(n), ptr(a), ptr(b), ptr(pi), ptr(pj), ptr(pv), npairs.value,
+                               C.byref(npairs)))
+    spec = HamiltonianSpec(n.value, a, b, pi, pj, pv)
+    spec.validate()
+    return spec
+
+
+def save_spec(spec: HamiltonianSpec, path: str) -> None:  # hamiltonian.cpp:162-177
+    check(K.lib.vqmc_save_spec(path.encode(), spec.n, ptr(spec.alpha), ptr(spec.beta), ptr(spec.pair_i),
+                               ptr(spec.pair_j), ptr(spec.pair_value), len(spec.pair_i)))
+
+
+def diagonal_energy(spec: HamiltonianSpec, x) -> float:
+    """H_xx (hamiltonian.cpp:61-69) of one configuration (host, fp64, the reference's order)."""
+    x = np.asarray(x, np.float64).reshape(-1)
+    if x.shape != (spec.n,):
+        raise ValueError(f"configuration length {x.size} does not match spec n = {spec.n}")
+    s = 1.0 - 2.0 * x
+    e = 0.0
+    for i in range(spec.n):
+        e -= spec.beta[i] * s[i]
+    for i, j, v in zip(spec.pair_i, spec.pair_j, spec.pair_value):
+        e -= v * s[i] * s[j]
+    return e
+
+
 # ---------------------------------------------------------------------------
 # L2 model (models.hpp)
 # ---------------------------------------------------------------------------
@@ -201,10 +274,18 @@ class DeviceReplica:
             self.version = self.model._version
             self.device_newer = False
 
-    def set_problem(self, problem: MaxCutProblem) -> None:
+    def set_problem(self, problem) -> None:
+        """A MaxCutProblem (edges; the exact integer-cut path) or a HamiltonianSpec (TIM)."""
         if self.problem_id is not problem:
-            e = np.ascontiguousarray(problem.graph.edges, np.int32)
-            check(K.lib.vqmc_gpu_set_edges(self.h, ptr(e), len(e)))
+            if isinstance(problem, HamiltonianSpec):
+                if problem.n != self.model.n:
+                    raise ValueError("spec n does not match the model")
+                check(K.lib.vqmc_gpu_set_spec(self.h, ptr(problem.alpha), ptr(problem.beta), ptr(problem.pair_i),
+                                              ptr(problem.pair_j), ptr(problem.pair_value), len(problem.pair_i)))
+            else:
+                check(K.lib.vqmc_gpu_clear_spec(self.h))
+                e = np.ascontiguousarray(problem.graph.edges, np.int32)
+                check(K.lib.vqmc_gpu_set_edges(self.h, ptr(e), len(e)))
             self.problem_id = problem
 
     def get_params(self) -> np.ndarray:
@@ -319,12 +400,21 @@ def forward_pass_count(kind: str, n: int, batch_size: int) -> int:  # sampler.cp
 # ---------------------------------------------------------------------------
 # L4 estimator (estimator.hpp)
 # ---------------------------------------------------------------------------
-def local_energy_batch(problem: MaxCutProblem, model: MadeModel, configs, cached_log_psi=None) -> np.ndarray:
-    """Max-Cut (diagonal) branch of local_energy_batch (estimator.hpp:43-57)."""
+def local_energy_batch(problem, model: MadeModel, configs, cached_log_psi=None) -> np.ndarray:
+    """local_energy_batch (estimator.hpp:43-90).  MaxCutProblem: the diagonal branch (exact
+    integer cuts).  HamiltonianSpec: the diagonal plus the flipped-neighbour terms
+    -alpha_k exp(log psi(x ^ e_k) - cached_log_psi) (cached_log_psi: SampleBatch::log_psi; None =
+    the model's own log psi of the configurations)."""
     bits, B = _bits(model, configs)
     dev = model.device()
     dev.set_problem(problem)
     out = np.empty(B)
+    if isinstance(problem, HamiltonianSpec):
+        c = None if cached_log_psi is None else np.ascontiguousarray(cached_log_psi, np.float64)
+        if c is not None and c.shape != (B,):
+            raise ValueError("cached log psi length does not match the batch")
+        check(K.lib.vqmc_gpu_local_energy(dev.h, ptr(bits), B, ptr(c), ptr(out)))
+        return out
     check(K.lib.vqmc_gpu_maxcut_energy(dev.h, ptr(bits), B, None, ptr(out)))
     if not np.all(np.isfinite(out)):
         raise RuntimeError("non-finite local energy (amplitude underflow?)")
@@ -479,8 +569,10 @@ class StepStats:
 
 @dataclasses.dataclass
 class RunConfig:
-    """The Max-Cut / MADE / AUTO / {ADAM, SGD + SR} slice of RunConfig (trainer.hpp:31-58)."""
-    problem: Optional[MaxCutProblem] = None
+    """The MADE / AUTO / {ADAM, SGD + SR} slice of RunConfig (trainer.hpp:31-58).  `problem` is the
+    reference's `maxcut` (a MaxCutProblem: exact cut path, best/mean cut reported) or its `spec`
+    (a HamiltonianSpec, e.g. random_tim: local energies with the off-diagonal branch)."""
+    problem: Optional[object] = None
     hidden: int = 0
     optimizer: str = "adam"
     lr: float = 0.0
@@ -536,7 +628,11 @@ def train(cfg: RunConfig, comm=None) -> RunResult:
     cut statistics), and the returned StepStats are pooled over all world*L*minibatch samples,
     like the reference's (trainer.cpp:246-256)."""
     if cfg.problem is None:
-        raise ValueError("a Max-Cut problem is required")
+        raise ValueError("a problem (MaxCutProblem or HamiltonianSpec) is required")
+    if isinstance(cfg.problem, HamiltonianSpec):
+        cfg.problem.validate()
+        if cfg.optimizer != "adam":
+            raise ValueError("general (TIM) specs train with ADAM on the B200 path")
     if cfg.workers < 1:
         raise ValueError("workers must be >= 1")
     if cfg.iterations < 1:
@@ -545,7 +641,7 @@ def train(cfg: RunConfig, comm=None) -> RunResult:
         raise ValueError("minibatch must be >= 2")
     if cfg.optimizer not in ("adam", "sgd_sr"):
         raise ValueError("the B200 path implements the ADAM and SGD + SR optimizers")
-    n = cfg.problem.graph.n
+    n = cfg.problem.n if isinstance(cfg.problem, HamiltonianSpec) else cfg.problem.graph.n
     h = cfg.hidden if cfg.hidden > 0 else default_made_hidden(n)
     model = made_init(n, h, cfg.seed)
     lr = resolve_lr(cfg)
@@ -586,11 +682,14 @@ def train(cfg: RunConfig, comm=None) -> RunResult:
         acc_time += wall
         if cfg.target is not None:
             ev = evaluate(cfg, model, eval_stream)
-            if ev[2] >= cfg.target:
+            hit = ev[0] <= cfg.target if isinstance(cfg.problem, HamiltonianSpec) else ev[2] >= cfg.target
+            if hit:  # trainer.cpp:265-273
                 result.hit_time, result.hit_iteration = acc_time, it + 1
                 break
     ev = evaluate(cfg, model, eval_stream)
     result.final_energy, result.final_energy_std, result.best_cut, result.mean_cut = ev
+    if isinstance(cfg.problem, HamiltonianSpec):  # no cut (trainer.cpp:296-299 only for maxcut)
+        result.best_cut = result.mean_cut = None
     result.final_params = model.parameters().copy()
     result.total_time = time.perf_counter() - t_run
     result.made = model

@@ -255,11 +255,18 @@ struct DeviceGuard {
 // Sticky device flag: a logit of the fp16-pair GEMMs was not finite (operand overflow).  The
 // reference computes in fp64 and would not overflow here, so fail loudly (runtime_error, like
 // the reference's non-finite local-energy check, estimator.hpp:85-87) instead of drawing junk.
+// Bit 1: a general spec's local energy was not finite (estimator.hpp:85-87).
 static void check_flag(Handle* H, uint32_t v) {
   if (!v) return;
   VQMC_CUDA(cudaMemsetAsync(H->d_flag, 0, sizeof(uint32_t), H->stream));
   H->next_call = ~0ull;  // (the device step counters are re-seeded from the caller's next call)
-  throw NumericError("non-finite logit in the tail sampler (fp16 operand range exceeded)");
+  if (v & 1u) throw NumericError("non-finite logit in the tail sampler (fp16 operand range exceeded)");
+  throw NumericError("non-finite local energy (amplitude underflow?)");
+}
+static void sync_check_flag(Handle* H) {
+  VQMC_CUDA(cudaMemcpyAsync(H->h_scal + 8, H->d_flag, sizeof(uint32_t), cudaMemcpyDeviceToHost, H->stream));
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  check_flag(H, *reinterpret_cast<const uint32_t*>(H->h_scal + 8));
 }
 
 // Side stream of the concurrent backward / gradient all-reduce (high priority) and its events.
@@ -314,12 +321,10 @@ static void sample_into(Handle* H, int B, int workers, const double* uniforms_ho
   if (want_log_psi) launch_finalize_logpsi(H, B, H->tail_tiles);  // the training step never reads log psi
 }
 
-// Forward from configurations already in H->X.
+// Forward from configurations already in H->X (models.cpp:51-70): layer 1 and the tcgen05
+// layer-2 GEMM with the given-bits epilogue (spec.cu), log psi into H->log_psi.
 static void forward_given(Handle* H, int B, double* cond) {
-  RngSpec none{0, 0, 0, 1, nullptr};
-  launch_head_v2(H, B, nullptr, none, true, cond);
-  launch_z2(H, B, H->L.Hd, nullptr, none, true, cond);
-  launch_finalize_logpsi(H, B, H->tail_tiles);
+  forward_plain(H, B, cond, nullptr, nullptr, nullptr, H->log_psi);
 }
 
 // The step's host-visible results live in one device block (read back with one copy):
@@ -648,6 +653,8 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   if (H->ev_dg1) cudaEventDestroy(H->ev_dg1);
   free_sr(H);
   free_dense_energy(H);
+  spec_free(H);
+  if (H->d_lstat) cudaFree(H->d_lstat);
   if (H->d_edges_bank) cudaFree(H->d_edges_bank);
   void* ptrs[] = {H->P, H->G, H->Mo, H->Vo, H->W1Tp, H->W2cp, H->W2h, H->W2l, H->d_deg, H->d_comp_k,
                   H->d_comp_off, H->d_edges, H->X, H->G1, H->G1h, H->G1l, H->wG1h, H->wG1l, H->Dh, H->Dl,
@@ -761,6 +768,48 @@ int vqmc_gpu_maxcut_energy(vqmc_gpu_t* g, const uint32_t* bits, int B, int32_t* 
   if (cut_out) std::memcpy(cut_out, cuts.data(), (size_t)B * sizeof(int32_t));
   if (local_out)  // l_b = (|E| - 2 cut_b) / 4 (exact in fp64), as the device statistics use it
     for (int b = 0; b < B; ++b) local_out[b] = 0.25 * ((double)H->num_edges - 2.0 * (double)cuts[b]);
+  API_CATCH
+}
+
+int vqmc_gpu_set_spec(vqmc_gpu_t* g, const double* alpha, const double* beta, const int32_t* pair_i,
+                      const int32_t* pair_j, const double* pair_value, int64_t num_pairs) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  spec_set(H, alpha, beta, pair_i, pair_j, pair_value, num_pairs);
+  API_CATCH
+}
+
+int vqmc_gpu_clear_spec(vqmc_gpu_t* g) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  spec_free(H);
+  H->invalidate_graph();
+  API_CATCH
+}
+
+int vqmc_gpu_local_energy(vqmc_gpu_t* g, const uint32_t* bits, int B, const double* cached_log_psi,
+                          double* local_out) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  DeviceGuard dg(H->device);
+  check_B(B);
+  if (!H->spec) return vqmc_gpu_maxcut_energy(g, bits, B, nullptr, local_out);  // the diagonal branch
+  H->ensure_batch(B);
+  upload_bits(H, bits, B);
+  const double* dc = nullptr;
+  if (cached_log_psi) {
+    double* c = spec_cached_buffer(H, B);
+    VQMC_CUDA(cudaMemcpyAsync(c, cached_log_psi, (size_t)B * sizeof(double), cudaMemcpyHostToDevice, H->stream));
+    dc = c;
+  }
+  double* dl = spec_local_buffer(H, B);
+  launch_spec_local(H, B, dc, dl);
+  if (local_out)
+    VQMC_CUDA(cudaMemcpyAsync(local_out, dl, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+  sync_check_flag(H);
   API_CATCH
 }
 
@@ -949,6 +998,35 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
   if (t0) record_event(H, H->ev[5]);
 }
 
+// The same iteration on a general spec (TIM): the sampler keeps log psi (the cached value of the
+// off-diagonal ratios, trainer.cpp:157-162), fp64 local energies with the flipped-neighbour
+// branch (spec.cu), weights from them, the serial backward, the gradient all-reduce plus a small
+// fp64 one of the energy sums, and Adam (skipped when the step's flag is set).
+static void enqueue_train_step_spec(Handle* H, int minibatch, int workers, const double* uniforms, uint64_t seed,
+                                    uint64_t stream0) {
+  const int B = minibatch * workers;
+  H->kt_count = 0;
+  const bool tm = H->phase_timing >= 2, t0 = H->phase_timing >= 1;
+  if (t0) record_event(H, H->ev[0]);
+  sample_into(H, B, workers, uniforms, seed, stream0, 0, /*device_call=*/true, /*want_log_psi=*/true);
+  if (tm) record_event(H, H->ev[1]);
+  double* dl = spec_local_buffer(H, B);
+  launch_spec_local(H, B, H->log_psi, dl);                                 // local_energy_batch (:161)
+  launch_weights_from_locals(H, B, minibatch, true, dl, H->d_lstat);      // gradient_from_locals (:164)
+  if (tm) record_event(H, H->ev[2]);
+  launch_backward(H, B, /*wg1_done=*/true);
+  if (tm) record_event(H, H->ev[3]);
+  if (H->nccl_comm) {
+    nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)H->L.total, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
+               "ncclAllReduce");
+    nccl_check(g_nccl.AllReduce(H->d_lstat, H->d_lstat, 2, ncclFloat64, ncclSum, H->nccl_comm, H->stream),
+               "ncclAllReduce (energy sums)");
+  }
+  if (tm) record_event(H, H->ev[4]);
+  launch_adam(H, 1.0f / (float)(workers * H->nranks), /*gated=*/true);
+  if (t0) record_event(H, H->ev[5]);
+}
+
 }  // namespace vqmc_b200
 
 extern "C" {
@@ -979,6 +1057,32 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
     H->cur_b1 = beta1;
     H->cur_b2 = beta2;
     H->cur_eps = eps;
+  }
+  if (H->spec) {  // general spec (TIM): eager, no captured graph
+    if (2 + 2 * workers > H->lstat_cap) {
+      if (H->d_lstat) VQMC_CUDA(cudaFree(H->d_lstat));
+      H->d_lstat = nullptr;
+      VQMC_CUDA(cudaMalloc((void**)&H->d_lstat, (size_t)(2 + 2 * workers) * sizeof(double)));
+      H->lstat_cap = 2 + 2 * workers;
+    }
+    enqueue_train_step_spec(H, minibatch, workers, uniforms, seed, stream0);
+    H->next_call = call + 1;
+    H->next_t = t + 1;
+    if (stats_out) {
+      read_step_results(H, workers);
+      double ls[2];
+      VQMC_CUDA(cudaMemcpy(ls, H->d_lstat, sizeof(ls), cudaMemcpyDeviceToHost));
+      const double N = (double)B * H->nranks;
+      const double mean = ls[0] / N;
+      stats_out->energy_mean = mean;
+      stats_out->energy_var = N > 1 ? std::max(0.0, (ls[1] - N * mean * mean) / (N - 1)) : 0.0;
+      stats_out->grad_norm = std::sqrt(H->h_scal[0]);
+      stats_out->cut_sum = 0;
+      stats_out->cut_sq_sum = 0;
+      stats_out->best_cut = 0;
+      stats_out->batch = (int32_t)N;
+    }
+    return VQMC_OK;
   }
   const bool graphable = H->graph_enabled && uniforms == nullptr;
   Handle::GraphKey key;
@@ -1191,6 +1295,23 @@ int vqmc_gpu_evaluate(vqmc_gpu_t* g, int B, const double* uniforms, uint64_t see
   if (B < 2) throw std::invalid_argument("variance needs at least two samples");
   check_stats_batch(B);
   sample_into(H, B, 1, uniforms, seed, stream, call);
+  if (H->spec) {  // general spec: energy and std of the fp64 local energies; no cut (trainer.cpp:91-108)
+    double* dl = spec_local_buffer(H, B);
+    launch_spec_local(H, B, H->log_psi, dl);
+    std::vector<double> l((size_t)B);
+    VQMC_CUDA(cudaMemcpyAsync(l.data(), dl, (size_t)B * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+    sync_check_flag(H);
+    double sum = 0.0;
+    for (double v : l) sum += v;
+    const double mean = sum / (double)B;
+    double ss = 0.0;
+    for (double v : l) ss += (v - mean) * (v - mean);
+    out[0] = mean;
+    out[1] = std::sqrt(ss / (double)(B - 1));
+    out[2] = 0.0;
+    out[3] = 0.0;
+    return VQMC_OK;
+  }
   launch_energy(H, B);
   launch_weights_from_locals(H, B, B);
   VQMC_CUDA(cudaMemcpyAsync(H->h_istat, H->d_istat, 3 * sizeof(int64_t), cudaMemcpyDeviceToHost, H->stream));

@@ -463,6 +463,103 @@ struct SpDotEpi {
   }
 };
 
+// Forward of GIVEN configurations (made_forward + bernoulli_log_likelihood, models.cpp:51-70):
+// rows = samples, columns = every output i (the layer-1 activations [G1 | 1] come from
+// z1_given_kernel, so no sampling chain is involved).  Per output: the clamped conditional, the
+// log term of the given bit (fp32, 32 per fp64 add), D = 0.5 (x - p_raw) as an fp16 pair (the
+// backward's operand) and optionally p, log p_i(x_i) and log p_i(1 - x_i) - log p_i(x_i).
+//
+// NBR: the rows are single-site-flipped neighbours (estimator.hpp:64-72): row r is sample
+// b0 + r % Bc with bit sites[r / Bc] flipped; only outputs i >= that site are summed (the earlier
+// conditionals and terms are the unflipped sample's), and nothing but the log-prob partials is
+// written.
+template <bool NBR>
+struct GivenEpiT {
+  int rows, n, np, W;
+  const uint32_t* X;
+  __half* Dh;  // [B][np] (!NBR; nullptr: not written)
+  __half* Dl;
+  double* lp_part;  // [kParts * tiles_n][rows]
+  double* cond;     // [B][n] clamped p (optional, !NBR)
+  float* lterm;     // [B][n] log p_i(x_i) (optional, !NBR)
+  float* fterm;     // [B][n] log p_i(1 - x_i) - log p_i(x_i) (optional, !NBR)
+  uint32_t* flag;   // non-finite logit (fp16 operand overflow)
+  int Bc, b0;       // NBR row map
+  const int32_t* sites;
+  int part;
+  UmmaTile tile;
+  double lps;
+  int rb, rk;
+  static constexpr int kParts = Umma2Cfg<kTailBN>::kEpiSets;
+  __device__ void init() {}
+  __device__ void begin_row(int r, const UmmaArgs&) {
+    lps = 0.0;
+    rb = r;
+    rk = 0;
+    if (NBR && r < rows) {
+      rb = b0 + r % Bc;
+      rk = sites[r / Bc];
+    }
+  }
+  __device__ void chunk(int r, int cb, const float (&v)[32], const UmmaArgs&) {
+    if (r >= rows) return;
+    if (NBR && cb + 32 <= rk) return;  // every output of the chunk precedes the flipped site
+    uint32_t word = X[(size_t)rb * W + (cb >> 5)];
+    if (NBR && (rk >> 5) == (cb >> 5)) word ^= 1u << (rk & 31);
+    const size_t rowe = (size_t)rb * n, rowD = (size_t)rb * np;
+    float lsum = 0.f;
+    bool bad = false;
+#pragma unroll
+    for (int jh = 0; jh < 32; jh += 16) {
+      uint32_t dh[8], dl[8];
+#pragma unroll
+      for (int j = jh; j < jh + 16; j += 2) {
+        float d[2];
+#pragma unroll
+        for (int t = 0; t < 2; ++t) {
+          const int c = cb + j + t;
+          const bool valid = c < n && (!NBR || c >= rk);
+          const float z = v[j + t];
+          bad |= !(fabsf(z) < INFINITY);
+          const int x = (word >> (j + t)) & 1;
+          const UnitPre q = unit_pre(z);
+          const Unit u = unit_post(q, x);
+          if (valid) lsum += u.logt;
+          d[t] = valid ? u.D : 0.f;
+          if (!NBR && valid) {
+            if (cond) cond[rowe + c] = u.p;
+            if (lterm) lterm[rowe + c] = u.logt;
+            if (fterm) fterm[rowe + c] = unit_post(q, 1 - x).logt - u.logt;
+          }
+        }
+        if (!NBR) ptx::split_f16x2(d[0], d[1], dh[(j - jh) / 2], dl[(j - jh) / 2]);
+      }
+      if (!NBR && Dh) {
+        if (cb + 32 <= n) {
+          uint4* ph = reinterpret_cast<uint4*>(Dh + rowD + cb + jh);
+          uint4* pl = reinterpret_cast<uint4*>(Dl + rowD + cb + jh);
+          ph[0] = make_uint4(dh[0], dh[1], dh[2], dh[3]);
+          ph[1] = make_uint4(dh[4], dh[5], dh[6], dh[7]);
+          pl[0] = make_uint4(dl[0], dl[1], dl[2], dl[3]);
+          pl[1] = make_uint4(dl[4], dl[5], dl[6], dl[7]);
+        } else {
+          const __half* hh = reinterpret_cast<const __half*>(dh);
+          const __half* hl = reinterpret_cast<const __half*>(dl);
+          for (int t = 0; t < 16 && cb + jh + t < n; ++t) {
+            Dh[rowD + cb + jh + t] = hh[t];
+            Dl[rowD + cb + jh + t] = hl[t];
+          }
+        }
+      }
+    }
+    if (bad) atomicOr(flag, 1u);
+    lps += (double)lsum;
+  }
+  __device__ void end_row(int r, const UmmaArgs&) {
+    if (r < rows) lp_part[(size_t)(kParts * tile.tn + part) * rows + r] = lps;
+  }
+};
+
 // ===========================================================================
 // Helper kernels: 16-bit pairs of operands
 // ===========================================================================
@@ -607,6 +704,42 @@ int launch_sp_umma(Handle* H, int B) {
   launch_umma2<BN, false, false, SpDotEpi, false, kElemF16>(H, "sr_sp_umma", ah, al, bh, bl, B, L.n, K, 1, e,
                                                            H->stream);
   return SpDotEpi::kParts * ((L.n + BN - 1) / BN);
+}
+
+// Forward of the configurations in H->X over every output (after z1_given_kernel wrote [G1 | 1]):
+// log-prob partials into lp_part (H->tail_tiles of them per row), D pairs, optional p / log terms.
+void launch_given_umma(Handle* H, int B, double* cond, float* lterm, float* fterm) {
+  const Layout& L = H->L;
+  constexpr int BN = kTailBN;
+  const int K = L.h + 1;
+  const CUtensorMap ah = tmap_kmajor(H->G1h, K, B, H->hp18, kUmmaBM, kElemF16);
+  const CUtensorMap al = tmap_kmajor(H->G1l, K, B, H->hp18, kUmmaBM, kElemF16);
+  const CUtensorMap bh = tmap_kmajor(H->W2h, K, L.n, H->hp18, BN / 2, kElemF16);
+  const CUtensorMap bl = tmap_kmajor(H->W2l, K, L.n, H->hp18, BN / 2, kElemF16);
+  GivenEpiT<false> e{B,     L.n,  H->np8, L.W,     H->X,  H->Dh,   H->Dl,   H->lp_part, cond, lterm,
+                     fterm, H->d_flag, 0,   0,       nullptr, 0,     {},      0.0,        0,    0};
+  H->tail_tiles = GivenEpiT<false>::kParts * ((L.n + BN - 1) / BN);
+  launch_umma2<BN, false, false, GivenEpiT<false>, false, kElemF16>(H, "z2_given_umma", ah, al, bh, bl, B, L.n, K,
+                                                                    1, e, H->stream);
+}
+
+// Flipped-neighbour forward (TIM local energy): `rows` = Bc samples x sites rows of [G1' | 1] in
+// Nh / Nl; per row the fp64 partials of sum_{i >= site} log p_i(x'_i) into part
+// [kParts * tiles][rows]; returns the partial count per row.
+int launch_nbr_umma(Handle* H, int rows, int Bc, int b0, const int32_t* sites, const __half* Nh, const __half* Nl,
+                    double* part) {
+  const Layout& L = H->L;
+  constexpr int BN = kTailBN;
+  const int K = L.h + 1;
+  const CUtensorMap ah = tmap_kmajor(Nh, K, rows, H->hp18, kUmmaBM, kElemF16);
+  const CUtensorMap al = tmap_kmajor(Nl, K, rows, H->hp18, kUmmaBM, kElemF16);
+  const CUtensorMap bh = tmap_kmajor(H->W2h, K, L.n, H->hp18, BN / 2, kElemF16);
+  const CUtensorMap bl = tmap_kmajor(H->W2l, K, L.n, H->hp18, BN / 2, kElemF16);
+  GivenEpiT<true> e{rows, L.n, H->np8, L.W, H->X, nullptr, nullptr, part, nullptr, nullptr,
+                    nullptr, H->d_flag, Bc, b0, sites, 0, {}, 0.0, 0, 0};
+  launch_umma2<BN, false, false, GivenEpiT<true>, false, kElemF16>(H, "tim_nbr_umma", ah, al, bh, bl, rows, L.n, K, 1,
+                                                                   e, H->stream);
+  return GivenEpiT<true>::kParts * ((L.n + BN - 1) / BN);
 }
 
 // gW1T[j][k] = sum_b X[b][j] dz1[b][k] (j < Hd) and gb1[k] (the ones column j = Hd):

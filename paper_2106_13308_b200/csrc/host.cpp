@@ -1,5 +1,5 @@
 // Host utilities of the B200 VQMC library (no GPU needed): RNG streams, MADE
-// initialisation, graph generators and the graph text format.  These are the
+// initialisation, graph / TIM generators and the instance text formats.  These are the
 // product's own C++ implementations of the reference's host-side functions
 // (cited per function); tests check them against the independent oracle.
 #include <cmath>
@@ -210,6 +210,95 @@ int vqmc_save_graph(const char* path, int n, const int32_t* edges, int64_t ne) {
   if (!out) throw std::runtime_error(std::string("cannot open ") + path + " for writing");
   out << "graph " << n << "\n";
   for (int64_t t = 0; t < ne; ++t) out << "edge " << (edges[2 * t] + 1) << " " << (edges[2 * t + 1] + 1) << "\n";
+  HOST_CATCH
+}
+
+// random_tim (hamiltonian.cpp:126-142): alpha_i ~ U[0,1) for every site, then beta_i ~ U[-1,1),
+// then the n(n-1)/2 pairs (row-major i < j) ~ U[-1,1), all from make_stream(seed).
+int vqmc_random_tim(int n, uint64_t seed, double* alpha, double* beta, int32_t* pair_i, int32_t* pair_j,
+                    double* pair_value) {
+  HOST_TRY
+  if (n < 1) throw std::invalid_argument("random_tim requires n >= 1");
+  auto rng = make_stream(seed, 0);
+  std::uniform_real_distribution<double> unit(0.0, 1.0);
+  std::uniform_real_distribution<double> symmetric(-1.0, 1.0);
+  for (int i = 0; i < n; ++i) alpha[i] = unit(rng);
+  for (int i = 0; i < n; ++i) beta[i] = symmetric(rng);
+  int64_t t = 0;
+  for (int i = 0; i < n; ++i)
+    for (int j = i + 1; j < n; ++j, ++t) {
+      pair_i[t] = i;
+      pair_j[t] = j;
+      pair_value[t] = symmetric(rng);
+    }
+  HOST_CATCH
+}
+
+// load_spec (hamiltonian.cpp:204-234): "tim <n>", then "alpha i v" / "beta i v" / "pair i j v"
+// (1-based; i < j).  Call with alpha == NULL to get *n_out and *num_pairs first.  Validation
+// (negative alpha, duplicate pairs) is HamiltonianSpec::validate's, done by vqmc_gpu_set_spec.
+int vqmc_load_spec(const char* path, int* n_out, double* alpha, double* beta, int32_t* pair_i, int32_t* pair_j,
+                   double* pair_value, int64_t cap, int64_t* num_pairs) {
+  HOST_TRY
+  const auto lines = read_lines(path);
+  const auto& header = lines.front();
+  const std::string p(path);
+  if (header.size() != 2 || header[0] != "tim") throw std::runtime_error(p + ": expected 'tim <n>' header");
+  const int n = std::stoi(header[1]);
+  if (n < 1) throw std::runtime_error(p + ": n must be >= 1");
+  auto parse = [&](const std::string& t) {
+    const int idx = std::stoi(t);
+    if (idx < 1 || idx > n) throw std::runtime_error(p + ": index out of range: " + t);
+    return idx - 1;
+  };
+  std::vector<double> a(n, 0.0), b(n, 0.0);
+  std::vector<int32_t> pi, pj;
+  std::vector<double> pv;
+  for (size_t k = 1; k < lines.size(); ++k) {
+    const auto& t = lines[k];
+    if (t[0] == "alpha" && t.size() == 3) {
+      a[parse(t[1])] = std::stod(t[2]);
+    } else if (t[0] == "beta" && t.size() == 3) {
+      b[parse(t[1])] = std::stod(t[2]);
+    } else if (t[0] == "pair" && t.size() == 4) {
+      const int i = parse(t[1]), j = parse(t[2]);
+      if (i >= j) throw std::runtime_error(p + ": pair indices must satisfy i < j");
+      pi.push_back(i);
+      pj.push_back(j);
+      pv.push_back(std::stod(t[3]));
+    } else {
+      throw std::runtime_error(p + ": malformed line starting with '" + t[0] + "'");
+    }
+  }
+  *n_out = n;
+  *num_pairs = (int64_t)pi.size();
+  if (alpha) {
+    if (cap < (int64_t)pi.size()) throw std::invalid_argument("pair buffer too small");
+    std::memcpy(alpha, a.data(), sizeof(double) * n);
+    std::memcpy(beta, b.data(), sizeof(double) * n);
+    for (size_t t = 0; t < pi.size(); ++t) {
+      pair_i[t] = pi[t];
+      pair_j[t] = pj[t];
+      pair_value[t] = pv[t];
+    }
+  }
+  HOST_CATCH
+}
+
+// save_spec (hamiltonian.cpp:162-177): zero fields are omitted, 17 significant digits.
+int vqmc_save_spec(const char* path, int n, const double* alpha, const double* beta, const int32_t* pair_i,
+                   const int32_t* pair_j, const double* pair_value, int64_t num_pairs) {
+  HOST_TRY
+  std::ofstream out(path);
+  if (!out) throw std::runtime_error(std::string("cannot open ") + path + " for writing");
+  out.precision(17);
+  out << "tim " << n << "\n";
+  for (int i = 0; i < n; ++i)
+    if (alpha[i] != 0.0) out << "alpha " << (i + 1) << " " << alpha[i] << "\n";
+  for (int i = 0; i < n; ++i)
+    if (beta[i] != 0.0) out << "beta " << (i + 1) << " " << beta[i] << "\n";
+  for (int64_t t = 0; t < num_pairs; ++t)
+    out << "pair " << (pair_i[t] + 1) << " " << (pair_j[t] + 1) << " " << pair_value[t] << "\n";
   HOST_CATCH
 }
 

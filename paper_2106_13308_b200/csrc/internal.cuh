@@ -83,6 +83,7 @@ struct Layout {
 
 struct Handle;
 struct RngSpec;
+struct SpecState;  // general Ising spec (TIM) and its scratch (spec.cu)
 // Timing event on the handle's stream; inside a graph capture it becomes an external event
 // record node so replays still record (and can be timed).
 void record_event(Handle* h, cudaEvent_t ev);
@@ -127,7 +128,10 @@ bool dense_energy_preferred(int n, int64_t num_edges);
 void setup_dense_energy(Handle* h);  // after the edge list is uploaded
 void free_dense_energy(Handle* h);
 void launch_energy_dense(Handle* h, int B);
-void launch_weights_from_locals(Handle* h, int B, int seg, bool with_wg1 = false);
+// lin: fp64 local energies of a general spec (else the Max-Cut cuts of the energy kernel); lstat:
+// [sum l, sum l^2, then per segment] (general spec only)
+void launch_weights_from_locals(Handle* h, int B, int seg, bool with_wg1 = false, const double* lin = nullptr,
+                                double* lstat = nullptr);
 void launch_cuts_reduce(Handle* h, int B);
 void launch_backward(Handle* h, int B, bool wg1_done = false);
 void launch_backward_tail(Handle* h, int B);  // dg1, dz1, gW1 (+ finalize)
@@ -149,6 +153,15 @@ void launch_sr_grad_from_G(Handle* h, double scale);
 void launch_sr_apply(Handle* h, double lr, const double* delta);
 bool sr_solve(Handle* h, int B, double lambda, double tol, int max_iterations, bool centered, int* iterations,
               double* residual, double* gnorm_out);
+// general Ising specs / plain forward (spec.cu)
+void spec_set(Handle* h, const double* alpha, const double* beta, const int32_t* pi, const int32_t* pj,
+              const double* pv, int64_t np);
+void spec_free(Handle* h);
+void forward_plain(Handle* h, int B, double* d_cond, float* d_lterm, float* d_fterm, float* d_z1, double* d_lp_out);
+void launch_spec_local(Handle* h, int B, const double* d_cached, double* d_local);
+double* spec_local_buffer(Handle* h, int B);
+double* spec_cached_buffer(Handle* h, int B);
+void launch_given_umma(Handle* h, int B, double* cond, float* lterm, float* fterm);
 void set_error(const std::string& msg);
 int status_of(const std::exception& ex);
 // hyper-parameters from h->d_step; gated: skip the update when the step's non-finite-logit flag is set
@@ -170,6 +183,9 @@ struct Handle {
   std::vector<int32_t> degrees;
   std::vector<double> theta_host;  // reference-order copy (masked / dead entries)
   int64_t num_edges = 0;
+  SpecState* spec = nullptr;  // general Ising spec (vqmc_gpu_set_spec): the local energy of TIM problems
+  double* d_lstat = nullptr;  // general spec: [sum l, sum l^2, per segment (sum l, sum l^2)] of the last step
+  int lstat_cap = 0;
 
   // model
   float* P = nullptr;      // live params [L.total]

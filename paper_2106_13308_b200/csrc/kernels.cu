@@ -1,9 +1,10 @@
 // VQMC step kernels for sm_100a: energy, statistics / REINFORCE weights, the backward's elementwise
-// passes and Adam (the GEMMs are tcgen05 kernels in gemm.cu, the head sampler is head.cu).
+// passes and Adam (the GEMMs are tcgen05 kernels in gemm.cu, the head sampler is head.cu, the plain
+// forward of given configurations and general-spec energies are spec.cu).
 //
 // Reference path (arxiv/paper_2106_13308, /root/reference/proj):
 //   auto_sample            proj/src/sampler.cpp:35-59      -> head_v2_kernel (head.cu) + tail GEMM (gemm.cu)
-//   made_forward           proj/src/models.cpp:51-62       -> head_v2_kernel(given) + z2_given_kernel
+//   made_forward           proj/src/models.cpp:51-62       -> z1_given_kernel + z2_given_umma (spec.cu, gemm.cu)
 //   local_energy_batch     proj/include/vqmc/estimator.hpp:43-57 -> energy_kernel
 //   energy_and_variance +
 //   gradient_from_locals   estimator.hpp:94-119            -> stats_weights_kernel
@@ -24,67 +25,6 @@
 #include "ptx.cuh"
 
 namespace vqmc_b200 {
-
-// ===========================================================================
-// z2 GEMM with the MADE output epilogue: Z[b][c] = G1[b] . W2m[c] + b2[c] for
-// columns c in [col0, n).  In the sampler (given == 0) these are the "tail"
-// outputs c >= Hd, all conditionally independent given the completed hidden
-// layer, so they are one dense GEMM; the epilogue draws x = [u < p], packs the
-// bits, and emits D and the per-tile log-prob partials.  given != 0 replays X
-// (made_forward from configurations).
-// ===========================================================================
-namespace z2cfg {
-constexpr int BM = 64, BN = 128, BK = 16, TM = 8, TN = 8;
-using T = SimtTile<BM, BN, BK, TM, TN>;
-}  // namespace z2cfg
-
-struct LoadG1 {  // A(m = sample, k = hidden) = G1[m][k]
-  static constexpr bool kMMajor = false;
-  const float* G1;
-  int B, h;
-  __device__ float operator()(int m, int k) const { return m < B ? G1[(size_t)m * h + k] : 0.f; }
-};
-struct LoadW2 {  // B(n = output, k = hidden) = W2m[n][k]
-  static constexpr bool kMMajor = false;
-  const float* W2;
-  int n, h;
-  __device__ float operator()(int c, int k) const { return c < n ? W2[(size_t)c * h + k] : 0.f; }
-};
-
-__global__ void __launch_bounds__(z2cfg::T::NT) z2_given_kernel(
-    int B, int n, int np, int h, int W, int colbase, int col0, const float* __restrict__ G1,
-    const float* __restrict__ W2, const float* __restrict__ b2, const uint32_t* __restrict__ X,
-    __half* __restrict__ Dh, __half* __restrict__ Dl, double* __restrict__ lp_part,
-    double* __restrict__ cond) {
-  using namespace z2cfg;
-  __shared__ __align__(16) float smem[BK * (BM + BN)];
-  const int m0 = blockIdx.y * BM;
-  const int n0 = colbase + blockIdx.x * BN;
-  float acc[TM][TN];
-  simt_mainloop<BM, BN, BK, TM, TN>(acc, m0, n0, 0, h, LoadG1{G1, B, h}, LoadW2{W2, n, h}, smem);
-  const int tid = threadIdx.x, tx = tid % T::NTX, ty = tid / T::NTX;
-#pragma unroll
-  for (int r = 0; r < TM; ++r) {
-    const int b = m0 + T::row(ty, r);
-    double lps = 0.0;
-    if (b < B) {
-#pragma unroll
-      for (int c = 0; c < TN; ++c) {
-        const int col = n0 + T::col(tx, c);
-        if (col < col0 || col >= n) continue;
-        const float z = acc[r][c] + b2[col];
-        const int x = (X[(size_t)b * W + (col >> 5)] >> (col & 31)) & 1;
-        const Unit u = unit_terms(z, x);
-        ptx::split_f16(u.D, Dh[(size_t)b * np + col], Dl[(size_t)b * np + col]);
-        lps += (double)u.logt;
-        if (cond) cond[(size_t)b * n + col] = u.p;
-      }
-    }
-#pragma unroll
-    for (int o = T::NTX / 2; o > 0; o >>= 1) lps += __shfl_xor_sync(kFull, lps, o);
-    if (tx == 0 && b < B) lp_part[(size_t)blockIdx.x * B + b] = lps;
-  }
-}
 
 // log_psi = (head + sum of tail partials) / 2, one warp per sample (fixed reduction order).
 __global__ void finalize_logpsi_kernel(int B, int tiles, const double* __restrict__ lp_head,
@@ -340,9 +280,10 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
                                                              int64_t* __restrict__ istat, int h, int ld,
                                                              const float* __restrict__ G1, __half* __restrict__ wgh,
                                                              __half* __restrict__ wgl, float* __restrict__ rstat,
-                                                             int nranks, int rank) {
+                                                             int nranks, int rank, const double* __restrict__ lin,
+                                                             double* __restrict__ lstat) {
   extern __shared__ float sw[];  // [B] weights of the whole batch (per CTA)
-  __shared__ double sd[32];
+  __shared__ double sd[32], sd2[32];
   __shared__ long long si[32], sq[32];
   __shared__ int sm[32];
   __shared__ float smax[32];
@@ -369,15 +310,21 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
   float wmax = 0.f;
   for (int sgi = 0; sgi < segs; ++sgi) {
     const int base = sgi * seg;
-    double s = 0.0;
+    double s = 0.0, s2 = 0.0;
     long long cs = 0, cq = 0;
     int cm = 0;
     for (int b = tid; b < seg; b += blockDim.x) {
       int c = 0;
-      for (int k = 0; k < chunks; ++k) c += cpart[(size_t)k * B + base + b];
-      const double lb = 0.25 * ((double)nE - 2.0 * (double)c);  // l_b = (|E| - 2 cut_b) / 4, exact
+      double lb;
+      if (lin) {  // general spec: fp64 local energies (estimator.hpp:43-90)
+        lb = lin[base + b];
+        s2 += lb * lb;
+      } else {
+        for (int k = 0; k < chunks; ++k) c += cpart[(size_t)k * B + base + b];
+        lb = 0.25 * ((double)nE - 2.0 * (double)c);  // l_b = (|E| - 2 cut_b) / 4, exact
+      }
       if (lead) {
-        cut[base + b] = c;
+        if (!lin) cut[base + b] = c;
         local[base + b] = lb;
       }
       s += lb;
@@ -388,30 +335,42 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
       s += __shfl_xor_sync(kFull, s, o);
+      s2 += __shfl_xor_sync(kFull, s2, o);
       cs += __shfl_xor_sync(kFull, cs, o);
       cq += __shfl_xor_sync(kFull, cq, o);
       cm = max(cm, __shfl_xor_sync(kFull, cm, o));
     }
-    if (lane == 0) { sd[warp] = s; si[warp] = cs; sq[warp] = cq; sm[warp] = cm; }
+    if (lane == 0) { sd[warp] = s; sd2[warp] = s2; si[warp] = cs; sq[warp] = cq; sm[warp] = cm; }
     __syncthreads();
     if (tid == 0) {
-      double t = 0.0;
+      double t = 0.0, t2 = 0.0;
       long long a = 0, q = 0;
       int mx = 0;
-      for (int i = 0; i < nw; ++i) { t += sd[i]; a += si[i]; q += sq[i]; mx = max(mx, sm[i]); }
+      for (int i = 0; i < nw; ++i) { t += sd[i]; t2 += sd2[i]; a += si[i]; q += sq[i]; mx = max(mx, sm[i]); }
       smean = t / (double)seg;
       if (lead) {
         istat[3 * sgi + 0] = a;
         istat[3 * sgi + 1] = q;
         istat[3 * sgi + 2] = mx;
+        if (lstat) {  // [0, 2): the rank's sums of l and l^2 (all-reduced across ranks); [2 + 2 s ...) per segment
+          lstat[2 + 2 * sgi] = t;
+          lstat[3 + 2 * sgi] = t2;
+          lstat[0] = (sgi ? lstat[0] : 0.0) + t;
+          lstat[1] = (sgi ? lstat[1] : 0.0) + t2;
+        }
       }
     }
     __syncthreads();
     const double mean = smean;
     for (int b = tid; b < seg; b += blockDim.x) {
-      int c = 0;
-      for (int k = 0; k < chunks; ++k) c += cpart[(size_t)k * B + base + b];
-      const double lb = 0.25 * ((double)nE - 2.0 * (double)c);
+      double lb;
+      if (lin) {
+        lb = lin[base + b];
+      } else {
+        int c = 0;
+        for (int k = 0; k < chunks; ++k) c += cpart[(size_t)k * B + base + b];
+        lb = 0.25 * ((double)nE - 2.0 * (double)c);
+      }
       const float wb = (float)(2.0 * (lb - mean) / (double)seg);
       sw[base + b] = wb;
       wmax = fmaxf(wmax, fabsf(wb));
@@ -752,22 +711,10 @@ void launch_params_refresh(Handle* H) {
 
 void launch_z2(Handle* H, int B, int col0, const double* uni, RngSpec rng, bool given, double* cond,
                bool want_lp) {
-  if (!given) {
-    launch_tail_umma(H, B, uni, rng, want_lp);
-    return;
-  }
-  const Layout& L = H->L;
-  const int colbase = (col0 / 32) * 32;
-  const int tiles = col0 >= L.n ? 0 : (L.n - colbase + z2cfg::BN - 1) / z2cfg::BN;
-  H->tail_tiles = tiles;
-  if (tiles == 0) return;
-  dim3 grid(tiles, (B + z2cfg::BM - 1) / z2cfg::BM);
-  KScope ks(H, "z2_given");
-  z2_given_kernel<<<grid, z2cfg::T::NT, 0, H->stream>>>(B, L.n, H->np8, L.h, L.W, colbase, col0, H->G1,
-                                                        H->P + L.off_w2, H->P + L.off_b2, H->X, H->Dh, H->Dl,
-                                                        H->lp_part, cond);
-  LAUNCH_CHECK();
-  H->launches++;
+  (void)col0;
+  (void)cond;
+  if (given) throw std::logic_error("launch_z2: given configurations go through forward_plain (spec.cu)");
+  launch_tail_umma(H, B, uni, rng, want_lp);
 }
 
 void launch_finalize_logpsi(Handle* H, int B, int tiles) {
@@ -833,7 +780,7 @@ void launch_cuts_reduce(Handle* H, int B) {
   H->launches++;
 }
 
-void launch_weights_from_locals(Handle* H, int B, int seg, bool with_wg1) {
+void launch_weights_from_locals(Handle* H, int B, int seg, bool with_wg1, const double* lin, double* lstat) {
   const Layout& L = H->L;
   const size_t smem = (size_t)B * sizeof(float);
   ensure_smem_attr((const void*)stats_weights_kernel, smem);
@@ -843,7 +790,7 @@ void launch_weights_from_locals(Handle* H, int B, int seg, bool with_wg1) {
   launch_k(H, stats_weights_kernel, dim3(grid), dim3(1024), smem, B / seg, seg, H->cut_chunks, H->num_edges,
            (const int32_t*)H->cpart, H->cut, H->local, H->w, H->d_wscale, H->d_istat, L.h, (int)H->hp18,
            (const float*)(with_wg1 ? H->G1 : nullptr), H->wG1h, H->wG1l,
-           (float*)(with_wg1 && H->nccl_comm ? H->G + L.total : nullptr), H->nranks, H->rank);
+           (float*)(with_wg1 && H->nccl_comm && !lin ? H->G + L.total : nullptr), H->nranks, H->rank, lin, lstat);
   LAUNCH_CHECK();
   H->launches++;
 }

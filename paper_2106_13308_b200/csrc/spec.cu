@@ -1,0 +1,516 @@
+// General Ising specs (the TIM branch of the reference) and the plain forward of given
+// configurations, for sm_100a.
+//
+//   H = -sum_i (alpha_i X_i + beta_i Z_i) - sum_{i<j} beta_ij Z_i Z_j      hamiltonian.hpp:26-44
+//   l(x) = H_xx - sum_{k: alpha_k > 0} alpha_k psi(x ^ e_k) / psi(x)        estimator.hpp:43-90
+//
+// The reference evaluates every flipped neighbour with a full forward pass (B s rows of n
+// conditionals, chunked).  Here the MADE structure does most of that work once:
+//   * a flip of bit k >= Hd (the largest hidden degree) changes no hidden unit, so
+//     log psi(x ^ e_k) - log psi(x) = (log p_k(1 - x_k) - log p_k(x_k)) / 2 comes from the base
+//     forward's logit of output k alone (fterm);
+//   * a flip of bit k < Hd changes z1 by +-W1m[:, k] (one rank-1 update of the base z1) and only
+//     the conditionals of outputs i >= k: the neighbour rows [relu(z1 +- W1m[:, k]) | 1] go through
+//     the tcgen05 pair GEMM with [W2m | b2] (launch_nbr_umma) whose epilogue sums
+//     log p_i(x'_i) for i >= k; the base's suffix sum of the same terms is subtracted.
+// The diagonal H_xx is an fp64 sum over the pair list on bit-sliced spins (32 samples per word).
+//
+// Plain forward (made_forward + log_prob, models.cpp:51-70, for log_psi / weighted_grad / SR /
+// TIM): z1_given_kernel writes [G1 | 1] (fp32 and the fp16 pair), the spins' bf16 operand of gW1
+// and optionally z1; launch_given_umma runs the layer-2 GEMM over every output with the
+// given-bits epilogue.  No sampling chain is involved.
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <algorithm>
+#include <cmath>
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "device_common.cuh"
+#include "internal.cuh"
+#include "ptx.cuh"
+
+namespace vqmc_b200 {
+
+#define SPEC_LAUNCH_CHECK() VQMC_CUDA(cudaGetLastError())
+
+int launch_nbr_umma(Handle* H, int rows, int Bc, int b0, const int32_t* sites, const __half* Nh, const __half* Nl,
+                    double* part);
+void launch_given_umma(Handle* H, int B, double* cond, float* lterm, float* fterm);
+
+template <class T>
+static void salloc(T** p, size_t count) {
+  if (*p) VQMC_CUDA(cudaFree(*p));
+  *p = nullptr;
+  if (count) VQMC_CUDA(cudaMalloc((void**)p, count * sizeof(T)));
+}
+template <class T>
+static void sfree(T*& p) {
+  if (p) cudaFree(p);
+  p = nullptr;
+}
+
+// ===========================================================================
+// Layer 1 of given configurations: z1[b][k] = b1[k] + sum_{j < Hd} x_bj W1T[j][k] (the live W1T
+// holds only inputs below the largest degree; masked entries are exact zeros).  kS samples per
+// CTA (spins staged as floats in shared memory), one thread per hidden unit.
+// ===========================================================================
+constexpr int kZ1S = 8;
+__global__ void __launch_bounds__(1024) z1_given_kernel(int B, int h, int Hd, int W, int hp, int hd1p,
+                                                        const uint32_t* __restrict__ X,
+                                                        const float* __restrict__ W1T, const float* __restrict__ b1,
+                                                        float* __restrict__ G1, __half* __restrict__ G1h,
+                                                        __half* __restrict__ G1l, __nv_bfloat16* __restrict__ Xf,
+                                                        float* __restrict__ Z1) {
+  __shared__ __align__(16) float xs[kZ1S][kMaxHidden];
+  const int b0 = blockIdx.x * kZ1S, tid = threadIdx.x;
+  const int Hd4 = (Hd + 3) & ~3;
+  for (int t = tid; t < kZ1S * Hd4; t += blockDim.x) {
+    const int s = t / Hd4, j = t % Hd4, b = b0 + s;
+    float x = 0.f;
+    if (b < B && j < Hd) {
+      x = (float)((X[(size_t)b * W + (j >> 5)] >> (j & 31)) & 1u);
+      Xf[(size_t)b * hd1p + j] = __float2bfloat16_rn(x);
+    }
+    xs[s][j] = x;
+    if (b < B && j == 0) Xf[(size_t)b * hd1p + Hd] = __float2bfloat16_rn(1.f);  // ones column: gb1
+  }
+  __syncthreads();
+  for (int k = tid; k < h; k += blockDim.x) {
+    float acc[kZ1S];
+    const float bk = b1[k];
+#pragma unroll
+    for (int s = 0; s < kZ1S; ++s) acc[s] = bk;
+    for (int j = 0; j < Hd4; j += 4) {
+      float w[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) w[u] = j + u < Hd ? W1T[(size_t)(j + u) * h + k] : 0.f;
+#pragma unroll
+      for (int s = 0; s < kZ1S; ++s) {
+        const float4 xv = *reinterpret_cast<const float4*>(&xs[s][j]);
+        acc[s] = fmaf(xv.x, w[0], acc[s]);
+        acc[s] = fmaf(xv.y, w[1], acc[s]);
+        acc[s] = fmaf(xv.z, w[2], acc[s]);
+        acc[s] = fmaf(xv.w, w[3], acc[s]);
+      }
+    }
+#pragma unroll
+    for (int s = 0; s < kZ1S; ++s) {
+      const int b = b0 + s;
+      if (b >= B) break;
+      const float g = fmaxf(acc[s], 0.f);
+      G1[(size_t)b * h + k] = g;
+      ptx::split_f16(g, G1h[(size_t)b * hp + k], G1l[(size_t)b * hp + k]);
+      if (Z1) Z1[(size_t)b * h + k] = acc[s];
+    }
+  }
+}
+
+// log_psi[b] = (lp_head[b] (optional) + sum of the row's partials) / 2
+__global__ void finalize_lp_kernel(int B, int tiles, const double* __restrict__ lp_part,
+                                   double* __restrict__ out) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  double s = 0.0;
+  for (int t = lane; t < tiles; t += 32) s += lp_part[(size_t)t * B + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
+  if (lane == 0) out[b] = 0.5 * s;  // log_psi_batch = log_prob / 2 (models.cpp:126-128)
+}
+
+// Forward of the configurations in H->X: [G1 | 1], D, log psi (into lp_out), optional p and
+// per-output log terms / flip deltas and z1.
+void forward_plain(Handle* H, int B, double* cond, float* lterm, float* fterm, float* Z1, double* lp_out) {
+  const Layout& L = H->L;
+  {
+    KScope ks(H, "z1_given");
+    const int threads = std::min(1024, (L.h + 31) & ~31);
+    z1_given_kernel<<<(B + kZ1S - 1) / kZ1S, threads, 0, H->stream>>>(
+        B, L.h, L.Hd, L.W, H->hp18, H->hd18, H->X, H->P + L.off_w1t, H->P + L.off_b1, H->G1, H->G1h, H->G1l, H->Xfb,
+        Z1);
+    SPEC_LAUNCH_CHECK();
+    H->launches++;
+  }
+  launch_given_umma(H, B, cond, lterm, fterm);
+  H->launches++;
+  {
+    KScope ks(H, "finalize_logpsi");
+    finalize_lp_kernel<<<(B + 7) / 8, 256, 0, H->stream>>>(B, H->tail_tiles, H->lp_part, lp_out);
+    SPEC_LAUNCH_CHECK();
+    H->launches++;
+  }
+}
+
+// ===========================================================================
+// Diagonal energy (hamiltonian.cpp:61-69): 32 samples per CTA as bit-sliced node words
+// T[i] (bit l = spin i of sample b0 + l, built with one ballot per node); warps split the CTA's
+// chunk of the pair list, every lane accumulates its sample in fp64:
+//   -beta_i s_i = x_i ? beta_i : -beta_i,   -v s_i s_j = (x_i ^ x_j) ? v : -v.
+// Partials per (pair chunk, sample); the combine kernel sums them in a fixed order.
+// ===========================================================================
+__global__ void __launch_bounds__(256) spec_diag_kernel(int B, int n, int W, int Wp, const uint32_t* __restrict__ X,
+                                                        const double* __restrict__ beta, int64_t np,
+                                                        int64_t per_chunk, const int32_t* __restrict__ pi,
+                                                        const int32_t* __restrict__ pj,
+                                                        const double* __restrict__ pv, double* __restrict__ dpart) {
+  extern __shared__ uint32_t sm[];
+  uint32_t* xs = sm;             // [32][Wp]
+  uint32_t* T = sm + 32 * Wp;    // [n]
+  __shared__ double red[8][32];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int b0 = blockIdx.x * 32;
+  for (int t = tid; t < 32 * W; t += blockDim.x) {
+    const int s = t / W, w = t % W;
+    xs[s * Wp + w] = b0 + s < B ? X[(size_t)(b0 + s) * W + w] : 0u;
+  }
+  __syncthreads();
+  for (int i = warp; i < n; i += 8) {
+    const uint32_t bit = (xs[lane * Wp + (i >> 5)] >> (i & 31)) & 1u;
+    const uint32_t word = __ballot_sync(kFull, bit);
+    if (lane == 0) T[i] = word;
+  }
+  __syncthreads();
+  double acc = 0.0;
+  if (blockIdx.y == 0)
+    for (int i = warp; i < n; i += 8) {
+      const double bi = beta[i];
+      acc += ((T[i] >> lane) & 1u) ? bi : -bi;
+    }
+  const int64_t p0 = (int64_t)blockIdx.y * per_chunk, p1 = min(np, p0 + per_chunk);
+  for (int64_t p = p0 + warp; p < p1; p += 8) {
+    const uint32_t w = T[pi[p]] ^ T[pj[p]];
+    const double v = pv[p];
+    acc += ((w >> lane) & 1u) ? v : -v;
+  }
+  red[warp][lane] = acc;
+  __syncthreads();
+  if (warp == 0) {
+    double s = 0.0;
+#pragma unroll
+    for (int k = 0; k < 8; ++k) s += red[k][lane];
+    if (b0 + lane < B) dpart[(size_t)blockIdx.y * B + b0 + lane] = s;
+  }
+}
+
+// ===========================================================================
+// Neighbour rows: row r = t * Bc + (b - b0), site k = sites[t] < Hd:
+//   [G1' | 1] = [relu(z1_b + (x_bk ? -1 : 1) W1T[k]) | 1]   (fp16 pair, row stride hp)
+// ===========================================================================
+__global__ void nbr_build_kernel(int rows, int Bc, int b0, int h, int hp, int W, const int32_t* __restrict__ sites,
+                                 const uint32_t* __restrict__ X, const float* __restrict__ Z1,
+                                 const float* __restrict__ W1T, __half* __restrict__ Nh, __half* __restrict__ Nl) {
+  const int64_t total = (int64_t)rows * hp;
+  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / hp), kk = (int)(e % hp);
+    const int t = r / Bc, b = b0 + r % Bc, k = sites[t];
+    float g = 0.f;
+    if (kk < h) {
+      const bool x = (X[(size_t)b * W + (k >> 5)] >> (k & 31)) & 1u;
+      const float wk = W1T[(size_t)k * h + kk];
+      g = fmaxf(Z1[(size_t)b * h + kk] + (x ? -wk : wk), 0.f);
+    } else if (kk == h) {
+      g = 1.f;
+    }
+    ptx::split_f16(g, Nh[e], Nl[e]);
+  }
+}
+
+// nb[t * B + b] = sum of the neighbour row's partials (fixed order)
+__global__ void nbr_reduce_kernel(int rows, int Bc, int b0, int B, int parts, const double* __restrict__ part,
+                                  double* __restrict__ nb) {
+  const int r = blockIdx.x * blockDim.x + threadIdx.x;
+  if (r >= rows) return;
+  double s = 0.0;
+  for (int p = 0; p < parts; ++p) s += part[(size_t)p * rows + r];
+  nb[(size_t)(r / Bc) * B + b0 + r % Bc] = s;
+}
+
+// ===========================================================================
+// Local energies (estimator.hpp:59-89), one warp per sample:
+//   d_k = log psi(x ^ e_k) - cached_b
+//       = (nb_k - sum_{i >= k} lterm_i) / 2 + (lpf_b - cached_b)    k < Hd
+//       = fterm_k / 2 + (lpf_b - cached_b)                           k >= Hd
+//   shift = max_k d_k if > 50 else 0;  l_b = H_xx - e^shift sum_k alpha_k e^(d_k - shift)
+// The suffix sums come from a running warp scan of lterm (fp64); pass 0 finds the shift,
+// pass 1 accumulates.
+// ===========================================================================
+__global__ void spec_local_kernel(int B, int n, int Hd, int S, const int32_t* __restrict__ site_of,
+                                  const double* __restrict__ alpha_s, int chunks, const double* __restrict__ dpart,
+                                  const float* __restrict__ lterm, const float* __restrict__ fterm,
+                                  const double* __restrict__ nb, const double* __restrict__ lpf,
+                                  const double* __restrict__ cached, double* __restrict__ local,
+                                  uint32_t* __restrict__ nonfinite) {
+  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (b >= B) return;
+  double diag = 0.0;
+  for (int c = lane; c < chunks; c += 32) diag += dpart[(size_t)c * B + b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) diag += __shfl_xor_sync(kFull, diag, o);
+  double acc = 0.0;
+  if (S > 0) {
+    const double corr = lpf[b] - cached[b];
+    const float* lt = lterm + (size_t)b * n;
+    const float* ft = fterm + (size_t)b * n;
+    // total of the base log terms (the suffix sums are total - prefix)
+    double tot = 0.0;
+    for (int i = lane; i < n; i += 32) tot += (double)lt[i];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
+    double shift = 0.0;
+    for (int pass = 0; pass < 2; ++pass) {
+      double mx = 0.0, sum = 0.0, prefix = 0.0;
+      for (int i0 = 0; i0 < n; i0 += 32) {
+        const int i = i0 + lane;
+        const int q = i < n ? site_of[i] : -1;
+        double d = 0.0;
+        if (i0 < Hd) {  // exclusive prefix of lterm over this chunk (only needed for head sites)
+          const double v = i < n ? (double)lt[i] : 0.0;
+          double incl = v;
+#pragma unroll
+          for (int o = 1; o < 32; o <<= 1) {
+            const double t = __shfl_up_sync(kFull, incl, o);
+            if (lane >= o) incl += t;
+          }
+          if (q >= 0 && i < Hd) d = 0.5 * (nb[(size_t)q * B + b] - (tot - (prefix + incl - v))) + corr;
+          prefix += __shfl_sync(kFull, incl, 31);
+        }
+        if (q >= 0 && i >= Hd) d = 0.5 * (double)ft[i] + corr;
+        if (q >= 0) {
+          if (pass == 0) mx = fmax(mx, d);
+          else sum -= alpha_s[q] * exp(d - shift);
+        }
+      }
+      if (pass == 0) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
+        shift = mx > 50.0 ? mx : 0.0;
+      } else {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
+        acc = sum;
+      }
+    }
+    acc *= exp(shift);
+  }
+  if (lane == 0) {
+    const double l = diag + acc;
+    local[b] = l;
+    if (!isfinite(l)) atomicOr(nonfinite, 2u);  // (bit 1: non-finite local energy; bit 0: logit overflow)
+  }
+}
+
+// ===========================================================================
+// Host side
+// ===========================================================================
+struct SpecState {
+  int n = 0, S = 0, sH = 0;
+  int64_t np = 0, per_chunk = 1;
+  int chunks = 1;
+  double* alpha_s = nullptr;  // [S] alpha of the sites (alpha > 0, ascending)
+  int32_t* sites = nullptr;   // [S]
+  int32_t* site_of = nullptr; // [n] site index or -1
+  double* beta = nullptr;     // [n]
+  int32_t *pi = nullptr, *pj = nullptr;
+  double* pv = nullptr;
+  // batch scratch
+  int cap_B = 0;
+  float *Z1 = nullptr, *lterm = nullptr, *fterm = nullptr;
+  double *lpf = nullptr, *dpart = nullptr, *nb = nullptr, *local = nullptr, *cached = nullptr;
+  int cap_R = 0, cap_parts = 0;
+  __half *Nh = nullptr, *Nl = nullptr;
+  double* nbpart = nullptr;
+  std::vector<double> alpha_host, beta_host;
+  std::vector<int32_t> pi_host, pj_host;
+  std::vector<double> pv_host;
+};
+
+static void validate_spec(int n, const double* alpha, const double* beta, const int32_t* pi, const int32_t* pj,
+                          int64_t np) {  // HamiltonianSpec::validate (hamiltonian.cpp:36-54)
+  if (np < 0) throw InvalidArgument("num_pairs must be >= 0");
+  for (int i = 0; i < n; ++i)
+    if (!(alpha[i] >= 0.0)) throw InvalidArgument("alpha must be non-negative");
+  (void)beta;
+  std::vector<uint64_t> keys((size_t)np);
+  for (int64_t t = 0; t < np; ++t) {
+    if (pi[t] < 0 || pj[t] >= n || pi[t] >= pj[t])
+      throw InvalidArgument("pair indices must satisfy 0 <= i < j < n");
+    keys[t] = ((uint64_t)(uint32_t)pi[t] << 32) | (uint32_t)pj[t];
+  }
+  std::vector<uint64_t> sorted = keys;
+  std::sort(sorted.begin(), sorted.end());
+  for (size_t t = 1; t < sorted.size(); ++t)
+    if (sorted[t] == sorted[t - 1])
+      throw InvalidArgument("duplicate pair (" + std::to_string((sorted[t] >> 32) + 1) + "," +
+                            std::to_string((sorted[t] & 0xffffffffu) + 1) + ")");
+}
+
+void spec_free(Handle* H) {
+  SpecState* s = H->spec;
+  if (!s) return;
+  sfree(s->alpha_s);
+  sfree(s->sites);
+  sfree(s->site_of);
+  sfree(s->beta);
+  sfree(s->pi);
+  sfree(s->pj);
+  sfree(s->pv);
+  sfree(s->Z1);
+  sfree(s->lterm);
+  sfree(s->fterm);
+  sfree(s->lpf);
+  sfree(s->dpart);
+  sfree(s->nb);
+  sfree(s->local);
+  sfree(s->cached);
+  sfree(s->Nh);
+  sfree(s->Nl);
+  sfree(s->nbpart);
+  delete s;
+  H->spec = nullptr;
+}
+
+void spec_set(Handle* H, const double* alpha, const double* beta, const int32_t* pi, const int32_t* pj,
+              const double* pv, int64_t np) {
+  const int n = H->L.n;
+  if (!alpha || !beta || (np > 0 && (!pi || !pj || !pv))) throw InvalidArgument("null spec array");
+  validate_spec(n, alpha, beta, pi, pj, np);
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+  spec_free(H);
+  H->invalidate_graph();
+  SpecState* s = new SpecState();
+  H->spec = s;
+  s->n = n;
+  s->np = np;
+  std::vector<int32_t> sites, site_of(n, -1);
+  std::vector<double> as;
+  for (int i = 0; i < n; ++i)
+    if (alpha[i] > 0.0) {
+      site_of[i] = (int32_t)sites.size();
+      sites.push_back(i);
+      as.push_back(alpha[i]);
+    }
+  s->S = (int)sites.size();
+  s->sH = 0;
+  while (s->sH < s->S && sites[s->sH] < H->L.Hd) ++s->sH;
+  s->alpha_host.assign(alpha, alpha + n);
+  s->beta_host.assign(beta, beta + n);
+  s->pi_host.assign(pi, pi + np);
+  s->pj_host.assign(pj, pj + np);
+  s->pv_host.assign(pv, pv + np);
+  auto up = [&](auto** d, const auto* src, size_t cnt) {
+    salloc(d, std::max<size_t>(cnt, 1));
+    if (cnt) VQMC_CUDA(cudaMemcpy(*d, src, cnt * sizeof(**d), cudaMemcpyHostToDevice));
+  };
+  up(&s->alpha_s, as.data(), as.size());
+  up(&s->sites, sites.data(), sites.size());
+  up(&s->site_of, site_of.data(), site_of.size());
+  up(&s->beta, beta, (size_t)n);
+  up(&s->pi, pi, (size_t)np);
+  up(&s->pj, pj, (size_t)np);
+  up(&s->pv, pv, (size_t)np);
+  // pair chunks: >= 4096 pairs per CTA row, at most 256 chunks
+  s->chunks = (int)std::min<int64_t>(256, std::max<int64_t>(1, (np + 8191) / 8192));
+  s->per_chunk = std::max<int64_t>(1, (np + s->chunks - 1) / s->chunks);
+}
+
+static void spec_ensure(Handle* H, int B) {
+  SpecState* s = H->spec;
+  const Layout& L = H->L;
+  if (B > s->cap_B) {
+    salloc(&s->dpart, (size_t)s->chunks * B);
+    salloc(&s->local, (size_t)B);
+    salloc(&s->cached, (size_t)B);
+    salloc(&s->lpf, (size_t)B);
+    if (s->S > 0) {
+      salloc(&s->Z1, (size_t)B * L.h);
+      salloc(&s->lterm, (size_t)B * L.n);
+      salloc(&s->fterm, (size_t)B * L.n);
+      salloc(&s->nb, (size_t)std::max(1, s->sH) * B);
+    }
+    s->cap_B = B;
+  }
+  if (s->sH > 0) {
+    // neighbour rows per GEMM launch: at most 32768 (whole samples' site sets)
+    const int64_t want = std::min<int64_t>((int64_t)B * s->sH, std::max<int64_t>(s->sH, 32768));
+    const int parts = 3 * ((L.n + kTailBN - 1) / kTailBN) + 3;
+    if (want > s->cap_R || parts > s->cap_parts) {
+      const int R = (int)std::max<int64_t>(want, s->cap_R);
+      salloc(&s->Nh, (size_t)R * H->hp18 + 128);
+      salloc(&s->Nl, (size_t)R * H->hp18 + 128);
+      salloc(&s->nbpart, (size_t)parts * R);
+      s->cap_R = R;
+      s->cap_parts = parts;
+    }
+  }
+}
+
+// local_energy_batch (estimator.hpp:43-90) of the configurations in H->X with the cached log psi
+// in d_cached (device, [B]; nullptr: the model's own log psi of the configurations); local
+// energies into d_local (device).  A non-finite local energy sets bit 1 of the handle's sticky
+// flag (the step's Adam then skips the update and the host raises NumericError).
+void launch_spec_local(Handle* H, int B, const double* d_cached, double* d_local) {
+  SpecState* s = H->spec;
+  if (!s) throw InvalidArgument("no Hamiltonian spec set on this handle (vqmc_gpu_set_spec)");
+  spec_ensure(H, B);
+  const Layout& L = H->L;
+  {
+    KScope ks(H, "spec_diag");
+    const int Wp = L.W | 1;  // odd row stride: conflict-free ballot reads
+    const size_t smem = (size_t)(32 * Wp + L.n) * sizeof(uint32_t);
+    ensure_smem_attr((const void*)spec_diag_kernel, smem);
+    spec_diag_kernel<<<dim3((B + 31) / 32, s->chunks), 256, smem, H->stream>>>(
+        B, L.n, L.W, Wp, H->X, s->beta, s->np, s->per_chunk, s->pi, s->pj, s->pv, s->dpart);
+    SPEC_LAUNCH_CHECK();
+    H->launches++;
+  }
+  if (s->S > 0) {
+    forward_plain(H, B, nullptr, s->lterm, s->fterm, s->Z1, s->lpf);
+    if (!d_cached) d_cached = s->lpf;
+    if (s->sH > 0) {
+      const int Bc = std::max(1, std::min(B, s->cap_R / s->sH));
+      for (int b0 = 0; b0 < B; b0 += Bc) {
+        const int bc = std::min(Bc, B - b0), rows = bc * s->sH;
+        {
+          KScope ks(H, "tim_nbr_build");
+          const int64_t total = (int64_t)rows * H->hp18;
+          const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+          nbr_build_kernel<<<grid, 256, 0, H->stream>>>(rows, bc, b0, L.h, H->hp18, L.W, s->sites, H->X, s->Z1,
+                                                         H->P + L.off_w1t, s->Nh, s->Nl);
+          SPEC_LAUNCH_CHECK();
+          H->launches++;
+        }
+        const int parts = launch_nbr_umma(H, rows, bc, b0, s->sites, s->Nh, s->Nl, s->nbpart);
+        H->launches++;
+        {
+          KScope ks(H, "tim_nbr_reduce");
+          nbr_reduce_kernel<<<(rows + 255) / 256, 256, 0, H->stream>>>(rows, bc, b0, B, parts, s->nbpart, s->nb);
+          SPEC_LAUNCH_CHECK();
+          H->launches++;
+        }
+      }
+    }
+  }
+  {
+    KScope ks(H, "spec_local");
+    spec_local_kernel<<<(B + 7) / 8, 256, 0, H->stream>>>(B, L.n, L.Hd, s->S, s->site_of, s->alpha_s, s->chunks,
+                                                          s->dpart, s->lterm, s->fterm, s->nb, s->lpf,
+                                                          d_cached ? d_cached : s->lpf, d_local, H->d_flag);
+    SPEC_LAUNCH_CHECK();
+    H->launches++;
+  }
+}
+
+double* spec_local_buffer(Handle* H, int B) {
+  spec_ensure(H, B);
+  return H->spec->local;
+}
+double* spec_cached_buffer(Handle* H, int B) {
+  spec_ensure(H, B);
+  return H->spec->cached;
+}
+
+}  // namespace vqmc_b200

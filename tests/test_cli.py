@@ -59,18 +59,48 @@ def test_config_precedence_and_parsing(tmp_path):  # cli_test.sh:49-63
     ["solve", "--problem", "maxcut", "--n", 6, "--model", "made", "--sampler", "mcmc"],  # pairing
     ["solve", "--problem", "maxcut", "--n", 6, "--model", "rbm", "--sampler", "auto"],
     ["solve", "--problem", "maxcut", "--n", 6, "--iterations", "abc"],
-    ["gen-instance", "--problem", "tim", "--n", 4, "--out", "/tmp/x.txt"],  # outside the path
+    ["gen-instance", "--problem", "ising", "--n", 4, "--out", "/tmp/x.txt"],  # not in {tim, maxcut}
+    ["solve", "--problem", "tim", "--n", 6, "--optimizer", "sgd"],  # plain SGD is outside the path
     ["bogus"],
 ])
 def test_usage_errors_exit_1(args):  # cli_test.sh:65-78
     assert run(*args).returncode == 1
 
 
-def test_tim_instance_rejected(tmp_path):
+def test_gen_instance_tim_matches_reference_generator(tmp_path):  # vqmc.cpp:533-537, hamiltonian.cpp:126-177
+    p = tmp_path / "t7.txt"
+    r = run("gen-instance", "--problem", "tim", "--n", 7, "--seed", 2, "--out", p)
+    assert r.returncode == 0
+    lines = [ln.split() for ln in p.read_text().strip().split("\n")]
+    assert lines[0] == ["tim", "7"]
+    ref = O.random_tim(7, 2)
+    alpha = np.zeros(7); beta = np.zeros(7); pairs = []
+    for t in lines[1:]:
+        if t[0] == "alpha":
+            alpha[int(t[1]) - 1] = float(t[2])
+        elif t[0] == "beta":
+            beta[int(t[1]) - 1] = float(t[2])
+        else:
+            pairs.append((int(t[1]) - 1, int(t[2]) - 1, float(t[3])))
+    assert np.array_equal(alpha, ref.alpha) and np.array_equal(beta, ref.beta)  # %.17g round-trips
+    assert np.array_equal(np.array([q[2] for q in pairs]), ref.pv)
+    assert np.array_equal(np.array([q[0] for q in pairs]), ref.pi)
+
+
+def test_tim_instance_resolution_and_validation(tmp_path):
+    dry = {"VQMC_CLI_DRYRUN": "1"}
     p = tmp_path / "t.txt"
-    p.write_text("tim 3\nalpha 1 0.5\n")
-    r = run("solve", "--instance", p, "--iterations", 2)
-    assert r.returncode == 1 and "TIM" in r.stderr
+    p.write_text("tim 3\nalpha 1 0.5\npair 1 3 -0.25  # comment\n")
+    r = run("solve", "--instance", p, "--iterations", 2, env=dry)
+    assert r.returncode == 0 and "problem tim" in r.stdout and "n 3 " in r.stdout
+    r = run("solve", "--n", 9, "--workers", 4, "--gpus", 2, env=dry)  # --problem defaults to tim
+    assert r.returncode == 0 and "problem tim gpus 2" in r.stdout
+    p.write_text("tim 3\nalpha 1 -0.5\n")  # HamiltonianSpec::validate
+    r = run("solve", "--instance", p, "--iterations", 2, env=dry)
+    assert r.returncode == 1 and "alpha must be non-negative" in r.stderr
+    p.write_text("tim 3\npair 2 1 0.5\n")  # load_spec: i < j
+    r = run("solve", "--instance", p, env=dry)
+    assert r.returncode == 1 and "i < j" in r.stderr
 
 
 @pytest.mark.gpu
@@ -139,3 +169,24 @@ def test_solve_target_reports_hit(tmp_path):  # vqmc.cpp:240-243 (hitting-time m
     assert r.returncode == 0, r.stderr
     s = json.loads((out / "summary.json").read_text())
     assert s["hit_iteration"] == 1 and s["hit_time_s"] > 0 and s["iterations_run"] == 1
+
+
+@pytest.mark.gpu
+def test_solve_tim_instance(tmp_path):
+    """solve on a TIM instance file (vqmc.cpp:119-140, 194-263): ADAM on random_tim(12, 100) with the
+    reference's streams lands near the reference's converged energy; no cut in the summary."""
+    p = tmp_path / "t12.txt"
+    run("gen-instance", "--problem", "tim", "--n", 12, "--seed", 100, "--out", p)
+    out = tmp_path / "run"
+    r = run("solve", "--instance", p, "--iterations", 300, "--minibatch", 1024, "--seed", 0, "--reference-streams",
+            "--out", out)
+    assert r.returncode == 0, r.stderr
+    s = json.loads((out / "summary.json").read_text())
+    assert s["config"]["problem"] == "tim" and "best_cut" not in s and s["iterations_run"] == 300
+    ref = O.train_spec(O.random_tim(12, 100), iterations=300, minibatch=1024, seed=0)["final_energy"]
+    assert abs(s["final_energy"] - ref) <= 0.03 * abs(ref)
+    rows = (out / "curve.csv").read_text().strip().split("\n")
+    assert len(rows) == 301
+    r = run("solve", "--problem", "tim", "--n", 10, "--iterations", 3, "--minibatch", 64, "--gpus", 64,
+            "--workers", 64, "--out", tmp_path / "x")
+    assert r.returncode == 1 and "visible" in r.stderr

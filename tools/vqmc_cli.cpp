@@ -1,8 +1,10 @@
 // vqmc — command-line drop-in for the reference's `vqmc` tool (proj/tools/vqmc.cpp) on the
 // B200 path.  Same subcommands, flags, config-file precedence, output files and exit codes
 // (0 ok, 1 usage, 2 numerical, 3 sample-test reject; vqmc.cpp:35-37) for the north-star
-// workload (Max-Cut, MADE, AUTO sampler, ADAM or SGD + SR).  Configurations outside that path
-// (TIM instances, RBM/MCMC) are rejected as usage errors with an explicit message.
+// workload (Max-Cut, MADE, AUTO sampler, ADAM or SGD + SR) and TIM instances (ADAM).
+// Configurations outside that path (RBM/MCMC, plain SGD, the TIM ground-state eigensolver) are
+// rejected as usage errors with an explicit message.  `--gpus G` spreads the `--workers` over G
+// GPUs (one host thread and NCCL rank each).
 //
 // CLI11 and nlohmann/json are not available in this image; the parser below implements the
 // subset of CLI11 behaviour the reference relies on: `--flag value` and `--flag=value`,
@@ -213,6 +215,7 @@ int run_solve(const Args& a) {
   cfg.eval_batch = (int)a.geti("eval-batch", 1024);
   cfg.workers = (int)a.geti("workers", 1);
   cfg.device = (int)a.geti("device", 0);
+  cfg.gpus = (int)a.geti("gpus", 1);
   cfg.reference_streams = a.flags.count("reference-streams") > 0;
   if (optimizer == "sgd_sr") {  // vqmc.cpp:416-425
     cfg.optimizer = vqmc::OptimizerKind::kSgdSr;
@@ -231,25 +234,34 @@ int run_solve(const Args& a) {
   vqmc::Graph g;
   try {
     if (!instance.empty()) {
-      if (sniff_header(instance) != "graph")
-        throw UsageError(instance + ": TIM instances are outside the B200 path (Max-Cut graphs only)");
-      g = vqmc::load_graph(instance);
+      if (sniff_header(instance) == "graph") {
+        g = vqmc::load_graph(instance);
+      } else {
+        cfg.spec = vqmc::load_spec(instance);
+      }
     } else if (n < 1) {
       throw UsageError("--n: either --instance or --n is required");
     } else if (problem == "maxcut") {
       g = vqmc::random_maxcut_graph(n, cfg.seed);
     } else {
-      throw UsageError("random TIM instances are outside the B200 path (use --problem maxcut)");
+      cfg.spec = vqmc::random_tim(n, cfg.seed);
     }
-    cfg.maxcut = vqmc::maxcut_spec(g);
+    if (!cfg.spec) cfg.maxcut = vqmc::maxcut_spec(g);
   } catch (const UsageError&) {
     throw;
   } catch (const std::exception& e) {
     std::cerr << "error: " << e.what() << "\n";
     return kExitUsage;
   }
+  const bool is_maxcut = cfg.maxcut.has_value();
+  if (!is_maxcut) {
+    g.n = cfg.spec->n;
+    if (cfg.optimizer == vqmc::OptimizerKind::kSgdSr)
+      throw UsageError("the B200 path trains TIM instances with ADAM (sgd_sr is implemented for Max-Cut)");
+  }
 
   if (std::getenv("VQMC_CLI_DRYRUN")) {  // test hook: print the resolved configuration
+    std::cout << "problem " << (is_maxcut ? "maxcut" : "tim") << " gpus " << cfg.gpus << "\n";
     std::cout << "n " << g.n << " edges " << g.edges.size() << " seed " << cfg.seed << " iterations "
               << cfg.iterations << " minibatch " << cfg.minibatch << " eval_batch " << cfg.eval_batch
               << " workers " << cfg.workers << " hidden " << cfg.hidden << " lr " << cfg.lr << "\n";
@@ -280,7 +292,7 @@ int run_solve(const Args& a) {
     }
   }
   JObj c;  // config_echo (vqmc.cpp:142-179)
-  c.kv["problem"] = jstr("maxcut");
+  c.kv["problem"] = jstr(is_maxcut ? "maxcut" : "tim");
   c.kv["instance"] = jstr(instance);
   c.kv["n"] = std::to_string(g.n);
   c.kv["seed"] = std::to_string(cfg.seed);
@@ -314,8 +326,10 @@ int run_solve(const Args& a) {
   s.kv["total_time_s"] = jnum(res.total_time);
   s.kv["replicas_identical"] = res.replicas_identical ? "true" : "false";
   s.kv["phase_times_s"] = ph.dump(2, 2);
-  s.kv["best_cut"] = jnum(*res.best_cut);
-  s.kv["mean_cut"] = jnum(*res.mean_cut);
+  if (res.best_cut) {
+    s.kv["best_cut"] = jnum(*res.best_cut);
+    s.kv["mean_cut"] = jnum(*res.mean_cut);
+  }
   if (res.hit_time) {
     s.kv["hit_time_s"] = jnum(*res.hit_time);
     s.kv["hit_iteration"] = std::to_string(res.hit_iteration);
@@ -323,7 +337,7 @@ int run_solve(const Args& a) {
   std::ofstream(out_dir + "/summary.json") << s.dump() << "\n";
   if (a.has("save-model")) vqmc::save_model(*res.made, a.get("save-model", ""));
   std::cout << "final energy " << res.final_energy << " +- " << res.final_energy_std << "\n";
-  std::cout << "best cut " << *res.best_cut << " mean cut " << *res.mean_cut << "\n";
+  if (res.best_cut) std::cout << "best cut " << *res.best_cut << " mean cut " << *res.mean_cut << "\n";
   std::cout << "wrote " << out_dir << "/curve.csv and " << out_dir << "/summary.json\n";
   return 0;
 }
@@ -425,15 +439,17 @@ int run_gen(const Args& a) {  // gen-instance (vqmc.cpp:469-488)
   if (!a.has("problem") || !a.has("n") || !a.has("out")) throw UsageError("--problem, --n and --out are required");
   const std::string problem = a.get("problem", "");
   if (problem != "tim" && problem != "maxcut") throw UsageError("--problem: not in {tim, maxcut}");
-  if (problem == "tim") throw UsageError("random TIM instances are outside the B200 path");
   const std::string out = a.get("out", "");
-  vqmc::save_graph(vqmc::random_maxcut_graph((int)a.geti("n", 0), (uint64_t)a.geti("seed", 0)), out);
+  const int n = (int)a.geti("n", 0);
+  const uint64_t seed = (uint64_t)a.geti("seed", 0);
+  if (problem == "tim") vqmc::save_spec(vqmc::random_tim(n, seed), out);  // vqmc.cpp:478-481
+  else vqmc::save_graph(vqmc::random_maxcut_graph(n, seed), out);
   std::cout << "wrote " << out << "\n";
   return 0;
 }
 
 void usage() {
-  std::cout << "vqmc (B200): variational Monte Carlo for Max-Cut with MADE + AUTO + ADAM\n"
+  std::cout << "vqmc (B200): variational Monte Carlo (Max-Cut, TIM) with MADE + AUTO + ADAM / SGD + SR\n"
                "subcommands: solve | oracle | sample-test | gen-instance\n";
 }
 
@@ -467,7 +483,7 @@ int main(int argc, char** argv) {
                            {"config", "instance", "problem", "n", "seed", "model", "sampler", "hidden", "chains",
                             "burn-in", "thinning", "optimizer", "lr", "sr-lambda", "sr-tol", "sr-maxiter",
                             "iterations", "minibatch", "eval-batch", "workers", "target", "out", "save-model",
-                            "device"},
+                            "device", "gpus"},
                            {"mcmc-reburn", "sr-fallback", "sr-uncentered", "reference-streams"});
       return run_solve(a);
     }
