@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstring>
 #include <map>
 #include <mutex>
 #include <utility>
@@ -949,5 +950,65 @@ extern "C" int vqmc_test_energy_rate(vqmc_gpu_t* g, int B, int iters, float* ms_
   H->X = saved;
   H->cap_B = saved_cap;
   cudaFree(X);
+  return VQMC_OK;
+}
+
+// ===========================================================================
+// Forward / TIM local-energy throughput hook (profiles): B device-resident random configurations
+// in the handle's batch buffers; mode 0 = the plain forward (log_psi_batch: z1_given + the tcgen05
+// given-bits GEMM + finalize), mode 1 = local_energy_batch of the handle's spec (diagonal, base
+// forward, neighbour GEMMs, combine).  Timed with CUDA events over `iters` calls after one warm-up;
+// then one pass with per-kernel events (names_out: cap slots of 32 chars).
+// ===========================================================================
+extern "C" int vqmc_test_forward_rate(vqmc_gpu_t* g, int B, int iters, int mode, float* ms_per_call, char* names_out,
+                                      float* kms_out, int cap, int* count) {
+  using namespace vqmc_b200;
+  Handle* H = reinterpret_cast<Handle*>(g);
+  try {
+    if (mode == 1 && !H->spec) throw InvalidArgument("mode 1 needs a spec (vqmc_gpu_set_spec)");
+    H->ensure_batch(B);
+    const int64_t words = (int64_t)B * H->L.W;
+    random_bits_kernel<<<148 * 8, 256, 0, H->stream>>>(words, H->L.n, H->L.W, 12345, H->X);
+    VQMC_CUDA(cudaGetLastError());
+    auto call = [&] {
+      if (mode == 0) forward_plain(H, B, nullptr, nullptr, nullptr, nullptr, H->log_psi);
+      else launch_spec_local(H, B, nullptr, spec_local_buffer(H, B));
+    };
+    cudaEvent_t e0, e1;
+    VQMC_CUDA(cudaEventCreate(&e0));
+    VQMC_CUDA(cudaEventCreate(&e1));
+    call();  // warm-up (allocations, smem attributes)
+    VQMC_CUDA(cudaEventRecord(e0, H->stream));
+    for (int i = 0; i < iters; ++i) call();
+    VQMC_CUDA(cudaEventRecord(e1, H->stream));
+    VQMC_CUDA(cudaEventSynchronize(e1));
+    float ms = 0.f;
+    VQMC_CUDA(cudaEventElapsedTime(&ms, e0, e1));
+    *ms_per_call = ms / std::max(1, iters);
+    cudaEventDestroy(e0);
+    cudaEventDestroy(e1);
+    const bool kt = H->ktimer;
+    H->ktimer = true;
+    H->kt_count = 0;
+    call();
+    H->ktimer = kt;
+    VQMC_CUDA(cudaStreamSynchronize(H->stream));
+    const int c = std::min(cap, H->kt_count);
+    for (int i = 0; i < c; ++i) {
+      VQMC_CUDA(cudaEventElapsedTime(&kms_out[i], H->kt_start[i], H->kt_end[i]));
+      std::strncpy(names_out + 32 * i, H->kt_name[i], 31);
+      names_out[32 * i + 31] = 0;
+    }
+    *count = c;
+    uint32_t flag = 0;
+    VQMC_CUDA(cudaMemcpy(&flag, H->d_flag, sizeof(flag), cudaMemcpyDeviceToHost));
+    if (flag) {
+      VQMC_CUDA(cudaMemset(H->d_flag, 0, sizeof(flag)));
+      throw NumericError("non-finite value in the timed forward");
+    }
+  } catch (const std::exception& ex) {
+    set_error(ex.what());
+    return status_of(ex);
+  }
   return VQMC_OK;
 }

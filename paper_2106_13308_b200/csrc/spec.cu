@@ -145,76 +145,132 @@ void forward_plain(Handle* H, int B, double* cond, float* lterm, float* fterm, f
 }
 
 // ===========================================================================
-// Diagonal energy (hamiltonian.cpp:61-69): 32 samples per CTA as bit-sliced node words
-// T[i] (bit l = spin i of sample b0 + l, built with one ballot per node); warps split the CTA's
-// chunk of the pair list, every lane accumulates its sample in fp64:
-//   -beta_i s_i = x_i ? beta_i : -beta_i,   -v s_i s_j = (x_i ^ x_j) ? v : -v.
-// Partials per (pair chunk, sample); the combine kernel sums them in a fixed order.
+// Diagonal energy (hamiltonian.cpp:61-69).  G <= 32 samples per CTA as bit-sliced node words
+// T[i] (bit l = spin i of sample b0 + l, one ballot per node); threads stream the CTA's chunk of
+// the pair list with coalesced loads and every thread keeps G fp64 accumulators:
+//   -beta_i s_i = x_i ? beta_i : -beta_i,   -v s_i s_j = (x_i ^ x_j) ? v : -v
+//   = 2 sum_{bit set} v - sum v   (one predicated add per sample and pair).
+// Dense mode (the complete row-major pair list of random_tim): only the values are read, the
+// indices follow from the position; a warp walks row i (lanes over j) and its mirror row
+// n - 2 - i, so every warp task has n - 1 pairs.  Partials per (chunk, sample).
 // ===========================================================================
-__global__ void __launch_bounds__(256) spec_diag_kernel(int B, int n, int W, int Wp, const uint32_t* __restrict__ X,
-                                                        const double* __restrict__ beta, int64_t np,
+// Bit-sliced spins of G-sample groups: Tg[g][i] bit l = spin i of sample g G + l (one warp per
+// 32 nodes: lane l loads sample l's word, 32 ballots transpose it).
+__global__ void spec_slice_kernel(int B, int n, int W, int G, const uint32_t* __restrict__ X,
+                                  uint32_t* __restrict__ Tg) {
+  const int lane = threadIdx.x & 31;
+  const int w = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;  // word column
+  const int g = blockIdx.y;
+  if (w >= W) return;
+  const int b = g * G + lane;
+  const uint32_t xw = lane < G && b < B ? X[(size_t)b * W + w] : 0u;
+  uint32_t mine = 0;
+#pragma unroll
+  for (int t = 0; t < 32; ++t) {
+    const uint32_t word = __ballot_sync(kFull, (xw >> t) & 1u);
+    if (lane == t) mine = word;
+  }
+  if (32 * w + lane < n) Tg[(size_t)g * n + 32 * w + lane] = mine;
+}
+
+template <int G>
+__global__ void __launch_bounds__(256) spec_diag_kernel(int B, int n, const uint32_t* __restrict__ Tg,
+                                                        const double* __restrict__ beta, int dense, int64_t np,
                                                         int64_t per_chunk, const int32_t* __restrict__ pi,
                                                         const int32_t* __restrict__ pj,
                                                         const double* __restrict__ pv, double* __restrict__ dpart) {
-  extern __shared__ uint32_t sm[];
-  uint32_t* xs = sm;             // [32][Wp]
-  uint32_t* T = sm + 32 * Wp;    // [n]
-  __shared__ double red[8][32];
+  extern __shared__ uint32_t T[];  // [n]
+  __shared__ double red[8][G];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-  const int b0 = blockIdx.x * 32;
-  for (int t = tid; t < 32 * W; t += blockDim.x) {
-    const int s = t / W, w = t % W;
-    xs[s * Wp + w] = b0 + s < B ? X[(size_t)(b0 + s) * W + w] : 0u;
-  }
+  const int b0 = blockIdx.x * G;
+  for (int i = tid; i < n; i += blockDim.x) T[i] = Tg[(size_t)blockIdx.x * n + i];
   __syncthreads();
-  for (int i = warp; i < n; i += 8) {
-    const uint32_t bit = (xs[lane * Wp + (i >> 5)] >> (i & 31)) & 1u;
-    const uint32_t word = __ballot_sync(kFull, bit);
-    if (lane == 0) T[i] = word;
-  }
-  __syncthreads();
-  double acc = 0.0;
+  double acc[G];
+#pragma unroll
+  for (int l = 0; l < G; ++l) acc[l] = 0.0;
+  double vsum = 0.0;
+  auto add = [&](uint32_t w, double v) {
+    vsum += v;
+#pragma unroll
+    for (int l = 0; l < G; ++l)
+      if ((w >> l) & 1u) acc[l] += v;
+  };
   if (blockIdx.y == 0)
-    for (int i = warp; i < n; i += 8) {
-      const double bi = beta[i];
-      acc += ((T[i] >> lane) & 1u) ? bi : -bi;
+    for (int i = tid; i < n; i += blockDim.x) add(T[i], beta[i]);  // x_i ? +beta : -beta
+  if (dense) {
+    // row pairs (i, n - 2 - i), i < (n - 1) / 2 (+ the middle row when n - 1 is odd); 4 loads in
+    // flight per lane
+    const int64_t r0 = (int64_t)blockIdx.y * per_chunk, r1 = min((int64_t)(n / 2), r0 + per_chunk);
+    for (int64_t rp = r0 + warp; rp < r1; rp += 8) {
+      for (int half = 0; half < 2; ++half) {
+        const int i = half ? n - 2 - (int)rp : (int)rp;
+        if (half && i <= (int)rp) break;  // (the middle row is walked once)
+        const double* row = pv + ((int64_t)i * n - (int64_t)i * (i + 1) / 2) - (i + 1);  // row[j], j > i
+        const uint32_t ti = T[i];
+        int j = i + 1 + lane;
+        for (; j + 96 < n; j += 128) {
+          const double v0 = row[j], v1 = row[j + 32], v2 = row[j + 64], v3 = row[j + 96];
+          add(ti ^ T[j], v0);
+          add(ti ^ T[j + 32], v1);
+          add(ti ^ T[j + 64], v2);
+          add(ti ^ T[j + 96], v3);
+        }
+        for (; j < n; j += 32) add(ti ^ T[j], row[j]);
+      }
     }
-  const int64_t p0 = (int64_t)blockIdx.y * per_chunk, p1 = min(np, p0 + per_chunk);
-  for (int64_t p = p0 + warp; p < p1; p += 8) {
-    const uint32_t w = T[pi[p]] ^ T[pj[p]];
-    const double v = pv[p];
-    acc += ((w >> lane) & 1u) ? v : -v;
+  } else {
+    const int64_t p0 = (int64_t)blockIdx.y * per_chunk, p1 = min(np, p0 + per_chunk);
+#pragma unroll 4
+    for (int64_t p = p0 + tid; p < p1; p += blockDim.x) add(T[pi[p]] ^ T[pj[p]], pv[p]);
   }
-  red[warp][lane] = acc;
+  // sample l: 2 acc_l - vsum (vsum covers the fields and the pairs this thread saw)
+#pragma unroll
+  for (int l = 0; l < G; ++l) {
+    double v = 2.0 * acc[l] - vsum;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    if (lane == 0) red[warp][l] = v;
+  }
   __syncthreads();
-  if (warp == 0) {
+  if (tid < G) {
     double s = 0.0;
 #pragma unroll
-    for (int k = 0; k < 8; ++k) s += red[k][lane];
-    if (b0 + lane < B) dpart[(size_t)blockIdx.y * B + b0 + lane] = s;
+    for (int k = 0; k < 8; ++k) s += red[k][tid];
+    if (b0 + tid < B) dpart[(size_t)blockIdx.y * B + b0 + tid] = s;
   }
 }
 
 // ===========================================================================
 // Neighbour rows: row r = t * Bc + (b - b0), site k = sites[t] < Hd:
 //   [G1' | 1] = [relu(z1_b + (x_bk ? -1 : 1) W1T[k]) | 1]   (fp16 pair, row stride hp)
+// One warp per row: coalesced z1 / W1T reads, 4-byte (half2) stores.
 // ===========================================================================
-__global__ void nbr_build_kernel(int rows, int Bc, int b0, int h, int hp, int W, const int32_t* __restrict__ sites,
-                                 const uint32_t* __restrict__ X, const float* __restrict__ Z1,
-                                 const float* __restrict__ W1T, __half* __restrict__ Nh, __half* __restrict__ Nl) {
-  const int64_t total = (int64_t)rows * hp;
-  for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < total; e += (int64_t)gridDim.x * blockDim.x) {
-    const int r = (int)(e / hp), kk = (int)(e % hp);
+__global__ void __launch_bounds__(256) nbr_build_kernel(int rows, int Bc, int b0, int h, int hp, int W,
+                                                        const int32_t* __restrict__ sites,
+                                                        const uint32_t* __restrict__ X, const float* __restrict__ Z1,
+                                                        const float* __restrict__ W1T, __half* __restrict__ Nh,
+                                                        __half* __restrict__ Nl) {
+  const int lane = threadIdx.x & 31;
+  const int nw = (gridDim.x * blockDim.x) >> 5;
+  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
     const int t = r / Bc, b = b0 + r % Bc, k = sites[t];
-    float g = 0.f;
-    if (kk < h) {
-      const bool x = (X[(size_t)b * W + (k >> 5)] >> (k & 31)) & 1u;
-      const float wk = W1T[(size_t)k * h + kk];
-      g = fmaxf(Z1[(size_t)b * h + kk] + (x ? -wk : wk), 0.f);
-    } else if (kk == h) {
-      g = 1.f;
+    const bool x = (X[(size_t)b * W + (k >> 5)] >> (k & 31)) & 1u;
+    const float* z = Z1 + (size_t)b * h;
+    const float* wk = W1T + (size_t)k * h;
+    __half2* oh = reinterpret_cast<__half2*>(Nh + (size_t)r * hp);
+    __half2* ol = reinterpret_cast<__half2*>(Nl + (size_t)r * hp);
+    for (int c = 2 * lane; c < hp; c += 64) {
+      float g[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const int kk = c + u;
+        g[u] = kk < h ? fmaxf(z[kk] + (x ? -wk[kk] : wk[kk]), 0.f) : (kk == h ? 1.f : 0.f);
+      }
+      uint32_t hi, lo;
+      ptx::split_f16x2(g[0], g[1], hi, lo);
+      oh[c >> 1] = *reinterpret_cast<const __half2*>(&hi);
+      ol[c >> 1] = *reinterpret_cast<const __half2*>(&lo);
     }
-    ptx::split_f16(g, Nh[e], Nl[e]);
   }
 }
 
@@ -229,77 +285,109 @@ __global__ void nbr_reduce_kernel(int rows, int Bc, int b0, int B, int parts, co
 }
 
 // ===========================================================================
-// Local energies (estimator.hpp:59-89), one warp per sample:
+// Local energies (estimator.hpp:59-89), one CTA per sample:
 //   d_k = log psi(x ^ e_k) - cached_b
 //       = (nb_k - sum_{i >= k} lterm_i) / 2 + (lpf_b - cached_b)    k < Hd
 //       = fterm_k / 2 + (lpf_b - cached_b)                           k >= Hd
-//   shift = max_k d_k if > 50 else 0;  l_b = H_xx - e^shift sum_k alpha_k e^(d_k - shift)
-// The suffix sums come from a running warp scan of lterm (fp64); pass 0 finds the shift,
-// pass 1 accumulates.
+//   shift = max(0, max_k d_k) if > 50 else 0;  l_b = H_xx - e^shift sum_k alpha_k e^(d_k - shift)
+// The suffix sums are total - prefix, the prefixes of the first Hd terms come from one block
+// scan (fp64).
 // ===========================================================================
-__global__ void spec_local_kernel(int B, int n, int Hd, int S, const int32_t* __restrict__ site_of,
-                                  const double* __restrict__ alpha_s, int chunks, const double* __restrict__ dpart,
-                                  const float* __restrict__ lterm, const float* __restrict__ fterm,
-                                  const double* __restrict__ nb, const double* __restrict__ lpf,
-                                  const double* __restrict__ cached, double* __restrict__ local,
-                                  uint32_t* __restrict__ nonfinite) {
-  const int b = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (b >= B) return;
-  double diag = 0.0;
-  for (int c = lane; c < chunks; c += 32) diag += dpart[(size_t)c * B + b];
+template <int T>
+__device__ __forceinline__ double block_sum(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
-  for (int o = 16; o > 0; o >>= 1) diag += __shfl_xor_sync(kFull, diag, o);
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  if (T == 32) return v;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = 0.0;
+#pragma unroll
+  for (int k = 0; k < T / 32; ++k) s += red[k];
+  return s;
+}
+template <int T>
+__device__ __forceinline__ double block_max(double v, double* red) {
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(kFull, v, o));
+  if (T == 32) return v;
+  __syncthreads();
+  if (lane == 0) red[warp] = v;
+  __syncthreads();
+  double s = red[0];
+#pragma unroll
+  for (int k = 1; k < T / 32; ++k) s = fmax(s, red[k]);
+  return s;
+}
+
+// T threads per sample (32 for small models, 256 for large ones)
+template <int T>
+__global__ void __launch_bounds__(T) spec_local_kernel(int B, int n, int Hd, int S, int sH,
+                                                       const int32_t* __restrict__ sites,
+                                                       const double* __restrict__ alpha_s, int chunks,
+                                                       const double* __restrict__ dpart,
+                                                       const float* __restrict__ lterm,
+                                                       const float* __restrict__ fterm,
+                                                       const double* __restrict__ nb,
+                                                       const double* __restrict__ lpf,
+                                                       const double* __restrict__ cached, double* __restrict__ local,
+                                                       uint32_t* __restrict__ flag) {
+  __shared__ double red[T / 32];
+  __shared__ double pre[kMaxHidden + 1];  // exclusive prefix of lterm over the head positions
+  const int b = blockIdx.x, tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  double v = 0.0;
+  for (int c = tid; c < chunks; c += T) v += dpart[(size_t)c * B + b];
+  const double diag = block_sum<T>(v, red);
   double acc = 0.0;
   if (S > 0) {
     const double corr = lpf[b] - cached[b];
     const float* lt = lterm + (size_t)b * n;
     const float* ft = fterm + (size_t)b * n;
-    // total of the base log terms (the suffix sums are total - prefix)
-    double tot = 0.0;
-    for (int i = lane; i < n; i += 32) tot += (double)lt[i];
+    v = 0.0;
+    for (int i = tid; i < n; i += T) v += (double)lt[i];
+    const double tot = block_sum<T>(v, red);
+    if (sH > 0) {  // block scan of lterm[0 .. Hd): E consecutive terms per thread (Hd <= 1024)
+      const int E = (Hd + T - 1) / T, i0 = tid * E;
+      double run = 0.0;
+      for (int u = 0; u < E; ++u)
+        if (i0 + u < Hd) run += (double)lt[i0 + u];
+      double incl = run;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) tot += __shfl_xor_sync(kFull, tot, o);
-    double shift = 0.0;
-    for (int pass = 0; pass < 2; ++pass) {
-      double mx = 0.0, sum = 0.0, prefix = 0.0;
-      for (int i0 = 0; i0 < n; i0 += 32) {
-        const int i = i0 + lane;
-        const int q = i < n ? site_of[i] : -1;
-        double d = 0.0;
-        if (i0 < Hd) {  // exclusive prefix of lterm over this chunk (only needed for head sites)
-          const double v = i < n ? (double)lt[i] : 0.0;
-          double incl = v;
-#pragma unroll
-          for (int o = 1; o < 32; o <<= 1) {
-            const double t = __shfl_up_sync(kFull, incl, o);
-            if (lane >= o) incl += t;
-          }
-          if (q >= 0 && i < Hd) d = 0.5 * (nb[(size_t)q * B + b] - (tot - (prefix + incl - v))) + corr;
-          prefix += __shfl_sync(kFull, incl, 31);
-        }
-        if (q >= 0 && i >= Hd) d = 0.5 * (double)ft[i] + corr;
-        if (q >= 0) {
-          if (pass == 0) mx = fmax(mx, d);
-          else sum -= alpha_s[q] * exp(d - shift);
-        }
+      for (int o = 1; o < 32; o <<= 1) {
+        const double t = __shfl_up_sync(kFull, incl, o);
+        if (lane >= o) incl += t;
       }
-      if (pass == 0) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) mx = fmax(mx, __shfl_xor_sync(kFull, mx, o));
-        shift = mx > 50.0 ? mx : 0.0;
-      } else {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(kFull, sum, o);
-        acc = sum;
+      double base = incl - run;
+      if (T > 32) {
+        __syncthreads();
+        if (lane == 31) red[warp] = incl;
+        __syncthreads();
+        for (int k = 0; k < warp; ++k) base += red[k];
       }
+      for (int u = 0; u < E && i0 + u < Hd; ++u) {
+        pre[i0 + u] = base;
+        base += (double)lt[i0 + u];
+      }
+      __syncthreads();
     }
-    acc *= exp(shift);
+    auto d_of = [&](int q) {
+      const int k = sites[q];
+      return q < sH ? 0.5 * (nb[(size_t)q * B + b] - (tot - pre[k])) + corr : 0.5 * (double)ft[k] + corr;
+    };
+    double mx = 0.0;  // (the reference's running maximum starts at 0)
+    for (int q = tid; q < S; q += T) mx = fmax(mx, d_of(q));
+    mx = block_max<T>(mx, red);
+    const double shift = mx > 50.0 ? mx : 0.0;
+    v = 0.0;
+    for (int q = tid; q < S; q += T) v -= alpha_s[q] * exp(d_of(q) - shift);
+    acc = block_sum<T>(v, red) * exp(shift);
   }
-  if (lane == 0) {
+  if (tid == 0) {
     const double l = diag + acc;
     local[b] = l;
-    if (!isfinite(l)) atomicOr(nonfinite, 2u);  // (bit 1: non-finite local energy; bit 0: logit overflow)
+    if (!isfinite(l)) atomicOr(flag, 2u);  // (bit 1: non-finite local energy; bit 0: logit overflow)
   }
 }
 
@@ -310,6 +398,7 @@ struct SpecState {
   int n = 0, S = 0, sH = 0;
   int64_t np = 0, per_chunk = 1;
   int chunks = 1;
+  bool dense = false;  // pairs are the complete row-major upper triangle
   double* alpha_s = nullptr;  // [S] alpha of the sites (alpha > 0, ascending)
   int32_t* sites = nullptr;   // [S]
   int32_t* site_of = nullptr; // [n] site index or -1
@@ -320,6 +409,7 @@ struct SpecState {
   int cap_B = 0;
   float *Z1 = nullptr, *lterm = nullptr, *fterm = nullptr;
   double *lpf = nullptr, *dpart = nullptr, *nb = nullptr, *local = nullptr, *cached = nullptr;
+  uint32_t* Tg = nullptr;  // bit-sliced spins of the sample groups (diagonal kernel)
   int cap_R = 0, cap_parts = 0;
   __half *Nh = nullptr, *Nl = nullptr;
   double* nbpart = nullptr;
@@ -363,6 +453,7 @@ void spec_free(Handle* H) {
   sfree(s->fterm);
   sfree(s->lpf);
   sfree(s->dpart);
+  sfree(s->Tg);
   sfree(s->nb);
   sfree(s->local);
   sfree(s->cached);
@@ -412,9 +503,23 @@ void spec_set(Handle* H, const double* alpha, const double* beta, const int32_t*
   up(&s->pi, pi, (size_t)np);
   up(&s->pj, pj, (size_t)np);
   up(&s->pv, pv, (size_t)np);
-  // pair chunks: >= 4096 pairs per CTA row, at most 256 chunks
-  s->chunks = (int)std::min<int64_t>(256, std::max<int64_t>(1, (np + 8191) / 8192));
-  s->per_chunk = std::max<int64_t>(1, (np + s->chunks - 1) / s->chunks);
+  // complete row-major pair list (random_tim): the diagonal kernel reads only the values
+  s->dense = n >= 2 && np == (int64_t)n * (n - 1) / 2;
+  for (int64_t t = 0, i = 0, j = 1; s->dense && t < np; ++t) {
+    if (pi[t] != i || pj[t] != j) s->dense = false;
+    if (++j == n) {
+      ++i;
+      j = i + 1;
+    }
+  }
+  if (s->dense) {  // chunks of row pairs (n / 2 tasks of n - 1 pairs): ~one task per warp, <= 1184 chunks
+    const int64_t tasks = std::max(1, n / 2);
+    s->per_chunk = std::max<int64_t>(8, (tasks + 1183) / 1184);
+    s->chunks = (int)((tasks + s->per_chunk - 1) / s->per_chunk);
+  } else {  // chunks of >= 8192 pairs, at most 256
+    s->chunks = (int)std::min<int64_t>(256, std::max<int64_t>(1, (np + 8191) / 8192));
+    s->per_chunk = std::max<int64_t>(1, (np + s->chunks - 1) / s->chunks);
+  }
 }
 
 static void spec_ensure(Handle* H, int B) {
@@ -422,6 +527,7 @@ static void spec_ensure(Handle* H, int B) {
   const Layout& L = H->L;
   if (B > s->cap_B) {
     salloc(&s->dpart, (size_t)s->chunks * B);
+    salloc(&s->Tg, (size_t)B * L.n);  // (groups of >= 1 sample: at most B groups)
     salloc(&s->local, (size_t)B);
     salloc(&s->cached, (size_t)B);
     salloc(&s->lpf, (size_t)B);
@@ -434,8 +540,9 @@ static void spec_ensure(Handle* H, int B) {
     s->cap_B = B;
   }
   if (s->sH > 0) {
-    // neighbour rows per GEMM launch: at most 32768 (whole samples' site sets)
-    const int64_t want = std::min<int64_t>((int64_t)B * s->sH, std::max<int64_t>(s->sH, 32768));
+    // neighbour rows per GEMM launch: whole samples' site sets, up to ~256 MB of operand pairs
+    const int64_t budget = (int64_t)(256 << 20) / (4 * (int64_t)H->hp18);
+    const int64_t want = std::min<int64_t>((int64_t)B * s->sH, std::max<int64_t>(s->sH, budget));
     const int parts = 3 * ((L.n + kTailBN - 1) / kTailBN) + 3;
     if (want > s->cap_R || parts > s->cap_parts) {
       const int R = (int)std::max<int64_t>(want, s->cap_R);
@@ -459,11 +566,27 @@ void launch_spec_local(Handle* H, int B, const double* d_cached, double* d_local
   const Layout& L = H->L;
   {
     KScope ks(H, "spec_diag");
-    const int Wp = L.W | 1;  // odd row stride: conflict-free ballot reads
-    const size_t smem = (size_t)(32 * Wp + L.n) * sizeof(uint32_t);
-    ensure_smem_attr((const void*)spec_diag_kernel, smem);
-    spec_diag_kernel<<<dim3((B + 31) / 32, s->chunks), 256, smem, H->stream>>>(
-        B, L.n, L.W, Wp, H->X, s->beta, s->np, s->per_chunk, s->pi, s->pj, s->pv, s->dpart);
+    // samples per CTA: 32, or fewer for small batches (more CTAs over the pair chunks)
+    const int G = B >= 32 ? 32 : B >= 16 ? 16 : B >= 8 ? 8 : B >= 4 ? 4 : B >= 2 ? 2 : 1;
+    const int groups = (B + G - 1) / G;
+    spec_slice_kernel<<<dim3((L.W + 7) / 8, groups), 256, 0, H->stream>>>(B, L.n, L.W, G, H->X, s->Tg);
+    SPEC_LAUNCH_CHECK();
+    H->launches++;
+    const size_t smem = (size_t)L.n * sizeof(uint32_t);
+    const dim3 grid(groups, s->chunks);
+    auto go = [&](auto kern) {
+      ensure_smem_attr((const void*)kern, smem);
+      kern<<<grid, 256, smem, H->stream>>>(B, L.n, s->Tg, s->beta, s->dense ? 1 : 0, s->np, s->per_chunk, s->pi,
+                                           s->pj, s->pv, s->dpart);
+    };
+    switch (G) {
+      case 32: go(spec_diag_kernel<32>); break;
+      case 16: go(spec_diag_kernel<16>); break;
+      case 8: go(spec_diag_kernel<8>); break;
+      case 4: go(spec_diag_kernel<4>); break;
+      case 2: go(spec_diag_kernel<2>); break;
+      default: go(spec_diag_kernel<1>); break;
+    }
     SPEC_LAUNCH_CHECK();
     H->launches++;
   }
@@ -476,8 +599,7 @@ void launch_spec_local(Handle* H, int B, const double* d_cached, double* d_local
         const int bc = std::min(Bc, B - b0), rows = bc * s->sH;
         {
           KScope ks(H, "tim_nbr_build");
-          const int64_t total = (int64_t)rows * H->hp18;
-          const int grid = (int)std::min<int64_t>((total + 255) / 256, 148 * 16);
+          const int grid = (int)std::min<int64_t>(((int64_t)rows + 7) / 8, 148 * 16);
           nbr_build_kernel<<<grid, 256, 0, H->stream>>>(rows, bc, b0, L.h, H->hp18, L.W, s->sites, H->X, s->Z1,
                                                          H->P + L.off_w1t, s->Nh, s->Nl);
           SPEC_LAUNCH_CHECK();
@@ -496,9 +618,15 @@ void launch_spec_local(Handle* H, int B, const double* d_cached, double* d_local
   }
   {
     KScope ks(H, "spec_local");
-    spec_local_kernel<<<(B + 7) / 8, 256, 0, H->stream>>>(B, L.n, L.Hd, s->S, s->site_of, s->alpha_s, s->chunks,
-                                                          s->dpart, s->lterm, s->fterm, s->nb, s->lpf,
-                                                          d_cached ? d_cached : s->lpf, d_local, H->d_flag);
+    const double* dc = d_cached ? d_cached : s->lpf;
+    if (L.n <= 256 && s->chunks <= 64)
+      spec_local_kernel<32><<<B, 32, 0, H->stream>>>(B, L.n, L.Hd, s->S, s->sH, s->sites, s->alpha_s, s->chunks,
+                                                     s->dpart, s->lterm, s->fterm, s->nb, s->lpf, dc, d_local,
+                                                     H->d_flag);
+    else
+      spec_local_kernel<256><<<B, 256, 0, H->stream>>>(B, L.n, L.Hd, s->S, s->sH, s->sites, s->alpha_s, s->chunks,
+                                                       s->dpart, s->lterm, s->fterm, s->nb, s->lpf, dc, d_local,
+                                                       H->d_flag);
     SPEC_LAUNCH_CHECK();
     H->launches++;
   }
