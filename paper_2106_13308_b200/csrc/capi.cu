@@ -598,6 +598,7 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
     H->head_Hdp = H->head_fast ? kp : 32 * ((Hd + 31) / 32);
     const char* hv = std::getenv("VQMC_HEAD");  // "3": keep the v3 head sampler (A/B measurements)
     H->head_v4 = H->head_fast && !(hv && hv[0] == '3');
+    H->head_v5 = H->head_v4 && !(hv && hv[0] == '4');
     if (H->head_v4) {
       const int KG = kp / 128, nwords = (h + 31) / 32;
       const size_t af = (size_t)nwords * KG * 2 * 8192, tri = (size_t)nwords * 32 * 64;  // halves, floats

@@ -965,6 +965,248 @@ __global__ void __launch_bounds__(32 * (kH4Warps + 1), 1) head_v4_kernel(const _
   }
 }
 
+// ===========================================================================
+// Head sampler v5: v4's arithmetic with the chain and the tensor-core updates on separate warps.
+//
+// In v4 every warp both runs its sample's serial chain and owns tiles of the rank-32 updates, so
+// each word pays chain + all of the word's MMAs + two CTA barriers.  But the next word's chain
+// only needs ITS OWN 32 slots (tiles 2m + 2, 2m + 3) updated; the updates of the later tiles can
+// run while that chain runs.  v5: 8 chain warps (one sample each) and 8 tile warps (tile j is
+// owned by warp j mod 8, accumulators for all 8 samples), synchronised by mbarriers:
+//   tile warps:  wait B(m) -> MMAs of round r0 = (2m + 2) / 8 (holds tiles 2m + 2, 2m + 3) ->
+//                their owners publish Z(m + 1) -> the remaining rounds of word m
+//   chain warps: wait Z(m) -> 32-bit chain -> outputs -> stage B(m) = (x, g_hi, g_lo)
+// so the critical path per word is chain + one round of MMAs instead of chain + all rounds.
+// Z and B are double-buffered by word parity; the producer warp streams TRI and A chunks as in v4.
+// Shared memory: mbarriers @0 (256 B) | Zx [2][2][32][8] f32 @256 (4 KB) | B staging
+// [2][3][8][40] f16 @4352 (3840 B) | TRI [2][64][32] f32 @8192 | ring [kH4Ring][16 KB] @24576.
+// ===========================================================================
+constexpr int kH5Smem = 24576 + kH4Ring * kH4Chunk;
+
+template <int KG, bool GIVEN>
+__global__ void __launch_bounds__(32 * (2 * kH4Warps + 1), 1) head_v5_kernel(const __grid_constant__ HeadV4Args A) {
+  extern __shared__ __align__(1024) unsigned char smem_raw[];
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem_raw);  // [kH4Ring] A chunks
+  uint64_t* empty = full + kH4Ring;                          // [kH4Ring]
+  uint64_t* tfull = empty + kH4Ring;                         // [2] TRI blocks
+  uint64_t* tempty = tfull + 2;                              // [2]
+  uint64_t* zfull = tempty + 2;                              // [2] Z(m) published (64 lanes)
+  uint64_t* zempty = zfull + 2;                              // [2] Z(m) read by the chain warps (8)
+  uint64_t* bfull = zempty + 2;                              // [2] B(m) staged (256 lanes)
+  uint64_t* bempty = bfull + 2;                              // [2] B(m) read by the tile warps (8)
+  float* Zx = reinterpret_cast<float*>(smem_raw + 256);      // [2][2][32][8]
+  __half* Bs = reinterpret_cast<__half*>(smem_raw + 4352);   // [2][3][8][kH4BStride]
+  float* tri_s = reinterpret_cast<float*>(smem_raw + 8192);  // [2][64][32]
+  unsigned char* ring = smem_raw + 24576;                    // [kH4Ring][16 KB]
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int h = A.h, nwords = A.nwords, T = A.T;
+  const int cta_b0 = kH4Warps * blockIdx.x;
+  if (threadIdx.x == 0) {
+    for (int r = 0; r < kH4Ring; ++r) {
+      mbar_init(&full[r], 1);
+      mbar_init(&empty[r], kH4Warps);
+    }
+    for (int p = 0; p < 2; ++p) {
+      mbar_init(&tfull[p], 1);
+      mbar_init(&tempty[p], kH4Warps);
+      mbar_init(&zfull[p], 64);
+      mbar_init(&zempty[p], kH4Warps);
+      mbar_init(&bfull[p], 32 * kH4Warps);
+      mbar_init(&bempty[p], kH4Warps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  ptx::pdl_trigger();
+  ptx::pdl_wait();  // thresholds (previous kernel) complete
+  const int rounds = (T + 7) >> 3;
+
+  if (warp == 2 * kH4Warps) {  // ---------------- producer: TRI blocks and A-operand chunks ----------------
+    if (lane == 0) {
+      int slot = 0, use = 0;
+      auto tri_copy = [&](int m) {
+        const int p = m & 1;
+        if (m >= 2) mbar_wait_sleep(&tempty[p], ((m >> 1) - 1) & 1);
+        mbar_expect_tx(&tfull[p], kH4Tri);
+        bulk_g2s(tri_s + p * 2048, A.TRI + (size_t)m * 2048, kH4Tri, &tfull[p]);
+      };
+      tri_copy(0);
+      for (int m = 0; m + 1 < nwords; ++m) {
+        tri_copy(m + 1);
+        for (int r = (2 * m + 2) >> 3; r < rounds; ++r) {
+          for (int z = 0; z < 2; ++z) {
+            if (use > 0) mbar_wait_sleep(&empty[slot], (use - 1) & 1);
+            mbar_expect_tx(&full[slot], kH4Chunk);
+            bulk_g2s(ring + (size_t)slot * kH4Chunk, A.AF + head4_chunk_off(KG, m, r, z), kH4Chunk, &full[slot]);
+            if (++slot == kH4Ring) {
+              slot = 0;
+              ++use;
+            }
+          }
+        }
+      }
+    }
+    return;
+  }
+
+  const int g = lane >> 2, t4 = lane & 3;
+  if (warp >= kH4Warps) {  // ---------------- tile warp: tiles j = 8 r + w, all 8 samples ----------------
+    const int w = warp - kH4Warps;
+    float acc1[KG][4], acc2[KG][4];  // rows g, g + 8 of the tile, columns (samples) 2 t4, 2 t4 + 1
+#pragma unroll
+    for (int r = 0; r < KG; ++r) {
+      const int s0 = 16 * (8 * r + w) + g, s1 = s0 + 8;
+      const float a0 = s0 < h ? A.b1[s0] : 0.f, a1 = s1 < h ? A.b1[s1] : 0.f;
+      const float c0 = s0 < h ? A.b2[s0] : 0.f, c1 = s1 < h ? A.b2[s1] : 0.f;
+      acc1[r][0] = acc1[r][1] = a0;
+      acc1[r][2] = acc1[r][3] = a1;
+      acc2[r][0] = acc2[r][1] = c0;
+      acc2[r][2] = acc2[r][3] = c1;
+    }
+    // publish Z(m): the owners of tiles 2m, 2m + 1 write their [slot][sample] values
+    auto publish = [&](int m) {
+      const bool own0 = w == ((2 * m) & 7), own1 = w == ((2 * m + 1) & 7);
+      if (!own0 && !own1) return;
+      const int pz = m & 1, r = (2 * m) >> 3, base = own1 ? 16 : 0;
+      if (m >= 2) mbar_wait(&zempty[pz], ((m >> 1) - 1) & 1);
+      float* zx = Zx + pz * 512;
+#pragma unroll
+      for (int rr = 0; rr < KG; ++rr) {
+        if (rr == r) {
+          zx[(base + g) * 8 + 2 * t4] = acc1[rr][0];
+          zx[(base + g) * 8 + 2 * t4 + 1] = acc1[rr][1];
+          zx[(base + g + 8) * 8 + 2 * t4] = acc1[rr][2];
+          zx[(base + g + 8) * 8 + 2 * t4 + 1] = acc1[rr][3];
+          zx[256 + (base + g) * 8 + 2 * t4] = acc2[rr][0];
+          zx[256 + (base + g) * 8 + 2 * t4 + 1] = acc2[rr][1];
+          zx[256 + (base + g + 8) * 8 + 2 * t4] = acc2[rr][2];
+          zx[256 + (base + g + 8) * 8 + 2 * t4 + 1] = acc2[rr][3];
+        }
+      }
+      mbar_arrive(&zfull[pz]);
+    };
+    publish(0);
+    int slot = 0, use = 0;
+    for (int m = 0; m + 1 < nwords; ++m) {
+      const int pb = m & 1;
+      mbar_wait(&bfull[pb], (m >> 1) & 1);
+      const __half* Bx = Bs + pb * (3 * 8 * kH4BStride);
+      const __half* Bgh = Bx + 8 * kH4BStride;
+      const __half* Bgl = Bgh + 8 * kH4BStride;
+      uint32_t bx[2][2], bh[2][2], bl[2][2];
+#pragma unroll
+      for (int ks = 0; ks < 2; ++ks) {
+        const int o = g * kH4BStride + 16 * ks + 2 * t4;
+        bx[ks][0] = *reinterpret_cast<const uint32_t*>(Bx + o);
+        bx[ks][1] = *reinterpret_cast<const uint32_t*>(Bx + o + 8);
+        bh[ks][0] = *reinterpret_cast<const uint32_t*>(Bgh + o);
+        bh[ks][1] = *reinterpret_cast<const uint32_t*>(Bgh + o + 8);
+        bl[ks][0] = *reinterpret_cast<const uint32_t*>(Bgl + o);
+        bl[ks][1] = *reinterpret_cast<const uint32_t*>(Bgl + o + 8);
+      }
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bempty[pb]);
+      const int r0 = (2 * m + 2) >> 3;
+#pragma unroll
+      for (int r = 0; r < KG; ++r) {
+        if (r < r0 || r >= rounds) continue;
+        const int j = 8 * r + w;
+        const bool live = j >= 2 * m + 2 && j < T;
+        // the round's two chunks (z = 0: W1 -> acc1, z = 1: W2 -> acc2) feed independent accumulator
+        // chains: wait for both, then interleave their MMAs (same per-accumulator order as v4)
+        const int s1 = slot + 1 == kH4Ring ? 0 : slot + 1, u1 = slot + 1 == kH4Ring ? use + 1 : use;
+        mbar_wait(&full[slot], use & 1);
+        mbar_wait(&full[s1], u1 & 1);
+        if (live) {
+          const unsigned char* c0 = ring + (size_t)slot * kH4Chunk + (size_t)w * 2048 + lane * 16;
+          const unsigned char* c1 = ring + (size_t)s1 * kH4Chunk + (size_t)w * 2048 + lane * 16;
+#pragma unroll
+          for (int ks = 0; ks < 2; ++ks) {
+            const uint4 ah = *reinterpret_cast<const uint4*>(c0 + ks * 1024);
+            const uint4 al = *reinterpret_cast<const uint4*>(c0 + ks * 1024 + 512);
+            const uint4 vh = *reinterpret_cast<const uint4*>(c1 + ks * 1024);
+            const uint4 vl = *reinterpret_cast<const uint4*>(c1 + ks * 1024 + 512);
+            h4_mma(acc1[r], ah, bx[ks][0], bx[ks][1]);
+            h4_mma(acc2[r], vh, bh[ks][0], bh[ks][1]);
+            h4_mma(acc1[r], al, bx[ks][0], bx[ks][1]);
+            h4_mma(acc2[r], vh, bl[ks][0], bl[ks][1]);
+            h4_mma(acc2[r], vl, bh[ks][0], bh[ks][1]);
+          }
+        }
+        __syncwarp();
+        if (lane == 0) {
+          mbar_arrive(&empty[slot]);
+          mbar_arrive(&empty[s1]);
+        }
+        slot = s1 + 1 == kH4Ring ? 0 : s1 + 1;
+        use = s1 + 1 == kH4Ring ? u1 + 1 : u1;
+        if (r == r0) publish(m + 1);  // tiles 2m + 2, 2m + 3 now hold every update of words <= m
+      }
+    }
+    return;
+  }
+
+  // ---------------- chain warp `warp`: sample b ----------------
+  const int w = warp, b = cta_b0 + w;
+  const bool bvalid = b < A.B;
+  float thr = (bvalid && lane < A.Hd8) ? A.thr[(size_t)b * A.Hd8 + lane] : INFINITY;
+  double lp = 0.0;
+  for (int m = 0; m < nwords; ++m) {
+    const int pz = m & 1;
+    mbar_wait(&zfull[pz], (m >> 1) & 1);
+    float z1c = Zx[pz * 512 + lane * 8 + w], z2c = Zx[pz * 512 + 256 + lane * 8 + w];
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&zempty[pz]);
+    // ---- serial chain over the word's 32 bits ----
+    const int p = m & 1;
+    mbar_wait(&tfull[p], (m >> 1) & 1);
+    const float* tw = tri_s + p * 2048 + lane;  // tw[32 l] = W1[32m + lane][32m + l], tw[32 (32 + l)] = W2[...]
+#pragma unroll
+    for (int l = 0; l < 32; ++l) {
+      const float t1 = tw[32 * l], t2 = tw[32 * (32 + l)];
+      const float g0 = fmaxf(z1c, 0.f), g1 = fmaxf(z1c + t1, 0.f);  // (on lane l: t1 = W1[i][i])
+      float v = (thr < z2c) ? -g1 : g0;                             // x in the sign bit
+      v = __shfl_sync(kFull, v, l);
+      const float xf = (__float_as_uint(v) >> 31) ? 1.f : 0.f;
+      z1c = fmaf(xf, t1, z1c);           // lanes >= l (t1 = 0 above this lane's diagonal)
+      z2c = fmaf(fabsf(v), t2, z2c);     // lanes > l
+    }
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&tempty[p]);
+    const bool x = thr < z2c;  // this lane's bit (its logit no longer changes)
+    const float gl = fmaxf(z1c, 0.f);
+    if (m + 1 < nwords) {  // ---- stage B(m) = (x, g_hi, g_lo), [sample][bit]: the tile warps wait on it ----
+      const int pb = m & 1;
+      if (m >= 2) mbar_wait(&bempty[pb], ((m >> 1) - 1) & 1);
+      __half* Bx = Bs + pb * (3 * 8 * kH4BStride);
+      __half gh, glo;
+      ptx::split_f16(gl, gh, glo);
+      Bx[w * kH4BStride + lane] = __float2half_rn(x ? 1.f : 0.f);
+      Bx[8 * kH4BStride + w * kH4BStride + lane] = gh;
+      Bx[16 * kH4BStride + w * kH4BStride + lane] = glo;
+      mbar_arrive(&bfull[pb]);
+    }
+    // ---- outputs of the word's bits (one per lane; off the critical path) ----
+    {
+      const int ib = 32 * m + lane;
+      const bool mine = bvalid && ib < h;
+      if (mine)
+        lp += head_emit(b, ib, z2c, z1c, x ? 1 : 0, A.n, h, A.hp, A.np, A.hd1p, A.G1, A.G1h, A.G1l, A.Dh, A.Dl, A.Xf,
+                        A.cond);
+      const uint32_t word = __ballot_sync(kFull, mine && x);
+      if (!GIVEN && bvalid && lane == 0) A.X[(size_t)b * A.W + m] = word;
+      const int ibn = 32 * (m + 1) + lane;  // next word's threshold
+      thr = (bvalid && ibn < A.Hd8) ? A.thr[(size_t)b * A.Hd8 + ibn] : INFINITY;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) lp += __shfl_xor_sync(kFull, lp, o);
+  if (bvalid && lane == 0) {
+    A.lp_head[b] = lp;
+    A.Xf[(size_t)b * A.hd1p + h] = __float2bfloat16_rn(1.f);  // ones column: gb1 = 1^T dz1
+  }
+}
+
 // Padded, completion-ordered copies of the head blocks (refreshed after every update):
 //   W1Tp[j][k] = W1m[k][j]           j < Hd, k < h (row stride hp)
 //   W2cp[c][i] = W2m[i][comp_k[c]]   c < h,  i < Hd (row stride Hdp)
@@ -1152,8 +1394,9 @@ static void head_v3_launch(Handle* H, int B, const double* uni, RngSpec rng, dou
 template <int KG, bool GIVEN>
 static void head_v4_launch(Handle* H, int B, const double* uni, RngSpec rng, double* cond) {
   const Layout& L = H->L;
-  const size_t smem = 4096 + 2 * kH4Tri + (size_t)kH4Ring * kH4Chunk;
-  ensure_smem_attr((const void*)head_v4_kernel<KG, GIVEN>, smem);
+  const size_t smem = H->head_v5 ? (size_t)kH5Smem : 4096 + 2 * kH4Tri + (size_t)kH4Ring * kH4Chunk;
+  ensure_smem_attr((const void*)head_v4_kernel<KG, GIVEN>, 4096 + 2 * kH4Tri + (size_t)kH4Ring * kH4Chunk);
+  ensure_smem_attr((const void*)head_v5_kernel<KG, GIVEN>, kH5Smem);
   const int grid = (B + kH4Warps - 1) / kH4Warps;
   const int Hd8 = (L.Hd + 7) & ~7;
   {
@@ -1169,7 +1412,10 @@ static void head_v4_launch(Handle* H, int B, const double* uni, RngSpec rng, dou
                         Hd8,      H->h4.AF, H->h4.TRI,    H->P + L.off_b1, H->P + L.off_b2, H->X,
                         H->G1,    H->G1h,   H->G1l,       H->hp18,  H->Dh,           H->Dl,
                         H->np8,   H->Xfb,   H->hd18,      H->lp_head, cond,          H->thr};
-  launch_k(H, head_v4_kernel<KG, GIVEN>, dim3(grid), dim3(32 * (kH4Warps + 1)), smem, args);
+  if (H->head_v5)
+    launch_k(H, head_v5_kernel<KG, GIVEN>, dim3(grid), dim3(32 * (2 * kH4Warps + 1)), smem, args);
+  else
+    launch_k(H, head_v4_kernel<KG, GIVEN>, dim3(grid), dim3(32 * (kH4Warps + 1)), smem, args);
   VQMC_CUDA(cudaGetLastError());
   H->launches++;
 }

@@ -210,6 +210,7 @@ struct Handle {
   std::vector<int32_t> comp_off_host;  // [Hd + 1]
   bool head_fast = false;  // bit i completes exactly hidden unit i (head v3, lane-permuted staging)
   bool head_v4 = false;    // head_fast and the v4 sampler (tensor-core word updates; VQMC_HEAD=3 keeps v3)
+  bool head_v5 = false;    // v4's staging with chain / tile warps specialised (VQMC_HEAD=4 keeps v4)
   Head4Stage h4{nullptr, nullptr, 0};  // v4 staging (head4.cuh)
   bool w1skip = false;     // deg_k <= k + 1 for all k (W1 columns below the current word are dead)
   int32_t* d_deg = nullptr;
