@@ -32,7 +32,14 @@ $(CLI): tools/vqmc_cli.cpp include/vqmc_b200/vqmc.hpp include/vqmc_b200.h $(LIB)
 oracle:
 	$(MAKE) -s -C oracle
 
+# timeline-instrumented copy of the library (tools/tail_trace.py): umma2 kernels record %globaltimer
+TRACE_LIB := paper_2106_13308_b200/lib/trace/libvqmc_trace.so
+trace: $(TRACE_LIB)
+$(TRACE_LIB): $(SRC) $(HOSTSRC) $(HDRS)
+	@mkdir -p paper_2106_13308_b200/lib/trace
+	$(NVCC) $(ARCH) -O3 -std=c++17 -Xcompiler -fPIC -Iinclude -DVQMC_TAIL_TRACE -shared -o $@ $(SRC) $(HOSTSRC) -ldl -lpthread
+
 clean:
 	rm -rf build paper_2106_13308_b200/lib paper_2106_13308_b200/bin oracle/_build
 
-.PHONY: all oracle clean
+.PHONY: all oracle clean trace

@@ -544,7 +544,7 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   if (H->L.total >= (int64_t(1) << 31)) throw std::invalid_argument("model too large for the device layout (> 2^31 live parameters)");
   H->hp8 = (h + 7) & ~7;
   H->hp18 = (h + 1 + 7) & ~7;
-  H->np8 = (n + 7) & ~7;
+  H->np8 = (n + 15) & ~15;  // (32-byte rows: the sampler epilogue writes D with 256-bit stores)
   H->hd18 = (Hd + 1 + 7) & ~7;
   H->d = 2LL * h * n + h + n;
   H->degrees.assign(degrees, degrees + h);

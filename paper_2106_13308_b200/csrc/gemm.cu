@@ -124,12 +124,12 @@ static void launch_umma(Handle* H, const char* name, const CUtensorMap& ah, cons
 }
 
 // CTA-pair launch: clusters of 2, one pair per 2 SMs (persistent over pair tiles of 256 x BN).
-template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT, int EK>
+template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT, int EK, int SETS = 0, int CHUNK = 32>
 static void launch_umma2(Handle* H, const char* name, const CUtensorMap& ah, const CUtensorMap& al,
                          const CUtensorMap& bh, const CUtensorMap& bl, int M, int N, int K, int splits, Epi epi,
                          cudaStream_t stream) {
-  using Cfg = Umma2Cfg<BN>;
-  auto kern = umma2_kernel<BN, A_MN, B_MN, Epi, A_EXACT, EK>;
+  using Cfg = Umma2Cfg<BN, SETS, CHUNK>;
+  auto kern = umma2_kernel<BN, A_MN, B_MN, Epi, A_EXACT, EK, SETS, CHUNK>;
   ensure_smem_attr((const void*)kern, Cfg::kSmem);
   const int nkb = (K + Cfg::kBK - 1) / Cfg::kBK;
   UmmaArgs args{M, N, K, (nkb + splits - 1) / splits, (N + BN - 1) / BN, (M + 2 * kUmmaBM - 1) / (2 * kUmmaBM), splits};
@@ -189,8 +189,14 @@ struct StoreEpi {  // test: C[row][col] = acc
 // pair; Philox keys are per row.  The epilogue warp sets take alternate 32-column chunks and
 // each writes its own log-prob partial (lp_part[kParts * tile + part]): deterministic.
 // (kTailBN: internal.cuh)
+// kTailCh: accumulator columns per epilogue call of the tail sampler; with 16-column chunks the
+// 12 chunks of a 192-column tile split evenly over 4 epilogue sets (16 epilogue warps), with
+// 32-column chunks over 3 sets.
+constexpr int kTailCh = 16;
+constexpr int kTailSets = kTailCh == 16 ? 4 : 0;
 template <bool PROD>  // PROD: production draws (Philox) and no log-probabilities (the training step)
 struct TailSampleEpiT {
+  static constexpr int CH = kTailCh;
   int B, n, np, W, colbase, col_lo;  // outputs in [col_lo, n) are drawn here
   const double* uni;
   RngSpec rng;
@@ -220,26 +226,31 @@ struct TailSampleEpiT {
       c1 = (uint32_t)(b - s * rng.seg);
     }
   }
-  __device__ void chunk(int b, int col0, const float (&v)[32], const UmmaArgs& a) {
+  __device__ void chunk(int b, int col0, const float (&v)[CH], const UmmaArgs& a) {
     if (b >= B) return;
     const int cb = colbase + col0;
-    if (cb >= col_lo && cb + 32 <= n) chunk_t<true>(b, cb, v);  // every output of the chunk is drawn here
+    if (cb >= col_lo && cb + CH <= n) chunk_t<true>(b, cb, v);  // every output of the chunk is drawn here
     else chunk_t<false>(b, cb, v);
   }
   template <bool FULL>
-  __device__ __forceinline__ void chunk_t(int b, int cb, const float (&v)[32]) {
+  __device__ __forceinline__ void chunk_t(int b, int cb, const float (&v)[CH]) {
     constexpr bool full = FULL;
     constexpr float kThrLo = (float)(kProbEps * 4294967296.0), kThrHi = (float)((1.0 - kProbEps) * 4294967296.0);
     const size_t rowD = (size_t)b * np;
     uint32_t word = 0;
-    float lsum = 0.f;  // 32 log terms in fp32, then one fp64 add
+    float lsum = 0.f;  // CH log terms in fp32, then one fp64 add
     bool bad = false;
 #pragma unroll
-    for (int jh = 0; jh < 32; jh += 16) {  // two halves of 16 outputs: 16-byte stores, fewer live registers
+    for (int jh = 0; jh < CH; jh += 16) {  // halves of 16 outputs: 16-byte stores, fewer live registers
       uint32_t dh[8], dl[8];
 #pragma unroll
       for (int j = jh; j < jh + 16; j += 4) {
         uint32_t r[4];
+#ifdef VQMC_TAIL_TRACE
+        if (g_tail_exp & 2) {
+          r[0] = r[1] = r[2] = r[3] = c1 * 2654435761u + (uint32_t)(cb + j);
+        } else
+#endif
         if (PROD || uni == nullptr) philox4_k(k0, k1, (uint32_t)((cb + j) >> 2), c1, c2, c3, r);
         float d[4];
 #pragma unroll
@@ -274,13 +285,14 @@ struct TailSampleEpiT {
         ptx::split_f16x2(d[0], d[1], dh[(j - jh) / 2], dl[(j - jh) / 2]);
         ptx::split_f16x2(d[2], d[3], dh[(j - jh) / 2 + 1], dl[(j - jh) / 2 + 1]);
       }
-      if (full) {
-        uint4* ph = reinterpret_cast<uint4*>(Dh + rowD + cb + jh);
-        uint4* pl = reinterpret_cast<uint4*>(Dl + rowD + cb + jh);
-        ph[0] = make_uint4(dh[0], dh[1], dh[2], dh[3]);
-        ph[1] = make_uint4(dh[4], dh[5], dh[6], dh[7]);
-        pl[0] = make_uint4(dl[0], dl[1], dl[2], dl[3]);
-        pl[1] = make_uint4(dl[4], dl[5], dl[6], dl[7]);
+#ifdef VQMC_TAIL_TRACE
+      if (g_tail_exp & 1) {
+        if (dh[0] == 0x7fffffffu && dl[1] == 0x7fffffffu) atomicOr(flag, 4u);  // (keep the values live)
+      } else
+#endif
+      if (full) {  // one full 32-byte sector per row and half (np % 16 == 0, cb % 16 == 0)
+        ptx::st_global_v8(Dh + rowD + cb + jh, dh);
+        ptx::st_global_v8(Dl + rowD + cb + jh, dl);
       } else {
         const __half* hh = reinterpret_cast<const __half*>(dh);
         const __half* hl = reinterpret_cast<const __half*>(dl);
@@ -295,14 +307,20 @@ struct TailSampleEpiT {
       }
     }
     if (bad) atomicOr(flag, 1u);
-    if (cb < col_lo) atomicOr(&X[(size_t)b * W + (cb >> 5)], word);  // shares the word with the head
-    else X[(size_t)b * W + (cb >> 5)] = word;
+    uint32_t* xw = &X[(size_t)b * W + (cb >> 5)];
+    if (CH == 32) {
+      if (cb < col_lo) atomicOr(xw, word);  // shares the word with the head
+      else *xw = word;
+    } else {  // a 16-bit half of the word
+      if (cb < col_lo) atomicOr(xw, word << (cb & 16));
+      else reinterpret_cast<uint16_t*>(xw)[(cb >> 4) & 1] = (uint16_t)word;
+    }
     if (!PROD) lps += (double)lsum;
   }
   __device__ void end_row(int b, const UmmaArgs&) {
     if (!PROD && lp_part && b < B) lp_part[(size_t)(kParts * tile.tn + part) * B + b] = lps;
   }
-  static constexpr int kParts = Umma2Cfg<kTailBN>::kEpiSets;  // one log-prob partial per epilogue set
+  static constexpr int kParts = Umma2Cfg<kTailBN, kTailSets, kTailCh>::kEpiSets;  // one log-prob partial per set
 };
 
 struct PartialEpi {  // split-K partial: out[z][row][col]
@@ -536,12 +554,8 @@ struct GivenEpiT {
       }
       if (!NBR && Dh) {
         if (cb + 32 <= n) {
-          uint4* ph = reinterpret_cast<uint4*>(Dh + rowD + cb + jh);
-          uint4* pl = reinterpret_cast<uint4*>(Dl + rowD + cb + jh);
-          ph[0] = make_uint4(dh[0], dh[1], dh[2], dh[3]);
-          ph[1] = make_uint4(dh[4], dh[5], dh[6], dh[7]);
-          pl[0] = make_uint4(dl[0], dl[1], dl[2], dl[3]);
-          pl[1] = make_uint4(dl[4], dl[5], dl[6], dl[7]);
+          ptx::st_global_v8(Dh + rowD + cb + jh, dh);
+          ptx::st_global_v8(Dl + rowD + cb + jh, dl);
         } else {
           const __half* hh = reinterpret_cast<const __half*>(dh);
           const __half* hl = reinterpret_cast<const __half*>(dl);
@@ -637,13 +651,13 @@ void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng, bool wan
   if (uni == nullptr && !want_lp) {  // training step: Philox draws, no log-probabilities
     TailSampleEpiT<true> e{B, L.n, H->np8, L.W, colbase, L.Hd, nullptr, rng, H->X, H->Dh, H->Dl, nullptr,
                            H->d_flag, 0, {}, 0.0, 0, 0, 0, 0, 0};
-    launch_umma2<BN, false, false, TailSampleEpiT<true>, false, kElemF16>(H, "z2_tail_umma", ah, al, bh, bl, B, ncols,
-                                                                          K, 1, e, H->stream);
+    launch_umma2<BN, false, false, TailSampleEpiT<true>, false, kElemF16, kTailSets, kTailCh>(
+        H, "z2_tail_umma", ah, al, bh, bl, B, ncols, K, 1, e, H->stream);
   } else {
     TailSampleEpiT<false> e{B,   L.n, H->np8, L.W, colbase, L.Hd, uni, rng, H->X, H->Dh, H->Dl,
                             want_lp ? H->lp_part : nullptr, H->d_flag, 0, {}, 0.0, 0, 0, 0, 0, 0};
-    launch_umma2<BN, false, false, TailSampleEpiT<false>, false, kElemF16>(H, "z2_tail_umma", ah, al, bh, bl, B,
-                                                                           ncols, K, 1, e, H->stream);
+    launch_umma2<BN, false, false, TailSampleEpiT<false>, false, kElemF16, kTailSets, kTailCh>(
+        H, "z2_tail_umma", ah, al, bh, bl, B, ncols, K, 1, e, H->stream);
   }
 }
 
@@ -967,3 +981,28 @@ extern "C" int vqmc_test_umma2_gemm(int M, int N, int K, int a_mn, int b_mn, int
   release();
   return VQMC_OK;
 }
+
+#ifdef VQMC_TAIL_TRACE
+// Trace hook (built only with -DVQMC_TAIL_TRACE): run the tail sampler GEMM of B samples once on
+// the handle and copy the per-CTA timeline (g_tail_trace) out.
+extern "C" int vqmc_test_tail_trace(vqmc_gpu_t* g, int B, unsigned long long* out, int exp_mask) {
+  using namespace vqmc_b200;
+  Handle* H = reinterpret_cast<Handle*>(g);
+  try {
+    VQMC_CUDA(cudaMemcpyToSymbol(g_tail_exp, &exp_mask, sizeof(int)));
+    H->ensure_batch(B);
+    RngSpec rng{1, 1, 0, B, nullptr};
+    void* tp = nullptr;
+    VQMC_CUDA(cudaGetSymbolAddress(&tp, g_tail_trace));
+    VQMC_CUDA(cudaMemset(tp, 0, sizeof(g_tail_trace)));
+    launch_tail_umma(H, B, nullptr, rng, false);
+    launch_tail_umma(H, B, nullptr, rng, false);
+    VQMC_CUDA(cudaStreamSynchronize(H->stream));
+    VQMC_CUDA(cudaMemcpyFromSymbol(out, g_tail_trace, sizeof(g_tail_trace)));
+  } catch (const std::exception& ex) {
+    set_error(ex.what());
+    return status_of(ex);
+  }
+  return VQMC_OK;
+}
+#endif

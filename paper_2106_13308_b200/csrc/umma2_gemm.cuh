@@ -25,6 +25,20 @@
 #include "umma_gemm.cuh"
 
 namespace vqmc_b200 {
+#ifdef VQMC_TAIL_TRACE
+// per CTA: [0] start, then per local tile j < 6: [1 + 4j] MMA start, [2 + 4j] MMA end (commit issued),
+// [3 + 4j] epilogue start (accumulator ready), [4 + 4j] epilogue end (set 0, warp 4); [31] CTA end
+__device__ unsigned long long g_tail_trace[148 * 32];
+__device__ int g_tail_exp;  // experiment mask of the tail epilogue (1: no D stores, 2: no Philox)
+__device__ __forceinline__ unsigned long long gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define TAIL_TRACE(slot) g_tail_trace[blockIdx.x * 32 + (slot)] = gtime()
+#else
+#define TAIL_TRACE(slot)
+#endif
 namespace ptx {
 
 __device__ __forceinline__ uint32_t cluster_ctarank() {
@@ -96,7 +110,9 @@ __host__ __device__ constexpr uint32_t idesc_f16_m256(int N, bool a_mn, bool b_m
 
 }  // namespace ptx
 
-template <int BN>
+// SETS: epilogue warp sets (0 = automatic); CHUNK: accumulator columns per epilogue call (32 or 16;
+// 16-column chunks let 4 sets share a 192-column tile evenly).
+template <int BN, int SETS = 0, int CHUNK = 32>
 struct Umma2Cfg {  // 16-bit operand pairs only; per CTA: A 128 rows, B BN / 2 rows
   static constexpr int kBK = 64;                            // K per stage (128-byte rows)
   static constexpr int kABytes = kUmmaBM * 128;             // 16 KB
@@ -104,22 +120,25 @@ struct Umma2Cfg {  // 16-bit operand pairs only; per CTA: A 128 rows, B BN / 2 r
   static constexpr int kStageBytes = 2 * kABytes + 2 * kBBytes;
   static constexpr int kStages = (200 * 1024) / kStageBytes > 6 ? 6 : (200 * 1024) / kStageBytes;
   static constexpr int kTmemCols = 2 * BN <= 64 ? 64 : 2 * BN <= 128 ? 128 : 2 * BN <= 256 ? 256 : 512;
-  static constexpr int kChunks = BN / 32;
-  // epilogue warp sets of 4 warps, each taking whole 32-column chunks (balanced: 6 chunks -> 3 sets)
-  static constexpr int kEpiSets = kChunks % 4 == 0 ? 4 : (kChunks % 3 == 0 ? 3 : (kChunks < 4 ? kChunks : 4));
+  static constexpr int kChunk = CHUNK;
+  static constexpr int kChunks = BN / CHUNK;
+  // epilogue warp sets of 4 warps, each taking whole chunks (balanced: 6 chunks -> 3 sets)
+  static constexpr int kEpiSets =
+      SETS ? SETS : (kChunks % 4 == 0 ? 4 : (kChunks % 3 == 0 ? 3 : (kChunks < 4 ? kChunks : 4)));
   static constexpr int kThreads = 128 + 128 * kEpiSets;
   static constexpr size_t kSmem = 1024 + (size_t)kStages * kStageBytes + 256;
   static_assert(BN % 32 == 0 && BN >= 64 && BN <= 256, "pair tile N");
+  static_assert(CHUNK == 16 || CHUNK == 32, "epilogue chunk");
 };
 
 // Pair tile t -> (n = t % tiles_n, m = (t / tiles_n) % tiles_m, split = t / (tiles_n tiles_m)); tiles_m
 // counts 256-row tiles.  Epilogue rows are m0 + 128 rank + 32 q + lane (UmmaTile.tm = 2 tm + rank).
-template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT, int EK>
-__global__ void __launch_bounds__(Umma2Cfg<BN>::kThreads, 1)
+template <int BN, bool A_MN, bool B_MN, class Epi, bool A_EXACT, int EK, int SETS = 0, int CHUNK = 32>
+__global__ void __launch_bounds__(Umma2Cfg<BN, SETS, CHUNK>::kThreads, 1)
     umma2_kernel(const __grid_constant__ CUtensorMap tA_hi, const __grid_constant__ CUtensorMap tA_lo,
                  const __grid_constant__ CUtensorMap tB_hi, const __grid_constant__ CUtensorMap tB_lo, UmmaArgs args,
                  Epi epi) {
-  using Cfg = Umma2Cfg<BN>;
+  using Cfg = Umma2Cfg<BN, SETS, CHUNK>;
   static_assert(EK != kElemTF32, "pair kernel: 16-bit operand pairs");
   static_assert(!B_MN || (BN / 2) % 64 == 0, "MN-major B: each CTA's half must be whole 64-element atoms");
   extern __shared__ __align__(1024) unsigned char smem_raw[];
@@ -167,6 +186,7 @@ __global__ void __launch_bounds__(Umma2Cfg<BN>::kThreads, 1)
   const uint32_t tmem = *tmem_slot;
   ptx::pdl_trigger();
   ptx::pdl_wait();
+  if (threadIdx.x == 0) TAIL_TRACE(0);
 
   if (warp == 0) {
     if (lane == 0) {  // ---------------- TMA producer (both CTAs) ----------------
@@ -217,6 +237,7 @@ __global__ void __launch_bounds__(Umma2Cfg<BN>::kThreads, 1)
         const int kb0 = c.z * args.kblk_per_split, kb1 = min(nkb, kb0 + args.kblk_per_split);
         const int buf = j & 1;
         if (j >= 2) ptx::mbar_wait(&tempty[buf], ((j >> 1) - 1) & 1);  // both epilogues drained it
+        if (j < 6) TAIL_TRACE(1 + 4 * j);
         ptx::tc_fence_after();
         const uint32_t acc = tmem + (uint32_t)(buf * BN);
         for (int kb = kb0; kb < kb1; ++kb) {
@@ -244,6 +265,7 @@ __global__ void __launch_bounds__(Umma2Cfg<BN>::kThreads, 1)
           }
         }
         ptx::mma_commit_pair(&tfull[buf]);  // both CTAs' accumulators of this tile are complete
+        if (j < 6) TAIL_TRACE(2 + 4 * j);
       }
     }
   } else if (warp >= 4) {  // ---------------- epilogue (both CTAs) ----------------
@@ -262,24 +284,27 @@ __global__ void __launch_bounds__(Umma2Cfg<BN>::kThreads, 1)
       const int row = m0 + 32 * q + lane;
       ptx::mbar_wait(&tfull[buf], (j >> 1) & 1);
       ptx::tc_fence_after();
+      if (warp == 4 && lane == 0 && j < 6) TAIL_TRACE(3 + 4 * j);
       e.part = part;
       e.tile = c;
       e.begin_row(row, args);
       const bool has_k = kb1 > kb0;
       const uint32_t trow = tmem + ((uint32_t)(32 * q) << 16) + (uint32_t)(buf * BN);
 #pragma unroll 1
-      for (int cc = 32 * part; cc < BN; cc += 32 * Cfg::kEpiSets) {
+      for (int cc = CHUNK * part; cc < BN; cc += CHUNK * Cfg::kEpiSets) {
         if (n0 + cc >= args.N) break;
-        float v[32];
+        float v[CHUNK];
         if (has_k) {
-          ptx::tmem_ld32(trow + (uint32_t)cc, v);
+          if constexpr (CHUNK == 32) ptx::tmem_ld32(trow + (uint32_t)cc, v);
+          else ptx::tmem_ld16(trow + (uint32_t)cc, v);
         } else {
 #pragma unroll
-          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+          for (int i = 0; i < CHUNK; ++i) v[i] = 0.f;
         }
         e.chunk(row, n0 + cc, v, args);
       }
       e.end_row(row, args);
+      if (warp == 4 && lane == 0 && j < 6) TAIL_TRACE(4 + 4 * j);
       ptx::tc_fence_before();
       __syncwarp();
       if (lane == 0) ptx::mbar_arrive_cluster(buf ? tempty_leader1 : tempty_leader0);
@@ -287,6 +312,7 @@ __global__ void __launch_bounds__(Umma2Cfg<BN>::kThreads, 1)
   }
   ptx::tc_fence_before();
   ptx::cluster_sync();  // both CTAs done (the leader's MMAs read the peer's smem until here)
+  if (threadIdx.x == 0) TAIL_TRACE(31);
   if (warp == 2) ptx::tmem_dealloc_pair<Cfg::kTmemCols>(tmem);
 }
 
