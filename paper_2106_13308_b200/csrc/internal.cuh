@@ -274,6 +274,22 @@ struct Handle {
   float *sr_dz1 = nullptr, *sr_p1f = nullptr;
   unsigned* d_pmax = nullptr;
   int sr_cap_B = 0;
+  // SR's device-resident CG loop: one captured iteration under a conditional WHILE node
+  // (VQMC_SR_HOST_LOOP=1 keeps the host-driven loop)
+  bool sr_device_loop = true;
+  cudaGraphExec_t sr_gexec = nullptr;
+  struct SrGraphKey {
+    bool valid = false;
+    int B = 0, cap_B = 0, sr_cap_B = 0;
+    bool centered = true;
+    double lambda = 0.0, tol = 0.0;
+    int max_it = 0;
+    bool operator==(const SrGraphKey& o) const {
+      return valid && o.valid && B == o.B && cap_B == o.cap_B && sr_cap_B == o.sr_cap_B && centered == o.centered &&
+             lambda == o.lambda && tol == o.tol && max_it == o.max_it;
+    }
+  };
+  SrGraphKey sr_gkey;
   int gpart_n = 0;
   uint32_t* d_flag = nullptr;  // sticky non-finite flag (logit overflow in the fp16-pair GEMMs)
   double* d_host_stage = nullptr;

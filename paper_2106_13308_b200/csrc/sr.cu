@@ -23,6 +23,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 
 #include "device_common.cuh"
 #include "internal.cuh"
@@ -136,6 +137,53 @@ __global__ void __launch_bounds__(kVecThreads) cg_p_kernel(int64_t total, int64_
 __global__ void sr_apply_kernel(int64_t total, double lr, const double* __restrict__ delta, float* __restrict__ P) {
   for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x)
     P[t] = (float)((double)P[t] - lr * delta[t]);
+}
+
+// Device-resident CG loop (one captured iteration under a conditional WHILE node): the convergence
+// test of conjugate_gradient (optimizer.cpp:58-60) on the device.  st = scal + 4: [0] rs0 = g.g,
+// [1] final r.r, [2] iterations, [3] beta.  Stops the loop (and leaves p stale) on convergence or at
+// the iteration budget, else prepares beta, rs and the p-range maximum for the p update.
+__global__ void __launch_bounds__(kVecThreads) cg_check_kernel(cudaGraphConditionalHandle cond, int cnt,
+                                                              const double* __restrict__ part,
+                                                              double* __restrict__ scal, double tol, int max_it,
+                                                              unsigned* __restrict__ pmax) {
+  double s = 0.0;
+  for (int i = threadIdx.x; i < cnt; i += blockDim.x) s += part[i];
+  s = block_sum256(s);
+  if (threadIdx.x == 0) {
+    double* st = scal + 4;
+    const int it = (int)st[2] + 1;
+    st[2] = (double)it;
+    if (sqrt(s) <= tol * sqrt(st[0]) || it >= max_it) {  // (the host loop's test, same roundings)
+      st[1] = s;
+      cudaGraphSetConditional(cond, 0);
+    } else {
+      st[3] = s / scal[0];
+      scal[0] = s;
+      *pmax = 0u;
+    }
+  }
+}
+__global__ void cg_state_init_kernel(double* __restrict__ scal) {
+  scal[4] = scal[0];
+  scal[5] = scal[0];
+  scal[6] = 0.0;
+}
+// p = r + beta p with beta from the device state
+__global__ void __launch_bounds__(kVecThreads) cg_p_dev_kernel(int64_t total, int64_t lo,
+                                                              const double* __restrict__ scal,
+                                                              const double* __restrict__ r, double* __restrict__ p,
+                                                              unsigned* __restrict__ pmax) {
+  const double beta = scal[7];
+  float m = 0.f;
+  for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < total; t += (int64_t)gridDim.x * blockDim.x) {
+    const double v = r[t] + beta * p[t];
+    p[t] = v;
+    if (t >= lo) m = fmaxf(m, (float)fabs(v));
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
+  if ((threadIdx.x & 31) == 0 && m > 0.f) atomicMax(pmax, __float_as_uint(m));
 }
 
 // max |p| over the [W2 | b2] range (float bits; atomicMax of non-negative floats is order-free)
@@ -574,9 +622,9 @@ void ensure_sr(Handle* H, int B) {
     alloc(&H->SRl, (size_t)L.n * H->hp18);
     alloc(&H->cg_part, (size_t)kVecBlocks);
     alloc(&H->sr_p1f, (size_t)L.Hd * 4 * ((L.h + 3) / 4));
-    alloc(&H->d_sr_scal, (size_t)4);
+    alloc(&H->d_sr_scal, (size_t)8);  // [0] rs [1] alpha [2] q sum; device CG loop: [4] rs0 [5] rs [6] it [7] beta
     alloc(&H->d_pmax, (size_t)1);
-    VQMC_CUDA(cudaMallocHost((void**)&H->h_sr_scal, 4 * sizeof(double)));
+    VQMC_CUDA(cudaMallocHost((void**)&H->h_sr_scal, 8 * sizeof(double)));
   }
   if (B > H->sr_cap_B) {
     if (H->sr_q) cudaFree(H->sr_q);
@@ -593,6 +641,8 @@ void ensure_sr(Handle* H, int B) {
 }
 
 void free_sr(Handle* H) {
+  if (H->sr_gexec) cudaGraphExecDestroy(H->sr_gexec);
+  H->sr_gexec = nullptr;
   void* ptrs[] = {H->cg_x, H->cg_r, H->cg_p, H->cg_g, H->cg_ap, H->sr_S, H->sr_C, H->SRh, H->SRl, H->cg_part, H->d_sr_scal, H->d_pmax,
                   H->sr_q, H->sp_part, H->sr_dz1, H->sr_q1, H->sr_p1f};
   for (void* p : ptrs)
@@ -710,6 +760,70 @@ bool sr_solve(Handle* H, int B, double lambda, double tol, int max_iterations, b
   sr_pmax_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(L.off_w2, L.total, H->cg_p, H->d_pmax);
   SR_CHECK();
   H->launches++;
+  static const bool host_loop = [] {
+    const char* e = std::getenv("VQMC_SR_HOST_LOOP");
+    return e && e[0] == '1';
+  }();
+  if (H->nranks == 1 && max_iterations > 0 && H->sr_device_loop && !host_loop) {
+    // one graph launch runs the whole solve: the iterations repeat under a conditional node until
+    // the device-side test stops them (no host round trip per iteration)
+    cg_state_init_kernel<<<1, 1, 0, H->stream>>>(H->d_sr_scal);
+    SR_CHECK();
+    Handle::SrGraphKey key{true, B, H->cap_B, H->sr_cap_B, centered, lambda, tol, max_iterations};
+    if (!H->sr_gexec || !(H->sr_gkey == key)) {
+      if (H->sr_gexec) cudaGraphExecDestroy(H->sr_gexec);
+      H->sr_gexec = nullptr;
+      cudaGraph_t g = nullptr;
+      VQMC_CUDA(cudaGraphCreate(&g, 0));
+      try {
+        cudaGraphConditionalHandle cond;
+        VQMC_CUDA(cudaGraphConditionalHandleCreate(&cond, g, 1, cudaGraphCondAssignDefault));
+        cudaGraphNodeParams np{};
+        np.type = cudaGraphNodeTypeConditional;
+        np.conditional.handle = cond;
+        np.conditional.type = cudaGraphCondTypeWhile;
+        np.conditional.size = 1;
+        cudaGraphNode_t node;
+        VQMC_CUDA(cudaGraphAddNode(&node, g, nullptr, 0, &np));
+        cudaGraph_t body = np.conditional.phGraph_out[0];
+        VQMC_CUDA(cudaStreamBeginCaptureToGraph(H->stream, body, nullptr, nullptr, 0, cudaStreamCaptureModeThreadLocal));
+        H->capturing = true;
+        try {
+          apply_fisher(H, B, centered);
+          cg_pap_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, H->G, H->cg_p, lambda, H->cg_part);
+          cg_alpha_kernel<<<1, kVecThreads, 0, H->stream>>>(kVecBlocks, H->cg_part, H->d_sr_scal);
+          cg_xr_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, H->d_sr_scal, H->G, H->cg_p, lambda,
+                                                                   H->cg_x, H->cg_r, H->cg_part);
+          cg_check_kernel<<<1, kVecThreads, 0, H->stream>>>(cond, kVecBlocks, H->cg_part, H->d_sr_scal, tol,
+                                                            max_iterations, H->d_pmax);
+          cg_p_dev_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, L.off_w2, H->d_sr_scal, H->cg_r,
+                                                                      H->cg_p, H->d_pmax);
+          SR_CHECK();
+        } catch (...) {
+          H->capturing = false;
+          cudaGraph_t tmp = nullptr;
+          cudaStreamEndCapture(H->stream, &tmp);
+          throw;
+        }
+        H->capturing = false;
+        VQMC_CUDA(cudaStreamEndCapture(H->stream, &body));
+        VQMC_CUDA(cudaGraphInstantiate(&H->sr_gexec, g, 0));
+      } catch (...) {
+        cudaGraphDestroy(g);
+        throw;
+      }
+      cudaGraphDestroy(g);
+      H->sr_gkey = key;
+    }
+    VQMC_CUDA(cudaGraphLaunch(H->sr_gexec, H->stream));
+    VQMC_CUDA(cudaMemcpyAsync(H->h_sr_scal, H->d_sr_scal, 8 * sizeof(double), cudaMemcpyDeviceToHost, H->stream));
+    VQMC_CUDA(cudaStreamSynchronize(H->stream));
+    const int it = (int)H->h_sr_scal[6];
+    H->launches += (int64_t)it * 10;
+    *iterations = it;
+    *residual = std::sqrt(H->h_sr_scal[5]) / rhs_norm;
+    return *residual <= tol;
+  }
   for (int it = 0; it < max_iterations; ++it) {
     apply_fisher(H, B, centered);
     cg_pap_kernel<<<kVecBlocks, kVecThreads, 0, H->stream>>>(total, H->G, H->cg_p, lambda, H->cg_part);

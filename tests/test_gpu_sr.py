@@ -202,3 +202,42 @@ def test_sr_step_through_nccl_matches_single_gpu(monkeypatch):
     finally:
         for hd in hs:
             K.lib.vqmc_gpu_destroy(hd)
+
+
+_CG_SCRIPT = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1]); sys.path.insert(0, sys.argv[1] + "/oracle")
+import pyoracle as O
+from paper_2106_13308_b200 import api
+n, B, seed = 100, 512, 4
+h = O.default_made_hidden(n)
+m = O.made_init(n, h, seed)
+x = np.ascontiguousarray(O.auto_sample(m, B, seed=seed, stream=1, mode=1)[0], np.uint8)
+e = O.random_maxcut_graph(n, seed)
+g = O.gradient_from_locals(m, x, O.local_energy(n, e, x)[0])
+model = api.MadeModel(n, h, m.degrees, m.theta)
+info = {}
+d = api.sr_direction(api.SrConfig(lam=1e-3, tol=1e-6, max_iterations=200), g, api.fisher_estimate(model, x), info)
+np.save(sys.argv[2], np.concatenate([d, [info["iterations"], info["residual"]]]))
+"""
+
+
+def test_sr_device_cg_loop_equals_host_loop(tmp_path):
+    """The device-resident CG loop (one captured iteration under a conditional WHILE node, the
+    convergence test on the device) takes the host loop's decisions: identical direction, iteration
+    count and residual (VQMC_SR_HOST_LOOP=1 runs the host-driven loop)."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    script = tmp_path / "cg.py"
+    script.write_text(_CG_SCRIPT)
+    outs = []
+    for host in ("0", "1"):
+        out = tmp_path / f"cg_{host}.npy"
+        env = dict(os.environ, VQMC_SR_HOST_LOOP=host)
+        subprocess.run([sys.executable, str(script), root, str(out)], check=True, env=env, timeout=300)
+        outs.append(np.load(out))
+    dev, host = outs
+    assert dev[-2] == host[-2] and dev[-2] > 0  # iterations
+    assert np.array_equal(dev, host)
