@@ -439,7 +439,9 @@ def run_ours(args):
         "phase_ms": {k: round(v / args.steps, 5) for k, v in
                      zip(["sample", "energy+weights", "backward", "allreduce", "adam+refresh"], phase)},
         "phase_ms_note": "phase and kernel events come from a second K-step pass (event nodes between kernels "
-                         "add overhead); ms_per_step uses whole-step events only",
+                         "add overhead); per-kernel events run the backward in the SERIAL schedule (one stream; "
+                         "the timed steps overlap gW2 + its all-reduce with dg1 -> dz1 -> gW1 on a side stream); "
+                         "ms_per_step uses whole-step events of the concurrent schedule only",
         "kernels": kernels,
         "head_latency": head_lat,
         "roofline": roof,
