@@ -15,6 +15,7 @@
 
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <mutex>
@@ -740,7 +741,14 @@ void launch_energy(Handle* H, int B) {
     // two per SM) while a chunk keeps >= 2 passes' worth of entries; groups are spread over the CTAs
     const int64_t per_max = std::min<int64_t>(63 * kCutThreads, (int64_t)((cap - tw) / 4)) & ~int64_t(31);
     int64_t chunks = std::max<int64_t>(1, (nEp + per_max - 1) / per_max);
-    while (chunks * groups * 2 <= 2 * 148 && nEp / (2 * chunks) >= 2 * kCutThreads) chunks *= 2;
+    // small batches: at most 4 edge chunks (each chunk's CTA redoes its group's bit transposes;
+    // measured at B = 1024, N = 10k: 4 chunks 11.1 us, 8 chunks 13.2 us, 1 chunk 13.2 us)
+    static const int64_t max_chunks = [] {
+      const char* e = std::getenv("VQMC_CUT_MAXCHUNKS");
+      return e ? std::max<int64_t>(1, atoll(e)) : (int64_t)4;
+    }();
+    while (chunks * groups * 2 <= 2 * 148 && nEp / (2 * chunks) >= 2 * kCutThreads && 2 * chunks <= max_chunks)
+      chunks *= 2;
     int64_t per = std::max<int64_t>(32, ((nEp + chunks - 1) / chunks + 31) & ~int64_t(31));
     chunks = std::max<int64_t>(1, (nEp + per - 1) / per);
     const int ctas_y = (int)std::min<int64_t>(groups, std::max<int64_t>(1, (2 * 148) / chunks));
