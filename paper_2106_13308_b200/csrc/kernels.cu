@@ -188,6 +188,7 @@ __global__ void __launch_bounds__(kCutThreads, 2) maxcut_cut_kernel(int B, int W
     const int s0 = 32 * g, rows = min(32, B - s0);
     if (rows == 32) {
       if (tid == 0) {
+        ptx::fence_proxy_async_smem();  // (the previous group's generic transposed writes to T)
         ptx::mbar_expect_tx(&bar[0], 128u * (uint32_t)W);
         ptx::bulk_g2s(T, X + (size_t)s0 * W, 128u * (uint32_t)W, &bar[0]);
       }
