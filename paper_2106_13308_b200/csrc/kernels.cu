@@ -586,7 +586,8 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t lo, int64_t hi, fl
       const int64_t w = t - o.off_w2;
       if (o.vec_w2 && w >= w2_bulk0 && w < w2_end) {
         // bulk of W2 (rows >= Hd): 4 consecutive entries of one row -> 8-byte stores of both halves
-        const unsigned i = (unsigned)w / (unsigned)o.h, k = (unsigned)w - i * (unsigned)o.h;
+        unsigned i, k;
+        w2_row(o, (unsigned)w, i, k);
         uint2 hi, lo;
         ptx::split_f16x2(p4[u].x, p4[u].y, hi.x, lo.x);
         ptx::split_f16x2(p4[u].z, p4[u].w, hi.y, lo.y);
@@ -863,7 +864,8 @@ void launch_set_step(Handle* H, uint64_t call, int64_t t, double lr, double b1, 
 static AdamOut adam_out(const Handle* H, bool gated) {
   const Layout& L = H->L;
   const bool vec = (L.h % 4) == 0 && (L.off_w2 % 4) == 0;
-  return AdamOut{L.h, H->hp18, L.Hd, H->head_hpk, H->head_Hdp, H->head_fast, vec, L.off_b1, L.off_w2, L.off_b2,
+  return AdamOut{L.h, H->hp18, L.Hd, H->head_hpk, H->head_Hdp, 1.f / (float)L.h, H->head_fast, vec, L.off_b1,
+                 L.off_w2, L.off_b2,
                  H->d_comp_pos, H->W1Tp, H->W2cp, H->W2h, H->W2l,
                  gated ? H->d_flag : nullptr, H->head_v4, H->h4};
 }
