@@ -661,9 +661,9 @@ void launch_tail_umma(Handle* H, int B, const double* uni, RngSpec rng, bool wan
   }
 }
 
-void launch_dg1_umma(Handle* H, int B) {
+template <int BN>
+static void launch_dg1_bn(Handle* H, int B) {
   const Layout& L = H->L;
-  constexpr int BN = 256;  // CTA pairs: 256 samples x 256 hidden units, split-K over the outputs
   const int mt = (B + 2 * kUmmaBM - 1) / (2 * kUmmaBM), nt = (L.h + BN - 1) / BN;
   const int nkb = (L.n + Umma2Cfg<BN>::kBK - 1) / Umma2Cfg<BN>::kBK;
   // (split count from the whole GPU, not the current SM partition: results independent of it)
@@ -679,6 +679,15 @@ void launch_dg1_umma(Handle* H, int B) {
   PartialEpi e{H->Epart, B, L.h, 0, {}};
   launch_umma2<BN, false, true, PartialEpi, false, kElemF16>(H, "bw_dg1_umma", ah, al, bh, bl, B, L.h, L.n, splits,
                                                              e, H->stream);
+}
+
+// dg1 on CTA pairs: 256 samples x BN hidden units per tile, split-K over the outputs (the MN-major B
+// halves must be whole 64-element atoms: BN in {128, 256}).  Measured (B = 1024, scripts/gemm_rate
+// hook): h = 424, K = 10^4: BN 256 30.7 us vs 128 33.7-42.2; h = 363, K = 5000: 128 26.8 vs 256
+// 39.3; h = 239, K = 1000: 128 18.6 vs 256 26.8-30.7.
+void launch_dg1_umma(Handle* H, int B) {
+  if (H->L.h > 384) launch_dg1_bn<256>(H, B);
+  else launch_dg1_bn<128>(H, B);
 }
 
 void launch_gw2_umma(Handle* H, int B, bool wg1_done, cudaStream_t stream) {
