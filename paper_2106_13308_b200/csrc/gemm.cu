@@ -239,7 +239,7 @@ struct TailSampleEpiT {
     const size_t rowD = (size_t)b * np;
     uint32_t word = 0;
     float lsum = 0.f;  // CH log terms in fp32, then one fp64 add
-    bool bad = false;
+    float nanacc = 0.f;
 #pragma unroll
     for (int jh = 0; jh < CH; jh += 16) {  // halves of 16 outputs: 16-byte stores, fewer live registers
       uint32_t dh[8], dl[8];
@@ -259,22 +259,22 @@ struct TailSampleEpiT {
           const bool valid = full || (c >= col_lo && c < n);
           const float z = v[j + t];
           const float a = fabsf(z);
-          bad |= !(a < INFINITY);
+          nanacc = fmaf(a, 0.f, nanacc);  // (stays 0 unless a logit is inf / NaN: one op per output)
           const float e = ptx::ex2_approx(a * -1.4426950408889634f);  // exp(-|z|)
           const float rr = ptx::rcp_approx(1.f + e);
           const float er = e * rr;
           const float praw = z >= 0.f ? rr : er, qraw = z >= 0.f ? er : rr;  // sigmoid(z), 1 - sigmoid(z)
           const bool clamp = a >= kLogitHi;                                     // models.hpp:26 clamp active
           bool x;
-          if (PROD || uni == nullptr) {  // u = (r + 1/2) 2^-32 < clamp(p)
-            x = (float)r[t] + 0.5f < fminf(fmaxf(praw * 4294967296.f, kThrLo), kThrHi);
+          if (PROD || uni == nullptr) {  // u = (r + 1/2) 2^-32 < clamp(p), as r < clamp(p) 2^32 - 1/2
+            x = (float)r[t] < fminf(fmaxf(fmaf(praw, 4294967296.f, -0.5f), kThrLo - 0.5f), kThrHi - 0.5f);
           } else {
             const double p = clamp ? (z > 0.f ? 1.0 - kProbEps : kProbEps) : (double)praw;
             x = valid && uni[(size_t)c * B + b] < p;
           }
           x = x && valid;
           word |= (uint32_t)x << (j + t);
-          d[t] = (clamp || !valid) ? 0.f : (x ? 0.5f * qraw : -0.5f * praw);  // made_dz2, models.cpp:163-171
+          d[t] = (clamp || !valid) ? 0.f : 0.5f * (x ? qraw : -praw);  // made_dz2, models.cpp:163-171
           if (!PROD && lp_part && valid) {
             const float L = log1pf(e);
             const float lg = clamp ? ((z > 0.f) == x ? -1.00000005e-7f : -16.11809565095832f)
@@ -306,7 +306,7 @@ struct TailSampleEpiT {
         }
       }
     }
-    if (bad) atomicOr(flag, 1u);
+    if (!(nanacc == 0.f)) atomicOr(flag, 1u);
     uint32_t* xw = &X[(size_t)b * W + (cb >> 5)];
     if (CH == 32) {
       if (cb < col_lo) atomicOr(xw, word);  // shares the word with the head
