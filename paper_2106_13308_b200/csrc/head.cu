@@ -982,6 +982,20 @@ __global__ void __launch_bounds__(32 * (kH4Warps + 1), 1) head_v4_kernel(const _
 // [2][3][8][40] f16 @4352 (3840 B) | TRI [2][64][32] f32 @8192 | ring [kH4Ring][16 KB] @24576.
 // ===========================================================================
 constexpr int kH5Smem = 24576 + kH4Ring * kH4Chunk;
+#ifdef VQMC_TAIL_TRACE
+// per CTA: [0] start, per word m < 15: [1 + 4m] Z(m) received, [2 + 4m] chain done, [3 + 4m] outputs
+// done (chain warp 0), [4 + 4m] Z(m) published (its first owner); [63] chain warp 0 end
+__device__ unsigned long long g_head_trace[128 * 64];
+__device__ __forceinline__ unsigned long long head_gtime() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+#define HEAD_TRACE(cond, slot) \
+  if ((cond) && blockIdx.x < 128) g_head_trace[blockIdx.x * 64 + (slot)] = head_gtime()
+#else
+#define HEAD_TRACE(cond, slot)
+#endif
 
 template <int KG, bool GIVEN>
 __global__ void __launch_bounds__(32 * (2 * kH4Warps + 1), 1) head_v5_kernel(const __grid_constant__ HeadV4Args A) {
@@ -1019,6 +1033,7 @@ __global__ void __launch_bounds__(32 * (2 * kH4Warps + 1), 1) head_v5_kernel(con
   __syncthreads();
   ptx::pdl_trigger();
   ptx::pdl_wait();  // thresholds (previous kernel) complete
+  HEAD_TRACE(threadIdx.x == 0, 0);
   const int rounds = (T + 7) >> 3;
 
   if (warp == 2 * kH4Warps) {  // ---------------- producer: TRI blocks and A-operand chunks ----------------
@@ -1084,6 +1099,7 @@ __global__ void __launch_bounds__(32 * (2 * kH4Warps + 1), 1) head_v5_kernel(con
         }
       }
       mbar_arrive(&zfull[pz]);
+      HEAD_TRACE(own0 && lane == 0 && m < 15, 4 + 4 * m);
     };
     publish(0);
     int slot = 0, use = 0;
@@ -1154,6 +1170,7 @@ __global__ void __launch_bounds__(32 * (2 * kH4Warps + 1), 1) head_v5_kernel(con
   for (int m = 0; m < nwords; ++m) {
     const int pz = m & 1;
     mbar_wait(&zfull[pz], (m >> 1) & 1);
+    HEAD_TRACE(w == 0 && lane == 0 && m < 15, 1 + 4 * m);
     float z1c = Zx[pz * 512 + lane * 8 + w], z2c = Zx[pz * 512 + 256 + lane * 8 + w];
     __syncwarp();
     if (lane == 0) mbar_arrive(&zempty[pz]);
@@ -1173,6 +1190,7 @@ __global__ void __launch_bounds__(32 * (2 * kH4Warps + 1), 1) head_v5_kernel(con
     }
     __syncwarp();
     if (lane == 0) mbar_arrive(&tempty[p]);
+    HEAD_TRACE(w == 0 && lane == 0 && m < 15, 2 + 4 * m);
     const bool x = thr < z2c;  // this lane's bit (its logit no longer changes)
     const float gl = fmaxf(z1c, 0.f);
     if (m + 1 < nwords) {  // ---- stage B(m) = (x, g_hi, g_lo), [sample][bit]: the tile warps wait on it ----
@@ -1198,7 +1216,9 @@ __global__ void __launch_bounds__(32 * (2 * kH4Warps + 1), 1) head_v5_kernel(con
       const int ibn = 32 * (m + 1) + lane;  // next word's threshold
       thr = (bvalid && ibn < A.Hd8) ? A.thr[(size_t)b * A.Hd8 + ibn] : INFINITY;
     }
+    HEAD_TRACE(w == 0 && lane == 0 && m < 15, 3 + 4 * m);
   }
+  HEAD_TRACE(w == 0 && lane == 0, 63);
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) lp += __shfl_xor_sync(kFull, lp, o);
   if (bvalid && lane == 0) {
@@ -1469,3 +1489,26 @@ void launch_head_v2(Handle* H, int B, const double* uni, RngSpec rng, bool given
 }
 
 }  // namespace vqmc_b200
+
+#ifdef VQMC_TAIL_TRACE
+// Trace hook (trace build only): one production head launch on B samples, timeline out.
+extern "C" int vqmc_test_head_trace(vqmc_gpu_t* g, int B, unsigned long long* out) {
+  using namespace vqmc_b200;
+  Handle* H = reinterpret_cast<Handle*>(g);
+  try {
+    H->ensure_batch(B);
+    RngSpec rng{1, 1, 0, B, nullptr};
+    launch_head_v2(H, B, nullptr, rng, false, nullptr);
+    void* tp = nullptr;
+    VQMC_CUDA(cudaGetSymbolAddress(&tp, g_head_trace));
+    VQMC_CUDA(cudaMemset(tp, 0, sizeof(g_head_trace)));
+    launch_head_v2(H, B, nullptr, rng, false, nullptr);
+    VQMC_CUDA(cudaStreamSynchronize(H->stream));
+    VQMC_CUDA(cudaMemcpyFromSymbol(out, g_head_trace, sizeof(g_head_trace)));
+  } catch (const std::exception& ex) {
+    set_error(ex.what());
+    return status_of(ex);
+  }
+  return VQMC_OK;
+}
+#endif
