@@ -108,6 +108,37 @@ __global__ void __launch_bounds__(1024) z1_given_kernel(int B, int h, int Hd, in
   }
 }
 
+// Small batches (B < 64): one warp per (sample, hidden unit), lanes over the inputs (fixed-order
+// shuffle reduction): the CTA-per-8-samples kernel above would leave almost every SM idle.
+__global__ void __launch_bounds__(256) z1_given_small_kernel(int B, int h, int Hd, int W, int hp, int hd1p,
+                                                             const uint32_t* __restrict__ X,
+                                                             const float* __restrict__ W1T,
+                                                             const float* __restrict__ b1, float* __restrict__ G1,
+                                                             __half* __restrict__ G1h, __half* __restrict__ G1l,
+                                                             __nv_bfloat16* __restrict__ Xf,
+                                                             float* __restrict__ Z1) {
+  const int wid = (int)((blockIdx.x * blockDim.x + threadIdx.x) >> 5), lane = threadIdx.x & 31;
+  if (wid < B * ((Hd + 31) / 32)) {  // (the first warps also write the spins' bf16 operand)
+    const int b = wid / ((Hd + 31) / 32), j = 32 * (wid % ((Hd + 31) / 32)) + lane;
+    if (j < Hd) Xf[(size_t)b * hd1p + j] = __float2bfloat16_rn((float)((X[(size_t)b * W + (j >> 5)] >> (j & 31)) & 1u));
+    if (j == 0) Xf[(size_t)b * hd1p + Hd] = __float2bfloat16_rn(1.f);  // ones column: gb1
+  }
+  if (wid >= B * h) return;
+  const int b = wid / h, k = wid % h;
+  float acc = 0.f;
+  for (int j = lane; j < Hd; j += 32)
+    if ((X[(size_t)b * W + (j >> 5)] >> (j & 31)) & 1u) acc += W1T[(size_t)j * h + k];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) acc += __shfl_xor_sync(kFull, acc, o);
+  if (lane == 0) {
+    const float z = acc + b1[k];
+    const float g = fmaxf(z, 0.f);
+    G1[(size_t)b * h + k] = g;
+    ptx::split_f16(g, G1h[(size_t)b * hp + k], G1l[(size_t)b * hp + k]);
+    if (Z1) Z1[(size_t)b * h + k] = z;
+  }
+}
+
 // log_psi[b] = (lp_head[b] (optional) + sum of the row's partials) / 2
 __global__ void finalize_lp_kernel(int B, int tiles, const double* __restrict__ lp_part,
                                    double* __restrict__ out) {
@@ -127,10 +158,17 @@ void forward_plain(Handle* H, int B, double* cond, float* lterm, float* fterm, f
   const Layout& L = H->L;
   {
     KScope ks(H, "z1_given");
-    const int threads = std::min(1024, (L.h + 31) & ~31);
-    z1_given_kernel<<<(B + kZ1S - 1) / kZ1S, threads, 0, H->stream>>>(
-        B, L.h, L.Hd, L.W, H->hp18, H->hd18, H->X, H->P + L.off_w1t, H->P + L.off_b1, H->G1, H->G1h, H->G1l, H->Xfb,
-        Z1);
+    if (B < 64) {
+      const int64_t warps = std::max<int64_t>((int64_t)B * L.h, (int64_t)B * ((L.Hd + 31) / 32));
+      z1_given_small_kernel<<<(unsigned)((warps + 7) / 8), 256, 0, H->stream>>>(
+          B, L.h, L.Hd, L.W, H->hp18, H->hd18, H->X, H->P + L.off_w1t, H->P + L.off_b1, H->G1, H->G1h, H->G1l,
+          H->Xfb, Z1);
+    } else {
+      const int threads = std::min(1024, (L.h + 31) & ~31);
+      z1_given_kernel<<<(B + kZ1S - 1) / kZ1S, threads, 0, H->stream>>>(
+          B, L.h, L.Hd, L.W, H->hp18, H->hd18, H->X, H->P + L.off_w1t, H->P + L.off_b1, H->G1, H->G1h, H->G1l,
+          H->Xfb, Z1);
+    }
     SPEC_LAUNCH_CHECK();
     H->launches++;
   }
@@ -198,8 +236,8 @@ __global__ void __launch_bounds__(256) spec_diag_kernel(int B, int n, const uint
   if (blockIdx.y == 0)
     for (int i = tid; i < n; i += blockDim.x) add(T[i], beta[i]);  // x_i ? +beta : -beta
   if (dense) {
-    // row pairs (i, n - 2 - i), i < (n - 1) / 2 (+ the middle row when n - 1 is odd); 4 loads in
-    // flight per lane
+    // row pairs (i, n - 2 - i), i < (n - 1) / 2 (+ the middle row when n - 1 is odd); 8 loads in
+    // flight per lane (at B = 4 the walk is a pure stream of the n^2/2 values: latency-bound with 4)
     const int64_t r0 = (int64_t)blockIdx.y * per_chunk, r1 = min((int64_t)(n / 2), r0 + per_chunk);
     for (int64_t rp = r0 + warp; rp < r1; rp += 8) {
       for (int half = 0; half < 2; ++half) {
@@ -208,6 +246,13 @@ __global__ void __launch_bounds__(256) spec_diag_kernel(int B, int n, const uint
         const double* row = pv + ((int64_t)i * n - (int64_t)i * (i + 1) / 2) - (i + 1);  // row[j], j > i
         const uint32_t ti = T[i];
         int j = i + 1 + lane;
+        for (; j + 224 < n; j += 256) {
+          double v[8];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) v[u] = row[j + 32 * u];
+#pragma unroll
+          for (int u = 0; u < 8; ++u) add(ti ^ T[j + 32 * u], v[u]);
+        }
         for (; j + 96 < n; j += 128) {
           const double v0 = row[j], v1 = row[j + 32], v2 = row[j + 64], v3 = row[j + 96];
           add(ti ^ T[j], v0);

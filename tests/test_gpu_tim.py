@@ -70,7 +70,7 @@ def test_plain_forward_log_psi(n, B):
 
 
 @pytest.mark.parametrize("n,B,h", [(6, 64, 8), (12, 256, 0), (40, 128, 0), (100, 64, 0), (300, 32, 0),
-                                   (1000, 8, 0)])
+                                   (1000, 8, 0), (2000, 4, 0)])
 def test_tim_local_energy_parity(n, B, h):
     h = h or O.default_made_hidden(n)
     m = perturbed(n, h, 7, scale=0.5)
