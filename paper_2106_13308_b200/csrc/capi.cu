@@ -454,19 +454,26 @@ static std::vector<uint32_t> bank_order_edges(int W, const int32_t* edges, int64
       if (open.size() > kWindow) open.erase(open.begin());  // oldest leaves the window (padded later)
     }
   }
-  std::vector<uint32_t> out;
-  out.reserve(batches.size() * 32 + 32);
   const uint32_t zero = 32u * (uint32_t)W;  // 32 zero words after the transposed spins (kernel)
+  do batches.emplace_back();  // whole blocks of 4 batches (at least one)
+  while (batches.size() % 4);
   for (Batch& b : batches) {
     for (int k = b.cnt; k < 32; ++k) {  // pad: a zero word on a free bank on each side (XOR = 0)
       const uint32_t pu = (uint32_t)__builtin_ctz(~b.lu), pv = (uint32_t)__builtin_ctz(~b.lv);
       b.lu |= 1u << pu, b.lv |= 1u << pv;
       b.e[k] = (zero + pu) | (zero + pv) << 16;
     }
-    out.insert(out.end(), b.e, b.e + 32);
   }
-  if (out.empty())  // no edges: one batch of zero pairs
-    for (uint32_t k = 0; k < 32; ++k) out.push_back((zero + k) | (zero + k) << 16);
+  // entries as byte offsets (4 u | 4 v << 16; 32 W + 32 <= 16384 words), and within each block of
+  // 128 entries lane l's 16-byte quad holds entry l of the block's 4 batches: the kernel's warp reads
+  // one quad per lane and its q-th lookups are batch q's (conflict-free) entries
+  std::vector<uint32_t> out(batches.size() * 32);
+  for (size_t blk = 0; blk < batches.size() / 4; ++blk)
+    for (int q = 0; q < 4; ++q)
+      for (int l = 0; l < 32; ++l) {
+        const uint32_t e = batches[4 * blk + q].e[l];
+        out[128 * blk + 4 * l + q] = (e & 0xFFFFu) * 4u | ((e >> 16) * 4u) << 16;
+      }
   return out;
 }
 
@@ -477,7 +484,7 @@ static void upload_edges(Handle* H, const int32_t* edges, int64_t num_edges) {
   H->d_edges_bank = nullptr;
   H->num_edges_bank = 0;
   H->num_edges = num_edges;
-  if (32 * H->L.W + 32 <= 65536 && !dense_energy_preferred(H->L.n, num_edges)) {
+  if (32 * H->L.W + 32 <= 16384 && !dense_energy_preferred(H->L.n, num_edges)) {
     const std::vector<uint32_t> pk = bank_order_edges(H->L.W, edges, num_edges);
     VQMC_CUDA(cudaMalloc((void**)&H->d_edges_bank, pk.size() * sizeof(uint32_t)));
     VQMC_CUDA(cudaMemcpy(H->d_edges_bank, pk.data(), pk.size() * sizeof(uint32_t), cudaMemcpyHostToDevice));

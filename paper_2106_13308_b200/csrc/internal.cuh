@@ -217,8 +217,8 @@ struct Handle {
   int32_t* d_comp_k = nullptr;    // hidden units sorted by degree
   int32_t* d_comp_off = nullptr;  // [Hd + 1]: units with degree i+1 at [off[i], off[i+1])
   int2* d_edges = nullptr;
-  uint32_t* d_edges_bank = nullptr;  // packed u | v << 16, bank-ordered batches of 32 (upload_edges)
-  int64_t num_edges_bank = 0;        // entries incl. padding (multiple of 32)
+  uint32_t* d_edges_bank = nullptr;  // byte offsets 4u | 4v << 16, bank-ordered, quad-interleaved (upload_edges)
+  int64_t num_edges_bank = 0;        // entries incl. padding (multiple of 128)
   // dense-graph energy (energy_dense.cu): fp8 strictly-upper adjacency [n][32 W], node degrees, and
   // the fp8 expansion of the batch's spins [B][32 W]
   bool dense_energy = false;

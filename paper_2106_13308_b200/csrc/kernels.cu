@@ -139,9 +139,10 @@ __device__ __forceinline__ void csa(uint32_t& hi, uint32_t& lo, uint32_t a, uint
 // Max-Cut cut counts over bit-sliced samples (local_energy_batch's diagonal branch,
 // estimator.hpp:53-57; diagonal_energy hamiltonian.cpp:61-69; cut_value :121-124).
 //
-// Edges arrive bank-ordered and packed (upload_edges): entry e = u | v << 16, and every aligned
-// batch of 32 entries has pairwise-distinct u mod 32 and pairwise-distinct v mod 32, so the two
-// shared-memory lookups T[u], T[v] of a warp are conflict-free.  A CTA keeps its edge chunk
+// Edges arrive bank-ordered and packed (upload_edges): entry e = 4u | 4v << 16 (byte offsets),
+// in batches of 32 with pairwise-distinct u mod 32 and pairwise-distinct v mod 32, interleaved so
+// that a warp's 16-byte quad loads (lane l: entry l of four batches) hand each of its four lookup
+// rounds T[u], T[v] one batch: conflict-free, 1/4 load instruction per entry.  A CTA keeps its edge chunk
 // resident in shared memory and walks sample groups g = blockIdx.y, += gridDim.y (32 samples per
 // group): the group's packed rows arrive by one bulk copy into T, every thread reads one word
 // column into registers, and after a barrier writes it back transposed (in place: T[swz(node)] =
@@ -166,7 +167,7 @@ __global__ void __launch_bounds__(kCutThreads, 2) maxcut_cut_kernel(int B, int W
   constexpr int nwarps = kCutThreads / 32;
   const int groups = (B + 31) / 32;
   const int64_t e0 = (int64_t)blockIdx.x * per_chunk, e1 = min(nEp, e0 + per_chunk);
-  const int ne = (int)(e1 - e0);  // multiple of 32
+  const int ne = (int)(e1 - e0);  // multiple of 128
   ptx::pdl_trigger();
   ptx::pdl_wait();
   if (tid == 0) {
@@ -218,19 +219,26 @@ __global__ void __launch_bounds__(kCutThreads, 2) maxcut_cut_kernel(int B, int W
       edges_ready = true;
     }
     __syncthreads();
-    // 16 entries per thread per pass (entries tid + 512 k), Harley-Seal carry-save counting
+    // 16 entries per thread per pass (quads tid + 512 k: one 16-byte load each), Harley-Seal
+    // carry-save counting.  Entries are byte offsets into T; a quad past the chunk reads as zeros
+    // (both lookups hit word 0: XOR = 0).
+    const uint4* E4 = reinterpret_cast<const uint4*>(E);
+    const char* Tb = reinterpret_cast<const char*>(T);
+    auto cutmask = [&](uint32_t p) {  // samples in which this edge is cut
+      return *reinterpret_cast<const uint32_t*>(Tb + (p & 0xFFFFu)) ^ *reinterpret_cast<const uint32_t*>(Tb + (p >> 16));
+    };
+    const int nq = ne >> 2;
     uint32_t ones = 0, twos = 0, fours = 0, eights = 0, c16 = 0, c32 = 0;  // <= 63 per thread (launcher)
-    for (int base = 0; base < ne; base += 16 * kCutThreads) {
+    for (int qb = 0; qb < nq; qb += 4 * kCutThreads) {
       uint32_t c[16];
 #pragma unroll
-      for (int k = 0; k < 16; ++k) {
-        const int e = base + k * kCutThreads + tid;
-        uint32_t m = 0u;
-        if (e < ne) {
-          const uint32_t p = E[e];
-          m = T[p & 0xFFFFu] ^ T[p >> 16];  // samples in which this edge is cut
-        }
-        c[k] = m;
+      for (int k = 0; k < 4; ++k) {
+        const int q = qb + k * kCutThreads + tid;
+        const uint4 p = q < nq ? E4[q] : make_uint4(0u, 0u, 0u, 0u);
+        c[4 * k] = cutmask(p.x);
+        c[4 * k + 1] = cutmask(p.y);
+        c[4 * k + 2] = cutmask(p.z);
+        c[4 * k + 3] = cutmask(p.w);
       }
       uint32_t tA, tB, fA, fB, eA, eB, sx;
       csa(tA, ones, ones, c[0], c[1]);
@@ -741,7 +749,7 @@ void launch_energy(Handle* H, int B) {
     const int64_t nEp = H->num_edges_bank;
     // edge chunks: fit the remaining shared memory; small batches split further (more CTAs, up to
     // two per SM) while a chunk keeps >= 2 passes' worth of entries; groups are spread over the CTAs
-    const int64_t per_max = std::min<int64_t>(63 * kCutThreads, (int64_t)((cap - tw) / 4)) & ~int64_t(31);
+    const int64_t per_max = std::min<int64_t>(63 * kCutThreads, (int64_t)((cap - tw) / 4)) & ~int64_t(127);
     int64_t chunks = std::max<int64_t>(1, (nEp + per_max - 1) / per_max);
     // small batches: at most 4 edge chunks (each chunk's CTA redoes its group's bit transposes;
     // measured at B = 1024, N = 10k: 4 chunks 11.1 us, 8 chunks 13.2 us, 1 chunk 13.2 us)
@@ -751,7 +759,7 @@ void launch_energy(Handle* H, int B) {
     }();
     while (chunks * groups * 2 <= 2 * 148 && nEp / (2 * chunks) >= 2 * kCutThreads && 2 * chunks <= max_chunks)
       chunks *= 2;
-    int64_t per = std::max<int64_t>(32, ((nEp + chunks - 1) / chunks + 31) & ~int64_t(31));
+    int64_t per = std::max<int64_t>(128, ((nEp + chunks - 1) / chunks + 127) & ~int64_t(127));
     chunks = std::max<int64_t>(1, (nEp + per - 1) / per);
     const int ctas_y = (int)std::min<int64_t>(groups, std::max<int64_t>(1, (2 * 148) / chunks));
     const size_t smem = tw + (size_t)per * 4;

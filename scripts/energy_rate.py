@@ -49,6 +49,7 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--n", type=int, default=10000)
+    ap.add_argument("--only-b", type=int, default=0, help="edge-list path at this batch only (profiling)")
     args = ap.parse_args()
     peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json"))) if os.path.exists(
         os.path.join(ROOT, "MEASURED_PEAKS.json")) else {}
@@ -60,7 +61,7 @@ def main():
     g = api.random_regular_graph(n, 3, 0)
     E = len(g.edges)
     hd = handle(n, g.edges)
-    for B in (1024, 1 << 14, 1 << 17, 1 << 20):
+    for B in ((args.only_b,) if args.only_b else (1024, 1 << 14, 1 << 17, 1 << 20)):
         ms, ch = rate(hd, B, 20 if B <= (1 << 17) else 5)
         byts = 4.0 * B * W + 8.0 * E + 4.0 * B * ch
         gbs = byts / (ms * 1e-3) / 1e9
@@ -70,6 +71,8 @@ def main():
         out["edge_list"].append(rec)
         print(json.dumps(rec), flush=True)
     K.lib.vqmc_gpu_destroy(hd)
+    if args.only_b:
+        return
     gd = api.random_maxcut_graph(n, 0)
     Ed = len(gd.edges)
     hd = handle(n, gd.edges)

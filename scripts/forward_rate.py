@@ -77,7 +77,16 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--out", default=None)
     ap.add_argument("--iters", type=int, default=20)
+    ap.add_argument("--tim", default=None, help="only these TIM shapes, e.g. 10000:4,1000:1024 (no forward, no step)")
     a = ap.parse_args()
+    if a.tim:
+        for nb in a.tim.split(","):
+            n, B = map(int, nb.split(":"))
+            hd, m = handle(n, B, api.random_tim(n, 0))
+            ms, kern = rate(hd, B, a.iters, 1)
+            print(json.dumps(dict(n=n, B=B, ms=ms, kernels_ms=kern)), flush=True)
+            K.lib.vqmc_gpu_destroy(hd)
+        return
     res = {"device": "B200", "forward": [], "tim_local_energy": [], "tim_train_step": []}
     for n, B in ((10000, 1024), (5000, 1024), (1000, 1024)):
         hd, m = handle(n, B)
