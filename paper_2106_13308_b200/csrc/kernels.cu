@@ -111,11 +111,25 @@ __device__ __forceinline__ uint32_t transpose32_rot(uint32_t v, int lane) {
 }
 
 // 32 x 32 bit transpose of v[r] (row r, bit c = M[r][c]) in registers: afterwards v[c] bit r =
-// M[r][c].  Five delta-swap stages of 16 register pairs.
+// M[r][c].  Five delta-swap stages of 16 register pairs; the 16- and 8-bit stages are byte
+// permutes (one PRMT per output word).
 __device__ __forceinline__ void transpose32_regs(uint32_t (&v)[32]) {
   const uint32_t masks[5] = {0x0000FFFFu, 0x00FF00FFu, 0x0F0F0F0Fu, 0x33333333u, 0x55555555u};
 #pragma unroll
-  for (int t = 0; t < 5; ++t) {
+  for (int r = 0; r < 16; ++r) {
+    const uint32_t a = v[r], b = v[r + 16];
+    v[r] = __byte_perm(a, b, 0x5410);
+    v[r + 16] = __byte_perm(a, b, 0x7632);
+  }
+#pragma unroll
+  for (int r = 0; r < 32; ++r) {
+    if (r & 8) continue;
+    const uint32_t a = v[r], b = v[r + 8];
+    v[r] = __byte_perm(a, b, 0x6240);
+    v[r + 8] = __byte_perm(a, b, 0x7351);
+  }
+#pragma unroll
+  for (int t = 2; t < 5; ++t) {
     const int j = 16 >> t;
     const uint32_t m = masks[t];
 #pragma unroll
@@ -199,9 +213,9 @@ __global__ void __launch_bounds__(kCutThreads, 2) maxcut_cut_kernel(int B, int W
       __syncthreads();
     }
     // in-place transpose, one 32 x 32 bit block per thread in registers (thread w takes word column w:
-    // 32 conflict-free loads, 5 delta-swap stages, 32 stores).  T is swizzled so that those stores
-    // are conflict-free: node i lives at word swz(i) = i ^ ((i >> 5) & 31); the edge entries carry
-    // swizzled indices (upload_edges).
+    // 32 conflict-free loads, 5 delta-swap stages, 8 16-byte stores).  T is swizzled so that those
+    // stores are conflict-free: node i lives at word swz(i) = i ^ (((i >> 5) & 7) << 2); the edge
+    // entries carry swizzled indices (upload_edges).
     uint32_t v[32];
     const int w = tid;
     if (w < W) {
@@ -212,7 +226,8 @@ __global__ void __launch_bounds__(kCutThreads, 2) maxcut_cut_kernel(int B, int W
     if (w < W) {
       transpose32_regs(v);
 #pragma unroll
-      for (int j = 0; j < 32; ++j) T[32 * w + (j ^ (w & 31))] = v[j];  // node 32 w + j
+      for (int k = 0; k < 8; ++k)  // nodes 32 w + 4 k .. + 3, one 16-byte store
+        *reinterpret_cast<uint4*>(T + 32 * w + 4 * (k ^ (w & 7))) = make_uint4(v[4 * k], v[4 * k + 1], v[4 * k + 2], v[4 * k + 3]);
     }
     if (!edges_ready) {
       if (ne > 0) ptx::mbar_wait(&bar[1], 0);
@@ -233,12 +248,15 @@ __global__ void __launch_bounds__(kCutThreads, 2) maxcut_cut_kernel(int B, int W
       uint32_t c[16];
 #pragma unroll
       for (int k = 0; k < 4; ++k) {
-        const int q = qb + k * kCutThreads + tid;
-        const uint4 p = q < nq ? E4[q] : make_uint4(0u, 0u, 0u, 0u);
-        c[4 * k] = cutmask(p.x);
-        c[4 * k + 1] = cutmask(p.y);
-        c[4 * k + 2] = cutmask(p.z);
-        c[4 * k + 3] = cutmask(p.w);
+        c[4 * k] = c[4 * k + 1] = c[4 * k + 2] = c[4 * k + 3] = 0u;
+        if (qb + k * kCutThreads < nq) {  // (CTA-uniform: the last pass is usually partial)
+          const int q = qb + k * kCutThreads + tid;
+          const uint4 p = q < nq ? E4[q] : make_uint4(0u, 0u, 0u, 0u);
+          c[4 * k] = cutmask(p.x);
+          c[4 * k + 1] = cutmask(p.y);
+          c[4 * k + 2] = cutmask(p.z);
+          c[4 * k + 3] = cutmask(p.w);
+        }
       }
       uint32_t tA, tB, fA, fB, eA, eB, sx;
       csa(tA, ones, ones, c[0], c[1]);
