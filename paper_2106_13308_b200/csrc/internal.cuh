@@ -350,7 +350,7 @@ struct Handle {
   int kt_count = 0;
 
   int64_t launches = 0;
-  bool pdl = false;  // programmatic dependent launch for the step kernels (VQMC_PDL=1 enables; measured neutral)
+  bool pdl = true;  // programmatic dependent launch for the step kernels (VQMC_PDL=0 disables; -4 us per step)
   int tail_tiles = 0;  // column tiles of the last z2 launch (lp partials)
   int splits = 0;      // split-K factor of the dg1 GEMM
 
