@@ -288,8 +288,10 @@ __global__ void __launch_bounds__(256) spec_diag_kernel(int B, int n, const uint
 // ===========================================================================
 // Neighbour rows: row r = t * Bc + (b - b0), site k = sites[t] < Hd:
 //   [G1' | 1] = [relu(z1_b + (x_bk ? -1 : 1) W1T[k]) | 1]   (fp16 pair, row stride hp)
-// One warp per row: coalesced z1 / W1T reads, 4-byte (half2) stores.
+// One warp per group of kNbrR rows (the rows' site / spin / z1 / W1T loads all in flight before
+// use): coalesced z1 / W1T reads, 4-byte (half2) stores.
 // ===========================================================================
+constexpr int kNbrR = 4;
 __global__ void __launch_bounds__(256) nbr_build_kernel(int rows, int Bc, int b0, int h, int hp, int W,
                                                         const int32_t* __restrict__ sites,
                                                         const uint32_t* __restrict__ X, const float* __restrict__ Z1,
@@ -297,24 +299,40 @@ __global__ void __launch_bounds__(256) nbr_build_kernel(int rows, int Bc, int b0
                                                         __half* __restrict__ Nl) {
   const int lane = threadIdx.x & 31;
   const int nw = (gridDim.x * blockDim.x) >> 5;
-  for (int r = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; r < rows; r += nw) {
-    const int t = r / Bc, b = b0 + r % Bc, k = sites[t];
-    const bool x = (X[(size_t)b * W + (k >> 5)] >> (k & 31)) & 1u;
-    const float* z = Z1 + (size_t)b * h;
-    const float* wk = W1T + (size_t)k * h;
-    __half2* oh = reinterpret_cast<__half2*>(Nh + (size_t)r * hp);
-    __half2* ol = reinterpret_cast<__half2*>(Nl + (size_t)r * hp);
-    for (int c = 2 * lane; c < hp; c += 64) {
-      float g[2];
+  for (int r0 = kNbrR * ((blockIdx.x * blockDim.x + threadIdx.x) >> 5); r0 < rows; r0 += kNbrR * nw) {
+    int k[kNbrR], b[kNbrR];
+    bool x[kNbrR];
 #pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int kk = c + u;
-        g[u] = kk < h ? fmaxf(z[kk] + (x ? -wk[kk] : wk[kk]), 0.f) : (kk == h ? 1.f : 0.f);
+    for (int q = 0; q < kNbrR; ++q) {
+      const int r = min(r0 + q, rows - 1);  // (a clamped duplicate row is recomputed, not stored)
+      k[q] = sites[r / Bc];
+      b[q] = b0 + r % Bc;
+    }
+#pragma unroll
+    for (int q = 0; q < kNbrR; ++q) x[q] = (X[(size_t)b[q] * W + (k[q] >> 5)] >> (k[q] & 31)) & 1u;
+    for (int c = 2 * lane; c < hp; c += 64) {
+      float zv[kNbrR][2], wv[kNbrR][2];
+#pragma unroll
+      for (int q = 0; q < kNbrR; ++q)
+#pragma unroll
+        for (int u = 0; u < 2; ++u) {
+          const bool in = c + u < h;
+          zv[q][u] = in ? Z1[(size_t)b[q] * h + c + u] : 0.f;
+          wv[q][u] = in ? W1T[(size_t)k[q] * h + c + u] : 0.f;
+        }
+#pragma unroll
+      for (int q = 0; q < kNbrR; ++q) {
+        if (r0 + q >= rows) break;
+        float g[2];
+#pragma unroll
+        for (int u = 0; u < 2; ++u)
+          g[u] = c + u < h ? fmaxf(zv[q][u] + (x[q] ? -wv[q][u] : wv[q][u]), 0.f) : (c + u == h ? 1.f : 0.f);
+        uint32_t hi, lo;
+        ptx::split_f16x2(g[0], g[1], hi, lo);
+        const size_t o = ((size_t)(r0 + q) * hp + c) >> 1;
+        reinterpret_cast<__half2*>(Nh)[o] = *reinterpret_cast<const __half2*>(&hi);
+        reinterpret_cast<__half2*>(Nl)[o] = *reinterpret_cast<const __half2*>(&lo);
       }
-      uint32_t hi, lo;
-      ptx::split_f16x2(g[0], g[1], hi, lo);
-      oh[c >> 1] = *reinterpret_cast<const __half2*>(&hi);
-      ol[c >> 1] = *reinterpret_cast<const __half2*>(&lo);
     }
   }
 }
@@ -644,7 +662,7 @@ void launch_spec_local(Handle* H, int B, const double* d_cached, double* d_local
         const int bc = std::min(Bc, B - b0), rows = bc * s->sH;
         {
           KScope ks(H, "tim_nbr_build");
-          const int grid = (int)std::min<int64_t>(((int64_t)rows + 7) / 8, 148 * 16);
+          const int grid = (int)std::min<int64_t>(((int64_t)rows + 8 * kNbrR - 1) / (8 * kNbrR), 148 * 8);
           nbr_build_kernel<<<grid, 256, 0, H->stream>>>(rows, bc, b0, L.h, H->hp18, L.W, s->sites, H->X, s->Z1,
                                                          H->P + L.off_w1t, s->Nh, s->Nl);
           SPEC_LAUNCH_CHECK();
