@@ -337,6 +337,8 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
     }
   }
   float wmax = 0.f;
+  const bool one = seg <= (int)blockDim.x;  // one sample per thread and segment: l_b stays in a register
+  double lb_keep = 0.0;
   for (int sgi = 0; sgi < segs; ++sgi) {
     const int base = sgi * seg;
     double s = 0.0, s2 = 0.0;
@@ -360,6 +362,7 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
       cs += c;
       cq += (long long)c * c;
       cm = max(cm, c);
+      lb_keep = lb;
     }
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) {
@@ -371,13 +374,20 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
     }
     if (lane == 0) { sd[warp] = s; sd2[warp] = s2; si[warp] = cs; sq[warp] = cq; sm[warp] = cm; }
     __syncthreads();
-    if (tid == 0) {
-      double t = 0.0, t2 = 0.0;
-      long long a = 0, q = 0;
-      int mx = 0;
-      for (int i = 0; i < nw; ++i) { t += sd[i]; t2 += sd2[i]; a += si[i]; q += sq[i]; mx = max(mx, sm[i]); }
-      smean = t / (double)seg;
-      if (lead) {
+    if (warp == 0) {  // (Max-Cut: the l_b are multiples of 1/4, so every fp64 sum here is exact)
+      double t = lane < nw ? sd[lane] : 0.0, t2 = lane < nw ? sd2[lane] : 0.0;
+      long long a = lane < nw ? si[lane] : 0, q = lane < nw ? sq[lane] : 0;
+      int mx = lane < nw ? sm[lane] : 0;
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) {
+        t += __shfl_xor_sync(kFull, t, o);
+        t2 += __shfl_xor_sync(kFull, t2, o);
+        a += __shfl_xor_sync(kFull, a, o);
+        q += __shfl_xor_sync(kFull, q, o);
+        mx = max(mx, __shfl_xor_sync(kFull, mx, o));
+      }
+      if (lane == 0) smean = t / (double)seg;
+      if (lead && lane == 0) {
         istat[3 * sgi + 0] = a;
         istat[3 * sgi + 1] = q;
         istat[3 * sgi + 2] = mx;
@@ -393,7 +403,9 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
     const double mean = smean;
     for (int b = tid; b < seg; b += blockDim.x) {
       double lb;
-      if (lin) {
+      if (one) {
+        lb = lb_keep;
+      } else if (lin) {
         lb = lin[base + b];
       } else {
         int c = 0;
@@ -425,8 +437,9 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
   for (int o = 16; o > 0; o >>= 1) wmax = fmaxf(wmax, __shfl_xor_sync(kFull, wmax, o));
   if (lane == 0) smax[warp] = wmax;
   __syncthreads();
-  float m = 0.f;
-  for (int i = 0; i < nw; ++i) m = fmaxf(m, smax[i]);
+  float m = lane < nw ? smax[lane] : 0.f;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) m = fmaxf(m, __shfl_xor_sync(kFull, m, o));
   // wscale = 2^e >= m (1 when every weight is 0); w' = w * 2^-e exactly
   int e = 0;
   if (m > 0.f) frexpf(m, &e);  // m = f 2^e, f in [0.5, 1)
