@@ -332,8 +332,10 @@ struct Handle {
   // concurrent backward: gW2 (and its all-reduce) on cstream with gw2_sms SMs while dg1 -> dz1 ->
   // gW1 use the rest (gemm_sm_cap limits the persistent GEMM grids; 0 = no cap)
   bool concurrent_bw = true;
-  int gw2_sms = 72;
-  int adam_w2_sms = 100;  // SMs' worth of blocks for the [W2 | b2] Adam beside dz1 -> gW1 (VQMC_ADAM_SMS)
+  // (N = 10k sweep with PDL on, ms per step: gw2 56/60/62 0.185, 64 0.1774, 66-68 0.178-0.179,
+  // 72 0.180, 80 0.187; Adam 90 0.180, 100 0.179, 110 0.1774, 120 0.178, 148 0.181 at gw2 64)
+  int gw2_sms = 64;
+  int adam_w2_sms = 110;  // SMs' worth of blocks for the [W2 | b2] Adam beside dz1 -> gW1 (VQMC_ADAM_SMS)
   int gemm_sm_cap = 0;
   int gw1_splits = 4;  // max split-K of the gW1 GEMM (1: direct epilogue, no finalize; VQMC_GW1_SPLITS; 4 measured best)
 
