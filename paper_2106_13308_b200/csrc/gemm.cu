@@ -666,8 +666,12 @@ static void launch_dg1_bn(Handle* H, int B) {
   const Layout& L = H->L;
   const int mt = (B + 2 * kUmmaBM - 1) / (2 * kUmmaBM), nt = (L.h + BN - 1) / BN;
   const int nkb = (L.n + Umma2Cfg<BN>::kBK - 1) / Umma2Cfg<BN>::kBK;
-  // (split count from the whole GPU, not the current SM partition: results independent of it)
-  int splits = std::max(1, std::min(nkb, (gemm_sms(nullptr) / 2) / (mt * nt)));  // one pair tile per SM pair
+  // split count from the SMs the concurrent backward gives dg1 (whole GPU minus gW2's partition),
+  // one pair tile per SM pair in one round; a function of the configuration only, so the serial
+  // and concurrent schedules sum the same partials (results independent of the schedule)
+  const int avail = gemm_sms(nullptr) - H->gemm_sm_reserve;
+  const int dg1_sms = H->concurrent_bw ? avail - std::min(H->gw2_sms, avail - 16) : avail;
+  int splits = std::max(1, std::min(nkb, (dg1_sms / 2) / (mt * nt)));
   splits = std::min(splits, H->max_splits);
   const int per = (nkb + splits - 1) / splits;
   splits = (nkb + per - 1) / per;
