@@ -545,6 +545,7 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   VQMC_CUDA(cudaStreamCreateWithFlags(&H->stream, cudaStreamNonBlocking));
   if (const char* e = std::getenv("VQMC_PDL")) H->pdl = e[0] == '1';
   if (const char* e = std::getenv("VQMC_SERIAL_BW")) H->concurrent_bw = e[0] != '1';
+  H->gw2_sms = n >= 8192 ? 80 : 64;  // (gW2's 2 x ceil(n / 128) pair tiles in whole rounds; internal.cuh)
   if (const char* e = std::getenv("VQMC_GW2_SMS")) H->gw2_sms = std::max(2, atoi(e));
   if (const char* e = std::getenv("VQMC_GW1_SPLITS")) H->gw1_splits = atoi(e);
   if (const char* e = std::getenv("VQMC_ADAM_SMS")) H->adam_w2_sms = std::max(2, atoi(e));

@@ -332,8 +332,11 @@ struct Handle {
   // concurrent backward: gW2 (and its all-reduce) on cstream with gw2_sms SMs while dg1 -> dz1 ->
   // gW1 use the rest (gemm_sm_cap limits the persistent GEMM grids; 0 = no cap)
   bool concurrent_bw = true;
-  // (N = 10k sweep with PDL on, ms per step: gw2 56/60/62 0.185, 64 0.1774, 66-68 0.178-0.179,
-  // 72 0.180, 80 0.187; Adam 90 0.180, 100 0.179, 110 0.1774, 120 0.178, 148 0.181 at gw2 64)
+  // (N = 10k sweep with PDL on and dg1's split count following this partition, ms per step at Adam
+  // 110: gw2 56 0.185, 64 0.1768, 72 0.1789, 76 0.1780, 80 0.1749, 84 0.1754, 88 0.188, 96 0.191;
+  // Adam 100 / 110 / 120 at gw2 80: 0.1755 / 0.1749 / 0.1767)
+  // (N = 5000: 64 SMs 0.1448 vs 80 SMs 0.1498 ms: dg1's 12 pair tiles split 3 ways vs 2; N = 1000
+  // and G(10^4, 3/4) within 1%: 80 from N = 8192 up, else 64 -- capi.cu vqmc_gpu_create)
   int gw2_sms = 64;
   int adam_w2_sms = 110;  // SMs' worth of blocks for the [W2 | b2] Adam beside dz1 -> gW1 (VQMC_ADAM_SMS)
   int gemm_sm_cap = 0;
