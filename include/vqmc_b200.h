@@ -209,9 +209,14 @@ int vqmc_gpu_set_phase_timing(vqmc_gpu_t* g, int level);
 int vqmc_gpu_set_graph(vqmc_gpu_t* g, int enable);
 
 /* Per-kernel CUDA-event timing of the last train step (roofline evidence):
- * names_out = count slots of 32 chars, ms_out = count durations. */
+ * names_out = count slots of 32 chars, ms_out = count durations.  enable = 1: the backward runs
+ * serially (every kernel timed alone); enable = 2: timeline mode, the production (concurrent)
+ * schedule with events on both streams. */
 int vqmc_gpu_set_kernel_timing(vqmc_gpu_t* g, int enable);
 int vqmc_gpu_kernel_times(vqmc_gpu_t* g, char* names_out, float* ms_out, int cap, int* count);
+/* Timeline mode (kernel timing 2, phase timing >= 1): each kernel's start / end event of the last
+ * step in ms after the step-start event (start = when its stream reached it). */
+int vqmc_gpu_kernel_timeline(vqmc_gpu_t* g, char* names_out, float* start_ms, float* end_ms, int cap, int* count);
 
 /* ---- Host utilities of the same library (C++; no GPU needed) ---- */
 

@@ -66,6 +66,7 @@ _SIGS = {
     "vqmc_gpu_phase_times": [_vp, _vp],
     "vqmc_gpu_set_kernel_timing": [_vp, C.c_int],
     "vqmc_gpu_kernel_times": [_vp, _vp, _vp, C.c_int, C.POINTER(C.c_int)],
+    "vqmc_gpu_kernel_timeline": [_vp, _vp, _vp, _vp, C.c_int, C.POINTER(C.c_int)],
     "vqmc_default_made_hidden": [C.c_int],
     "vqmc_made_init": [C.c_int, C.c_int, _u64, _vp, _vp],
     "vqmc_stream_uniforms": [_u64, _u64, _u64, _i64, _vp],

@@ -628,7 +628,7 @@ int vqmc_gpu_create(int device, int n, int h, const int32_t* degrees, const doub
   VQMC_CUDA(cudaMemset(H->d_done, 0, sizeof(unsigned)));
   dalloc(&H->d_wscale, 1);
   ensure_istat(H, 64);  // (d_scal, d_flag, d_istat and their host mirror)
-  H->gpart_n = 148 * 4;
+  H->gpart_n = 148 * 8;  // Adam ||g||^2 partials: part 0 (<= half) + part 1, or one whole launch (<= 592)
   dalloc(&H->d_gpart, (size_t)H->gpart_n);
   for (auto& e : H->ev) VQMC_CUDA(cudaEventCreate(&e));
   for (int i = 0; i < Handle::kKtPool; ++i) {
@@ -960,7 +960,7 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
   launch_weights_from_locals(H, B, minibatch, true);  // gradient_from_locals weights (:164) + w' G1 operand
   if (tm) record_event(H, H->ev[2]);
   const Layout& L = H->L;
-  if (H->concurrent_bw && !H->ktimer) {
+  if (H->concurrent_bw && H->ktimer != 1) {
     // weighted_grad_log_psi with its two independent halves concurrent: gW2 / gb2 (and, multi-GPU,
     // their all-reduce: 99% of the gradient bytes) on cstream with gw2_sms SMs, dg1 -> dz1 -> gW1
     // on the main stream with the rest; then the small W1 / b1 all-reduce and the join.
@@ -982,7 +982,8 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
     // adam_step (:221) on [W2 | b2] as soon as its gradient is reduced and dg1 is done: it overlaps
     // dz1 -> gW1 on the main stream
     VQMC_CUDA(cudaStreamWaitEvent(H->cstream, H->ev_dg1, 0));
-    launch_adam_part(H, 1.0f / (float)(workers * H->nranks), 0, H->cstream);
+    const float gs = 1.0f / (float)(workers * H->nranks);
+    launch_adam_part(H, gs, 0, H->cstream);
     VQMC_CUDA(cudaEventRecord(H->ev_join, H->cstream));
     launch_backward_after_dg1(H, B);
     H->gemm_sm_cap = 0;
@@ -991,7 +992,7 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
       nccl_check(g_nccl.AllReduce(H->G, H->G, (size_t)L.off_w2, ncclFloat32, ncclSum, H->nccl_comm, H->stream),
                  "ncclAllReduce (W1, b1)");
     if (tm) record_event(H, H->ev[4]);
-    launch_adam_part(H, 1.0f / (float)(workers * H->nranks), 1, H->stream);  // [W1T | b1]
+    launch_adam_part(H, gs, 1, H->stream);  // [W1T | b1]
     VQMC_CUDA(cudaStreamWaitEvent(H->stream, H->ev_join, 0));
     if (t0) record_event(H, H->ev[5]);
     return;
@@ -1369,7 +1370,23 @@ int vqmc_gpu_set_phase_timing(vqmc_gpu_t* g, int enable) {
 
 int vqmc_gpu_set_kernel_timing(vqmc_gpu_t* g, int enable) {
   API_TRY
-  reinterpret_cast<Handle*>(g)->ktimer = enable != 0;
+  reinterpret_cast<Handle*>(g)->ktimer = enable <= 0 ? 0 : enable >= 2 ? 2 : 1;
+  API_CATCH
+}
+
+int vqmc_gpu_kernel_timeline(vqmc_gpu_t* g, char* names_out, float* start_ms, float* end_ms, int cap, int* count) {
+  API_TRY
+  Handle* H = reinterpret_cast<Handle*>(g);
+  if (H->phase_timing < 1) throw std::invalid_argument("kernel timeline needs phase timing >= 1 (the step-start event)");
+  VQMC_CUDA(cudaDeviceSynchronize());
+  const int c = std::min(cap, H->kt_count);
+  for (int i = 0; i < c; ++i) {
+    VQMC_CUDA(cudaEventElapsedTime(&start_ms[i], H->ev[0], H->kt_start[i]));
+    VQMC_CUDA(cudaEventElapsedTime(&end_ms[i], H->ev[0], H->kt_end[i]));
+    std::strncpy(names_out + 32 * i, H->kt_name[i], 31);
+    names_out[32 * i + 31] = 0;
+  }
+  *count = c;
   API_CATCH
 }
 

@@ -153,8 +153,8 @@ static void launch_umma2(Handle* H, const char* name, const CUtensorMap& ah, con
   }
   cfg.attrs = at;
   cfg.numAttrs = na;
-  if (H && stream == H->stream) {  // (kernel timing events live on the handle's main stream)
-    KScope ks(H, name);
+  if (H && (stream == H->stream || H->ktimer == 2)) {  // (timeline mode: events on the side stream too)
+    KScope ks(H, name, stream);
     VQMC_CUDA(cudaLaunchKernelEx(&cfg, kern, ah, al, bh, bl, args, epi));
     H->launches++;
   } else {

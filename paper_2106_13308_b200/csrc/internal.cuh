@@ -87,6 +87,7 @@ struct SpecState;  // general Ising spec (TIM) and its scratch (spec.cu)
 // Timing event on the handle's stream; inside a graph capture it becomes an external event
 // record node so replays still record (and can be timed).
 void record_event(Handle* h, cudaEvent_t ev);
+void record_event_on(Handle* h, cudaEvent_t ev, cudaStream_t stream);
 
 // Per-step scalars kept in device memory so a captured CUDA graph of the step can be replayed:
 // they describe the step about to run; the step's last kernel (Adam) advances call / t and the
@@ -102,7 +103,8 @@ struct StepParams {
 struct KScope {
   Handle* H;
   int slot;
-  KScope(Handle* h, const char* name);
+  cudaStream_t s;
+  KScope(Handle* h, const char* name, cudaStream_t stream = nullptr);  // (nullptr: the handle's stream)
   ~KScope();
 };
 
@@ -306,7 +308,7 @@ struct Handle {
   struct GraphKey {
     bool valid = false;
     int minibatch = 0, workers = 0, phase_timing = 0;
-    bool ktimer = false;
+    int ktimer = 0;
     uint64_t seed = 0, stream0 = 0;
     bool operator==(const GraphKey& o) const {
       return valid && o.valid && minibatch == o.minibatch && workers == o.workers && phase_timing == o.phase_timing &&
@@ -348,7 +350,7 @@ struct Handle {
   float phase_ms[5] = {0, 0, 0, 0, 0};
 
   // per-kernel event timing (bench roofline): pool of event pairs reused each step
-  bool ktimer = false;
+  int ktimer = 0;  // 1: per-kernel events, serial backward; 2: timeline (events on both streams, concurrent schedule)
   static constexpr int kKtPool = 128;
   cudaEvent_t kt_start[kKtPool] = {}, kt_end[kKtPool] = {};
   const char* kt_name[kKtPool] = {};

@@ -554,6 +554,51 @@ __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __re
   }
 }
 
+// The end of every Adam block: the block's partial of
+// ||g||^2 into gpart[block_base + block]; the last of total_blocks blocks (shared done counter)
+// sums them in a fixed order, resets the counter and advances the device step counters.
+__device__ __forceinline__ void adam_block_finish(double sq, const StepParams* sp, double* __restrict__ gpart,
+                                                  int block_base, int total_blocks, unsigned* __restrict__ done,
+                                                  double* __restrict__ gnorm2) {
+  __shared__ double red[8];
+  __shared__ bool last;
+#pragma unroll
+  for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(kFull, sq, off);
+  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    gpart[block_base + blockIdx.x] = s;
+    __threadfence();
+    last = atomicAdd(done, 1u) == (unsigned)total_blocks - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  {  // fixed-order final sum by the last block: strided thread sums, then a fixed shuffle tree
+    __threadfence();
+    double s = 0.0;
+    for (int i = threadIdx.x; i < total_blocks; i += blockDim.x) s += ((volatile double*)gpart)[i];
+#pragma unroll
+    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
+    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    double s = 0.0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
+    *gnorm2 = s;
+    *done = 0u;
+    // advance the device step counters for the next step (every other block has read them):
+    // Philox call + 1, Adam t + 1 and its bias corrections (optimizer.cpp:28-29)
+    StepParams* w = const_cast<StepParams*>(sp);
+    w->call += 1;
+    w->t += 1;
+    w->bc1 = (float)(1.0 - pow((double)w->b1, (double)w->t));
+    w->bc2 = (float)(1.0 - pow((double)w->b2, (double)w->t));
+  }
+}
+
 // ===========================================================================
 // Adam over the live parameter buffer (optimizer.cpp:21-35), fp32 master
 // weights, gradient scaled by 1/L (allreduce_mean's division, trainer.cpp:334).
@@ -658,43 +703,7 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t lo, int64_t hi, fl
     adam_side_writes(o, t, p);
   }
   sq += (double)sqf;
-  __shared__ double red[8];
-  __shared__ bool last;
-#pragma unroll
-  for (int off = 16; off > 0; off >>= 1) sq += __shfl_xor_sync(kFull, sq, off);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = sq;
-  __syncthreads();
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-    gpart[block_base + blockIdx.x] = s;
-    __threadfence();
-    last = atomicAdd(done, 1u) == (unsigned)total_blocks - 1;
-  }
-  __syncthreads();
-  if (!last) return;
-  {  // fixed-order final sum by the last block: strided thread sums, then a fixed shuffle tree
-    __threadfence();
-    double s = 0.0;
-    for (int i = threadIdx.x; i < total_blocks; i += blockDim.x) s += ((volatile double*)gpart)[i];
-#pragma unroll
-    for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
-    if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
-    __syncthreads();
-  }
-  if (threadIdx.x == 0) {
-    double s = 0.0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
-    *gnorm2 = s;
-    *done = 0u;
-    // advance the device step counters for the next step (every other block has read them):
-    // Philox call + 1, Adam t + 1 and its bias corrections (optimizer.cpp:28-29)
-    StepParams* w = const_cast<StepParams*>(sp);
-    w->call += 1;
-    w->t += 1;
-    w->bc1 = (float)(1.0 - pow((double)w->b1, (double)w->t));
-    w->bc2 = (float)(1.0 - pow((double)w->b2, (double)w->t));
-  }
+  adam_block_finish(sq, sp, gpart, block_base, total_blocks, done, gnorm2);
 }
 
 __global__ void sum_partials_kernel(int cnt, const double* __restrict__ part, double* __restrict__ out) {
@@ -730,19 +739,20 @@ void ensure_smem_attr(const void* kern, size_t bytes) {
   have = bytes;
 }
 
-void record_event(Handle* H, cudaEvent_t ev) {
-  if (H->capturing) VQMC_CUDA(cudaEventRecordWithFlags(ev, H->stream, cudaEventRecordExternal));
-  else VQMC_CUDA(cudaEventRecord(ev, H->stream));
+void record_event_on(Handle* H, cudaEvent_t ev, cudaStream_t stream) {
+  if (H->capturing) VQMC_CUDA(cudaEventRecordWithFlags(ev, stream, cudaEventRecordExternal));
+  else VQMC_CUDA(cudaEventRecord(ev, stream));
 }
+void record_event(Handle* H, cudaEvent_t ev) { record_event_on(H, ev, H->stream); }
 
-KScope::KScope(Handle* h, const char* name) : H(h), slot(-1) {
+KScope::KScope(Handle* h, const char* name, cudaStream_t stream) : H(h), slot(-1), s(stream ? stream : h->stream) {
   if (!H->ktimer || H->kt_count >= Handle::kKtPool) return;
   slot = H->kt_count++;
   H->kt_name[slot] = name;
-  record_event(H, H->kt_start[slot]);
+  record_event_on(H, H->kt_start[slot], s);
 }
 KScope::~KScope() {
-  if (slot >= 0) record_event(H, H->kt_end[slot]);
+  if (slot >= 0) record_event_on(H, H->kt_end[slot], s);
 }
 
 // Derived device copies of the parameters (after set_params): the head sampler's staged
@@ -911,8 +921,9 @@ static AdamOut adam_out(const Handle* H, bool gated) {
 
 void launch_adam(Handle* H, float grad_scale, bool gated) {  // the whole live buffer in one launch
   KScope ks(H, "adam");
-  launch_k(H, adam_kernel, dim3(H->gpart_n), dim3(256), 0, (int64_t)0, H->L.total, grad_scale,
-           (const StepParams*)H->d_step, H->P, (const float*)H->G, H->Mo, H->Vo, H->d_gpart, 0, H->gpart_n, H->d_done,
+  const int nb = std::min(H->gpart_n, 148 * 4);  // (4 resident 256-thread blocks per SM)
+  launch_k(H, adam_kernel, dim3(nb), dim3(256), 0, (int64_t)0, H->L.total, grad_scale,
+           (const StepParams*)H->d_step, H->P, (const float*)H->G, H->Mo, H->Vo, H->d_gpart, 0, nb, H->d_done,
            H->d_scal, adam_out(H, gated));
   LAUNCH_CHECK();
   H->launches++;
@@ -923,10 +934,13 @@ void launch_adam(Handle* H, float grad_scale, bool gated) {  // the whole live b
 void launch_adam_part(Handle* H, float grad_scale, int part, cudaStream_t stream) {
   const Layout& L = H->L;
   // part 0 runs beside dz1 -> gW1: 4 blocks on each of the SMs gW2 used (4 x 256 threads fill an SM)
-  const int blocks0 = std::min(H->gpart_n - H->gpart_n / 16, 4 * std::max(2, H->adam_w2_sms));
-  const int blocks1 = H->gpart_n / 16;
+  const int blocks0 = std::min(H->gpart_n / 2, 4 * std::max(2, H->adam_w2_sms));
+  // part 1 ([W1T | b1], ~1% of the parameters) on 74 blocks: its time is mostly fixed (block
+  // partials, the last block's final sum); 37 / 74 / 148 blocks: 0.1749 / 0.1740 / 0.1744 ms per step
+  const int blocks1 = std::min(H->gpart_n - blocks0, H->gpart_n / 16);
   const int64_t lo = part == 0 ? L.off_w2 : 0, hi = part == 0 ? L.total : L.off_w2;
   const int nb = part == 0 ? blocks0 : blocks1;
+  KScope ks(H, part == 0 ? "adam_w2" : "adam_w1", stream);
   cudaLaunchConfig_t cfg{};
   cfg.gridDim = dim3(nb);
   cfg.blockDim = dim3(256);
@@ -1037,8 +1051,8 @@ extern "C" int vqmc_test_forward_rate(vqmc_gpu_t* g, int B, int iters, int mode,
     *ms_per_call = ms / std::max(1, iters);
     cudaEventDestroy(e0);
     cudaEventDestroy(e1);
-    const bool kt = H->ktimer;
-    H->ktimer = true;
+    const int kt = H->ktimer;
+    H->ktimer = 1;
     H->kt_count = 0;
     call();
     H->ktimer = kt;
