@@ -17,8 +17,8 @@ struct AdamHyper {
     b1 = sp->b1;
     b2 = sp->b2;
     eps = sp->eps;
-    ibc1 = 1.f / sp->bc1;
-    ibc2 = 1.f / sp->bc2;
+    ibc1 = sp->ibc1;  // (= 1.f / sp->bc1, formed once per step)
+    ibc2 = sp->ibc2;
   }
   // one element; g is already scaled by 1/L
   // (explicit roundings and FMAs: every kernel that inlines this gives bitwise the same update;

@@ -96,7 +96,9 @@ struct StepParams {
   uint64_t call;  // Philox counter of this step
   int64_t t;      // Adam step count of this step (1-based)
   float lr, b1, b2, eps;
-  float bc1, bc2;  // 1 - beta^t
+  float bc1, bc2;    // 1 - beta^t
+  float ibc1, ibc2;  // 1 / bc (fp32 division, once)
+  float nbc1, nbc2, nibc1, nibc2;  // the same for t + 1 (Adam's first block, off the step's tail)
 };
 
 // RAII per-kernel event pair (active only when Handle::ktimer is set).

@@ -594,8 +594,27 @@ __device__ __forceinline__ void adam_block_finish(double sq, const StepParams* s
     StepParams* w = const_cast<StepParams*>(sp);
     w->call += 1;
     w->t += 1;
-    w->bc1 = (float)(1.0 - pow((double)w->b1, (double)w->t));
-    w->bc2 = (float)(1.0 - pow((double)w->b2, (double)w->t));
+    w->bc1 = w->nbc1;  // (formed for t + 1 by the first Adam block: adam_next_bias)
+    w->bc2 = w->nbc2;
+    w->ibc1 = w->nibc1;
+    w->ibc2 = w->nibc2;
+  }
+}
+
+// Bias corrections of step t (optimizer.cpp:28-29) and their reciprocals.
+__device__ __forceinline__ void adam_bias(float b1, float b2, int64_t t, float& bc1, float& bc2, float& ibc1,
+                                          float& ibc2) {
+  bc1 = (float)(1.0 - pow((double)b1, (double)t));
+  bc2 = (float)(1.0 - pow((double)b2, (double)t));
+  ibc1 = 1.f / bc1;
+  ibc2 = 1.f / bc2;
+}
+// Thread 0 of the first Adam block: the next step's bias corrections (two fp64 pows) while the
+// other blocks run, so the last block only copies them.
+__device__ __forceinline__ void adam_next_bias(const StepParams* sp, int block_base) {
+  if (block_base == 0 && blockIdx.x == 0 && threadIdx.x == 0) {
+    StepParams* w = const_cast<StepParams*>(sp);
+    adam_bias(w->b1, w->b2, w->t + 1, w->nbc1, w->nbc2, w->nibc1, w->nibc2);
   }
 }
 
@@ -624,6 +643,7 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t lo, int64_t hi, fl
   ptx::pdl_wait();
   AdamHyper hp;
   hp.load(sp);
+  adam_next_bias(sp, block_base);
   float sqf = 0.f;  // fp32 partial of ||g||^2 per element group, summed into fp64 per thread
   double sq = 0.0;
   auto upd = [&](float g, float& m, float& v, float& p) {
@@ -900,8 +920,8 @@ __global__ void set_step_kernel(StepParams* sp, uint64_t call, int64_t t, float 
   sp->b1 = b1;
   sp->b2 = b2;
   sp->eps = eps;
-  sp->bc1 = (float)(1.0 - pow((double)b1, (double)t));
-  sp->bc2 = (float)(1.0 - pow((double)b2, (double)t));
+  adam_bias(b1, b2, t, sp->bc1, sp->bc2, sp->ibc1, sp->ibc2);
+  adam_bias(b1, b2, t + 1, sp->nbc1, sp->nbc2, sp->nibc1, sp->nibc2);
 }
 
 void launch_set_step(Handle* H, uint64_t call, int64_t t, double lr, double b1, double b2, double eps) {
