@@ -570,13 +570,14 @@ __device__ __forceinline__ void adam_block_finish(double sq, const StepParams* s
     double s = 0.0;
     for (int i = 0; i < (int)(blockDim.x >> 5); ++i) s += red[i];
     gpart[block_base + blockIdx.x] = s;
-    __threadfence();
-    last = atomicAdd(done, 1u) == (unsigned)total_blocks - 1;
+    unsigned prev;  // acq_rel: publishes this block's partial, and (last block) acquires everyone's
+    asm volatile("atom.acq_rel.gpu.global.add.u32 %0, [%1], 1;" : "=r"(prev) : "l"(done) : "memory");
+    last = prev == (unsigned)total_blocks - 1;
   }
   __syncthreads();
   if (!last) return;
   {  // fixed-order final sum by the last block: strided thread sums, then a fixed shuffle tree
-    __threadfence();
+    __threadfence();  // (orders the other threads' reads after thread 0's acquire)
     double s = 0.0;
     for (int i = threadIdx.x; i < total_blocks; i += blockDim.x) s += ((volatile double*)gpart)[i];
 #pragma unroll
@@ -965,6 +966,13 @@ void launch_adam_part(Handle* H, float grad_scale, int part, cudaStream_t stream
   cfg.gridDim = dim3(nb);
   cfg.blockDim = dim3(256);
   cfg.stream = stream;
+  cudaLaunchAttribute at[1];
+  if (H->pdl) {  // (adam_kernel waits before touching global memory)
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+  }
   VQMC_CUDA(cudaLaunchKernelEx(&cfg, adam_kernel, lo, hi, grad_scale, (const StepParams*)H->d_step, H->P,
                                (const float*)H->G, H->Mo, H->Vo, H->d_gpart, part == 0 ? 0 : blocks0, blocks0 + blocks1,
                                H->d_done, H->d_scal, adam_out(H, true)));
