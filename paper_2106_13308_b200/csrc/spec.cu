@@ -236,8 +236,9 @@ __global__ void __launch_bounds__(256) spec_diag_kernel(int B, int n, const uint
   if (blockIdx.y == 0)
     for (int i = tid; i < n; i += blockDim.x) add(T[i], beta[i]);  // x_i ? +beta : -beta
   if (dense) {
-    // row pairs (i, n - 2 - i), i < (n - 1) / 2 (+ the middle row when n - 1 is odd); 8 loads in
-    // flight per lane (at B = 4 the walk is a pure stream of the n^2/2 values: latency-bound with 4)
+    // row pairs (i, n - 2 - i), i < (n - 1) / 2 (+ the middle row when n - 1 is odd); 16 loads in
+    // flight per lane for <= 4 samples per CTA, else 8 (at B = 4 the walk is a pure stream of the
+    // n^2/2 values: latency-bound)
     const int64_t r0 = (int64_t)blockIdx.y * per_chunk, r1 = min((int64_t)(n / 2), r0 + per_chunk);
     for (int64_t rp = r0 + warp; rp < r1; rp += 8) {
       for (int half = 0; half < 2; ++half) {
@@ -246,6 +247,14 @@ __global__ void __launch_bounds__(256) spec_diag_kernel(int B, int n, const uint
         const double* row = pv + ((int64_t)i * n - (int64_t)i * (i + 1) / 2) - (i + 1);  // row[j], j > i
         const uint32_t ti = T[i];
         int j = i + 1 + lane;
+        constexpr int D = G <= 4 ? 16 : 8;  // loads in flight per lane (few accumulators: go deeper)
+        for (; j + 32 * (D - 1) < n; j += 32 * D) {
+          double v[D];
+#pragma unroll
+          for (int u = 0; u < D; ++u) v[u] = row[j + 32 * u];
+#pragma unroll
+          for (int u = 0; u < D; ++u) add(ti ^ T[j + 32 * u], v[u]);
+        }
         for (; j + 224 < n; j += 256) {
           double v[8];
 #pragma unroll
