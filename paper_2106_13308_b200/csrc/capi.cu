@@ -346,12 +346,18 @@ static void ensure_istat(Handle* H, int segs) {
 
 // one copy of the step's results (||g||^2, flag, cut statistics of `segs` segments, and with a
 // communicator the reduced statistics limbs of all ranks); blocks
-static void read_step_results(Handle* H, int segs) {
+// The step's scalar results (grad norm, flag, per-segment cut sums; multi-GPU: the all-reduced
+// statistics limbs) into the pinned host mirrors.  Captured into the step's graph, so a replay
+// ends with them already copied.
+static void enqueue_results_copy(Handle* H, int segs) {
   VQMC_CUDA(cudaMemcpyAsync(H->h_scal, H->d_scal, (16 + (size_t)3 * segs) * 8, cudaMemcpyDeviceToHost, H->stream));
   if (H->nccl_comm)
     VQMC_CUDA(cudaMemcpyAsync(H->h_rstat, H->G + H->L.total, rstat_count(H->nranks) * sizeof(float),
                               cudaMemcpyDeviceToHost, H->stream));
-  VQMC_CUDA(cudaStreamSynchronize(H->stream));
+}
+static void read_step_results(Handle* H, int segs, bool copied = false) {
+  if (!copied) enqueue_results_copy(H, segs);
+  VQMC_CUDA(cudaStreamSynchronize(H->stream));  // (a busy-wait measured the same)
   check_flag(H, *reinterpret_cast<const uint32_t*>(H->h_scal + 8));
 }
 
@@ -1104,10 +1110,12 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
   key.ktimer = H->ktimer;
   key.seed = seed;
   key.stream0 = stream0;
+  bool copied = false;
   if (!graphable) {
     enqueue_train_step(H, minibatch, workers, uniforms, seed, stream0);
   } else if (H->gexec && H->gkey == key) {
     VQMC_CUDA(cudaGraphLaunch(H->gexec, H->stream));  // replay the captured step
+    copied = true;
   } else if (!H->graph_warm || !(H->gkey == key)) {
     if (H->gexec) {
       cudaGraphExecDestroy(H->gexec);
@@ -1122,6 +1130,7 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
     H->capturing = true;
     try {
       enqueue_train_step(H, minibatch, workers, uniforms, seed, stream0);
+      enqueue_results_copy(H, workers);  // (the replay ends with the scalars on the host)
       H->capturing = false;
     } catch (...) {
       H->capturing = false;
@@ -1134,11 +1143,12 @@ int vqmc_gpu_train_step(vqmc_gpu_t* g, int minibatch, int workers, const double*
     cudaGraphDestroy(graph);
     H->gkey = key;
     VQMC_CUDA(cudaGraphLaunch(H->gexec, H->stream));
+    copied = true;
   }
   H->next_call = call + 1;
   H->next_t = t + 1;
   if (stats_out) {
-    read_step_results(H, workers);
+    read_step_results(H, workers, copied);
     const CutTotals t = step_totals(H, workers, B);
     pooled_stats(H->num_edges, t.N, t.cs, t.cq, &stats_out->energy_mean, &stats_out->energy_var);
     stats_out->grad_norm = std::sqrt(H->h_scal[0]);
