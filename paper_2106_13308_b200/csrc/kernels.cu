@@ -663,50 +663,55 @@ __global__ void __launch_bounds__(256, 4) adam_kernel(int64_t lo, int64_t hi, fl
   P += 4 * q_lo;
   const int64_t t_off = 4 * q_lo;  // element index of the shifted base
   const int64_t w2_bulk0 = (int64_t)o.Hd * o.h, w2_end = o.off_b2 - o.off_w2;  // W2 rows >= Hd
-  constexpr int U = 2;  // float4 groups per thread per iteration: all loads in flight before any math
-  for (int64_t q0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; q0 < nq; q0 += U * stride) {
-    float4 g4[U], m4[U], v4[U], p4[U];
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t q = q0 + u * stride;
-      if (q < nq) {
-        g4[u] = reinterpret_cast<const float4*>(G)[q];
-        m4[u] = reinterpret_cast<float4*>(M)[q];
-        v4[u] = reinterpret_cast<float4*>(V)[q];
-        p4[u] = reinterpret_cast<float4*>(P)[q];
-      }
+  // one float4 group per thread per iteration, the next group's loads issued before this one's math
+  // (software pipelining: the loads stay in flight through the update arithmetic)
+  int64_t q = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  float4 g4, m4, v4, p4;
+  if (q < nq) {
+    g4 = reinterpret_cast<const float4*>(G)[q];
+    m4 = reinterpret_cast<float4*>(M)[q];
+    v4 = reinterpret_cast<float4*>(V)[q];
+    p4 = reinterpret_cast<float4*>(P)[q];
+  }
+  for (; q < nq; q += stride) {
+    const int64_t qn = q + stride;
+    float4 gn, mn, vn, pn;
+    if (qn < nq) {
+      gn = reinterpret_cast<const float4*>(G)[qn];
+      mn = reinterpret_cast<float4*>(M)[qn];
+      vn = reinterpret_cast<float4*>(V)[qn];
+      pn = reinterpret_cast<float4*>(P)[qn];
     }
-#pragma unroll
-    for (int u = 0; u < U; ++u) {
-      const int64_t q = q0 + u * stride;
-      if (q >= nq) break;
-      upd(g4[u].x, m4[u].x, v4[u].x, p4[u].x);
-      upd(g4[u].y, m4[u].y, v4[u].y, p4[u].y);
-      upd(g4[u].z, m4[u].z, v4[u].z, p4[u].z);
-      upd(g4[u].w, m4[u].w, v4[u].w, p4[u].w);
-      reinterpret_cast<float4*>(M)[q] = m4[u];
-      reinterpret_cast<float4*>(V)[q] = v4[u];
-      reinterpret_cast<float4*>(P)[q] = p4[u];
-      const int64_t t = t_off + 4 * q;
-      const int64_t w = t - o.off_w2;
-      if (o.vec_w2 && w >= w2_bulk0 && w < w2_end) {
-        // bulk of W2 (rows >= Hd): 4 consecutive entries of one row -> 8-byte stores of both halves
-        unsigned i, k;
-        w2_row(o, (unsigned)w, i, k);
-        uint2 hi, lo;
-        ptx::split_f16x2(p4[u].x, p4[u].y, hi.x, lo.x);
-        ptx::split_f16x2(p4[u].z, p4[u].w, hi.y, lo.y);
-        *reinterpret_cast<uint2*>(o.W2h + (size_t)i * o.hp18 + k) = hi;
-        *reinterpret_cast<uint2*>(o.W2l + (size_t)i * o.hp18 + k) = lo;
-      } else {
-        adam_side_writes(o, t, p4[u].x);
-        adam_side_writes(o, t + 1, p4[u].y);
-        adam_side_writes(o, t + 2, p4[u].z);
-        adam_side_writes(o, t + 3, p4[u].w);
-      }
+    upd(g4.x, m4.x, v4.x, p4.x);
+    upd(g4.y, m4.y, v4.y, p4.y);
+    upd(g4.z, m4.z, v4.z, p4.z);
+    upd(g4.w, m4.w, v4.w, p4.w);
+    reinterpret_cast<float4*>(M)[q] = m4;
+    reinterpret_cast<float4*>(V)[q] = v4;
+    reinterpret_cast<float4*>(P)[q] = p4;
+    const int64_t t = t_off + 4 * q;
+    const int64_t w = t - o.off_w2;
+    if (o.vec_w2 && w >= w2_bulk0 && w < w2_end) {
+      // bulk of W2 (rows >= Hd): 4 consecutive entries of one row -> 8-byte stores of both halves
+      unsigned i, k;
+      w2_row(o, (unsigned)w, i, k);
+      uint2 hi, lo;
+      ptx::split_f16x2(p4.x, p4.y, hi.x, lo.x);
+      ptx::split_f16x2(p4.z, p4.w, hi.y, lo.y);
+      *reinterpret_cast<uint2*>(o.W2h + (size_t)i * o.hp18 + k) = hi;
+      *reinterpret_cast<uint2*>(o.W2l + (size_t)i * o.hp18 + k) = lo;
+    } else {
+      adam_side_writes(o, t, p4.x);
+      adam_side_writes(o, t + 1, p4.y);
+      adam_side_writes(o, t + 2, p4.z);
+      adam_side_writes(o, t + 3, p4.w);
     }
-    sq += (double)sqf;  // (at most 8 fp32 terms per partial: ||g||^2 keeps ~fp32-grade relative error)
+    sq += (double)sqf;  // (4 fp32 terms per partial: ||g||^2 keeps ~fp32-grade relative error)
     sqf = 0.f;
+    g4 = gn;
+    m4 = mn;
+    v4 = vn;
+    p4 = pn;
   }
   G -= t_off;
   M -= t_off;
