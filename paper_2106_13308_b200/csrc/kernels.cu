@@ -492,17 +492,18 @@ __global__ void dz1_kernel(int B, int h, int hp, int splits, const float* __rest
   const size_t t4 = 4 * ((size_t)blockIdx.x * blockDim.x + threadIdx.x);
   if (t4 >= total) return;
   if ((h & 3) == 0) {
+    const int b = (int)(t4 / h), k = (int)(t4 % h);
+    const float4 g = *reinterpret_cast<const float4*>(G1 + t4);
+    const float wb = w[b];
     float4 s = make_float4(0.f, 0.f, 0.f, 0.f);
-    for (int z = 0; z < splits; ++z) {
+#pragma unroll 4
+    for (int z = 0; z < splits; ++z) {  // (unrolled: the partials' loads in flight together, same order of adds)
       const float4 p = *reinterpret_cast<const float4*>(Epart + (size_t)z * total + t4);
       s.x += p.x;
       s.y += p.y;
       s.z += p.z;
       s.w += p.w;
     }
-    const int b = (int)(t4 / h), k = (int)(t4 % h);
-    const float4 g = *reinterpret_cast<const float4*>(G1 + t4);
-    const float wb = w[b];
     const float d[4] = {g.x > 0.f ? s.x * wb : 0.f, g.y > 0.f ? s.y * wb : 0.f, g.z > 0.f ? s.z * wb : 0.f,
                         g.w > 0.f ? s.w * wb : 0.f};  // relu'(z1) = [z1 > 0] (models.cpp:181)
     __nv_bfloat16 hi[4], lo[4];
@@ -535,6 +536,7 @@ __global__ void gw1_finalize_kernel(int h, int Hd, int splits, const float* __re
   for (int t = t4; t < t4 + 4 && t < total; t += n4) {
     float s[4] = {0.f, 0.f, 0.f, 0.f};
     if (n4 == 4) {
+#pragma unroll 4
       for (int z = 0; z < splits; ++z) {
         const float4 p = *reinterpret_cast<const float4*>(part + (size_t)z * total + t);
         s[0] += p.x;
