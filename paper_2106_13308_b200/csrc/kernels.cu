@@ -351,6 +351,7 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
         lb = lin[base + b];
         s2 += lb * lb;
       } else {
+#pragma unroll 4
         for (int k = 0; k < chunks; ++k) c += cpart[(size_t)k * B + base + b];
         lb = 0.25 * ((double)nE - 2.0 * (double)c);  // l_b = (|E| - 2 cut_b) / 4, exact
       }
@@ -409,6 +410,7 @@ __global__ void __launch_bounds__(1024) stats_weights_kernel(int segs, int seg, 
         lb = lin[base + b];
       } else {
         int c = 0;
+#pragma unroll 4
         for (int k = 0; k < chunks; ++k) c += cpart[(size_t)k * B + base + b];
         lb = 0.25 * ((double)nE - 2.0 * (double)c);
       }
