@@ -189,11 +189,11 @@ struct StoreEpi {  // test: C[row][col] = acc
 // pair; Philox keys are per row.  The epilogue warp sets take alternate 32-column chunks and
 // each writes its own log-prob partial (lp_part[kParts * tile + part]): deterministic.
 // (kTailBN: internal.cuh)
-// kTailCh: accumulator columns per epilogue call of the tail sampler; with 16-column chunks the
-// 12 chunks of a 192-column tile split evenly over 4 epilogue sets (16 epilogue warps), with
-// 32-column chunks over 3 sets.
+// kTailCh: accumulator columns per epilogue call of the tail sampler; the 12 16-column chunks of a
+// 192-column tile split evenly over 3 epilogue sets (12 epilogue warps at up to 128 registers:
+// 43.0 us; 4 sets at 96 registers: 44.3 us).
 constexpr int kTailCh = 16;
-constexpr int kTailSets = kTailCh == 16 ? 4 : 0;
+constexpr int kTailSets = kTailCh == 16 ? 3 : 0;
 template <bool PROD>  // PROD: production draws (Philox) and no log-probabilities (the training step)
 struct TailSampleEpiT {
   static constexpr int CH = kTailCh;
