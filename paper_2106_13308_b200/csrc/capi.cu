@@ -278,6 +278,7 @@ static void ensure_side_stream(Handle* H) {
   VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_fork, cudaEventDisableTiming));
   VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_join, cudaEventDisableTiming));
   VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_dg1, cudaEventDisableTiming));
+  VQMC_CUDA(cudaEventCreateWithFlags(&H->ev_dz1, cudaEventDisableTiming));
 }
 
 static void check_B(int B) {
@@ -667,6 +668,7 @@ int vqmc_gpu_destroy(vqmc_gpu_t* g) {
   if (H->ev_fork) cudaEventDestroy(H->ev_fork);
   if (H->ev_join) cudaEventDestroy(H->ev_join);
   if (H->ev_dg1) cudaEventDestroy(H->ev_dg1);
+  if (H->ev_dz1) cudaEventDestroy(H->ev_dz1);
   free_sr(H);
   free_dense_energy(H);
   spec_free(H);
@@ -985,13 +987,14 @@ static void enqueue_train_step(Handle* H, int minibatch, int workers, const doub
     H->gemm_sm_cap = avail - std::min(H->gw2_sms, avail - 16);
     launch_dg1_umma(H, B);  // the step's last read of the W2 operand pairs
     VQMC_CUDA(cudaEventRecord(H->ev_dg1, H->stream));
-    // adam_step (:221) on [W2 | b2] as soon as its gradient is reduced and dg1 is done: it overlaps
-    // dz1 -> gW1 on the main stream
-    VQMC_CUDA(cudaStreamWaitEvent(H->cstream, H->ev_dg1, 0));
     const float gs = 1.0f / (float)(workers * H->nranks);
+    // adam_step (:221) on [W2 | b2] once its gradient is reduced and dz1 (after dg1, the last
+    // reader of the W2 pairs) is done: gW1's CTAs, enqueued first, take the SMs before Adam's
+    // blocks fill them (gW1 15 vs 29 us; step -2 us vs starting Adam right after dg1)
+    launch_backward_after_dg1(H, B, H->ev_dz1);
+    VQMC_CUDA(cudaStreamWaitEvent(H->cstream, H->ev_dz1, 0));
     launch_adam_part(H, gs, 0, H->cstream);
     VQMC_CUDA(cudaEventRecord(H->ev_join, H->cstream));
-    launch_backward_after_dg1(H, B);
     H->gemm_sm_cap = 0;
     if (tm) record_event(H, H->ev[3]);
     if (H->nccl_comm)

@@ -139,7 +139,8 @@ void launch_weights_from_locals(Handle* h, int B, int seg, bool with_wg1 = false
 void launch_cuts_reduce(Handle* h, int B);
 void launch_backward(Handle* h, int B, bool wg1_done = false);
 void launch_backward_tail(Handle* h, int B);  // dg1, dz1, gW1 (+ finalize)
-void launch_backward_after_dg1(Handle* h, int B);  // dz1, gW1 (+ finalize)
+// dz1, gW1 (+ finalize); after_dz1 (optional) is recorded on the stream between dz1 and gW1
+void launch_backward_after_dg1(Handle* h, int B, cudaEvent_t after_dz1 = nullptr);
 void launch_dg1_umma(Handle* h, int B);
 int gemm_sms(const Handle* h);  // SMs the persistent GEMMs may use
 void launch_tail_umma(Handle* h, int B, const double* d_uniforms, RngSpec rng, bool want_lp);
@@ -331,7 +332,7 @@ struct Handle {
   void* nccl_comm = nullptr;
   int nranks = 1, rank = 0;
   cudaStream_t cstream = nullptr;
-  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_dg1 = nullptr;
+  cudaEvent_t ev_fork = nullptr, ev_join = nullptr, ev_dg1 = nullptr, ev_dz1 = nullptr;
   int gemm_sm_reserve = 0;
   // concurrent backward: gW2 (and its all-reduce) on cstream with gw2_sms SMs while dg1 -> dz1 ->
   // gW1 use the rest (gemm_sm_cap limits the persistent GEMM grids; 0 = no cap)
@@ -342,7 +343,8 @@ struct Handle {
   // (N = 5000: 64 SMs 0.1448 vs 80 SMs 0.1498 ms: dg1's 12 pair tiles split 3 ways vs 2; N = 1000
   // and G(10^4, 3/4) within 1%: 80 from N = 8192 up, else 64 -- capi.cu vqmc_gpu_create)
   int gw2_sms = 64;
-  int adam_w2_sms = 110;  // SMs' worth of blocks for the [W2 | b2] Adam beside dz1 -> gW1 (VQMC_ADAM_SMS)
+  // (started after dz1: 110 0.1707, 130 0.1696, 140 0.1702, 148 0.1700 ms)
+  int adam_w2_sms = 130;  // SMs' worth of blocks for the [W2 | b2] Adam beside gW1 (VQMC_ADAM_SMS)
   int gemm_sm_cap = 0;
   int gw1_splits = 4;  // max split-K of the gW1 GEMM (1: direct epilogue, no finalize; VQMC_GW1_SPLITS; 4 measured best)
 

@@ -897,7 +897,7 @@ void launch_backward_tail(Handle* H, int B) {
 }
 
 // dz1 -> gW1 (+ finalize)
-void launch_backward_after_dg1(Handle* H, int B) {
+void launch_backward_after_dg1(Handle* H, int B, cudaEvent_t after_dz1) {
   using namespace bwcfg;
   const Layout& L = H->L;
   {
@@ -908,6 +908,7 @@ void launch_backward_after_dg1(Handle* H, int B) {
     LAUNCH_CHECK();
     H->launches++;
   }
+  if (after_dz1) VQMC_CUDA(cudaEventRecord(after_dz1, H->stream));
   {
     int splits = 1;
     launch_gw1_umma(H, B, splits);  // gW1 (tcgen05): direct epilogue, or split-K partials
