@@ -583,7 +583,8 @@ __device__ __forceinline__ void adam_block_finish(double sq, const StepParams* s
   {  // fixed-order final sum by the last block: strided thread sums, then a fixed shuffle tree
     __threadfence();  // (orders the other threads' reads after thread 0's acquire)
     double s = 0.0;
-    for (int i = threadIdx.x; i < total_blocks; i += blockDim.x) s += ((volatile double*)gpart)[i];
+#pragma unroll 4
+    for (int i = threadIdx.x; i < total_blocks; i += blockDim.x) s += __ldcg(gpart + i);  // (L2: other blocks' partials)
 #pragma unroll
     for (int off = 16; off > 0; off >>= 1) s += __shfl_xor_sync(kFull, s, off);
     if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
@@ -966,9 +967,9 @@ void launch_adam_part(Handle* H, float grad_scale, int part, cudaStream_t stream
   const Layout& L = H->L;
   // part 0 runs beside dz1 -> gW1: 4 blocks on each of the SMs gW2 used (4 x 256 threads fill an SM)
   const int blocks0 = std::min(H->gpart_n / 2, 4 * std::max(2, H->adam_w2_sms));
-  // part 1 ([W1T | b1], ~1% of the parameters) on 74 blocks: its time is mostly fixed (block
-  // partials, the last block's final sum); 37 / 74 / 148 blocks: 0.1749 / 0.1740 / 0.1744 ms per step
-  const int blocks1 = std::min(H->gpart_n - blocks0, H->gpart_n / 16);
+  // part 1 ([W1T | b1], ~1% of the parameters) on 148 blocks: one float4 group per thread (its time
+  // is mostly load latency and the last block's final sum: 17.6 -> 15.3 us vs 74 blocks)
+  const int blocks1 = std::min(H->gpart_n - blocks0, H->gpart_n / 8);
   const int64_t lo = part == 0 ? L.off_w2 : 0, hi = part == 0 ? L.total : L.off_w2;
   const int nb = part == 0 ? blocks0 : blocks1;
   KScope ks(H, part == 0 ? "adam_w2" : "adam_w1", stream);
