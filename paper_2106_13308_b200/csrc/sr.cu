@@ -207,14 +207,17 @@ __device__ __forceinline__ int pmax_exp(const unsigned* pmax) {
 __global__ void sr_split_kernel(int n, int h, int ld, const double* __restrict__ p, int64_t off_w2, int64_t off_b2,
                                 const int32_t* __restrict__ deg, const unsigned* __restrict__ pmax,
                                 __half* __restrict__ hi, __half* __restrict__ lo) {
-  const int i = blockIdx.y, c = blockIdx.x * blockDim.x + threadIdx.x;  // row i, column c
-  if (i >= n || c >= ld) return;
-  const size_t t = (size_t)i * ld + c;
-  const int e = pmax_exp(pmax);
-  double x = 0.0;
-  if (c < h) x = deg[c] < i + 1 ? p[off_w2 + (int64_t)i * h + c] : 0.0;  // M2(i, c)
-  else if (c == h) x = p[off_b2 + i];
-  ptx::split_f16((float)ldexp(x, -e), hi[t], lo[t]);
+  // one CTA per row i (columns strided over the threads); x 2^-e as one exact fp64 multiply
+  const int i = blockIdx.x;
+  if (i >= n) return;
+  const double sc = ldexp(1.0, -pmax_exp(pmax));
+  for (int c = threadIdx.x; c < ld; c += blockDim.x) {
+    double x = 0.0;
+    if (c < h) x = deg[c] < i + 1 ? p[off_w2 + (int64_t)i * h + c] : 0.0;  // M2(i, c)
+    else if (c == h) x = p[off_b2 + i];
+    const size_t t = (size_t)i * ld + c;
+    ptx::split_f16((float)(x * sc), hi[t], lo[t]);
+  }
 }
 
 // dz1 = (D W2m) relu'(z1) of the batch (unweighted; fixed during a solve), from dg1's split-K partials
@@ -544,7 +547,7 @@ double sum_parts(Handle* H, const double* part, int cnt) {
 // batch's G1 / D / X and dg1 partials.
 void apply_fisher(Handle* H, int B, bool centered) {
   const Layout& L = H->L;
-  sr_split_kernel<<<dim3((unsigned)((H->hp18 + 127) / 128), (unsigned)L.n), 128, 0, H->stream>>>(L.n, L.h, H->hp18, H->cg_p, L.off_w2,
+  sr_split_kernel<<<(unsigned)L.n, 128, 0, H->stream>>>(L.n, L.h, H->hp18, H->cg_p, L.off_w2,
                                                                          L.off_b2, H->d_deg, H->d_pmax, H->SRh,
                                                                          H->SRl);
   SR_CHECK();
