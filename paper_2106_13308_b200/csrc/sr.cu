@@ -240,46 +240,50 @@ __global__ void sr_p1f_kernel(int Hd, int h, int ld, const double* __restrict__ 
 }
 
 // W1 half of q without the bias term: sum_k dz1_b[k] sum_{j: x_b[j] = 1} P1f[j][k], one CTA per
-// sample, 16-byte row loads, four set bits in flight.  part[b] (one partial per sample).
-constexpr int kQ1Threads = 128, kQ1Per = kMaxHidden / (4 * kQ1Threads);
+// sample, 16-byte row loads.  part[b] (one partial per sample).
+constexpr int kQ1Threads = 128;
+// Warp w takes the spin words m = w, w + 4, ...: the CTA's four warps walk four disjoint sets of
+// rows at once (a quarter of the serial L2 round trips of one row set per CTA); lane l holds the
+// float4 columns l + 32 u (U of them), R set-bit rows in flight per lane.
+template <int U, int R>
 __global__ void __launch_bounds__(kQ1Threads) sr_q1_kernel(int B, int h, int Hd, int W, int ld,
                                                            const uint32_t* __restrict__ X, const float* __restrict__ dz1,
                                                            const float* __restrict__ P1f, double* __restrict__ part) {
-  const int b = blockIdx.x;
-  float4 acc[kQ1Per];
+  const int b = blockIdx.x, warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  float4 acc[U];
 #pragma unroll
-  for (int u = 0; u < kQ1Per; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
+  for (int u = 0; u < U; ++u) acc[u] = make_float4(0.f, 0.f, 0.f, 0.f);
   const int nq = ld / 4;  // float4 columns per row
-  int jl[4];
+  int jl[R];
   int cnt = 0;
   auto flush = [&](int n) {
-    float4 v[4][kQ1Per];
+    float4 v[R][U];
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int u = 0; u < kQ1Per; ++u) {
-        const int c = threadIdx.x + kQ1Threads * u;
+      for (int u = 0; u < U; ++u) {
+        const int c = lane + 32 * u;
         v[r][u] = (r < n && c < nq) ? reinterpret_cast<const float4*>(P1f + (size_t)jl[r] * ld)[c]
                                     : make_float4(0.f, 0.f, 0.f, 0.f);
       }
 #pragma unroll
-    for (int r = 0; r < 4; ++r)
+    for (int r = 0; r < R; ++r)
 #pragma unroll
-      for (int u = 0; u < kQ1Per; ++u) {
+      for (int u = 0; u < U; ++u) {
         acc[u].x += v[r][u].x;
         acc[u].y += v[r][u].y;
         acc[u].z += v[r][u].z;
         acc[u].w += v[r][u].w;
       }
   };
-  for (int w = 0; w * 32 < Hd; ++w) {
+  for (int w = warp; w * 32 < Hd; w += kQ1Threads / 32) {
     uint32_t bits = X[(size_t)b * W + w];
     if (Hd - 32 * w < 32) bits &= (1u << (Hd - 32 * w)) - 1u;
     while (bits) {
       jl[cnt++] = 32 * w + __ffs(bits) - 1;
       bits &= bits - 1u;
-      if (cnt == 4) {
-        flush(4);
+      if (cnt == R) {
+        flush(R);
         cnt = 0;
       }
     }
@@ -287,20 +291,20 @@ __global__ void __launch_bounds__(kQ1Threads) sr_q1_kernel(int B, int h, int Hd,
   if (cnt) flush(cnt);
   double s = 0.0;
 #pragma unroll
-  for (int u = 0; u < kQ1Per; ++u) {
-    const int c = threadIdx.x + kQ1Threads * u;
+  for (int u = 0; u < U; ++u) {
+    const int c = lane + 32 * u;
     if (c < nq) {
       const float* d = dz1 + (size_t)b * h + 4 * c;  // (rows of h floats: not 16-byte aligned in general)
-      const float a[4] = {acc[u].x, acc[u].y, acc[u].z, acc[u].w};
+      const float a4[4] = {acc[u].x, acc[u].y, acc[u].z, acc[u].w};
 #pragma unroll
       for (int i = 0; i < 4; ++i)
-        if (4 * c + i < h) s += (double)d[i] * a[i];
+        if (4 * c + i < h) s += (double)d[i] * a4[i];
     }
   }
   __shared__ double red[kQ1Threads / 32];
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(kFull, s, o);
-  if ((threadIdx.x & 31) == 0) red[threadIdx.x >> 5] = s;
+  if (lane == 0) red[warp] = s;
   __syncthreads();
   if (threadIdx.x == 0) {
     double t = 0.0;
@@ -557,7 +561,10 @@ void apply_fisher(Handle* H, int B, bool centered) {
     const int64_t tp = (int64_t)L.Hd * ld;
     sr_p1f_kernel<<<(unsigned)((tp + 255) / 256), 256, 0, H->stream>>>(L.Hd, L.h, ld, H->cg_p + L.off_w1t, H->d_deg,
                                                                        H->sr_p1f);
-    sr_q1_kernel<<<B, kQ1Threads, 0, H->stream>>>(B, L.h, L.Hd, L.W, ld, H->X, H->sr_dz1, H->sr_p1f, H->sr_q1);
+    if (ld / 4 <= 128)
+      sr_q1_kernel<4, 4><<<B, kQ1Threads, 0, H->stream>>>(B, L.h, L.Hd, L.W, ld, H->X, H->sr_dz1, H->sr_p1f, H->sr_q1);
+    else
+      sr_q1_kernel<8, 2><<<B, kQ1Threads, 0, H->stream>>>(B, L.h, L.Hd, L.W, ld, H->X, H->sr_dz1, H->sr_p1f, H->sr_q1);
     sr_q_kernel<<<(B + 7) / 8, 256, 0, H->stream>>>(B, L.h, H->sr_dz1, H->cg_p + L.off_b1, H->sr_q1, 1, H->sp_part,
                                                     nparts, H->d_pmax, H->sr_q);
   }
